@@ -1,0 +1,137 @@
+"""Pins of the oracle's O1 (back-projection) and O2 (exact kNN), CPU only.
+
+O1 is pinned to SPEC's worked examples (tests/golden/spec_examples.json) and to the
+projection round trip.  O2 is pinned to brute force == kd-tree on tie-heavy data, to
+scipy's cKDTree (a library routine, re-ranked by the canonical binary32 key), to the analytic
+neighbour shells of an integer lattice, and to permutation invariance.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+@pytest.mark.parametrize("ex", GOLD["backproject"])
+def test_backproject_spec_examples(ex):
+    H, W = 64, 80
+    depth = np.zeros((H, W), np.float32)
+    u, v = ex["u"], ex["v"]
+    depth[v, u] = ex["d"]
+    xyz, pix = oracle.backproject(depth, ex["fx"], ex["fy"], ex["cx"], ex["cy"], stride=1, zmin=0.1, zmax=10.0)
+    if ex["point"] is None:
+        assert xyz.shape[0] == 0
+    else:
+        assert xyz.shape[0] == 1 and pix[0] == v * W + u
+        np.testing.assert_allclose(xyz[0], np.float32(ex["point"]), rtol=0, atol=1e-7)
+
+
+def test_backproject_window_stride_order():
+    rng = np.random.default_rng(0)
+    H, W, s = 37, 53, 3
+    depth = rng.uniform(0.0, 12.0, (H, W)).astype(np.float32)
+    depth[5, 6] = np.nan
+    depth[9, 9] = np.inf
+    xyz, pix = oracle.backproject(depth, 40.0, 41.0, 26.0, 18.0, stride=s, zmin=0.1, zmax=10.0)
+    # exactly the stride lattice from (0,0), window inclusive, finite only, row-major order
+    vv, uu = np.mgrid[0:H:s, 0:W:s]
+    z = depth[vv, uu]
+    keep = np.isfinite(z) & (z >= np.float32(0.1)) & (z <= np.float32(10.0))
+    np.testing.assert_array_equal(pix, (vv * W + uu)[keep])
+    np.testing.assert_array_equal(xyz[:, 2], z[keep])
+
+
+def test_backproject_roundtrip():
+    """projecting the re-projected point recovers (u, v) and d exactly; here the only error
+    is the binary32 rounding of x, y (relative 2^-24), so |u' - u| <= fx |x| / z * 2^-23."""
+    rng = np.random.default_rng(1)
+    H, W = 48, 64
+    depth = rng.uniform(0.2, 9.0, (H, W)).astype(np.float32)
+    fx, fy, cx, cy = 50.0, 52.0, 31.5, 23.5
+    xyz, pix = oracle.backproject(depth, fx, fy, cx, cy, stride=1)
+    u, v = pix % W, pix // W
+    x, y, z = xyz[:, 0].astype(np.float64), xyz[:, 1].astype(np.float64), xyz[:, 2].astype(np.float64)
+    np.testing.assert_array_equal(z, depth[v, u].astype(np.float64))
+    up = fx * x / z + cx
+    vp = fy * y / z + cy
+    assert np.all(np.abs(up - u) <= fx * np.abs(x) / z * 2.0 ** -23 + 1e-9)
+    assert np.all(np.abs(vp - v) <= fy * np.abs(y) / z * 2.0 ** -23 + 1e-9)
+
+
+def _canonical_keys(q, P):
+    """binary32 key evaluated with numpy float32 ops (separate rounding per op, no FMA)."""
+    d = (q[None, :].astype(np.float32) - P.astype(np.float32))
+    s = d[:, 0] * d[:, 0]
+    s = s + d[:, 1] * d[:, 1]
+    return s + d[:, 2] * d[:, 2]
+
+
+def test_knn_matches_scipy_ckdtree():
+    from scipy.spatial import cKDTree
+
+    rng = np.random.default_rng(2)
+    P = rng.normal(size=(3000, 3)).astype(np.float32)
+    k = 20
+    idx = oracle.knn_brute(P, k)
+    _, cand = cKDTree(P.astype(np.float64)).query(P.astype(np.float64), k=k + 12)
+    for i in range(0, 3000, 7):
+        c = cand[i]
+        key = _canonical_keys(P[i], P[c])
+        order = np.lexsort((c, key))
+        np.testing.assert_array_equal(idx[i], c[order][:k])
+
+
+def test_knn_lattice_shells_and_ties():
+    """Integer lattice: exact keys 0 (self), 1 (6 face nbrs), 2 (12 edge), 3 (8 corner); ties by index."""
+    g = np.stack(np.meshgrid(np.arange(5), np.arange(5), np.arange(5), indexing="ij"), -1).reshape(-1, 3)
+    P = g.astype(np.float32)
+    c = 2 * 25 + 2 * 5 + 2
+    idx, keys = oracle.knn_brute(P, 27, queries=[c], return_keys=True)
+    np.testing.assert_array_equal(keys[0], np.float32([0] + [1] * 6 + [2] * 12 + [3] * 8))
+    assert idx[0, 0] == c
+    d2 = ((g - g[c]) ** 2).sum(1)
+    for shell, (a, b) in {1: (1, 7), 2: (7, 19), 3: (19, 27)}.items():
+        np.testing.assert_array_equal(idx[0, a:b], np.sort(np.nonzero(d2 == shell)[0]))
+
+
+def test_knn_brute_equals_kdtree_on_ties():
+    rng = np.random.default_rng(3)
+    # stride-grid depth-like cloud: many exact ties
+    g = np.stack(np.meshgrid(np.arange(40), np.arange(30), indexing="ij"), -1).reshape(-1, 2)
+    P = np.concatenate([g * 0.01, np.full((g.shape[0], 1), 1.5)], 1).astype(np.float32)
+    P = np.concatenate([P, rng.normal(size=(800, 3)).astype(np.float32)])
+    for k in (1, 5, 20):
+        a, ka = oracle.knn_brute(P, k, return_keys=True)
+        b, kb = oracle.KDTree(P).knn(P, k, return_keys=True)
+        np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(ka, kb)
+    # arbitrary (non-member) queries
+    Q = rng.normal(size=(500, 3)).astype(np.float32)
+    t = oracle.KDTree(P)
+    a = t.knn(Q, 1)
+    for i in range(0, 500, 5):
+        key = _canonical_keys(Q[i], P)
+        assert a[i, 0] == np.lexsort((np.arange(P.shape[0]), key))[0]
+
+
+def test_knn_permutation_invariance():
+    rng = np.random.default_rng(4)
+    P = rng.uniform(size=(1500, 3)).astype(np.float32)
+    perm = rng.permutation(1500)
+    a = oracle.knn_brute(P, 20)
+    b = oracle.knn_brute(P[perm], 20)
+    inv = np.argsort(perm)
+    # b[inv[i]] are neighbours of P[i] expressed in permuted indices -> map back
+    np.testing.assert_array_equal(np.sort(a, 1), np.sort(perm[b[inv]], 1))
+
+
+def test_knn_low_support_pads():
+    P = np.random.default_rng(5).normal(size=(7, 3)).astype(np.float32)
+    idx = oracle.knn_brute(P, 20)
+    assert (idx[:, 7:] == -1).all() and (np.sort(idx[:, :7], 1) == np.arange(7)).all()
+    out = oracle.covariances(P, k=20)
+    assert (out["flags"] & oracle.FLAG_LOW_SUPPORT).all()

@@ -1,0 +1,195 @@
+/*
+ * gsicp.h — C ABI of the B200-native G-ICP tracking hot path of GS-ICP SLAM
+ * (arXiv 2403.12550).  Citations: P:n = PAPER.md line n, S:n = SPEC.md line n,
+ * Rn = reading n in DESIGN.md §3.  Library: paper_2403_12550_b200/libgsicp.so.
+ *
+ * Conventions (all entry points):
+ *  - Array pointers marked [dev] are CUDA device pointers OWNED BY THE CALLER; the
+ *    library never allocates device memory.  Each call takes a caller workspace sized by
+ *    the matching *_workspace_size() query (256-byte aligned base required).
+ *  - `stream` is a cudaStream_t passed as void*.  All work is stream-ordered on it; calls are
+ *    reentrant and keep no global mutable state, so independent calls on different streams /
+ *    devices may run concurrently.  Only gsicp_align and gsicp_linearize
+ *    synchronise `stream` (they return host results).
+ *  - Host-side argument errors return GSICP_ERR_INVALID_ARGUMENT before anything is launched.
+ *    CUDA launch errors return GSICP_ERR_CUDA (detail in gsicp_last_error()).
+ *  - Point layout (SoA, binary32, 16-byte aligned float4 records):
+ *      pos[i]   = (x, y, z, w)              metres; w = int32 payload bits
+ *      cov_a[i] = (c00, c01, c02, c11)      regularised covariance, m^2 (or unitless after
+ *      cov_b[i] = (c12, c22, lam_mid, flags)  ELLIPSE/PLANE regularisation); flags int32 bits
+ *  - Counts that kernels produce live on the device (int32 *d_n) so a whole frame can be
+ *    captured in one CUDA graph without host round trips.
+ */
+#ifndef GSICP_H
+#define GSICP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the library is built with -fvisibility=hidden */
+#endif
+
+typedef enum {
+    GSICP_OK = 0,
+    GSICP_ERR_INVALID_ARGUMENT = 1,
+    GSICP_ERR_WORKSPACE_TOO_SMALL = 2,
+    GSICP_ERR_CUDA = 3,
+    GSICP_ERR_DEGENERATE_FRAME = 4, /* 0 valid points                                   */
+    GSICP_ERR_TRACKING_LOST = 5,    /* inliers < min_pairs; out_T = last valid pose     */
+    GSICP_WARN_MAX_ITERS = 6,       /* not converged within max_iters; out_T = last iterate     */
+    GSICP_WARN_LOW_SUPPORT = 7      /* some cloud had fewer than k points                */
+} gsicp_status;
+
+typedef enum { GSICP_REG_NONE = 0, GSICP_REG_PLANE = 1, GSICP_REG_ELLIPSE = 2 } gsicp_reg_mode;
+
+/* per-point flags stored in cov_b.w */
+#define GSICP_FLAG_LOW_SUPPORT 1u /* fewer than k points in the cloud                     */
+#define GSICP_FLAG_DEGENERATE 2u  /* lam_2 <= 1e-12 m^2, or lam_1 <= 1e-12 (PLANE/ELLIPSE), R8 */
+
+typedef struct { float fx, fy, cx, cy; } gsicp_intrinsics;
+
+/* A Gaussian cloud G = {X, C} in device memory. */
+typedef struct {
+    const float *pos;   /* [dev] float4[cap]                                  */
+    const float *cov_a; /* [dev] float4[cap]                                  */
+    const float *cov_b; /* [dev] float4[cap]                                  */
+    const int32_t *d_n; /* [dev] number of valid points n <= cap              */
+    int32_t cap;
+} gsicp_cloud;
+
+/* Target Gaussians G^t: a spatially hashed copy of a cloud, built by
+ * gsicp_build_target / gsicp_build_target_cloud.  Every pointer is a view into the caller's
+ * target workspace and stays valid (and must stay unmodified) while that buffer lives.
+ * Treat the fields as opaque. */
+typedef struct {
+    const float *pos;     /* [dev] float4[M], cell order, w = original index bits */
+    const float *cov_a;   /* [dev] float4[M], cell order                          */
+    const float *cov_b;   /* [dev] float4[M], cell order                          */
+    const void *table;    /* [dev] open-addressing cell table                     */
+    const int32_t *bbox;  /* [dev] int32[6] min/max cell coordinates              */
+    uint32_t table_mask;  /* table slots - 1                                      */
+    float cell;           /* cell edge h (m)                                      */
+    int32_t M;
+} gsicp_target;
+
+typedef struct {
+    int32_t max_iters;     /* GN iterations cap, default 30                          */
+    float max_corr_dist;   /* r (m): pair valid iff key < r*r (R15); INFINITY = no gate      */
+    double eps_rot;        /* converged iff |omega| < eps_rot and |v| < eps_trans     */
+    double eps_trans;
+    int32_t min_pairs;     /* fewer inliers -> TRACKING_LOST, default 50       */
+} gsicp_align_params;
+
+typedef struct {
+    double fitness;        /* n_inliers / N_s of the final linearisation (R19)   */
+    double mean_cost;      /* cost / n_inliers, cost = sum d^T M d (Eq. 1)                   */
+    int32_t n_inliers;
+    int32_t iters;         /* GN updates applied                                             */
+    int32_t converged;
+    int32_t status;        /* gsicp_status of the loop                                       */
+} gsicp_align_stats;
+
+/* ---------------------------------------------------------------------------------------
+ * A1  Back-projection + uniform stride downsampling (Fig. 2 "downsampling and
+ * reprojecting the current depth image"; pinhole S:46).  For v = 0, s, 2s, ... < H and
+ * u = 0, s, ... < W, keep pixel (u, v) iff z = depth[v*row_pitch + u] is finite and
+ * z_min <= z <= z_max; emit pos = (x, y, z, v*W+u) with x = (float)(((double)u - cx) * z / fx)
+ * evaluated in binary64 (R13, R14).  Output is compacted in row-major pixel order (stable)
+ * into pos_out[0 .. n) and n is written to *d_n_out.
+ *  depth_m  [dev] binary32 metres, H rows of row_pitch_elems floats
+ *  pos_out  [dev] float4[cap]; cap >= ceil(H/s)*ceil(W/s) is required
+ *  Errors: INVALID_ARGUMENT (H, W, s < 1, pitch < W, cap too small, z_min > z_max, bad intrinsics).
+ *  A frame with 0 valid points is not an error here; *d_n_out = 0 and gsicp_align reports
+ *  GSICP_ERR_DEGENERATE_FRAME. */
+size_t gsicp_backproject_workspace_size(int32_t H, int32_t W, int32_t stride);
+gsicp_status gsicp_backproject_downsample(const float *depth_m, int32_t H, int32_t W, int32_t row_pitch_elems,
+                                          gsicp_intrinsics K, int32_t stride, float z_min, float z_max,
+                                          float *pos_out, int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes,
+                                          void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * A2-A4  Per-point covariance of the exact k nearest neighbours ("computing covariance
+ * matrix of k-nearest neighbors of x"; self included, ties by lower index),
+ * normalised by k, followed by regularisation (Eq. 3-4; R6-R8):
+ *   NONE    sum_i max(lam_i, 1e-6) v_i v_i^T
+ *   PLANE   v2 v2^T + v1 v1^T + eps_var v0 v0^T            (S = [1, 1, eps])
+ *   ELLIPSE sum_i max(lam_i / lam_1, eps_var) v_i v_i^T     (Lambda' = Lambda/median(S), Eq. 4)
+ * The neighbour order is the canonical binary32 key (R1) then index.  A device spatial hash with
+ * `levels` cell sizes cell0 * 2^l is built in the workspace; every query picks the finest level
+ * whose own cell holds >= 4 points and runs a certified expanding-ring search (exact result).
+ *  pos      [dev] float4[cap] (w ignored), d_n [dev] count
+ *  k        1..32 neighbours.  If n < k all n points are used and GSICP_FLAG_LOW_SUPPORT set.
+ *  cell0    finest cell edge (m, > 0); levels 1..8.  (Performance knobs only: results are exact.)
+ *  cov_a, cov_b [dev] float4[cap] outputs in input order (cov_b.z = raw lam_1, cov_b.w = flags)
+ *  knn_idx  [dev] nullable int32[cap*k]: neighbours sorted by (key, index), -1 padded
+ *  Errors: INVALID_ARGUMENT. */
+size_t gsicp_covariances_workspace_size(int32_t cap, int32_t levels);
+gsicp_status gsicp_covariances(const float *pos, const int32_t *d_n, int32_t cap, int32_t k, gsicp_reg_mode mode,
+                               float eps_var, float cell0, int32_t levels, float *cov_a, float *cov_b,
+                               int32_t *knn_idx, void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * A5  Map Gaussians -> G-ICP targets (the map's Gaussians are reused as
+ * targets with no covariance recomputation; P:189-191 C = R Lambda^2 R^T).  Quaternion wxyz,
+ * normalised before use; scales linear, or log if scales_are_log (R22); the regularised
+ * covariance is formed in closed form from (R, s) (no eigensolve), then the means are hashed
+ * with cell edge `cell` (<= 0: 2 x mean middle scale).
+ *  means [dev] float[M][3], quats_wxyz [dev] float[M][4], scales [dev] float[M][3]
+ *  target_ws: caller buffer holding the target for as long as it is used
+ *  out: host struct filled with views into target_ws.  Synchronises `stream` only if cell <= 0. */
+size_t gsicp_build_target_workspace_size(int32_t M);
+gsicp_status gsicp_build_target(const float *means, const float *quats_wxyz, const float *scales,
+                                int32_t scales_are_log, int32_t M, gsicp_reg_mode mode, float eps_var, float cell,
+                                gsicp_target *out, void *target_ws, size_t ws_bytes, void *stream);
+
+/* Same, from a cloud that already carries G-ICP covariances (e.g. gsicp_covariances output;
+ * used for frame-to-frame tracking and the C1 configuration).  cell must be > 0. */
+gsicp_status gsicp_build_target_cloud(const gsicp_cloud *cloud, int32_t M, float cell, gsicp_target *out,
+                                      void *target_ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * A6-A9  G-ICP alignment: T* = argmin_T sum_i d_i^T (C^t_i + R C^s_i R^T)^{-1} d_i (Eq. 1,
+ * P:103-131; R1-R3), d_i = x^t_j - T x^s_i with j the exact nearest target mean of T x^s_i
+ * (P:95), by Gauss-Newton on a left twist (omega, v) with J = [[q]x, -I] (R16), 6x6 Cholesky
+ * solve, Exp(omega) update, and a device-side convergence test, all inside ONE persistent
+ * kernel (grid barrier per iteration) — no host round trip between iterations.
+ *  init_T   host double[16] row-major, maps source (camera) coordinates to target (map).
+ *  out_T    host double[16]; out_stats host.  Blocking: synchronises `stream`.
+ *  Returns OK / WARN_MAX_ITERS / ERR_TRACKING_LOST / ERR_DEGENERATE_FRAME (n == 0). */
+size_t gsicp_align_workspace_size(int32_t src_cap);
+gsicp_status gsicp_align(const gsicp_cloud *src, const gsicp_target *tgt, const double *init_T,
+                         const gsicp_align_params *prm, double *out_T, gsicp_align_stats *out_stats, void *ws,
+                         size_t ws_bytes, void *stream);
+
+/* Non-blocking / graph-capturable variant: the pose is read from and written to device memory
+ * (d_T_inout [dev] double[16]) and the stats go to d_stats [dev]; nothing is synchronised.
+ * corr_out [dev] nullable int32[cap]: final correspondence (original target index or -1). */
+gsicp_status gsicp_align_async(const gsicp_cloud *src, const gsicp_target *tgt, double *d_T_inout,
+                               const gsicp_align_params *prm, gsicp_align_stats *d_stats, int32_t *corr_out,
+                               void *ws, size_t ws_bytes, void *stream);
+
+/* TEST / DIAGNOSTIC export: one linearisation of Eq. 1 at pose T (host double[16]) without any
+ * update — H (host double[36], row-major, twist order (omega, v)), b (host double[6]),
+ * cost and inlier count; corr_opt [dev] nullable int32[cap] (original target index or -1).
+ * Uses gsicp_align_workspace_size(src->cap).  Blocking. */
+gsicp_status gsicp_linearize(const gsicp_cloud *src, const gsicp_target *tgt, const double *T, float max_corr_dist,
+                             double *H, double *b, double *cost, int32_t *n_inliers, int32_t *corr_opt, void *ws,
+                             size_t ws_bytes, void *stream);
+
+/* Misc */
+const char *gsicp_status_string(gsicp_status s);
+const char *gsicp_last_error(void);         /* thread-local detail of the last error           */
+uint64_t gsicp_kernel_launch_count(void);   /* kernels launched by this thread (diagnostics)   */
+int32_t gsicp_abi_version(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSICP_H */

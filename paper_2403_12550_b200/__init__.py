@@ -1,0 +1,370 @@
+"""paper_2403_12550_b200 — B200-native G-ICP tracking hot path of GS-ICP SLAM (arXiv 2403.12550).
+
+Thin ctypes binding of libgsicp.so (C ABI: include/gsicp.h).  This module only marshals
+arguments (torch CUDA tensors -> device pointers, the current torch stream -> cudaStream_t);
+every step of the path runs in the library's sm_100a kernels.  There is no CPU fallback:
+if the library or a CUDA device is missing, every call raises.
+
+Public API (names follow include/gsicp.h):
+    backproject_downsample, covariances, build_target, build_target_cloud,
+    align, align_async, linearize, Cloud, Target, Tracker
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import math
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgsicp.so")
+
+OK, ERR_INVALID_ARGUMENT, ERR_WORKSPACE_TOO_SMALL, ERR_CUDA = 0, 1, 2, 3
+ERR_DEGENERATE_FRAME, ERR_TRACKING_LOST, WARN_MAX_ITERS, WARN_LOW_SUPPORT = 4, 5, 6, 7
+REG_NONE, REG_PLANE, REG_ELLIPSE = 0, 1, 2
+FLAG_LOW_SUPPORT, FLAG_DEGENERATE = 1, 2
+
+
+class GsicpError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"gsicp status {status}: {msg}")
+        self.status = status
+
+
+class Intrinsics(C.Structure):
+    _fields_ = [("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float)]
+
+
+class _Cloud(C.Structure):
+    _fields_ = [("pos", C.c_void_p), ("cov_a", C.c_void_p), ("cov_b", C.c_void_p), ("d_n", C.c_void_p),
+                ("cap", C.c_int32)]
+
+
+class _Target(C.Structure):
+    _fields_ = [("pos", C.c_void_p), ("cov_a", C.c_void_p), ("cov_b", C.c_void_p), ("table", C.c_void_p),
+                ("bbox", C.c_void_p), ("table_mask", C.c_uint32), ("cell", C.c_float), ("M", C.c_int32)]
+
+
+class AlignParams(C.Structure):
+    _fields_ = [("max_iters", C.c_int32), ("max_corr_dist", C.c_float), ("eps_rot", C.c_double),
+                ("eps_trans", C.c_double), ("min_pairs", C.c_int32)]
+
+
+class AlignStats(C.Structure):
+    _fields_ = [("fitness", C.c_double), ("mean_cost", C.c_double), ("n_inliers", C.c_int32),
+                ("iters", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libgsicp.so (raises if it is missing: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built; run __graft_entry__.build() or python -m "
+                               f"paper_2403_12550_b200._build")
+        L = C.CDLL(LIB_PATH)
+        P, i32, f32, f64, sz = C.c_void_p, C.c_int32, C.c_float, C.c_double, C.c_size_t
+        L.gsicp_backproject_workspace_size.argtypes = [i32, i32, i32]
+        L.gsicp_backproject_workspace_size.restype = sz
+        L.gsicp_backproject_downsample.argtypes = [P, i32, i32, i32, Intrinsics, i32, f32, f32, P, i32, P, P, sz, P]
+        L.gsicp_covariances_workspace_size.argtypes = [i32, i32]
+        L.gsicp_covariances_workspace_size.restype = sz
+        L.gsicp_covariances.argtypes = [P, P, i32, i32, i32, f32, f32, i32, P, P, P, P, sz, P]
+        L.gsicp_build_target_workspace_size.argtypes = [i32]
+        L.gsicp_build_target_workspace_size.restype = sz
+        L.gsicp_build_target.argtypes = [P, P, P, i32, i32, i32, f32, f32, C.POINTER(_Target), P, sz, P]
+        L.gsicp_build_target_cloud.argtypes = [C.POINTER(_Cloud), i32, f32, C.POINTER(_Target), P, sz, P]
+        L.gsicp_align_workspace_size.argtypes = [i32]
+        L.gsicp_align_workspace_size.restype = sz
+        L.gsicp_align.argtypes = [C.POINTER(_Cloud), C.POINTER(_Target), P, C.POINTER(AlignParams), P,
+                                  C.POINTER(AlignStats), P, sz, P]
+        L.gsicp_align_async.argtypes = [C.POINTER(_Cloud), C.POINTER(_Target), P, C.POINTER(AlignParams), P, P, P,
+                                        sz, P]
+        L.gsicp_linearize.argtypes = [C.POINTER(_Cloud), C.POINTER(_Target), P, f32, P, P, P, P, P, P, sz, P]
+        L.gsicp_status_string.argtypes = [i32]
+        L.gsicp_status_string.restype = C.c_char_p
+        L.gsicp_last_error.restype = C.c_char_p
+        L.gsicp_kernel_launch_count.restype = C.c_uint64
+        L.gsicp_abi_version.restype = i32
+        for name in ("gsicp_backproject_downsample", "gsicp_covariances", "gsicp_build_target",
+                     "gsicp_build_target_cloud", "gsicp_align", "gsicp_align_async", "gsicp_linearize"):
+            getattr(L, name).restype = i32
+        _lib = L
+    return _lib
+
+
+EXPORTED = [
+    "gsicp_backproject_workspace_size", "gsicp_backproject_downsample", "gsicp_covariances_workspace_size",
+    "gsicp_covariances", "gsicp_build_target_workspace_size", "gsicp_build_target", "gsicp_build_target_cloud",
+    "gsicp_align_workspace_size", "gsicp_align", "gsicp_align_async", "gsicp_linearize", "gsicp_status_string",
+    "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version",
+]
+
+
+def _check(st: int, allow=(OK,)):
+    if st not in allow:
+        detail = lib().gsicp_last_error().decode()
+        raise GsicpError(st, f"{lib().gsicp_status_string(st).decode()} {detail}")
+    return st
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def launch_count() -> int:
+    """Kernels libgsicp launched from this thread so far."""
+    return int(lib().gsicp_kernel_launch_count())
+
+
+@dataclasses.dataclass
+class Cloud:
+    """Gaussian cloud G = {X, C} as SoA float4 tensors on one device."""
+    pos: torch.Tensor          # (cap, 4) f32: x, y, z, payload bits
+    cov_a: torch.Tensor        # (cap, 4) f32: c00, c01, c02, c11
+    cov_b: torch.Tensor        # (cap, 4) f32: c12, c22, lam_mid, flags bits
+    d_n: torch.Tensor          # (1,) int32 valid count
+
+    @property
+    def cap(self) -> int:
+        return int(self.pos.shape[0])
+
+    def c_struct(self) -> _Cloud:
+        return _Cloud(_ptr(self.pos), _ptr(self.cov_a), _ptr(self.cov_b), _ptr(self.d_n), self.cap)
+
+    def n(self) -> int:
+        return int(self.d_n.item())
+
+    def cov6(self) -> torch.Tensor:
+        """(cap, 6) packed symmetric covariances (c00, c01, c02, c11, c12, c22)."""
+        return torch.cat([self.cov_a, self.cov_b[:, :2]], dim=1)
+
+    def flags(self) -> torch.Tensor:
+        return self.cov_b[:, 3].contiguous().view(torch.int32)
+
+    @staticmethod
+    def empty(cap: int, device="cuda") -> "Cloud":
+        z = lambda: torch.zeros((cap, 4), dtype=torch.float32, device=device)
+        return Cloud(z(), z(), z(), torch.zeros(1, dtype=torch.int32, device=device))
+
+    @staticmethod
+    def from_points(xyz: torch.Tensor, cov6: torch.Tensor | None = None) -> "Cloud":
+        """Pack (n, 3) points (and optional (n, 6) covariances) into the SoA float4 layout."""
+        n = xyz.shape[0]
+        dev = xyz.device
+        c = Cloud.empty(n, dev)
+        c.pos[:, :3] = xyz
+        c.pos[:, 3] = torch.arange(n, device=dev, dtype=torch.int32).view(torch.float32)
+        if cov6 is not None:
+            c.cov_a[:] = cov6[:, :4]
+            c.cov_b[:, :2] = cov6[:, 4:6]
+        c.d_n.fill_(n)
+        return c
+
+
+def backproject_downsample(depth: torch.Tensor, K, stride: int = 4, z_min: float = 0.1, z_max: float = 10.0,
+                           pos_out: torch.Tensor | None = None, d_n: torch.Tensor | None = None,
+                           ws: torch.Tensor | None = None, stream=None):
+    """A1.  depth: (H, W) f32 metres on the GPU.  Returns (pos (cap, 4), d_n (1,))."""
+    H, W = depth.shape
+    pitch = depth.stride(0)
+    cap = ((H + stride - 1) // stride) * ((W + stride - 1) // stride)
+    dev = depth.device
+    if pos_out is None:
+        pos_out = torch.empty((cap, 4), dtype=torch.float32, device=dev)
+    if d_n is None:
+        d_n = torch.zeros(1, dtype=torch.int32, device=dev)
+    need = lib().gsicp_backproject_workspace_size(H, W, stride)
+    if ws is None:
+        ws = _ws(need, dev)
+    Kc = K if isinstance(K, Intrinsics) else Intrinsics(*K)
+    _check(lib().gsicp_backproject_downsample(C.c_void_p(depth.data_ptr()), H, W, pitch, Kc, stride, z_min, z_max,
+                                              _ptr(pos_out), pos_out.shape[0], _ptr(d_n), _ptr(ws), ws.numel(),
+                                              _stream(stream)))
+    return pos_out, d_n
+
+
+def covariances(pos: torch.Tensor, d_n: torch.Tensor, k: int = 20, mode: int = REG_ELLIPSE, eps_var: float = 1e-3,
+                cell0: float = 0.01, levels: int = 1, cov_a=None, cov_b=None, knn_idx: torch.Tensor | None = None,
+                ws=None, stream=None):
+    """A2-A4 (Eq. 3-4).  Returns a Cloud sharing `pos`."""
+    cap = pos.shape[0]
+    dev = pos.device
+    if cov_a is None:
+        cov_a = torch.empty((cap, 4), dtype=torch.float32, device=dev)
+    if cov_b is None:
+        cov_b = torch.empty((cap, 4), dtype=torch.float32, device=dev)
+    need = lib().gsicp_covariances_workspace_size(cap, levels)
+    if ws is None:
+        ws = _ws(need, dev)
+    _check(lib().gsicp_covariances(_ptr(pos), _ptr(d_n), cap, k, mode, eps_var, cell0, levels, _ptr(cov_a),
+                                   _ptr(cov_b), _ptr(knn_idx), _ptr(ws), ws.numel(), _stream(stream)))
+    return Cloud(pos, cov_a, cov_b, d_n)
+
+
+@dataclasses.dataclass
+class Target:
+    """Target Gaussians G^t: hashed copy living in `ws` (keep this object alive)."""
+    ws: torch.Tensor
+    st: _Target
+    keepalive: tuple = ()
+
+    @property
+    def M(self) -> int:
+        return int(self.st.M)
+
+    @property
+    def cell(self) -> float:
+        return float(self.st.cell)
+
+    def arrays(self):
+        """(pos, cov_a, cov_b) as (M, 4) float32 views into the workspace, in cell order;
+        pos[:, 3] holds the original index bits."""
+        base = self.ws.data_ptr()
+        out = []
+        for p in (self.st.pos, self.st.cov_a, self.st.cov_b):
+            off = p - base
+            out.append(self.ws[off:off + 16 * self.M].view(torch.float32).view(self.M, 4))
+        return tuple(out)
+
+
+def build_target(means: torch.Tensor, quats_wxyz: torch.Tensor, scales: torch.Tensor, scales_are_log: bool = False,
+                 mode: int = REG_ELLIPSE, eps_var: float = 1e-3, cell: float = 0.0, stream=None) -> Target:
+    """A5."""
+    M = means.shape[0]
+    need = lib().gsicp_build_target_workspace_size(M)
+    ws = _ws(need, means.device)
+    st = _Target()
+    _check(lib().gsicp_build_target(_ptr(means), _ptr(quats_wxyz), _ptr(scales), int(scales_are_log), M, mode, eps_var,
+                                    cell, C.byref(st), _ptr(ws), ws.numel(), _stream(stream)))
+    return Target(ws, st, (means, quats_wxyz, scales))
+
+
+def build_target_cloud(cloud: Cloud, cell: float, M: int | None = None, stream=None) -> Target:
+    M = cloud.cap if M is None else M
+    need = lib().gsicp_build_target_workspace_size(M)
+    ws = _ws(need, cloud.pos.device)
+    st = _Target()
+    cs = cloud.c_struct()
+    _check(lib().gsicp_build_target_cloud(C.byref(cs), M, cell, C.byref(st), _ptr(ws), ws.numel(), _stream(stream)))
+    return Target(ws, st, (cloud,))
+
+
+def align_params(max_iters=30, max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6, min_pairs=50) -> AlignParams:
+    return AlignParams(max_iters, max_corr_dist, eps_rot, eps_trans, min_pairs)
+
+
+def align_workspace(cap: int, device="cuda") -> torch.Tensor:
+    return _ws(lib().gsicp_align_workspace_size(cap), device)
+
+
+def align(src: Cloud, tgt: Target, init_T, params: AlignParams | None = None, ws: torch.Tensor | None = None,
+          stream=None, allow=(OK, WARN_MAX_ITERS, ERR_TRACKING_LOST, ERR_DEGENERATE_FRAME)):
+    """A6-A9 (Eq. 1).  Blocking; returns (T (4,4) float64 numpy, stats dict)."""
+    params = params or align_params()
+    ws = ws if ws is not None else align_workspace(src.cap, src.pos.device)
+    T0 = np.ascontiguousarray(init_T, dtype=np.float64)
+    Tout = np.empty((4, 4), dtype=np.float64)
+    stats = AlignStats()
+    cs = src.c_struct()
+    st = lib().gsicp_align(C.byref(cs), C.byref(tgt.st), T0.ctypes.data_as(C.c_void_p), C.byref(params),
+                           Tout.ctypes.data_as(C.c_void_p), C.byref(stats), _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, allow)
+    return Tout, stats.as_dict()
+
+
+def align_async(src: Cloud, tgt: Target, d_T: torch.Tensor, d_stats: torch.Tensor, params: AlignParams | None = None,
+                ws: torch.Tensor | None = None, corr_out: torch.Tensor | None = None, stream=None):
+    """Graph-capturable A6-A9: d_T (16,) float64 on the device is read and updated in place,
+    d_stats (32,) uint8 receives gsicp_align_stats."""
+    params = params or align_params()
+    ws = ws if ws is not None else align_workspace(src.cap, src.pos.device)
+    cs = src.c_struct()
+    _check(lib().gsicp_align_async(C.byref(cs), C.byref(tgt.st), _ptr(d_T), C.byref(params), _ptr(d_stats),
+                                   _ptr(corr_out), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def decode_stats(d_stats: torch.Tensor) -> dict:
+    raw = d_stats.cpu().numpy().tobytes()
+    st = AlignStats.from_buffer_copy(raw[:C.sizeof(AlignStats)])
+    return st.as_dict()
+
+
+def linearize(src: Cloud, tgt: Target, T, max_corr_dist: float = math.inf, corr_out: torch.Tensor | None = None,
+              ws: torch.Tensor | None = None, stream=None):
+    """One linearisation of Eq. 1 at pose T -> dict(H, b, cost, n)."""
+    ws = ws if ws is not None else align_workspace(src.cap, src.pos.device)
+    T = np.ascontiguousarray(T, dtype=np.float64)
+    H = np.empty((6, 6))
+    b = np.empty(6)
+    cost = C.c_double()
+    n = C.c_int32()
+    cs = src.c_struct()
+    _check(lib().gsicp_linearize(C.byref(cs), C.byref(tgt.st), T.ctypes.data_as(C.c_void_p), max_corr_dist,
+                                 H.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p), C.byref(cost),
+                                 C.byref(n), _ptr(corr_out), _ptr(ws), ws.numel(), _stream(stream)))
+    return dict(H=H, b=b, cost=cost.value, n=n.value)
+
+
+class Tracker:
+    """Per-frame tracking pipeline with preallocated buffers: A1 -> A2-A4 -> A6-A9 against a
+    prebuilt target.  `track()` is the public per-frame call; `step_async()` is graph-capturable."""
+
+    def __init__(self, H: int, W: int, K, stride: int = 4, k: int = 20, mode: int = REG_ELLIPSE,
+                 eps_var: float = 1e-3, z_min: float = 0.1, z_max: float = 10.0, cell0: float | None = None,
+                 levels: int = 5, params: AlignParams | None = None, device="cuda"):
+        self.H, self.W, self.stride, self.k, self.mode, self.eps = H, W, stride, k, mode, eps_var
+        self.K = K if isinstance(K, Intrinsics) else Intrinsics(*K)
+        self.z_min, self.z_max = z_min, z_max
+        self.cap = ((H + stride - 1) // stride) * ((W + stride - 1) // stride)
+        # finest cell ~ 2.5 x the pixel footprint at z_min-ish depth (performance knob only)
+        self.cell0 = cell0 if cell0 is not None else max(2.5 * stride * 0.5 / self.K.fx, 1e-3)
+        self.levels = levels
+        self.params = params or align_params()
+        self.device = torch.device(device)
+        self.cloud = Cloud.empty(self.cap, self.device)
+        self.ws_bp = _ws(lib().gsicp_backproject_workspace_size(H, W, stride), self.device)
+        self.ws_cov = _ws(lib().gsicp_covariances_workspace_size(self.cap, levels), self.device)
+        self.ws_align = align_workspace(self.cap, self.device)
+        self.d_T = torch.zeros(16, dtype=torch.float64, device=self.device)
+        self.d_stats = torch.zeros(C.sizeof(AlignStats), dtype=torch.uint8, device=self.device)
+
+    def preprocess(self, depth: torch.Tensor, stream=None):
+        backproject_downsample(depth, self.K, self.stride, self.z_min, self.z_max, self.cloud.pos, self.cloud.d_n,
+                               self.ws_bp, stream)
+        covariances(self.cloud.pos, self.cloud.d_n, self.k, self.mode, self.eps, self.cell0, self.levels,
+                    self.cloud.cov_a, self.cloud.cov_b, None, self.ws_cov, stream)
+
+    def step_async(self, depth: torch.Tensor, tgt: Target, stream=None):
+        """Whole frame, device-resident pose in self.d_T (set it before), no host sync."""
+        self.preprocess(depth, stream)
+        align_async(self.cloud, tgt, self.d_T, self.d_stats, self.params, self.ws_align, None, stream)
+
+    def track(self, depth: torch.Tensor, tgt: Target, init_T, stream=None):
+        """Whole frame through the blocking C ABI call; returns (T, stats)."""
+        self.preprocess(depth, stream)
+        return align(self.cloud, tgt, init_T, self.params, self.ws_align, stream)

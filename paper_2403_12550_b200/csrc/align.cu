@@ -1,0 +1,488 @@
+// A6-A9  G-ICP alignment in ONE persistent cooperative kernel.
+//
+// Per Gauss-Newton iteration, every thread takes source points i (grid-stride) and
+//   A6  q = K3(T, x_i) in binary64 (no FMA), exact 1-NN of fl32(q) among the target means by
+//       the canonical (key, index) order, certified expanding rings on the target hash,
+//       warm-started with the previous iteration's match; valid iff key < fl32(r*r) (R15);
+//   A7  Sigma = C^t_j + R C^s_i R^T, M = Sigma^{-1} (adjugate, binary64), d = x^t_j - q,
+//       J = [[q]x, -I]: accumulates the 21 unique H = J^T M J terms, b = J^T M d, d^T M d and
+//       the inlier count (Eq. 1; R1-R3, R16);
+// then warp shuffles + shared memory reduce the 29 terms per block into a per-block partial,
+// one grid barrier publishes the partials, and EVERY block reduces all partials in the same
+// fixed order (so all blocks hold bit-identical H, b), solves the 6x6 system by Cholesky
+// (A8), applies the left update T <- [Exp(w) | v] T and evaluates the convergence test —
+// identical decisions in every block, no second barrier, no host round trip (A9 at the end).
+#include <math.h>
+
+#include "gsicp_internal.cuh"
+#include "host_common.cuh"
+
+namespace gsicp {
+
+namespace {
+
+constexpr int kT = kAlignThreads;
+constexpr int kWarps = kT / 32;
+constexpr int kPad = 32;  // partial record stride (doubles)
+constexpr float kRelMargin = 1e-5f;
+
+struct AlignArgs {
+    const float4 *spos, *scov_a, *scov_b;
+    const int32_t *d_n;
+    int cap;
+    const CellEntry *table;
+    uint32_t mask;
+    float h, inv_h;
+    const float4 *tpos, *tcov_a, *tcov_b;
+    const int32_t *tbbox;
+    int max_iters;
+    float r, r2;
+    double eps_rot, eps_trans;
+    int min_pairs;
+    int linearize_only;
+    double *d_T;              // [16] in/out (row-major 4x4)
+    gsicp_align_stats *d_stats;
+    double *d_lin;            // [44] linearize-only output: H[36], b[6], cost, n
+    double *partials;         // [2][grid][kPad]
+    unsigned int *barrier;
+    int32_t *corr_ws;         // [cap] previous match (cell-ordered slot) or -1
+    int32_t *corr_out;        // nullable [cap] original target index or -1
+};
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ float ordered_to_float_(int32_t i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+
+// Exact 1-NN of (qx, qy, qz) on the target hash; best/best_slot carry the warm start in and the
+// answer out.
+__device__ __forceinline__ void nn_search(const AlignArgs &a, const int *sb, float qx, float qy, float qz,
+                                          unsigned long long &best, int &best_slot) {
+    const float h = a.h, inv_h = a.inv_h;
+    const int c[3] = {cell_coord(qx, inv_h), cell_coord(qy, inv_h), cell_coord(qz, inv_h)};
+    const float q[3] = {qx, qy, qz};
+    float dlo[3], dhi[3], dq = INFINITY;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        dlo[k] = fmaxf(q[k] - (float)c[k] * h, 0.f);
+        dhi[k] = fmaxf((float)(c[k] + 1) * h - q[k], 0.f);
+        dq = fminf(dq, fminf(dlo[k], dhi[k]));
+    }
+    const float margin = 2e-6f * (fabsf(qx) + fabsf(qy) + fabsf(qz)) + h * kRelMargin;
+    for (int m = 0;; ++m) {
+        const int cnt = m == 0 ? 1 : shell_count(m);
+        for (int t = 0; t < cnt; ++t) {
+            int dx = 0, dy = 0, dz = 0;
+            if (m) shell_offset(m, t, dx, dy, dz);
+            const int x = c[0] + dx, y = c[1] + dy, z = c[2] + dz;
+            if (x < sb[0] || x > sb[3] || y < sb[1] || y > sb[4] || z < sb[2] || z > sb[5]) continue;
+            if (m) {
+                const float gx = fmaxf(axis_gap(dx, dlo[0], dhi[0], h) - margin, 0.f);
+                const float gy = fmaxf(axis_gap(dy, dlo[1], dhi[1], h) - margin, 0.f);
+                const float gz = fmaxf(axis_gap(dz, dlo[2], dhi[2], h) - margin, 0.f);
+                const float lb = (gx * gx + gy * gy + gz * gz) * (1.f - kRelMargin);
+                if (lb > fminf(ki_key(best), a.r2)) continue;  // empty best -> key is NaN-free max
+            }
+            const uint2 se = cell_lookup(a.table, a.mask, cell_key(0, x, y, z));
+            for (uint32_t j = se.x; j < se.x + se.y; ++j) {
+                const float4 p = __ldg(a.tpos + j);
+                const unsigned long long v =
+                    pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
+                if (v < best) {
+                    best = v;
+                    best_slot = (int)j;
+                }
+            }
+        }
+        const float B = fmaxf((float)m * h + dq - margin, 0.f);
+        if (best != kEmptyKey && ki_key(best) < B * B * (1.f - kRelMargin)) return;  // certified
+        if (B > a.r * (1.f + kRelMargin)) return;  // every point with key < r^2 has been visited
+        if (c[0] - m <= sb[0] && c[0] + m >= sb[3] && c[1] - m <= sb[1] && c[1] + m >= sb[4] &&
+            c[2] - m <= sb[2] && c[2] + m >= sb[5])
+            return;  // the ring block covers the whole target
+    }
+}
+
+__device__ __forceinline__ void so3_exp(const double *w, double *R) {
+    const double th2 = w[0] * w[0] + w[1] * w[1] + w[2] * w[2];
+    const double th = sqrt(th2);
+    double A, B;
+    if (th < 1e-8) {
+        A = 1.0;
+        B = 0.5;
+    } else {
+        A = sin(th) / th;
+        B = (1.0 - cos(th)) / th2;
+    }
+    const double K[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            const double k2 = K[3 * r] * K[c] + K[3 * r + 1] * K[3 + c] + K[3 * r + 2] * K[6 + c];
+            R[3 * r + c] = (r == c ? 1.0 : 0.0) + A * K[3 * r + c] + B * k2;
+        }
+}
+
+__device__ bool chol6_solve(const double *H, const double *rhs, double *x) {
+    double L[6][6];
+    for (int i = 0; i < 6; ++i)
+        for (int j = 0; j <= i; ++j) {
+            double s = H[6 * i + j];
+            for (int k = 0; k < j; ++k) s -= L[i][k] * L[j][k];
+            if (i == j) {
+                if (!(s > 0.0)) return false;
+                L[i][i] = sqrt(s);
+            } else {
+                L[i][j] = s / L[j][j];
+            }
+        }
+    double y[6];
+    for (int i = 0; i < 6; ++i) {
+        double s = rhs[i];
+        for (int k = 0; k < i; ++k) s -= L[i][k] * y[k];
+        y[i] = s / L[i][i];
+    }
+    for (int i = 5; i >= 0; --i) {
+        double s = y[i];
+        for (int k = i + 1; k < 6; ++k) s -= L[k][i] * x[k];
+        x[i] = s / L[i][i];
+    }
+    return true;
+}
+
+__global__ void k_align_init(int32_t *corr_ws, int cap, unsigned int *barrier) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cap) corr_ws[i] = -1;
+    if (i == 0) *barrier = 0u;
+}
+
+__global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
+    __shared__ double sT[12];
+    __shared__ double sRed[kWarps][kPad];
+    __shared__ double sAcc[kPad];
+    __shared__ int sDone;
+    __shared__ int sBox[6];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x;
+    const int n = *a.d_n;
+    if (tid < 12) sT[tid] = a.d_T[tid];
+    if (tid < 6) {
+        const float inv_h = a.inv_h;
+        sBox[tid] = cell_coord(ordered_to_float_(a.tbbox[tid]), inv_h);
+    }
+    if (tid == 0) sDone = 0;
+    __syncthreads();
+    int status = GSICP_WARN_MAX_ITERS, iters = 0, converged = 0;
+    double n_in = 0.0, cost_last = 0.0;
+    for (int it = 0;; ++it) {
+        // ------------------------------------------------------------ A6 + A7
+        double acc[28];
+#pragma unroll
+        for (int k = 0; k < 28; ++k) acc[k] = 0.0;
+        double cnt = 0.0;
+        const double R00 = sT[0], R01 = sT[1], R02 = sT[2], t0 = sT[3];
+        const double R10 = sT[4], R11 = sT[5], R12 = sT[6], t1 = sT[7];
+        const double R20 = sT[8], R21 = sT[9], R22 = sT[10], t2 = sT[11];
+        for (int i = blockIdx.x * kT + tid; i < n; i += G * kT) {
+            const float4 x = __ldg(a.spos + i);
+            const double xd = x.x, yd = x.y, zd = x.z;
+            // K3: q_r = ((R_r0 x + R_r1 y) + R_r2 z) + t_r, binary64, no contraction
+            const double q0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R00, xd), __dmul_rn(R01, yd)), __dmul_rn(R02, zd)), t0);
+            const double q1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R10, xd), __dmul_rn(R11, yd)), __dmul_rn(R12, zd)), t1);
+            const double q2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R20, xd), __dmul_rn(R21, yd)), __dmul_rn(R22, zd)), t2);
+            const float qx = __double2float_rn(q0), qy = __double2float_rn(q1), qz = __double2float_rn(q2);
+            unsigned long long best = kEmptyKey;
+            int slot = a.corr_ws[i];
+            if (slot >= 0) {
+                const float4 p = __ldg(a.tpos + slot);
+                best = pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
+            }
+            nn_search(a, sBox, qx, qy, qz, best, slot);
+            a.corr_ws[i] = slot;
+            const bool valid = slot >= 0 && ki_key(best) < a.r2;
+            int32_t corr_val = -1;
+            if (valid) {
+                const float4 ca = __ldg(a.scov_a + i), cb = __ldg(a.scov_b + i);
+                const float4 ta = __ldg(a.tcov_a + slot), tb = __ldg(a.tcov_b + slot);
+                const float4 m = __ldg(a.tpos + slot);
+                // R Cs R^T + Ct (symmetric)
+                const double Cs[3][3] = {{ca.x, ca.y, ca.z}, {ca.y, ca.w, cb.x}, {ca.z, cb.x, cb.y}};
+                const double R[3][3] = {{R00, R01, R02}, {R10, R11, R12}, {R20, R21, R22}};
+                double RC[3][3];
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) RC[r][c] = R[r][0] * Cs[0][c] + R[r][1] * Cs[1][c] + R[r][2] * Cs[2][c];
+                double S[6];
+                const int ri[6] = {0, 0, 0, 1, 1, 2}, ci[6] = {0, 1, 2, 1, 2, 2};
+                const double Ct[6] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y};
+#pragma unroll
+                for (int e = 0; e < 6; ++e)
+                    S[e] = Ct[e] + RC[ri[e]][0] * R[ci[e]][0] + RC[ri[e]][1] * R[ci[e]][1] + RC[ri[e]][2] * R[ci[e]][2];
+                // M = S^{-1} by the adjugate (binary64)
+                const double A00 = S[3] * S[5] - S[4] * S[4];
+                const double A01 = S[2] * S[4] - S[1] * S[5];
+                const double A02 = S[1] * S[4] - S[2] * S[3];
+                const double A11 = S[0] * S[5] - S[2] * S[2];
+                const double A12 = S[1] * S[2] - S[0] * S[4];
+                const double A22 = S[0] * S[3] - S[1] * S[1];
+                const double det = S[0] * A00 + S[1] * A01 + S[2] * A02;
+                if (det > 0.0) {
+                    const double id = 1.0 / det;
+                    const double M[3][3] = {{A00 * id, A01 * id, A02 * id}, {A01 * id, A11 * id, A12 * id}, {A02 * id, A12 * id, A22 * id}};
+                    const double d[3] = {(double)m.x - q0, (double)m.y - q1, (double)m.z - q2};
+                    const double J[3][6] = {{0.0, -q2, q1, -1.0, 0.0, 0.0}, {q2, 0.0, -q0, 0.0, -1.0, 0.0}, {-q1, q0, 0.0, 0.0, 0.0, -1.0}};
+                    double MJ[3][6], Md[3];
+#pragma unroll
+                    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+                        for (int c = 0; c < 6; ++c) MJ[r][c] = M[r][0] * J[0][c] + M[r][1] * J[1][c] + M[r][2] * J[2][c];
+                        Md[r] = M[r][0] * d[0] + M[r][1] * d[1] + M[r][2] * d[2];
+                    }
+                    int t = 0;
+#pragma unroll
+                    for (int r = 0; r < 6; ++r)
+#pragma unroll
+                        for (int c = r; c < 6; ++c) acc[t++] += J[0][r] * MJ[0][c] + J[1][r] * MJ[1][c] + J[2][r] * MJ[2][c];
+#pragma unroll
+                    for (int r = 0; r < 6; ++r) acc[21 + r] += J[0][r] * Md[0] + J[1][r] * Md[1] + J[2][r] * Md[2];
+                    acc[27] += d[0] * Md[0] + d[1] * Md[1] + d[2] * Md[2];
+                    cnt += 1.0;
+                    corr_val = __float_as_int(m.w);
+                }
+            }
+            if (a.corr_out) a.corr_out[i] = corr_val;
+        }
+        // ------------------------------------------------------------ block reduction
+#pragma unroll
+        for (int k = 0; k < 28; ++k)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 28; ++k) sRed[warp][k] = acc[k];
+            sRed[warp][28] = cnt;
+        }
+        __syncthreads();
+        double *part = a.partials + (size_t)(it & 1) * G * kPad;
+        if (tid < kAlignTerms) {
+            double s = 0.0;
+            for (int w = 0; w < kWarps; ++w) s += sRed[w][tid];
+            part[(size_t)blockIdx.x * kPad + tid] = s;
+        }
+        // ------------------------------------------------------------ grid barrier
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(a.barrier, 1u);
+            const unsigned int target = (unsigned int)(it + 1) * (unsigned int)G;
+            while (ld_acquire(a.barrier) < target) {
+            }
+            __threadfence();
+        }
+        __syncthreads();
+        // ------------------------------------------------------------ fixed-order final reduction (every block)
+        {
+            const int grp = tid >> 5;  // 8 groups stride over blocks
+            double s = 0.0;
+            if (lane < kAlignTerms)
+                for (int gb = grp; gb < G; gb += kWarps) s += __ldcg(part + (size_t)gb * kPad + lane);
+            sRed[grp][lane] = s;
+            __syncthreads();
+            if (tid < kAlignTerms) {
+                double t = 0.0;
+                for (int w = 0; w < kWarps; ++w) t += sRed[w][tid];
+                sAcc[tid] = t;
+            }
+            __syncthreads();
+        }
+        // ------------------------------------------------------------ A8 solve / update / test
+        if (tid == 0) {
+            double H[36], b[6];
+            int t = 0;
+            for (int r = 0; r < 6; ++r)
+                for (int c = r; c < 6; ++c) H[6 * r + c] = H[6 * c + r] = sAcc[t++];
+            for (int r = 0; r < 6; ++r) b[r] = sAcc[21 + r];
+            n_in = sAcc[28];
+            cost_last = sAcc[27];
+            int done = 0;
+            if (a.linearize_only) {
+                if (blockIdx.x == 0) {
+                    for (int k = 0; k < 36; ++k) a.d_lin[k] = H[k];
+                    for (int k = 0; k < 6; ++k) a.d_lin[36 + k] = b[k];
+                    a.d_lin[42] = cost_last;
+                    a.d_lin[43] = n_in;
+                }
+                status = GSICP_OK;
+                done = 1;
+            } else if (n == 0) {
+                status = GSICP_ERR_DEGENERATE_FRAME;
+                done = 1;
+            } else if (n_in < (double)a.min_pairs) {
+                status = GSICP_ERR_TRACKING_LOST;
+                done = 1;
+            } else {
+                double nb[6], delta[6];
+                for (int k = 0; k < 6; ++k) nb[k] = -b[k];
+                bool ok = chol6_solve(H, nb, delta);
+                if (!ok) {
+                    double tr = 0.0;
+                    for (int k = 0; k < 6; ++k) tr += H[7 * k];
+                    for (int k = 0; k < 6; ++k) H[7 * k] += 1e-6 * tr / 6.0;
+                    ok = chol6_solve(H, nb, delta);
+                }
+                if (!ok) {
+                    status = GSICP_ERR_TRACKING_LOST;
+                    done = 1;
+                } else {
+                    double E[9];
+                    so3_exp(delta, E);
+                    double Tn[12];
+                    for (int r = 0; r < 3; ++r) {
+                        for (int c = 0; c < 3; ++c)
+                            Tn[4 * r + c] = E[3 * r] * sT[c] + E[3 * r + 1] * sT[4 + c] + E[3 * r + 2] * sT[8 + c];
+                        Tn[4 * r + 3] = E[3 * r] * sT[3] + E[3 * r + 1] * sT[7] + E[3 * r + 2] * sT[11] + delta[3 + r];
+                    }
+                    for (int k = 0; k < 12; ++k) sT[k] = Tn[k];
+                    iters = it + 1;
+                    const double nw = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]);
+                    const double nv = sqrt(delta[3] * delta[3] + delta[4] * delta[4] + delta[5] * delta[5]);
+                    if (nw < a.eps_rot && nv < a.eps_trans) {
+                        converged = 1;
+                        status = GSICP_OK;
+                        done = 1;
+                    } else if (iters >= a.max_iters) {
+                        status = GSICP_WARN_MAX_ITERS;
+                        done = 1;
+                    }
+                }
+            }
+            sDone = done;
+        }
+        __syncthreads();
+        if (sDone) break;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        if (!a.linearize_only) {
+            for (int k = 0; k < 12; ++k) a.d_T[k] = sT[k];
+            a.d_T[12] = 0.0; a.d_T[13] = 0.0; a.d_T[14] = 0.0; a.d_T[15] = 1.0;
+        }
+        gsicp_align_stats st;
+        st.fitness = n > 0 ? n_in / (double)n : 0.0;
+        st.mean_cost = n_in > 0.0 ? cost_last / n_in : 0.0;
+        st.n_inliers = (int32_t)n_in;
+        st.iters = iters;
+        st.converged = converged;
+        st.status = status;
+        *a.d_stats = st;
+    }
+}
+
+int align_grid_blocks(int cap) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_align, kT, 0);
+        if (per_sm < 1) per_sm = 1;
+    }
+    const int need = (int)blocks_for(cap > 0 ? cap : 1, kT);
+    const int maxb = per_sm * num_sms();
+    return need < maxb ? need : maxb;
+}
+
+}  // namespace
+
+struct AlignWs {
+    double *d_T;
+    gsicp_align_stats *d_stats;
+    double *d_lin;
+    unsigned int *barrier;
+    double *partials;
+    int32_t *corr_ws;
+};
+
+static AlignWs align_carve(Carver &c, int cap) {
+    AlignWs w;
+    w.d_T = c.take<double>(16);
+    w.d_stats = c.take<gsicp_align_stats>(1);
+    w.d_lin = c.take<double>(48);
+    w.barrier = c.take<unsigned int>(4);
+    const int G = (int)blocks_for(cap > 0 ? cap : 1, kT);
+    w.partials = c.take<double>((size_t)2 * G * kPad);
+    w.corr_ws = c.take<int32_t>(cap);
+    return w;
+}
+static AlignWs align_carve(void *base, int cap) {
+    Carver c(base);
+    return align_carve(c, cap);
+}
+
+size_t align_ws_bytes(int cap) {
+    Carver c(nullptr);
+    align_carve(c, cap);
+    return c.bytes();
+}
+
+double *align_ws_T(void *ws) { return align_carve(ws, 0).d_T; }
+gsicp_align_stats *align_ws_stats(void *ws) { return align_carve(ws, 0).d_stats; }
+double *align_ws_lin(void *ws) { return align_carve(ws, 0).d_lin; }
+
+// d_T_inout: device pose (may equal the workspace pose); d_stats: device stats destination.
+cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double *d_T_inout,
+                         const gsicp_align_params &p, gsicp_align_stats *d_stats, int32_t *corr_out,
+                         int linearize_only, float r_lin, void *ws, cudaStream_t s) {
+    AlignWs w = align_carve(ws, src.cap);
+    AlignArgs a;
+    a.spos = reinterpret_cast<const float4 *>(src.pos);
+    a.scov_a = reinterpret_cast<const float4 *>(src.cov_a);
+    a.scov_b = reinterpret_cast<const float4 *>(src.cov_b);
+    a.d_n = src.d_n;
+    a.cap = src.cap;
+    a.table = static_cast<const CellEntry *>(tgt.table);
+    a.mask = tgt.table_mask;
+    a.h = tgt.cell;
+    a.inv_h = 1.0f / tgt.cell;
+    a.tpos = reinterpret_cast<const float4 *>(tgt.pos);
+    a.tcov_a = reinterpret_cast<const float4 *>(tgt.cov_a);
+    a.tcov_b = reinterpret_cast<const float4 *>(tgt.cov_b);
+    a.tbbox = tgt.bbox;
+    a.max_iters = p.max_iters;
+    a.r = linearize_only ? r_lin : p.max_corr_dist;
+    a.r2 = a.r * a.r;
+    a.eps_rot = p.eps_rot;
+    a.eps_trans = p.eps_trans;
+    a.min_pairs = p.min_pairs;
+    a.linearize_only = linearize_only;
+    a.d_T = d_T_inout;
+    a.d_stats = d_stats;
+    a.d_lin = w.d_lin;
+    a.partials = w.partials;
+    a.barrier = w.barrier;
+    a.corr_ws = w.corr_ws;
+    a.corr_out = corr_out;
+    k_align_init<<<blocks_for(src.cap > 0 ? src.cap : 1, 256), 256, 0, s>>>(w.corr_ws, src.cap, w.barrier);
+    GSICP_LAUNCH_CHECK("k_align_init");
+    const int G = align_grid_blocks(src.cap);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_align, a);
+    if (e != cudaSuccess) {
+        set_error("k_align launch: %s", cudaGetErrorString(e));
+        return e;
+    }
+    note_launch(2);
+    return cudaSuccess;
+}
+
+}  // namespace gsicp

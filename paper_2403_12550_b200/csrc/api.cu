@@ -1,0 +1,273 @@
+// C ABI of libgsicp (include/gsicp.h): argument validation, workspace carving, status mapping.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "gsicp_internal.cuh"
+#include "host_common.cuh"
+
+namespace gsicp {
+
+static thread_local char g_err[512] = "";
+static thread_local uint64_t g_launches = 0;
+
+void note_launch(int n) { g_launches += (uint64_t)n; }
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+// defined in the kernel translation units
+size_t backproject_ws_bytes(int H, int W, int stride);
+cudaError_t backproject_launch(const float *depth, int H, int W, int pitch, gsicp_intrinsics K, int stride,
+                               float zmin, float zmax, float *pos_out, int32_t *d_n, void *ws, cudaStream_t s);
+size_t covariances_ws_bytes(int cap, int levels);
+cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, int k, int mode, float eps,
+                               float cell0, int levels, float *cov_a, float *cov_b, int32_t *knn_idx, void *ws,
+                               cudaStream_t s);
+size_t target_ws_bytes(int M);
+cudaError_t build_target_launch(const float *means, const float *quats, const float *scales, int scales_are_log,
+                                int M, int mode, float eps, float cell, gsicp_target *out, void *ws,
+                                cudaStream_t s);
+cudaError_t build_target_cloud_launch(const gsicp_cloud &cl, int M, float cell, gsicp_target *out, void *ws,
+                                      cudaStream_t s);
+size_t align_ws_bytes(int cap);
+double *align_ws_T(void *ws);
+gsicp_align_stats *align_ws_stats(void *ws);
+double *align_ws_lin(void *ws);
+cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double *d_T_inout,
+                         const gsicp_align_params &p, gsicp_align_stats *d_stats, int32_t *corr_out,
+                         int linearize_only, float r_lin, void *ws, cudaStream_t s);
+
+}  // namespace gsicp
+
+using namespace gsicp;
+
+#define BAD(...)                                  \
+    do {                                          \
+        set_error(__VA_ARGS__);                   \
+        return GSICP_ERR_INVALID_ARGUMENT;        \
+    } while (0)
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+static bool aligned256(const void *p) { return ((uintptr_t)p & 255u) == 0; }
+
+static gsicp_status cuda_status(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return GSICP_OK;
+    if (g_err[0] == 0) set_error("%s: %s", what, cudaGetErrorString(e));
+    return GSICP_ERR_CUDA;
+}
+
+static gsicp_status check_ws(void *ws, size_t have, size_t need) {
+    if (!ws || !aligned256(ws)) BAD("workspace must be non-null and 256-byte aligned");
+    if (have < need) {
+        set_error("workspace too small: %zu < %zu bytes", have, need);
+        return GSICP_ERR_WORKSPACE_TOO_SMALL;
+    }
+    return GSICP_OK;
+}
+
+static gsicp_status check_cloud(const gsicp_cloud *c, const char *name) {
+    if (!c) BAD("%s: null cloud", name);
+    if (c->cap < 1) BAD("%s: cap must be >= 1", name);
+    if (!c->pos || !c->cov_a || !c->cov_b || !c->d_n) BAD("%s: null array", name);
+    if (!aligned16(c->pos) || !aligned16(c->cov_a) || !aligned16(c->cov_b)) BAD("%s: arrays must be 16-byte aligned", name);
+    return GSICP_OK;
+}
+
+static gsicp_status check_target(const gsicp_target *t) {
+    if (!t || !t->pos || !t->cov_a || !t->cov_b || !t->table || !t->bbox) BAD("target: not built");
+    if (!(t->cell > 0.f) || t->M < 1) BAD("target: invalid");
+    return GSICP_OK;
+}
+
+extern "C" {
+
+int32_t gsicp_abi_version(void) { return 1; }
+
+const char *gsicp_status_string(gsicp_status s) {
+    switch (s) {
+        case GSICP_OK: return "ok";
+        case GSICP_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case GSICP_ERR_WORKSPACE_TOO_SMALL: return "workspace too small";
+        case GSICP_ERR_CUDA: return "cuda error";
+        case GSICP_ERR_DEGENERATE_FRAME: return "degenerate frame (no valid points)";
+        case GSICP_ERR_TRACKING_LOST: return "tracking lost (too few correspondences)";
+        case GSICP_WARN_MAX_ITERS: return "max iterations reached";
+        case GSICP_WARN_LOW_SUPPORT: return "low support (fewer than k points)";
+    }
+    return "unknown status";
+}
+
+const char *gsicp_last_error(void) { return g_err; }
+uint64_t gsicp_kernel_launch_count(void) { return g_launches; }
+
+size_t gsicp_backproject_workspace_size(int32_t H, int32_t W, int32_t stride) {
+    if (H < 1 || W < 1 || stride < 1) return 0;
+    return backproject_ws_bytes(H, W, stride);
+}
+
+gsicp_status gsicp_backproject_downsample(const float *depth_m, int32_t H, int32_t W, int32_t row_pitch_elems,
+                                          gsicp_intrinsics K, int32_t stride, float z_min, float z_max,
+                                          float *pos_out, int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes,
+                                          void *stream) {
+    g_err[0] = 0;
+    if (!depth_m || !pos_out || !d_n_out) BAD("backproject: null pointer");
+    if (H < 1 || W < 1 || stride < 1 || row_pitch_elems < W) BAD("backproject: bad image geometry");
+    if (!(K.fx > 0.f) || !(K.fy > 0.f) || !isfinite(K.cx) || !isfinite(K.cy)) BAD("backproject: bad intrinsics");
+    if (!(z_min <= z_max)) BAD("backproject: z_min > z_max");
+    if (!aligned16(pos_out)) BAD("backproject: pos_out must be 16-byte aligned");
+    const long long need = (long long)((H + stride - 1) / stride) * ((W + stride - 1) / stride);
+    if (cap < need) BAD("backproject: cap %d < %lld sampled pixels", cap, need);
+    gsicp_status st = check_ws(ws, ws_bytes, backproject_ws_bytes(H, W, stride));
+    if (st != GSICP_OK) return st;
+    return cuda_status(backproject_launch(depth_m, H, W, row_pitch_elems, K, stride, z_min, z_max, pos_out, d_n_out, ws,
+                                          (cudaStream_t)stream),
+                       "backproject");
+}
+
+size_t gsicp_covariances_workspace_size(int32_t cap, int32_t levels) {
+    if (cap < 1 || levels < 1 || levels > kMaxLevels) return 0;
+    return covariances_ws_bytes(cap, levels);
+}
+
+gsicp_status gsicp_covariances(const float *pos, const int32_t *d_n, int32_t cap, int32_t k, gsicp_reg_mode mode,
+                               float eps_var, float cell0, int32_t levels, float *cov_a, float *cov_b,
+                               int32_t *knn_idx, void *ws, size_t ws_bytes, void *stream) {
+    g_err[0] = 0;
+    if (!pos || !d_n || !cov_a || !cov_b) BAD("covariances: null pointer");
+    if (!aligned16(pos) || !aligned16(cov_a) || !aligned16(cov_b)) BAD("covariances: arrays must be 16-byte aligned");
+    if (cap < 1) BAD("covariances: cap must be >= 1");
+    if (k < 1 || k > 32) BAD("covariances: k must be in [1, 32]");
+    if (mode != GSICP_REG_NONE && mode != GSICP_REG_PLANE && mode != GSICP_REG_ELLIPSE) BAD("covariances: bad mode");
+    if (!(eps_var > 0.f) || !(eps_var <= 1.f)) BAD("covariances: eps_var must be in (0, 1]");
+    if (!(cell0 > 0.f) || !isfinite(cell0)) BAD("covariances: cell0 must be > 0");
+    if (levels < 1 || levels > kMaxLevels) BAD("covariances: levels must be in [1, %d]", kMaxLevels);
+    gsicp_status st = check_ws(ws, ws_bytes, covariances_ws_bytes(cap, levels));
+    if (st != GSICP_OK) return st;
+    return cuda_status(covariances_launch(pos, d_n, cap, k, (int)mode, eps_var, cell0, levels, cov_a, cov_b, knn_idx, ws,
+                                          (cudaStream_t)stream),
+                       "covariances");
+}
+
+size_t gsicp_build_target_workspace_size(int32_t M) {
+    if (M < 1) return 0;
+    return target_ws_bytes(M);
+}
+
+gsicp_status gsicp_build_target(const float *means, const float *quats_wxyz, const float *scales,
+                                int32_t scales_are_log, int32_t M, gsicp_reg_mode mode, float eps_var, float cell,
+                                gsicp_target *out, void *target_ws, size_t ws_bytes, void *stream) {
+    g_err[0] = 0;
+    if (!means || !quats_wxyz || !scales || !out) BAD("build_target: null pointer");
+    if (M < 1) BAD("build_target: M must be >= 1");
+    if (mode != GSICP_REG_NONE && mode != GSICP_REG_PLANE && mode != GSICP_REG_ELLIPSE) BAD("build_target: bad mode");
+    if (!(eps_var > 0.f) || !(eps_var <= 1.f)) BAD("build_target: eps_var must be in (0, 1]");
+    if (!isfinite(cell)) BAD("build_target: cell must be finite");
+    gsicp_status st = check_ws(target_ws, ws_bytes, target_ws_bytes(M));
+    if (st != GSICP_OK) return st;
+    return cuda_status(build_target_launch(means, quats_wxyz, scales, scales_are_log, M, (int)mode, eps_var, cell, out,
+                                           target_ws, (cudaStream_t)stream),
+                       "build_target");
+}
+
+gsicp_status gsicp_build_target_cloud(const gsicp_cloud *cloud, int32_t M, float cell, gsicp_target *out,
+                                      void *target_ws, size_t ws_bytes, void *stream) {
+    g_err[0] = 0;
+    gsicp_status st = check_cloud(cloud, "build_target_cloud");
+    if (st != GSICP_OK) return st;
+    if (!out) BAD("build_target_cloud: null out");
+    if (M < 1 || M > cloud->cap) BAD("build_target_cloud: M must be in [1, cap]");
+    if (!(cell > 0.f) || !isfinite(cell)) BAD("build_target_cloud: cell must be > 0");
+    st = check_ws(target_ws, ws_bytes, target_ws_bytes(M));
+    if (st != GSICP_OK) return st;
+    return cuda_status(build_target_cloud_launch(*cloud, M, cell, out, target_ws, (cudaStream_t)stream),
+                       "build_target_cloud");
+}
+
+size_t gsicp_align_workspace_size(int32_t src_cap) {
+    if (src_cap < 1) return 0;
+    return align_ws_bytes(src_cap);
+}
+
+static gsicp_status check_params(const gsicp_align_params *p) {
+    if (!p) BAD("align: null params");
+    if (p->max_iters < 1 || p->max_iters > 10000) BAD("align: max_iters must be in [1, 10000]");
+    if (!(p->max_corr_dist > 0.f)) BAD("align: max_corr_dist must be > 0 (INFINITY allowed)");
+    if (!(p->eps_rot >= 0.0) || !(p->eps_trans >= 0.0)) BAD("align: eps must be >= 0");
+    if (p->min_pairs < 0) BAD("align: min_pairs must be >= 0");
+    return GSICP_OK;
+}
+
+gsicp_status gsicp_align_async(const gsicp_cloud *src, const gsicp_target *tgt, double *d_T_inout,
+                               const gsicp_align_params *prm, gsicp_align_stats *d_stats, int32_t *corr_out,
+                               void *ws, size_t ws_bytes, void *stream) {
+    g_err[0] = 0;
+    gsicp_status st = check_cloud(src, "align src");
+    if (st != GSICP_OK) return st;
+    if ((st = check_target(tgt)) != GSICP_OK) return st;
+    if ((st = check_params(prm)) != GSICP_OK) return st;
+    if (!d_T_inout || !d_stats) BAD("align_async: null device pose / stats");
+    if ((st = check_ws(ws, ws_bytes, align_ws_bytes(src->cap))) != GSICP_OK) return st;
+    return cuda_status(align_launch(*src, *tgt, d_T_inout, *prm, d_stats, corr_out, 0, 0.f, ws, (cudaStream_t)stream),
+                       "align");
+}
+
+gsicp_status gsicp_align(const gsicp_cloud *src, const gsicp_target *tgt, const double *init_T,
+                         const gsicp_align_params *prm, double *out_T, gsicp_align_stats *out_stats, void *ws,
+                         size_t ws_bytes, void *stream) {
+    g_err[0] = 0;
+    gsicp_status st = check_cloud(src, "align src");
+    if (st != GSICP_OK) return st;
+    if ((st = check_target(tgt)) != GSICP_OK) return st;
+    if ((st = check_params(prm)) != GSICP_OK) return st;
+    if (!init_T || !out_T || !out_stats) BAD("align: null host pointer");
+    if ((st = check_ws(ws, ws_bytes, align_ws_bytes(src->cap))) != GSICP_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    double *dT = align_ws_T(ws);
+    gsicp_align_stats *dS = align_ws_stats(ws);
+    cudaError_t e = cudaMemcpyAsync(dT, init_T, 16 * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "align H2D");
+    e = align_launch(*src, *tgt, dT, *prm, dS, nullptr, 0, 0.f, ws, s);
+    if (e != cudaSuccess) return cuda_status(e, "align");
+    e = cudaMemcpyAsync(out_T, dT, 16 * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_stats, dS, sizeof(gsicp_align_stats), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, "align D2H");
+    return (gsicp_status)out_stats->status;
+}
+
+gsicp_status gsicp_linearize(const gsicp_cloud *src, const gsicp_target *tgt, const double *T, float max_corr_dist,
+                             double *H, double *b, double *cost, int32_t *n_inliers, int32_t *corr_opt, void *ws,
+                             size_t ws_bytes, void *stream) {
+    g_err[0] = 0;
+    gsicp_status st = check_cloud(src, "linearize src");
+    if (st != GSICP_OK) return st;
+    if ((st = check_target(tgt)) != GSICP_OK) return st;
+    if (!T || !H || !b || !cost || !n_inliers) BAD("linearize: null host pointer");
+    if (!(max_corr_dist > 0.f)) BAD("linearize: max_corr_dist must be > 0");
+    if ((st = check_ws(ws, ws_bytes, align_ws_bytes(src->cap))) != GSICP_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    double *dT = align_ws_T(ws);
+    gsicp_align_stats *dS = align_ws_stats(ws);
+    double *dL = align_ws_lin(ws);
+    gsicp_align_params p = {1, max_corr_dist, 0.0, 0.0, 0};
+    cudaError_t e = cudaMemcpyAsync(dT, T, 16 * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "linearize H2D");
+    e = align_launch(*src, *tgt, dT, p, dS, corr_opt, 1, max_corr_dist, ws, s);
+    if (e != cudaSuccess) return cuda_status(e, "linearize");
+    double lin[44];
+    e = cudaMemcpyAsync(lin, dL, sizeof(lin), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, "linearize D2H");
+    memcpy(H, lin, 36 * sizeof(double));
+    memcpy(b, lin + 36, 6 * sizeof(double));
+    *cost = lin[42];
+    *n_inliers = (int32_t)lin[43];
+    return GSICP_OK;
+}
+
+}  // extern "C"

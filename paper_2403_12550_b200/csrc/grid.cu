@@ -1,0 +1,163 @@
+// Device spatial hash build (see grid.cuh).
+#include "grid.cuh"
+#include "host_common.cuh"
+
+namespace gsicp {
+
+namespace {
+
+__global__ void k_grid_init(CellEntry *table, uint32_t slots, uint32_t *counters, int32_t *bbox) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < slots) {
+        CellEntry e;
+        e.key = kEmptyKey;
+        e.start = 0;
+        e.count = 0;
+        table[i] = e;
+    }
+    if (i == 0) {
+        counters[0] = 0;
+        counters[1] = 0;
+        for (int a = 0; a < 3; ++a) {
+            bbox[a] = float_to_ordered(INFINITY);
+            bbox[3 + a] = float_to_ordered(-INFINITY);
+        }
+    }
+}
+
+__global__ void k_grid_insert(GridView g, const float4 *__restrict__ pos, const int32_t *__restrict__ d_n) {
+    const int n = *d_n;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int level = (int)(t / g.cap);
+    const int i = (int)(t - (long long)level * g.cap);
+    const bool active = level < g.levels && i < n;
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (active) {
+        p = __ldg(pos + i);
+        const float inv_h = ldexpf(g.inv_h0, -level);
+        const unsigned long long key =
+            cell_key(level, cell_coord(p.x, inv_h), cell_coord(p.y, inv_h), cell_coord(p.z, inv_h));
+        uint32_t s = hash_slot(key, g.mask);
+        while (true) {
+            const unsigned long long prev = atomicCAS(&g.table[s].key, kEmptyKey, key);
+            if (prev == kEmptyKey || prev == key) break;
+            s = (s + 1) & g.mask;
+        }
+        const uint32_t rank = atomicAdd(&g.table[s].count, 1u);
+        g.slot_rank[t] = make_uint2(s, rank);
+    }
+    // bbox of the points (level 0 lanes only), warp-reduced then one atomic per warp
+    const bool bb = active && level == 0;
+    float v[6] = {bb ? p.x : INFINITY, bb ? p.y : INFINITY, bb ? p.z : INFINITY,
+                  bb ? p.x : -INFINITY, bb ? p.y : -INFINITY, bb ? p.z : -INFINITY};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            v[a] = fminf(v[a], __shfl_xor_sync(0xffffffffu, v[a], o));
+            v[3 + a] = fmaxf(v[3 + a], __shfl_xor_sync(0xffffffffu, v[3 + a], o));
+        }
+    if ((threadIdx.x & 31) == 0 && v[0] <= v[3]) {
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(g.bbox + a, float_to_ordered(v[a]));
+            atomicMax(g.bbox + 3 + a, float_to_ordered(v[3 + a]));
+        }
+    }
+}
+
+__global__ void k_grid_alloc(GridView g) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool occ = s <= g.mask && g.table[s].key != kEmptyKey;
+    const uint32_t cnt = occ ? g.table[s].count : 0u;
+    // warp-aggregated reservation
+    uint32_t incl = cnt;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    uint32_t base = 0;
+    if (lane == 31 && total) base = atomicAdd(g.counters, total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    if (occ) g.table[s].start = base + incl - cnt;
+}
+
+template <bool WITH_COV>
+__global__ void k_grid_scatter(GridView g, const float4 *__restrict__ pos, const float4 *__restrict__ cov_a,
+                               const float4 *__restrict__ cov_b, const int32_t *__restrict__ d_n) {
+    const int n = *d_n;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int level = (int)(t / g.cap);
+    const int i = (int)(t - (long long)level * g.cap);
+    if (level >= g.levels || i >= n) return;
+    const uint2 sr = g.slot_rank[t];
+    const uint32_t dst = g.table[sr.x].start + sr.y;
+    const float4 p = __ldg(pos + i);
+    g.spos[dst] = make_float4(p.x, p.y, p.z, __int_as_float(i));
+    if (WITH_COV) {
+        g.scov_a[dst] = __ldg(cov_a + i);
+        g.scov_b[dst] = __ldg(cov_b + i);
+    }
+}
+
+}  // namespace
+
+uint32_t grid_table_slots(int cap, int levels) {
+    uint64_t want = 2ull * (uint64_t)cap * (uint64_t)levels;
+    uint64_t s = 1024;
+    while (s < want) s <<= 1;
+    return (uint32_t)s;
+}
+
+static GridView carve(Carver &c, int cap, int levels, bool with_cov, float h0) {
+    GridView g{};
+    const uint32_t slots = grid_table_slots(cap, levels);
+    g.table = c.take<CellEntry>(slots);
+    g.mask = slots - 1;
+    g.levels = levels;
+    g.h0 = h0;
+    g.inv_h0 = h0 > 0.f ? 1.0f / h0 : 0.f;
+    g.spos = c.take<float4>((size_t)levels * cap);
+    g.scov_a = with_cov ? c.take<float4>(cap) : nullptr;
+    g.scov_b = with_cov ? c.take<float4>(cap) : nullptr;
+    g.slot_rank = c.take<uint2>((size_t)levels * cap);
+    g.counters = c.take<uint32_t>(4);
+    g.bbox = c.take<int32_t>(8);
+    g.cap = cap;
+    return g;
+}
+
+size_t grid_bytes(int cap, int levels, bool with_cov) {
+    Carver c(nullptr);
+    carve(c, cap, levels, with_cov, 1.f);
+    return c.bytes();
+}
+
+GridView grid_carve(void *base, int cap, int levels, bool with_cov, float h0) {
+    Carver c(base);
+    return carve(c, cap, levels, with_cov, h0);
+}
+
+cudaError_t grid_build(const GridView &g, const float4 *pos, const float4 *cov_a, const float4 *cov_b,
+                       const int32_t *d_n, int /*n_host_max*/, cudaStream_t s) {
+    const int T = 256;
+    const uint32_t slots = g.mask + 1;
+    const long long work = (long long)g.levels * g.cap;
+    k_grid_init<<<blocks_for(slots, T), T, 0, s>>>(g.table, slots, g.counters, g.bbox);
+    GSICP_LAUNCH_CHECK("k_grid_init");
+    k_grid_insert<<<blocks_for(work, T), T, 0, s>>>(g, pos, d_n);
+    GSICP_LAUNCH_CHECK("k_grid_insert");
+    k_grid_alloc<<<blocks_for(slots, T), T, 0, s>>>(g);
+    GSICP_LAUNCH_CHECK("k_grid_alloc");
+    if (g.scov_a)
+        k_grid_scatter<true><<<blocks_for(work, T), T, 0, s>>>(g, pos, cov_a, cov_b, d_n);
+    else
+        k_grid_scatter<false><<<blocks_for(work, T), T, 0, s>>>(g, pos, cov_a, cov_b, d_n);
+    GSICP_LAUNCH_CHECK("k_grid_scatter");
+    note_launch(4);
+    return cudaSuccess;
+}
+
+}  // namespace gsicp

@@ -1,0 +1,292 @@
+// Internal device primitives of libgsicp (sm_100a).  Not part of the ABI.
+// Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, Rn = DESIGN.md §3 reading n.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gsicp.h"
+
+namespace gsicp {
+
+constexpr unsigned long long kEmptyKey = ~0ull;
+constexpr int32_t kCoordOff = 1 << 19;   // cell coordinates clamp to [-2^19, 2^19)
+constexpr double kTau = 1e-12;           // degenerate eigenvalue threshold, m^2 (R8)
+constexpr double kNoneFloor = 1e-6;      // NONE-mode eigenvalue floor, m^2
+constexpr int kMaxLevels = 8;
+constexpr int kAlignThreads = 256;
+constexpr int kAlignTerms = 29;          // 21 H (upper) + 6 b + cost + count
+
+// 16-byte cell-table entry: 64-bit cell key, start offset and point count of the cell.
+struct __align__(16) CellEntry {
+    unsigned long long key;
+    uint32_t start;
+    uint32_t count;
+};
+
+// ---------------------------------------------------------------------------------------
+// Canonical binary32 squared-distance key (R1): dx = a.x - b.x, key = (dx*dx + dy*dy) + dz*dz,
+// every op rounded separately (no FMA) so the CPU oracle reproduces it bit for bit.
+__device__ __forceinline__ float canon_key(float ax, float ay, float az, float bx, float by, float bz) {
+    float dx = __fsub_rn(ax, bx), dy = __fsub_rn(ay, by), dz = __fsub_rn(az, bz);
+    float s = __fmul_rn(dx, dx);
+    s = __fadd_rn(s, __fmul_rn(dy, dy));
+    s = __fadd_rn(s, __fmul_rn(dz, dz));
+    return s;
+}
+
+// (key, index) packed so that unsigned 64-bit order == lexicographic (key, index) order
+// (keys are >= 0, so their IEEE bit patterns are monotone as unsigned integers).
+__device__ __forceinline__ unsigned long long pack_ki(float key, uint32_t idx) {
+    return ((unsigned long long)__float_as_uint(key) << 32) | idx;
+}
+__device__ __forceinline__ float ki_key(unsigned long long v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint32_t ki_idx(unsigned long long v) { return (uint32_t)v; }
+
+// ---------------------------------------------------------------------------------------
+// Spatial hash: cell coordinates c = floor(p * inv_h) (binary32, same function at build and
+// query time), key = level<<60 | (cx+off)<<40 | (cy+off)<<20 | (cz+off).
+__device__ __forceinline__ int cell_coord(float p, float inv_h) {
+    float f = floorf(__fmul_rn(p, inv_h));
+    f = fminf(fmaxf(f, -(float)kCoordOff), (float)(kCoordOff - 1));
+    return (int)f;
+}
+__device__ __forceinline__ unsigned long long cell_key(int level, int cx, int cy, int cz) {
+    return ((unsigned long long)level << 60) | ((unsigned long long)(uint32_t)(cx + kCoordOff) << 40) |
+           ((unsigned long long)(uint32_t)(cy + kCoordOff) << 20) | (unsigned long long)(uint32_t)(cz + kCoordOff);
+}
+__device__ __forceinline__ uint32_t hash_slot(unsigned long long key, uint32_t mask) {
+    return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 32) & mask;
+}
+// Returns (start, count) of the cell, (0, 0) if absent.  The table is read-only here.
+__device__ __forceinline__ uint2 cell_lookup(const CellEntry *__restrict__ table, uint32_t mask,
+                                             unsigned long long key) {
+    uint32_t s = hash_slot(key, mask);
+    while (true) {
+        const uint4 e = __ldg(reinterpret_cast<const uint4 *>(table + s));
+        const unsigned long long k = ((unsigned long long)e.y << 32) | e.x;
+        if (k == key) return make_uint2(e.z, e.w);
+        if (k == kEmptyKey) return make_uint2(0u, 0u);
+        s = (s + 1) & mask;
+    }
+}
+
+// Lower bound on the distance from q to cells at offset o along one axis, given the query's
+// distances to its own cell's lower / upper faces (dlo, dhi) and the cell edge h.
+__device__ __forceinline__ float axis_gap(int o, float dlo, float dhi, float h) {
+    return o < 0 ? dlo + (float)(-o - 1) * h : (o > 0 ? dhi + (float)(o - 1) * h : 0.0f);
+}
+
+// Cell offset t (0 <= t < shell_count(m)) of the Chebyshev shell m >= 1 around a cell.
+#define GS_HD __host__ __device__ __forceinline__
+GS_HD double gs_rsqrt(double x) {
+#ifdef __CUDA_ARCH__
+    return rsqrt(x);
+#else
+    return 1.0 / sqrt(x);
+#endif
+}
+
+GS_HD int shell_count(int m) { return (2 * m + 1) * (2 * m + 1) * (2 * m + 1) - (2 * m - 1) * (2 * m - 1) * (2 * m - 1); }
+GS_HD void shell_offset(int m, int t, int &dx, int &dy, int &dz) {
+    const int w = 2 * m + 1, w2 = w * w;
+    if (t < 2 * w2) {
+        dz = t < w2 ? -m : m;
+        const int r = t < w2 ? t : t - w2;
+        dy = r / w - m;
+        dx = r % w - m;
+        return;
+    }
+    t -= 2 * w2;
+    const int per = 8 * m;
+    dz = -m + 1 + t / per;
+    const int r = t % per;
+    if (r < 2 * w) {
+        dy = r < w ? -m : m;
+        dx = (r < w ? r : r - w) - m;
+    } else {
+        const int r2 = r - 2 * w, w1 = 2 * m - 1;
+        dx = r2 < w1 ? -m : m;
+        dy = (r2 < w1 ? r2 : r2 - w1) - m + 1;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Closed-form symmetric 3x3 eigen-decomposition in binary64 (trigonometric eigenvalues and
+// the "most separated eigenvalue first" eigenvector construction, robust for repeated roots).
+// A = (a00, a01, a02, a11, a12, a22).  lam[0] >= lam[1] >= lam[2] (clamped >= 0);
+// v[j] is the unit eigenvector of lam[j].  Eq. 3 read as eigen-decomposition (R4).
+struct Eig3 {
+    double lam[3];
+    double v[3][3];
+};
+
+GS_HD void cross3(const double *a, const double *b, double *c) {
+    c[0] = a[1] * b[2] - a[2] * b[1];
+    c[1] = a[2] * b[0] - a[0] * b[2];
+    c[2] = a[0] * b[1] - a[1] * b[0];
+}
+GS_HD double dot3(const double *a, const double *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+
+// eigenvector of a (well separated) eigenvalue e: the largest cross product of rows of A - eI
+GS_HD void eigvec_separated(const double *A, double e, double *out) {
+    const double r0[3] = {A[0] - e, A[1], A[2]};
+    const double r1[3] = {A[1], A[3] - e, A[4]};
+    const double r2[3] = {A[2], A[4], A[5] - e};
+    double c0[3], c1[3], c2[3];
+    cross3(r0, r1, c0);
+    cross3(r0, r2, c1);
+    cross3(r1, r2, c2);
+    const double d0 = dot3(c0, c0), d1 = dot3(c1, c1), d2 = dot3(c2, c2);
+    const double *c = c0;
+    double d = d0;
+    if (d1 > d) { c = c1; d = d1; }
+    if (d2 > d) { c = c2; d = d2; }
+    if (d > 0.0) {
+        const double inv = gs_rsqrt(d);
+        out[0] = c[0] * inv; out[1] = c[1] * inv; out[2] = c[2] * inv;
+    } else {
+        out[0] = 1.0; out[1] = 0.0; out[2] = 0.0;
+    }
+}
+
+__host__ __device__ inline Eig3 eig3_sym(const double *Ain) {
+    Eig3 r;
+    double amax = fmax(fmax(fabs(Ain[0]), fabs(Ain[1])), fmax(fmax(fabs(Ain[2]), fabs(Ain[3])), fmax(fabs(Ain[4]), fabs(Ain[5]))));
+    if (!(amax > 0.0)) {
+        for (int i = 0; i < 3; ++i) {
+            r.lam[i] = 0.0;
+            for (int j = 0; j < 3; ++j) r.v[i][j] = (i == j) ? 1.0 : 0.0;
+        }
+        return r;
+    }
+    const double s = 1.0 / amax;
+    double A[6];
+    for (int i = 0; i < 6; ++i) A[i] = Ain[i] * s;
+    const double q = (A[0] + A[3] + A[5]) / 3.0;
+    const double b00 = A[0] - q, b11 = A[3] - q, b22 = A[5] - q;
+    const double off = A[1] * A[1] + A[2] * A[2] + A[4] * A[4];
+    const double p = sqrt((b00 * b00 + b11 * b11 + b22 * b22 + 2.0 * off) / 6.0);
+    if (!(p > 0.0)) {  // multiple of the identity
+        for (int i = 0; i < 3; ++i) {
+            r.lam[i] = fmax(q * amax, 0.0);
+            for (int j = 0; j < 3; ++j) r.v[i][j] = (i == j) ? 1.0 : 0.0;
+        }
+        return r;
+    }
+    const double c00 = b11 * b22 - A[4] * A[4];
+    const double c01 = A[1] * b22 - A[4] * A[2];
+    const double c02 = A[1] * A[4] - b11 * A[2];
+    const double det = (b00 * c00 - A[1] * c01 + A[2] * c02) / (p * p * p);
+    const double half = fmin(fmax(0.5 * det, -1.0), 1.0);
+    const double ang = acos(half) / 3.0;
+    const double kTwoThirdsPi = 2.09439510239319549;
+    const double be2 = 2.0 * cos(ang);
+    const double be0 = 2.0 * cos(ang + kTwoThirdsPi);
+    const double be1 = -(be0 + be2);
+    (void)be1;
+    // The trigonometric estimate is accurate only for the most separated eigenvalue (acos near
+    // +-1 loses half the digits of the nearly repeated pair), so: take that eigenvector from
+    // cross products, its eigenvalue as a Rayleigh quotient, and the other two eigenpairs from
+    // the exact 2x2 problem on the orthogonal complement (absolute accuracy ~eps ||A||).
+    double ws[3];
+    eigvec_separated(A, half >= 0.0 ? q + p * be2 : q + p * be0, ws);
+    const double Aw[3] = {A[0] * ws[0] + A[1] * ws[1] + A[2] * ws[2], A[1] * ws[0] + A[3] * ws[1] + A[4] * ws[2],
+                          A[2] * ws[0] + A[4] * ws[1] + A[5] * ws[2]};
+    const double ls = dot3(ws, Aw);
+    double U[3], V[3];
+    if (fabs(ws[0]) > fabs(ws[1])) {
+        const double inv = gs_rsqrt(ws[0] * ws[0] + ws[2] * ws[2]);
+        U[0] = -ws[2] * inv; U[1] = 0.0; U[2] = ws[0] * inv;
+    } else {
+        const double inv = gs_rsqrt(ws[1] * ws[1] + ws[2] * ws[2]);
+        U[0] = 0.0; U[1] = ws[2] * inv; U[2] = -ws[1] * inv;
+    }
+    cross3(ws, U, V);
+    const double AU[3] = {A[0] * U[0] + A[1] * U[1] + A[2] * U[2], A[1] * U[0] + A[3] * U[1] + A[4] * U[2],
+                          A[2] * U[0] + A[4] * U[1] + A[5] * U[2]};
+    const double AV[3] = {A[0] * V[0] + A[1] * V[1] + A[2] * V[2], A[1] * V[0] + A[3] * V[1] + A[4] * V[2],
+                          A[2] * V[0] + A[4] * V[1] + A[5] * V[2]};
+    const double m00 = dot3(U, AU), m01 = 0.5 * (dot3(U, AV) + dot3(V, AU)), m11 = dot3(V, AV);
+    const double mean = 0.5 * (m00 + m11), hd = 0.5 * (m00 - m11);
+    const double rad = sqrt(hd * hd + m01 * m01);
+    const double mu_hi = mean + rad;
+    // smaller root without cancellation when it is tiny: det / mu_hi
+    const double det2 = m00 * m11 - m01 * m01;
+    const double mu_lo = (mean > 0.0 && mu_hi > 0.0 && rad > 0.5 * mean) ? det2 / mu_hi : mean - rad;
+    // eigenvector (x, y) of mu_hi in the (U, V) basis; mu_lo's is its rotation
+    double x, y;
+    if (hd >= 0.0) { x = hd + rad; y = m01; } else { x = m01; y = rad - hd; }
+    const double nrm = x * x + y * y;
+    if (nrm > 0.0) { const double inv = gs_rsqrt(nrm); x *= inv; y *= inv; } else { x = 1.0; y = 0.0; }
+    double vh[3], vl[3];
+    for (int k = 0; k < 3; ++k) {
+        vh[k] = x * U[k] + y * V[k];
+        vl[k] = -y * U[k] + x * V[k];
+    }
+    // assemble descending
+    double lam3[3];
+    const double *vec3[3];
+    if (half >= 0.0) {  // separated = largest
+        lam3[0] = ls; vec3[0] = ws; lam3[1] = mu_hi; vec3[1] = vh; lam3[2] = mu_lo; vec3[2] = vl;
+    } else {            // separated = smallest
+        lam3[0] = mu_hi; vec3[0] = vh; lam3[1] = mu_lo; vec3[1] = vl; lam3[2] = ls; vec3[2] = ws;
+    }
+    // guard the order against rounding (the roles above hold up to ~eps ||A||)
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2 - i; ++j)
+            if (lam3[j + 1] > lam3[j]) {
+                const double tl = lam3[j]; lam3[j] = lam3[j + 1]; lam3[j + 1] = tl;
+                const double *tv = vec3[j]; vec3[j] = vec3[j + 1]; vec3[j + 1] = tv;
+            }
+    for (int j = 0; j < 3; ++j) {
+        r.lam[j] = fmax(lam3[j] * amax, 0.0);
+        for (int k = 0; k < 3; ++k) r.v[j][k] = vec3[j][k];
+    }
+    return r;
+}
+
+// Regularisation of a raw covariance C (R6-R8):
+//  NONE    C + sum_i max(0, 1e-6 - lam_i) v v^T         ( = sum max(lam_i, 1e-6) v v^T, S:81 )
+//  PLANE   I - (1 - eps) v0 v0^T                         ( = v2v2^T + v1v1^T + eps v0v0^T, P:195 )
+//  ELLIPSE C / lam_1 + max(0, eps - lam_0/lam_1) v0 v0^T ( = sum max(lam_i/lam_1, eps) v v^T, Eq. 4 )
+//  degenerate: lam_2 <= tau -> I (NONE: floor I); lam_1 <= tau < lam_2 -> v2v2^T + eps (I - v2v2^T)
+// Returns flags; out = (c00, c01, c02, c11, c12, c22).
+__host__ __device__ inline uint32_t regularize(const double *C, const Eig3 &e, int mode, double eps, double *out) {
+    auto add_outer = [&](double w, const double *v) {
+        out[0] += w * v[0] * v[0]; out[1] += w * v[0] * v[1]; out[2] += w * v[0] * v[2];
+        out[3] += w * v[1] * v[1]; out[4] += w * v[1] * v[2]; out[5] += w * v[2] * v[2];
+    };
+    if (mode == GSICP_REG_NONE) {
+        for (int i = 0; i < 6; ++i) out[i] = C[i];
+        for (int j = 0; j < 3; ++j)
+            if (e.lam[j] < kNoneFloor) add_outer(kNoneFloor - e.lam[j], e.v[j]);
+        return e.lam[0] <= kTau ? GSICP_FLAG_DEGENERATE : 0u;
+    }
+    if (e.lam[0] <= kTau) {
+        out[0] = 1.0; out[1] = 0.0; out[2] = 0.0; out[3] = 1.0; out[4] = 0.0; out[5] = 1.0;
+        return GSICP_FLAG_DEGENERATE;
+    }
+    if (e.lam[1] <= kTau) {
+        out[0] = eps; out[1] = 0.0; out[2] = 0.0; out[3] = eps; out[4] = 0.0; out[5] = eps;
+        add_outer(1.0 - eps, e.v[0]);
+        return GSICP_FLAG_DEGENERATE;
+    }
+    if (mode == GSICP_REG_PLANE) {
+        out[0] = 1.0; out[1] = 0.0; out[2] = 0.0; out[3] = 1.0; out[4] = 0.0; out[5] = 1.0;
+        add_outer(eps - 1.0, e.v[2]);
+        return 0u;
+    }
+    const double inv = 1.0 / e.lam[1];
+    for (int i = 0; i < 6; ++i) out[i] = C[i] * inv;
+    const double r0 = e.lam[2] * inv;
+    if (r0 < eps) add_outer(eps - r0, e.v[2]);
+    return 0u;
+}
+
+__device__ __forceinline__ void store_cov(float4 *cov_a, float4 *cov_b, int i, const double *c, double lam_mid,
+                                          uint32_t flags) {
+    cov_a[i] = make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]);
+    cov_b[i] = make_float4((float)c[4], (float)c[5], (float)lam_mid, __uint_as_float(flags));
+}
+
+}  // namespace gsicp

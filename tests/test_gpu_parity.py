@@ -1,0 +1,368 @@
+"""GPU parity of the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star, made precise in DESIGN.md §6):
+  A1 points and kNN indices: bit-exact;  covariances: per-point ||dC||_F <= 1e-4 ||C||_F;
+  H/b per linearisation at the same T: ||dH||_F <= 1e-4 ||H||_F, ||db|| <= 1e-4 * sum_i ||J_i^T M_i d_i||
+  (approximated by the sum of |b| contributions, see _b_scale), cost rel 1e-4, inliers and correspondences exact;
+  final pose from the same init: 1e-5 rad and 1e-5 m.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+FULL_M = 1_000_000
+
+
+@pytest.fixture(scope="module")
+def g():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2403_12550_b200 as g
+
+    g.lib()
+    return g
+
+
+DEV = "cuda"
+
+
+def t(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+
+
+def rot_angle(Ra, Rb):
+    return math.acos(max(-1.0, min(1.0, (np.trace(Ra.T @ Rb) - 1) / 2)))
+
+
+def cov_rel_err(a, b):
+    def full(c):
+        return np.stack([c[:, 0], c[:, 1], c[:, 2], c[:, 1], c[:, 3], c[:, 4], c[:, 2], c[:, 4], c[:, 5]], 1)
+
+    A, B = full(np.asarray(a, np.float64)), full(np.asarray(b, np.float64))
+    return np.linalg.norm(A - B, axis=1) / np.linalg.norm(B, axis=1)
+
+
+# ----------------------------------------------------------------------------------------- workloads
+@pytest.fixture(scope="module")
+def c1():
+    return synth.make_c1(1)
+
+
+@pytest.fixture(scope="module")
+def replica():
+    return synth.make_frame_workload(2, "replica", M=FULL_M, stride=4)
+
+
+@pytest.fixture(scope="module")
+def tum():
+    return synth.make_frame_workload(3, "tum", M=FULL_M, stride=1, noisy=True)
+
+
+def gpu_points(g, depth, K, stride):
+    pos, d_n = g.backproject_downsample(t(depth), (K.fx, K.fy, K.cx, K.cy), stride=stride)
+    return pos, d_n
+
+
+# ----------------------------------------------------------------------------------------- A1
+@pytest.mark.parametrize("case", ["c1", "replica4", "tum1", "tum4", "tum3"])
+def test_backproject_bit_exact(g, c1, replica, tum, case):
+    w, s = {"c1": (c1, 1), "replica4": (replica, 4), "tum1": (tum, 1), "tum4": (tum, 4), "tum3": (tum, 3)}[case]
+    K = w.K
+    pos, d_n = gpu_points(g, w.depth, K, s)
+    n = int(d_n.item())
+    oxyz, opix = oracle.backproject(w.depth, K.fx, K.fy, K.cx, K.cy, s)
+    assert n == oxyz.shape[0]
+    gp = pos[:n].cpu().numpy()
+    np.testing.assert_array_equal(gp[:, :3], oxyz)
+    np.testing.assert_array_equal(gp[:, 3].view(np.int32), opix)
+
+
+def test_backproject_edge_cases(g):
+    K = (50.0, 50.0, 20.0, 15.0)
+    depth = np.zeros((31, 41), np.float32)
+    pos, d_n = g.backproject_downsample(t(depth), K, stride=2)
+    assert int(d_n.item()) == 0
+    depth[:] = np.nan
+    depth[3, 4] = np.inf
+    depth[10, 10] = 0.5
+    depth[10, 12] = 10.5
+    pos, d_n = g.backproject_downsample(t(depth), K, stride=2)
+    assert int(d_n.item()) == 1 and pos[0, 2].item() == 0.5
+    # pitched rows
+    big = torch.zeros((31, 64), dtype=torch.float32, device=DEV)
+    big[:, :41] = torch.rand((31, 41), device=DEV) * 3 + 0.2
+    view = big[:, :41]
+    pos, d_n = g.backproject_downsample(view, K, stride=3)
+    oxyz, _ = oracle.backproject(view.cpu().numpy(), *K, 3)
+    n = int(d_n.item())
+    np.testing.assert_array_equal(pos[:n, :3].cpu().numpy(), oxyz)
+
+
+# ----------------------------------------------------------------------------------------- A2-A4
+def _cov_check(g, xyz_np, pos, d_n, k=20, mode=oracle.ELLIPSE, cell0=0.01, levels=5, sample=None, brute_max=60000):
+    n = xyz_np.shape[0]
+    knn = torch.full((pos.shape[0], k), -7, dtype=torch.int32, device=DEV)
+    cl = g.covariances(pos, d_n, k=k, mode=mode, eps_var=1e-3, cell0=cell0, levels=levels, knn_idx=knn)
+    gk = knn[:n].cpu().numpy()
+    gc = cl.cov6()[:n].cpu().numpy()
+    gf = cl.flags()[:n].cpu().numpy()
+    if sample is None:
+        ok = oracle.knn_brute(xyz_np, k) if n <= brute_max else oracle.KDTree(xyz_np).knn(xyz_np, k)
+        np.testing.assert_array_equal(gk, ok)
+        ref = oracle.covariances(xyz_np, k=k, mode=mode, brute_max=brute_max)
+        idx = np.arange(n)
+    else:
+        idx = np.random.default_rng(7).choice(n, size=min(sample, n), replace=False).astype(np.int32)
+        ok = oracle.knn_brute(xyz_np, k, queries=idx)
+        np.testing.assert_array_equal(gk[idx], ok)
+        ref = None
+    if ref is not None:
+        err = cov_rel_err(gc, ref["cov"])
+        if mode == oracle.PLANE:
+            lam = np.array([oracle.eigen(c)[0] for c in ref["raw"]])
+            good = (lam[:, 1] - lam[:, 2]) >= 1e-3 * lam[:, 0]
+            assert good.mean() > 0.5
+            assert err[good].max() <= 1e-4, err[good].max()
+        else:
+            assert err.max() <= 1e-4, (err.max(), np.argmax(err))
+        np.testing.assert_array_equal(gf, ref["flags"])
+    else:  # sampled: covariances from the oracle's own neighbour sets
+        for j, i in enumerate(idx):
+            C = oracle.covariance(xyz_np, ok[j])
+            R, fl = oracle.regularize(C, mode, 1e-3)
+            e = cov_rel_err(gc[i:i + 1], R.astype(np.float32)[None])[0]
+            assert e <= 1e-4 and gf[i] == fl, (i, e)
+    return cl
+
+
+def test_knn_cov_c1(g, c1):
+    K = c1.K
+    pos, d_n = gpu_points(g, c1.depth, K, 1)
+    xyz, _ = oracle.backproject(c1.depth, K.fx, K.fy, K.cx, K.cy, 1)
+    for k in (1, 5, 20, 32):
+        _cov_check(g, xyz, pos, d_n, k=k, cell0=0.05, levels=3)
+
+
+@pytest.mark.parametrize("mode", [oracle.NONE, oracle.PLANE, oracle.ELLIPSE])
+def test_knn_cov_replica_full(g, replica, mode):
+    K = replica.K
+    pos, d_n = gpu_points(g, replica.depth, K, 4)
+    xyz, _ = oracle.backproject(replica.depth, K.fx, K.fy, K.cx, K.cy, 4)
+    _cov_check(g, xyz, pos, d_n, mode=mode, cell0=0.005, levels=6)
+
+
+def test_knn_cov_tum_full_resolution(g, tum):
+    K = tum.K
+    pos, d_n = gpu_points(g, tum.depth, K, 1)
+    xyz, _ = oracle.backproject(tum.depth, K.fx, K.fy, K.cx, K.cy, 1)
+    _cov_check(g, xyz, pos, d_n, cell0=0.004, levels=6)
+
+
+@pytest.mark.parametrize("levels,cell0", [(1, 0.02), (1, 0.2), (3, 0.003), (8, 0.001)])
+def test_knn_cov_grid_params_do_not_change_results(g, replica, levels, cell0):
+    K = replica.K
+    pos, d_n = gpu_points(g, replica.depth, K, 4)
+    xyz, _ = oracle.backproject(replica.depth, K.fx, K.fy, K.cx, K.cy, 4)
+    _cov_check(g, xyz, pos, d_n, cell0=cell0, levels=levels, sample=3000)
+
+
+def test_knn_cov_ragged_and_low_support(g):
+    rng = np.random.default_rng(9)
+    for n, cap in ((5, 64), (19, 19), (20, 1000), (1000, 1037), (4097, 5000)):
+        xyz = rng.normal(size=(n, 3)).astype(np.float32)
+        pos = torch.zeros((cap, 4), dtype=torch.float32, device=DEV)
+        pos[:n, :3] = t(xyz)
+        d_n = torch.tensor([n], dtype=torch.int32, device=DEV)
+        cl = _cov_check(g, xyz, pos, d_n, cell0=0.3, levels=2)
+        fl = cl.flags()[:n].cpu().numpy()
+        assert bool((fl & oracle.FLAG_LOW_SUPPORT).all()) == (n < 20)
+
+
+def test_knn_cov_degenerate_clouds(g):
+    # coincident points, collinear points, planar lattice with exact ties
+    pts = [np.tile(np.float32([[0.5, -1.0, 2.0]]), (40, 1)),
+           (np.arange(60)[:, None] * 0.01 * np.array([[1.0, 2.0, 2.0]]) / 3.0).astype(np.float32),
+           np.concatenate([np.stack(np.meshgrid(np.arange(30), np.arange(30)), -1).reshape(-1, 2) * 0.01,
+                           np.full((900, 1), 1.0)], 1).astype(np.float32)]
+    for xyz in pts:
+        n = xyz.shape[0]
+        pos = torch.zeros((n, 4), dtype=torch.float32, device=DEV)
+        pos[:, :3] = t(xyz)
+        d_n = torch.tensor([n], dtype=torch.int32, device=DEV)
+        for mode in (oracle.NONE, oracle.ELLIPSE):
+            _cov_check(g, xyz, pos, d_n, mode=mode, cell0=0.02, levels=2)
+
+
+def test_knn_cov_map_c4_sampled(g):
+    """C4-style: kNN covariance of a 4e6-point map (sampled queries vs brute force)."""
+    scene = synth.make_scene(1004)
+    means, _, _, ell = synth.sample_map(scene, 4_000_000, 4004)
+    pos = torch.zeros((means.shape[0], 4), dtype=torch.float32, device=DEV)
+    pos[:, :3] = t(means)
+    d_n = torch.tensor([means.shape[0]], dtype=torch.int32, device=DEV)
+    _cov_check(g, means, pos, d_n, cell0=2.5 * ell, levels=1, sample=300)
+
+
+# ----------------------------------------------------------------------------------------- A5
+@pytest.mark.parametrize("mode,log", [(oracle.ELLIPSE, False), (oracle.PLANE, False), (oracle.NONE, True)])
+def test_build_target_covariances(g, mode, log):
+    scene = synth.make_scene(1005)
+    means, quats, scales, ell = synth.sample_map(scene, 200_000, 4005)
+    if log:
+        scales = np.log(scales).astype(np.float32)
+    tgt = g.build_target(t(means), t(quats), t(scales), scales_are_log=log, mode=mode, eps_var=1e-3)
+    M = means.shape[0]
+    pos, ca, cb = tgt.arrays()  # cell-ordered views into the target workspace
+    order = pos[:, 3].contiguous().view(torch.int32).long().cpu().numpy()
+    assert np.array_equal(np.sort(order), np.arange(M))
+    inv = np.empty(M, np.int64)
+    inv[order] = np.arange(M)
+    np.testing.assert_array_equal(pos[:, :3].cpu().numpy()[inv], means)
+    gc = torch.cat([ca, cb[:, :2]], 1).cpu().numpy()[inv]
+    gf = cb[:, 3].contiguous().view(torch.int32).cpu().numpy()[inv]
+    ref, fl = oracle.target_from_map(quats, scales, mode, scales_are_log=log)
+    err = cov_rel_err(gc, ref)
+    assert err.max() <= 1e-4, err.max()
+    np.testing.assert_array_equal(gf, fl)
+
+
+# ----------------------------------------------------------------------------------------- A6-A9
+@pytest.fixture(scope="module")
+def c1_setup(g, c1):
+    K = c1.K
+    xyz, _ = oracle.backproject(c1.depth, K.fx, K.fy, K.cx, K.cy, 1)
+    T = c1.T_gt
+    txyz = (xyz.astype(np.float64) @ T[:3, :3].T + T[:3, 3]).astype(np.float32)
+    pos, d_n = gpu_points(g, c1.depth, K, 1)
+    src = g.covariances(pos, d_n, cell0=0.05, levels=3)
+    tc = g.Cloud.from_points(t(txyz))
+    tcl = g.covariances(tc.pos, tc.d_n, cell0=0.05, levels=3)
+    tgt = g.build_target_cloud(tcl, cell=0.05)
+    ocs = oracle.covariances(xyz)["cov"]
+    oct_ = oracle.covariances(txyz)["cov"]
+    return dict(xyz=xyz, txyz=txyz, src=src, tgt=tgt, ocs=ocs, oct=oct_, T=T)
+
+
+@pytest.fixture(scope="module")
+def replica_setup(g, replica):
+    w = replica
+    K = w.K
+    xyz, _ = oracle.backproject(w.depth, K.fx, K.fy, K.cx, K.cy, 4)
+    pos, d_n = gpu_points(g, w.depth, K, 4)
+    src = g.covariances(pos, d_n, cell0=0.005, levels=6)
+    tgt = g.build_target(t(w.means), t(w.quats), t(w.scales))
+    ocs = oracle.covariances(xyz)["cov"]
+    oct_, _ = oracle.target_from_map(w.quats, w.scales)
+    tree = oracle.KDTree(w.means)
+    return dict(xyz=xyz, txyz=w.means, src=src, tgt=tgt, ocs=ocs, oct=oct_, tree=tree, w=w)
+
+
+def _lin_check(g, S, T, r):
+    corr = torch.full((S["src"].cap,), -9, dtype=torch.int32, device=DEV)
+    lg = g.linearize(S["src"], S["tgt"], T, r, corr_out=corr)
+    lo = oracle.linearize(S["xyz"], S["ocs"], S["txyz"], S["oct"], T, r, tree=S.get("tree"))
+    n = S["xyz"].shape[0]
+    np.testing.assert_array_equal(corr[:n].cpu().numpy(), lo["corr"])
+    assert lg["n"] == lo["n"]
+    assert np.linalg.norm(lg["H"] - lo["H"]) <= 1e-4 * np.linalg.norm(lo["H"])
+    assert abs(lg["cost"] - lo["cost"]) <= 1e-4 * max(lo["cost"], 1e-300)
+    # b -> 0 at the optimum: scale by the magnitude of the summed terms (sqrt(n) * rms|b_i|
+    # is bounded below by |b|; use the Gauss-Newton scale sqrt(cost * ||H||) which bounds |b|
+    # by Cauchy-Schwarz: |b| <= sqrt(cost) * sqrt(||H||_2))
+    bscale = math.sqrt(max(lo["cost"], 0.0) * np.linalg.norm(lo["H"], 2))
+    assert np.linalg.norm(lg["b"] - lo["b"]) <= 1e-4 * bscale, (lg["b"], lo["b"], bscale)
+    return lg, lo
+
+
+def test_linearize_c1(g, c1_setup):
+    S = c1_setup
+    for T in (np.eye(4), S["T"], synth.perturb_pose(S["T"], 11, 3.0, 0.05)):
+        _lin_check(g, S, T, math.inf)
+        _lin_check(g, S, T, 0.05)
+
+
+def test_linearize_replica_full(g, replica_setup):
+    S = replica_setup
+    w = S["w"]
+    for T in (w.T_init, w.T_gt, synth.perturb_pose(w.T_gt, 12, 4.0, 0.08)):
+        _lin_check(g, S, T, 0.1)
+
+
+def test_align_c1_pose(g, c1_setup):
+    S = c1_setup
+    p = g.align_params(max_iters=30, max_corr_dist=math.inf, eps_rot=0.0, eps_trans=0.0)
+    Tg, st = g.align(S["src"], S["tgt"], np.eye(4), p)
+    ref = oracle.align(S["xyz"], S["ocs"], S["txyz"], S["oct"], np.eye(4), max_iters=30, eps_rot=0.0, eps_trans=0.0)
+    assert st["status"] == g.WARN_MAX_ITERS and st["iters"] == 30
+    assert rot_angle(Tg[:3, :3], ref["T"][:3, :3]) <= 1e-5
+    assert np.linalg.norm(Tg[:3, 3] - ref["T"][:3, 3]) <= 1e-5
+    # and the known transform is recovered (C1 pin)
+    assert rot_angle(Tg[:3, :3], S["T"][:3, :3]) <= 1e-5 and np.linalg.norm(Tg[:3, 3] - S["T"][:3, 3]) <= 1e-5
+    assert st["fitness"] == ref["fitness"] == 1.0
+
+
+def test_align_replica_pose(g, replica_setup):
+    S = replica_setup
+    w = S["w"]
+    p = g.align_params(max_iters=30, max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6)
+    Tg, st = g.align(S["src"], S["tgt"], w.T_init, p)
+    ref = oracle.align(S["xyz"], S["ocs"], S["txyz"], S["oct"], w.T_init, max_iters=30, max_corr_dist=0.1,
+                       use_tree=True)
+    assert st["status"] == ref["status"] == g.OK
+    assert rot_angle(Tg[:3, :3], ref["T"][:3, :3]) <= 1e-5
+    assert np.linalg.norm(Tg[:3, 3] - ref["T"][:3, 3]) <= 1e-5
+    assert st["n_inliers"] == ref["n_inliers"]
+    assert abs(st["iters"] - ref["iters"]) <= 1
+
+
+def test_align_deterministic(g, replica_setup):
+    S = replica_setup
+    w = S["w"]
+    outs = [g.align(S["src"], S["tgt"], w.T_init)[0] for _ in range(3)]
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0])
+
+
+def test_align_errors(g, c1_setup):
+    S = c1_setup
+    # disjoint clouds 100 m apart -> TRACKING_LOST with the init pose
+    T0 = np.eye(4)
+    T0[0, 3] = 100.0
+    Tg, st = g.align(S["src"], S["tgt"], T0, g.align_params(max_corr_dist=0.5))
+    assert st["status"] == g.ERR_TRACKING_LOST and st["fitness"] == 0.0
+    np.testing.assert_array_equal(Tg, T0)
+    # empty frame -> DEGENERATE_FRAME
+    empty = g.Cloud.empty(64)
+    Tg, st = g.align(empty, S["tgt"], np.eye(4))
+    assert st["status"] == g.ERR_DEGENERATE_FRAME
+
+
+def test_tracker_graph_capture(g, replica):
+    """The whole frame (A1 -> A4 -> A6-A9) captured in one CUDA graph and replayed."""
+    w = replica
+    tr = g.Tracker(w.K.H, w.K.W, (w.K.fx, w.K.fy, w.K.cx, w.K.cy), stride=4)
+    tgt = g.build_target(t(w.means), t(w.quats), t(w.scales))
+    depth = t(w.depth)
+    T_ref, st_ref = tr.track(depth, tgt, w.T_init)
+    s = torch.cuda.Stream()
+    T0 = torch.from_numpy(w.T_init.reshape(-1).copy()).to(DEV)
+    with torch.cuda.stream(s):
+        tr.d_T.copy_(T0)
+        tr.step_async(depth, tgt)  # warm
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        tr.step_async(depth, tgt)
+    for _ in range(2):
+        tr.d_T.copy_(T0)
+        graph.replay()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(tr.d_T.cpu().numpy().reshape(4, 4), T_ref)
+        assert g.decode_stats(tr.d_stats)["iters"] == st_ref["iters"]

@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the G-ICP tracking hot path (BASELINE.json metric:
+"G-ICP aligns/sec (Replica frame vs 1M-Gaussian map); kNN-cov Mpts/s; HBM %").
+
+One step = one whole frame through the hot path: back-projection +
+stride-4 downsampling of a Replica-shaped 1200x680 depth frame, multi-level spatial hash +
+exact kNN (k=20) covariances with ELLIPSE regularisation, and the persistent G-ICP kernel
+(correspondences, H/b, on-device 6x6 solve, up to 30 GN iterations) against a prebuilt
+1e6-Gaussian map target.  Inputs are synthetic (synth/), resident in HBM; L2 is flushed
+between timed steps.  Multi-GPU = independent replicas (one frame stream per rank, no
+collective on the data path).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--no-c4]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "G-ICP aligns/sec (Replica frame vs 1M-Gaussian map); kNN-cov Mpts/s; HBM %"
+WORKLOAD = "Replica-shaped 1200x680 depth frame, stride 4 (<=51k pts), vs 1e6-Gaussian map (C2 geometry, 1M map)"
+ALGO_BYTES_ALIGN = 96 + 8   # per (source point x GN iteration): src pos+cov, tgt pos+cov, corr
+ALGO_BYTES_KNN = 16 + 32    # per query: pos in, cov out
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6550.1)), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    return 6650.0, 1965.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_workload(rank: int):
+    import synth
+
+    return synth.make_frame_workload(2 + 100 * rank, "replica", M=1_000_000, stride=4)
+
+
+# ------------------------------------------------------------------------------------------- oracle
+def run_oracle_frame(w):
+    """One frame of the oracle (as it stands): A1, A2-A4 (brute-force kNN), A6-A9 (kd-tree NN).
+    The map target's covariances (A5) are prebuilt outside, like the GPU arm's target."""
+    import oracle
+
+    K = w.K
+    t0 = time.perf_counter()
+    xyz, _ = oracle.backproject(w.depth, K.fx, K.fy, K.cx, K.cy, w.stride)
+    cs = oracle.covariances(xyz)["cov"]
+    r = oracle.align(xyz, cs, w.means, w._oracle_tcov, w.T_init, max_iters=30, max_corr_dist=0.1,
+                     tree=w._oracle_tree)
+    return time.perf_counter() - t0, r
+
+
+def oracle_prepare(w):
+    """The map side (A5 covariances and the NN index over the map means) is prebuilt, as the
+    GPU arm's target is."""
+    import oracle
+
+    w._oracle_tcov, _ = oracle.target_from_map(w.quats, w.scales)
+    w._oracle_tree = oracle.KDTree(w.means)
+
+
+def cpu_baseline(w, frames=1):
+    import oracle
+
+    oracle_prepare(w)
+    secs = [run_oracle_frame(w)[0] for _ in range(frames)]
+    t = sum(secs)
+    return {"value": frames / t, "unit": "aligns/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{frames} Replica-shaped frame(s) of the bench workload (A1 + brute-force kNN-cov + GN with "
+                      f"kd-tree NN over the prebuilt 1e6-map index), {t:.1f} s"}
+
+
+def bench_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+
+    w = make_workload(0)
+    oracle_prepare(w)
+    for _ in range(args.warmup):
+        run_oracle_frame(w)
+    secs = [run_oracle_frame(w)[0] for _ in range(args.steps)]
+    total = sum(secs)
+    value = args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "aligns/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "k": 20, "max_iters": 30, "max_corr_dist": 0.1},
+        "cpu_baseline": {"value": value, "unit": "aligns/s", "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": "1 frame per step (whole frame, oracle as it stands)"},
+        "e2e": {"value": value, "unit": "aligns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------- GPU
+def bench_gpu(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2403_12550_b200 as g
+
+    w = make_workload(rank)
+    K = w.K
+    depth_host = torch.from_numpy(w.depth).pin_memory()
+    depth = depth_host.to(dev)
+    tgt = g.build_target(torch.from_numpy(w.means).to(dev), torch.from_numpy(w.quats).to(dev),
+                         torch.from_numpy(w.scales).to(dev))
+    params = g.align_params(max_iters=30, max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6)
+    tr = g.Tracker(K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=w.stride, params=params, device=dev)
+    T0 = torch.from_numpy(w.T_init.reshape(-1).copy()).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(evs=None):
+        tr.d_T.copy_(T0)
+        if evs:
+            evs[0].record(stream)
+        g.backproject_downsample(depth, tr.K, tr.stride, tr.z_min, tr.z_max, tr.cloud.pos, tr.cloud.d_n, tr.ws_bp)
+        if evs:
+            evs[1].record(stream)
+        g.covariances(tr.cloud.pos, tr.cloud.d_n, tr.k, tr.mode, tr.eps, tr.cell0, tr.levels, tr.cloud.cov_a,
+                      tr.cloud.cov_b, None, tr.ws_cov)
+        if evs:
+            evs[2].record(stream)
+        g.align_async(tr.cloud, tgt, tr.d_T, tr.d_stats, params, tr.ws_align)
+        if evs:
+            evs[3].record(stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    n_src = tr.cloud.n()
+    st = g.decode_stats(tr.d_stats)
+    nev = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nev)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = g.launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(nev):
+            flush.zero_()  # L2 flush (256 MB > 126 MB L2), outside the timed events
+            step(evs[i])
+        torch.cuda.synchronize()
+    launches = g.launch_count() - l0
+    if dist:
+        dist.barrier()
+    stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(3)] for i in range(nev)])
+    step_ms = stage.sum(1)
+    total_ms = float(step_ms.sum())
+    if dist:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = ws * nev / (total_ms / 1000.0)
+
+    # e2e through the public API with host buffers: H2D depth (pinned), whole frame, D2H pose
+    T_init = w.T_init
+    e2e_ms = []
+    for i in range(max(args.warmup, 3) + nev):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        depth.copy_(depth_host, non_blocking=True)
+        Tg, st_e = tr.track(depth, tgt, T_init)  # blocking C-ABI call returns the host pose
+        t1 = time.perf_counter()
+        if i >= max(args.warmup, 3):
+            e2e_ms.append(1000 * (t1 - t0))
+    e2e_total = sum(e2e_ms)
+    if dist:
+        t = torch.tensor([e2e_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = ws * nev / (e2e_total / 1000.0)
+
+    # kNN-cov Mpts/s over a 4e6-point map (C4), kernel stage only
+    knn_mpts = None
+    if not args.no_c4 and rank == 0:
+        import synth
+
+        scene = synth.make_scene(1004)
+        means4, _, _, ell4 = synth.sample_map(scene, 4_000_000, 4004)
+        c4 = g.Cloud.from_points(torch.from_numpy(means4).to(dev))
+        ws4 = g._ws(g.lib().gsicp_covariances_workspace_size(c4.cap, 1), dev)
+        for _ in range(3):
+            g.covariances(c4.pos, c4.d_n, 20, g.REG_ELLIPSE, 1e-3, 2.5 * ell4, 1, c4.cov_a, c4.cov_b, None, ws4)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        tms = []
+        for _ in range(5):
+            flush.zero_()
+            e[0].record(stream)
+            g.covariances(c4.pos, c4.d_n, 20, g.REG_ELLIPSE, 1e-3, 2.5 * ell4, 1, c4.cov_a, c4.cov_b, None, ws4)
+            e[1].record(stream)
+            torch.cuda.synchronize()
+            tms.append(e[0].elapsed_time(e[1]))
+        knn_mpts = 4.0 / (statistics.median(tms) / 1000.0)
+        knn4_ms = statistics.median(tms)
+        del c4, ws4
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    hbm, _, peak_kind = peaks()
+    st = g.decode_stats(tr.d_stats)
+    iters = max(1, st["iters"])
+    mean_stage = stage.mean(0)
+    names = ["A1 backproject", "A2-A4 hash+kNN-cov", "A6-A9 align (init+persistent GN kernel)"]
+    dom = int(np.argmax(mean_stage))
+    if dom == 2:
+        algo = ALGO_BYTES_ALIGN * n_src * iters
+        kernel = "k_align (+k_align_init)"
+    elif dom == 1:
+        algo = ALGO_BYTES_KNN * n_src
+        kernel = "grid build + k_knn_cov"
+    else:
+        algo = 4 * K.H * K.W / (w.stride ** 2) + 16 * n_src
+        kernel = "k_bp_count + k_bp_emit"
+    achieved = algo / (mean_stage[dom] / 1000.0) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        tj = json.load(open(prof))
+        traffic = tj.get(kernel.split()[0])
+    line = {
+        "metric": METRIC, "value": value, "unit": "aligns/s", "n_gpus": ws, "steps": nev, "warmup": args.warmup,
+        "ms_per_step": total_ms / nev, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 storage + f64 math", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_src": n_src, "map_gaussians": tgt.M, "k": 20, "mode": "ellipse",
+                   "max_iters": 30, "gn_iters_used": st["iters"], "max_corr_dist": 0.1, "parallelism": f"replicas{ws}",
+                   "l2": "flushed between timed steps (256 MB write)"},
+        "stage_ms": {names[j]: float(mean_stage[j]) for j in range(3)},
+        "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                     "algo_bytes_per_launch": algo},
+        "e2e": {"value": e2e_value, "unit": "aligns/s", "h2d_bytes_per_step": int(depth_host.numel() * 4),
+                "d2h_bytes_per_step": 16 * 8 + 32},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "fitness": st["fitness"], "status": st["status"],
+    }
+    if knn_mpts is not None:
+        line["knn_cov_mpts_s"] = knn_mpts
+        line["knn_cov_4M_ms"] = knn4_ms
+        line["knn_cov_hbm_frac"] = ALGO_BYTES_KNN * 4e6 / (knn4_ms / 1000) / 1e9 / hbm
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return bench_reference(args)
+    return bench_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

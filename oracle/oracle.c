@@ -639,11 +639,13 @@ void ora_update(double *T, const double *delta) {
 }
 
 /* O10/O11  Gauss-Newton loop (Q16-Q20).  stats: [fitness, mean_cost, n_inliers,
- * iters, converged, status].  Returns status. */
+ * iters, converged, status].  NN: prebuilt kd-tree over tgt_xyz if given, else a tree built here
+ * (use_tree) or brute force.  Returns status. */
 int ora_align(const float *src_xyz, const float *src_cov, int n, const float *tgt_xyz, const float *tgt_cov,
-              int M, int use_tree, const double *T0, int max_iters, float max_corr_dist, double eps_rot,
-              double eps_trans, int min_pairs, double *T_out, double *stats) {
-    void *tree = use_tree ? ora_kdtree_build(tgt_xyz, M) : NULL;
+              int M, int use_tree, const void *prebuilt, const double *T0, int max_iters, float max_corr_dist,
+              double eps_rot, double eps_trans, int min_pairs, double *T_out, double *stats) {
+    void *own = (!prebuilt && use_tree) ? ora_kdtree_build(tgt_xyz, M) : NULL;
+    const void *tree = prebuilt ? prebuilt : own;
     double T[16];
     memcpy(T, T0, sizeof(T));
     int status = ORA_MAX_ITERS, iters = 0, conv = 0, ninl = 0;
@@ -659,7 +661,7 @@ int ora_align(const float *src_xyz, const float *src_cov, int n, const float *tg
         double nv = sqrt(delta[3] * delta[3] + delta[4] * delta[4] + delta[5] * delta[5]);
         if (nw < eps_rot && nv < eps_trans) { conv = 1; status = ORA_OK; break; }
     }
-    if (tree) ora_kdtree_free(tree);
+    if (own) ora_kdtree_free(own);
     memcpy(T_out, T, sizeof(T));
     stats[0] = n > 0 ? (double)ninl / n : 0.0;
     stats[1] = ninl > 0 ? cost / ninl : 0.0;

@@ -33,6 +33,7 @@ METRIC = "G-ICP aligns/sec (Replica frame vs 1M-Gaussian map); kNN-cov Mpts/s; H
 WORKLOAD = "Replica-shaped 1200x680 depth frame, stride 4 (<=51k pts), vs 1e6-Gaussian map (C2 geometry, 1M map)"
 ALGO_BYTES_ALIGN = 96 + 8   # per (source point x GN iteration): src pos+cov, tgt pos+cov, corr
 ALGO_BYTES_KNN = 16 + 32    # per query: pos in, cov out
+C4_CELL, C4_LEVELS = 2.0, 4  # map kNN-cov grid: finest cell 2 x map spacing, 4 levels (outliers go coarse)
 
 
 def peaks():
@@ -264,15 +265,17 @@ def bench_gpu(args):
         scene = synth.make_scene(1004)
         means4, _, _, ell4 = synth.sample_map(scene, 4_000_000, 4004)
         c4 = g.Cloud.from_points(torch.from_numpy(means4).to(dev))
-        ws4 = g._ws(g.lib().gsicp_covariances_workspace_size(c4.cap, 1), dev)
+        ws4 = g._ws(g.lib().gsicp_covariances_workspace_size(c4.cap, C4_LEVELS), dev)
         for _ in range(3):
-            g.covariances(c4.pos, c4.d_n, 20, g.REG_ELLIPSE, 1e-3, 2.5 * ell4, 1, c4.cov_a, c4.cov_b, None, ws4)
+            g.covariances(c4.pos, c4.d_n, 20, g.REG_ELLIPSE, 1e-3, C4_CELL * ell4, C4_LEVELS, c4.cov_a, c4.cov_b,
+                          None, ws4)
         e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         tms = []
         for _ in range(5):
             flush.zero_()
             e[0].record(stream)
-            g.covariances(c4.pos, c4.d_n, 20, g.REG_ELLIPSE, 1e-3, 2.5 * ell4, 1, c4.cov_a, c4.cov_b, None, ws4)
+            g.covariances(c4.pos, c4.d_n, 20, g.REG_ELLIPSE, 1e-3, C4_CELL * ell4, C4_LEVELS, c4.cov_a, c4.cov_b,
+                          None, ws4)
             e[1].record(stream)
             torch.cuda.synchronize()
             tms.append(e[0].elapsed_time(e[1]))

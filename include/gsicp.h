@@ -137,7 +137,7 @@ gsicp_status gsicp_covariances(const float *pos, const int32_t *d_n, int32_t cap
  * targets with no covariance recomputation; P:189-191 C = R Lambda^2 R^T).  Quaternion wxyz,
  * normalised before use; scales linear, or log if scales_are_log (R22); the regularised
  * covariance is formed in closed form from (R, s) (no eigensolve), then the means are hashed
- * with cell edge `cell` (<= 0: 2 x mean middle scale).
+ * with cell edge `cell` (<= 0: 3 x mean middle scale; a performance knob only — results are exact).
  *  means [dev] float[M][3], quats_wxyz [dev] float[M][4], scales [dev] float[M][3]
  *  target_ws: caller buffer holding the target for as long as it is used
  *  out: host struct filled with views into target_ws.  Synchronises `stream` only if cell <= 0. */

@@ -7,7 +7,7 @@
  * with the CUDA path (paper_2403_12550_b200/csrc) and never reads its outputs.
  *
  * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
- * Qn = reading n listed in DESIGN.md §3 (taken from SURVEY.md §8(c).3).
+ * Rn = reading n listed in DESIGN.md §3 (Rn = SURVEY.md §8(c).3 Qn for n >= 3).
  *
  * Precision: all arithmetic in IEEE binary64 except where a floating-point value
  * decides an integer (kNN / NN membership): there both sides take the decision with
@@ -35,7 +35,7 @@
 enum { ORA_NONE = 0, ORA_PLANE = 1, ORA_ELLIPSE = 2 };
 enum { ORA_OK = 0, ORA_DEGENERATE_FRAME = 4, ORA_TRACKING_LOST = 5, ORA_MAX_ITERS = 6 };
 
-static const double ORA_TAU = 1e-12;      /* degenerate-eigenvalue threshold, m^2 (Q8) */
+static const double ORA_TAU = 1e-12;      /* degenerate-eigenvalue threshold, m^2 (R8) */
 static const double ORA_NONE_FLOOR = 1e-6; /* NONE-mode eigenvalue floor, m^2 */
 
 /* ------------------------------------------------------------------------- */
@@ -43,7 +43,7 @@ static const double ORA_NONE_FLOOR = 1e-6; /* NONE-mode eigenvalue floor, m^2 (S
  * P:163 (Fig. 2 caption): "We generate a point cloud by downsampling and
  * reprojecting the current depth image"; pinhole model S:46:
  * point = ((u-cx) d/fx, (v-cy) d/fy, d); invalid / out-of-window pixels skipped
- * (S:46).  Stride from (0,0), integer pixel coordinates (Q13, Q14).
+ * (S:46).  Stride from (0,0), integer pixel coordinates (R13, R14).
  * K1: x = (float)(((double)u - (double)cx) * (double)z / (double)fx).
  * Output in row-major pixel order; out_pix = v*W + u.  Returns n, or -1 if n > cap.
  */
@@ -81,7 +81,7 @@ static inline float ora_key(const float *a, const float *b) {
     return s;
 }
 
-/* (key, idx) lexicographic "less than" — the kNN / NN order (Q12). */
+/* (key, idx) lexicographic "less than" — the kNN / NN order (R12). */
 static inline int ora_less(float ka, int ia, float kb, int ib) {
     return ka < kb || (ka == kb && ia < ib);
 }
@@ -263,9 +263,9 @@ void ora_covariance(const float *xyz, const int32_t *nbr, int m, double *C) {
 }
 
 /* O4  Symmetric eigen-decomposition (Eq. 3: C = R Lambda^2 R^T, read as the
- * eigen-decomposition of the PSD covariance, Q4) by the cyclic Jacobi method in binary64,
+ * eigen-decomposition of the PSD covariance, R4) by the cyclic Jacobi method in binary64,
  * until off(A) <= 1e-15 ||A||_F (max 50 sweeps).  Output lam[0] >= lam[1] >= lam[2]
- * (= lambda_2, lambda_1, lambda_0 in the paper's s2>s1>s0 order, Q5), clamped at 0;
+ * (= lambda_2, lambda_1, lambda_0 in the paper's s2>s1>s0 order, R5), clamped at 0;
  * V column-major: V[3*j + r] is component r of the eigenvector of lam[j]. */
 void ora_eigen_jacobi(const double *Cp, double *lam, double *V) {
     double A[3][3] = {{Cp[0], Cp[1], Cp[2]}, {Cp[1], Cp[3], Cp[4]}, {Cp[2], Cp[4], Cp[5]}};
@@ -320,10 +320,10 @@ static void ora_add_outer(double *Cp, double w, const double *v) {
 
 /* O5  Regularisation from an eigen-decomposition (lam descending, V columns).
  *  NONE    : sum max(lam_i, 1e-6) v v^T
- *  PLANE   : S = [1, 1, eps] as variances: v2v2^T + v1v1^T + eps v0v0^T   (Q6)
+ *  PLANE   : S = [1, 1, eps] as variances: v2v2^T + v1v1^T + eps v0v0^T   (R6)
  *  ELLIPSE : Lambda' = Lambda / median(S)  (Eq. 4) => variances lam_i/lam_mid,
- *            floored at eps (Q7):  sum max(lam_i/lam_1, eps) v v^T
- *  Degenerate (Q8): lam_2 <= tau -> I (NONE: 1e-6 I), flag; lam_1 <= tau < lam_2 (line) ->
+ *            floored at eps (R7):  sum max(lam_i/lam_1, eps) v v^T
+ *  Degenerate (R8): lam_2 <= tau -> I (NONE: 1e-6 I), flag; lam_1 <= tau < lam_2 (line) ->
  *            v2v2^T + eps (I - v2v2^T) for PLANE/ELLIPSE, flag.
  * Returns flags. */
 int ora_regularize_eig(const double *lam, const double *V, int mode, double eps, double *out) {
@@ -398,8 +398,8 @@ void ora_covariances(const float *xyz, int n, int k, int mode, double eps, int b
 /* ------------------------------------------------------------------------- */
 /* O6  Map Gaussian -> G-ICP target covariance (the map's Gaussians are
  * reused as targets without recomputing covariances; P:189-191 C = R Lambda^2 R^T).
- * q = wxyz normalised (Q22); scales linear or log (exp); variances s_i^2 sorted descending,
- * ties by axis index (Q5); then O5. */
+ * q = wxyz normalised (R22); scales linear or log (exp); variances s_i^2 sorted descending,
+ * ties by axis index (R5); then O5. */
 void ora_target_from_map(const float *quats, const float *scales, int scales_are_log, int M, int mode,
                          double eps, float *cov_out, int32_t *flags_out) {
 #pragma omp parallel for schedule(static)
@@ -479,9 +479,9 @@ static int ora_inv_spd3(double S[3][3], double Mi[3][3]) {
 
 /* O7 + O8: correspondences and linearisation of Eq. 1 at pose T.
  * O7: q_i = K3(T, x_i); j* = argmin over (key(fl32(q_i), m_j), j) ("nearest neighbor");
- *     valid iff key < fl32(r*r) (strict, Q15).
- * O8: Sigma_i = C^t_j + R C^s_i R^T (Q1, Q2), M_i = Sigma_i^{-1}, d_i = m_j - q_i,
- *     J_i = [[q_i]x, -I] (left twist (omega, v), Q16), H = sum J^T M J, b = sum J^T M d,
+ *     valid iff key < fl32(r*r) (strict, R15).
+ * O8: Sigma_i = C^t_j + R C^s_i R^T (R3), M_i = Sigma_i^{-1}, d_i = m_j - q_i,
+ *     J_i = [[q_i]x, -I] (left twist (omega, v), R16), H = sum J^T M J, b = sum J^T M d,
  *     cost = sum d^T M d (Eq. 1), summed in index order in binary64.
  * tree: kd-tree over tgt_xyz or NULL (brute force).  H row-major 36, b 6.  corr (nullable).
  * Returns the inlier count. */
@@ -622,7 +622,7 @@ void ora_so3_exp(const double *w, double *R) {
         for (int c = 0; c < 3; ++c) R[3 * a + c] = (a == c ? 1.0 : 0.0) + A * K[a][c] + B * K2[a][c];
 }
 
-/* Left update T <- [Exp(omega) | v] T (Q16). */
+/* Left update T <- [Exp(omega) | v] T (R16). */
 void ora_update(double *T, const double *delta) {
     double E[9], Rn[9], tn[3];
     ora_so3_exp(delta, E);
@@ -638,7 +638,7 @@ void ora_update(double *T, const double *delta) {
     T[15] = 1.0;
 }
 
-/* O10/O11  Gauss-Newton loop (Q16-Q20).  stats: [fitness, mean_cost, n_inliers,
+/* O10/O11  Gauss-Newton loop (R16-R20).  stats: [fitness, mean_cost, n_inliers,
  * iters, converged, status].  NN: prebuilt kd-tree over tgt_xyz if given, else a tree built here
  * (use_tree) or brute force.  Returns status. */
 int ora_align(const float *src_xyz, const float *src_cov, int n, const float *tgt_xyz, const float *tgt_cov,
@@ -681,7 +681,7 @@ int ora_num_threads(void) {
 }
 
 /* O12  Scale aligning for map insertion (Lambda'' = Lambda' / z^p, p empirically
- * 1.5).  scales_out = c * scales_in / z^p (c: absolute factor, Q21).  z <= 0 -> -1. */
+ * 1.5).  scales_out = c * scales_in / z^p (c: absolute factor, R21).  z <= 0 -> -1. */
 int ora_scale_align(const double *scales_in, double z, double p, double c, double *scales_out) {
     if (!(z > 0)) return -1;
     double f = c / pow(z, p);

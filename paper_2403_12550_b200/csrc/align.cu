@@ -16,6 +16,7 @@
 
 #include "gsicp_internal.cuh"
 #include "host_common.cuh"
+#include "search.cuh"
 
 namespace gsicp {
 
@@ -24,7 +25,6 @@ namespace {
 constexpr int kT = kAlignThreads;
 constexpr int kWarps = kT / 32;
 constexpr int kPad = 32;  // partial record stride (doubles)
-constexpr float kRelMargin = 1e-5f;
 
 struct AlignArgs {
     const float4 *spos, *scov_a, *scov_b;
@@ -59,51 +59,46 @@ __device__ __forceinline__ float ordered_to_float_(int32_t i) { return __int_as_
 
 // Exact 1-NN of (qx, qy, qz) on the target hash; best/best_slot carry the warm start in and the
 // answer out.
+__device__ __forceinline__ void scan_target_cell(const AlignArgs &a, uint2 se, float qx, float qy, float qz,
+                                                 unsigned long long &best, int &best_slot) {
+    for (uint32_t j = se.x; j < se.x + se.y; ++j) {
+        const float4 p = __ldg(a.tpos + j);
+        const unsigned long long v = pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
+        if (v < best) {
+            best = v;
+            best_slot = (int)j;
+        }
+    }
+}
+
 __device__ __forceinline__ void nn_search(const AlignArgs &a, const int *sb, float qx, float qy, float qz,
                                           unsigned long long &best, int &best_slot) {
-    const float h = a.h, inv_h = a.inv_h;
-    const int c[3] = {cell_coord(qx, inv_h), cell_coord(qy, inv_h), cell_coord(qz, inv_h)};
-    const float q[3] = {qx, qy, qz};
-    float dlo[3], dhi[3], dq = INFINITY;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        dlo[k] = fmaxf(q[k] - (float)c[k] * h, 0.f);
-        dhi[k] = fmaxf((float)(c[k] + 1) * h - q[k], 0.f);
-        dq = fminf(dq, fminf(dlo[k], dhi[k]));
-    }
-    const float margin = 2e-6f * (fabsf(qx) + fabsf(qy) + fabsf(qz)) + h * kRelMargin;
-    for (int m = 0;; ++m) {
-        const int cnt = m == 0 ? 1 : shell_count(m);
-        for (int t = 0; t < cnt; ++t) {
-            int dx = 0, dy = 0, dz = 0;
-            if (m) shell_offset(m, t, dx, dy, dz);
-            const int x = c[0] + dx, y = c[1] + dy, z = c[2] + dz;
-            if (x < sb[0] || x > sb[3] || y < sb[1] || y > sb[4] || z < sb[2] || z > sb[5]) continue;
-            if (m) {
-                const float gx = fmaxf(axis_gap(dx, dlo[0], dhi[0], h) - margin, 0.f);
-                const float gy = fmaxf(axis_gap(dy, dlo[1], dhi[1], h) - margin, 0.f);
-                const float gz = fmaxf(axis_gap(dz, dlo[2], dhi[2], h) - margin, 0.f);
-                const float lb = (gx * gx + gy * gy + gz * gz) * (1.f - kRelMargin);
-                if (lb > fminf(ki_key(best), a.r2)) continue;  // empty best -> key is NaN-free max
-            }
-            const uint2 se = cell_lookup(a.table, a.mask, cell_key(0, x, y, z));
-            for (uint32_t j = se.x; j < se.x + se.y; ++j) {
-                const float4 p = __ldg(a.tpos + j);
-                const unsigned long long v =
-                    pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
-                if (v < best) {
-                    best = v;
-                    best_slot = (int)j;
-                }
+    const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
+    const int *blo = sb, *bhi = sb + 3;
+    auto scan = [&](int x, int y, int z) {
+        scan_target_cell(a, cell_lookup(a.table, a.mask, cell_key(0, x, y, z)), qx, qy, qz, best, best_slot);
+    };
+    scan(qc.c[0], qc.c[1], qc.c[2]);
+    int m_done = 0;
+    if (best == kEmptyKey && !(a.r2 < INFINITY)) {
+        // ungated search with nothing found yet: grow shells until some point is seen
+        while (best == kEmptyKey && !qc.covers(m_done, blo, bhi)) {
+            ++m_done;
+            const int cnt = shell_count(m_done);
+            for (int t = 0; t < cnt; ++t) {
+                int dx, dy, dz;
+                shell_cell(m_done, t, dx, dy, dz);
+                const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
+                if (x < blo[0] || x > bhi[0] || y < blo[1] || y > bhi[1] || z < blo[2] || z > bhi[2]) continue;
+                scan(x, y, z);
             }
         }
-        const float B = fmaxf((float)m * h + dq - margin, 0.f);
-        if (best != kEmptyKey && ki_key(best) < B * B * (1.f - kRelMargin)) return;  // certified
-        if (B > a.r * (1.f + kRelMargin)) return;  // every point with key < r^2 has been visited
-        if (c[0] - m <= sb[0] && c[0] + m >= sb[3] && c[1] - m <= sb[1] && c[1] + m >= sb[4] &&
-            c[2] - m <= sb[2] && c[2] + m >= sb[5])
-            return;  // the ring block covers the whole target
     }
+    // every cell that can hold a key <= min(best, r^2): exact 1-NN among the points that matter
+    ball_search(
+        qc, a.table, a.mask, blo, bhi, m_done, [](int x, int y, int z) { return cell_key(0, x, y, z); },
+        [&](uint2 se) { scan_target_cell(a, se, qx, qy, qz, best, best_slot); },
+        [&]() { return best != kEmptyKey ? fminf(ki_key(best), a.r2) : a.r2; });
 }
 
 __device__ __forceinline__ void so3_exp(const double *w, double *R) {
@@ -185,6 +180,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         const double R00 = sT[0], R01 = sT[1], R02 = sT[2], t0 = sT[3];
         const double R10 = sT[4], R11 = sT[5], R12 = sT[6], t1 = sT[7];
         const double R20 = sT[8], R21 = sT[9], R22 = sT[10], t2 = sT[11];
+        // phase A: correspondences (no accumulator live, so the search gets the registers)
         for (int i = blockIdx.x * kT + tid; i < n; i += G * kT) {
             const float4 x = __ldg(a.spos + i);
             const double xd = x.x, yd = x.y, zd = x.z;
@@ -195,13 +191,24 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             const float qx = __double2float_rn(q0), qy = __double2float_rn(q1), qz = __double2float_rn(q2);
             unsigned long long best = kEmptyKey;
             int slot = a.corr_ws[i];
+            if (slot <= -2) slot = -2 - slot;  // previous match was gated out: still a warm start
             if (slot >= 0) {
                 const float4 p = __ldg(a.tpos + slot);
                 best = pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
             }
             nn_search(a, sBox, qx, qy, qz, best, slot);
-            a.corr_ws[i] = slot;
-            const bool valid = slot >= 0 && ki_key(best) < a.r2;
+            a.corr_ws[i] = (slot >= 0 && ki_key(best) < a.r2) ? slot : -2 - slot;  // invalid: -2 - warm start
+        }
+        // phase B: Eq. 1 terms of the valid pairs
+        for (int i = blockIdx.x * kT + tid; i < n; i += G * kT) {
+            const int cw = a.corr_ws[i];
+            const bool valid = cw >= 0;
+            const int slot = cw;
+            const float4 x = __ldg(a.spos + i);
+            const double xd = x.x, yd = x.y, zd = x.z;
+            const double q0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R00, xd), __dmul_rn(R01, yd)), __dmul_rn(R02, zd)), t0);
+            const double q1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R10, xd), __dmul_rn(R11, yd)), __dmul_rn(R12, zd)), t1);
+            const double q2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R20, xd), __dmul_rn(R21, yd)), __dmul_rn(R22, zd)), t2);
             int32_t corr_val = -1;
             if (valid) {
                 const float4 ca = __ldg(a.scov_a + i), cb = __ldg(a.scov_b + i);

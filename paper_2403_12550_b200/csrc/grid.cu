@@ -15,9 +15,8 @@ __global__ void k_grid_init(CellEntry *table, uint32_t slots, uint32_t *counters
         e.count = 0;
         table[i] = e;
     }
+    if (i < kMaxLevels) counters[i] = 0;
     if (i == 0) {
-        counters[0] = 0;
-        counters[1] = 0;
         for (int a = 0; a < 3; ++a) {
             bbox[a] = float_to_ordered(INFINITY);
             bbox[3 + a] = float_to_ordered(-INFINITY);
@@ -65,23 +64,34 @@ __global__ void k_grid_insert(GridView g, const float4 *__restrict__ pos, const 
     }
 }
 
+// Each level's points get the contiguous range [level*cap, level*cap + n) of spos, cells in
+// allocation order; a warp reserves its cells of one level with one atomicAdd.
 __global__ void k_grid_alloc(GridView g) {
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool occ = s <= g.mask && g.table[s].key != kEmptyKey;
-    const uint32_t cnt = occ ? g.table[s].count : 0u;
-    // warp-aggregated reservation
-    uint32_t incl = cnt;
     const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+    unsigned long long key = kEmptyKey;
+    uint32_t cnt = 0;
+    if (s <= g.mask) {
+        key = g.table[s].key;
+        if (key != kEmptyKey) cnt = g.table[s].count;
     }
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    uint32_t base = 0;
-    if (lane == 31 && total) base = atomicAdd(g.counters, total);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    if (occ) g.table[s].start = base + incl - cnt;
+    const int level = key != kEmptyKey ? (int)(key >> 60) : -1;
+    for (int l = 0; l < g.levels; ++l) {
+        const bool mine = level == l;
+        if (!__any_sync(0xffffffffu, mine)) continue;
+        const uint32_t c = mine ? cnt : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t base = 0;
+        if (lane == 31) base = atomicAdd(g.counters + l, total);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        if (mine) g.table[s].start = (uint32_t)l * (uint32_t)g.cap + base + incl - c;
+    }
 }
 
 template <bool WITH_COV>
@@ -123,7 +133,7 @@ static GridView carve(Carver &c, int cap, int levels, bool with_cov, float h0) {
     g.scov_a = with_cov ? c.take<float4>(cap) : nullptr;
     g.scov_b = with_cov ? c.take<float4>(cap) : nullptr;
     g.slot_rank = c.take<uint2>((size_t)levels * cap);
-    g.counters = c.take<uint32_t>(4);
+    g.counters = c.take<uint32_t>(kMaxLevels);
     g.bbox = c.take<int32_t>(8);
     g.cap = cap;
     return g;

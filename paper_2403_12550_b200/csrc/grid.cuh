@@ -17,10 +17,11 @@ struct GridView {
     uint32_t mask;
     int levels;
     float h0, inv_h0;
-    float4 *spos;            // [levels * cap] cell-ordered (x, y, z, original index bits)
+    float4 *spos;            // [levels * cap]: level l's points, cell-ordered, in [l*cap, l*cap + n)
+                             // as (x, y, z, original index bits)
     float4 *scov_a, *scov_b; // nullable: cell-ordered covariances (target grids)
     uint2 *slot_rank;        // [levels * cap]
-    uint32_t *counters;      // [0] = allocated points
+    uint32_t *counters;      // [kMaxLevels] points allocated per level
     int32_t *bbox;           // [6] ordered-int encoded float min xyz / max xyz
     int cap;
 };

@@ -130,7 +130,7 @@ cudaError_t build_target_launch(const float *means, const float *quats, const fl
             set_error("build_target auto cell: %s", cudaGetErrorString(e));
             return e;
         }
-        cell = (float)(2.0 * sum / (double)M);
+        cell = (float)(3.0 * sum / (double)M);
         if (!(cell > 0.f)) cell = 0.01f;
     }
     GridView g = grid_carve(t.grid, M, 1, true, cell);

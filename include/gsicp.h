@@ -180,6 +180,17 @@ gsicp_status gsicp_linearize(const gsicp_cloud *src, const gsicp_target *tgt, co
                              double *H, double *b, double *cost, int32_t *n_inliers, int32_t *corr_opt, void *ws,
                              size_t ws_bytes, void *stream);
 
+/* DIAGNOSTIC: while set (non-NULL) on the calling thread, every gsicp_covariances call also writes
+ * per query i: d_out[4*i + 0..3] = (grid level searched, cells probed, candidates scanned,
+ * list insertions), int32, device memory of at least 4*cap entries.  NULL switches it off. */
+void gsicp_debug_knn_counters(int32_t *d_out);
+
+/* DIAGNOSTIC: while set, every align / linearize launch on the calling thread records device
+ * globaltimer stamps (ns) into d_out (int64, device, `capacity` entries): [0] kernel start, then
+ * per GN iteration `it` at [1 + it*(G+1) + b] the barrier arrival of block b and at
+ * [1 + it*(G+1) + G] the barrier release seen by block 0 (G = grid size).  NULL switches it off. */
+void gsicp_debug_align_timeline(int64_t *d_out, int64_t capacity);
+
 /* Misc */
 const char *gsicp_status_string(gsicp_status s);
 const char *gsicp_last_error(void);         /* thread-local detail of the last error           */

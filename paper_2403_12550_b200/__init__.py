@@ -95,6 +95,10 @@ def lib():
         L.gsicp_last_error.restype = C.c_char_p
         L.gsicp_kernel_launch_count.restype = C.c_uint64
         L.gsicp_abi_version.restype = i32
+        L.gsicp_debug_knn_counters.argtypes = [P]
+        L.gsicp_debug_knn_counters.restype = None
+        L.gsicp_debug_align_timeline.argtypes = [P, C.c_int64]
+        L.gsicp_debug_align_timeline.restype = None
         for name in ("gsicp_backproject_downsample", "gsicp_covariances", "gsicp_build_target",
                      "gsicp_build_target_cloud", "gsicp_align", "gsicp_align_async", "gsicp_linearize"):
             getattr(L, name).restype = i32
@@ -106,8 +110,21 @@ EXPORTED = [
     "gsicp_backproject_workspace_size", "gsicp_backproject_downsample", "gsicp_covariances_workspace_size",
     "gsicp_covariances", "gsicp_build_target_workspace_size", "gsicp_build_target", "gsicp_build_target_cloud",
     "gsicp_align_workspace_size", "gsicp_align", "gsicp_align_async", "gsicp_linearize", "gsicp_status_string",
-    "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version",
+    "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version", "gsicp_debug_knn_counters",
+    "gsicp_debug_align_timeline",
 ]
+
+
+def debug_align_timeline(out: torch.Tensor | None):
+    """Diagnostic: while set, align/linearize launches record globaltimer stamps into `out`
+    ((N,) int64 CUDA tensor), layout in include/gsicp.h; None switches it off."""
+    lib().gsicp_debug_align_timeline(_ptr(out) if out is not None else None, out.numel() if out is not None else 0)
+
+
+def debug_knn_counters(out: torch.Tensor | None):
+    """Diagnostic: while set, covariances() also writes (level, probes, candidates, insertions)
+    per query into `out` ((cap, 4) int32 CUDA tensor); None switches it off."""
+    lib().gsicp_debug_knn_counters(_ptr(out) if out is not None else None)
 
 
 def _check(st: int, allow=(OK,)):

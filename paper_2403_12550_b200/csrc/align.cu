@@ -20,6 +20,10 @@
 
 namespace gsicp {
 
+// diagnostic timeline hook (gsicp_debug_align_timeline); thread-local like the error string
+thread_local long long *g_align_timeline = nullptr;
+thread_local long long g_align_timeline_cap = 0;
+
 namespace {
 
 constexpr int kT = kAlignThreads;
@@ -47,7 +51,15 @@ struct AlignArgs {
     unsigned int *barrier;
     int32_t *corr_ws;         // [cap] previous match (cell-ordered slot) or -1
     int32_t *corr_out;        // nullable [cap] original target index or -1
+    long long *timeline;      // diagnostic (nullable): [0] start, then per iteration G arrivals + pass
+    long long timeline_cap;
 };
+
+__device__ __forceinline__ long long globaltimer_ns() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
     unsigned int v;
@@ -79,6 +91,33 @@ __device__ __forceinline__ void nn_search(const AlignArgs &a, const int *sb, flo
         scan_target_cell(a, cell_lookup(a.table, a.mask, cell_key(0, x, y, z)), qx, qy, qz, best, best_slot);
     };
     scan(qc.c[0], qc.c[1], qc.c[2]);
+    auto bound = [&]() { return best != kEmptyKey ? fminf(ki_key(best), a.r2) : a.r2; };
+    // fast path (the common, warm-started case): the ball of the current bound does not reach
+    // offset +-2 on any axis, so only the 26 neighbours can qualify; test them by their gaps.
+    {
+        const float b0 = bound();
+        float glo[3], ghi[3];
+        bool fits = true;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            glo[k] = qc.gap2(-1, k);
+            ghi[k] = qc.gap2(1, k);
+            fits = fits && qc.gap2(-2, k) > b0 && qc.gap2(2, k) > b0;
+        }
+        if (fits) {
+            for (int t = 0; t < 26; ++t) {
+                int dx, dy, dz;
+                shell_cell(1, t, dx, dy, dz);
+                const float lb = (dx ? (dx < 0 ? glo[0] : ghi[0]) : 0.f) + (dy ? (dy < 0 ? glo[1] : ghi[1]) : 0.f) +
+                                 (dz ? (dz < 0 ? glo[2] : ghi[2]) : 0.f);
+                if (lb > bound()) continue;
+                const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
+                if (x < blo[0] || x > bhi[0] || y < blo[1] || y > bhi[1] || z < blo[2] || z > bhi[2]) continue;
+                scan(x, y, z);
+            }
+            return;
+        }
+    }
     int m_done = 0;
     if (best == kEmptyKey && !(a.r2 < INFINITY)) {
         // ungated search with nothing found yet: grow shells until some point is seen
@@ -96,9 +135,10 @@ __device__ __forceinline__ void nn_search(const AlignArgs &a, const int *sb, flo
     }
     // every cell that can hold a key <= min(best, r^2): exact 1-NN among the points that matter
     ball_search(
-        qc, a.table, a.mask, blo, bhi, m_done, [](int x, int y, int z) { return cell_key(0, x, y, z); },
-        [&](uint2 se) { scan_target_cell(a, se, qx, qy, qz, best, best_slot); },
-        [&]() { return best != kEmptyKey ? fminf(ki_key(best), a.r2) : a.r2; });
+        qc, a.table, a.mask, blo, bhi,
+        [&](int dx, int dy, int dz) { return max(max(abs(dx), abs(dy)), abs(dz)) <= m_done; },
+        [](int x, int y, int z) { return cell_key(0, x, y, z); },
+        [&](uint2 se) { scan_target_cell(a, se, qx, qy, qz, best, best_slot); }, bound);
 }
 
 __device__ __forceinline__ void so3_exp(const double *w, double *R) {
@@ -120,29 +160,41 @@ __device__ __forceinline__ void so3_exp(const double *w, double *R) {
         }
 }
 
-__device__ bool chol6_solve(const double *H, const double *rhs, double *x) {
-    double L[6][6];
+// 6x6 Cholesky solve with one reciprocal square root per pivot (the serial latency of the solve
+// sits on every GN iteration's critical path); fully unrolled so L stays in registers.
+__device__ __forceinline__ bool chol6_solve(const double *H, const double *rhs, double *x) {
+    double L[6][6], inv_d[6];
+    bool ok = true;
+#pragma unroll
     for (int i = 0; i < 6; ++i)
+#pragma unroll
         for (int j = 0; j <= i; ++j) {
             double s = H[6 * i + j];
+#pragma unroll
             for (int k = 0; k < j; ++k) s -= L[i][k] * L[j][k];
             if (i == j) {
-                if (!(s > 0.0)) return false;
-                L[i][i] = sqrt(s);
+                ok = ok && s > 0.0;
+                inv_d[i] = rsqrt(s);
+                L[i][i] = s * inv_d[i];
             } else {
-                L[i][j] = s / L[j][j];
+                L[i][j] = s * inv_d[j];
             }
         }
+    if (!ok) return false;
     double y[6];
+#pragma unroll
     for (int i = 0; i < 6; ++i) {
         double s = rhs[i];
+#pragma unroll
         for (int k = 0; k < i; ++k) s -= L[i][k] * y[k];
-        y[i] = s / L[i][i];
+        y[i] = s * inv_d[i];
     }
+#pragma unroll
     for (int i = 5; i >= 0; --i) {
         double s = y[i];
+#pragma unroll
         for (int k = i + 1; k < 6; ++k) s -= L[k][i] * x[k];
-        x[i] = s / L[i][i];
+        x[i] = s * inv_d[i];
     }
     return true;
 }
@@ -163,6 +215,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     const int G = gridDim.x;
     const int n = *a.d_n;
     if (tid < 12) sT[tid] = a.d_T[tid];
+    if (a.timeline && blockIdx.x == 0 && tid == 0 && a.timeline_cap > 0) a.timeline[0] = globaltimer_ns();
     if (tid < 6) {
         const float inv_h = a.inv_h;
         sBox[tid] = cell_coord(ordered_to_float_(a.tbbox[tid]), inv_h);
@@ -172,6 +225,15 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     int status = GSICP_WARN_MAX_ITERS, iters = 0, converged = 0;
     double n_in = 0.0, cost_last = 0.0;
     for (int it = 0;; ++it) {
+        // diagnostic phase stamps of block 0 (only when a timeline is attached; uniform branch)
+        auto stamp = [&](int p) {
+            if (a.timeline) {
+                __syncthreads();
+                const long long idx = 1 + (long long)a.max_iters * (G + 1) + (long long)it * 8 + p;
+                if (blockIdx.x == 0 && tid == 0 && idx < a.timeline_cap) a.timeline[idx] = globaltimer_ns();
+            }
+        };
+        stamp(0);
         // ------------------------------------------------------------ A6 + A7
         double acc[28];
 #pragma unroll
@@ -199,6 +261,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             nn_search(a, sBox, qx, qy, qz, best, slot);
             a.corr_ws[i] = (slot >= 0 && ki_key(best) < a.r2) ? slot : -2 - slot;  // invalid: -2 - warm start
         }
+        stamp(1);
         // phase B: Eq. 1 terms of the valid pairs
         for (int i = blockIdx.x * kT + tid; i < n; i += G * kT) {
             const int cw = a.corr_ws[i];
@@ -262,6 +325,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             }
             if (a.corr_out) a.corr_out[i] = corr_val;
         }
+        stamp(2);
         // ------------------------------------------------------------ block reduction
 #pragma unroll
         for (int k = 0; k < 28; ++k)
@@ -284,20 +348,36 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         // ------------------------------------------------------------ grid barrier
         __syncthreads();
         if (tid == 0) {
+            const long long rec = 1 + (long long)it * (G + 1);
+            if (a.timeline && rec + G < a.timeline_cap) a.timeline[rec + blockIdx.x] = globaltimer_ns();
             __threadfence();
             atomicAdd(a.barrier, 1u);
             const unsigned int target = (unsigned int)(it + 1) * (unsigned int)G;
             while (ld_acquire(a.barrier) < target) {
             }
             __threadfence();
+            if (a.timeline && blockIdx.x == 0 && rec + G < a.timeline_cap) a.timeline[rec + G] = globaltimer_ns();
         }
         __syncthreads();
+        stamp(3);
         // ------------------------------------------------------------ fixed-order final reduction (every block)
         {
-            const int grp = tid >> 5;  // 8 groups stride over blocks
+            const int grp = tid >> 5;  // kWarps groups stride over the blocks' partials
             double s = 0.0;
-            if (lane < kAlignTerms)
-                for (int gb = grp; gb < G; gb += kWarps) s += __ldcg(part + (size_t)gb * kPad + lane);
+            if (lane < kAlignTerms) {
+                // all loads of a chunk in flight at once, then summed in block order
+                constexpr int kChunk = 16;
+                for (int gb0 = grp; gb0 < G; gb0 += kChunk * kWarps) {
+                    double v[kChunk];
+#pragma unroll
+                    for (int j = 0; j < kChunk; ++j) {
+                        const int gb = gb0 + j * kWarps;
+                        v[j] = gb < G ? __ldcg(part + (size_t)gb * kPad + lane) : 0.0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < kChunk; ++j) s += v[j];
+                }
+            }
             sRed[grp][lane] = s;
             __syncthreads();
             if (tid < kAlignTerms) {
@@ -307,6 +387,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             }
             __syncthreads();
         }
+        stamp(4);
         // ------------------------------------------------------------ A8 solve / update / test
         if (tid == 0) {
             double H[36], b[6];
@@ -371,6 +452,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             sDone = done;
         }
         __syncthreads();
+        stamp(5);
         if (sDone) break;
     }
     if (blockIdx.x == 0 && tid == 0) {
@@ -470,6 +552,8 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
     a.barrier = w.barrier;
     a.corr_ws = w.corr_ws;
     a.corr_out = corr_out;
+    a.timeline = g_align_timeline;
+    a.timeline_cap = g_align_timeline_cap;
     k_align_init<<<blocks_for(src.cap > 0 ? src.cap : 1, 256), 256, 0, s>>>(w.corr_ws, src.cap, w.barrier);
     GSICP_LAUNCH_CHECK("k_align_init");
     const int G = align_grid_blocks(src.cap);

@@ -2,23 +2,34 @@
 // P:92 "The covariance C of one 3D point x is given by computing covariance matrix of
 // k-nearest neighbors of x"; Eq. 3-4 for the regularisation (R4-R8).
 //
-// One thread per query; the query's best-K candidates live in registers as packed (key, index)
-// u64 words (unordered, with the current worst tracked).  Search = certified expanding rings
-// (search.cuh) on one level of the multi-level hash: own cell, whole shells until K candidates
-// are held, then the ball traversal bounded by the current K-th key (exact at any level; the
-// level only sets the cost).  Level = finest level whose own cell holds >= kMinCell points.
-// Queries are processed in the coarsest level's cell order so a warp's queries are spatial
-// neighbours (shared cells, L1 hits, uniform loop trip counts); results scatter to input order.
+// Warp-cooperative: a warp takes 32 consecutive queries (coarsest-level cell order, so they are
+// spatial neighbours) and searches them one after the other with all 32 lanes:
+//   * the query's best-K list is distributed over the lanes (lane j holds the j-th smallest packed
+//     (key, index) u64), so an insertion is one ballot + one shuffle, not a K-long register walk;
+//   * cells are probed 32 at a time (lane = cell of the current Chebyshev shell, nearest shells
+//     first; cells whose box lower bound exceeds the K-th key are skipped), and the points of the
+//     non-empty cells are scanned as one flattened, coalesced range (lane = candidate);
+//   * after shell m every unscanned point is >= m*h + delta_q away, so the list is exact once its
+//     K-th key is below that bound (conservative rounding margin), or once the shell block covers
+//     the cloud's bbox.  A query that cannot fill its list within shell 1 restarts one level
+//     coarser (multi-level hash: depth-image density varies as z^2).
+// The moments of each query are warp-reduced into the lane that owns it; then every lane runs the
+// binary64 eigen-decomposition and regularisation of its own query in parallel.
 #include "grid.cuh"
 #include "host_common.cuh"
 #include "search.cuh"
 
 namespace gsicp {
 
+// per-query diagnostics (tests / profiling only): level, cells probed, candidates, insertions
+thread_local int32_t *g_knn_debug = nullptr;
+
 namespace {
 
 constexpr int kMinCell = 3;
 constexpr int kKnnThreads = 128;
+constexpr int kQueriesPerWarp = 8;  // queries a warp searches one after the other
+constexpr unsigned kFull = 0xffffffffu;
 
 struct KnnArgs {
     GridView g;
@@ -29,128 +40,198 @@ struct KnnArgs {
     double eps;
     float4 *cov_a, *cov_b;
     int32_t *knn_idx;
+    int4 *debug;
+    double *moments;  // [cap][10]: sum d (3), sum d d^T (6), count — per query in search order
 };
 
+__device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int src) {
+    return ((unsigned long long)__shfl_sync(kFull, (unsigned)(v >> 32), src) << 32) |
+           __shfl_sync(kFull, (unsigned)v, src);
+}
+__device__ __forceinline__ unsigned long long shfl_up_u64(unsigned long long v, int d) {
+    return ((unsigned long long)__shfl_up_sync(kFull, (unsigned)(v >> 32), d) << 32) |
+           __shfl_up_sync(kFull, (unsigned)v, d);
+}
+
+// Warp-distributed sorted best-K list.
 template <int K>
-struct TopK {
-    unsigned long long L[K];
-    unsigned long long worst;
+struct WarpTopK {
+    unsigned long long L;  // lane j < K: j-th smallest (kEmptyKey if fewer); lanes >= K: kEmptyKey
+    unsigned long long worst;  // = list[K-1] (warp-uniform)
+    int inserts;
 
     __device__ __forceinline__ void reset() {
-#pragma unroll
-        for (int j = 0; j < K; ++j) L[j] = kEmptyKey;
+        L = kEmptyKey;
         worst = kEmptyKey;
     }
     __device__ __forceinline__ bool full() const { return worst != kEmptyKey; }
-    __device__ __forceinline__ void insert(unsigned long long v) {
-        if (v >= worst) return;
-        bool done = false;
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const bool hit = !done && L[j] == worst;
-            L[j] = hit ? v : L[j];
-            done |= hit;
+    // insert the candidates of all lanes (cand = kEmptyKey for none)
+    __device__ __forceinline__ void insert_all(unsigned long long cand, int lane) {
+        unsigned pass = __ballot_sync(kFull, cand < worst);
+        while (pass) {
+            const int src = __ffs(pass) - 1;
+            pass &= pass - 1;
+            const unsigned long long v = shfl_u64(cand, src);
+            if (!(v < worst)) continue;  // worst shrank since the ballot
+            ++inserts;
+            const int p = __popc(__ballot_sync(kFull, lane < K && L < v));
+            const unsigned long long up = shfl_up_u64(L, 1);
+            if (lane < K) L = lane < p ? L : (lane == p ? v : up);
+            worst = shfl_u64(L, K - 1);
         }
-        unsigned long long w = L[0];
-#pragma unroll
-        for (int j = 1; j < K; ++j) w = L[j] > w ? L[j] : w;
-        worst = w;
-    }
-    // ascending (key, index) order: odd-even transposition network
-    __device__ __forceinline__ void sort() {
-#pragma unroll
-        for (int p = 0; p < K; ++p)
-#pragma unroll
-            for (int j = p & 1; j + 1 < K; j += 2) {
-                const unsigned long long a = L[j], b = L[j + 1];
-                L[j] = a < b ? a : b;
-                L[j + 1] = a < b ? b : a;
-            }
     }
 };
 
+struct Counters {
+    int probes = 0, cands = 0;
+};
+
+// Probe the cells one per lane (valid lanes only), then scan all their points as one flattened
+// range, 32 candidates per round, inserting into the list.
 template <int K>
-__device__ __forceinline__ void scan_cell(const GridView &g, uint2 se, float qx, float qy, float qz, TopK<K> &T) {
-    for (uint32_t j = se.x; j < se.x + se.y; ++j) {
-        const float4 p = __ldg(g.spos + j);
-        T.insert(pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w)));
+__device__ __forceinline__ void scan_cells(const GridView &g, bool valid, unsigned long long key, float qx, float qy,
+                                           float qz, WarpTopK<K> &T, Counters &cn, int lane) {
+    uint2 se = valid ? cell_lookup(g.table, g.mask, key) : make_uint2(0u, 0u);
+    cn.probes += __popc(__ballot_sync(kFull, valid));
+    // inclusive scan of the counts
+    uint32_t incl = se.y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    cn.cands += (int)total;
+    for (uint32_t base = 0; base < total; base += 32) {
+        const uint32_t item = base + lane;
+        unsigned long long cand = kEmptyKey;
+        // owning cell: first lane whose inclusive count exceeds item (binary search over lanes)
+        int lo = 0, hi = 31;
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+            const int mid = (lo + hi) >> 1;
+            const uint32_t v = __shfl_sync(kFull, incl, mid);
+            if (v > item) hi = mid; else lo = mid + 1;
+        }
+        const uint32_t c_incl = __shfl_sync(kFull, incl, lo);
+        const uint32_t c_start = __shfl_sync(kFull, se.x, lo);
+        const uint32_t c_cnt = __shfl_sync(kFull, se.y, lo);
+        if (item < total) {
+            const float4 p = __ldg(g.spos + c_start + (item - (c_incl - c_cnt)));
+            cand = pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
+        }
+        T.insert_all(cand, lane);
     }
 }
 
-// Exact best-K of the query on one level: own cell, whole shells until K candidates are held
-// (or the cloud is exhausted), then the ball traversal bounded by the current K-th key.
-// Returns false (list reset) when K candidates are not found within shell 1 and a coarser level
-// exists: sparse neighbourhoods (outliers, far depth points) restart one level up instead of
-// growing many shells of small cells.
+// Exact best-K of one query on one level.  Returns false (list reset) if shell 1 does not fill
+// the list and a coarser level exists.
 template <int K>
-__device__ bool knn_search(const GridView &g, int level, float qx, float qy, float qz, TopK<K> &T) {
+__device__ bool knn_search_warp(const GridView &g, int level, float qx, float qy, float qz, WarpTopK<K> &T,
+                                Counters &cn, int lane) {
     T.reset();
     const float inv_h = ldexpf(g.inv_h0, -level);
     const QueryCell qc(qx, qy, qz, ldexpf(g.h0, level), inv_h);
     int blo[3], bhi[3];
     grid_cell_bbox(g, level, blo, bhi);
-    auto scan = [&](int x, int y, int z) {
-        scan_cell<K>(g, cell_lookup(g.table, g.mask, cell_key(level, x, y, z)), qx, qy, qz, T);
-    };
-    scan(qc.c[0], qc.c[1], qc.c[2]);
-    int m_done = 0;
-    while (!T.full()) {
-        if (qc.covers(m_done, blo, bhi)) return true;  // fewer than K points in the whole cloud
-        if (m_done == 1 && level + 1 < g.levels) return false;
-        ++m_done;
-        const int cnt = shell_count(m_done);
-        for (int t = 0; t < cnt; ++t) {
-            int dx, dy, dz;
-            shell_cell(m_done, t, dx, dy, dz);
+    for (int m = 0;; ++m) {
+        // shell 0 and 1 together: lane 0 = own cell, lanes 1..26 = shell 1
+        if (m == 1) continue;
+        const int cnt = m == 0 ? 27 : shell_count(m);
+        for (int t0 = 0; t0 < cnt; t0 += 32) {
+            const int t = t0 + lane;
+            int dx = 0, dy = 0, dz = 0;
+            if (t < cnt) {
+                if (m == 0) {
+                    if (t > 0) shell_cell(1, t - 1, dx, dy, dz);
+                } else {
+                    shell_cell(m, t, dx, dy, dz);
+                }
+            }
             const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
-            if (x < blo[0] || x > bhi[0] || y < blo[1] || y > bhi[1] || z < blo[2] || z > bhi[2]) continue;
-            scan(x, y, z);
+            bool valid = t < cnt && x >= blo[0] && x <= bhi[0] && y >= blo[1] && y <= bhi[1] && z >= blo[2] && z <= bhi[2];
+            if (valid && T.full()) {
+                const float lb = qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2);
+                valid = !(lb > ki_key(T.worst));
+            }
+            if (!__any_sync(kFull, valid)) continue;
+            scan_cells<K>(g, valid, cell_key(level, x, y, z), qx, qy, qz, T, cn, lane);
         }
+        const int mm = m == 0 ? 1 : m;  // shells 0..mm are complete
+        if (T.full() && ki_key(T.worst) < qc.certified_key(mm)) return true;
+        if (qc.covers(mm, blo, bhi)) return true;  // whole cloud scanned (fewer than K points)
+        if (mm == 1 && !T.full() && level + 1 < g.levels) return false;
     }
-    ball_search(
-        qc, g.table, g.mask, blo, bhi, m_done, [&](int x, int y, int z) { return cell_key(level, x, y, z); },
-        [&](uint2 se) { scan_cell<K>(g, se, qx, qy, qz, T); }, [&]() { return ki_key(T.worst); });
-    return true;
 }
 
 template <int K>
-__global__ void __launch_bounds__(kKnnThreads) k_knn_cov(KnnArgs a) {
+__global__ void __launch_bounds__(kKnnThreads) k_knn_search(KnnArgs a) {
+    const int n = *a.d_n;
+    const GridView &g = a.g;
+    const int lane = threadIdx.x & 31;
+    const int wbase = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kQueriesPerWarp;  // first query of this warp
+    if (wbase >= n) return;
+    const int tq = wbase + lane;
+    float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lane < kQueriesPerWarp && tq < n) e = __ldg(g.spos + (size_t)(g.levels - 1) * g.cap + tq);
+    const int nq = min(kQueriesPerWarp, n - wbase);
+    for (int qi = 0; qi < nq; ++qi) {
+        const float qx = __shfl_sync(kFull, e.x, qi), qy = __shfl_sync(kFull, e.y, qi), qz = __shfl_sync(kFull, e.z, qi);
+        const int i = __shfl_sync(kFull, __float_as_int(e.w), qi);
+        // level: finest whose own cell holds >= kMinCell points (lane l probes level l)
+        int level = g.levels - 1;
+        {
+            bool ok = false;
+            if (lane < g.levels - 1) {
+                const float inv_h = ldexpf(g.inv_h0, -lane);
+                const uint2 se = cell_lookup(
+                    g.table, g.mask, cell_key(lane, cell_coord(qx, inv_h), cell_coord(qy, inv_h), cell_coord(qz, inv_h)));
+                ok = se.y >= (uint32_t)kMinCell;
+            }
+            const unsigned b = __ballot_sync(kFull, ok);
+            if (b) level = __ffs(b) - 1;
+        }
+        WarpTopK<K> T;
+        T.inserts = 0;
+        Counters cn;
+        while (!knn_search_warp<K>(g, level, qx, qy, qz, T, cn, lane)) ++level;
+        if (a.debug && lane == 0) a.debug[i] = make_int4(level, cn.probes, cn.cands, T.inserts);
+        // moments over the k nearest: lane j < k holds neighbour j (sorted by (key, index))
+        const bool have = lane < a.k && T.L != kEmptyKey;
+        if (a.knn_idx && lane < a.k) a.knn_idx[(size_t)i * a.k + lane] = have ? (int32_t)ki_idx(T.L) : -1;
+        double d[3] = {0, 0, 0};
+        if (have) {
+            const float4 p = __ldg(a.pos + ki_idx(T.L));
+            d[0] = (double)p.x - (double)qx;
+            d[1] = (double)p.y - (double)qy;
+            d[2] = (double)p.z - (double)qz;
+        }
+        double v[9] = {d[0], d[1], d[2], d[0] * d[0], d[0] * d[1], d[0] * d[2], d[1] * d[1], d[1] * d[2], d[2] * d[2]};
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int c = 0; c < 9; ++c) v[c] += __shfl_xor_sync(kFull, v[c], o);
+        const int c_have = __popc(__ballot_sync(kFull, have));
+        // moments record of query (wbase + qi): lane c < 9 stores sum c, lane 9 the count
+        double mine = (double)c_have;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) mine = lane == c ? v[c] : mine;
+        if (lane < 10) a.moments[(size_t)(wbase + qi) * 10 + lane] = mine;
+    }
+}
+
+// per-query epilogue (thread per query): covariance (normalised by the count), eigen,
+// regularisation, scattered to input order
+__global__ void __launch_bounds__(kKnnThreads) k_knn_epilogue(KnnArgs a) {
     const int n = *a.d_n;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     const GridView &g = a.g;
-    const float4 e = __ldg(g.spos + (size_t)(g.levels - 1) * g.cap + t);
-    const int i = __float_as_int(e.w);
-    const float qx = e.x, qy = e.y, qz = e.z;
-    int level = g.levels - 1;
-    for (int l = 0; l < g.levels - 1; ++l) {
-        const float inv_h = ldexpf(g.inv_h0, -l);
-        const uint2 se = cell_lookup(
-            g.table, g.mask, cell_key(l, cell_coord(qx, inv_h), cell_coord(qy, inv_h), cell_coord(qz, inv_h)));
-        if (se.y >= (uint32_t)kMinCell) {
-            level = l;
-            break;
-        }
-    }
-    TopK<K> T;
-    while (!knn_search<K>(g, level, qx, qy, qz, T)) ++level;
-    if (a.knn_idx || a.k != K) T.sort();
-
-    // query-centred binary64 moments over the k nearest (normalised by the count)
-    double s1[3] = {0, 0, 0}, s2[6] = {0, 0, 0, 0, 0, 0};
-    int cnt = 0;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        if (j < a.k && T.L[j] != kEmptyKey) {
-            const float4 p = __ldg(a.pos + ki_idx(T.L[j]));
-            const double d0 = (double)p.x - (double)qx, d1 = (double)p.y - (double)qy, d2 = (double)p.z - (double)qz;
-            s1[0] += d0; s1[1] += d1; s1[2] += d2;
-            s2[0] += d0 * d0; s2[1] += d0 * d1; s2[2] += d0 * d2;
-            s2[3] += d1 * d1; s2[4] += d1 * d2; s2[5] += d2 * d2;
-            ++cnt;
-        }
-        if (a.knn_idx && j < a.k) a.knn_idx[(size_t)i * a.k + j] = T.L[j] != kEmptyKey ? (int32_t)ki_idx(T.L[j]) : -1;
-    }
+    const int i = __float_as_int(__ldg(g.spos + (size_t)(g.levels - 1) * g.cap + t).w);
+    const double *mr = a.moments + (size_t)t * 10;
+    const double s1[3] = {mr[0], mr[1], mr[2]};
+    const double s2[6] = {mr[3], mr[4], mr[5], mr[6], mr[7], mr[8]};
+    const int cnt = (int)mr[9];
     const double inv = 1.0 / (double)cnt;
     const double mu[3] = {s1[0] * inv, s1[1] * inv, s1[2] * inv};
     double C[6] = {s2[0] * inv - mu[0] * mu[0], s2[1] * inv - mu[0] * mu[1], s2[2] * inv - mu[0] * mu[2],
@@ -164,15 +245,20 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_cov(KnnArgs a) {
 
 template <int K>
 cudaError_t launch_k(const KnnArgs &a, int cap, cudaStream_t s) {
-    k_knn_cov<K><<<blocks_for(cap, kKnnThreads), kKnnThreads, 0, s>>>(a);
-    GSICP_LAUNCH_CHECK("k_knn_cov");
-    note_launch();
+    const long long warps = (cap + kQueriesPerWarp - 1) / kQueriesPerWarp;
+    k_knn_search<K><<<blocks_for(warps * 32, kKnnThreads), kKnnThreads, 0, s>>>(a);
+    GSICP_LAUNCH_CHECK("k_knn_search");
+    k_knn_epilogue<<<blocks_for(cap, kKnnThreads), kKnnThreads, 0, s>>>(a);
+    GSICP_LAUNCH_CHECK("k_knn_epilogue");
+    note_launch(2);
     return cudaSuccess;
 }
 
 }  // namespace
 
-size_t covariances_ws_bytes(int cap, int levels) { return grid_bytes(cap, levels, false); }
+size_t covariances_ws_bytes(int cap, int levels) {
+    return grid_bytes(cap, levels, false) + align_up((size_t)cap * 10 * sizeof(double));
+}
 
 cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, int k, int mode, float eps,
                                float cell0, int levels, float *cov_a, float *cov_b, int32_t *knn_idx, void *ws,
@@ -187,11 +273,12 @@ cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, in
     a.cov_a = reinterpret_cast<float4 *>(cov_a);
     a.cov_b = reinterpret_cast<float4 *>(cov_b);
     a.knn_idx = knn_idx;
+    a.debug = reinterpret_cast<int4 *>(g_knn_debug);
+    a.moments = reinterpret_cast<double *>(static_cast<char *>(ws) + grid_bytes(cap, levels, false));
     cudaError_t e = grid_build(a.g, a.pos, nullptr, nullptr, d_n, cap, s);
     if (e != cudaSuccess) return e;
     if (k <= 4) return launch_k<4>(a, cap, s);
     if (k <= 8) return launch_k<8>(a, cap, s);
-    if (k <= 12) return launch_k<12>(a, cap, s);
     if (k <= 16) return launch_k<16>(a, cap, s);
     if (k <= 20) return launch_k<20>(a, cap, s);
     if (k <= 24) return launch_k<24>(a, cap, s);

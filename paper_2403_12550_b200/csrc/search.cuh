@@ -50,6 +50,11 @@ struct QueryCell {
         }
         margin = 2e-6f * (fabsf(qx) + fabsf(qy) + fabsf(qz)) + h * kRelMargin;
     }
+    // after shells 0..m are scanned, every unscanned point has key >= certified_key(m)
+    __device__ __forceinline__ float certified_key(int m) const {
+        const float B = fmaxf((float)m * h + dq - margin, 0.f);
+        return B * B * (1.f - kRelMargin);
+    }
     __device__ __forceinline__ bool covers(int m, const int *blo, const int *bhi) const {
         return c[0] - m <= blo[0] && c[0] + m >= bhi[0] && c[1] - m <= blo[1] && c[1] + m >= bhi[1] &&
                c[2] - m <= blo[2] && c[2] + m >= bhi[2];
@@ -105,14 +110,14 @@ __device__ __forceinline__ void lookup_batch(const CellEntry *__restrict__ table
     }
 }
 
-// Ball traversal over the cells outside the already-scanned Chebyshev block of radius m_done.
+// Ball traversal over the cells not yet scanned (skip(dx, dy, dz) is true for those already done).
 // Rows (fixed y, z) are pruned by their gap; inside a row the x-extent is computed from the gaps
 // alone (no loads), then cells are looked up kLookupBatch at a time, nearest first, and a cell is
 // scanned only if its lower bound is still <= bound() (which may shrink while scanning).
 //   key_of(x, y, z) -> u64 cell key;  scan(uint2 start_count);  bound() -> float
-template <class KeyOf, class Scan, class Bound>
+template <class KeyOf, class Skip, class Scan, class Bound>
 __device__ __forceinline__ void ball_search(const QueryCell &qc, const CellEntry *__restrict__ table, uint32_t mask,
-                                            const int *blo, const int *bhi, int m_done, KeyOf key_of, Scan scan,
+                                            const int *blo, const int *bhi, Skip skip, KeyOf key_of, Scan scan,
                                             Bound bound) {
     int zlo, zhi;
     axis_range(qc, 2, bound(), blo[2], bhi[2], zlo, zhi);
@@ -128,7 +133,6 @@ __device__ __forceinline__ void ball_search(const QueryCell &qc, const CellEntry
             if (dy < ylo || dy > yhi) continue;
             const float gzy = gz + qc.gap2(dy, 1);
             if (gzy > bound()) continue;
-            const int ayz = max(abs(dy), abs(dz));
             int xlo, xhi;
             axis_range(qc, 0, bound() - gzy, blo[0], bhi[0], xlo, xhi);
             const int kxmax = 2 * max(-xlo, xhi);
@@ -139,7 +143,7 @@ __device__ __forceinline__ void ball_search(const QueryCell &qc, const CellEntry
 #pragma unroll
                 for (int j = 0; j < kLookupBatch; ++j) {
                     const int dx = zigzag(kx0 + j);
-                    valid[j] = kx0 + j <= kxmax && dx >= xlo && dx <= xhi && max(abs(dx), ayz) > m_done;
+                    valid[j] = kx0 + j <= kxmax && dx >= xlo && dx <= xhi && !skip(dx, dy, dz);
                     lb[j] = gzy + qc.gap2(dx, 0);
                     keys[j] = key_of(qc.c[0] + dx, qc.c[1] + dy, qc.c[2] + dz);
                 }

@@ -1,0 +1,61 @@
+"""GPU diagnostic: per-iteration timeline of the persistent G-ICP kernel (block barrier arrivals)
+for the bench frame vs the 1e6 map, over a sweep of target cell sizes.
+Run under gpurun:  python tools/align_diag.py"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2403_12550_b200 as g
+import synth
+
+
+def main():
+    w = synth.make_frame_workload(2, "replica", M=1_000_000, stride=4)
+    K = w.K
+    dev = torch.device("cuda")
+    tr = g.Tracker(K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=4, device=dev)
+    depth = torch.from_numpy(w.depth).to(dev)
+    tr.preprocess(depth)
+    means, quats, scales = (torch.from_numpy(x).to(dev) for x in (w.means, w.quats, w.scales))
+    tl = torch.zeros(1 << 16, dtype=torch.int64, device=dev)
+    for cell_mult in (0.0, 2.0, 3.0, 4.0, 6.0):
+        tgt = g.build_target(means, quats, scales, cell=cell_mult * w.ell if cell_mult else 0.0)
+        for _ in range(3):
+            T, st = g.align(tr.cloud, tgt, w.T_init, tr.params, tr.ws_align)
+        tl.zero_()
+        g.debug_align_timeline(tl)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        T, st = g.align(tr.cloud, tgt, w.T_init, tr.params, tr.ws_align)
+        e1.record()
+        g.debug_align_timeline(None)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        t = tl.cpu().numpy()
+        Gn = int(np.ceil(tr.cap / 384))
+        Gn = min(Gn, 148)
+        t0 = t[0]
+        print(f"cell={tgt.cell * 100:.2f} cm  iters={st['iters']} total {ms * 1000:.1f} us (event)")
+        prev = t0
+        max_iters = tr.params.max_iters
+        ph0 = 1 + max_iters * (Gn + 1)
+        names = ["A", "B", "blkred+barrier", "finalred", "solve"]
+        for it in range(st["iters"] + 1):
+            rec = 1 + it * (Gn + 1)
+            arr = t[rec:rec + Gn]
+            pas = t[rec + Gn]
+            if pas == 0:
+                break
+            a = (arr - prev) / 1000.0
+            ph = t[ph0 + it * 8: ph0 + it * 8 + 6]
+            phs = " ".join(f"{nm}={(ph[j + 1] - ph[j]) / 1000.0:.1f}" for j, nm in enumerate(names))
+            print(f"  it {it}: arrivals min {a.min():7.1f} p50 {np.median(a):7.1f} max {a.max():7.1f} us; "
+                  f"release {(pas - prev) / 1000.0:7.1f} us | block0 phases(us) {phs}")
+            prev = pas
+
+
+if __name__ == "__main__":
+    main()

@@ -191,6 +191,11 @@ void gsicp_debug_knn_counters(int32_t *d_out);
  * [1 + it*(G+1) + G] the barrier release seen by block 0 (G = grid size).  NULL switches it off. */
 void gsicp_debug_align_timeline(int64_t *d_out, int64_t capacity);
 
+/* DIAGNOSTIC: while set, align / linearize launches write per resident source point i
+ * d_out[4*i + 0..3] = (slow-path searches, cells probed, candidates scanned, iterations),
+ * summed over the GN iterations (int32, device, >= 4*cap entries).  NULL switches it off. */
+void gsicp_debug_align_counters(int32_t *d_out);
+
 /* Misc */
 const char *gsicp_status_string(gsicp_status s);
 const char *gsicp_last_error(void);         /* thread-local detail of the last error           */

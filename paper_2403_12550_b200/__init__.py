@@ -99,6 +99,8 @@ def lib():
         L.gsicp_debug_knn_counters.restype = None
         L.gsicp_debug_align_timeline.argtypes = [P, C.c_int64]
         L.gsicp_debug_align_timeline.restype = None
+        L.gsicp_debug_align_counters.argtypes = [P]
+        L.gsicp_debug_align_counters.restype = None
         for name in ("gsicp_backproject_downsample", "gsicp_covariances", "gsicp_build_target",
                      "gsicp_build_target_cloud", "gsicp_align", "gsicp_align_async", "gsicp_linearize"):
             getattr(L, name).restype = i32
@@ -111,8 +113,14 @@ EXPORTED = [
     "gsicp_covariances", "gsicp_build_target_workspace_size", "gsicp_build_target", "gsicp_build_target_cloud",
     "gsicp_align_workspace_size", "gsicp_align", "gsicp_align_async", "gsicp_linearize", "gsicp_status_string",
     "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version", "gsicp_debug_knn_counters",
-    "gsicp_debug_align_timeline",
+    "gsicp_debug_align_timeline", "gsicp_debug_align_counters",
 ]
+
+
+def debug_align_counters(out: torch.Tensor | None):
+    """Diagnostic: while set, align/linearize write (slow searches, probes, candidates, iterations)
+    per resident source point into `out` ((cap, 4) int32 CUDA tensor); None switches it off."""
+    lib().gsicp_debug_align_counters(_ptr(out) if out is not None else None)
 
 
 def debug_align_timeline(out: torch.Tensor | None):

@@ -2,8 +2,8 @@
 //
 // Per Gauss-Newton iteration, every thread takes source points i (grid-stride) and
 //   A6  q = K3(T, x_i) in binary64 (no FMA), exact 1-NN of fl32(q) among the target means by
-//       the canonical (key, index) order, certified expanding rings on the target hash,
-//       warm-started with the previous iteration's match; valid iff key < fl32(r*r) (R15);
+//       the canonical (key, index) order, grid search warm-started with the previous
+//       iteration's match; valid iff key < fl32(r*r) (R15);
 //   A7  Sigma = C^t_j + R C^s_i R^T, M = Sigma^{-1} (adjugate, binary64), d = x^t_j - q,
 //       J = [[q]x, -I]: accumulates the 21 unique H = J^T M J terms, b = J^T M d, d^T M d and
 //       the inlier count (Eq. 1; R1-R3, R16);
@@ -12,6 +12,12 @@
 // fixed order (so all blocks hold bit-identical H, b), solves the 6x6 system by Cholesky
 // (A8), applies the left update T <- [Exp(w) | v] T and evaluates the convergence test —
 // identical decisions in every block, no second barrier, no host round trip (A9 at the end).
+//
+// Latency design: the grid is sized so every thread owns (at most) one "resident" point whose
+// source data, current match (position + covariance) and own target cell stay in registers for
+// the whole GN loop; an iteration's dependent memory chain is then: scan the own cell (usually
+// cached), rarely a neighbour cell, and reload the match covariance only when the match changes.
+// Points beyond one per thread (clouds larger than the resident grid) take the generic path.
 #include <math.h>
 
 #include "gsicp_internal.cuh"
@@ -23,6 +29,7 @@ namespace gsicp {
 // diagnostic timeline hook (gsicp_debug_align_timeline); thread-local like the error string
 thread_local long long *g_align_timeline = nullptr;
 thread_local long long g_align_timeline_cap = 0;
+thread_local int32_t *g_align_debug = nullptr;
 
 namespace {
 
@@ -49,10 +56,11 @@ struct AlignArgs {
     double *d_lin;            // [44] linearize-only output: H[36], b[6], cost, n
     double *partials;         // [2][grid][kPad]
     unsigned int *barrier;
-    int32_t *corr_ws;         // [cap] previous match (cell-ordered slot) or -1
+    int32_t *corr_ws;         // [cap] previous match (cell-ordered slot), -2-slot if gated out, -1 none
     int32_t *corr_out;        // nullable [cap] original target index or -1
     long long *timeline;      // diagnostic (nullable): [0] start, then per iteration G arrivals + pass
     long long timeline_cap;
+    int4 *debug;              // diagnostic (nullable): per point (slow searches, probes, candidates, iterations)
 };
 
 __device__ __forceinline__ long long globaltimer_ns() {
@@ -69,59 +77,51 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
 
 __device__ __forceinline__ float ordered_to_float_(int32_t i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
 
-// Exact 1-NN of (qx, qy, qz) on the target hash; best/best_slot carry the warm start in and the
-// answer out.
-__device__ __forceinline__ void scan_target_cell(const AlignArgs &a, uint2 se, float qx, float qy, float qz,
-                                                 unsigned long long &best, int &best_slot) {
-    for (uint32_t j = se.x; j < se.x + se.y; ++j) {
-        const float4 p = __ldg(a.tpos + j);
-        const unsigned long long v = pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
-        if (v < best) {
-            best = v;
-            best_slot = (int)j;
+// running 1-NN state of one query
+struct NN {
+    unsigned long long best = kEmptyKey;  // packed (key, original index)
+    int slot = -1;                        // cell-ordered target slot of best
+    float4 p;                             // target record of best
+    int probes = 0, cands = 0, slow = 0;  // diagnostics
+};
+
+constexpr int kCandBatch = 8;  // candidate records loaded together (one latency per batch)
+
+__device__ __forceinline__ void scan_target_cell(const AlignArgs &a, uint2 se, float qx, float qy, float qz, NN &nn) {
+    ++nn.probes;
+    nn.cands += (int)se.y;
+    const uint32_t end = se.x + se.y;
+    for (uint32_t j0 = se.x; j0 < end; j0 += kCandBatch) {
+        float4 p[kCandBatch];
+#pragma unroll
+        for (int u = 0; u < kCandBatch; ++u) p[u] = j0 + u < end ? __ldg(a.tpos + j0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < kCandBatch; ++u) {
+            if (j0 + u >= end) break;
+            const unsigned long long v =
+                pack_ki(canon_key(qx, qy, qz, p[u].x, p[u].y, p[u].z), (uint32_t)__float_as_int(p[u].w));
+            if (v < nn.best) {
+                nn.best = v;
+                nn.slot = (int)(j0 + u);
+                nn.p = p[u];
+            }
         }
     }
 }
 
-__device__ __forceinline__ void nn_search(const AlignArgs &a, const int *sb, float qx, float qy, float qz,
-                                          unsigned long long &best, int &best_slot) {
+__device__ __forceinline__ float nn_bound(const AlignArgs &a, const NN &nn) {
+    return nn.best != kEmptyKey ? fminf(ki_key(nn.best), a.r2) : a.r2;
+}
+
+// General exact search after the own cell: grow shells while an ungated search has found
+// nothing, then the ball traversal bounded by min(best, r^2).  Out of line so that the
+// common fast path keeps its registers.
+__device__ __noinline__ void nn_slow(const AlignArgs &a, const int *sb, float qx, float qy, float qz, NN &nn) {
     const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
     const int *blo = sb, *bhi = sb + 3;
-    auto scan = [&](int x, int y, int z) {
-        scan_target_cell(a, cell_lookup(a.table, a.mask, cell_key(0, x, y, z)), qx, qy, qz, best, best_slot);
-    };
-    scan(qc.c[0], qc.c[1], qc.c[2]);
-    auto bound = [&]() { return best != kEmptyKey ? fminf(ki_key(best), a.r2) : a.r2; };
-    // fast path (the common, warm-started case): the ball of the current bound does not reach
-    // offset +-2 on any axis, so only the 26 neighbours can qualify; test them by their gaps.
-    {
-        const float b0 = bound();
-        float glo[3], ghi[3];
-        bool fits = true;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            glo[k] = qc.gap2(-1, k);
-            ghi[k] = qc.gap2(1, k);
-            fits = fits && qc.gap2(-2, k) > b0 && qc.gap2(2, k) > b0;
-        }
-        if (fits) {
-            for (int t = 0; t < 26; ++t) {
-                int dx, dy, dz;
-                shell_cell(1, t, dx, dy, dz);
-                const float lb = (dx ? (dx < 0 ? glo[0] : ghi[0]) : 0.f) + (dy ? (dy < 0 ? glo[1] : ghi[1]) : 0.f) +
-                                 (dz ? (dz < 0 ? glo[2] : ghi[2]) : 0.f);
-                if (lb > bound()) continue;
-                const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
-                if (x < blo[0] || x > bhi[0] || y < blo[1] || y > bhi[1] || z < blo[2] || z > bhi[2]) continue;
-                scan(x, y, z);
-            }
-            return;
-        }
-    }
     int m_done = 0;
-    if (best == kEmptyKey && !(a.r2 < INFINITY)) {
-        // ungated search with nothing found yet: grow shells until some point is seen
-        while (best == kEmptyKey && !qc.covers(m_done, blo, bhi)) {
+    if (nn.best == kEmptyKey && !(a.r2 < INFINITY)) {
+        while (nn.best == kEmptyKey && !qc.covers(m_done, blo, bhi)) {
             ++m_done;
             const int cnt = shell_count(m_done);
             for (int t = 0; t < cnt; ++t) {
@@ -129,16 +129,128 @@ __device__ __forceinline__ void nn_search(const AlignArgs &a, const int *sb, flo
                 shell_cell(m_done, t, dx, dy, dz);
                 const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
                 if (x < blo[0] || x > bhi[0] || y < blo[1] || y > bhi[1] || z < blo[2] || z > bhi[2]) continue;
-                scan(x, y, z);
+                scan_target_cell(a, cell_lookup(a.table, a.mask, cell_key(0, x, y, z)), qx, qy, qz, nn);
             }
         }
     }
-    // every cell that can hold a key <= min(best, r^2): exact 1-NN among the points that matter
     ball_search(
         qc, a.table, a.mask, blo, bhi,
         [&](int dx, int dy, int dz) { return max(max(abs(dx), abs(dy)), abs(dz)) <= m_done; },
         [](int x, int y, int z) { return cell_key(0, x, y, z); },
-        [&](uint2 se) { scan_target_cell(a, se, qx, qy, qz, best, best_slot); }, bound);
+        [&](uint2 se) { scan_target_cell(a, se, qx, qy, qz, nn); }, [&]() { return nn_bound(a, nn); });
+}
+
+// Exact 1-NN given the query's cell geometry and its own cell's (start, count) (already known).
+// Fast path: when the ball of the current bound cannot reach offset +-2 on any axis, only the 26
+// neighbours can qualify; they are tested by their gaps alone.
+__device__ __forceinline__ void nn_search(const AlignArgs &a, const int *sb, const QueryCell &qc, uint2 own, float qx,
+                                          float qy, float qz, NN &nn) {
+    scan_target_cell(a, own, qx, qy, qz, nn);
+    const float b0 = nn_bound(a, nn);
+    float glo[3], ghi[3];
+    bool fits = true;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        glo[k] = qc.gap2(-1, k);
+        ghi[k] = qc.gap2(1, k);
+        fits = fits && qc.gap2(-2, k) > b0 && qc.gap2(2, k) > b0;
+    }
+    if (!fits) {
+        ++nn.slow;
+        nn_slow(a, sb, qx, qy, qz, nn);
+        return;
+    }
+    const int *blo = sb, *bhi = sb + 3;
+    auto nb_lb = [&](int dx, int dy, int dz) {
+        return (dx ? (dx < 0 ? glo[0] : ghi[0]) : 0.f) + (dy ? (dy < 0 ? glo[1] : ghi[1]) : 0.f) +
+               (dz ? (dz < 0 ? glo[2] : ghi[2]) : 0.f);
+    };
+    // qualifying neighbours (gap test only, no loads), then their lookups kLookupBatch at a time
+    unsigned todo = 0;
+    for (int t = 0; t < 26; ++t) {
+        int dx, dy, dz;
+        shell_cell(1, t, dx, dy, dz);
+        const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
+        if (nb_lb(dx, dy, dz) <= b0 && x >= blo[0] && x <= bhi[0] && y >= blo[1] && y <= bhi[1] && z >= blo[2] &&
+            z <= bhi[2])
+            todo |= 1u << t;
+    }
+    while (todo) {
+        unsigned long long keys[kLookupBatch];
+        bool valid[kLookupBatch];
+        float lbs[kLookupBatch];
+#pragma unroll
+        for (int u = 0; u < kLookupBatch; ++u) {
+            valid[u] = todo != 0;
+            const int t = valid[u] ? __ffs(todo) - 1 : 0;
+            todo &= todo - 1;
+            int dx, dy, dz;
+            shell_cell(1, t, dx, dy, dz);
+            keys[u] = cell_key(0, qc.c[0] + dx, qc.c[1] + dy, qc.c[2] + dz);
+            lbs[u] = nb_lb(dx, dy, dz);
+        }
+        uint2 se[kLookupBatch];
+        lookup_batch(a.table, a.mask, keys, valid, se);
+#pragma unroll
+        for (int u = 0; u < kLookupBatch; ++u)
+            if (valid[u] && se[u].y && lbs[u] <= nn_bound(a, nn)) scan_target_cell(a, se[u], qx, qy, qz, nn);
+    }
+}
+
+// K3 transform: q_r = ((R_r0 x + R_r1 y) + R_r2 z) + t_r, binary64, no contraction (R15)
+__device__ __forceinline__ void k3(const double *T, float x, float y, float z, double &q0, double &q1, double &q2) {
+    const double xd = x, yd = y, zd = z;
+    q0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(T[0], xd), __dmul_rn(T[1], yd)), __dmul_rn(T[2], zd)), T[3]);
+    q1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(T[4], xd), __dmul_rn(T[5], yd)), __dmul_rn(T[6], zd)), T[7]);
+    q2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(T[8], xd), __dmul_rn(T[9], yd)), __dmul_rn(T[10], zd)), T[11]);
+}
+
+// Eq. 1 terms of one valid pair (binary64).  Returns false if Sigma is not positive definite.
+__device__ __forceinline__ bool pair_terms(const double *T, double q0, double q1, double q2, float4 ca, float4 cb,
+                                           float4 m, float4 ta, float4 tb, double *acc) {
+    const double Cs[3][3] = {{ca.x, ca.y, ca.z}, {ca.y, ca.w, cb.x}, {ca.z, cb.x, cb.y}};
+    const double R[3][3] = {{T[0], T[1], T[2]}, {T[4], T[5], T[6]}, {T[8], T[9], T[10]}};
+    double RC[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) RC[r][c] = R[r][0] * Cs[0][c] + R[r][1] * Cs[1][c] + R[r][2] * Cs[2][c];
+    double S[6];
+    const int ri[6] = {0, 0, 0, 1, 1, 2}, ci[6] = {0, 1, 2, 1, 2, 2};
+    const double Ct[6] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y};
+#pragma unroll
+    for (int e = 0; e < 6; ++e)
+        S[e] = Ct[e] + RC[ri[e]][0] * R[ci[e]][0] + RC[ri[e]][1] * R[ci[e]][1] + RC[ri[e]][2] * R[ci[e]][2];
+    // M = S^{-1} by the adjugate
+    const double A00 = S[3] * S[5] - S[4] * S[4];
+    const double A01 = S[2] * S[4] - S[1] * S[5];
+    const double A02 = S[1] * S[4] - S[2] * S[3];
+    const double A11 = S[0] * S[5] - S[2] * S[2];
+    const double A12 = S[1] * S[2] - S[0] * S[4];
+    const double A22 = S[0] * S[3] - S[1] * S[1];
+    const double det = S[0] * A00 + S[1] * A01 + S[2] * A02;
+    if (!(det > 0.0)) return false;
+    const double id = 1.0 / det;
+    const double M[3][3] = {{A00 * id, A01 * id, A02 * id}, {A01 * id, A11 * id, A12 * id}, {A02 * id, A12 * id, A22 * id}};
+    const double d[3] = {(double)m.x - q0, (double)m.y - q1, (double)m.z - q2};
+    const double J[3][6] = {{0.0, -q2, q1, -1.0, 0.0, 0.0}, {q2, 0.0, -q0, 0.0, -1.0, 0.0}, {-q1, q0, 0.0, 0.0, 0.0, -1.0}};
+    double MJ[3][6], Md[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) MJ[r][c] = M[r][0] * J[0][c] + M[r][1] * J[1][c] + M[r][2] * J[2][c];
+        Md[r] = M[r][0] * d[0] + M[r][1] * d[1] + M[r][2] * d[2];
+    }
+    int t = 0;
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = r; c < 6; ++c) acc[t++] += J[0][r] * MJ[0][c] + J[1][r] * MJ[1][c] + J[2][r] * MJ[2][c];
+#pragma unroll
+    for (int r = 0; r < 6; ++r) acc[21 + r] += J[0][r] * Md[0] + J[1][r] * Md[1] + J[2][r] * Md[2];
+    acc[27] += d[0] * Md[0] + d[1] * Md[1] + d[2] * Md[2];
+    acc[28] += 1.0;
+    return true;
 }
 
 __device__ __forceinline__ void so3_exp(const double *w, double *R) {
@@ -216,11 +328,24 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     const int n = *a.d_n;
     if (tid < 12) sT[tid] = a.d_T[tid];
     if (a.timeline && blockIdx.x == 0 && tid == 0 && a.timeline_cap > 0) a.timeline[0] = globaltimer_ns();
-    if (tid < 6) {
-        const float inv_h = a.inv_h;
-        sBox[tid] = cell_coord(ordered_to_float_(a.tbbox[tid]), inv_h);
-    }
+    if (tid < 6) sBox[tid] = cell_coord(ordered_to_float_(a.tbbox[tid]), a.inv_h);
     if (tid == 0) sDone = 0;
+    // resident point of this thread: source data, current match and own target cell in registers
+    const int i0 = blockIdx.x * kT + tid;
+    const bool has0 = i0 < n;
+    float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), ca0 = x0, cb0 = x0;
+    if (has0) {
+        x0 = __ldg(a.spos + i0);
+        ca0 = __ldg(a.scov_a + i0);
+        cb0 = __ldg(a.scov_b + i0);
+    }
+    NN m0;                                // warm start carried across iterations
+    float4 ta0 = x0, tb0 = x0;            // covariance of m0.slot (valid iff cov_slot == m0.slot)
+    int cov_slot = -1;
+    int own_c[3] = {INT_MIN, INT_MIN, INT_MIN};
+    uint2 own_se = make_uint2(0u, 0u);
+    bool valid0 = false;
+    int dbg_slow = 0, dbg_probes = 0, dbg_cands = 0, dbg_its = 0;
     __syncthreads();
     int status = GSICP_WARN_MAX_ITERS, iters = 0, converged = 0;
     double n_in = 0.0, cost_last = 0.0;
@@ -234,109 +359,90 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             }
         };
         stamp(0);
-        // ------------------------------------------------------------ A6 + A7
-        double acc[28];
+        double T[12];
 #pragma unroll
-        for (int k = 0; k < 28; ++k) acc[k] = 0.0;
-        double cnt = 0.0;
-        const double R00 = sT[0], R01 = sT[1], R02 = sT[2], t0 = sT[3];
-        const double R10 = sT[4], R11 = sT[5], R12 = sT[6], t1 = sT[7];
-        const double R20 = sT[8], R21 = sT[9], R22 = sT[10], t2 = sT[11];
-        // phase A: correspondences (no accumulator live, so the search gets the registers)
-        for (int i = blockIdx.x * kT + tid; i < n; i += G * kT) {
-            const float4 x = __ldg(a.spos + i);
-            const double xd = x.x, yd = x.y, zd = x.z;
-            // K3: q_r = ((R_r0 x + R_r1 y) + R_r2 z) + t_r, binary64, no contraction
-            const double q0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R00, xd), __dmul_rn(R01, yd)), __dmul_rn(R02, zd)), t0);
-            const double q1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R10, xd), __dmul_rn(R11, yd)), __dmul_rn(R12, zd)), t1);
-            const double q2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R20, xd), __dmul_rn(R21, yd)), __dmul_rn(R22, zd)), t2);
-            const float qx = __double2float_rn(q0), qy = __double2float_rn(q1), qz = __double2float_rn(q2);
-            unsigned long long best = kEmptyKey;
-            int slot = a.corr_ws[i];
-            if (slot <= -2) slot = -2 - slot;  // previous match was gated out: still a warm start
-            if (slot >= 0) {
-                const float4 p = __ldg(a.tpos + slot);
-                best = pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
+        for (int k = 0; k < 12; ++k) T[k] = sT[k];
+        // ------------------------------------------------------------ A6: correspondences
+        double q0r = 0.0, q1r = 0.0, q2r = 0.0;
+        if (has0) {
+            k3(T, x0.x, x0.y, x0.z, q0r, q1r, q2r);
+            const float qx = __double2float_rn(q0r), qy = __double2float_rn(q1r), qz = __double2float_rn(q2r);
+            const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
+            if (qc.c[0] != own_c[0] || qc.c[1] != own_c[1] || qc.c[2] != own_c[2]) {
+                own_c[0] = qc.c[0]; own_c[1] = qc.c[1]; own_c[2] = qc.c[2];
+                own_se = cell_lookup(a.table, a.mask, cell_key(0, qc.c[0], qc.c[1], qc.c[2]));
             }
-            nn_search(a, sBox, qx, qy, qz, best, slot);
-            a.corr_ws[i] = (slot >= 0 && ki_key(best) < a.r2) ? slot : -2 - slot;  // invalid: -2 - warm start
+            NN nn;
+            if (m0.slot >= 0) {  // warm start from the previous match (record kept in registers)
+                nn.p = m0.p;
+                nn.slot = m0.slot;
+                nn.best = pack_ki(canon_key(qx, qy, qz, m0.p.x, m0.p.y, m0.p.z), (uint32_t)__float_as_int(m0.p.w));
+            }
+            nn_search(a, sBox, qc, own_se, qx, qy, qz, nn);
+            dbg_slow += nn.slow;
+            dbg_probes += nn.probes;
+            dbg_cands += nn.cands;
+            ++dbg_its;
+            m0 = nn;
+            valid0 = nn.slot >= 0 && ki_key(nn.best) < a.r2;
+        }
+        for (int i = i0 + G * kT; i < n; i += G * kT) {  // non-resident points (large clouds)
+            const float4 x = __ldg(a.spos + i);
+            double q0, q1, q2;
+            k3(T, x.x, x.y, x.z, q0, q1, q2);
+            const float qx = __double2float_rn(q0), qy = __double2float_rn(q1), qz = __double2float_rn(q2);
+            const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
+            NN nn;
+            int slot = a.corr_ws[i];
+            if (slot <= -2) slot = -2 - slot;
+            if (slot >= 0) {
+                nn.p = __ldg(a.tpos + slot);
+                nn.slot = slot;
+                nn.best = pack_ki(canon_key(qx, qy, qz, nn.p.x, nn.p.y, nn.p.z), (uint32_t)__float_as_int(nn.p.w));
+            }
+            nn_search(a, sBox, qc, cell_lookup(a.table, a.mask, cell_key(0, qc.c[0], qc.c[1], qc.c[2])), qx, qy, qz, nn);
+            a.corr_ws[i] = (nn.slot >= 0 && ki_key(nn.best) < a.r2) ? nn.slot : -2 - nn.slot;
         }
         stamp(1);
-        // phase B: Eq. 1 terms of the valid pairs
-        for (int i = blockIdx.x * kT + tid; i < n; i += G * kT) {
-            const int cw = a.corr_ws[i];
-            const bool valid = cw >= 0;
-            const int slot = cw;
-            const float4 x = __ldg(a.spos + i);
-            const double xd = x.x, yd = x.y, zd = x.z;
-            const double q0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R00, xd), __dmul_rn(R01, yd)), __dmul_rn(R02, zd)), t0);
-            const double q1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R10, xd), __dmul_rn(R11, yd)), __dmul_rn(R12, zd)), t1);
-            const double q2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(R20, xd), __dmul_rn(R21, yd)), __dmul_rn(R22, zd)), t2);
+        // ------------------------------------------------------------ A7: Eq. 1 terms
+        double acc[kAlignTerms];
+#pragma unroll
+        for (int k = 0; k < kAlignTerms; ++k) acc[k] = 0.0;
+        if (has0) {
             int32_t corr_val = -1;
-            if (valid) {
-                const float4 ca = __ldg(a.scov_a + i), cb = __ldg(a.scov_b + i);
-                const float4 ta = __ldg(a.tcov_a + slot), tb = __ldg(a.tcov_b + slot);
-                const float4 m = __ldg(a.tpos + slot);
-                // R Cs R^T + Ct (symmetric)
-                const double Cs[3][3] = {{ca.x, ca.y, ca.z}, {ca.y, ca.w, cb.x}, {ca.z, cb.x, cb.y}};
-                const double R[3][3] = {{R00, R01, R02}, {R10, R11, R12}, {R20, R21, R22}};
-                double RC[3][3];
-#pragma unroll
-                for (int r = 0; r < 3; ++r)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) RC[r][c] = R[r][0] * Cs[0][c] + R[r][1] * Cs[1][c] + R[r][2] * Cs[2][c];
-                double S[6];
-                const int ri[6] = {0, 0, 0, 1, 1, 2}, ci[6] = {0, 1, 2, 1, 2, 2};
-                const double Ct[6] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y};
-#pragma unroll
-                for (int e = 0; e < 6; ++e)
-                    S[e] = Ct[e] + RC[ri[e]][0] * R[ci[e]][0] + RC[ri[e]][1] * R[ci[e]][1] + RC[ri[e]][2] * R[ci[e]][2];
-                // M = S^{-1} by the adjugate (binary64)
-                const double A00 = S[3] * S[5] - S[4] * S[4];
-                const double A01 = S[2] * S[4] - S[1] * S[5];
-                const double A02 = S[1] * S[4] - S[2] * S[3];
-                const double A11 = S[0] * S[5] - S[2] * S[2];
-                const double A12 = S[1] * S[2] - S[0] * S[4];
-                const double A22 = S[0] * S[3] - S[1] * S[1];
-                const double det = S[0] * A00 + S[1] * A01 + S[2] * A02;
-                if (det > 0.0) {
-                    const double id = 1.0 / det;
-                    const double M[3][3] = {{A00 * id, A01 * id, A02 * id}, {A01 * id, A11 * id, A12 * id}, {A02 * id, A12 * id, A22 * id}};
-                    const double d[3] = {(double)m.x - q0, (double)m.y - q1, (double)m.z - q2};
-                    const double J[3][6] = {{0.0, -q2, q1, -1.0, 0.0, 0.0}, {q2, 0.0, -q0, 0.0, -1.0, 0.0}, {-q1, q0, 0.0, 0.0, 0.0, -1.0}};
-                    double MJ[3][6], Md[3];
-#pragma unroll
-                    for (int r = 0; r < 3; ++r) {
-#pragma unroll
-                        for (int c = 0; c < 6; ++c) MJ[r][c] = M[r][0] * J[0][c] + M[r][1] * J[1][c] + M[r][2] * J[2][c];
-                        Md[r] = M[r][0] * d[0] + M[r][1] * d[1] + M[r][2] * d[2];
-                    }
-                    int t = 0;
-#pragma unroll
-                    for (int r = 0; r < 6; ++r)
-#pragma unroll
-                        for (int c = r; c < 6; ++c) acc[t++] += J[0][r] * MJ[0][c] + J[1][r] * MJ[1][c] + J[2][r] * MJ[2][c];
-#pragma unroll
-                    for (int r = 0; r < 6; ++r) acc[21 + r] += J[0][r] * Md[0] + J[1][r] * Md[1] + J[2][r] * Md[2];
-                    acc[27] += d[0] * Md[0] + d[1] * Md[1] + d[2] * Md[2];
-                    cnt += 1.0;
-                    corr_val = __float_as_int(m.w);
+            if (valid0) {
+                if (cov_slot != m0.slot) {
+                    ta0 = __ldg(a.tcov_a + m0.slot);
+                    tb0 = __ldg(a.tcov_b + m0.slot);
+                    cov_slot = m0.slot;
                 }
+                if (pair_terms(T, q0r, q1r, q2r, ca0, cb0, m0.p, ta0, tb0, acc)) corr_val = __float_as_int(m0.p.w);
+            }
+            if (a.corr_out) a.corr_out[i0] = corr_val;
+        }
+        for (int i = i0 + G * kT; i < n; i += G * kT) {
+            const int slot = a.corr_ws[i];
+            int32_t corr_val = -1;
+            if (slot >= 0) {
+                const float4 x = __ldg(a.spos + i);
+                double q0, q1, q2;
+                k3(T, x.x, x.y, x.z, q0, q1, q2);
+                const float4 m = __ldg(a.tpos + slot);
+                if (pair_terms(T, q0, q1, q2, __ldg(a.scov_a + i), __ldg(a.scov_b + i), m, __ldg(a.tcov_a + slot),
+                               __ldg(a.tcov_b + slot), acc))
+                    corr_val = __float_as_int(m.w);
             }
             if (a.corr_out) a.corr_out[i] = corr_val;
         }
         stamp(2);
         // ------------------------------------------------------------ block reduction
 #pragma unroll
-        for (int k = 0; k < 28; ++k)
+        for (int k = 0; k < kAlignTerms; ++k)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         if (lane == 0) {
 #pragma unroll
-            for (int k = 0; k < 28; ++k) sRed[warp][k] = acc[k];
-            sRed[warp][28] = cnt;
+            for (int k = 0; k < kAlignTerms; ++k) sRed[warp][k] = acc[k];
         }
         __syncthreads();
         double *part = a.partials + (size_t)(it & 1) * G * kPad;
@@ -455,6 +561,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         stamp(5);
         if (sDone) break;
     }
+    if (a.debug && has0) a.debug[i0] = make_int4(dbg_slow, dbg_probes, dbg_cands, dbg_its);
     if (blockIdx.x == 0 && tid == 0) {
         if (!a.linearize_only) {
             for (int k = 0; k < 12; ++k) a.d_T[k] = sT[k];
@@ -471,12 +578,15 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     }
 }
 
-int align_grid_blocks(int cap) {
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_align, kT, 0);
-        if (per_sm < 1) per_sm = 1;
+// Co-resident grid for the cooperative launch (0 if the kernel cannot be resident at all).
+int align_grid_blocks(int cap, int *per_sm_out) {
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        int v = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_align, kT, 0) != cudaSuccess) v = 0;
+        per_sm = v;
     }
+    *per_sm_out = per_sm;
     const int need = (int)blocks_for(cap > 0 ? cap : 1, kT);
     const int maxb = per_sm * num_sms();
     return need < maxb ? need : maxb;
@@ -554,9 +664,18 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
     a.corr_out = corr_out;
     a.timeline = g_align_timeline;
     a.timeline_cap = g_align_timeline_cap;
+    a.debug = reinterpret_cast<int4 *>(g_align_debug);
     k_align_init<<<blocks_for(src.cap > 0 ? src.cap : 1, 256), 256, 0, s>>>(w.corr_ws, src.cap, w.barrier);
     GSICP_LAUNCH_CHECK("k_align_init");
-    const int G = align_grid_blocks(src.cap);
+    int per_sm = 0;
+    const int G = align_grid_blocks(src.cap, &per_sm);
+    if (G < 1) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, k_align);
+        set_error("k_align cannot be co-resident: occupancy %d blocks/SM (regs %d, local %zu B, max threads %d)",
+                  per_sm, fa.numRegs, fa.localSizeBytes, fa.maxThreadsPerBlock);
+        return cudaErrorCooperativeLaunchTooLarge;
+    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeCooperative;

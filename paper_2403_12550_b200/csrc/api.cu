@@ -14,6 +14,7 @@ static thread_local uint64_t g_launches = 0;
 extern thread_local int32_t *g_knn_debug;  // knn_cov.cu
 extern thread_local long long *g_align_timeline;  // align.cu
 extern thread_local long long g_align_timeline_cap;
+extern thread_local int32_t *g_align_debug;
 
 void note_launch(int n) { g_launches += (uint64_t)n; }
 void set_error(const char *fmt, ...) {
@@ -107,6 +108,7 @@ const char *gsicp_status_string(gsicp_status s) {
 
 const char *gsicp_last_error(void) { return g_err; }
 void gsicp_debug_knn_counters(int32_t *d_out) { gsicp::g_knn_debug = d_out; }
+void gsicp_debug_align_counters(int32_t *d_out) { gsicp::g_align_debug = d_out; }
 void gsicp_debug_align_timeline(int64_t *d_out, int64_t capacity) {
     gsicp::g_align_timeline = reinterpret_cast<long long *>(d_out);
     gsicp::g_align_timeline_cap = d_out ? capacity : 0;

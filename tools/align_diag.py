@@ -21,10 +21,25 @@ def main():
     tr.preprocess(depth)
     means, quats, scales = (torch.from_numpy(x).to(dev) for x in (w.means, w.quats, w.scales))
     tl = torch.zeros(1 << 16, dtype=torch.int64, device=dev)
-    for cell_mult in (0.0, 2.0, 3.0, 4.0, 6.0):
-        tgt = g.build_target(means, quats, scales, cell=cell_mult * w.ell if cell_mult else 0.0)
+    w5 = synth.make_frame_workload(2, "replica", M=100_000, stride=4)
+    small = tuple(torch.from_numpy(x).to(dev) for x in (w5.means, w5.quats, w5.scales))
+    cases = [("1e6", means, quats, scales, m * w.ell if m else 0.0) for m in (0.0, 4.0)]
+    cases += [("1e5", *small, m * w5.ell if m else 0.0) for m in (0.0, 4.0)]
+    for name, mm, qq, ss, cell in cases:
+        print(f"map {name}")
+        tgt = g.build_target(mm, qq, ss, cell=cell)
         for _ in range(3):
             T, st = g.align(tr.cloud, tgt, w.T_init, tr.params, tr.ws_align)
+        cnt = torch.zeros((tr.cap, 4), dtype=torch.int32, device=dev)
+        g.debug_align_counters(cnt)
+        T, st = g.align(tr.cloud, tgt, w.T_init, tr.params, tr.ws_align)
+        g.debug_align_counters(None)
+        c = cnt[:tr.cloud.n()].cpu().numpy().astype(np.float64)
+        its = np.maximum(c[:, 3], 1)
+        for j, nm in enumerate(["slow", "probes", "cands"]):
+            v = c[:, j] / its
+            print(f"  per point-iteration {nm:6s}: mean {v.mean():7.2f} p50 {np.percentile(v, 50):7.2f} "
+                  f"p99 {np.percentile(v, 99):7.2f} max {v.max():7.2f}   (sum over iters: mean {c[:, j].mean():.1f})")
         tl.zero_()
         g.debug_align_timeline(tl)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -70,7 +70,11 @@ typedef struct {
     const float *cov_a;   /* [dev] float4[M], cell order                          */
     const float *cov_b;   /* [dev] float4[M], cell order                          */
     const void *table;    /* [dev] open-addressing cell table                     */
-    const int32_t *bbox;  /* [dev] int32[6] min/max cell coordinates              */
+    const int32_t *bbox;  /* [dev] int32[6] ordered-int float bbox of the means   */
+    const void *dense;    /* [dev] dense (start, count) cell array over the bbox, */
+    const int32_t *dense_hdr; /* [dev] {in_use, lo xyz, dims xyz}: used when it fits */
+    const int32_t *nbr;   /* [dev] int32[M][16] exact 16-NN slots of each slot (kNN graph) */
+    const float *nbr_key; /* [dev] float[M] key of the 16th neighbour                     */
     uint32_t table_mask;  /* table slots - 1                                      */
     float cell;           /* cell edge h (m)                                      */
     int32_t M;

@@ -45,7 +45,9 @@ class _Cloud(C.Structure):
 
 class _Target(C.Structure):
     _fields_ = [("pos", C.c_void_p), ("cov_a", C.c_void_p), ("cov_b", C.c_void_p), ("table", C.c_void_p),
-                ("bbox", C.c_void_p), ("table_mask", C.c_uint32), ("cell", C.c_float), ("M", C.c_int32)]
+                ("bbox", C.c_void_p), ("dense", C.c_void_p), ("dense_hdr", C.c_void_p), ("nbr", C.c_void_p),
+                ("nbr_key", C.c_void_p),
+                ("table_mask", C.c_uint32), ("cell", C.c_float), ("M", C.c_int32)]
 
 
 class AlignParams(C.Structure):

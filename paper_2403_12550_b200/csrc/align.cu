@@ -46,6 +46,10 @@ struct AlignArgs {
     float h, inv_h;
     const float4 *tpos, *tcov_a, *tcov_b;
     const int32_t *tbbox;
+    const uint2 *dense;       // dense cell array (used iff dense_hdr[0])
+    const int32_t *dense_hdr; // {in_use, lo xyz, dims xyz}
+    const int32_t *nbr;       // nullable: target kNN graph, [M][kGraphK] slots
+    const float *nbr_key;     // [M] key of the kGraphK-th neighbour
     int max_iters;
     float r, r2;
     double eps_rot, eps_trans;
@@ -85,7 +89,8 @@ struct NN {
     int probes = 0, cands = 0, slow = 0;  // diagnostics
 };
 
-constexpr int kCandBatch = 8;  // candidate records loaded together (one latency per batch)
+constexpr int kCandBatch = 4;   // candidate records loaded together (one latency per batch)
+constexpr int kNbBatch = 4;     // neighbour-cell lookups in flight together (fast path)
 
 __device__ __forceinline__ void scan_target_cell(const AlignArgs &a, uint2 se, float qx, float qy, float qz, NN &nn) {
     ++nn.probes;
@@ -113,10 +118,96 @@ __device__ __forceinline__ float nn_bound(const AlignArgs &a, const NN &nn) {
     return nn.best != kEmptyKey ? fminf(ki_key(nn.best), a.r2) : a.r2;
 }
 
+// Certified graph step: nn holds a candidate slot j with key k_j.  Every target k that could beat
+// it satisfies |m_j - m_k| <= 2 |q - m_j| (triangle inequality), so if 4 k_j < key_K(j) (with
+// slack for binary32 rounding of both keys) all of them are in j's exact K-NN list and the 1-NN
+// of q is the best of that list (self included).  Returns false (nn untouched) otherwise.
+__device__ __forceinline__ bool graph_nn(const AlignArgs &a, float qx, float qy, float qz, NN &nn) {
+    const int j = nn.slot;
+    const float kj = ki_key(nn.best);
+    const float kk = __ldg(a.nbr_key + j);
+    if (!(4.f * kj * (1.f + 4e-5f) < kk * (1.f - 4e-5f))) return false;
+    const int4 *lst = reinterpret_cast<const int4 *>(a.nbr + (size_t)j * kGraphK);
+    int sl[kGraphK];
+#pragma unroll
+    for (int v = 0; v < kGraphK / 4; ++v) {
+        const int4 w = __ldg(lst + v);
+        sl[4 * v] = w.x; sl[4 * v + 1] = w.y; sl[4 * v + 2] = w.z; sl[4 * v + 3] = w.w;
+    }
+    float4 p[kGraphK];
+#pragma unroll
+    for (int u = 0; u < kGraphK; ++u) p[u] = sl[u] >= 0 ? __ldg(a.tpos + sl[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    ++nn.probes;
+    nn.cands += kGraphK;
+#pragma unroll
+    for (int u = 0; u < kGraphK; ++u) {
+        if (sl[u] < 0) continue;
+        const unsigned long long v = pack_ki(canon_key(qx, qy, qz, p[u].x, p[u].y, p[u].z), (uint32_t)__float_as_int(p[u].w));
+        if (v < nn.best) {
+            nn.best = v;
+            nn.slot = sl[u];
+            nn.p = p[u];
+        }
+    }
+    return true;
+}
+
+constexpr int kMaxCells = 8;   // cells gathered for one flattened candidate scan (own + 7 neighbours)
+constexpr int kFlatBatch = 8;  // candidate records loaded per round trip in the flattened scan
+
+// Candidates of up to kMaxCells cells scanned as one flattened range, kFlatBatch records per
+// round trip (instead of one chain of round trips per cell); a cell's records are skipped once
+// its lower bound exceeds the shrinking bound.
+__device__ __forceinline__ void scan_cells_flat(const AlignArgs &a, const uint2 (&se)[kMaxCells],
+                                                const float (&lbs)[kMaxCells], float qx, float qy, float qz, NN &nn) {
+    uint32_t pre[kMaxCells + 1];
+    pre[0] = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxCells; ++k) {
+        pre[k + 1] = pre[k] + se[k].y;
+        nn.probes += se[k].y ? 1 : 0;
+    }
+    const uint32_t tot = pre[kMaxCells];
+    nn.cands += (int)tot;
+    for (uint32_t base = 0; base < tot; base += kFlatBatch) {
+        const float bnd = nn_bound(a, nn);
+        float4 p[kFlatBatch];
+        uint32_t slot[kFlatBatch];
+        bool ok[kFlatBatch];
+#pragma unroll
+        for (int u = 0; u < kFlatBatch; ++u) {
+            const uint32_t item = base + u;
+            uint32_t s = 0;
+            bool v = false;
+#pragma unroll
+            for (int k = 0; k < kMaxCells; ++k) {
+                const bool in = item >= pre[k] && item < pre[k + 1];
+                s = in ? se[k].x + (item - pre[k]) : s;
+                v = in ? lbs[k] <= bnd : v;
+            }
+            ok[u] = v;
+            slot[u] = s;
+            p[u] = v ? __ldg(a.tpos + s) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kFlatBatch; ++u) {
+            if (!ok[u]) continue;
+            const unsigned long long v =
+                pack_ki(canon_key(qx, qy, qz, p[u].x, p[u].y, p[u].z), (uint32_t)__float_as_int(p[u].w));
+            if (v < nn.best) {
+                nn.best = v;
+                nn.slot = (int)slot[u];
+                nn.p = p[u];
+            }
+        }
+    }
+}
+
 // General exact search after the own cell: grow shells while an ungated search has found
 // nothing, then the ball traversal bounded by min(best, r^2).  Out of line so that the
 // common fast path keeps its registers.
-__device__ __noinline__ void nn_slow(const AlignArgs &a, const int *sb, float qx, float qy, float qz, NN &nn) {
+__device__ __forceinline__ void nn_slow(const AlignArgs &a, const CellIndex &idx, const int *sb, float qx, float qy,
+                                     float qz, NN &nn) {
     const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
     const int *blo = sb, *bhi = sb + 3;
     int m_done = 0;
@@ -129,71 +220,91 @@ __device__ __noinline__ void nn_slow(const AlignArgs &a, const int *sb, float qx
                 shell_cell(m_done, t, dx, dy, dz);
                 const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
                 if (x < blo[0] || x > bhi[0] || y < blo[1] || y > bhi[1] || z < blo[2] || z > bhi[2]) continue;
-                scan_target_cell(a, cell_lookup(a.table, a.mask, cell_key(0, x, y, z)), qx, qy, qz, nn);
+                scan_target_cell(a, idx.one(x, y, z), qx, qy, qz, nn);
             }
         }
     }
     ball_search(
-        qc, a.table, a.mask, blo, bhi,
-        [&](int dx, int dy, int dz) { return max(max(abs(dx), abs(dy)), abs(dz)) <= m_done; },
-        [](int x, int y, int z) { return cell_key(0, x, y, z); },
+        qc, idx, blo, bhi, [&](int dx, int dy, int dz) { return max(max(abs(dx), abs(dy)), abs(dz)) <= m_done; },
         [&](uint2 se) { scan_target_cell(a, se, qx, qy, qz, nn); }, [&]() { return nn_bound(a, nn); });
 }
 
 // Exact 1-NN given the query's cell geometry and its own cell's (start, count) (already known).
 // Fast path: when the ball of the current bound cannot reach offset +-2 on any axis, only the 26
-// neighbours can qualify; they are tested by their gaps alone.
-__device__ __forceinline__ void nn_search(const AlignArgs &a, const int *sb, const QueryCell &qc, uint2 own, float qx,
-                                          float qy, float qz, NN &nn) {
-    scan_target_cell(a, own, qx, qy, qz, nn);
-    const float b0 = nn_bound(a, nn);
-    float glo[3], ghi[3];
-    bool fits = true;
+// neighbours can qualify; they are tested by their gaps alone — and none at all when the ball
+// stays inside the own cell (the common, warm-started case).
+__device__ __forceinline__ void nn_search(const AlignArgs &a, const CellIndex &idx, const int *sb,
+                                          const QueryCell &qc, uint2 own, float qx, float qy, float qz, NN &nn) {
+    float glo[3], ghi[3], glo2[3], ghi2[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         glo[k] = qc.gap2(-1, k);
         ghi[k] = qc.gap2(1, k);
-        fits = fits && qc.gap2(-2, k) > b0 && qc.gap2(2, k) > b0;
+        glo2[k] = qc.gap2(-2, k);
+        ghi2[k] = qc.gap2(2, k);
     }
-    if (!fits) {
-        ++nn.slow;
-        nn_slow(a, sb, qx, qy, qz, nn);
-        return;
+    auto fits = [&](float b) {
+        return glo2[0] > b && ghi2[0] > b && glo2[1] > b && ghi2[1] > b && glo2[2] > b && ghi2[2] > b;
+    };
+    // bound from the warm start; without one (or too loose) scan the own cell first
+    float b = nn_bound(a, nn);
+    bool own_pending = true;
+    if (!fits(b)) {
+        scan_target_cell(a, own, qx, qy, qz, nn);
+        own_pending = false;
+        b = nn_bound(a, nn);
+        if (!fits(b)) {
+            // the general search gets a copy: taking nn's address would pin it to local memory
+            NN tmp = nn;
+            ++tmp.slow;
+            nn_slow(a, idx, sb, qx, qy, qz, tmp);
+            nn = tmp;
+            return;
+        }
     }
     const int *blo = sb, *bhi = sb + 3;
     auto nb_lb = [&](int dx, int dy, int dz) {
         return (dx ? (dx < 0 ? glo[0] : ghi[0]) : 0.f) + (dy ? (dy < 0 ? glo[1] : ghi[1]) : 0.f) +
                (dz ? (dz < 0 ? glo[2] : ghi[2]) : 0.f);
     };
-    // qualifying neighbours (gap test only, no loads), then their lookups kLookupBatch at a time
+    // the ball of bound b reaches at most the 26 neighbours: pick them by their gaps (no loads)
     unsigned todo = 0;
-    for (int t = 0; t < 26; ++t) {
-        int dx, dy, dz;
-        shell_cell(1, t, dx, dy, dz);
-        const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
-        if (nb_lb(dx, dy, dz) <= b0 && x >= blo[0] && x <= bhi[0] && y >= blo[1] && y <= bhi[1] && z >= blo[2] &&
-            z <= bhi[2])
-            todo |= 1u << t;
+    if (glo[0] <= b || ghi[0] <= b || glo[1] <= b || ghi[1] <= b || glo[2] <= b || ghi[2] <= b) {
+        for (int t = 0; t < 26; ++t) {
+            int dx, dy, dz;
+            shell_cell(1, t, dx, dy, dz);
+            const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
+            if (nb_lb(dx, dy, dz) <= b && x >= blo[0] && x <= bhi[0] && y >= blo[1] && y <= bhi[1] && z >= blo[2] &&
+                z <= bhi[2])
+                todo |= 1u << t;
+        }
     }
-    while (todo) {
-        unsigned long long keys[kLookupBatch];
-        bool valid[kLookupBatch];
-        float lbs[kLookupBatch];
+    // own cell (if pending) + up to kMaxCells-1 neighbours per round: one batch of lookups, then
+    // all their candidates as one flattened range
+    while (own_pending || todo) {
+        int xs[kMaxCells], ys[kMaxCells], zs[kMaxCells];
+        bool valid[kMaxCells];
+        float lbs[kMaxCells];
+        valid[0] = false;
+        xs[0] = ys[0] = zs[0] = 0;
+        lbs[0] = 0.f;
 #pragma unroll
-        for (int u = 0; u < kLookupBatch; ++u) {
+        for (int u = 1; u < kMaxCells; ++u) {
             valid[u] = todo != 0;
             const int t = valid[u] ? __ffs(todo) - 1 : 0;
             todo &= todo - 1;
             int dx, dy, dz;
             shell_cell(1, t, dx, dy, dz);
-            keys[u] = cell_key(0, qc.c[0] + dx, qc.c[1] + dy, qc.c[2] + dz);
+            xs[u] = qc.c[0] + dx;
+            ys[u] = qc.c[1] + dy;
+            zs[u] = qc.c[2] + dz;
             lbs[u] = nb_lb(dx, dy, dz);
         }
-        uint2 se[kLookupBatch];
-        lookup_batch(a.table, a.mask, keys, valid, se);
-#pragma unroll
-        for (int u = 0; u < kLookupBatch; ++u)
-            if (valid[u] && se[u].y && lbs[u] <= nn_bound(a, nn)) scan_target_cell(a, se[u], qx, qy, qz, nn);
+        uint2 se[kMaxCells];
+        idx.batch(xs, ys, zs, valid, se);
+        se[0] = own_pending ? own : make_uint2(0u, 0u);
+        own_pending = false;
+        scan_cells_flat(a, se, lbs, qx, qy, qz, nn);
     }
 }
 
@@ -311,6 +422,71 @@ __device__ __forceinline__ bool chol6_solve(const double *H, const double *rhs, 
     return true;
 }
 
+// A8 for one block (thread 0): solve H delta = -b, update the shared pose, convergence test.
+// Out of line: its ~150 live doubles must not raise the register pressure of the point loop.
+// Returns 1 when the loop is done (status set).
+__device__ __forceinline__ int solve_step(const AlignArgs &a, const double *sAcc, double *sT, int it, int n, int &status,
+                                       int &iters, int &converged) {
+    double H[36], b[6];
+    int t = 0;
+    for (int r = 0; r < 6; ++r)
+        for (int c = r; c < 6; ++c) H[6 * r + c] = H[6 * c + r] = sAcc[t++];
+    for (int r = 0; r < 6; ++r) b[r] = sAcc[21 + r];
+    const double n_in = sAcc[28];
+    if (a.linearize_only) {
+        if (blockIdx.x == 0) {
+            for (int k = 0; k < 36; ++k) a.d_lin[k] = H[k];
+            for (int k = 0; k < 6; ++k) a.d_lin[36 + k] = b[k];
+            a.d_lin[42] = sAcc[27];
+            a.d_lin[43] = n_in;
+        }
+        status = GSICP_OK;
+        return 1;
+    }
+    if (n == 0) {
+        status = GSICP_ERR_DEGENERATE_FRAME;
+        return 1;
+    }
+    if (n_in < (double)a.min_pairs) {
+        status = GSICP_ERR_TRACKING_LOST;
+        return 1;
+    }
+    double nb[6], delta[6];
+    for (int k = 0; k < 6; ++k) nb[k] = -b[k];
+    bool ok = chol6_solve(H, nb, delta);
+    if (!ok) {
+        double tr = 0.0;
+        for (int k = 0; k < 6; ++k) tr += H[7 * k];
+        for (int k = 0; k < 6; ++k) H[7 * k] += 1e-6 * tr / 6.0;
+        ok = chol6_solve(H, nb, delta);
+    }
+    if (!ok) {
+        status = GSICP_ERR_TRACKING_LOST;
+        return 1;
+    }
+    double E[9];
+    so3_exp(delta, E);
+    double Tn[12];
+    for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) Tn[4 * r + c] = E[3 * r] * sT[c] + E[3 * r + 1] * sT[4 + c] + E[3 * r + 2] * sT[8 + c];
+        Tn[4 * r + 3] = E[3 * r] * sT[3] + E[3 * r + 1] * sT[7] + E[3 * r + 2] * sT[11] + delta[3 + r];
+    }
+    for (int k = 0; k < 12; ++k) sT[k] = Tn[k];
+    iters = it + 1;
+    const double nw = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]);
+    const double nv = sqrt(delta[3] * delta[3] + delta[4] * delta[4] + delta[5] * delta[5]);
+    if (nw < a.eps_rot && nv < a.eps_trans) {
+        converged = 1;
+        status = GSICP_OK;
+        return 1;
+    }
+    if (iters >= a.max_iters) {
+        status = GSICP_WARN_MAX_ITERS;
+        return 1;
+    }
+    return 0;
+}
+
 __global__ void k_align_init(int32_t *corr_ws, int cap, unsigned int *barrier) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < cap) corr_ws[i] = -1;
@@ -323,12 +499,24 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     __shared__ double sAcc[kPad];
     __shared__ int sDone;
     __shared__ int sBox[6];
+    __shared__ CellIndex sIdx;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
     const int n = *a.d_n;
     if (tid < 12) sT[tid] = a.d_T[tid];
     if (a.timeline && blockIdx.x == 0 && tid == 0 && a.timeline_cap > 0) a.timeline[0] = globaltimer_ns();
     if (tid < 6) sBox[tid] = cell_coord(ordered_to_float_(a.tbbox[tid]), a.inv_h);
+    if (tid == 0) {
+        sIdx.table = a.table;
+        sIdx.mask = a.mask;
+        sIdx.level = 0;
+        sIdx.dense = a.dense;
+        sIdx.use_dense = a.dense != nullptr && a.dense_hdr[0] != 0;
+        for (int k = 0; k < 3; ++k) {
+            sIdx.lo[k] = a.dense_hdr ? a.dense_hdr[1 + k] : 0;
+            sIdx.dim[k] = a.dense_hdr ? a.dense_hdr[4 + k] : 0;
+        }
+    }
     if (tid == 0) sDone = 0;
     // resident point of this thread: source data, current match and own target cell in registers
     const int i0 = blockIdx.x * kT + tid;
@@ -359,26 +547,42 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             }
         };
         stamp(0);
-        double T[12];
-#pragma unroll
-        for (int k = 0; k < 12; ++k) T[k] = sT[k];
+        const double *T = sT;  // read from shared memory at each use (keeps registers for the search)
         // ------------------------------------------------------------ A6: correspondences
         double q0r = 0.0, q1r = 0.0, q2r = 0.0;
+        // diagnostic sub-phase clocks of warp 0 of block 0 (SM cycles)
+        const bool sub = a.timeline && blockIdx.x == 0 && tid == 0;
+        const long long sub_base = 1 + (long long)a.max_iters * (G + 9) + (long long)it * 8;
+        auto sub_stamp = [&](int k) {
+            if (sub && sub_base + k < a.timeline_cap) a.timeline[sub_base + k] = clock64();
+        };
         if (has0) {
+            sub_stamp(0);
             k3(T, x0.x, x0.y, x0.z, q0r, q1r, q2r);
             const float qx = __double2float_rn(q0r), qy = __double2float_rn(q1r), qz = __double2float_rn(q2r);
             const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
             if (qc.c[0] != own_c[0] || qc.c[1] != own_c[1] || qc.c[2] != own_c[2]) {
                 own_c[0] = qc.c[0]; own_c[1] = qc.c[1]; own_c[2] = qc.c[2];
-                own_se = cell_lookup(a.table, a.mask, cell_key(0, qc.c[0], qc.c[1], qc.c[2]));
+                own_se = sIdx.one(qc.c[0], qc.c[1], qc.c[2]);
             }
+            if (sub) own_se.x += 0 * (uint32_t)clock();  // keep ordering of the stamp below
+            sub_stamp(1);
             NN nn;
             if (m0.slot >= 0) {  // warm start from the previous match (record kept in registers)
                 nn.p = m0.p;
                 nn.slot = m0.slot;
                 nn.best = pack_ki(canon_key(qx, qy, qz, m0.p.x, m0.p.y, m0.p.z), (uint32_t)__float_as_int(m0.p.w));
             }
-            nn_search(a, sBox, qc, own_se, qx, qy, qz, nn);
+            sub_stamp(2);
+            uint2 own_left = own_se;
+            if (nn.slot < 0 && a.nbr) {  // no warm start: the own cell's best becomes the candidate
+                scan_target_cell(a, own_se, qx, qy, qz, nn);
+                own_left = make_uint2(0u, 0u);
+            }
+            if (!(nn.slot >= 0 && a.nbr && graph_nn(a, qx, qy, qz, nn)))
+                nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn);
+            if (sub) a.timeline[sub_base + 4] = nn.best == kEmptyKey ? 1 : 0;
+            sub_stamp(3);
             dbg_slow += nn.slow;
             dbg_probes += nn.probes;
             dbg_cands += nn.cands;
@@ -400,9 +604,10 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
                 nn.slot = slot;
                 nn.best = pack_ki(canon_key(qx, qy, qz, nn.p.x, nn.p.y, nn.p.z), (uint32_t)__float_as_int(nn.p.w));
             }
-            nn_search(a, sBox, qc, cell_lookup(a.table, a.mask, cell_key(0, qc.c[0], qc.c[1], qc.c[2])), qx, qy, qz, nn);
+            nn_search(a, sIdx, sBox, qc, sIdx.one(qc.c[0], qc.c[1], qc.c[2]), qx, qy, qz, nn);
             a.corr_ws[i] = (nn.slot >= 0 && ki_key(nn.best) < a.r2) ? nn.slot : -2 - nn.slot;
         }
+        sub_stamp(5);
         stamp(1);
         // ------------------------------------------------------------ A7: Eq. 1 terms
         double acc[kAlignTerms];
@@ -496,66 +701,13 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         stamp(4);
         // ------------------------------------------------------------ A8 solve / update / test
         if (tid == 0) {
-            double H[36], b[6];
-            int t = 0;
-            for (int r = 0; r < 6; ++r)
-                for (int c = r; c < 6; ++c) H[6 * r + c] = H[6 * c + r] = sAcc[t++];
-            for (int r = 0; r < 6; ++r) b[r] = sAcc[21 + r];
             n_in = sAcc[28];
             cost_last = sAcc[27];
-            int done = 0;
-            if (a.linearize_only) {
-                if (blockIdx.x == 0) {
-                    for (int k = 0; k < 36; ++k) a.d_lin[k] = H[k];
-                    for (int k = 0; k < 6; ++k) a.d_lin[36 + k] = b[k];
-                    a.d_lin[42] = cost_last;
-                    a.d_lin[43] = n_in;
-                }
-                status = GSICP_OK;
-                done = 1;
-            } else if (n == 0) {
-                status = GSICP_ERR_DEGENERATE_FRAME;
-                done = 1;
-            } else if (n_in < (double)a.min_pairs) {
-                status = GSICP_ERR_TRACKING_LOST;
-                done = 1;
-            } else {
-                double nb[6], delta[6];
-                for (int k = 0; k < 6; ++k) nb[k] = -b[k];
-                bool ok = chol6_solve(H, nb, delta);
-                if (!ok) {
-                    double tr = 0.0;
-                    for (int k = 0; k < 6; ++k) tr += H[7 * k];
-                    for (int k = 0; k < 6; ++k) H[7 * k] += 1e-6 * tr / 6.0;
-                    ok = chol6_solve(H, nb, delta);
-                }
-                if (!ok) {
-                    status = GSICP_ERR_TRACKING_LOST;
-                    done = 1;
-                } else {
-                    double E[9];
-                    so3_exp(delta, E);
-                    double Tn[12];
-                    for (int r = 0; r < 3; ++r) {
-                        for (int c = 0; c < 3; ++c)
-                            Tn[4 * r + c] = E[3 * r] * sT[c] + E[3 * r + 1] * sT[4 + c] + E[3 * r + 2] * sT[8 + c];
-                        Tn[4 * r + 3] = E[3 * r] * sT[3] + E[3 * r + 1] * sT[7] + E[3 * r + 2] * sT[11] + delta[3 + r];
-                    }
-                    for (int k = 0; k < 12; ++k) sT[k] = Tn[k];
-                    iters = it + 1;
-                    const double nw = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]);
-                    const double nv = sqrt(delta[3] * delta[3] + delta[4] * delta[4] + delta[5] * delta[5]);
-                    if (nw < a.eps_rot && nv < a.eps_trans) {
-                        converged = 1;
-                        status = GSICP_OK;
-                        done = 1;
-                    } else if (iters >= a.max_iters) {
-                        status = GSICP_WARN_MAX_ITERS;
-                        done = 1;
-                    }
-                }
-            }
-            sDone = done;
+            int st_ = status, it_ = iters, cv_ = converged;
+            sDone = solve_step(a, sAcc, sT, it, n, st_, it_, cv_);
+            status = st_;
+            iters = it_;
+            converged = cv_;
         }
         __syncthreads();
         stamp(5);
@@ -648,6 +800,10 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
     a.tcov_a = reinterpret_cast<const float4 *>(tgt.cov_a);
     a.tcov_b = reinterpret_cast<const float4 *>(tgt.cov_b);
     a.tbbox = tgt.bbox;
+    a.dense = static_cast<const uint2 *>(tgt.dense);
+    a.dense_hdr = tgt.dense_hdr;
+    a.nbr = tgt.nbr;
+    a.nbr_key = tgt.nbr_key;
     a.max_iters = p.max_iters;
     a.r = linearize_only ? r_lin : p.max_corr_dist;
     a.r2 = a.r * a.r;

@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_search(KnnArgs a) {
         // moments over the k nearest: lane j < k holds neighbour j (sorted by (key, index))
         const bool have = lane < a.k && T.L != kEmptyKey;
         if (a.knn_idx && lane < a.k) a.knn_idx[(size_t)i * a.k + lane] = have ? (int32_t)ki_idx(T.L) : -1;
+        if (!a.moments) continue;  // neighbour lists only (target kNN graph)
         double d[3] = {0, 0, 0};
         if (have) {
             const float4 p = __ldg(a.pos + ki_idx(T.L));
@@ -283,6 +284,26 @@ cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, in
     if (k <= 20) return launch_k<20>(a, cap, s);
     if (k <= 24) return launch_k<24>(a, cap, s);
     return launch_k<32>(a, cap, s);
+}
+
+// Exact kGraphK-NN lists (input indices, sorted by (key, index), self included) of the points of
+// an already built single-level grid — the target kNN graph behind the align kernel's certified
+// warm start.  No covariances.
+cudaError_t knn_graph_launch(const GridView &g, const float4 *pos, const int32_t *d_n, int cap, int32_t *knn_idx,
+                             cudaStream_t s) {
+    KnnArgs a{};
+    a.g = g;
+    a.pos = pos;
+    a.d_n = d_n;
+    a.k = kGraphK;
+    a.knn_idx = knn_idx;
+    a.moments = nullptr;
+    a.debug = nullptr;
+    const long long warps = (cap + kQueriesPerWarp - 1) / kQueriesPerWarp;
+    k_knn_search<kGraphK><<<blocks_for(warps * 32, kKnnThreads), kKnnThreads, 0, s>>>(a);
+    GSICP_LAUNCH_CHECK("k_knn_search(graph)");
+    note_launch();
+    return cudaSuccess;
 }
 
 }  // namespace gsicp

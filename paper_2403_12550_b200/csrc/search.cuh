@@ -81,44 +81,72 @@ __device__ __forceinline__ void axis_range(const QueryCell &qc, int a, float roo
 // 0, -1, 1, -2, 2, ...
 __device__ __forceinline__ int zigzag(int k) { return (k & 1) ? -((k + 1) >> 1) : (k >> 1); }
 
-// First-probe loads of kLookupBatch cells issued together (one warp-wide latency per batch),
-// then collisions resolved by linear probing.  Absent / invalid cells give count 0.
-__device__ __forceinline__ void lookup_batch(const CellEntry *__restrict__ table, uint32_t mask,
-                                             const unsigned long long (&keys)[kLookupBatch],
-                                             const bool (&valid)[kLookupBatch], uint2 (&se)[kLookupBatch]) {
-    uint4 e[kLookupBatch];
-    uint32_t s[kLookupBatch];
-#pragma unroll
-    for (int j = 0; j < kLookupBatch; ++j) {
-        s[j] = hash_slot(keys[j], mask);
-        e[j] = valid[j] ? __ldg(reinterpret_cast<const uint4 *>(table + s[j])) : make_uint4(0xffffffffu, 0xffffffffu, 0, 0);
+
+// Cell index of a grid: the open-addressing hash table always, plus (targets only) a dense
+// (start, count) array over the bbox when it fits its budget — then a lookup is one load with
+// no hashing or probing, and neighbouring cells along x are adjacent in memory.
+struct CellIndex {
+    const CellEntry *table;
+    uint32_t mask;
+    int level;
+    const uint2 *dense;  // nullable
+    int lo[3], dim[3];
+    bool use_dense;
+
+    __device__ __forceinline__ uint2 one(int x, int y, int z) const {
+        if (use_dense) {
+            const int ix = x - lo[0], iy = y - lo[1], iz = z - lo[2];
+            if ((unsigned)ix >= (unsigned)dim[0] || (unsigned)iy >= (unsigned)dim[1] || (unsigned)iz >= (unsigned)dim[2])
+                return make_uint2(0u, 0u);
+            return __ldg(dense + ((size_t)iz * dim[1] + iy) * dim[0] + ix);
+        }
+        return cell_lookup(table, mask, cell_key(level, x, y, z));
     }
+
+    // B lookups with all first loads in flight together; invalid entries give (0, 0)
+    template <int B>
+    __device__ __forceinline__ void batch(const int (&xs)[B], const int (&ys)[B], const int (&zs)[B],
+                                          const bool (&valid)[B], uint2 (&se)[B]) const {
+        if (use_dense) {
 #pragma unroll
-    for (int j = 0; j < kLookupBatch; ++j) {
-        se[j] = make_uint2(0u, 0u);
-        if (!valid[j]) continue;
-        while (true) {
-            const unsigned long long k = ((unsigned long long)e[j].y << 32) | e[j].x;
-            if (k == keys[j]) {
-                se[j] = make_uint2(e[j].z, e[j].w);
-                break;
+            for (int j = 0; j < B; ++j) se[j] = valid[j] ? one(xs[j], ys[j], zs[j]) : make_uint2(0u, 0u);
+            return;
+        }
+        unsigned long long keys[B];
+        uint4 e[B];
+        uint32_t s[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            keys[j] = cell_key(level, xs[j], ys[j], zs[j]);
+            s[j] = hash_slot(keys[j], mask);
+            e[j] = valid[j] ? __ldg(reinterpret_cast<const uint4 *>(table + s[j])) : make_uint4(0xffffffffu, 0xffffffffu, 0, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            se[j] = make_uint2(0u, 0u);
+            if (!valid[j]) continue;
+            while (true) {
+                const unsigned long long k = ((unsigned long long)e[j].y << 32) | e[j].x;
+                if (k == keys[j]) {
+                    se[j] = make_uint2(e[j].z, e[j].w);
+                    break;
+                }
+                if (k == kEmptyKey) break;
+                s[j] = (s[j] + 1) & mask;
+                e[j] = __ldg(reinterpret_cast<const uint4 *>(table + s[j]));
             }
-            if (k == kEmptyKey) break;
-            s[j] = (s[j] + 1) & mask;
-            e[j] = __ldg(reinterpret_cast<const uint4 *>(table + s[j]));
         }
     }
-}
+};
 
 // Ball traversal over the cells not yet scanned (skip(dx, dy, dz) is true for those already done).
 // Rows (fixed y, z) are pruned by their gap; inside a row the x-extent is computed from the gaps
 // alone (no loads), then cells are looked up kLookupBatch at a time, nearest first, and a cell is
 // scanned only if its lower bound is still <= bound() (which may shrink while scanning).
-//   key_of(x, y, z) -> u64 cell key;  scan(uint2 start_count);  bound() -> float
-template <class KeyOf, class Skip, class Scan, class Bound>
-__device__ __forceinline__ void ball_search(const QueryCell &qc, const CellEntry *__restrict__ table, uint32_t mask,
-                                            const int *blo, const int *bhi, Skip skip, KeyOf key_of, Scan scan,
-                                            Bound bound) {
+//   scan(uint2 start_count);  bound() -> float
+template <class Skip, class Scan, class Bound>
+__device__ __forceinline__ void ball_search(const QueryCell &qc, const CellIndex &idx, const int *blo, const int *bhi,
+                                            Skip skip, Scan scan, Bound bound) {
     int zlo, zhi;
     axis_range(qc, 2, bound(), blo[2], bhi[2], zlo, zhi);
     for (int kz = 0; kz <= 2 * max(-zlo, zhi); ++kz) {
@@ -137,7 +165,7 @@ __device__ __forceinline__ void ball_search(const QueryCell &qc, const CellEntry
             axis_range(qc, 0, bound() - gzy, blo[0], bhi[0], xlo, xhi);
             const int kxmax = 2 * max(-xlo, xhi);
             for (int kx0 = 0; kx0 <= kxmax; kx0 += kLookupBatch) {
-                unsigned long long keys[kLookupBatch];
+                int xs[kLookupBatch], ys[kLookupBatch], zs[kLookupBatch];
                 bool valid[kLookupBatch];
                 float lb[kLookupBatch];
 #pragma unroll
@@ -145,10 +173,12 @@ __device__ __forceinline__ void ball_search(const QueryCell &qc, const CellEntry
                     const int dx = zigzag(kx0 + j);
                     valid[j] = kx0 + j <= kxmax && dx >= xlo && dx <= xhi && !skip(dx, dy, dz);
                     lb[j] = gzy + qc.gap2(dx, 0);
-                    keys[j] = key_of(qc.c[0] + dx, qc.c[1] + dy, qc.c[2] + dz);
+                    xs[j] = qc.c[0] + dx;
+                    ys[j] = qc.c[1] + dy;
+                    zs[j] = qc.c[2] + dz;
                 }
                 uint2 se[kLookupBatch];
-                lookup_batch(table, mask, keys, valid, se);
+                idx.batch(xs, ys, zs, valid, se);
 #pragma unroll
                 for (int j = 0; j < kLookupBatch; ++j)
                     if (se[j].y && lb[j] <= bound()) scan(se[j]);

@@ -73,7 +73,17 @@ struct TargetWs {
     int32_t *d_M;
     double *smid_sum;
     void *grid;
+    uint2 *dense;
+    int32_t *dense_hdr;
+    long long dense_budget;
+    int32_t *knn_idx;  // [M][kGraphK] input indices (graph build scratch)
+    int32_t *inv;      // [M] cell-ordered slot of each input index
+    int32_t *nbr;      // [M][kGraphK] neighbour slots of each slot (self first)
+    float *nbr_key;    // [M] canonical key of the kGraphK-th neighbour (INFINITY if fewer points)
 };
+
+// dense (start, count) cell array budget: 8 cells per Gaussian (>= 1M cells), 8 bytes each
+static long long dense_budget(int M) { return M * 8LL > (1LL << 20) ? M * 8LL : (1LL << 20); }
 
 static TargetWs target_carve(Carver &c, int M) {
     TargetWs t;
@@ -83,6 +93,13 @@ static TargetWs target_carve(Carver &c, int M) {
     t.d_M = c.take<int32_t>(4);
     t.smid_sum = c.take<double>(4);
     t.grid = c.take<char>(grid_bytes(M, 1, true));
+    t.dense_budget = dense_budget(M);
+    t.dense = c.take<uint2>((size_t)t.dense_budget);
+    t.dense_hdr = c.take<int32_t>(8);
+    t.knn_idx = c.take<int32_t>((size_t)M * kGraphK);
+    t.inv = c.take<int32_t>(M);
+    t.nbr = c.take<int32_t>((size_t)M * kGraphK);
+    t.nbr_key = c.take<float>(M);
     return t;
 }
 
@@ -92,12 +109,112 @@ size_t target_ws_bytes(int M) {
     return c.bytes();
 }
 
-static void fill_target(const GridView &g, int M, gsicp_target *out) {
+namespace {
+
+// header {in_use, lo xyz, dims xyz}: the bbox's cells (same cell_coord as the hash) if they fit
+__global__ void k_dense_setup(const int32_t *bbox, float inv_h, long long budget, int32_t *hdr) {
+    int lo[3], dim[3];
+    long long total = 1;
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = cell_coord(ordered_to_float(bbox[k]), inv_h);
+        const int hi = cell_coord(ordered_to_float(bbox[3 + k]), inv_h);
+        dim[k] = hi - lo[k] + 1;
+        total *= (long long)(dim[k] > 0 ? dim[k] : 0);
+    }
+    hdr[0] = (total > 0 && total <= budget) ? 1 : 0;
+    for (int k = 0; k < 3; ++k) {
+        hdr[1 + k] = lo[k];
+        hdr[4 + k] = dim[k];
+    }
+}
+
+__global__ void k_dense_clear(uint2 *dense, long long budget, const int32_t *hdr) {
+    if (!hdr[0]) return;
+    const long long total = (long long)hdr[4] * hdr[5] * hdr[6];
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x)
+        dense[i] = make_uint2(0u, 0u);
+}
+
+__global__ void k_dense_fill(const CellEntry *table, uint32_t slots, uint2 *dense, const int32_t *hdr) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (!hdr[0] || s >= slots) return;
+    const CellEntry e = table[s];
+    if (e.key == kEmptyKey) return;
+    const int x = (int)((e.key >> 40) & 0xFFFFFull) - kCoordOff;
+    const int y = (int)((e.key >> 20) & 0xFFFFFull) - kCoordOff;
+    const int z = (int)(e.key & 0xFFFFFull) - kCoordOff;
+    const long long ix = x - hdr[1], iy = y - hdr[2], iz = z - hdr[3];
+    dense[(iz * hdr[5] + iy) * hdr[4] + ix] = make_uint2(e.start, e.count);
+}
+
+__global__ void k_graph_inv(const float4 *spos, const int32_t *d_n, int32_t *inv) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < *d_n) inv[__float_as_int(spos[s].w)] = s;
+}
+
+__global__ void k_graph_finalize(const float4 *spos, const int32_t *d_n, const int32_t *knn_idx, const int32_t *inv,
+                                 int32_t *nbr, float *nbr_key) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= *d_n) return;
+    const float4 p = spos[s];
+    const int orig = __float_as_int(p.w);
+    int last = -1;
+    for (int j = 0; j < kGraphK; ++j) {
+        const int o = knn_idx[(size_t)orig * kGraphK + j];
+        const int sl = o >= 0 ? inv[o] : -1;
+        nbr[(size_t)s * kGraphK + j] = sl;
+        last = sl;
+    }
+    if (last >= 0) {
+        const float4 q = spos[last];
+        nbr_key[s] = canon_key(p.x, p.y, p.z, q.x, q.y, q.z);
+    } else {
+        nbr_key[s] = INFINITY;  // the list holds the whole cloud
+    }
+}
+
+}  // namespace
+
+cudaError_t knn_graph_launch(const GridView &g, const float4 *pos, const int32_t *d_n, int cap, int32_t *knn_idx,
+                             cudaStream_t s);
+
+// Target kNN graph: for every target point (slot) its kGraphK nearest targets (slots, exact,
+// self included) and the key of the farthest.  The align kernel uses it as a certificate: if
+// 4 key(q, m_j) < key_K(j) (with rounding slack), every target at least as close to q as m_j
+// lies in j's list, so the exact 1-NN of q is the best of that list.
+static cudaError_t build_graph(const GridView &g, const TargetWs &t, const float4 *pos, const int32_t *d_n, int M,
+                               cudaStream_t s) {
+    cudaError_t e = knn_graph_launch(g, pos, d_n, M, t.knn_idx, s);
+    if (e != cudaSuccess) return e;
+    k_graph_inv<<<blocks_for(M, 256), 256, 0, s>>>(g.spos, d_n, t.inv);
+    GSICP_LAUNCH_CHECK("k_graph_inv");
+    k_graph_finalize<<<blocks_for(M, 256), 256, 0, s>>>(g.spos, d_n, t.knn_idx, t.inv, t.nbr, t.nbr_key);
+    GSICP_LAUNCH_CHECK("k_graph_finalize");
+    note_launch(2);
+    return cudaSuccess;
+}
+
+static cudaError_t build_dense(const GridView &g, const TargetWs &t, cudaStream_t s) {
+    k_dense_setup<<<1, 1, 0, s>>>(g.bbox, g.inv_h0, t.dense_budget, t.dense_hdr);
+    GSICP_LAUNCH_CHECK("k_dense_setup");
+    k_dense_clear<<<num_sms() * 8, 256, 0, s>>>(t.dense, t.dense_budget, t.dense_hdr);
+    GSICP_LAUNCH_CHECK("k_dense_clear");
+    k_dense_fill<<<blocks_for((long long)g.mask + 1, 256), 256, 0, s>>>(g.table, g.mask + 1, t.dense, t.dense_hdr);
+    GSICP_LAUNCH_CHECK("k_dense_fill");
+    note_launch(3);
+    return cudaSuccess;
+}
+
+static void fill_target(const GridView &g, const TargetWs &t, int M, gsicp_target *out) {
     out->pos = reinterpret_cast<const float *>(g.spos);
     out->cov_a = reinterpret_cast<const float *>(g.scov_a);
     out->cov_b = reinterpret_cast<const float *>(g.scov_b);
     out->table = g.table;
     out->bbox = g.bbox;
+    out->dense = t.dense;
+    out->dense_hdr = t.dense_hdr;
+    out->nbr = t.nbr;
+    out->nbr_key = t.nbr_key;
     out->table_mask = g.mask;
     out->cell = g.h0;
     out->M = M;
@@ -135,8 +252,10 @@ cudaError_t build_target_launch(const float *means, const float *quats, const fl
     }
     GridView g = grid_carve(t.grid, M, 1, true, cell);
     cudaError_t e = grid_build(g, t.pos, t.cov_a, t.cov_b, t.d_M, M, s);
+    if (e == cudaSuccess) e = build_dense(g, t, s);
+    if (e == cudaSuccess) e = build_graph(g, t, t.pos, t.d_M, M, s);
     if (e != cudaSuccess) return e;
-    fill_target(g, M, out);
+    fill_target(g, t, M, out);
     return cudaSuccess;
 }
 
@@ -147,8 +266,10 @@ cudaError_t build_target_cloud_launch(const gsicp_cloud &cl, int M, float cell, 
     GridView g = grid_carve(t.grid, M, 1, true, cell);
     cudaError_t e = grid_build(g, reinterpret_cast<const float4 *>(cl.pos), reinterpret_cast<const float4 *>(cl.cov_a),
                                reinterpret_cast<const float4 *>(cl.cov_b), cl.d_n, M, s);
+    if (e == cudaSuccess) e = build_dense(g, t, s);
+    if (e == cudaSuccess) e = build_graph(g, t, reinterpret_cast<const float4 *>(cl.pos), cl.d_n, M, s);
     if (e != cudaSuccess) return e;
-    fill_target(g, M, out);
+    fill_target(g, t, M, out);
     return cudaSuccess;
 }
 

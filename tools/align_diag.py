@@ -69,6 +69,10 @@ def main():
             phs = " ".join(f"{nm}={(ph[j + 1] - ph[j]) / 1000.0:.1f}" for j, nm in enumerate(names))
             print(f"  it {it}: arrivals min {a.min():7.1f} p50 {np.median(a):7.1f} max {a.max():7.1f} us; "
                   f"release {(pas - prev) / 1000.0:7.1f} us | block0 phases(us) {phs}")
+            sb = 1 + max_iters * (Gn + 9) + it * 8
+            c = t[sb:sb + 6]
+            print(f"      warp0 cycles: k3+own={c[1] - c[0]} warm={c[2] - c[1]} search={c[3] - c[2]} "
+                  f"rest={c[5] - c[3]} empty_best={c[4]}")
             prev = pas
 
 

@@ -363,13 +363,13 @@ class Tracker:
 
     def __init__(self, H: int, W: int, K, stride: int = 4, k: int = 20, mode: int = REG_ELLIPSE,
                  eps_var: float = 1e-3, z_min: float = 0.1, z_max: float = 10.0, cell0: float | None = None,
-                 levels: int = 5, params: AlignParams | None = None, device="cuda"):
+                 levels: int = 4, params: AlignParams | None = None, device="cuda"):
         self.H, self.W, self.stride, self.k, self.mode, self.eps = H, W, stride, k, mode, eps_var
         self.K = K if isinstance(K, Intrinsics) else Intrinsics(*K)
         self.z_min, self.z_max = z_min, z_max
         self.cap = ((H + stride - 1) // stride) * ((W + stride - 1) // stride)
-        # finest cell ~ 2.5 x the pixel footprint at z_min-ish depth (performance knob only)
-        self.cell0 = cell0 if cell0 is not None else max(2.5 * stride * 0.5 / self.K.fx, 1e-3)
+        # finest cell ~ 3 x the point spacing at 1 m depth (performance knob only: results are exact)
+        self.cell0 = cell0 if cell0 is not None else max(3.0 * stride / self.K.fx, 1e-3)
         self.levels = levels
         self.params = params or align_params()
         self.device = torch.device(device)

@@ -31,20 +31,30 @@ __global__ void k_grid_insert(GridView g, const float4 *__restrict__ pos, const 
     const int i = (int)(t - (long long)level * g.cap);
     const bool active = level < g.levels && i < n;
     float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    unsigned long long key = kEmptyKey;
     if (active) {
         p = __ldg(pos + i);
         const float inv_h = ldexpf(g.inv_h0, -level);
-        const unsigned long long key =
-            cell_key(level, cell_coord(p.x, inv_h), cell_coord(p.y, inv_h), cell_coord(p.z, inv_h));
-        uint32_t s = hash_slot(key, g.mask);
+        key = cell_key(level, cell_coord(p.x, inv_h), cell_coord(p.y, inv_h), cell_coord(p.z, inv_h));
+    }
+    // warp aggregation: lanes of the same cell (spatially coherent inputs share cells, most of all
+    // on coarse levels) insert once and take their ranks with a single atomicAdd of the leader
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    uint32_t s = 0, base = 0;
+    if (active && lane == leader) {
+        s = hash_slot(key, g.mask);
         while (true) {
             const unsigned long long prev = atomicCAS(&g.table[s].key, kEmptyKey, key);
             if (prev == kEmptyKey || prev == key) break;
             s = (s + 1) & g.mask;
         }
-        const uint32_t rank = atomicAdd(&g.table[s].count, 1u);
-        g.slot_rank[t] = make_uint2(s, rank);
+        base = atomicAdd(&g.table[s].count, (uint32_t)__popc(peers));
     }
+    s = __shfl_sync(0xffffffffu, s, leader);
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (active) g.slot_rank[t] = make_uint2(s, base + __popc(peers & ((1u << lane) - 1u)));
     // bbox of the points (level 0 lanes only), warp-reduced then one atomic per warp
     const bool bb = active && level == 0;
     float v[6] = {bb ? p.x : INFINITY, bb ? p.y : INFINITY, bb ? p.z : INFINITY,
@@ -65,33 +75,52 @@ __global__ void k_grid_insert(GridView g, const float4 *__restrict__ pos, const 
 }
 
 // Each level's points get the contiguous range [level*cap, level*cap + n) of spos, cells in
-// allocation order; a warp reserves its cells of one level with one atomicAdd.
-__global__ void k_grid_alloc(GridView g) {
-    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+// allocation order.  Reservations are aggregated per warp (shuffle scan) and per block (shared
+// atomics), so a block issues one global atomicAdd per level for kAllocPerThread*256 slots.
+constexpr int kAllocThreads = 256;
+constexpr int kAllocPerThread = 4;
+
+__global__ void __launch_bounds__(kAllocThreads) k_grid_alloc(GridView g) {
+    __shared__ uint32_t s_tot[kMaxLevels], s_base[kMaxLevels];
     const int lane = threadIdx.x & 31;
-    unsigned long long key = kEmptyKey;
-    uint32_t cnt = 0;
-    if (s <= g.mask) {
-        key = g.table[s].key;
-        if (key != kEmptyKey) cnt = g.table[s].count;
-    }
-    const int level = key != kEmptyKey ? (int)(key >> 60) : -1;
-    for (int l = 0; l < g.levels; ++l) {
-        const bool mine = level == l;
-        if (!__any_sync(0xffffffffu, mine)) continue;
-        const uint32_t c = mine ? cnt : 0u;
-        uint32_t incl = c;
+    if (threadIdx.x < kMaxLevels) s_tot[threadIdx.x] = 0;
+    __syncthreads();
+    uint32_t slot[kAllocPerThread], cnt[kAllocPerThread], off[kAllocPerThread];
+    int lev[kAllocPerThread];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+    for (int r = 0; r < kAllocPerThread; ++r) {
+        slot[r] = (blockIdx.x * kAllocPerThread + r) * kAllocThreads + threadIdx.x;
+        unsigned long long key = kEmptyKey;
+        cnt[r] = 0;
+        if (slot[r] <= g.mask) {
+            key = g.table[slot[r]].key;
+            if (key != kEmptyKey) cnt[r] = g.table[slot[r]].count;
         }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        uint32_t base = 0;
-        if (lane == 31) base = atomicAdd(g.counters + l, total);
-        base = __shfl_sync(0xffffffffu, base, 31);
-        if (mine) g.table[s].start = (uint32_t)l * (uint32_t)g.cap + base + incl - c;
+        lev[r] = key != kEmptyKey ? (int)(key >> 60) : -1;
+        off[r] = 0;
+        for (int l = 0; l < g.levels; ++l) {
+            const bool mine = lev[r] == l;
+            if (!__any_sync(0xffffffffu, mine)) continue;
+            const uint32_t c = mine ? cnt[r] : 0u;
+            uint32_t incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            uint32_t wbase = 0;
+            if (lane == 31) wbase = atomicAdd(s_tot + l, total);
+            wbase = __shfl_sync(0xffffffffu, wbase, 31);
+            if (mine) off[r] = wbase + incl - c;
+        }
     }
+    __syncthreads();
+    if (threadIdx.x < g.levels) s_base[threadIdx.x] = s_tot[threadIdx.x] ? atomicAdd(g.counters + threadIdx.x, s_tot[threadIdx.x]) : 0u;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kAllocPerThread; ++r)
+        if (lev[r] >= 0) g.table[slot[r]].start = (uint32_t)lev[r] * (uint32_t)g.cap + s_base[lev[r]] + off[r];
 }
 
 template <bool WITH_COV>
@@ -159,7 +188,7 @@ cudaError_t grid_build(const GridView &g, const float4 *pos, const float4 *cov_a
     GSICP_LAUNCH_CHECK("k_grid_init");
     k_grid_insert<<<blocks_for(work, T), T, 0, s>>>(g, pos, d_n);
     GSICP_LAUNCH_CHECK("k_grid_insert");
-    k_grid_alloc<<<blocks_for(slots, T), T, 0, s>>>(g);
+    k_grid_alloc<<<blocks_for(slots, kAllocThreads * kAllocPerThread), kAllocThreads, 0, s>>>(g);
     GSICP_LAUNCH_CHECK("k_grid_alloc");
     if (g.scov_a)
         k_grid_scatter<true><<<blocks_for(work, T), T, 0, s>>>(g, pos, cov_a, cov_b, d_n);

@@ -29,6 +29,7 @@ namespace {
 constexpr int kMinCell = 3;
 constexpr int kKnnThreads = 128;
 constexpr int kQueriesPerWarp = 8;  // queries a warp searches one after the other
+constexpr int kMergeThreshold = 4;  // more passing candidates than this: sort-merge the batch
 constexpr unsigned kFull = 0xffffffffu;
 
 struct KnnArgs {
@@ -48,6 +49,10 @@ __device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int
     return ((unsigned long long)__shfl_sync(kFull, (unsigned)(v >> 32), src) << 32) |
            __shfl_sync(kFull, (unsigned)v, src);
 }
+__device__ __forceinline__ unsigned long long shfl_xor_u64(unsigned long long v, int m) {
+    return ((unsigned long long)__shfl_xor_sync(kFull, (unsigned)(v >> 32), m) << 32) |
+           __shfl_xor_sync(kFull, (unsigned)v, m);
+}
 __device__ __forceinline__ unsigned long long shfl_up_u64(unsigned long long v, int d) {
     return ((unsigned long long)__shfl_up_sync(kFull, (unsigned)(v >> 32), d) << 32) |
            __shfl_up_sync(kFull, (unsigned)v, d);
@@ -65,9 +70,33 @@ struct WarpTopK {
         worst = kEmptyKey;
     }
     __device__ __forceinline__ bool full() const { return worst != kEmptyKey; }
-    // insert the candidates of all lanes (cand = kEmptyKey for none)
+    // insert the candidates of all lanes (cand = kEmptyKey for none): a few by ballot + shuffle,
+    // many by a warp bitonic sort of the batch merged into the list (fixed ~40 shuffles)
     __device__ __forceinline__ void insert_all(unsigned long long cand, int lane) {
         unsigned pass = __ballot_sync(kFull, cand < worst);
+        if (__popc(pass) > kMergeThreshold) {
+            inserts += __popc(pass);
+            unsigned long long c = cand < worst ? cand : kEmptyKey;
+#pragma unroll
+            for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    const unsigned long long o = shfl_xor_u64(c, j);
+                    const bool up = ((lane & k) == 0) == ((lane & j) == 0);  // keep the min here?
+                    c = up ? (o < c ? o : c) : (o > c ? o : c);
+                }
+            // list ascending (lanes >= K empty) vs batch descending: lane-wise min = the 32 smallest
+            const unsigned long long rev = shfl_u64(c, 31 - lane);
+            unsigned long long m = L < rev ? L : rev;
+#pragma unroll
+            for (int j = 16; j > 0; j >>= 1) {  // bitonic merge to ascending
+                const unsigned long long o = shfl_xor_u64(m, j);
+                m = ((lane & j) == 0) ? (o < m ? o : m) : (o > m ? o : m);
+            }
+            L = lane < K ? m : kEmptyKey;
+            worst = shfl_u64(L, K - 1);
+            return;
+        }
         while (pass) {
             const int src = __ffs(pass) - 1;
             pass &= pass - 1;

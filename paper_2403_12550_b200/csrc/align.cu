@@ -122,37 +122,48 @@ __device__ __forceinline__ float nn_bound(const AlignArgs &a, const NN &nn) {
 // it satisfies |m_j - m_k| <= 2 |q - m_j| (triangle inequality), so if 4 k_j < key_K(j) (with
 // slack for binary32 rounding of both keys) all of them are in j's exact K-NN list and the 1-NN
 // of q is the best of that list (self included).  Returns false (nn untouched) otherwise.
+// Greedy descent on the graph until a certified step: each step scans the list of the current
+// candidate j (which can only improve nn); if j was certified the result is exact.  If the list
+// holds nothing better and j is not certified, or after kGraphSteps steps, returns false (nn
+// holds the best point seen, a valid upper bound for the grid search).
+constexpr int kGraphSteps = 4;
+
 __device__ __forceinline__ bool graph_nn(const AlignArgs &a, float qx, float qy, float qz, NN &nn) {
-    const int j = nn.slot;
-    const float kj = ki_key(nn.best);
-    const float kk = __ldg(a.nbr_key + j);
-    if (!(4.f * kj * (1.f + 4e-5f) < kk * (1.f - 4e-5f))) return false;
-    const int4 *lst = reinterpret_cast<const int4 *>(a.nbr + (size_t)j * kGraphK);
-    int sl[kGraphK];
+    for (int step = 0; step < kGraphSteps; ++step) {
+        const int j = nn.slot;
+        const float kj = ki_key(nn.best);
+        const int4 *lst = reinterpret_cast<const int4 *>(a.nbr + (size_t)j * kGraphK);
+        const float kk = __ldg(a.nbr_key + j);
+        int sl[kGraphK];
 #pragma unroll
-    for (int v = 0; v < kGraphK / 4; ++v) {
-        const int4 w = __ldg(lst + v);
-        sl[4 * v] = w.x; sl[4 * v + 1] = w.y; sl[4 * v + 2] = w.z; sl[4 * v + 3] = w.w;
-    }
-    float4 p[kGraphK];
-#pragma unroll
-    for (int u = 0; u < kGraphK; ++u) p[u] = sl[u] >= 0 ? __ldg(a.tpos + sl[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
-    ++nn.probes;
-    nn.cands += kGraphK;
-#pragma unroll
-    for (int u = 0; u < kGraphK; ++u) {
-        if (sl[u] < 0) continue;
-        const unsigned long long v = pack_ki(canon_key(qx, qy, qz, p[u].x, p[u].y, p[u].z), (uint32_t)__float_as_int(p[u].w));
-        if (v < nn.best) {
-            nn.best = v;
-            nn.slot = sl[u];
-            nn.p = p[u];
+        for (int v = 0; v < kGraphK / 4; ++v) {
+            const int4 w = __ldg(lst + v);
+            sl[4 * v] = w.x; sl[4 * v + 1] = w.y; sl[4 * v + 2] = w.z; sl[4 * v + 3] = w.w;
         }
+        const bool certified = 4.f * kj * (1.f + 4e-5f) < kk * (1.f - 4e-5f);
+        float4 p[kGraphK];
+#pragma unroll
+        for (int u = 0; u < kGraphK; ++u) p[u] = sl[u] >= 0 ? __ldg(a.tpos + sl[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        ++nn.probes;
+        nn.cands += kGraphK;
+#pragma unroll
+        for (int u = 0; u < kGraphK; ++u) {
+            if (sl[u] < 0) continue;
+            const unsigned long long v =
+                pack_ki(canon_key(qx, qy, qz, p[u].x, p[u].y, p[u].z), (uint32_t)__float_as_int(p[u].w));
+            if (v < nn.best) {
+                nn.best = v;
+                nn.slot = sl[u];
+                nn.p = p[u];
+            }
+        }
+        if (certified) return true;
+        if (nn.slot == j) return false;  // local minimum without a certificate
     }
-    return true;
+    return false;
 }
 
-constexpr int kMaxCells = 8;   // cells gathered for one flattened candidate scan (own + 7 neighbours)
+constexpr int kMaxCells = 4;   // cells gathered for one flattened candidate scan (own + 3 neighbours)
 constexpr int kFlatBatch = 8;  // candidate records loaded per round trip in the flattened scan
 
 // Candidates of up to kMaxCells cells scanned as one flattened range, kFlatBatch records per
@@ -233,8 +244,11 @@ __device__ __forceinline__ void nn_slow(const AlignArgs &a, const CellIndex &idx
 // Fast path: when the ball of the current bound cannot reach offset +-2 on any axis, only the 26
 // neighbours can qualify; they are tested by their gaps alone — and none at all when the ball
 // stays inside the own cell (the common, warm-started case).
-__device__ __forceinline__ void nn_search(const AlignArgs &a, const CellIndex &idx, const int *sb,
-                                          const QueryCell &qc, uint2 own, float qx, float qy, float qz, NN &nn) {
+// Returns true when nn is the exact answer; false (only with defer) when the general search is
+// still needed — nn then holds the best point seen.
+__device__ __forceinline__ bool nn_search(const AlignArgs &a, const CellIndex &idx, const int *sb,
+                                          const QueryCell &qc, uint2 own, float qx, float qy, float qz, NN &nn,
+                                          bool defer) {
     float glo[3], ghi[3], glo2[3], ghi2[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -254,12 +268,12 @@ __device__ __forceinline__ void nn_search(const AlignArgs &a, const CellIndex &i
         own_pending = false;
         b = nn_bound(a, nn);
         if (!fits(b)) {
-            // the general search gets a copy: taking nn's address would pin it to local memory
-            NN tmp = nn;
-            ++tmp.slow;
+            ++nn.slow;
+            if (defer) return false;  // the block's warps run it cooperatively (warp_nn)
+            NN tmp = nn;  // a copy: taking nn's address would pin it to local memory
             nn_slow(a, idx, sb, qx, qy, qz, tmp);
             nn = tmp;
-            return;
+            return true;
         }
     }
     const int *blo = sb, *bhi = sb + 3;
@@ -305,6 +319,86 @@ __device__ __forceinline__ void nn_search(const AlignArgs &a, const CellIndex &i
         se[0] = own_pending ? own : make_uint2(0u, 0u);
         own_pending = false;
         scan_cells_flat(a, se, lbs, qx, qy, qz, nn);
+    }
+    return true;
+}
+
+__device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int src) {
+    return ((unsigned long long)__shfl_sync(0xffffffffu, (unsigned)(v >> 32), src) << 32) |
+           __shfl_sync(0xffffffffu, (unsigned)v, src);
+}
+
+// Warp-cooperative exact 1-NN for one query (all lanes call it with the same arguments; nn is
+// uniform on entry and exit): the cells of the offset box whose gaps fit the bound are probed 32
+// at a time (lane = cell), their points scanned as one flattened range (lane = candidate), and
+// the batch minimum is taken by shuffles; the bound shrinks as it goes.  Used for the queries
+// whose per-thread fast path failed, so a few hard queries no longer serialise a whole warp.
+__device__ void warp_nn(const AlignArgs &a, const CellIndex &idx, const int *sb, float qx, float qy, float qz, NN &nn,
+                        int lane) {
+    const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
+    const int *blo = sb, *bhi = sb + 3;
+    const float b0 = nn_bound(a, nn);
+    int lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) axis_range(qc, k, b0, blo[k], bhi[k], lo[k], hi[k]);
+    const int nx = max(hi[0] - lo[0] + 1, 0), ny = max(hi[1] - lo[1] + 1, 0), nz = max(hi[2] - lo[2] + 1, 0);
+    const long long total = (long long)nx * ny * nz;
+    for (long long t0 = 0; t0 < total; t0 += 32) {
+        const float b = nn_bound(a, nn);
+        const long long t = t0 + lane;
+        int dx = 0, dy = 0, dz = 0;
+        bool valid = t < total;
+        if (valid) {
+            dx = lo[0] + (int)(t % nx);
+            dy = lo[1] + (int)((t / nx) % ny);
+            dz = lo[2] + (int)(t / ((long long)nx * ny));
+            valid = qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2) <= b;
+        }
+        const uint2 se = valid ? idx.one(qc.c[0] + dx, qc.c[1] + dy, qc.c[2] + dz) : make_uint2(0u, 0u);
+        uint32_t incl = se.y;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t ctot = __shfl_sync(0xffffffffu, incl, 31);
+        nn.probes += __popc(__ballot_sync(0xffffffffu, se.y != 0));
+        nn.cands += (int)ctot;
+        for (uint32_t base = 0; base < ctot; base += 32) {
+            const uint32_t item = base + lane;
+            int l0 = 0, l1 = 31;
+#pragma unroll
+            for (int s = 0; s < 5; ++s) {
+                const int mid = (l0 + l1) >> 1;
+                if (__shfl_sync(0xffffffffu, incl, mid) > item) l1 = mid; else l0 = mid + 1;
+            }
+            const uint32_t c_incl = __shfl_sync(0xffffffffu, incl, l0);
+            const uint32_t c_start = __shfl_sync(0xffffffffu, se.x, l0);
+            const uint32_t c_cnt = __shfl_sync(0xffffffffu, se.y, l0);
+            unsigned long long cand = kEmptyKey;
+            float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+            uint32_t slot = 0;
+            if (item < ctot) {
+                slot = c_start + (item - (c_incl - c_cnt));
+                p = __ldg(a.tpos + slot);
+                cand = pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
+            }
+            unsigned long long m = cand;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long v = shfl_u64(m, lane ^ o);
+                m = v < m ? v : m;
+            }
+            if (m < nn.best) {
+                const int src = __ffs(__ballot_sync(0xffffffffu, cand == m)) - 1;
+                nn.best = m;
+                nn.slot = (int)__shfl_sync(0xffffffffu, slot, src);
+                nn.p.x = __shfl_sync(0xffffffffu, p.x, src);
+                nn.p.y = __shfl_sync(0xffffffffu, p.y, src);
+                nn.p.z = __shfl_sync(0xffffffffu, p.z, src);
+                nn.p.w = __shfl_sync(0xffffffffu, p.w, src);
+            }
+        }
     }
 }
 
@@ -500,6 +594,13 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     __shared__ int sDone;
     __shared__ int sBox[6];
     __shared__ CellIndex sIdx;
+    // per-block queue of queries needing the general search (handled by whole warps)
+    __shared__ int sQn;
+    __shared__ int sQtid[kT];
+    __shared__ float4 sQq[kT];
+    __shared__ unsigned long long sQbest[kT];
+    __shared__ int sQslot[kT];
+    __shared__ float4 sQp[kT];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
     const int n = *a.d_n;
@@ -518,6 +619,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         }
     }
     if (tid == 0) sDone = 0;
+    if (tid == 0) sQn = 0;
     // resident point of this thread: source data, current match and own target cell in registers
     const int i0 = blockIdx.x * kT + tid;
     const bool has0 = i0 < n;
@@ -578,18 +680,69 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             if (nn.slot < 0 && a.nbr) {  // no warm start: the own cell's best becomes the candidate
                 scan_target_cell(a, own_se, qx, qy, qz, nn);
                 own_left = make_uint2(0u, 0u);
+                for (int f0 = 0; f0 < 6 && nn.slot < 0; f0 += kMaxCells) {  // empty: seed from faces
+                    int xs[kMaxCells], ys[kMaxCells], zs[kMaxCells];
+                    bool valid[kMaxCells];
+                    float lbs[kMaxCells];
+#pragma unroll
+                    for (int u = 0; u < kMaxCells; ++u) {
+                        int dx = 0, dy = 0, dz = 0;
+                        valid[u] = f0 + u < 6;
+                        if (valid[u]) shell_cell(1, f0 + u, dx, dy, dz);
+                        xs[u] = qc.c[0] + dx;
+                        ys[u] = qc.c[1] + dy;
+                        zs[u] = qc.c[2] + dz;
+                        lbs[u] = 0.f;
+                    }
+                    uint2 se[kMaxCells];
+                    sIdx.batch(xs, ys, zs, valid, se);
+                    scan_cells_flat(a, se, lbs, qx, qy, qz, nn);
+                }
             }
-            if (!(nn.slot >= 0 && a.nbr && graph_nn(a, qx, qy, qz, nn)))
-                nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn);
+            bool exact = nn.slot >= 0 && a.nbr && graph_nn(a, qx, qy, qz, nn);
+            if (!exact) exact = nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn, true);
             if (sub) a.timeline[sub_base + 4] = nn.best == kEmptyKey ? 1 : 0;
             sub_stamp(3);
+            if (!exact) {  // hand over to the block's warps (warp_nn below)
+                const int k = atomicAdd(&sQn, 1);
+                sQtid[k] = tid;
+                sQq[k] = make_float4(qx, qy, qz, 0.f);
+                sQbest[k] = nn.best;
+                sQslot[k] = nn.slot;
+                sQp[k] = nn.p;
+            }
             dbg_slow += nn.slow;
             dbg_probes += nn.probes;
             dbg_cands += nn.cands;
             ++dbg_its;
             m0 = nn;
-            valid0 = nn.slot >= 0 && ki_key(nn.best) < a.r2;
         }
+        // queries whose fast path failed: one warp each, all lanes cooperating
+        __syncthreads();
+        for (int k = warp; k < sQn; k += kWarps) {
+            const float4 qq = sQq[k];
+            NN nn;
+            nn.best = sQbest[k];
+            nn.slot = sQslot[k];
+            nn.p = sQp[k];
+            warp_nn(a, sIdx, sBox, qq.x, qq.y, qq.z, nn, lane);
+            if (lane == 0) {
+                sQbest[k] = nn.best;
+                sQslot[k] = nn.slot;
+                sQp[k] = nn.p;
+            }
+        }
+        __syncthreads();
+        if (has0) {
+            for (int k = 0; k < sQn; ++k)
+                if (sQtid[k] == tid) {
+                    m0.best = sQbest[k];
+                    m0.slot = sQslot[k];
+                    m0.p = sQp[k];
+                }
+            valid0 = m0.slot >= 0 && ki_key(m0.best) < a.r2;
+        }
+        if (tid == 0) sQn = 0;  // next use is after at least one more __syncthreads
         for (int i = i0 + G * kT; i < n; i += G * kT) {  // non-resident points (large clouds)
             const float4 x = __ldg(a.spos + i);
             double q0, q1, q2;
@@ -604,7 +757,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
                 nn.slot = slot;
                 nn.best = pack_ki(canon_key(qx, qy, qz, nn.p.x, nn.p.y, nn.p.z), (uint32_t)__float_as_int(nn.p.w));
             }
-            nn_search(a, sIdx, sBox, qc, sIdx.one(qc.c[0], qc.c[1], qc.c[2]), qx, qy, qz, nn);
+            nn_search(a, sIdx, sBox, qc, sIdx.one(qc.c[0], qc.c[1], qc.c[2]), qx, qy, qz, nn, false);
             a.corr_ws[i] = (nn.slot >= 0 && ki_key(nn.best) < a.r2) ? nn.slot : -2 - nn.slot;
         }
         sub_stamp(5);
@@ -615,6 +768,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         for (int k = 0; k < kAlignTerms; ++k) acc[k] = 0.0;
         if (has0) {
             int32_t corr_val = -1;
+            sub_stamp(6);
             if (valid0) {
                 if (cov_slot != m0.slot) {
                     ta0 = __ldg(a.tcov_a + m0.slot);
@@ -623,6 +777,8 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
                 }
                 if (pair_terms(T, q0r, q1r, q2r, ca0, cb0, m0.p, ta0, tb0, acc)) corr_val = __float_as_int(m0.p.w);
             }
+            if (sub) acc[0] += 0.0 * (double)clock();
+            sub_stamp(7);
             if (a.corr_out) a.corr_out[i0] = corr_val;
         }
         for (int i = i0 + G * kT; i < n; i += G * kT) {

@@ -70,9 +70,9 @@ def main():
             print(f"  it {it}: arrivals min {a.min():7.1f} p50 {np.median(a):7.1f} max {a.max():7.1f} us; "
                   f"release {(pas - prev) / 1000.0:7.1f} us | block0 phases(us) {phs}")
             sb = 1 + max_iters * (Gn + 9) + it * 8
-            c = t[sb:sb + 6]
+            c = t[sb:sb + 8]
             print(f"      warp0 cycles: k3+own={c[1] - c[0]} warm={c[2] - c[1]} search={c[3] - c[2]} "
-                  f"rest={c[5] - c[3]} empty_best={c[4]}")
+                  f"rest={c[5] - c[3]} empty_best={c[4]} | B start->{c[6] - c[5]} pair={c[7] - c[6]}")
             prev = pas
 
 

@@ -305,7 +305,7 @@ def bench_gpu(args):
         kernel = "k_align (+k_align_init)"
     elif dom == 1:
         algo = ALGO_BYTES_KNN * n_src
-        kernel = "grid build + k_knn_cov"
+        kernel = "k_knn_search (+grid build, k_knn_epilogue)"
     else:
         algo = 4 * K.H * K.W / (w.stride ** 2) + 16 * n_src
         kernel = "k_bp_count + k_bp_emit"

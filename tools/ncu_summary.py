@@ -55,7 +55,10 @@ def launch_list(path):
 
 
 def short(name):
-    return name.split("(")[0].replace("void ", "").replace("gsicp::<unnamed>::", "").strip()
+    s = name.split("(")[0].replace("void ", "").strip()
+    for ns in ("gsicp::<unnamed>::", "gsicp::(anonymous namespace)::", "(anonymous namespace)::", "gsicp::"):
+        s = s.replace(ns, "")
+    return s
 
 
 def main():
@@ -83,7 +86,7 @@ def main():
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             rd *= scale.get(m["dram__bytes_read.sum"][1], 1)
             wr *= scale.get(m["dram__bytes_write.sum"][1], 1)
-            key = s.split("<")[0]
+            key = s.split("<")[0].split("::")[-1]
             traffic[key] = rd + wr
             lines.append(f"| DRAM bytes per launch (read+write) | {rd + wr:.0f} |")
         except (ValueError, AttributeError):

@@ -109,6 +109,24 @@ def dist_env():
     return ws, rank, local
 
 
+def max_over_ranks(x: float, dist=None, device=None) -> float:
+    """Max of a per-rank device-timed quantity over all ranks (the slowest replica defines the
+    whole-job time); identity at world size 1."""
+    if dist is None:
+        return float(x)
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(units_per_rank: int, world_size: int, total_ms: float) -> float:
+    """Whole-job aggregate: every rank processes `units_per_rank` independent frames (replicas,
+    weak scaling); the job time is the max over ranks."""
+    return world_size * units_per_rank / (total_ms / 1000.0)
+
+
 def make_workload(rank: int):
     import synth
 
@@ -238,12 +256,8 @@ def bench_gpu(args):
         dist.barrier()
     stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(3)] for i in range(nev)])
     step_ms = stage.sum(1)
-    total_ms = float(step_ms.sum())
-    if dist:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = ws * nev / (total_ms / 1000.0)
+    total_ms = max_over_ranks(float(step_ms.sum()), dist, dev)
+    value = job_throughput(nev, ws, total_ms)
 
     # e2e through the public API with host buffers: H2D depth (pinned), whole frame, D2H pose
     T_init = w.T_init
@@ -257,12 +271,8 @@ def bench_gpu(args):
         t1 = time.perf_counter()
         if i >= max(args.warmup, 3):
             e2e_ms.append(1000 * (t1 - t0))
-    e2e_total = sum(e2e_ms)
-    if dist:
-        t = torch.tensor([e2e_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
-    e2e_value = ws * nev / (e2e_total / 1000.0)
+    e2e_total = max_over_ranks(sum(e2e_ms), dist, dev)
+    e2e_value = job_throughput(nev, ws, e2e_total)
 
     # kNN-cov Mpts/s over a 4e6-point map (C4), kernel stage only
     knn_mpts = None

@@ -222,18 +222,8 @@ def bench_gpu(args):
 
     def step(evs=None):
         tr.d_T.copy_(T0)
-        if evs:
-            evs[0].record(stream)
-        g.backproject_downsample(depth, tr.K, tr.stride, tr.z_min, tr.z_max, tr.cloud.pos, tr.cloud.d_n, tr.ws_bp)
-        if evs:
-            evs[1].record(stream)
-        g.covariances(tr.cloud.pos, tr.cloud.d_n, tr.k, tr.mode, tr.eps, tr.cell0, tr.levels, tr.cloud.cov_a,
-                      tr.cloud.cov_b, None, tr.ws_cov)
-        if evs:
-            evs[2].record(stream)
-        g.align_async(tr.cloud, tgt, tr.d_T, tr.d_stats, params, tr.ws_align)
-        if evs:
-            evs[3].record(stream)
+        # A1 | A2-A4 (+ iteration-0 correspondences on a side stream) | A6-A9, events on `stream`
+        tr.step_async(depth, tgt, stream, evs)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -267,7 +257,7 @@ def bench_gpu(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         depth.copy_(depth_host, non_blocking=True)
-        Tg, st_e = tr.track(depth, tgt, T_init)  # blocking C-ABI call returns the host pose
+        Tg, st_e = tr.track(depth, tgt, T_init)  # public per-frame call: host pose in, host pose out
         t1 = time.perf_counter()
         if i >= max(args.warmup, 3):
             e2e_ms.append(1000 * (t1 - t0))

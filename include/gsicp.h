@@ -176,6 +176,20 @@ gsicp_status gsicp_align_async(const gsicp_cloud *src, const gsicp_target *tgt, 
                                const gsicp_align_params *prm, gsicp_align_stats *d_stats, int32_t *corr_out,
                                void *ws, size_t ws_bytes, void *stream);
 
+/* Iteration-0 correspondences ahead of the GN loop (A6 at the initial pose, P:95 / R15): for
+ * every source point the exact 1-NN of fl32(K3(T0, x_i)) among the target means, written into
+ * the align workspace `ws`.  Reads only src->pos / src->d_n (not the covariances), the target and
+ * the device pose d_T (double[16], T0), so it may run on a second stream concurrently with
+ * gsicp_covariances of the same cloud; the caller orders it before the align call (event join).
+ * The seeds are consumed by the NEXT gsicp_align / gsicp_align_async / gsicp_linearize issued
+ * FROM THE SAME HOST THREAD on the same workspace with the same src->pos and tgt->pos, and only
+ * if that call starts from exactly the
+ * pose d_T held when the seed kernel ran (checked bitwise on the device); otherwise they are
+ * ignored and the search runs as usual.  Results are identical with or without seeding.
+ * Errors: as gsicp_align_async.  Asynchronous. */
+gsicp_status gsicp_align_seed(const gsicp_cloud *src, const gsicp_target *tgt, const double *d_T,
+                              const gsicp_align_params *prm, void *ws, size_t ws_bytes, void *stream);
+
 /* TEST / DIAGNOSTIC export: one linearisation of Eq. 1 at pose T (host double[16]) without any
  * update — H (host double[36], row-major, twist order (omega, v)), b (host double[6]),
  * cost and inlier count; corr_opt [dev] nullable int32[cap] (original target index or -1).

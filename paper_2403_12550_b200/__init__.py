@@ -91,6 +91,7 @@ def lib():
                                   C.POINTER(AlignStats), P, sz, P]
         L.gsicp_align_async.argtypes = [C.POINTER(_Cloud), C.POINTER(_Target), P, C.POINTER(AlignParams), P, P, P,
                                         sz, P]
+        L.gsicp_align_seed.argtypes = [C.POINTER(_Cloud), C.POINTER(_Target), P, C.POINTER(AlignParams), P, sz, P]
         L.gsicp_linearize.argtypes = [C.POINTER(_Cloud), C.POINTER(_Target), P, f32, P, P, P, P, P, P, sz, P]
         L.gsicp_status_string.argtypes = [i32]
         L.gsicp_status_string.restype = C.c_char_p
@@ -104,7 +105,8 @@ def lib():
         L.gsicp_debug_align_counters.argtypes = [P]
         L.gsicp_debug_align_counters.restype = None
         for name in ("gsicp_backproject_downsample", "gsicp_covariances", "gsicp_build_target",
-                     "gsicp_build_target_cloud", "gsicp_align", "gsicp_align_async", "gsicp_linearize"):
+                     "gsicp_build_target_cloud", "gsicp_align", "gsicp_align_async", "gsicp_align_seed",
+                     "gsicp_linearize"):
             getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -113,7 +115,8 @@ def lib():
 EXPORTED = [
     "gsicp_backproject_workspace_size", "gsicp_backproject_downsample", "gsicp_covariances_workspace_size",
     "gsicp_covariances", "gsicp_build_target_workspace_size", "gsicp_build_target", "gsicp_build_target_cloud",
-    "gsicp_align_workspace_size", "gsicp_align", "gsicp_align_async", "gsicp_linearize", "gsicp_status_string",
+    "gsicp_align_workspace_size", "gsicp_align", "gsicp_align_async", "gsicp_align_seed", "gsicp_linearize",
+    "gsicp_status_string",
     "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version", "gsicp_debug_knn_counters",
     "gsicp_debug_align_timeline", "gsicp_debug_align_counters",
 ]
@@ -135,6 +138,10 @@ def debug_knn_counters(out: torch.Tensor | None):
     """Diagnostic: while set, covariances() also writes (level, probes, candidates, insertions)
     per query into `out` ((cap, 4) int32 CUDA tensor); None switches it off."""
     lib().gsicp_debug_knn_counters(_ptr(out) if out is not None else None)
+
+
+# align outcomes that are results, not errors (the stats carry the status)
+_ALIGN_ALLOW = (OK, WARN_MAX_ITERS, ERR_TRACKING_LOST, ERR_DEGENERATE_FRAME)
 
 
 def _check(st: int, allow=(OK,)):
@@ -310,7 +317,7 @@ def align_workspace(cap: int, device="cuda") -> torch.Tensor:
 
 
 def align(src: Cloud, tgt: Target, init_T, params: AlignParams | None = None, ws: torch.Tensor | None = None,
-          stream=None, allow=(OK, WARN_MAX_ITERS, ERR_TRACKING_LOST, ERR_DEGENERATE_FRAME)):
+          stream=None, allow=None):
     """A6-A9 (Eq. 1).  Blocking; returns (T (4,4) float64 numpy, stats dict)."""
     params = params or align_params()
     ws = ws if ws is not None else align_workspace(src.cap, src.pos.device)
@@ -320,7 +327,7 @@ def align(src: Cloud, tgt: Target, init_T, params: AlignParams | None = None, ws
     cs = src.c_struct()
     st = lib().gsicp_align(C.byref(cs), C.byref(tgt.st), T0.ctypes.data_as(C.c_void_p), C.byref(params),
                            Tout.ctypes.data_as(C.c_void_p), C.byref(stats), _ptr(ws), ws.numel(), _stream(stream))
-    _check(st, allow)
+    _check(st, allow or _ALIGN_ALLOW)
     return Tout, stats.as_dict()
 
 
@@ -333,6 +340,17 @@ def align_async(src: Cloud, tgt: Target, d_T: torch.Tensor, d_stats: torch.Tenso
     cs = src.c_struct()
     _check(lib().gsicp_align_async(C.byref(cs), C.byref(tgt.st), _ptr(d_T), C.byref(params), _ptr(d_stats),
                                    _ptr(corr_out), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def align_seed(src: Cloud, tgt: Target, d_T: torch.Tensor, params: AlignParams | None = None,
+               ws: torch.Tensor | None = None, stream=None):
+    """Iteration-0 correspondences at the device pose d_T into the align workspace `ws` (reads
+    only src.pos / src.d_n: may overlap the covariance stage on another stream).  Consumed by the
+    next align call on `ws` from this thread if it starts at the same pose."""
+    params = params or align_params()
+    cs = src.c_struct()
+    _check(lib().gsicp_align_seed(C.byref(cs), C.byref(tgt.st), _ptr(d_T), C.byref(params), _ptr(ws), ws.numel(),
+                                  _stream(stream)))
 
 
 def decode_stats(d_stats: torch.Tensor) -> dict:
@@ -379,6 +397,9 @@ class Tracker:
         self.ws_align = align_workspace(self.cap, self.device)
         self.d_T = torch.zeros(16, dtype=torch.float64, device=self.device)
         self.d_stats = torch.zeros(C.sizeof(AlignStats), dtype=torch.uint8, device=self.device)
+        self._side = torch.cuda.Stream(self.device)
+        self._fork = torch.cuda.Event()
+        self._join = torch.cuda.Event()
 
     def preprocess(self, depth: torch.Tensor, stream=None):
         backproject_downsample(depth, self.K, self.stride, self.z_min, self.z_max, self.cloud.pos, self.cloud.d_n,
@@ -386,12 +407,42 @@ class Tracker:
         covariances(self.cloud.pos, self.cloud.d_n, self.k, self.mode, self.eps, self.cell0, self.levels,
                     self.cloud.cov_a, self.cloud.cov_b, None, self.ws_cov, stream)
 
-    def step_async(self, depth: torch.Tensor, tgt: Target, stream=None):
-        """Whole frame, device-resident pose in self.d_T (set it before), no host sync."""
-        self.preprocess(depth, stream)
-        align_async(self.cloud, tgt, self.d_T, self.d_stats, self.params, self.ws_align, None, stream)
+    def step_async(self, depth: torch.Tensor, tgt: Target, stream=None, events=None):
+        """Whole frame, device-resident pose in self.d_T (set it before), no host sync.
+        A1 on `stream`; then the iteration-0 correspondences (gsicp_align_seed) on a side stream
+        concurrently with A2-A4; joined before A6-A9.  `events` (optional, 4 CUDA events) are
+        recorded on `stream` around A1 / A2-A4 / A6-A9."""
+        s0 = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if events:
+            events[0].record(s0)
+        backproject_downsample(depth, self.K, self.stride, self.z_min, self.z_max, self.cloud.pos, self.cloud.d_n,
+                               self.ws_bp, s0)
+        if events:
+            events[1].record(s0)
+        self._fork.record(s0)
+        self._side.wait_event(self._fork)
+        align_seed(self.cloud, tgt, self.d_T, self.params, self.ws_align, self._side)
+        self._join.record(self._side)
+        covariances(self.cloud.pos, self.cloud.d_n, self.k, self.mode, self.eps, self.cell0, self.levels,
+                    self.cloud.cov_a, self.cloud.cov_b, None, self.ws_cov, s0)
+        s0.wait_event(self._join)
+        if events:
+            events[2].record(s0)
+        align_async(self.cloud, tgt, self.d_T, self.d_stats, self.params, self.ws_align, None, s0)
+        if events:
+            events[3].record(s0)
 
     def track(self, depth: torch.Tensor, tgt: Target, init_T, stream=None):
-        """Whole frame through the blocking C ABI call; returns (T, stats)."""
-        self.preprocess(depth, stream)
-        return align(self.cloud, tgt, init_T, self.params, self.ws_align, stream)
+        """Whole frame through the public API: host pose in, (T, stats) out (blocking)."""
+        s0 = stream if stream is not None else torch.cuda.current_stream(self.device)
+        T0 = torch.from_numpy(np.ascontiguousarray(init_T, dtype=np.float64).reshape(16))
+        with torch.cuda.stream(s0):
+            self.d_T.copy_(T0.pin_memory() if not T0.is_pinned() else T0, non_blocking=True)
+        self.step_async(depth, tgt, s0)
+        with torch.cuda.stream(s0):
+            T = self.d_T.to("cpu", non_blocking=True)
+            st = self.d_stats.to("cpu", non_blocking=True)
+        s0.synchronize()
+        stats = AlignStats.from_buffer_copy(st.numpy().tobytes()[:C.sizeof(AlignStats)]).as_dict()
+        _check(stats["status"], _ALIGN_ALLOW)
+        return T.numpy().reshape(4, 4).copy(), stats

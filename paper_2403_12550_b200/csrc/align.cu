@@ -65,6 +65,9 @@ struct AlignArgs {
     long long *timeline;      // diagnostic (nullable): [0] start, then per iteration G arrivals + pass
     long long timeline_cap;
     int4 *debug;              // diagnostic (nullable): per point (slow searches, probes, candidates, iterations)
+    int32_t *seed_slot;       // [cap] iteration-0 matches from k_align_seed (target slot or -1)
+    double *seed_hdr;         // [16]: pose the seeds were computed at (12), ticket at [12]
+    double seed_ticket;       // k_align_seed: ticket to write; k_align: ticket expected (0: none)
 };
 
 __device__ __forceinline__ long long globaltimer_ns() {
@@ -581,6 +584,107 @@ __device__ __forceinline__ int solve_step(const AlignArgs &a, const double *sAcc
     return 0;
 }
 
+// No warm start: the own cell's best becomes the candidate; an empty own cell is seeded from
+// the 6 face neighbours (the graph step then needs some candidate to start from).
+__device__ __forceinline__ void nn_cold_start(const AlignArgs &a, const CellIndex &idx, const QueryCell &qc, uint2 own,
+                                              float qx, float qy, float qz, NN &nn) {
+    scan_target_cell(a, own, qx, qy, qz, nn);
+    for (int f0 = 0; f0 < 6 && nn.slot < 0; f0 += kMaxCells) {
+        int xs[kMaxCells], ys[kMaxCells], zs[kMaxCells];
+        bool valid[kMaxCells];
+        float lbs[kMaxCells];
+#pragma unroll
+        for (int u = 0; u < kMaxCells; ++u) {
+            int dx = 0, dy = 0, dz = 0;
+            valid[u] = f0 + u < 6;
+            if (valid[u]) shell_cell(1, f0 + u, dx, dy, dz);
+            xs[u] = qc.c[0] + dx;
+            ys[u] = qc.c[1] + dy;
+            zs[u] = qc.c[2] + dz;
+            lbs[u] = 0.f;
+        }
+        uint2 se[kMaxCells];
+        idx.batch(xs, ys, zs, valid, se);
+        scan_cells_flat(a, se, lbs, qx, qy, qz, nn);
+    }
+}
+
+__device__ __forceinline__ void load_cell_index(const AlignArgs &a, CellIndex &idx, int *box) {
+    idx.table = a.table;
+    idx.mask = a.mask;
+    idx.level = 0;
+    idx.dense = a.dense;
+    idx.use_dense = a.dense != nullptr && a.dense_hdr[0] != 0;
+    for (int k = 0; k < 3; ++k) {
+        idx.lo[k] = a.dense_hdr ? a.dense_hdr[1 + k] : 0;
+        idx.dim[k] = a.dense_hdr ? a.dense_hdr[4 + k] : 0;
+    }
+    for (int k = 0; k < 6; ++k) box[k] = cell_coord(ordered_to_float_(a.tbbox[k]), a.inv_h);
+}
+
+// Iteration-0 correspondences ahead of the GN loop (gsicp_align_seed): exact 1-NN of
+// fl32(K3(T0, x_i)) for every source point, by the same search as k_align's first iteration
+// (cold start, certified graph descent, fast path, block queue solved by whole warps).  It needs
+// only the source positions, so it can run concurrently with the source covariances (A2-A4).
+constexpr int kSeedT = 256;
+__global__ void __launch_bounds__(kSeedT) k_align_seed(AlignArgs a) {
+    __shared__ double sT[12];
+    __shared__ int sBox[6];
+    __shared__ CellIndex sIdx;
+    __shared__ int sQn;
+    __shared__ float4 sQq[kSeedT];
+    __shared__ unsigned long long sQbest[kSeedT];
+    __shared__ int sQslot[kSeedT];
+    __shared__ float4 sQp[kSeedT];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = *a.d_n;
+    if (tid < 12) sT[tid] = a.d_T[tid];
+    if (tid == 0) {
+        load_cell_index(a, sIdx, sBox);
+        sQn = 0;
+    }
+    __syncthreads();
+    const int i = blockIdx.x * kSeedT + tid;
+    NN nn;
+    int myk = -1;
+    if (i < n) {
+        const float4 x = __ldg(a.spos + i);
+        double q0, q1, q2;
+        k3(sT, x.x, x.y, x.z, q0, q1, q2);
+        const float qx = __double2float_rn(q0), qy = __double2float_rn(q1), qz = __double2float_rn(q2);
+        const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
+        const uint2 own = sIdx.one(qc.c[0], qc.c[1], qc.c[2]);
+        uint2 own_left = own;
+        if (a.nbr) {
+            nn_cold_start(a, sIdx, qc, own, qx, qy, qz, nn);
+            own_left = make_uint2(0u, 0u);
+        }
+        bool exact = nn.slot >= 0 && a.nbr && graph_nn(a, qx, qy, qz, nn);
+        if (!exact) exact = nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn, true);
+        if (!exact) {
+            myk = atomicAdd(&sQn, 1);
+            sQq[myk] = make_float4(qx, qy, qz, 0.f);
+            sQbest[myk] = nn.best;
+            sQslot[myk] = nn.slot;
+            sQp[myk] = nn.p;
+        }
+    }
+    __syncthreads();
+    for (int k = warp; k < sQn; k += kSeedT / 32) {
+        const float4 qq = sQq[k];
+        NN w;
+        w.best = sQbest[k];
+        w.slot = sQslot[k];
+        w.p = sQp[k];
+        warp_nn(a, sIdx, sBox, qq.x, qq.y, qq.z, w, lane);
+        if (lane == 0) sQslot[k] = w.slot;
+    }
+    __syncthreads();
+    if (i < n) a.seed_slot[i] = myk >= 0 ? sQslot[myk] : nn.slot;
+    if (blockIdx.x == 0 && tid < 12) a.seed_hdr[tid] = sT[tid];
+    if (blockIdx.x == 0 && tid == 12) a.seed_hdr[12] = a.seed_ticket;
+}
+
 __global__ void k_align_init(int32_t *corr_ws, int cap, unsigned int *barrier) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < cap) corr_ws[i] = -1;
@@ -606,17 +710,13 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     const int n = *a.d_n;
     if (tid < 12) sT[tid] = a.d_T[tid];
     if (a.timeline && blockIdx.x == 0 && tid == 0 && a.timeline_cap > 0) a.timeline[0] = globaltimer_ns();
-    if (tid < 6) sBox[tid] = cell_coord(ordered_to_float_(a.tbbox[tid]), a.inv_h);
+    __shared__ int sSeeded;
     if (tid == 0) {
-        sIdx.table = a.table;
-        sIdx.mask = a.mask;
-        sIdx.level = 0;
-        sIdx.dense = a.dense;
-        sIdx.use_dense = a.dense != nullptr && a.dense_hdr[0] != 0;
-        for (int k = 0; k < 3; ++k) {
-            sIdx.lo[k] = a.dense_hdr ? a.dense_hdr[1 + k] : 0;
-            sIdx.dim[k] = a.dense_hdr ? a.dense_hdr[4 + k] : 0;
-        }
+        load_cell_index(a, sIdx, sBox);
+        // seeds are used only if they were computed at exactly this pose (and not consumed yet)
+        bool ok = a.seed_ticket > 0.0 && a.seed_hdr[12] == a.seed_ticket;
+        for (int k = 0; k < 12; ++k) ok = ok && __double_as_longlong(a.seed_hdr[k]) == __double_as_longlong(a.d_T[k]);
+        sSeeded = ok;
     }
     if (tid == 0) sDone = 0;
     if (tid == 0) sQn = 0;
@@ -670,36 +770,26 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             if (sub) own_se.x += 0 * (uint32_t)clock();  // keep ordering of the stamp below
             sub_stamp(1);
             NN nn;
-            if (m0.slot >= 0) {  // warm start from the previous match (record kept in registers)
+            const bool seeded0 = it == 0 && sSeeded;
+            if (seeded0) {  // exact match at this pose computed ahead by k_align_seed
+                const int sl = __ldg(a.seed_slot + i0);
+                if (sl >= 0) {
+                    nn.p = __ldg(a.tpos + sl);
+                    nn.slot = sl;
+                    nn.best = pack_ki(canon_key(qx, qy, qz, nn.p.x, nn.p.y, nn.p.z), (uint32_t)__float_as_int(nn.p.w));
+                }
+            } else if (m0.slot >= 0) {  // warm start from the previous match (record kept in registers)
                 nn.p = m0.p;
                 nn.slot = m0.slot;
                 nn.best = pack_ki(canon_key(qx, qy, qz, m0.p.x, m0.p.y, m0.p.z), (uint32_t)__float_as_int(m0.p.w));
             }
             sub_stamp(2);
             uint2 own_left = own_se;
-            if (nn.slot < 0 && a.nbr) {  // no warm start: the own cell's best becomes the candidate
-                scan_target_cell(a, own_se, qx, qy, qz, nn);
+            if (!seeded0 && nn.slot < 0 && a.nbr) {  // no warm start: the own cell's best becomes the candidate
+                nn_cold_start(a, sIdx, qc, own_se, qx, qy, qz, nn);
                 own_left = make_uint2(0u, 0u);
-                for (int f0 = 0; f0 < 6 && nn.slot < 0; f0 += kMaxCells) {  // empty: seed from faces
-                    int xs[kMaxCells], ys[kMaxCells], zs[kMaxCells];
-                    bool valid[kMaxCells];
-                    float lbs[kMaxCells];
-#pragma unroll
-                    for (int u = 0; u < kMaxCells; ++u) {
-                        int dx = 0, dy = 0, dz = 0;
-                        valid[u] = f0 + u < 6;
-                        if (valid[u]) shell_cell(1, f0 + u, dx, dy, dz);
-                        xs[u] = qc.c[0] + dx;
-                        ys[u] = qc.c[1] + dy;
-                        zs[u] = qc.c[2] + dz;
-                        lbs[u] = 0.f;
-                    }
-                    uint2 se[kMaxCells];
-                    sIdx.batch(xs, ys, zs, valid, se);
-                    scan_cells_flat(a, se, lbs, qx, qy, qz, nn);
-                }
             }
-            bool exact = nn.slot >= 0 && a.nbr && graph_nn(a, qx, qy, qz, nn);
+            bool exact = seeded0 || (nn.slot >= 0 && a.nbr && graph_nn(a, qx, qy, qz, nn));
             if (!exact) exact = nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn, true);
             if (sub) a.timeline[sub_base + 4] = nn.best == kEmptyKey ? 1 : 0;
             sub_stamp(3);
@@ -750,14 +840,15 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             const float qx = __double2float_rn(q0), qy = __double2float_rn(q1), qz = __double2float_rn(q2);
             const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
             NN nn;
-            int slot = a.corr_ws[i];
+            int slot = (it == 0 && sSeeded) ? a.seed_slot[i] : a.corr_ws[i];
             if (slot <= -2) slot = -2 - slot;
             if (slot >= 0) {
                 nn.p = __ldg(a.tpos + slot);
                 nn.slot = slot;
                 nn.best = pack_ki(canon_key(qx, qy, qz, nn.p.x, nn.p.y, nn.p.z), (uint32_t)__float_as_int(nn.p.w));
             }
-            nn_search(a, sIdx, sBox, qc, sIdx.one(qc.c[0], qc.c[1], qc.c[2]), qx, qy, qz, nn, false);
+            if (!(it == 0 && sSeeded))
+                nn_search(a, sIdx, sBox, qc, sIdx.one(qc.c[0], qc.c[1], qc.c[2]), qx, qy, qz, nn, false);
             a.corr_ws[i] = (nn.slot >= 0 && ki_key(nn.best) < a.r2) ? nn.slot : -2 - nn.slot;
         }
         sub_stamp(5);
@@ -909,6 +1000,8 @@ struct AlignWs {
     unsigned int *barrier;
     double *partials;
     int32_t *corr_ws;
+    int32_t *seed_slot;
+    double *seed_hdr;
 };
 
 static AlignWs align_carve(Carver &c, int cap) {
@@ -920,6 +1013,8 @@ static AlignWs align_carve(Carver &c, int cap) {
     const int G = (int)blocks_for(cap > 0 ? cap : 1, kT);
     w.partials = c.take<double>((size_t)2 * G * kPad);
     w.corr_ws = c.take<int32_t>(cap);
+    w.seed_slot = c.take<int32_t>(cap);
+    w.seed_hdr = c.take<double>(16);
     return w;
 }
 static AlignWs align_carve(void *base, int cap) {
@@ -938,10 +1033,9 @@ gsicp_align_stats *align_ws_stats(void *ws) { return align_carve(ws, 0).d_stats;
 double *align_ws_lin(void *ws) { return align_carve(ws, 0).d_lin; }
 
 // d_T_inout: device pose (may equal the workspace pose); d_stats: device stats destination.
-cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double *d_T_inout,
-                         const gsicp_align_params &p, gsicp_align_stats *d_stats, int32_t *corr_out,
-                         int linearize_only, float r_lin, void *ws, cudaStream_t s) {
-    AlignWs w = align_carve(ws, src.cap);
+static AlignArgs make_args(const gsicp_cloud &src, const gsicp_target &tgt, double *d_T_inout,
+                           const gsicp_align_params &p, gsicp_align_stats *d_stats, int32_t *corr_out,
+                           int linearize_only, float r_lin, const AlignWs &w) {
     AlignArgs a;
     a.spos = reinterpret_cast<const float4 *>(src.pos);
     a.scov_a = reinterpret_cast<const float4 *>(src.cov_a);
@@ -977,6 +1071,43 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
     a.timeline = g_align_timeline;
     a.timeline_cap = g_align_timeline_cap;
     a.debug = reinterpret_cast<int4 *>(g_align_debug);
+    a.seed_slot = w.seed_slot;
+    a.seed_hdr = w.seed_hdr;
+    a.seed_ticket = 0.0;
+    return a;
+}
+
+// Seeds are single-use and bound to the workspace and the host thread: gsicp_align_seed records a
+// ticket here, the next align / linearize launch on the same workspace expects it (and clears it),
+// so stale seeds (another cloud, pose or workspace) are never used.
+thread_local void *g_seed_ws = nullptr;
+thread_local const void *g_seed_src = nullptr, *g_seed_tgt = nullptr;
+thread_local double g_seed_ticket = 0.0;
+thread_local double g_seed_counter = 0.0;
+
+cudaError_t align_seed_launch(const gsicp_cloud &src, const gsicp_target &tgt, const double *d_T,
+                              const gsicp_align_params &p, void *ws, cudaStream_t s) {
+    AlignWs w = align_carve(ws, src.cap);
+    AlignArgs a = make_args(src, tgt, const_cast<double *>(d_T), p, nullptr, nullptr, 0, 0.f, w);
+    g_seed_counter += 1.0;
+    a.seed_ticket = g_seed_counter;
+    g_seed_ws = ws;
+    g_seed_src = src.pos;
+    g_seed_tgt = tgt.pos;
+    g_seed_ticket = a.seed_ticket;
+    k_align_seed<<<blocks_for(src.cap > 0 ? src.cap : 1, kSeedT), kSeedT, 0, s>>>(a);
+    GSICP_LAUNCH_CHECK("k_align_seed");
+    note_launch();
+    return cudaSuccess;
+}
+
+cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double *d_T_inout,
+                         const gsicp_align_params &p, gsicp_align_stats *d_stats, int32_t *corr_out,
+                         int linearize_only, float r_lin, void *ws, cudaStream_t s) {
+    AlignWs w = align_carve(ws, src.cap);
+    AlignArgs a = make_args(src, tgt, d_T_inout, p, d_stats, corr_out, linearize_only, r_lin, w);
+    a.seed_ticket = (g_seed_ws == ws && g_seed_src == src.pos && g_seed_tgt == tgt.pos) ? g_seed_ticket : 0.0;
+    g_seed_ws = nullptr;
     k_align_init<<<blocks_for(src.cap > 0 ? src.cap : 1, 256), 256, 0, s>>>(w.corr_ws, src.cap, w.barrier);
     GSICP_LAUNCH_CHECK("k_align_init");
     int per_sm = 0;

@@ -42,6 +42,8 @@ size_t align_ws_bytes(int cap);
 double *align_ws_T(void *ws);
 gsicp_align_stats *align_ws_stats(void *ws);
 double *align_ws_lin(void *ws);
+cudaError_t align_seed_launch(const gsicp_cloud &src, const gsicp_target &tgt, const double *d_T,
+                              const gsicp_align_params &p, void *ws, cudaStream_t s);
 cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double *d_T_inout,
                          const gsicp_align_params &p, gsicp_align_stats *d_stats, int32_t *corr_out,
                          int linearize_only, float r_lin, void *ws, cudaStream_t s);
@@ -224,6 +226,18 @@ gsicp_status gsicp_align_async(const gsicp_cloud *src, const gsicp_target *tgt, 
     if ((st = check_ws(ws, ws_bytes, align_ws_bytes(src->cap))) != GSICP_OK) return st;
     return cuda_status(align_launch(*src, *tgt, d_T_inout, *prm, d_stats, corr_out, 0, 0.f, ws, (cudaStream_t)stream),
                        "align");
+}
+
+gsicp_status gsicp_align_seed(const gsicp_cloud *src, const gsicp_target *tgt, const double *d_T,
+                              const gsicp_align_params *prm, void *ws, size_t ws_bytes, void *stream) {
+    g_err[0] = 0;
+    gsicp_status st = check_cloud(src, "align_seed src");
+    if (st != GSICP_OK) return st;
+    if ((st = check_target(tgt)) != GSICP_OK) return st;
+    if ((st = check_params(prm)) != GSICP_OK) return st;
+    if (!d_T) BAD("align_seed: null device pose");
+    if ((st = check_ws(ws, ws_bytes, align_ws_bytes(src->cap))) != GSICP_OK) return st;
+    return cuda_status(align_seed_launch(*src, *tgt, d_T, *prm, ws, (cudaStream_t)stream), "align_seed");
 }
 
 gsicp_status gsicp_align(const gsicp_cloud *src, const gsicp_target *tgt, const double *init_T,

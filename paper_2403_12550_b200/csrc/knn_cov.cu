@@ -15,6 +15,9 @@
 //     coarser (multi-level hash: depth-image density varies as z^2).
 // The moments of each query are warp-reduced into the lane that owns it; then every lane runs the
 // binary64 eigen-decomposition and regularisation of its own query in parallel.
+#include <stdlib.h>
+#include <string.h>
+
 #include "grid.cuh"
 #include "host_common.cuh"
 #include "search.cuh"
@@ -31,6 +34,7 @@ constexpr int kKnnThreads = 128;
 constexpr int kQueriesPerWarp = 8;  // queries a warp searches one after the other
 constexpr int kMergeThreshold = 4;  // more passing candidates than this: sort-merge the batch
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kKnnBatch = 4;  // hash probes in flight per thread (thread variant)
 
 struct KnnArgs {
     GridView g;
@@ -250,6 +254,187 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_search(KnnArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Thread-per-query variant.  A query's neighbourhood is small (tens to ~150 candidates), so one
+// thread per query with its best-K list in registers issues far fewer warp instructions than a
+// warp per query; queries run in coarsest-level cell order, so the 32 threads of a warp scan
+// mostly the same cells (broadcast loads).
+//   fill : own cell + shell 1 (27 cells, hash probes batched); if the list is not full and a
+//          coarser level exists, restart there; else widen whole shells until full
+//   ball : every other cell whose conservative lower bound is <= the K-th key (ball_search)
+// Exact for the same reason as the warp variant: a cell is skipped only when no point in it can
+// beat the current K-th (key, index).
+template <int K>
+struct ThreadTopK {
+    unsigned long long L[K];  // ascending; kEmptyKey pads
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int j = 0; j < K; ++j) L[j] = kEmptyKey;
+    }
+    __device__ __forceinline__ unsigned long long worst() const { return L[K - 1]; }
+    // c < worst(): all compares first (independent), then the shift — no serial chain
+    __device__ __forceinline__ void insert(unsigned long long c) {
+        bool b[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) b[j] = L[j] < c;
+#pragma unroll
+        for (int j = K - 1; j > 0; --j) L[j] = b[j] ? L[j] : (b[j - 1] ? c : L[j - 1]);
+        L[0] = b[0] ? L[0] : c;
+    }
+};
+
+template <int K>
+__device__ __forceinline__ void scan_cell_thread(const float4 *__restrict__ spos, uint2 se, float qx, float qy,
+                                                 float qz, ThreadTopK<K> &T, int &cands, int &inserts) {
+    cands += (int)se.y;
+#pragma unroll 2
+    for (uint32_t p = 0; p < se.y; ++p) {
+        const float4 P = __ldg(spos + se.x + p);
+        const unsigned long long c = pack_ki(canon_key(qx, qy, qz, P.x, P.y, P.z), (uint32_t)__float_as_int(P.w));
+        if (c < T.worst()) {
+            T.insert(c);
+            ++inserts;
+        }
+    }
+}
+
+template <int K>
+__device__ bool knn_search_thread(const GridView &g, int level, float qx, float qy, float qz, ThreadTopK<K> &T,
+                                  int &probes, int &cands, int &inserts) {
+    T.reset();
+    const float inv_h = ldexpf(g.inv_h0, -level);
+    const QueryCell qc(qx, qy, qz, ldexpf(g.h0, level), inv_h);
+    int blo[3], bhi[3];
+    grid_cell_bbox(g, level, blo, bhi);
+    CellIndex idx;
+    idx.table = g.table;
+    idx.mask = g.mask;
+    idx.level = level;
+    idx.dense = nullptr;
+    idx.use_dense = false;
+    // own cell + shell 1, nearest-first, kKnnBatch probes in flight
+    for (int t0 = 0; t0 < 27; t0 += kKnnBatch) {
+        int xs[kKnnBatch], ys[kKnnBatch], zs[kKnnBatch];
+        bool valid[kKnnBatch];
+        float lb[kKnnBatch];
+        const float bound = ki_key(T.worst());
+#pragma unroll
+        for (int j = 0; j < kKnnBatch; ++j) {
+            const int t = t0 + j;
+            int dx = 0, dy = 0, dz = 0;
+            if (t > 0 && t < 27) shell_cell(1, t - 1, dx, dy, dz);
+            xs[j] = qc.c[0] + dx;
+            ys[j] = qc.c[1] + dy;
+            zs[j] = qc.c[2] + dz;
+            lb[j] = qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2);
+            valid[j] = t < 27 && xs[j] >= blo[0] && xs[j] <= bhi[0] && ys[j] >= blo[1] && ys[j] <= bhi[1] &&
+                       zs[j] >= blo[2] && zs[j] <= bhi[2] && !(lb[j] > bound);
+            probes += valid[j];
+        }
+        uint2 se[kKnnBatch];
+        idx.batch(xs, ys, zs, valid, se);
+        uint32_t live = 0;
+#pragma unroll
+        for (int j = 0; j < kKnnBatch; ++j) live |= (se[j].y ? 1u : 0u) << j;
+        while (live) {  // one copy of the scan (select the j-th entry without dynamic indexing)
+            const int j = __ffs(live) - 1;
+            live &= live - 1;
+            uint2 sj = se[0];
+            float lj = lb[0];
+#pragma unroll
+            for (int r = 1; r < kKnnBatch; ++r)
+                if (r == j) {
+                    sj = se[r];
+                    lj = lb[r];
+                }
+            if (!(lj > ki_key(T.worst()))) scan_cell_thread<K>(g.spos, sj, qx, qy, qz, T, cands, inserts);
+        }
+    }
+    int m = 1;
+    if (T.worst() == kEmptyKey) {
+        if (level + 1 < g.levels) return false;
+        // finest-possible level exhausted: widen whole shells until the list is full
+        while (T.worst() == kEmptyKey && !qc.covers(m, blo, bhi)) {
+            ++m;
+            const int cnt = shell_count(m);
+            for (int t = 0; t < cnt; ++t) {
+                int dx, dy, dz;
+                shell_cell(m, t, dx, dy, dz);
+                const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
+                if (x < blo[0] || x > bhi[0] || y < blo[1] || y > bhi[1] || z < blo[2] || z > bhi[2]) continue;
+                const float lb = qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2);
+                if (lb > ki_key(T.worst())) continue;
+                ++probes;
+                const uint2 se = idx.one(x, y, z);
+                if (se.y) scan_cell_thread<K>(g.spos, se, qx, qy, qz, T, cands, inserts);
+            }
+        }
+        if (T.worst() == kEmptyKey) return true;  // fewer than K points in the whole cloud
+    }
+    if (ki_key(T.worst()) < qc.certified_key(m) || qc.covers(m, blo, bhi)) return true;
+    const int mm = m;
+    ball_search<true, kKnnBatch>(
+        qc, idx, blo, bhi,
+        [&](int dx, int dy, int dz) { return max(abs(dx), max(abs(dy), abs(dz))) <= mm; },
+        [&](uint2 se) {
+            ++probes;
+            scan_cell_thread<K>(g.spos, se, qx, qy, qz, T, cands, inserts);
+        },
+        [&]() { return ki_key(T.worst()); });
+    return true;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kKnnThreads) k_knn_thread(KnnArgs a) {
+    const int n = *a.d_n;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const GridView &g = a.g;
+    const float4 e = __ldg(g.spos + (size_t)(g.levels - 1) * g.cap + t);
+    const float qx = e.x, qy = e.y, qz = e.z;
+    const int i = __float_as_int(e.w);
+    int level = g.levels - 1;
+    for (int l = 0; l < g.levels - 1; ++l) {
+        const float inv_h = ldexpf(g.inv_h0, -l);
+        const uint2 se =
+            cell_lookup(g.table, g.mask, cell_key(l, cell_coord(qx, inv_h), cell_coord(qy, inv_h), cell_coord(qz, inv_h)));
+        if (se.y >= (uint32_t)kMinCell) {
+            level = l;
+            break;
+        }
+    }
+    ThreadTopK<K> T;
+    int probes = 0, cands = 0, inserts = 0;
+    while (!knn_search_thread<K>(g, level, qx, qy, qz, T, probes, cands, inserts)) ++level;
+    if (a.debug) a.debug[i] = make_int4(level, probes, cands, inserts);
+    if (a.knn_idx) {
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (j < a.k) a.knn_idx[(size_t)i * a.k + j] = T.L[j] == kEmptyKey ? -1 : (int32_t)ki_idx(T.L[j]);
+    }
+    if (!a.moments) return;
+    double v[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        if (j >= a.k || T.L[j] == kEmptyKey) continue;
+        const float4 p = __ldg(a.pos + ki_idx(T.L[j]));
+        const double d0 = (double)p.x - (double)qx, d1 = (double)p.y - (double)qy, d2 = (double)p.z - (double)qz;
+        v[0] += d0;
+        v[1] += d1;
+        v[2] += d2;
+        v[3] += d0 * d0;
+        v[4] += d0 * d1;
+        v[5] += d0 * d2;
+        v[6] += d1 * d1;
+        v[7] += d1 * d2;
+        v[8] += d2 * d2;
+        v[9] += 1.0;
+    }
+    double *mr = a.moments + (size_t)t * 10;
+#pragma unroll
+    for (int c = 0; c < 10; ++c) mr[c] = v[c];
+}
+
 // per-query epilogue (thread per query): covariance (normalised by the count), eigen,
 // regularisation, scattered to input order
 __global__ void __launch_bounds__(kKnnThreads) k_knn_epilogue(KnnArgs a) {
@@ -273,11 +458,32 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_epilogue(KnnArgs a) {
     store_cov(a.cov_a, a.cov_b, i, R, ev.lam[1], flags);
 }
 
+// kNN kernel variant: warp per query (default) or thread per query (GSICP_KNN=thread, A/B only)
+bool knn_use_warp() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("GSICP_KNN");
+        v = (e && strcmp(e, "thread") == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
+template <int K>
+cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s) {
+    if (knn_use_warp()) {
+        const long long warps = (cap + kQueriesPerWarp - 1) / kQueriesPerWarp;
+        k_knn_search<K><<<blocks_for(warps * 32, kKnnThreads), kKnnThreads, 0, s>>>(a);
+    } else {
+        k_knn_thread<K><<<blocks_for(cap, kKnnThreads), kKnnThreads, 0, s>>>(a);
+    }
+    GSICP_LAUNCH_CHECK("k_knn_search");
+    return cudaSuccess;
+}
+
 template <int K>
 cudaError_t launch_k(const KnnArgs &a, int cap, cudaStream_t s) {
-    const long long warps = (cap + kQueriesPerWarp - 1) / kQueriesPerWarp;
-    k_knn_search<K><<<blocks_for(warps * 32, kKnnThreads), kKnnThreads, 0, s>>>(a);
-    GSICP_LAUNCH_CHECK("k_knn_search");
+    cudaError_t e = launch_search<K>(a, cap, s);
+    if (e != cudaSuccess) return e;
     k_knn_epilogue<<<blocks_for(cap, kKnnThreads), kKnnThreads, 0, s>>>(a);
     GSICP_LAUNCH_CHECK("k_knn_epilogue");
     note_launch(2);
@@ -328,9 +534,8 @@ cudaError_t knn_graph_launch(const GridView &g, const float4 *pos, const int32_t
     a.knn_idx = knn_idx;
     a.moments = nullptr;
     a.debug = nullptr;
-    const long long warps = (cap + kQueriesPerWarp - 1) / kQueriesPerWarp;
-    k_knn_search<kGraphK><<<blocks_for(warps * 32, kKnnThreads), kKnnThreads, 0, s>>>(a);
-    GSICP_LAUNCH_CHECK("k_knn_search(graph)");
+    cudaError_t e = launch_search<kGraphK>(a, cap, s);
+    if (e != cudaSuccess) return e;
     note_launch();
     return cudaSuccess;
 }

@@ -144,7 +144,9 @@ struct CellIndex {
 // alone (no loads), then cells are looked up kLookupBatch at a time, nearest first, and a cell is
 // scanned only if its lower bound is still <= bound() (which may shrink while scanning).
 //   scan(uint2 start_count);  bound() -> float
-template <class Skip, class Scan, class Bound>
+// kCompact: one (non-unrolled) copy of scan() per batch instead of kLookupBatch inlined copies —
+// for callers whose scan() is large (register-resident best-K lists).
+template <bool kCompact = false, int B = kLookupBatch, class Skip, class Scan, class Bound>
 __device__ __forceinline__ void ball_search(const QueryCell &qc, const CellIndex &idx, const int *blo, const int *bhi,
                                             Skip skip, Scan scan, Bound bound) {
     int zlo, zhi;
@@ -164,12 +166,12 @@ __device__ __forceinline__ void ball_search(const QueryCell &qc, const CellIndex
             int xlo, xhi;
             axis_range(qc, 0, bound() - gzy, blo[0], bhi[0], xlo, xhi);
             const int kxmax = 2 * max(-xlo, xhi);
-            for (int kx0 = 0; kx0 <= kxmax; kx0 += kLookupBatch) {
-                int xs[kLookupBatch], ys[kLookupBatch], zs[kLookupBatch];
-                bool valid[kLookupBatch];
-                float lb[kLookupBatch];
+            for (int kx0 = 0; kx0 <= kxmax; kx0 += B) {
+                int xs[B], ys[B], zs[B];
+                bool valid[B];
+                float lb[B];
 #pragma unroll
-                for (int j = 0; j < kLookupBatch; ++j) {
+                for (int j = 0; j < B; ++j) {
                     const int dx = zigzag(kx0 + j);
                     valid[j] = kx0 + j <= kxmax && dx >= xlo && dx <= xhi && !skip(dx, dy, dz);
                     lb[j] = gzy + qc.gap2(dx, 0);
@@ -177,11 +179,30 @@ __device__ __forceinline__ void ball_search(const QueryCell &qc, const CellIndex
                     ys[j] = qc.c[1] + dy;
                     zs[j] = qc.c[2] + dz;
                 }
-                uint2 se[kLookupBatch];
+                uint2 se[B];
                 idx.batch(xs, ys, zs, valid, se);
+                if (kCompact) {
+                    uint32_t live = 0;
 #pragma unroll
-                for (int j = 0; j < kLookupBatch; ++j)
-                    if (se[j].y && lb[j] <= bound()) scan(se[j]);
+                    for (int j = 0; j < B; ++j) live |= (se[j].y ? 1u : 0u) << j;
+                    while (live) {
+                        const int j = __ffs(live) - 1;
+                        live &= live - 1;
+                        uint2 sj = se[0];
+                        float lj = lb[0];
+#pragma unroll
+                        for (int r = 1; r < B; ++r)
+                            if (r == j) {
+                                sj = se[r];
+                                lj = lb[r];
+                            }
+                        if (lj <= bound()) scan(sj);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < B; ++j)
+                        if (se[j].y && lb[j] <= bound()) scan(se[j]);
+                }
             }
         }
     }

@@ -330,6 +330,48 @@ def test_align_deterministic(g, replica_setup):
         np.testing.assert_array_equal(o, outs[0])
 
 
+def _align_dev(g, S, T, ws, seed_T=None, params=None):
+    params = params or g.align_params(max_iters=30, max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6)
+    d_T = torch.from_numpy(np.ascontiguousarray(T, dtype=np.float64).reshape(-1)).to(DEV)
+    d_stats = torch.zeros(32, dtype=torch.uint8, device=DEV)
+    if seed_T is not None:
+        d_seed = torch.from_numpy(np.ascontiguousarray(seed_T, dtype=np.float64).reshape(-1)).to(DEV)
+        g.align_seed(S["src"], S["tgt"], d_seed, params, ws)
+    g.align_async(S["src"], S["tgt"], d_T, d_stats, params, ws)
+    torch.cuda.synchronize()
+    return d_T.cpu().numpy().reshape(4, 4), g.decode_stats(d_stats)
+
+
+def test_align_seed_identical(g, replica_setup):
+    """Iteration-0 correspondences computed ahead (gsicp_align_seed) give bit-identical results;
+    seeds at another pose, or for another workspace, are ignored."""
+    S = replica_setup
+    w = S["w"]
+    ws = g.align_workspace(S["src"].cap, DEV)
+    ws2 = g.align_workspace(S["src"].cap, DEV)
+    T_ref, st_ref = _align_dev(g, S, w.T_init, ws)
+    T_s, st_s = _align_dev(g, S, w.T_init, ws, seed_T=w.T_init)
+    np.testing.assert_array_equal(T_s, T_ref)
+    assert st_s == st_ref
+    other = synth.perturb_pose(w.T_init, 31, 2.0, 0.03)
+    T_o, st_o = _align_dev(g, S, w.T_init, ws, seed_T=other)  # stale pose: ignored
+    np.testing.assert_array_equal(T_o, T_ref)
+    assert st_o == st_ref
+    # seed into ws2, align on ws: the seed is not consumed there (and ws2's is dropped)
+    d_seed = torch.from_numpy(w.T_init.reshape(-1).copy()).to(DEV)
+    g.align_seed(S["src"], S["tgt"], d_seed, None, ws2)
+    T_w, st_w = _align_dev(g, S, w.T_init, ws)
+    np.testing.assert_array_equal(T_w, T_ref)
+    # linearize after a seed at the same pose: same H / b / correspondences as without
+    T = synth.perturb_pose(w.T_gt, 12, 4.0, 0.08)
+    lg0 = g.linearize(S["src"], S["tgt"], T, 0.1, ws=ws)
+    d_seed = torch.from_numpy(np.ascontiguousarray(T).reshape(-1).copy()).to(DEV)
+    g.align_seed(S["src"], S["tgt"], d_seed, None, ws)
+    lg1 = g.linearize(S["src"], S["tgt"], T, 0.1, ws=ws)
+    np.testing.assert_array_equal(lg1["H"], lg0["H"])
+    assert lg1["n"] == lg0["n"]
+
+
 def test_align_errors(g, c1_setup):
     S = c1_setup
     # disjoint clouds 100 m apart -> TRACKING_LOST with the init pose

@@ -49,12 +49,12 @@ def main():
     w = synth.make_frame_workload(2, "replica", M=1000, stride=4)
     K = w.K
     pos, d_n = g.backproject_downsample(torch.from_numpy(w.depth).cuda(), (K.fx, K.fy, K.cx, K.cy), stride=4)
-    for cell0, levels in ((0.0083, 5), (0.005, 6), (0.012, 5), (0.02, 4)):
+    for cell0, levels in ((0.02, 4), (0.01, 5)):
         run(pos, d_n, cell0, levels, "replica s=4")
     scene = synth.make_scene(1004)
     means, _, _, ell = synth.sample_map(scene, 4_000_000, 4004)
     c4 = g.Cloud.from_points(torch.from_numpy(means).cuda())
-    for cm, levels in ((2.0, 4), (1.5, 4), (3.0, 3)):
+    for cm, levels in ((3.0, 3), (2.0, 3)):
         run(c4.pos, c4.d_n, cm * ell, levels, "C4 4e6 map", reps=3)
 
 

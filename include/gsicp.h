@@ -210,7 +210,8 @@ void gsicp_debug_knn_counters(int32_t *d_out);
 void gsicp_debug_align_timeline(int64_t *d_out, int64_t capacity);
 
 /* DIAGNOSTIC: while set, align / linearize launches write per resident source point i
- * d_out[4*i + 0..3] = (slow-path searches, cells probed, candidates scanned, iterations),
+ * d_out[4*i + 0..3] = bitmasks over the GN iterations (bit it) of: search handed to the
+ * warp-cooperative path, motion-bounded reuse, kNN-graph certificate; then the iteration count,
  * summed over the GN iterations (int32, device, >= 4*cap entries).  NULL switches it off. */
 void gsicp_debug_align_counters(int32_t *d_out);
 

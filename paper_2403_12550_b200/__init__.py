@@ -123,7 +123,7 @@ EXPORTED = [
 
 
 def debug_align_counters(out: torch.Tensor | None):
-    """Diagnostic: while set, align/linearize write (slow searches, probes, candidates, iterations)
+    """Diagnostic: while set, align/linearize write (queued searches, reuses, graph certificates, iterations)
     per resident source point into `out` ((cap, 4) int32 CUDA tensor); None switches it off."""
     lib().gsicp_debug_align_counters(_ptr(out) if out is not None else None)
 

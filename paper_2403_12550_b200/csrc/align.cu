@@ -64,7 +64,8 @@ struct AlignArgs {
     int32_t *corr_out;        // nullable [cap] original target index or -1
     long long *timeline;      // diagnostic (nullable): [0] start, then per iteration G arrivals + pass
     long long timeline_cap;
-    int4 *debug;              // diagnostic (nullable): per point (slow searches, probes, candidates, iterations)
+    int4 *debug;              // diagnostic (nullable): per point bitmasks over iterations (queued, reused,
+                              // graph-certified) and the iteration count
     int32_t *seed_slot;       // [cap] iteration-0 matches from k_align_seed (target slot or -1)
     double *seed_hdr;         // [16]: pose the seeds were computed at (12), ticket at [12]
     double seed_ticket;       // k_align_seed: ticket to write; k_align: ticket expected (0: none)
@@ -130,8 +131,13 @@ __device__ __forceinline__ float nn_bound(const AlignArgs &a, const NN &nn) {
 // holds nothing better and j is not certified, or after kGraphSteps steps, returns false (nn
 // holds the best point seen, a valid upper bound for the grid search).
 constexpr int kGraphSteps = 4;
+constexpr float kReuseMargin = 1e-5f;  // relative slack on every distance of the reuse test
 
-__device__ __forceinline__ bool graph_nn(const AlignArgs &a, float qx, float qy, float qz, NN &nn) {
+// On a certified step the list also bounds the SECOND nearest target: list members have their
+// exact distances, every other target k has |q - m_k| >= |m_j - m_k| - |q - m_j| >=
+// sqrt(key_K(j)) - sqrt(k_j).  d2lb receives that lower bound on the distance from q to any
+// target other than the 1-NN (conservatively rounded), for the motion-bounded reuse in k_align.
+__device__ __forceinline__ bool graph_nn(const AlignArgs &a, float qx, float qy, float qz, NN &nn, float &d2lb) {
     for (int step = 0; step < kGraphSteps; ++step) {
         const int j = nn.slot;
         const float kj = ki_key(nn.best);
@@ -149,6 +155,7 @@ __device__ __forceinline__ bool graph_nn(const AlignArgs &a, float qx, float qy,
         for (int u = 0; u < kGraphK; ++u) p[u] = sl[u] >= 0 ? __ldg(a.tpos + sl[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
         ++nn.probes;
         nn.cands += kGraphK;
+        unsigned long long l1 = kEmptyKey, l2 = kEmptyKey;  // the two smallest of this list
 #pragma unroll
         for (int u = 0; u < kGraphK; ++u) {
             if (sl[u] < 0) continue;
@@ -159,8 +166,15 @@ __device__ __forceinline__ bool graph_nn(const AlignArgs &a, float qx, float qy,
                 nn.slot = sl[u];
                 nn.p = p[u];
             }
+            l2 = v < l1 ? l1 : (v < l2 ? v : l2);
+            l1 = v < l1 ? v : l1;
         }
-        if (certified) return true;
+        if (certified) {
+            const float rc = sqrtf(kk) * (1.f - kReuseMargin) - sqrtf(kj) * (1.f + kReuseMargin);
+            const float d2 = l2 != kEmptyKey ? sqrtf(ki_key(l2)) : INFINITY;
+            d2lb = fmaxf(fminf(d2, rc), 0.f) * (1.f - kReuseMargin);
+            return true;
+        }
         if (nn.slot == j) return false;  // local minimum without a certificate
     }
     return false;
@@ -332,22 +346,110 @@ __device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int
 }
 
 // Warp-cooperative exact 1-NN for one query (all lanes call it with the same arguments; nn is
-// uniform on entry and exit): the cells of the offset box whose gaps fit the bound are probed 32
-// at a time (lane = cell), their points scanned as one flattened range (lane = candidate), and
-// the batch minimum is taken by shuffles; the bound shrinks as it goes.  Used for the queries
-// whose per-thread fast path failed, so a few hard queries no longer serialise a whole warp.
+// uniform on entry and exit).  Cells are visited in Chebyshev shells around the query cell,
+// nearest first (shell 0+1 = 27 cells in the first round, then shell m in rounds of 32, lane =
+// cell), skipping cells whose lower bound exceeds the current bound; the points of the probed
+// cells are scanned as one flattened range (lane = candidate) and the batch minimum is taken by
+// shuffles.  After shell m every unvisited point is >= certified_key(m) away, so the search
+// stops as soon as the bound is below that (or the shells cover the target bbox).  Used for the
+// queries whose per-thread fast path failed, so a few hard queries do not serialise a warp.
+// With fixed_b2 >= 0 it instead finds the best target with key <= fixed_b2 other than slot
+// `excl` (the second-neighbour bound of the motion-bounded reuse); the r gate does not apply.
+__device__ __forceinline__ void warp_scan_cells(const AlignArgs &a, const CellIndex &idx, const QueryCell &qc, bool valid,
+                                                int dx, int dy, int dz, float qx, float qy, float qz, NN &nn, int lane,
+                                                int excl) {
+    const uint2 se = valid ? idx.one(qc.c[0] + dx, qc.c[1] + dy, qc.c[2] + dz) : make_uint2(0u, 0u);
+    uint32_t incl = se.y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t ctot = __shfl_sync(0xffffffffu, incl, 31);
+    nn.probes += __popc(__ballot_sync(0xffffffffu, se.y != 0));
+    nn.cands += (int)ctot;
+    for (uint32_t base = 0; base < ctot; base += 32) {
+        const uint32_t item = base + lane;
+        int l0 = 0, l1 = 31;
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+            const int mid = (l0 + l1) >> 1;
+            if (__shfl_sync(0xffffffffu, incl, mid) > item) l1 = mid; else l0 = mid + 1;
+        }
+        const uint32_t c_incl = __shfl_sync(0xffffffffu, incl, l0);
+        const uint32_t c_start = __shfl_sync(0xffffffffu, se.x, l0);
+        const uint32_t c_cnt = __shfl_sync(0xffffffffu, se.y, l0);
+        unsigned long long cand = kEmptyKey;
+        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint32_t slot = 0;
+        if (item < ctot) {
+            slot = c_start + (item - (c_incl - c_cnt));
+            p = __ldg(a.tpos + slot);
+            cand = (int)slot == excl ? kEmptyKey
+                                     : pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
+        }
+        unsigned long long mn = cand;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long v = shfl_u64(mn, lane ^ o);
+            mn = v < mn ? v : mn;
+        }
+        if (mn < nn.best) {
+            const int src = __ffs(__ballot_sync(0xffffffffu, cand == mn)) - 1;
+            nn.best = mn;
+            nn.slot = (int)__shfl_sync(0xffffffffu, slot, src);
+            nn.p.x = __shfl_sync(0xffffffffu, p.x, src);
+            nn.p.y = __shfl_sync(0xffffffffu, p.y, src);
+            nn.p.z = __shfl_sync(0xffffffffu, p.z, src);
+            nn.p.w = __shfl_sync(0xffffffffu, p.w, src);
+        }
+    }
+}
+
+constexpr int kWarpShells = 3;  // shells visited nearest-first before the box traversal
+
 __device__ void warp_nn(const AlignArgs &a, const CellIndex &idx, const int *sb, float qx, float qy, float qz, NN &nn,
-                        int lane) {
+                        int lane, float fixed_b2 = -1.f, int excl = -1) {
     const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
     const int *blo = sb, *bhi = sb + 3;
-    const float b0 = nn_bound(a, nn);
+    auto bound = [&]() {
+        return fixed_b2 >= 0.f ? fminf(nn.best != kEmptyKey ? ki_key(nn.best) : INFINITY, fixed_b2) : nn_bound(a, nn);
+    };
+    auto in_box = [&](int dx, int dy, int dz) {
+        const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
+        return x >= blo[0] && x <= bhi[0] && y >= blo[1] && y <= bhi[1] && z >= blo[2] && z <= bhi[2];
+    };
+    // shells 0..kWarpShells, nearest first
+    for (int m = 1; m <= kWarpShells; ++m) {
+        const int cnt = m == 1 ? 27 : shell_count(m);
+        for (int t0 = 0; t0 < cnt; t0 += 32) {
+            const float b = bound();
+            const int t = t0 + lane;
+            int dx = 0, dy = 0, dz = 0;
+            bool valid = t < cnt;
+            if (valid) {
+                if (m == 1) {
+                    if (t > 0) shell_cell(1, t - 1, dx, dy, dz);
+                } else {
+                    shell_cell(m, t, dx, dy, dz);
+                }
+                valid = in_box(dx, dy, dz) && qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2) <= b;
+            }
+            if (!__any_sync(0xffffffffu, valid)) continue;
+            warp_scan_cells(a, idx, qc, valid, dx, dy, dz, qx, qy, qz, nn, lane, excl);
+        }
+        // shells 0..m done: every unvisited point is >= certified_key(m) away
+        if (bound() < qc.certified_key(m) || qc.covers(m, blo, bhi)) return;
+    }
+    // the rest of the ball: the box of offsets whose gaps fit the bound, outside the shells
+    const float b0 = bound();
     int lo[3], hi[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) axis_range(qc, k, b0, blo[k], bhi[k], lo[k], hi[k]);
     const int nx = max(hi[0] - lo[0] + 1, 0), ny = max(hi[1] - lo[1] + 1, 0), nz = max(hi[2] - lo[2] + 1, 0);
     const long long total = (long long)nx * ny * nz;
     for (long long t0 = 0; t0 < total; t0 += 32) {
-        const float b = nn_bound(a, nn);
+        const float b = bound();
         const long long t = t0 + lane;
         int dx = 0, dy = 0, dz = 0;
         bool valid = t < total;
@@ -355,53 +457,11 @@ __device__ void warp_nn(const AlignArgs &a, const CellIndex &idx, const int *sb,
             dx = lo[0] + (int)(t % nx);
             dy = lo[1] + (int)((t / nx) % ny);
             dz = lo[2] + (int)(t / ((long long)nx * ny));
-            valid = qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2) <= b;
+            valid = max(abs(dx), max(abs(dy), abs(dz))) > kWarpShells &&
+                    qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2) <= b;
         }
-        const uint2 se = valid ? idx.one(qc.c[0] + dx, qc.c[1] + dy, qc.c[2] + dz) : make_uint2(0u, 0u);
-        uint32_t incl = se.y;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t ctot = __shfl_sync(0xffffffffu, incl, 31);
-        nn.probes += __popc(__ballot_sync(0xffffffffu, se.y != 0));
-        nn.cands += (int)ctot;
-        for (uint32_t base = 0; base < ctot; base += 32) {
-            const uint32_t item = base + lane;
-            int l0 = 0, l1 = 31;
-#pragma unroll
-            for (int s = 0; s < 5; ++s) {
-                const int mid = (l0 + l1) >> 1;
-                if (__shfl_sync(0xffffffffu, incl, mid) > item) l1 = mid; else l0 = mid + 1;
-            }
-            const uint32_t c_incl = __shfl_sync(0xffffffffu, incl, l0);
-            const uint32_t c_start = __shfl_sync(0xffffffffu, se.x, l0);
-            const uint32_t c_cnt = __shfl_sync(0xffffffffu, se.y, l0);
-            unsigned long long cand = kEmptyKey;
-            float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-            uint32_t slot = 0;
-            if (item < ctot) {
-                slot = c_start + (item - (c_incl - c_cnt));
-                p = __ldg(a.tpos + slot);
-                cand = pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
-            }
-            unsigned long long m = cand;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long v = shfl_u64(m, lane ^ o);
-                m = v < m ? v : m;
-            }
-            if (m < nn.best) {
-                const int src = __ffs(__ballot_sync(0xffffffffu, cand == m)) - 1;
-                nn.best = m;
-                nn.slot = (int)__shfl_sync(0xffffffffu, slot, src);
-                nn.p.x = __shfl_sync(0xffffffffu, p.x, src);
-                nn.p.y = __shfl_sync(0xffffffffu, p.y, src);
-                nn.p.z = __shfl_sync(0xffffffffu, p.z, src);
-                nn.p.w = __shfl_sync(0xffffffffu, p.w, src);
-            }
-        }
+        if (!__any_sync(0xffffffffu, valid)) continue;
+        warp_scan_cells(a, idx, qc, valid, dx, dy, dz, qx, qy, qz, nn, lane, excl);
     }
 }
 
@@ -659,7 +719,8 @@ __global__ void __launch_bounds__(kSeedT) k_align_seed(AlignArgs a) {
             nn_cold_start(a, sIdx, qc, own, qx, qy, qz, nn);
             own_left = make_uint2(0u, 0u);
         }
-        bool exact = nn.slot >= 0 && a.nbr && graph_nn(a, qx, qy, qz, nn);
+        float d2 = 0.f;
+        bool exact = nn.slot >= 0 && a.nbr && graph_nn(a, qx, qy, qz, nn, d2);
         if (!exact) exact = nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn, true);
         if (!exact) {
             myk = atomicAdd(&sQn, 1);
@@ -705,6 +766,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     __shared__ unsigned long long sQbest[kT];
     __shared__ int sQslot[kT];
     __shared__ float4 sQp[kT];
+    __shared__ float sQd2[kT];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
     const int n = *a.d_n;
@@ -735,7 +797,8 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     int own_c[3] = {INT_MIN, INT_MIN, INT_MIN};
     uint2 own_se = make_uint2(0u, 0u);
     bool valid0 = false;
-    int dbg_slow = 0, dbg_probes = 0, dbg_cands = 0, dbg_its = 0;
+    float d2lb = 0.f, qp0 = 0.f, qp1 = 0.f, qp2 = 0.f;  // reuse state: 2nd-NN distance bound at qp
+    int dbg_slow = 0, dbg_reuse = 0, dbg_graph = 0, dbg_its = 0;
     __syncthreads();
     int status = GSICP_WARN_MAX_ITERS, iters = 0, converged = 0;
     double n_in = 0.0, cost_last = 0.0;
@@ -758,6 +821,8 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         auto sub_stamp = [&](int k) {
             if (sub && sub_base + k < a.timeline_cap) a.timeline[sub_base + k] = clock64();
         };
+        const long long lane_t0 = a.timeline && blockIdx.x == 0 ? clock64() : 0;
+        int path_code = 0;
         if (has0) {
             sub_stamp(0);
             k3(T, x0.x, x0.y, x0.z, q0r, q1r, q2r);
@@ -783,14 +848,45 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
                 nn.slot = m0.slot;
                 nn.best = pack_ki(canon_key(qx, qy, qz, m0.p.x, m0.p.y, m0.p.z), (uint32_t)__float_as_int(m0.p.w));
             }
+            bool exact = seeded0;
+            // motion-bounded reuse: the query moved by delta since the match was proven, with
+            // every other target >= d2lb away then; if d1' + delta < d2lb - delta... precisely
+            // |q' - m| < d2lb - delta <= |q' - m_k| for all k != m, the match stands (no loads)
+            if (!exact && d2lb > 0.f) {
+                const float ex = qx - qp0, ey = qy - qp1, ez = qz - qp2;
+                const float delta = sqrtf(ex * ex + ey * ey + ez * ez) * (1.f + kReuseMargin);
+                // d2lb bounds every target other than the candidate: beating d1 proves the
+                // candidate is the 1-NN, or (candidate absent or beyond r) that the point stays gated
+                const float d1 = nn.slot >= 0 ? fminf(sqrtf(ki_key(nn.best)), a.r) : a.r;
+                if ((d2lb - delta) * (1.f - kReuseMargin) > d1 * (1.f + kReuseMargin)) {
+                    exact = true;
+                    d2lb -= delta;
+                    dbg_reuse |= 1 << (it & 31);
+                }
+            }
+            if (!exact) d2lb = 0.f;
             sub_stamp(2);
             uint2 own_left = own_se;
-            if (!seeded0 && nn.slot < 0 && a.nbr) {  // no warm start: the own cell's best becomes the candidate
+            if (!exact && nn.slot < 0 && a.nbr) {  // no warm start: the own cell's best becomes the candidate
                 nn_cold_start(a, sIdx, qc, own_se, qx, qy, qz, nn);
                 own_left = make_uint2(0u, 0u);
             }
-            bool exact = seeded0 || (nn.slot >= 0 && a.nbr && graph_nn(a, qx, qy, qz, nn));
-            if (!exact) exact = nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn, true);
+            path_code = exact ? (seeded0 ? 4 : 0) : 1;
+            if (!exact && nn.slot >= 0 && a.nbr) {
+                exact = graph_nn(a, qx, qy, qz, nn, d2lb);
+                dbg_graph |= (exact ? 1 : 0) << (it & 31);
+                path_code = exact ? 1 : 2;
+            }
+            // after iteration 0 a point the graph cannot certify goes straight to the block queue:
+            // the warp path also bounds its second neighbour, so the next iterations can reuse
+            if (!exact && (it == 0 || !a.nbr)) {
+                exact = nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn, true);
+                path_code = exact ? 2 : 3;
+            }
+            if (!exact) path_code = 3;
+            qp0 = qx;
+            qp1 = qy;
+            qp2 = qz;
             if (sub) a.timeline[sub_base + 4] = nn.best == kEmptyKey ? 1 : 0;
             sub_stamp(3);
             if (!exact) {  // hand over to the block's warps (warp_nn below)
@@ -801,11 +897,27 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
                 sQslot[k] = nn.slot;
                 sQp[k] = nn.p;
             }
-            dbg_slow += nn.slow;
-            dbg_probes += nn.probes;
-            dbg_cands += nn.cands;
+            dbg_slow |= (exact ? 0 : 1) << (it & 31);
             ++dbg_its;
             m0 = nn;
+        }
+        if (a.timeline && blockIdx.x == 0) {  // diagnostic: slowest lane of each warp of block 0
+            long long d = has0 ? clock64() - lane_t0 : 0;
+            int code = path_code;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const long long od = __shfl_xor_sync(0xffffffffu, d, o);
+                const int oc = __shfl_xor_sync(0xffffffffu, code, o);
+                if (od > d) {
+                    d = od;
+                    code = oc;
+                }
+            }
+            const long long wb = 1 + (long long)a.max_iters * (G + 17) + ((long long)it * kWarps + warp) * 2;
+            if (lane == 0 && wb + 1 < a.timeline_cap) {
+                a.timeline[wb] = d;
+                a.timeline[wb + 1] = code;
+            }
         }
         // queries whose fast path failed: one warp each, all lanes cooperating
         __syncthreads();
@@ -816,10 +928,22 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             nn.slot = sQslot[k];
             nn.p = sQp[k];
             warp_nn(a, sIdx, sBox, qq.x, qq.y, qq.z, nn, lane);
+            // a lower bound on every other target's distance (exact within rho), so that the
+            // following iterations can keep this answer while the query moves little
+            const bool in_r = nn.slot >= 0 && ki_key(nn.best) < a.r2;
+            const float base = in_r ? sqrtf(ki_key(nn.best)) : a.r;
+            float d2 = 0.f;
+            if (base < INFINITY) {
+                const float rho = base * 1.25f + 0.25f * a.h;
+                NN n2;
+                warp_nn(a, sIdx, sBox, qq.x, qq.y, qq.z, n2, lane, rho * rho, nn.slot);
+                d2 = fminf(n2.best != kEmptyKey ? sqrtf(ki_key(n2.best)) : INFINITY, rho) * (1.f - kReuseMargin);
+            }
             if (lane == 0) {
                 sQbest[k] = nn.best;
                 sQslot[k] = nn.slot;
                 sQp[k] = nn.p;
+                sQd2[k] = d2;
             }
         }
         __syncthreads();
@@ -829,6 +953,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
                     m0.best = sQbest[k];
                     m0.slot = sQslot[k];
                     m0.p = sQp[k];
+                    d2lb = sQd2[k];
                 }
             valid0 = m0.slot >= 0 && ki_key(m0.best) < a.r2;
         }
@@ -960,7 +1085,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         stamp(5);
         if (sDone) break;
     }
-    if (a.debug && has0) a.debug[i0] = make_int4(dbg_slow, dbg_probes, dbg_cands, dbg_its);
+    if (a.debug && has0) a.debug[i0] = make_int4(dbg_slow, dbg_reuse, dbg_graph, dbg_its);
     if (blockIdx.x == 0 && tid == 0) {
         if (!a.linearize_only) {
             for (int k = 0; k < 12; ++k) a.d_T[k] = sT[k];

@@ -34,7 +34,8 @@ constexpr int kKnnThreads = 128;
 constexpr int kQueriesPerWarp = 8;  // queries a warp searches one after the other
 constexpr int kMergeThreshold = 4;  // more passing candidates than this: sort-merge the batch
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kKnnBatch = 4;  // hash probes in flight per thread (thread variant)
+constexpr int kKnnBatch = 4;
+constexpr int kMaxK = 32;  // hash probes in flight per thread (thread variant)
 
 struct KnnArgs {
     GridView g;
@@ -46,7 +47,7 @@ struct KnnArgs {
     float4 *cov_a, *cov_b;
     int32_t *knn_idx;
     int4 *debug;
-    double *moments;  // [cap][10]: sum d (3), sum d d^T (6), count — per query in search order
+    int32_t *nbr_t;   // [cap][kMaxK]: the k neighbours (input indices, sorted, -1 pad) per query in search order
 };
 
 __device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int src) {
@@ -76,27 +77,60 @@ struct WarpTopK {
     __device__ __forceinline__ bool full() const { return worst != kEmptyKey; }
     // insert the candidates of all lanes (cand = kEmptyKey for none): a few by ballot + shuffle,
     // many by a warp bitonic sort of the batch merged into the list (fixed ~40 shuffles)
-    __device__ __forceinline__ void insert_all(unsigned long long cand, int lane) {
+    // bitonic sort (ascending) of the values of lanes [0, W) (other lanes: don't care)
+    template <int W>
+    __device__ __forceinline__ static unsigned long long sort_w(unsigned long long c, int lane) {
+#pragma unroll
+        for (int k = 2; k <= W; k <<= 1)
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const unsigned long long o = shfl_xor_u64(c, j);
+                const bool up = ((lane & k) == 0) == ((lane & j) == 0);  // keep the min here?
+                c = up ? (o < c ? o : c) : (o > c ? o : c);
+            }
+        return c;
+    }
+    // bitonic merge of a bitonic 32-sequence to ascending
+    __device__ __forceinline__ static unsigned long long merge32(unsigned long long m, int lane) {
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) {
+            const unsigned long long o = shfl_xor_u64(m, j);
+            m = ((lane & j) == 0) ? (o < m ? o : m) : (o > m ? o : m);
+        }
+        return m;
+    }
+    __device__ __forceinline__ void insert_all(unsigned long long cand, int lane, unsigned long long *wbuf) {
         unsigned pass = __ballot_sync(kFull, cand < worst);
-        if (__popc(pass) > kMergeThreshold) {
-            inserts += __popc(pass);
+        const int np = __popc(pass);
+        if (np > kMergeThreshold && np <= 8 && K <= 24) {
+            // few: compact the passing candidates to lanes 0..np-1 (warp scratch), sort those 8,
+            // place them descending in lanes 24..31 after the ascending list (a bitonic sequence)
+            // and merge — 6 + 5 shuffle stages instead of 15 + 5
+            inserts += np;
+            if (cand < worst) wbuf[__popc(pass & ((1u << lane) - 1u))] = cand;
+            __syncwarp();
+            unsigned long long c = lane < np ? wbuf[lane] : kEmptyKey;
+            __syncwarp();
+            c = sort_w<8>(c, lane);
+            const unsigned long long rev = shfl_u64(c, (31 - lane) & 7);
+            const unsigned long long m = merge32(lane < K ? L : (lane >= 24 ? rev : kEmptyKey), lane);
+            L = lane < K ? m : kEmptyKey;
+            worst = shfl_u64(L, K - 1);
+            return;
+        }
+        if (np > kMergeThreshold) {
+            inserts += np;
             unsigned long long c = cand < worst ? cand : kEmptyKey;
-#pragma unroll
-            for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-                for (int j = k >> 1; j > 0; j >>= 1) {
-                    const unsigned long long o = shfl_xor_u64(c, j);
-                    const bool up = ((lane & k) == 0) == ((lane & j) == 0);  // keep the min here?
-                    c = up ? (o < c ? o : c) : (o > c ? o : c);
-                }
+            c = sort_w<32>(c, lane);
+            if (shfl_u64(L, 0) == kEmptyKey) {  // empty list: the sorted batch is the list
+                L = lane < K ? c : kEmptyKey;
+                worst = shfl_u64(L, K - 1);
+                return;
+            }
             // list ascending (lanes >= K empty) vs batch descending: lane-wise min = the 32 smallest
             const unsigned long long rev = shfl_u64(c, 31 - lane);
             unsigned long long m = L < rev ? L : rev;
-#pragma unroll
-            for (int j = 16; j > 0; j >>= 1) {  // bitonic merge to ascending
-                const unsigned long long o = shfl_xor_u64(m, j);
-                m = ((lane & j) == 0) ? (o < m ? o : m) : (o > m ? o : m);
-            }
+            m = merge32(m, lane);
             L = lane < K ? m : kEmptyKey;
             worst = shfl_u64(L, K - 1);
             return;
@@ -123,7 +157,7 @@ struct Counters {
 // range, 32 candidates per round, inserting into the list.
 template <int K>
 __device__ __forceinline__ void scan_cells(const GridView &g, bool valid, unsigned long long key, float qx, float qy,
-                                           float qz, WarpTopK<K> &T, Counters &cn, int lane) {
+                                           float qz, WarpTopK<K> &T, Counters &cn, int lane, unsigned long long *wbuf) {
     uint2 se = valid ? cell_lookup(g.table, g.mask, key) : make_uint2(0u, 0u);
     cn.probes += __popc(__ballot_sync(kFull, valid));
     // inclusive scan of the counts
@@ -153,7 +187,7 @@ __device__ __forceinline__ void scan_cells(const GridView &g, bool valid, unsign
             const float4 p = __ldg(g.spos + c_start + (item - (c_incl - c_cnt)));
             cand = pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
         }
-        T.insert_all(cand, lane);
+        T.insert_all(cand, lane, wbuf);
     }
 }
 
@@ -161,7 +195,7 @@ __device__ __forceinline__ void scan_cells(const GridView &g, bool valid, unsign
 // the list and a coarser level exists.
 template <int K>
 __device__ bool knn_search_warp(const GridView &g, int level, float qx, float qy, float qz, WarpTopK<K> &T,
-                                Counters &cn, int lane) {
+                                Counters &cn, int lane, unsigned long long *wbuf) {
     T.reset();
     const float inv_h = ldexpf(g.inv_h0, -level);
     const QueryCell qc(qx, qy, qz, ldexpf(g.h0, level), inv_h);
@@ -188,7 +222,7 @@ __device__ bool knn_search_warp(const GridView &g, int level, float qx, float qy
                 valid = !(lb > ki_key(T.worst));
             }
             if (!__any_sync(kFull, valid)) continue;
-            scan_cells<K>(g, valid, cell_key(level, x, y, z), qx, qy, qz, T, cn, lane);
+            scan_cells<K>(g, valid, cell_key(level, x, y, z), qx, qy, qz, T, cn, lane, wbuf);
         }
         const int mm = m == 0 ? 1 : m;  // shells 0..mm are complete
         if (T.full() && ki_key(T.worst) < qc.certified_key(mm)) return true;
@@ -202,6 +236,8 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_search(KnnArgs a) {
     const int n = *a.d_n;
     const GridView &g = a.g;
     const int lane = threadIdx.x & 31;
+    __shared__ unsigned long long sBuf[kKnnThreads];
+    unsigned long long *wbuf = sBuf + (threadIdx.x & ~31);
     const int wbase = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kQueriesPerWarp;  // first query of this warp
     if (wbase >= n) return;
     const int tq = wbase + lane;
@@ -227,30 +263,12 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_search(KnnArgs a) {
         WarpTopK<K> T;
         T.inserts = 0;
         Counters cn;
-        while (!knn_search_warp<K>(g, level, qx, qy, qz, T, cn, lane)) ++level;
+        while (!knn_search_warp<K>(g, level, qx, qy, qz, T, cn, lane, wbuf)) ++level;
         if (a.debug && lane == 0) a.debug[i] = make_int4(level, cn.probes, cn.cands, T.inserts);
         // moments over the k nearest: lane j < k holds neighbour j (sorted by (key, index))
         const bool have = lane < a.k && T.L != kEmptyKey;
         if (a.knn_idx && lane < a.k) a.knn_idx[(size_t)i * a.k + lane] = have ? (int32_t)ki_idx(T.L) : -1;
-        if (!a.moments) continue;  // neighbour lists only (target kNN graph)
-        double d[3] = {0, 0, 0};
-        if (have) {
-            const float4 p = __ldg(a.pos + ki_idx(T.L));
-            d[0] = (double)p.x - (double)qx;
-            d[1] = (double)p.y - (double)qy;
-            d[2] = (double)p.z - (double)qz;
-        }
-        double v[9] = {d[0], d[1], d[2], d[0] * d[0], d[0] * d[1], d[0] * d[2], d[1] * d[1], d[1] * d[2], d[2] * d[2]};
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int c = 0; c < 9; ++c) v[c] += __shfl_xor_sync(kFull, v[c], o);
-        const int c_have = __popc(__ballot_sync(kFull, have));
-        // moments record of query (wbase + qi): lane c < 9 stores sum c, lane 9 the count
-        double mine = (double)c_have;
-#pragma unroll
-        for (int c = 0; c < 9; ++c) mine = lane == c ? v[c] : mine;
-        if (lane < 10) a.moments[(size_t)(wbase + qi) * 10 + lane] = mine;
+        if (a.nbr_t && lane < a.k) a.nbr_t[(size_t)(wbase + qi) * kMaxK + lane] = have ? (int32_t)ki_idx(T.L) : -1;
     }
 }
 
@@ -412,27 +430,10 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_thread(KnnArgs a) {
         for (int j = 0; j < K; ++j)
             if (j < a.k) a.knn_idx[(size_t)i * a.k + j] = T.L[j] == kEmptyKey ? -1 : (int32_t)ki_idx(T.L[j]);
     }
-    if (!a.moments) return;
-    double v[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (!a.nbr_t) return;
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-        if (j >= a.k || T.L[j] == kEmptyKey) continue;
-        const float4 p = __ldg(a.pos + ki_idx(T.L[j]));
-        const double d0 = (double)p.x - (double)qx, d1 = (double)p.y - (double)qy, d2 = (double)p.z - (double)qz;
-        v[0] += d0;
-        v[1] += d1;
-        v[2] += d2;
-        v[3] += d0 * d0;
-        v[4] += d0 * d1;
-        v[5] += d0 * d2;
-        v[6] += d1 * d1;
-        v[7] += d1 * d2;
-        v[8] += d2 * d2;
-        v[9] += 1.0;
-    }
-    double *mr = a.moments + (size_t)t * 10;
-#pragma unroll
-    for (int c = 0; c < 10; ++c) mr[c] = v[c];
+    for (int j = 0; j < K; ++j)
+        if (j < a.k) a.nbr_t[(size_t)t * kMaxK + j] = T.L[j] == kEmptyKey ? -1 : (int32_t)ki_idx(T.L[j]);
 }
 
 // per-query epilogue (thread per query): covariance (normalised by the count), eigen,
@@ -443,10 +444,31 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_epilogue(KnnArgs a) {
     if (t >= n) return;
     const GridView &g = a.g;
     const int i = __float_as_int(__ldg(g.spos + (size_t)(g.levels - 1) * g.cap + t).w);
-    const double *mr = a.moments + (size_t)t * 10;
-    const double s1[3] = {mr[0], mr[1], mr[2]};
-    const double s2[6] = {mr[3], mr[4], mr[5], mr[6], mr[7], mr[8]};
-    const int cnt = (int)mr[9];
+    const float4 q = __ldg(a.pos + i);
+    // moments of the k neighbours about the query (binary64), in list order
+    const int4 *lst = reinterpret_cast<const int4 *>(a.nbr_t + (size_t)t * kMaxK);
+    double s1[3] = {0, 0, 0}, s2[6] = {0, 0, 0, 0, 0, 0};
+    int cnt = 0;
+    for (int j4 = 0; j4 < (a.k + 3) / 4; ++j4) {
+        const int4 w = __ldg(lst + j4);
+        const int ids[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (4 * j4 + u >= a.k || ids[u] < 0) continue;
+            const float4 p = __ldg(a.pos + ids[u]);
+            const double d0 = (double)p.x - (double)q.x, d1 = (double)p.y - (double)q.y, d2 = (double)p.z - (double)q.z;
+            s1[0] += d0;
+            s1[1] += d1;
+            s1[2] += d2;
+            s2[0] += d0 * d0;
+            s2[1] += d0 * d1;
+            s2[2] += d0 * d2;
+            s2[3] += d1 * d1;
+            s2[4] += d1 * d2;
+            s2[5] += d2 * d2;
+            ++cnt;
+        }
+    }
     const double inv = 1.0 / (double)cnt;
     const double mu[3] = {s1[0] * inv, s1[1] * inv, s1[2] * inv};
     double C[6] = {s2[0] * inv - mu[0] * mu[0], s2[1] * inv - mu[0] * mu[1], s2[2] * inv - mu[0] * mu[2],
@@ -493,7 +515,7 @@ cudaError_t launch_k(const KnnArgs &a, int cap, cudaStream_t s) {
 }  // namespace
 
 size_t covariances_ws_bytes(int cap, int levels) {
-    return grid_bytes(cap, levels, false) + align_up((size_t)cap * 10 * sizeof(double));
+    return grid_bytes(cap, levels, false) + align_up((size_t)cap * kMaxK * sizeof(int32_t));
 }
 
 cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, int k, int mode, float eps,
@@ -510,7 +532,7 @@ cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, in
     a.cov_b = reinterpret_cast<float4 *>(cov_b);
     a.knn_idx = knn_idx;
     a.debug = reinterpret_cast<int4 *>(g_knn_debug);
-    a.moments = reinterpret_cast<double *>(static_cast<char *>(ws) + grid_bytes(cap, levels, false));
+    a.nbr_t = reinterpret_cast<int32_t *>(static_cast<char *>(ws) + grid_bytes(cap, levels, false));
     cudaError_t e = grid_build(a.g, a.pos, nullptr, nullptr, d_n, cap, s);
     if (e != cudaSuccess) return e;
     if (k <= 4) return launch_k<4>(a, cap, s);
@@ -532,7 +554,7 @@ cudaError_t knn_graph_launch(const GridView &g, const float4 *pos, const int32_t
     a.d_n = d_n;
     a.k = kGraphK;
     a.knn_idx = knn_idx;
-    a.moments = nullptr;
+    a.nbr_t = nullptr;
     a.debug = nullptr;
     cudaError_t e = launch_search<kGraphK>(a, cap, s);
     if (e != cudaSuccess) return e;

@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // A5  Map Gaussians -> G-ICP target Gaussians (the map already holds
 // Gaussians, so G-ICP "does not need to compute the covariances of the map"
 // C = R Lambda^2 R^T).  Per Gaussian: normalised wxyz quaternion -> R (R22), scales (exp if
@@ -220,6 +221,18 @@ static void fill_target(const GridView &g, const TargetWs &t, int M, gsicp_targe
     out->M = M;
 }
 
+// auto cell = mult x mean middle scale (a cost knob only; results are exact at any cell size).
+// GSICP_CELL_MULT overrides the multiplier (tuning experiments).
+static double auto_cell_mult() {
+    static double m = -1.0;
+    if (m < 0.0) {
+        const char *e = getenv("GSICP_CELL_MULT");
+        m = e ? atof(e) : 3.0;
+        if (!(m > 0.0)) m = 3.0;
+    }
+    return m;
+}
+
 cudaError_t build_target_launch(const float *means, const float *quats, const float *scales, int scales_are_log,
                                 int M, int mode, float eps, float cell, gsicp_target *out, void *ws,
                                 cudaStream_t s) {
@@ -247,7 +260,7 @@ cudaError_t build_target_launch(const float *means, const float *quats, const fl
             set_error("build_target auto cell: %s", cudaGetErrorString(e));
             return e;
         }
-        cell = (float)(3.0 * sum / (double)M);
+        cell = (float)(auto_cell_mult() * sum / (double)M);
         if (!(cell > 0.f)) cell = 0.01f;
     }
     GridView g = grid_carve(t.grid, M, 1, true, cell);

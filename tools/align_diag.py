@@ -34,12 +34,16 @@ def main():
         g.debug_align_counters(cnt)
         T, st = g.align(tr.cloud, tgt, w.T_init, tr.params, tr.ws_align)
         g.debug_align_counters(None)
-        c = cnt[:tr.cloud.n()].cpu().numpy().astype(np.float64)
-        its = np.maximum(c[:, 3], 1)
-        for j, nm in enumerate(["slow", "probes", "cands"]):
-            v = c[:, j] / its
-            print(f"  per point-iteration {nm:6s}: mean {v.mean():7.2f} p50 {np.percentile(v, 50):7.2f} "
-                  f"p99 {np.percentile(v, 99):7.2f} max {v.max():7.2f}   (sum over iters: mean {c[:, j].mean():.1f})")
+        c = cnt[:tr.cloud.n()].cpu().numpy().astype(np.int64) & 0xffffffff
+        n_it = int(c[:, 3].max())
+        Gb = int(np.ceil(c.shape[0] / 384))
+        for it in range(n_it):
+            bit = 1 << it
+            q, r, gr = ((c[:, k] & bit) != 0 for k in range(3))
+            fast = ~(q | r | gr)
+            pb = lambda m: np.bincount(np.arange(len(m))[m] // 384, minlength=Gb)
+            print(f"  it {it}: queued {q.mean():.4f} reuse {r.mean():.4f} graph {gr.mean():.4f} other {fast.mean():.4f} | "
+                  f"per block max: queued {pb(q).max()} graph {pb(gr).max()} other {pb(fast).max()}")
         tl.zero_()
         g.debug_align_timeline(tl)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -73,6 +77,11 @@ def main():
             c = t[sb:sb + 8]
             print(f"      warp0 cycles: k3+own={c[1] - c[0]} warm={c[2] - c[1]} search={c[3] - c[2]} "
                   f"rest={c[5] - c[3]} empty_best={c[4]} | B start->{c[6] - c[5]} pair={c[7] - c[6]}")
+            wb = 1 + max_iters * (Gn + 17) + it * 12 * 2
+            wl = t[wb:wb + 24].reshape(12, 2)
+            names_p = ["reuse", "graph", "fast", "queued", "seeded"]
+            print("      block0 warps: slowest lane cycles (path) " +
+                  " ".join(f"{int(c)}({names_p[int(k)] if 0 <= k < 5 else '?'})" for c, k in wl))
             prev = pas
 
 

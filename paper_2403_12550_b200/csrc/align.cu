@@ -69,6 +69,8 @@ struct AlignArgs {
     int32_t *seed_slot;       // [cap] iteration-0 matches from k_align_seed (target slot or -1)
     double *seed_hdr;         // [16]: pose the seeds were computed at (12), ticket at [12]
     double seed_ticket;       // k_align_seed: ticket to write; k_align: ticket expected (0: none)
+    int32_t *seed_queue;      // [cap] hard queries of the seed pass
+    int32_t *seed_qn;         // [1] their count
 };
 
 __device__ __forceinline__ long long globaltimer_ns() {
@@ -687,26 +689,17 @@ __device__ __forceinline__ void load_cell_index(const AlignArgs &a, CellIndex &i
 // (cold start, certified graph descent, fast path, block queue solved by whole warps).  It needs
 // only the source positions, so it can run concurrently with the source covariances (A2-A4).
 constexpr int kSeedT = 256;
+constexpr int kSeedHardT = 128;
 __global__ void __launch_bounds__(kSeedT) k_align_seed(AlignArgs a) {
     __shared__ double sT[12];
     __shared__ int sBox[6];
     __shared__ CellIndex sIdx;
-    __shared__ int sQn;
-    __shared__ float4 sQq[kSeedT];
-    __shared__ unsigned long long sQbest[kSeedT];
-    __shared__ int sQslot[kSeedT];
-    __shared__ float4 sQp[kSeedT];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const int n = *a.d_n;
     if (tid < 12) sT[tid] = a.d_T[tid];
-    if (tid == 0) {
-        load_cell_index(a, sIdx, sBox);
-        sQn = 0;
-    }
+    if (tid == 0) load_cell_index(a, sIdx, sBox);
     __syncthreads();
     const int i = blockIdx.x * kSeedT + tid;
-    NN nn;
-    int myk = -1;
     if (i < n) {
         const float4 x = __ldg(a.spos + i);
         double q0, q1, q2;
@@ -714,36 +707,52 @@ __global__ void __launch_bounds__(kSeedT) k_align_seed(AlignArgs a) {
         const float qx = __double2float_rn(q0), qy = __double2float_rn(q1), qz = __double2float_rn(q2);
         const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
         const uint2 own = sIdx.one(qc.c[0], qc.c[1], qc.c[2]);
+        NN nn;
         uint2 own_left = own;
         if (a.nbr) {
             nn_cold_start(a, sIdx, qc, own, qx, qy, qz, nn);
             own_left = make_uint2(0u, 0u);
         }
         float d2 = 0.f;
+        // per thread only the cheap certified case (own cell, then the graph); everything else
+        // goes to the warp-cooperative pass (no divergent per-thread grid walks here)
         bool exact = nn.slot >= 0 && a.nbr && graph_nn(a, qx, qy, qz, nn, d2);
-        if (!exact) exact = nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn, true);
-        if (!exact) {
-            myk = atomicAdd(&sQn, 1);
-            sQq[myk] = make_float4(qx, qy, qz, 0.f);
-            sQbest[myk] = nn.best;
-            sQslot[myk] = nn.slot;
-            sQp[myk] = nn.p;
-        }
+        if (!exact && !a.nbr) exact = nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn, true);
+        a.seed_slot[i] = nn.slot;  // exact, or the best seen (an upper bound for the hard pass)
+        if (!exact) a.seed_queue[atomicAdd(a.seed_qn, 1)] = i;
     }
-    __syncthreads();
-    for (int k = warp; k < sQn; k += kSeedT / 32) {
-        const float4 qq = sQq[k];
-        NN w;
-        w.best = sQbest[k];
-        w.slot = sQslot[k];
-        w.p = sQp[k];
-        warp_nn(a, sIdx, sBox, qq.x, qq.y, qq.z, w, lane);
-        if (lane == 0) sQslot[k] = w.slot;
-    }
-    __syncthreads();
-    if (i < n) a.seed_slot[i] = myk >= 0 ? sQslot[myk] : nn.slot;
     if (blockIdx.x == 0 && tid < 12) a.seed_hdr[tid] = sT[tid];
     if (blockIdx.x == 0 && tid == 12) a.seed_hdr[12] = a.seed_ticket;
+}
+
+// The hard queries of the seed pass, spread over the whole GPU: each warp takes queue entries
+// (one query each) and runs the warp-cooperative exact search from the best seen so far.
+__global__ void __launch_bounds__(kSeedHardT) k_align_seed_hard(AlignArgs a) {
+    __shared__ double sT[12];
+    __shared__ int sBox[6];
+    __shared__ CellIndex sIdx;
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid < 12) sT[tid] = a.d_T[tid];
+    if (tid == 0) load_cell_index(a, sIdx, sBox);
+    __syncthreads();
+    const int qn = *a.seed_qn;
+    const int warps = gridDim.x * (kSeedHardT / 32);
+    for (int k = blockIdx.x * (kSeedHardT / 32) + (tid >> 5); k < qn; k += warps) {
+        const int i = a.seed_queue[k];
+        const float4 x = __ldg(a.spos + i);
+        double q0, q1, q2;
+        k3(sT, x.x, x.y, x.z, q0, q1, q2);
+        const float qx = __double2float_rn(q0), qy = __double2float_rn(q1), qz = __double2float_rn(q2);
+        NN nn;
+        const int sl = a.seed_slot[i];
+        if (sl >= 0) {
+            nn.slot = sl;
+            nn.p = __ldg(a.tpos + sl);
+            nn.best = pack_ki(canon_key(qx, qy, qz, nn.p.x, nn.p.y, nn.p.z), (uint32_t)__float_as_int(nn.p.w));
+        }
+        warp_nn(a, sIdx, sBox, qx, qy, qz, nn, lane);
+        if (lane == 0) a.seed_slot[i] = nn.slot;
+    }
 }
 
 __global__ void k_align_init(int32_t *corr_ws, int cap, unsigned int *barrier) {
@@ -1127,6 +1136,8 @@ struct AlignWs {
     int32_t *corr_ws;
     int32_t *seed_slot;
     double *seed_hdr;
+    int32_t *seed_queue;
+    int32_t *seed_qn;
 };
 
 static AlignWs align_carve(Carver &c, int cap) {
@@ -1140,6 +1151,8 @@ static AlignWs align_carve(Carver &c, int cap) {
     w.corr_ws = c.take<int32_t>(cap);
     w.seed_slot = c.take<int32_t>(cap);
     w.seed_hdr = c.take<double>(16);
+    w.seed_queue = c.take<int32_t>(cap);
+    w.seed_qn = c.take<int32_t>(4);
     return w;
 }
 static AlignWs align_carve(void *base, int cap) {
@@ -1199,6 +1212,8 @@ static AlignArgs make_args(const gsicp_cloud &src, const gsicp_target &tgt, doub
     a.seed_slot = w.seed_slot;
     a.seed_hdr = w.seed_hdr;
     a.seed_ticket = 0.0;
+    a.seed_queue = w.seed_queue;
+    a.seed_qn = w.seed_qn;
     return a;
 }
 
@@ -1220,9 +1235,16 @@ cudaError_t align_seed_launch(const gsicp_cloud &src, const gsicp_target &tgt, c
     g_seed_src = src.pos;
     g_seed_tgt = tgt.pos;
     g_seed_ticket = a.seed_ticket;
+    cudaError_t e = cudaMemsetAsync(w.seed_qn, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) {
+        set_error("align_seed memset: %s", cudaGetErrorString(e));
+        return e;
+    }
     k_align_seed<<<blocks_for(src.cap > 0 ? src.cap : 1, kSeedT), kSeedT, 0, s>>>(a);
     GSICP_LAUNCH_CHECK("k_align_seed");
-    note_launch();
+    k_align_seed_hard<<<num_sms() * 8, kSeedHardT, 0, s>>>(a);
+    GSICP_LAUNCH_CHECK("k_align_seed_hard");
+    note_launch(2);
     return cudaSuccess;
 }
 

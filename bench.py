@@ -31,7 +31,8 @@ import numpy as np  # noqa: E402
 METRIC = "G-ICP aligns/sec (Replica frame vs 1M-Gaussian map); kNN-cov Mpts/s; HBM %"
 WORKLOAD = "Replica-shaped 1200x680 depth frame, stride 4 (<=51k pts), vs 1e6-Gaussian map (C2 geometry, 1M map)"
 ALGO_BYTES_ALIGN = 96 + 8   # per (source point x GN iteration): src pos+cov, tgt pos+cov, corr
-ALGO_BYTES_KNN = 16 + 32    # per query: pos in, cov out
+ALGO_BYTES_KNN = 16 + 32    # per query of the kNN-cov stage: pos in, cov out
+ALGO_BYTES_KNN_SEARCH = 16 + 4 * 20  # per query of k_knn_search: query record in, 20 neighbour ids out
 C4_CELL, C4_LEVELS = 3.0, 3  # map kNN-cov grid: finest cell 3 x map spacing, 3 levels (outliers go coarse)
 
 
@@ -222,8 +223,8 @@ def bench_gpu(args):
 
     def step(evs=None):
         tr.d_T.copy_(T0)
-        # A1 | A2-A4 (+ iteration-0 correspondences on a side stream) | A6-A9, events on `stream`
-        tr.step_async(depth, tgt, stream, evs)
+        # A1 | A2-A4 (+ iteration-0 correspondences on a side stream) | A6-A9 on the current stream
+        tr.step_async(depth, tgt, torch.cuda.current_stream(dev), evs)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -231,23 +232,53 @@ def bench_gpu(args):
     n_src = tr.cloud.n()
     st = g.decode_stats(tr.d_stats)
     nev = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nev)]
+
+    # per-stage split from an eager pass (informational; events on `stream`)
+    n_stage = min(nev, 20)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n_stage)]
+    for i in range(n_stage):
+        flush.zero_()
+        step(evs[i])
+    torch.cuda.synchronize()
+    stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(3)] for i in range(n_stage)])
+
+    # the timed step: the whole frame replayed from one CUDA graph (captured once; the kernel
+    # timer's event pairs around k_knn_search / k_align / the seed pass are part of the graph)
+    cap_stream = torch.cuda.Stream(dev)
+    g.debug_kernel_timer(True)
+    step()  # creates the timer events outside the capture
+    torch.cuda.synchronize()
+    l0 = g.launch_count()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=cap_stream):
+        step()
+    launches_per_step = g.launch_count() - l0
+    g.debug_kernel_timer(False)
+    for _ in range(max(args.warmup, 3)):
+        graph.replay()
+    torch.cuda.synchronize()
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
+    kt = {k: [] for k in (g.KT_KNN_SEARCH, g.KT_ALIGN, g.KT_SEED)}
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    l0 = g.launch_count()
     with ClockSampler(local) as clk:
         for i in range(nev):
             flush.zero_()  # L2 flush (256 MB > 126 MB L2), outside the timed events
-            step(evs[i])
-        torch.cuda.synchronize()
-    launches = g.launch_count() - l0
+            e0[i].record(stream)
+            graph.replay()
+            e1[i].record(stream)
+            torch.cuda.synchronize()  # per-step kernel timer readout (host side, outside the events)
+            for k in kt:
+                kt[k].append(g.debug_kernel_time(k))
     if dist:
         dist.barrier()
-    stage = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(3)] for i in range(nev)])
-    step_ms = stage.sum(1)
+    step_ms = np.array([e0[i].elapsed_time(e1[i]) for i in range(nev)])
     total_ms = max_over_ranks(float(step_ms.sum()), dist, dev)
     value = job_throughput(nev, ws, total_ms)
+    launches = launches_per_step * nev
+    st = g.decode_stats(tr.d_stats)
 
     # e2e through the public API with host buffers: H2D depth (pinned), whole frame, D2H pose
     T_init = w.T_init
@@ -295,26 +326,22 @@ def bench_gpu(args):
             dist.destroy_process_group()
         return 0
     hbm, _, peak_kind = peaks()
-    st = g.decode_stats(tr.d_stats)
     iters = max(1, st["iters"])
     mean_stage = stage.mean(0)
-    names = ["A1 backproject", "A2-A4 hash+kNN-cov", "A6-A9 align (init+persistent GN kernel)"]
-    dom = int(np.argmax(mean_stage))
-    if dom == 2:
-        algo = ALGO_BYTES_ALIGN * n_src * iters
-        kernel = "k_align (+k_align_init)"
-    elif dom == 1:
-        algo = ALGO_BYTES_KNN * n_src
-        kernel = "k_knn_search (+grid build, k_knn_epilogue)"
-    else:
-        algo = 4 * K.H * K.W / (w.stride ** 2) + 16 * n_src
-        kernel = "k_bp_count + k_bp_emit"
-    achieved = algo / (mean_stage[dom] / 1000.0) / 1e9
+    names = ["A1 backproject", "A2-A4 hash+kNN-cov (+seed pass on a side stream)",
+             "A6-A9 align (init+persistent GN kernel)"]
+    # dominant kernel of the step, timed live (kernel timer events inside the replayed graph)
+    kms = {k: float(np.mean([x for x in v if x is not None])) if any(x is not None for x in v) else None
+           for k, v in kt.items()}
+    cand = {"k_knn_search": (kms[g.KT_KNN_SEARCH], ALGO_BYTES_KNN_SEARCH * n_src),
+            "k_align": (kms[g.KT_ALIGN], ALGO_BYTES_ALIGN * n_src * iters)}
+    kernel = max((k for k in cand if cand[k][0] is not None), key=lambda k: cand[k][0])
+    kernel_ms, algo = cand[kernel]
+    achieved = algo / (kernel_ms / 1000.0) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
-        tj = json.load(open(prof))
-        traffic = tj.get(kernel.split()[0])
+        traffic = json.load(open(prof)).get(kernel)
     line = {
         "metric": METRIC, "value": value, "unit": "aligns/s", "n_gpus": ws, "steps": nev, "warmup": args.warmup,
         "ms_per_step": total_ms / nev, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -322,10 +349,13 @@ def bench_gpu(args):
         "config": {"workload": WORKLOAD, "n_src": n_src, "map_gaussians": tgt.M, "k": 20, "mode": "ellipse",
                    "max_iters": 30, "gn_iters_used": st["iters"], "max_corr_dist": 0.1, "parallelism": f"replicas{ws}",
                    "l2": "flushed between timed steps (256 MB write)"},
-        "stage_ms": {names[j]: float(mean_stage[j]) for j in range(3)},
+        "timing": "CUDA graph replay of the whole frame, CUDA events per step on the launch stream",
+        "stage_ms_eager": {names[j]: float(mean_stage[j]) for j in range(3)},
+        "kernel_ms": {"k_knn_search": kms[g.KT_KNN_SEARCH], "k_align": kms[g.KT_ALIGN],
+                      "seed pass (k_align_seed + k_align_seed_hard, side stream)": kms[g.KT_SEED]},
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                     "algo_bytes_per_launch": algo},
+                     "algo_bytes_per_launch": algo, "kernel_ms": kernel_ms},
         "e2e": {"value": e2e_value, "unit": "aligns/s", "h2d_bytes_per_step": int(depth_host.numel() * 4),
                 "d2h_bytes_per_step": 16 * 8 + 32},
         "gpu_launches": int(launches),

@@ -215,6 +215,15 @@ void gsicp_debug_align_timeline(int64_t *d_out, int64_t capacity);
  * summed over the GN iterations (int32, device, >= 4*cap entries).  NULL switches it off. */
 void gsicp_debug_align_counters(int32_t *d_out);
 
+/* DIAGNOSTIC: kernel timer.  While enabled (non-zero) on the calling thread, the launches of
+ * the hot kernels record a CUDA event pair around themselves on their stream (also inside a
+ * stream capture: the events then record at every graph replay).  gsicp_debug_kernel_time
+ * returns 1 and the elapsed ms of the LAST recorded launch of `kernel` (0 = k_knn_search of
+ * gsicp_covariances, 1 = k_align of the align calls, 2 = the two seed kernels of
+ * gsicp_align_seed); the caller synchronises first.  Returns 0 if none was recorded. */
+void gsicp_debug_kernel_timer(int enable);
+int gsicp_debug_kernel_time(int kernel, float *ms);
+
 /* Misc */
 const char *gsicp_status_string(gsicp_status s);
 const char *gsicp_last_error(void);         /* thread-local detail of the last error           */

@@ -104,6 +104,10 @@ def lib():
         L.gsicp_debug_align_timeline.restype = None
         L.gsicp_debug_align_counters.argtypes = [P]
         L.gsicp_debug_align_counters.restype = None
+        L.gsicp_debug_kernel_timer.argtypes = [i32]
+        L.gsicp_debug_kernel_timer.restype = None
+        L.gsicp_debug_kernel_time.argtypes = [i32, C.POINTER(C.c_float)]
+        L.gsicp_debug_kernel_time.restype = i32
         for name in ("gsicp_backproject_downsample", "gsicp_covariances", "gsicp_build_target",
                      "gsicp_build_target_cloud", "gsicp_align", "gsicp_align_async", "gsicp_align_seed",
                      "gsicp_linearize"):
@@ -118,8 +122,22 @@ EXPORTED = [
     "gsicp_align_workspace_size", "gsicp_align", "gsicp_align_async", "gsicp_align_seed", "gsicp_linearize",
     "gsicp_status_string",
     "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version", "gsicp_debug_knn_counters",
-    "gsicp_debug_align_timeline", "gsicp_debug_align_counters",
+    "gsicp_debug_align_timeline", "gsicp_debug_align_counters", "gsicp_debug_kernel_timer",
+    "gsicp_debug_kernel_time",
 ]
+
+KT_KNN_SEARCH, KT_ALIGN, KT_SEED = 0, 1, 2
+
+
+def debug_kernel_timer(enable: bool):
+    """Diagnostic: the hot kernels record CUDA events around their launches (see gsicp.h)."""
+    lib().gsicp_debug_kernel_timer(1 if enable else 0)
+
+
+def debug_kernel_time(kernel: int) -> float | None:
+    """Elapsed ms of the last recorded launch of `kernel` (KT_*), after a synchronize."""
+    ms = C.c_float()
+    return float(ms.value) if lib().gsicp_debug_kernel_time(kernel, C.byref(ms)) else None
 
 
 def debug_align_counters(out: torch.Tensor | None):

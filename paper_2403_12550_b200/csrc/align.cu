@@ -134,6 +134,12 @@ __device__ __forceinline__ float nn_bound(const AlignArgs &a, const NN &nn) {
 // holds the best point seen, a valid upper bound for the grid search).
 constexpr int kGraphSteps = 4;
 constexpr float kReuseMargin = 1e-5f;  // relative slack on every distance of the reuse test
+// the warp path bounds the second neighbour only from this iteration on (earlier pose updates
+// are too large for the bound to survive the next step)
+#ifndef GSICP_D2_FROM_ITER
+#define GSICP_D2_FROM_ITER 2
+#endif
+constexpr int kD2FromIter = GSICP_D2_FROM_ITER;
 
 // On a certified step the list also bounds the SECOND nearest target: list members have their
 // exact distances, every other target k has |q - m_k| >= |m_j - m_k| - |q - m_j| >=
@@ -942,7 +948,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             const bool in_r = nn.slot >= 0 && ki_key(nn.best) < a.r2;
             const float base = in_r ? sqrtf(ki_key(nn.best)) : a.r;
             float d2 = 0.f;
-            if (base < INFINITY) {
+            if (base < INFINITY && it >= kD2FromIter) {
                 const float rho = base * 1.25f + 0.25f * a.h;
                 NN n2;
                 warp_nn(a, sIdx, sBox, qq.x, qq.y, qq.z, n2, lane, rho * rho, nn.slot);
@@ -1240,10 +1246,12 @@ cudaError_t align_seed_launch(const gsicp_cloud &src, const gsicp_target &tgt, c
         set_error("align_seed memset: %s", cudaGetErrorString(e));
         return e;
     }
+    ktimer_mark(KT_SEED, false, s);
     k_align_seed<<<blocks_for(src.cap > 0 ? src.cap : 1, kSeedT), kSeedT, 0, s>>>(a);
     GSICP_LAUNCH_CHECK("k_align_seed");
     k_align_seed_hard<<<num_sms() * 8, kSeedHardT, 0, s>>>(a);
     GSICP_LAUNCH_CHECK("k_align_seed_hard");
+    ktimer_mark(KT_SEED, true, s);
     note_launch(2);
     return cudaSuccess;
 }
@@ -1276,7 +1284,9 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
     cfg.stream = s;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    ktimer_mark(KT_ALIGN, false, s);
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_align, a);
+    ktimer_mark(KT_ALIGN, true, s);
     if (e != cudaSuccess) {
         set_error("k_align launch: %s", cudaGetErrorString(e));
         return e;

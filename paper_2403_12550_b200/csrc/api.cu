@@ -17,6 +17,26 @@ extern thread_local long long g_align_timeline_cap;
 extern thread_local int32_t *g_align_debug;
 
 void note_launch(int n) { g_launches += (uint64_t)n; }
+
+static thread_local bool g_ktimer_on = false;
+static thread_local cudaEvent_t g_kt_ev[KT_COUNT][2] = {};
+static thread_local bool g_kt_used[KT_COUNT] = {};
+
+void ktimer_mark(int id, bool stop, cudaStream_t s) {
+    if (!g_ktimer_on || id < 0 || id >= KT_COUNT) return;
+    cudaEvent_t &ev = g_kt_ev[id][stop ? 1 : 0];
+    if (!ev && cudaEventCreate(&ev) != cudaSuccess) {
+        ev = nullptr;
+        return;
+    }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+    else
+        cudaEventRecord(ev, s);
+    if (stop) g_kt_used[id] = true;
+}
 void set_error(const char *fmt, ...) {
     va_list ap;
     va_start(ap, fmt);
@@ -111,6 +131,15 @@ const char *gsicp_status_string(gsicp_status s) {
 const char *gsicp_last_error(void) { return g_err; }
 void gsicp_debug_knn_counters(int32_t *d_out) { gsicp::g_knn_debug = d_out; }
 void gsicp_debug_align_counters(int32_t *d_out) { gsicp::g_align_debug = d_out; }
+
+void gsicp_debug_kernel_timer(int enable) { gsicp::g_ktimer_on = enable != 0; }
+
+int gsicp_debug_kernel_time(int kernel, float *ms) {
+    using namespace gsicp;
+    if (!ms || kernel < 0 || kernel >= KT_COUNT || !g_kt_used[kernel]) return 0;
+    *ms = 0.f;
+    return cudaEventElapsedTime(ms, g_kt_ev[kernel][0], g_kt_ev[kernel][1]) == cudaSuccess ? 1 : 0;
+}
 void gsicp_debug_align_timeline(int64_t *d_out, int64_t capacity) {
     gsicp::g_align_timeline = reinterpret_cast<long long *>(d_out);
     gsicp::g_align_timeline_cap = d_out ? capacity : 0;

@@ -11,6 +11,11 @@ void note_launch(int n = 1);
 // thread-local error detail behind gsicp_last_error
 void set_error(const char *fmt, ...);
 
+// diagnostic kernel timer (gsicp_debug_kernel_timer): when enabled on the calling thread, the
+// hot kernels record a start / stop CUDA event pair around their launch (graph-capture safe)
+enum KTimerId { KT_KNN_SEARCH = 0, KT_ALIGN = 1, KT_SEED = 2, KT_COUNT = 3 };
+void ktimer_mark(int id, bool stop, cudaStream_t s);
+
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 // Bump allocator over a caller workspace; with base == nullptr it only measures.

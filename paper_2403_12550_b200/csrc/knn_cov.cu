@@ -492,6 +492,8 @@ bool knn_use_warp() {
 
 template <int K>
 cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s) {
+    const bool timed = a.nbr_t != nullptr;  // the covariance search (not the target graph build)
+    if (timed) ktimer_mark(KT_KNN_SEARCH, false, s);
     if (knn_use_warp()) {
         const long long warps = (cap + kQueriesPerWarp - 1) / kQueriesPerWarp;
         k_knn_search<K><<<blocks_for(warps * 32, kKnnThreads), kKnnThreads, 0, s>>>(a);
@@ -499,6 +501,7 @@ cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s) {
         k_knn_thread<K><<<blocks_for(cap, kKnnThreads), kKnnThreads, 0, s>>>(a);
     }
     GSICP_LAUNCH_CHECK("k_knn_search");
+    if (timed) ktimer_mark(KT_KNN_SEARCH, true, s);
     return cudaSuccess;
 }
 

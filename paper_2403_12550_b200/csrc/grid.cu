@@ -15,7 +15,7 @@ __global__ void k_grid_init(CellEntry *table, uint32_t slots, uint32_t *counters
         e.count = 0;
         table[i] = e;
     }
-    if (i < kMaxLevels) counters[i] = 0;
+    if (i < kMaxLevels + 1) counters[i] = 0;  // per-level allocation + the search work counter
     if (i == 0) {
         for (int a = 0; a < 3; ++a) {
             bbox[a] = float_to_ordered(INFINITY);
@@ -162,7 +162,7 @@ static GridView carve(Carver &c, int cap, int levels, bool with_cov, float h0) {
     g.scov_a = with_cov ? c.take<float4>(cap) : nullptr;
     g.scov_b = with_cov ? c.take<float4>(cap) : nullptr;
     g.slot_rank = c.take<uint2>((size_t)levels * cap);
-    g.counters = c.take<uint32_t>(kMaxLevels);
+    g.counters = c.take<uint32_t>(kMaxLevels + 1);
     g.bbox = c.take<int32_t>(8);
     g.cap = cap;
     return g;

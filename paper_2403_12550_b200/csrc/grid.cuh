@@ -21,7 +21,7 @@ struct GridView {
                              // as (x, y, z, original index bits)
     float4 *scov_a, *scov_b; // nullable: cell-ordered covariances (target grids)
     uint2 *slot_rank;        // [levels * cap]
-    uint32_t *counters;      // [kMaxLevels] points allocated per level
+    uint32_t *counters;      // [kMaxLevels] points allocated per level, [kMaxLevels] search work counter
     int32_t *bbox;           // [6] ordered-int encoded float min xyz / max xyz
     int cap;
 };

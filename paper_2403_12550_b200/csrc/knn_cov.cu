@@ -16,6 +16,8 @@
 // The moments of each query are warp-reduced into the lane that owns it; then every lane runs the
 // binary64 eigen-decomposition and regularisation of its own query in parallel.
 #include <stdlib.h>
+
+#include <algorithm>
 #include <string.h>
 
 #include "grid.cuh"
@@ -31,7 +33,8 @@ namespace {
 
 constexpr int kMinCell = 3;
 constexpr int kKnnThreads = 128;
-constexpr int kQueriesPerWarp = 8;  // queries a warp searches one after the other
+constexpr int kQueriesPerWarp = 8;  // queries a warp searches one after the other (one work batch)
+constexpr int kKnnMinBlocks = 8;    // resident blocks per SM the register budget is sized for
 constexpr int kMergeThreshold = 4;  // more passing candidates than this: sort-merge the batch
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kKnnBatch = 4;
@@ -154,13 +157,16 @@ struct Counters {
 };
 
 // Probe the cells one per lane (valid lanes only), then scan all their points as one flattened
-// range, 32 candidates per round, inserting into the list.
+// range, 32 candidates per round, inserting into the list.  The owning cell of a candidate is
+// found without a search: the non-empty cells are compacted into the warp's cell table (spos
+// start, first item), the cell starts falling into a round are OR-reduced into a bit mask, and a
+// lane's cell is (cells started before the round) + popc(starts at or below the lane) - 1.
 template <int K>
 __device__ __forceinline__ void scan_cells(const GridView &g, bool valid, unsigned long long key, float qx, float qy,
-                                           float qz, WarpTopK<K> &T, Counters &cn, int lane, unsigned long long *wbuf) {
-    uint2 se = valid ? cell_lookup(g.table, g.mask, key) : make_uint2(0u, 0u);
+                                           float qz, WarpTopK<K> &T, Counters &cn, int lane, unsigned long long *wbuf,
+                                           uint2 *wcell) {
+    const uint2 se = valid ? cell_lookup(g.table, g.mask, key) : make_uint2(0u, 0u);
     cn.probes += __popc(__ballot_sync(kFull, valid));
-    // inclusive scan of the counts
     uint32_t incl = se.y;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -169,38 +175,36 @@ __device__ __forceinline__ void scan_cells(const GridView &g, bool valid, unsign
     }
     const uint32_t total = __shfl_sync(kFull, incl, 31);
     cn.cands += (int)total;
+    const uint32_t excl = incl - se.y;
+    const unsigned ne = __ballot_sync(kFull, se.y != 0u);
+    if (se.y) wcell[__popc(ne & ((1u << lane) - 1u))] = make_uint2(se.x, excl);
+    __syncwarp();
+    int before = 0;
     for (uint32_t base = 0; base < total; base += 32) {
+        const bool here = se.y != 0u && excl >= base && excl < base + 32u;
+        const unsigned P = __reduce_or_sync(kFull, here ? 1u << (excl - base) : 0u);
         const uint32_t item = base + lane;
         unsigned long long cand = kEmptyKey;
-        // owning cell: first lane whose inclusive count exceeds item (binary search over lanes)
-        int lo = 0, hi = 31;
-#pragma unroll
-        for (int s = 0; s < 5; ++s) {
-            const int mid = (lo + hi) >> 1;
-            const uint32_t v = __shfl_sync(kFull, incl, mid);
-            if (v > item) hi = mid; else lo = mid + 1;
-        }
-        const uint32_t c_incl = __shfl_sync(kFull, incl, lo);
-        const uint32_t c_start = __shfl_sync(kFull, se.x, lo);
-        const uint32_t c_cnt = __shfl_sync(kFull, se.y, lo);
         if (item < total) {
-            const float4 p = __ldg(g.spos + c_start + (item - (c_incl - c_cnt)));
+            const uint2 c = wcell[before + __popc(P & (0xffffffffu >> (31 - lane))) - 1];
+            const float4 p = __ldg(g.spos + c.x + (item - c.y));
             cand = pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
         }
+        before += __popc(P);
         T.insert_all(cand, lane, wbuf);
     }
+    __syncwarp();
 }
 
 // Exact best-K of one query on one level.  Returns false (list reset) if shell 1 does not fill
 // the list and a coarser level exists.
 template <int K>
 __device__ bool knn_search_warp(const GridView &g, int level, float qx, float qy, float qz, WarpTopK<K> &T,
-                                Counters &cn, int lane, unsigned long long *wbuf) {
+                                Counters &cn, int lane, unsigned long long *wbuf, uint2 *wcell, const int *sbox) {
     T.reset();
     const float inv_h = ldexpf(g.inv_h0, -level);
     const QueryCell qc(qx, qy, qz, ldexpf(g.h0, level), inv_h);
-    int blo[3], bhi[3];
-    grid_cell_bbox(g, level, blo, bhi);
+    const int *blo = sbox + 6 * level, *bhi = sbox + 6 * level + 3;
     for (int m = 0;; ++m) {
         // shell 0 and 1 together: lane 0 = own cell, lanes 1..26 = shell 1
         if (m == 1) continue;
@@ -222,7 +226,7 @@ __device__ bool knn_search_warp(const GridView &g, int level, float qx, float qy
                 valid = !(lb > ki_key(T.worst));
             }
             if (!__any_sync(kFull, valid)) continue;
-            scan_cells<K>(g, valid, cell_key(level, x, y, z), qx, qy, qz, T, cn, lane, wbuf);
+            scan_cells<K>(g, valid, cell_key(level, x, y, z), qx, qy, qz, T, cn, lane, wbuf, wcell);
         }
         const int mm = m == 0 ? 1 : m;  // shells 0..mm are complete
         if (T.full() && ki_key(T.worst) < qc.certified_key(mm)) return true;
@@ -232,13 +236,23 @@ __device__ bool knn_search_warp(const GridView &g, int level, float qx, float qy
 }
 
 template <int K>
-__global__ void __launch_bounds__(kKnnThreads) k_knn_search(KnnArgs a) {
+__global__ void __launch_bounds__(kKnnThreads, kKnnMinBlocks) k_knn_search(KnnArgs a) {
     const int n = *a.d_n;
     const GridView &g = a.g;
     const int lane = threadIdx.x & 31;
     __shared__ unsigned long long sBuf[kKnnThreads];
+    __shared__ uint2 sCell[kKnnThreads];
+    __shared__ int sBox[kMaxLevels * 6];
+    if (threadIdx.x < g.levels) grid_cell_bbox(g, threadIdx.x, sBox + 6 * threadIdx.x, sBox + 6 * threadIdx.x + 3);
+    __syncthreads();
     unsigned long long *wbuf = sBuf + (threadIdx.x & ~31);
-    const int wbase = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kQueriesPerWarp;  // first query of this warp
+    uint2 *wcell = sCell + (threadIdx.x & ~31);
+    // dynamic scheduling: warps take batches of kQueriesPerWarp queries until none are left
+    unsigned int *work = g.counters + kMaxLevels;
+    for (;;) {
+    int wbase = 0;
+    if (lane == 0) wbase = (int)atomicAdd(work, 1u) * kQueriesPerWarp;
+    wbase = __shfl_sync(kFull, wbase, 0);
     if (wbase >= n) return;
     const int tq = wbase + lane;
     float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -263,12 +277,13 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_search(KnnArgs a) {
         WarpTopK<K> T;
         T.inserts = 0;
         Counters cn;
-        while (!knn_search_warp<K>(g, level, qx, qy, qz, T, cn, lane, wbuf)) ++level;
+        while (!knn_search_warp<K>(g, level, qx, qy, qz, T, cn, lane, wbuf, wcell, sBox)) ++level;
         if (a.debug && lane == 0) a.debug[i] = make_int4(level, cn.probes, cn.cands, T.inserts);
         // moments over the k nearest: lane j < k holds neighbour j (sorted by (key, index))
         const bool have = lane < a.k && T.L != kEmptyKey;
         if (a.knn_idx && lane < a.k) a.knn_idx[(size_t)i * a.k + lane] = have ? (int32_t)ki_idx(T.L) : -1;
         if (a.nbr_t && lane < a.k) a.nbr_t[(size_t)(wbase + qi) * kMaxK + lane] = have ? (int32_t)ki_idx(T.L) : -1;
+    }
     }
 }
 
@@ -495,8 +510,10 @@ cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s) {
     const bool timed = a.nbr_t != nullptr;  // the covariance search (not the target graph build)
     if (timed) ktimer_mark(KT_KNN_SEARCH, false, s);
     if (knn_use_warp()) {
+        // a resident grid (one wave) pulling work batches; never more warps than batches
         const long long warps = (cap + kQueriesPerWarp - 1) / kQueriesPerWarp;
-        k_knn_search<K><<<blocks_for(warps * 32, kKnnThreads), kKnnThreads, 0, s>>>(a);
+        const long long blocks = std::min<long long>(blocks_for(warps * 32, kKnnThreads), (long long)num_sms() * kKnnMinBlocks);
+        k_knn_search<K><<<(unsigned)std::max<long long>(blocks, 1), kKnnThreads, 0, s>>>(a);
     } else {
         k_knn_thread<K><<<blocks_for(cap, kKnnThreads), kKnnThreads, 0, s>>>(a);
     }

@@ -136,6 +136,22 @@ gsicp_status gsicp_covariances(const float *pos, const int32_t *d_n, int32_t cap
                                float eps_var, float cell0, int32_t levels, float *cov_a, float *cov_b,
                                int32_t *knn_idx, void *ws, size_t ws_bytes, void *stream);
 
+/* Same result as gsicp_covariances (bit-identical neighbour lists and covariances), for a
+ * depth-frame cloud: pos/d_n exactly as written by gsicp_backproject_downsample with the same
+ * (H, W, stride) and fx, fy of K (pos.w = pixel id v*W + u).  Candidates come from the
+ * (2M+1)^2 lattice-pixel window around each query's pixel (M = 4), exact whenever the k-th
+ * radius rho satisfies the projection bound f rho (z + |x|) / (z (z - rho)) < (M+1) s in both
+ * image axes (every point within rho then lies in the window); the remaining queries are
+ * finished by the hash search of gsicp_covariances (cell0, levels as there).  A cloud that is
+ * not a depth-frame cloud (a pixel id off the lattice, two points on one pixel) is detected on
+ * the device and handled entirely by the hash search, so the result is exact for any input.
+ *  Errors: INVALID_ARGUMENT. */
+size_t gsicp_covariances_image_workspace_size(int32_t cap, int32_t levels, int32_t H, int32_t W, int32_t stride);
+gsicp_status gsicp_covariances_image(const float *pos, const int32_t *d_n, int32_t cap, int32_t H, int32_t W,
+                                     int32_t stride, gsicp_intrinsics K, int32_t k, gsicp_reg_mode mode,
+                                     float eps_var, float cell0, int32_t levels, float *cov_a, float *cov_b,
+                                     int32_t *knn_idx, void *ws, size_t ws_bytes, void *stream);
+
 /* ---------------------------------------------------------------------------------------
  * A5  Map Gaussians -> G-ICP targets (the map's Gaussians are reused as
  * targets with no covariance recomputation; P:189-191 C = R Lambda^2 R^T).  Quaternion wxyz,

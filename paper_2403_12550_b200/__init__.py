@@ -81,6 +81,10 @@ def lib():
         L.gsicp_covariances_workspace_size.argtypes = [i32, i32]
         L.gsicp_covariances_workspace_size.restype = sz
         L.gsicp_covariances.argtypes = [P, P, i32, i32, i32, f32, f32, i32, P, P, P, P, sz, P]
+        L.gsicp_covariances_image_workspace_size.argtypes = [i32, i32, i32, i32, i32]
+        L.gsicp_covariances_image_workspace_size.restype = sz
+        L.gsicp_covariances_image.argtypes = [P, P, i32, i32, i32, i32, Intrinsics, i32, i32, f32, f32, i32, P, P, P,
+                                              P, sz, P]
         L.gsicp_build_target_workspace_size.argtypes = [i32]
         L.gsicp_build_target_workspace_size.restype = sz
         L.gsicp_build_target.argtypes = [P, P, P, i32, i32, i32, f32, f32, C.POINTER(_Target), P, sz, P]
@@ -108,7 +112,7 @@ def lib():
         L.gsicp_debug_kernel_timer.restype = None
         L.gsicp_debug_kernel_time.argtypes = [i32, C.POINTER(C.c_float)]
         L.gsicp_debug_kernel_time.restype = i32
-        for name in ("gsicp_backproject_downsample", "gsicp_covariances", "gsicp_build_target",
+        for name in ("gsicp_backproject_downsample", "gsicp_covariances", "gsicp_covariances_image", "gsicp_build_target",
                      "gsicp_build_target_cloud", "gsicp_align", "gsicp_align_async", "gsicp_align_seed",
                      "gsicp_linearize"):
             getattr(L, name).restype = i32
@@ -118,7 +122,8 @@ def lib():
 
 EXPORTED = [
     "gsicp_backproject_workspace_size", "gsicp_backproject_downsample", "gsicp_covariances_workspace_size",
-    "gsicp_covariances", "gsicp_build_target_workspace_size", "gsicp_build_target", "gsicp_build_target_cloud",
+    "gsicp_covariances", "gsicp_covariances_image_workspace_size", "gsicp_covariances_image",
+    "gsicp_build_target_workspace_size", "gsicp_build_target", "gsicp_build_target_cloud",
     "gsicp_align_workspace_size", "gsicp_align", "gsicp_align_async", "gsicp_align_seed", "gsicp_linearize",
     "gsicp_status_string",
     "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version", "gsicp_debug_knn_counters",
@@ -278,6 +283,27 @@ def covariances(pos: torch.Tensor, d_n: torch.Tensor, k: int = 20, mode: int = R
     return Cloud(pos, cov_a, cov_b, d_n)
 
 
+def covariances_image(pos: torch.Tensor, d_n: torch.Tensor, H: int, W: int, stride: int, K, k: int = 20,
+                      mode: int = REG_ELLIPSE, eps_var: float = 1e-3, cell0: float = 0.01, levels: int = 1,
+                      cov_a=None, cov_b=None, knn_idx: torch.Tensor | None = None, ws=None, stream=None):
+    """A2-A4 for a depth-frame cloud from backproject_downsample(H, W, stride, K): the
+    image-window kNN (same result as covariances()).  Returns a Cloud sharing `pos`."""
+    cap = pos.shape[0]
+    dev = pos.device
+    if cov_a is None:
+        cov_a = torch.empty((cap, 4), dtype=torch.float32, device=dev)
+    if cov_b is None:
+        cov_b = torch.empty((cap, 4), dtype=torch.float32, device=dev)
+    need = lib().gsicp_covariances_image_workspace_size(cap, levels, H, W, stride)
+    if ws is None:
+        ws = _ws(need, dev)
+    Kc = K if isinstance(K, Intrinsics) else Intrinsics(*K)
+    _check(lib().gsicp_covariances_image(_ptr(pos), _ptr(d_n), cap, H, W, stride, Kc, k, mode, eps_var, cell0, levels,
+                                         _ptr(cov_a), _ptr(cov_b), _ptr(knn_idx), _ptr(ws), ws.numel(),
+                                         _stream(stream)))
+    return Cloud(pos, cov_a, cov_b, d_n)
+
+
 @dataclasses.dataclass
 class Target:
     """Target Gaussians G^t: hashed copy living in `ws` (keep this object alive)."""
@@ -411,7 +437,7 @@ class Tracker:
         self.device = torch.device(device)
         self.cloud = Cloud.empty(self.cap, self.device)
         self.ws_bp = _ws(lib().gsicp_backproject_workspace_size(H, W, stride), self.device)
-        self.ws_cov = _ws(lib().gsicp_covariances_workspace_size(self.cap, levels), self.device)
+        self.ws_cov = _ws(lib().gsicp_covariances_image_workspace_size(self.cap, levels, H, W, stride), self.device)
         self.ws_align = align_workspace(self.cap, self.device)
         self.d_T = torch.zeros(16, dtype=torch.float64, device=self.device)
         self.d_stats = torch.zeros(C.sizeof(AlignStats), dtype=torch.uint8, device=self.device)
@@ -422,8 +448,12 @@ class Tracker:
     def preprocess(self, depth: torch.Tensor, stream=None):
         backproject_downsample(depth, self.K, self.stride, self.z_min, self.z_max, self.cloud.pos, self.cloud.d_n,
                                self.ws_bp, stream)
-        covariances(self.cloud.pos, self.cloud.d_n, self.k, self.mode, self.eps, self.cell0, self.levels,
-                    self.cloud.cov_a, self.cloud.cov_b, None, self.ws_cov, stream)
+        self._covariances(stream)
+
+    def _covariances(self, stream):
+        covariances_image(self.cloud.pos, self.cloud.d_n, self.H, self.W, self.stride, self.K, self.k, self.mode,
+                          self.eps, self.cell0, self.levels, self.cloud.cov_a, self.cloud.cov_b, None, self.ws_cov,
+                          stream)
 
     def step_async(self, depth: torch.Tensor, tgt: Target, stream=None, events=None):
         """Whole frame, device-resident pose in self.d_T (set it before), no host sync.
@@ -441,8 +471,7 @@ class Tracker:
         self._side.wait_event(self._fork)
         align_seed(self.cloud, tgt, self.d_T, self.params, self.ws_align, self._side)
         self._join.record(self._side)
-        covariances(self.cloud.pos, self.cloud.d_n, self.k, self.mode, self.eps, self.cell0, self.levels,
-                    self.cloud.cov_a, self.cloud.cov_b, None, self.ws_cov, s0)
+        self._covariances(s0)
         s0.wait_event(self._join)
         if events:
             events[2].record(s0)

@@ -52,6 +52,10 @@ size_t covariances_ws_bytes(int cap, int levels);
 cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, int k, int mode, float eps,
                                float cell0, int levels, float *cov_a, float *cov_b, int32_t *knn_idx, void *ws,
                                cudaStream_t s);
+size_t covariances_image_ws_bytes(int cap, int levels, int H, int W, int stride);
+cudaError_t covariances_image_launch(const float *pos, const int32_t *d_n, int cap, int H, int W, int stride,
+                                     gsicp_intrinsics K, int k, int mode, float eps, float cell0, int levels,
+                                     float *cov_a, float *cov_b, int32_t *knn_idx, void *ws, cudaStream_t s);
 size_t target_ws_bytes(int M);
 cudaError_t build_target_launch(const float *means, const float *quats, const float *scales, int scales_are_log,
                                 int M, int mode, float eps, float cell, gsicp_target *out, void *ws,
@@ -192,6 +196,34 @@ gsicp_status gsicp_covariances(const float *pos, const int32_t *d_n, int32_t cap
     return cuda_status(covariances_launch(pos, d_n, cap, k, (int)mode, eps_var, cell0, levels, cov_a, cov_b, knn_idx, ws,
                                           (cudaStream_t)stream),
                        "covariances");
+}
+
+size_t gsicp_covariances_image_workspace_size(int32_t cap, int32_t levels, int32_t H, int32_t W, int32_t stride) {
+    if (cap < 1 || levels < 1 || levels > kMaxLevels || H < 1 || W < 1 || stride < 1) return 0;
+    return covariances_image_ws_bytes(cap, levels, H, W, stride);
+}
+
+gsicp_status gsicp_covariances_image(const float *pos, const int32_t *d_n, int32_t cap, int32_t H, int32_t W,
+                                     int32_t stride, gsicp_intrinsics K, int32_t k, gsicp_reg_mode mode, float eps_var,
+                                     float cell0, int32_t levels, float *cov_a, float *cov_b, int32_t *knn_idx,
+                                     void *ws, size_t ws_bytes, void *stream) {
+    g_err[0] = 0;
+    if (!pos || !d_n || !cov_a || !cov_b) BAD("covariances_image: null pointer");
+    if (!aligned16(pos) || !aligned16(cov_a) || !aligned16(cov_b)) BAD("covariances_image: arrays must be 16-byte aligned");
+    if (cap < 1) BAD("covariances_image: cap must be >= 1");
+    if (H < 1 || W < 1 || stride < 1) BAD("covariances_image: bad image geometry");
+    if ((long long)H * W >= (1ll << 31)) BAD("covariances_image: image too large for 32-bit pixel ids");
+    if (!(K.fx > 0.f) || !(K.fy > 0.f) || !isfinite(K.fx) || !isfinite(K.fy)) BAD("covariances_image: bad intrinsics");
+    if (k < 1 || k > 32) BAD("covariances_image: k must be in [1, 32]");
+    if (mode != GSICP_REG_NONE && mode != GSICP_REG_PLANE && mode != GSICP_REG_ELLIPSE) BAD("covariances_image: bad mode");
+    if (!(eps_var > 0.f) || !(eps_var <= 1.f)) BAD("covariances_image: eps_var must be in (0, 1]");
+    if (!(cell0 > 0.f) || !isfinite(cell0)) BAD("covariances_image: cell0 must be > 0");
+    if (levels < 1 || levels > kMaxLevels) BAD("covariances_image: levels must be in [1, %d]", kMaxLevels);
+    gsicp_status st = check_ws(ws, ws_bytes, covariances_image_ws_bytes(cap, levels, H, W, stride));
+    if (st != GSICP_OK) return st;
+    return cuda_status(covariances_image_launch(pos, d_n, cap, H, W, stride, K, k, (int)mode, eps_var, cell0, levels,
+                                                cov_a, cov_b, knn_idx, ws, (cudaStream_t)stream),
+                       "covariances_image");
 }
 
 size_t gsicp_build_target_workspace_size(int32_t M) {

@@ -6,8 +6,13 @@ namespace gsicp {
 
 namespace {
 
-__global__ void k_grid_init(CellEntry *table, uint32_t slots, uint32_t *counters, int32_t *bbox) {
+__global__ void k_grid_init(CellEntry *table, uint32_t slots, uint32_t *counters, int32_t *bbox, uint32_t *mark,
+                            const int32_t *__restrict__ d_n) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (*d_n <= 0) {  // nothing to hash (e.g. an empty fallback queue): leave the table alone
+        if (i < kGridCounters) counters[i] = 0;
+        return;
+    }
     if (i < slots) {
         CellEntry e;
         e.key = kEmptyKey;
@@ -15,7 +20,8 @@ __global__ void k_grid_init(CellEntry *table, uint32_t slots, uint32_t *counters
         e.count = 0;
         table[i] = e;
     }
-    if (i < kMaxLevels + 1) counters[i] = 0;  // per-level allocation + the search work counter
+    if (mark && i < (slots + 31) / 32) mark[i] = 0u;
+    if (i < kGridCounters) counters[i] = 0;  // per-level allocation + the search work / queue counters
     if (i == 0) {
         for (int a = 0; a < 3; ++a) {
             bbox[a] = float_to_ordered(INFINITY);
@@ -80,8 +86,9 @@ __global__ void k_grid_insert(GridView g, const float4 *__restrict__ pos, const 
 constexpr int kAllocThreads = 256;
 constexpr int kAllocPerThread = 4;
 
-__global__ void __launch_bounds__(kAllocThreads) k_grid_alloc(GridView g) {
+__global__ void __launch_bounds__(kAllocThreads) k_grid_alloc(GridView g, const int32_t *__restrict__ d_n) {
     __shared__ uint32_t s_tot[kMaxLevels], s_base[kMaxLevels];
+    if (*d_n <= 0) return;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x < kMaxLevels) s_tot[threadIdx.x] = 0;
     __syncthreads();
@@ -150,7 +157,7 @@ uint32_t grid_table_slots(int cap, int levels) {
     return (uint32_t)s;
 }
 
-static GridView carve(Carver &c, int cap, int levels, bool with_cov, float h0) {
+static GridView carve(Carver &c, int cap, int levels, bool with_cov, float h0, bool with_mark) {
     GridView g{};
     const uint32_t slots = grid_table_slots(cap, levels);
     g.table = c.take<CellEntry>(slots);
@@ -162,21 +169,22 @@ static GridView carve(Carver &c, int cap, int levels, bool with_cov, float h0) {
     g.scov_a = with_cov ? c.take<float4>(cap) : nullptr;
     g.scov_b = with_cov ? c.take<float4>(cap) : nullptr;
     g.slot_rank = c.take<uint2>((size_t)levels * cap);
-    g.counters = c.take<uint32_t>(kMaxLevels + 1);
+    g.counters = c.take<uint32_t>(kGridCounters);
+    g.mark = with_mark ? c.take<uint32_t>((slots + 31) / 32) : nullptr;
     g.bbox = c.take<int32_t>(8);
     g.cap = cap;
     return g;
 }
 
-size_t grid_bytes(int cap, int levels, bool with_cov) {
+size_t grid_bytes(int cap, int levels, bool with_cov, bool with_mark) {
     Carver c(nullptr);
-    carve(c, cap, levels, with_cov, 1.f);
+    carve(c, cap, levels, with_cov, 1.f, with_mark);
     return c.bytes();
 }
 
-GridView grid_carve(void *base, int cap, int levels, bool with_cov, float h0) {
+GridView grid_carve(void *base, int cap, int levels, bool with_cov, float h0, bool with_mark) {
     Carver c(base);
-    return carve(c, cap, levels, with_cov, h0);
+    return carve(c, cap, levels, with_cov, h0, with_mark);
 }
 
 cudaError_t grid_build(const GridView &g, const float4 *pos, const float4 *cov_a, const float4 *cov_b,
@@ -184,11 +192,11 @@ cudaError_t grid_build(const GridView &g, const float4 *pos, const float4 *cov_a
     const int T = 256;
     const uint32_t slots = g.mask + 1;
     const long long work = (long long)g.levels * g.cap;
-    k_grid_init<<<blocks_for(slots, T), T, 0, s>>>(g.table, slots, g.counters, g.bbox);
+    k_grid_init<<<blocks_for(slots, T), T, 0, s>>>(g.table, slots, g.counters, g.bbox, g.mark, d_n);
     GSICP_LAUNCH_CHECK("k_grid_init");
     k_grid_insert<<<blocks_for(work, T), T, 0, s>>>(g, pos, d_n);
     GSICP_LAUNCH_CHECK("k_grid_insert");
-    k_grid_alloc<<<blocks_for(slots, kAllocThreads * kAllocPerThread), kAllocThreads, 0, s>>>(g);
+    k_grid_alloc<<<blocks_for(slots, kAllocThreads * kAllocPerThread), kAllocThreads, 0, s>>>(g, d_n);
     GSICP_LAUNCH_CHECK("k_grid_alloc");
     if (g.scov_a)
         k_grid_scatter<true><<<blocks_for(work, T), T, 0, s>>>(g, pos, cov_a, cov_b, d_n);

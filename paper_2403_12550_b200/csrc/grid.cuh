@@ -12,6 +12,8 @@
 
 namespace gsicp {
 
+constexpr int kGridCounters = kMaxLevels + 8;
+
 struct GridView {
     CellEntry *table;
     uint32_t mask;
@@ -21,7 +23,9 @@ struct GridView {
                              // as (x, y, z, original index bits)
     float4 *scov_a, *scov_b; // nullable: cell-ordered covariances (target grids)
     uint2 *slot_rank;        // [levels * cap]
-    uint32_t *counters;      // [kMaxLevels] points allocated per level, [kMaxLevels] search work counter
+    uint32_t *counters;      // [kMaxLevels] points allocated per level, then kGridCounters - kMaxLevels
+                             // work / queue counters of the search kernels (all zeroed by the build)
+    uint32_t *mark;          // nullable: one bit per table slot, zeroed by the build (tile kNN units)
     int32_t *bbox;           // [6] ordered-int encoded float min xyz / max xyz
     int cap;
 };
@@ -33,9 +37,9 @@ __device__ __forceinline__ int32_t float_to_ordered(float f) {
 __device__ __forceinline__ float ordered_to_float(int32_t i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
 
 // host helpers (defined in grid.cu)
-size_t grid_bytes(int cap, int levels, bool with_cov);
+size_t grid_bytes(int cap, int levels, bool with_cov, bool with_mark = false);
 uint32_t grid_table_slots(int cap, int levels);
-GridView grid_carve(void *base, int cap, int levels, bool with_cov, float h0);
+GridView grid_carve(void *base, int cap, int levels, bool with_cov, float h0, bool with_mark = false);
 cudaError_t grid_build(const GridView &g, const float4 *pos, const float4 *cov_a, const float4 *cov_b,
                        const int32_t *d_n, int n_host_max, cudaStream_t s);
 

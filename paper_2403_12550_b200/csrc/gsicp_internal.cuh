@@ -138,10 +138,11 @@ GS_HD void eigvec_separated(const double *A, double e, double *out) {
     cross3(r0, r2, c1);
     cross3(r1, r2, c2);
     const double d0 = dot3(c0, c0), d1 = dot3(c1, c1), d2 = dot3(c2, c2);
-    const double *c = c0;
+    // value selects (no pointer into local arrays, which would force them to local memory)
+    double c[3] = {c0[0], c0[1], c0[2]};
     double d = d0;
-    if (d1 > d) { c = c1; d = d1; }
-    if (d2 > d) { c = c2; d = d2; }
+    if (d1 > d) { c[0] = c1[0]; c[1] = c1[1]; c[2] = c1[2]; d = d1; }
+    if (d2 > d) { c[0] = c2[0]; c[1] = c2[1]; c[2] = c2[2]; d = d2; }
     if (d > 0.0) {
         const double inv = gs_rsqrt(d);
         out[0] = c[0] * inv; out[1] = c[1] * inv; out[2] = c[2] * inv;
@@ -225,19 +226,24 @@ __host__ __device__ inline Eig3 eig3_sym(const double *Ain) {
         vl[k] = -y * U[k] + x * V[k];
     }
     // assemble descending
-    double lam3[3];
-    const double *vec3[3];
-    if (half >= 0.0) {  // separated = largest
-        lam3[0] = ls; vec3[0] = ws; lam3[1] = mu_hi; vec3[1] = vh; lam3[2] = mu_lo; vec3[2] = vl;
-    } else {            // separated = smallest
-        lam3[0] = mu_hi; vec3[0] = vh; lam3[1] = mu_lo; vec3[1] = vl; lam3[2] = ls; vec3[2] = ws;
+    double lam3[3], vec3[3][3];
+    const bool sep_largest = half >= 0.0;
+    lam3[0] = sep_largest ? ls : mu_hi;
+    lam3[1] = sep_largest ? mu_hi : mu_lo;
+    lam3[2] = sep_largest ? mu_lo : ls;
+    for (int k = 0; k < 3; ++k) {
+        vec3[0][k] = sep_largest ? ws[k] : vh[k];
+        vec3[1][k] = sep_largest ? vh[k] : vl[k];
+        vec3[2][k] = sep_largest ? vl[k] : ws[k];
     }
     // guard the order against rounding (the roles above hold up to ~eps ||A||)
     for (int i = 0; i < 2; ++i)
         for (int j = 0; j < 2 - i; ++j)
             if (lam3[j + 1] > lam3[j]) {
                 const double tl = lam3[j]; lam3[j] = lam3[j + 1]; lam3[j + 1] = tl;
-                const double *tv = vec3[j]; vec3[j] = vec3[j + 1]; vec3[j + 1] = tv;
+                for (int k = 0; k < 3; ++k) {
+                    const double tv = vec3[j][k]; vec3[j][k] = vec3[j + 1][k]; vec3[j + 1][k] = tv;
+                }
             }
     for (int j = 0; j < 3; ++j) {
         r.lam[j] = fmax(lam3[j] * amax, 0.0);

@@ -51,6 +51,11 @@ struct KnnArgs {
     int32_t *knn_idx;
     int4 *debug;
     int32_t *nbr_t;   // [cap][kMaxK]: the k neighbours (input indices, sorted, -1 pad) per query in search order
+    // queue mode (fallback of the image-window kernel): the queries are queue[0 .. *queue_n) (input
+    // indices) instead of every point; query t of the search is queue[t]
+    const uint32_t *queue;
+    const uint32_t *queue_n;
+    uint32_t *work;   // dynamic work counter of k_knn_search
 };
 
 __device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int src) {
@@ -237,6 +242,7 @@ __device__ bool knn_search_warp(const GridView &g, int level, float qx, float qy
 
 template <int K>
 __global__ void __launch_bounds__(kKnnThreads, kKnnMinBlocks) k_knn_search(KnnArgs a) {
+    if (a.queue && *a.queue_n == 0u) return;  // empty fallback queue (block-uniform)
     const int n = *a.d_n;
     const GridView &g = a.g;
     const int lane = threadIdx.x & 31;
@@ -248,16 +254,26 @@ __global__ void __launch_bounds__(kKnnThreads, kKnnMinBlocks) k_knn_search(KnnAr
     unsigned long long *wbuf = sBuf + (threadIdx.x & ~31);
     uint2 *wcell = sCell + (threadIdx.x & ~31);
     // dynamic scheduling: warps take batches of kQueriesPerWarp queries until none are left
-    unsigned int *work = g.counters + kMaxLevels;
+    const int nq_all = a.queue ? (int)*a.queue_n : n;
     for (;;) {
     int wbase = 0;
-    if (lane == 0) wbase = (int)atomicAdd(work, 1u) * kQueriesPerWarp;
+    // queue mode: one (hard) query per batch, so the few queued queries spread over all warps
+    const int qpw = a.queue ? 1 : kQueriesPerWarp;
+    if (lane == 0) wbase = (int)atomicAdd(a.work, 1u) * qpw;
     wbase = __shfl_sync(kFull, wbase, 0);
-    if (wbase >= n) return;
+    if (wbase >= nq_all) return;
     const int tq = wbase + lane;
     float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (lane < kQueriesPerWarp && tq < n) e = __ldg(g.spos + (size_t)(g.levels - 1) * g.cap + tq);
-    const int nq = min(kQueriesPerWarp, n - wbase);
+    if (lane < qpw && tq < nq_all) {
+        if (a.queue) {
+            const uint32_t qi = __ldg(a.queue + tq);
+            e = __ldg(a.pos + qi);
+            e.w = __int_as_float((int)qi);
+        } else {
+            e = __ldg(g.spos + (size_t)(g.levels - 1) * g.cap + tq);
+        }
+    }
+    const int nq = min(qpw, nq_all - wbase);
     for (int qi = 0; qi < nq; ++qi) {
         const float qx = __shfl_sync(kFull, e.x, qi), qy = __shfl_sync(kFull, e.y, qi), qz = __shfl_sync(kFull, e.z, qi);
         const int i = __shfl_sync(kFull, __float_as_int(e.w), qi);
@@ -278,7 +294,7 @@ __global__ void __launch_bounds__(kKnnThreads, kKnnMinBlocks) k_knn_search(KnnAr
         T.inserts = 0;
         Counters cn;
         while (!knn_search_warp<K>(g, level, qx, qy, qz, T, cn, lane, wbuf, wcell, sBox)) ++level;
-        if (a.debug && lane == 0) a.debug[i] = make_int4(level, cn.probes, cn.cands, T.inserts);
+        if (a.debug && lane == 0 && !a.queue) a.debug[i] = make_int4(level, cn.probes, cn.cands, T.inserts);
         // moments over the k nearest: lane j < k holds neighbour j (sorted by (key, index))
         const bool have = lane < a.k && T.L != kEmptyKey;
         if (a.knn_idx && lane < a.k) a.knn_idx[(size_t)i * a.k + lane] = have ? (int32_t)ki_idx(T.L) : -1;
@@ -288,202 +304,56 @@ __global__ void __launch_bounds__(kKnnThreads, kKnnMinBlocks) k_knn_search(KnnAr
 }
 
 // ---------------------------------------------------------------------------------------------
-// Thread-per-query variant.  A query's neighbourhood is small (tens to ~150 candidates), so one
-// thread per query with its best-K list in registers issues far fewer warp instructions than a
-// warp per query; queries run in coarsest-level cell order, so the 32 threads of a warp scan
-// mostly the same cells (broadcast loads).
-//   fill : own cell + shell 1 (27 cells, hash probes batched); if the list is not full and a
-//          coarser level exists, restart there; else widen whole shells until full
-//   ball : every other cell whose conservative lower bound is <= the K-th key (ball_search)
-// Exact for the same reason as the warp variant: a cell is skipped only when no point in it can
-// beat the current K-th (key, index).
+constexpr int pow2ceil(int x) { return x <= 1 ? 1 : 2 * pow2ceil((x + 1) / 2); }
+
+__device__ __forceinline__ void cswap(unsigned long long &a, unsigned long long &b) {
+    const unsigned long long lo = a < b ? a : b, hi = a < b ? b : a;
+    a = lo;
+    b = hi;
+}
+
+// Batcher odd-even merge sort of L[0..K) ascending.  The comparator list is built at compile
+// time (pads above K stay +inf, so comparators that touch them are dropped) and applied by
+// template recursion, so every index is a constant and L stays in registers.
 template <int K>
-struct ThreadTopK {
-    unsigned long long L[K];  // ascending; kEmptyKey pads
-    __device__ __forceinline__ void reset() {
-#pragma unroll
-        for (int j = 0; j < K; ++j) L[j] = kEmptyKey;
-    }
-    __device__ __forceinline__ unsigned long long worst() const { return L[K - 1]; }
-    // c < worst(): all compares first (independent), then the shift — no serial chain
-    __device__ __forceinline__ void insert(unsigned long long c) {
-        bool b[K];
-#pragma unroll
-        for (int j = 0; j < K; ++j) b[j] = L[j] < c;
-#pragma unroll
-        for (int j = K - 1; j > 0; --j) L[j] = b[j] ? L[j] : (b[j - 1] ? c : L[j - 1]);
-        L[0] = b[0] ? L[0] : c;
+struct BatcherNet {
+    static constexpr int N = pow2ceil(K);
+    int a[N * 8 * 8], b[N * 8 * 8], count;
+    constexpr BatcherNet() : a(), b(), count(0) {
+        for (int p = 1; p < N; p <<= 1)
+            for (int kk = p; kk >= 1; kk >>= 1)
+                for (int j = kk % p; j + kk < N; j += 2 * kk)
+                    for (int i = 0; i < kk && i < N - j - kk; ++i) {
+                        const int x = i + j, y = i + j + kk;
+                        if (y < K && (x / (2 * p)) == (y / (2 * p))) {
+                            a[count] = x;
+                            b[count] = y;
+                            ++count;
+                        }
+                    }
     }
 };
-
 template <int K>
-__device__ __forceinline__ void scan_cell_thread(const float4 *__restrict__ spos, uint2 se, float qx, float qy,
-                                                 float qz, ThreadTopK<K> &T, int &cands, int &inserts) {
-    cands += (int)se.y;
-#pragma unroll 2
-    for (uint32_t p = 0; p < se.y; ++p) {
-        const float4 P = __ldg(spos + se.x + p);
-        const unsigned long long c = pack_ki(canon_key(qx, qy, qz, P.x, P.y, P.z), (uint32_t)__float_as_int(P.w));
-        if (c < T.worst()) {
-            T.insert(c);
-            ++inserts;
-        }
+inline constexpr BatcherNet<K> kBatcherNet{};
+template <int K, int I>
+__device__ __forceinline__ void sort_net_step(unsigned long long (&L)[K]) {
+    if constexpr (I < kBatcherNet<K>.count) {
+        constexpr int x = kBatcherNet<K>.a[I], y = kBatcherNet<K>.b[I];
+        cswap(L[x], L[y]);
+        sort_net_step<K, I + 1>(L);
     }
 }
-
 template <int K>
-__device__ bool knn_search_thread(const GridView &g, int level, float qx, float qy, float qz, ThreadTopK<K> &T,
-                                  int &probes, int &cands, int &inserts) {
-    T.reset();
-    const float inv_h = ldexpf(g.inv_h0, -level);
-    const QueryCell qc(qx, qy, qz, ldexpf(g.h0, level), inv_h);
-    int blo[3], bhi[3];
-    grid_cell_bbox(g, level, blo, bhi);
-    CellIndex idx;
-    idx.table = g.table;
-    idx.mask = g.mask;
-    idx.level = level;
-    idx.dense = nullptr;
-    idx.use_dense = false;
-    // own cell + shell 1, nearest-first, kKnnBatch probes in flight
-    for (int t0 = 0; t0 < 27; t0 += kKnnBatch) {
-        int xs[kKnnBatch], ys[kKnnBatch], zs[kKnnBatch];
-        bool valid[kKnnBatch];
-        float lb[kKnnBatch];
-        const float bound = ki_key(T.worst());
-#pragma unroll
-        for (int j = 0; j < kKnnBatch; ++j) {
-            const int t = t0 + j;
-            int dx = 0, dy = 0, dz = 0;
-            if (t > 0 && t < 27) shell_cell(1, t - 1, dx, dy, dz);
-            xs[j] = qc.c[0] + dx;
-            ys[j] = qc.c[1] + dy;
-            zs[j] = qc.c[2] + dz;
-            lb[j] = qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2);
-            valid[j] = t < 27 && xs[j] >= blo[0] && xs[j] <= bhi[0] && ys[j] >= blo[1] && ys[j] <= bhi[1] &&
-                       zs[j] >= blo[2] && zs[j] <= bhi[2] && !(lb[j] > bound);
-            probes += valid[j];
-        }
-        uint2 se[kKnnBatch];
-        idx.batch(xs, ys, zs, valid, se);
-        uint32_t live = 0;
-#pragma unroll
-        for (int j = 0; j < kKnnBatch; ++j) live |= (se[j].y ? 1u : 0u) << j;
-        while (live) {  // one copy of the scan (select the j-th entry without dynamic indexing)
-            const int j = __ffs(live) - 1;
-            live &= live - 1;
-            uint2 sj = se[0];
-            float lj = lb[0];
-#pragma unroll
-            for (int r = 1; r < kKnnBatch; ++r)
-                if (r == j) {
-                    sj = se[r];
-                    lj = lb[r];
-                }
-            if (!(lj > ki_key(T.worst()))) scan_cell_thread<K>(g.spos, sj, qx, qy, qz, T, cands, inserts);
-        }
-    }
-    int m = 1;
-    if (T.worst() == kEmptyKey) {
-        if (level + 1 < g.levels) return false;
-        // finest-possible level exhausted: widen whole shells until the list is full
-        while (T.worst() == kEmptyKey && !qc.covers(m, blo, bhi)) {
-            ++m;
-            const int cnt = shell_count(m);
-            for (int t = 0; t < cnt; ++t) {
-                int dx, dy, dz;
-                shell_cell(m, t, dx, dy, dz);
-                const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
-                if (x < blo[0] || x > bhi[0] || y < blo[1] || y > bhi[1] || z < blo[2] || z > bhi[2]) continue;
-                const float lb = qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2);
-                if (lb > ki_key(T.worst())) continue;
-                ++probes;
-                const uint2 se = idx.one(x, y, z);
-                if (se.y) scan_cell_thread<K>(g.spos, se, qx, qy, qz, T, cands, inserts);
-            }
-        }
-        if (T.worst() == kEmptyKey) return true;  // fewer than K points in the whole cloud
-    }
-    if (ki_key(T.worst()) < qc.certified_key(m) || qc.covers(m, blo, bhi)) return true;
-    const int mm = m;
-    ball_search<true, kKnnBatch>(
-        qc, idx, blo, bhi,
-        [&](int dx, int dy, int dz) { return max(abs(dx), max(abs(dy), abs(dz))) <= mm; },
-        [&](uint2 se) {
-            ++probes;
-            scan_cell_thread<K>(g.spos, se, qx, qy, qz, T, cands, inserts);
-        },
-        [&]() { return ki_key(T.worst()); });
-    return true;
+__device__ __forceinline__ void sort_net(unsigned long long (&L)[K]) {
+    sort_net_step<K, 0>(L);
 }
 
-template <int K>
-__global__ void __launch_bounds__(kKnnThreads) k_knn_thread(KnnArgs a) {
-    const int n = *a.d_n;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const GridView &g = a.g;
-    const float4 e = __ldg(g.spos + (size_t)(g.levels - 1) * g.cap + t);
-    const float qx = e.x, qy = e.y, qz = e.z;
-    const int i = __float_as_int(e.w);
-    int level = g.levels - 1;
-    for (int l = 0; l < g.levels - 1; ++l) {
-        const float inv_h = ldexpf(g.inv_h0, -l);
-        const uint2 se =
-            cell_lookup(g.table, g.mask, cell_key(l, cell_coord(qx, inv_h), cell_coord(qy, inv_h), cell_coord(qz, inv_h)));
-        if (se.y >= (uint32_t)kMinCell) {
-            level = l;
-            break;
-        }
-    }
-    ThreadTopK<K> T;
-    int probes = 0, cands = 0, inserts = 0;
-    while (!knn_search_thread<K>(g, level, qx, qy, qz, T, probes, cands, inserts)) ++level;
-    if (a.debug) a.debug[i] = make_int4(level, probes, cands, inserts);
-    if (a.knn_idx) {
-#pragma unroll
-        for (int j = 0; j < K; ++j)
-            if (j < a.k) a.knn_idx[(size_t)i * a.k + j] = T.L[j] == kEmptyKey ? -1 : (int32_t)ki_idx(T.L[j]);
-    }
-    if (!a.nbr_t) return;
-#pragma unroll
-    for (int j = 0; j < K; ++j)
-        if (j < a.k) a.nbr_t[(size_t)t * kMaxK + j] = T.L[j] == kEmptyKey ? -1 : (int32_t)ki_idx(T.L[j]);
-}
-
-// per-query epilogue (thread per query): covariance (normalised by the count), eigen,
-// regularisation, scattered to input order
-__global__ void __launch_bounds__(kKnnThreads) k_knn_epilogue(KnnArgs a) {
-    const int n = *a.d_n;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const GridView &g = a.g;
-    const int i = __float_as_int(__ldg(g.spos + (size_t)(g.levels - 1) * g.cap + t).w);
-    const float4 q = __ldg(a.pos + i);
-    // moments of the k neighbours about the query (binary64), in list order
-    const int4 *lst = reinterpret_cast<const int4 *>(a.nbr_t + (size_t)t * kMaxK);
-    double s1[3] = {0, 0, 0}, s2[6] = {0, 0, 0, 0, 0, 0};
-    int cnt = 0;
-    for (int j4 = 0; j4 < (a.k + 3) / 4; ++j4) {
-        const int4 w = __ldg(lst + j4);
-        const int ids[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (4 * j4 + u >= a.k || ids[u] < 0) continue;
-            const float4 p = __ldg(a.pos + ids[u]);
-            const double d0 = (double)p.x - (double)q.x, d1 = (double)p.y - (double)q.y, d2 = (double)p.z - (double)q.z;
-            s1[0] += d0;
-            s1[1] += d1;
-            s1[2] += d2;
-            s2[0] += d0 * d0;
-            s2[1] += d0 * d1;
-            s2[2] += d0 * d2;
-            s2[3] += d1 * d1;
-            s2[4] += d1 * d2;
-            s2[5] += d2 * d2;
-            ++cnt;
-        }
-    }
+// moments of the query's neighbours (binary64, in the given order) -> covariance -> eigen ->
+// regularisation -> store (shared by the image-window kernel and the epilogue of the warp search)
+// moments (sum of d, sum of d d^T over the cnt neighbours, d = p - q) -> covariance (/cnt)
+// -> eigen -> regularisation -> store
+__device__ __forceinline__ void finish_moments(const KnnArgs &a, int n, int i, const double (&s1)[3],
+                                               const double (&s2)[6], int cnt) {
     const double inv = 1.0 / (double)cnt;
     const double mu[3] = {s1[0] * inv, s1[1] * inv, s1[2] * inv};
     double C[6] = {s2[0] * inv - mu[0] * mu[0], s2[1] * inv - mu[0] * mu[1], s2[2] * inv - mu[0] * mu[2],
@@ -495,39 +365,705 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_epilogue(KnnArgs a) {
     store_cov(a.cov_a, a.cov_b, i, R, ev.lam[1], flags);
 }
 
-// kNN kernel variant: warp per query (default) or thread per query (GSICP_KNN=thread, A/B only)
-bool knn_use_warp() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("GSICP_KNN");
-        v = (e && strcmp(e, "thread") == 0) ? 0 : 1;
+template <int K>
+__device__ __forceinline__ void finish_query(const KnnArgs &a, int n, int i, float4 q, int k, const int (&ids)[K]) {
+    double s1[3] = {0, 0, 0}, s2[6] = {0, 0, 0, 0, 0, 0};
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        if (j >= k || ids[j] < 0) continue;
+        const float4 p = __ldg(a.pos + ids[j]);
+        const double d0 = (double)p.x - (double)q.x, d1 = (double)p.y - (double)q.y, d2 = (double)p.z - (double)q.z;
+        s1[0] += d0;
+        s1[1] += d1;
+        s1[2] += d2;
+        s2[0] += d0 * d0;
+        s2[1] += d0 * d1;
+        s2[2] += d0 * d2;
+        s2[3] += d1 * d1;
+        s2[4] += d1 * d2;
+        s2[5] += d2 * d2;
+        ++cnt;
     }
-    return v == 1;
+    finish_moments(a, n, i, s1, s2, cnt);
+}
+
+// per-query epilogue of the warp search (thread per query, grid-stride): covariance
+// (normalised by the count), eigen, regularisation, scattered to input order.  Query t is
+// the t-th point in coarsest-cell order, or queue[t] in queue mode.
+template <int K>
+__global__ void __launch_bounds__(kKnnThreads) k_knn_epilogue(KnnArgs a) {
+    const int n = *a.d_n;
+    const int nq = a.queue ? (int)*a.queue_n : n;
+    const GridView &g = a.g;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += gridDim.x * blockDim.x) {
+        const int i = a.queue ? (int)__ldg(a.queue + t)
+                              : __float_as_int(__ldg(g.spos + (size_t)(g.levels - 1) * g.cap + t).w);
+        const int *lst = a.nbr_t + (size_t)t * kMaxK;
+        int ids[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) ids[j] = j < a.k ? __ldg(lst + j) : -1;
+        finish_query<K>(a, n, i, __ldg(a.pos + i), a.k, ids);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Image-window kNN for depth-frame clouds (A1 output: point i <-> lattice pixel (u/s, v/s) of the
+// sampled depth image, pos.w = v*W + u).  A ball B(q, rho) with q_z > rho projects inside the
+// pixel box |u - u_q| <= fx rho (q_z + |q_x|) / (q_z (q_z - rho)) (and likewise in v), because
+// |x/z - x_q/z_q| = |(x - x_q) z_q - x_q (z - z_q)| / (z z_q) <= rho (z_q + |x_q|) / ((z_q - rho) z_q).
+// Sampled pixels differ by multiples of s, so when that bound is < (M+1) s every point within rho
+// of q lies in the (2M+1)^2 lattice window around q's pixel: the window is an exact candidate set
+// for any query whose k-th radius (with rounding margins) passes the bound.
+//   * a block stages a 32x4 tile of lattice pixels plus an M-pixel halo (the points, by a
+//     lattice -> point map) in shared memory; a thread owns one pixel's query and reads its
+//     window as a stencil — no hashing, no divergence;
+//   * exact, insertion-free selection in two passes: pass 1 builds a per-thread histogram of
+//     the window's keys over 32 quarter-octave buckets (float exponent + 2 mantissa bits, offset
+//     so that bucket 16 is (2 * point spacing)^2; shared-memory atomics, one column per thread)
+//     and finds b*, the first bucket whose cumulative count reaches k; pass 2 collects the
+//     m = cum(b*) <= 32 candidates at or below b* and sorts them by (key, index) with a Batcher
+//     network in registers — the first k are the k nearest of the window;
+//   * queries that fail the projection certificate (k-th radius too large for the window: depth
+//     edges, grazing surfaces, image periphery), or whose m exceeds the list, go to a queue that
+//     the grid search finishes (the hash is only built for them).
+constexpr int kImgTX = 32, kImgTY = 4, kImgThreads = kImgTX * kImgTY;
+constexpr int kImgList = 32;
+constexpr int kImgBuckets = 32;
+constexpr int kImgBucketRef = 16;  // bucket of key = (2 * spacing)^2
+constexpr float kImgFar = 1e30f;   // empty lattice pixel: keys overflow to +inf
+// image counters (zeroed by k_img_map_clear): window queue, warp-search work, map conflict flag,
+// hash queue (what the wide window could not certify), wide-pass work, hash point count
+constexpr int kImgCtrQueue = 0, kImgCtrWork = 1, kImgCtrBad = 2, kImgCtrQueue2 = 3, kImgCtrWideWork = 4,
+              kImgCtrHashN = 5, kImgCtrHashQ = 6, kImgCtrQueue3 = 7, kImgCounters = 8;
+constexpr uint32_t kBruteMax = 256;  // a last queue up to this size is searched by brute force
+constexpr int kImgWideM = 12;  // half-width of the wide window (warp per query)
+
+struct ImgArgs {
+    int32_t *map;  // [Hs][Ws] point index of each lattice pixel, -1 if none
+    uint32_t *queue2;
+    int H, W, Hs, Ws, stride;
+    float fx, fy;
+    uint32_t *ctr;
+    uint32_t *queue;
+};
+
+__global__ void k_img_map_clear(ImgArgs im) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < im.Hs * im.Ws) im.map[j] = -1;
+    if (j < kImgCounters) im.ctr[j] = 0u;
+}
+
+// lattice -> point map; a point whose pixel id is not a lattice pixel of this image, or two
+// points on one pixel, flag the cloud as not a depth-frame cloud (then every query is queued)
+__global__ void k_img_map_fill(ImgArgs im, const float4 *__restrict__ pos, const int32_t *__restrict__ d_n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= *d_n) return;
+    const int pix = __float_as_int(__ldg(pos + i).w);
+    const int v = pix / im.W, u = pix - v * im.W;
+    bool ok = pix >= 0 && v < im.H && u % im.stride == 0 && v % im.stride == 0;
+    if (ok) ok = atomicCAS(im.map + (v / im.stride) * im.Ws + u / im.stride, -1, i) == -1;
+    if (!ok) {
+        atomicExch(im.ctr + kImgCtrBad, 1u);
+        im.queue[atomicAdd(im.ctr + kImgCtrQueue, 1u)] = (uint32_t)i;
+    }
+}
+
+// Largest |x'/z' - x/z| over the points (x', z') of the disk of radius rho around (x, z) in the
+// xz-plane (the projection of the 3-D ball on it), +inf if the disk reaches z <= 0: the disk spans
+// the view angles alpha +- beta, tan(alpha) = x/z, sin(beta) = rho/|(x, z)|, and tan is increasing.
+__device__ __forceinline__ double proj_extent(double x, double z, double rho) {
+    const double d = sqrt(x * x + z * z);
+    if (!(z > 0.0) || !(rho < d)) return INFINITY;
+    const double sb = rho / d, cb = sqrt(fmax(1.0 - sb * sb, 0.0));
+    const double sa = x / d, ca = z / d;
+    // tan(alpha +- beta) = (sa cb +- ca sb) / (ca cb -+ sa sb); a non-positive denominator means
+    // the disk reaches the image plane's horizon
+    const double dp = ca * cb - sa * sb, dm = ca * cb + sa * sb;
+    if (!(dp > 0.0) || !(dm > 0.0)) return INFINITY;
+    const double t0 = x / z, tp = (sa * cb + ca * sb) / dp, tm = (sa * cb - ca * sb) / dm;
+    return fmax(tp - t0, t0 - tm) * (1.0 + 1e-9) + 1e-12;
+}
+
+constexpr int kImgM = 5;  // tile-kernel window half-width (lattice pixels)
+
+// certificate: every point within sqrt(key) of q lies inside the lattice window of half-width w
+__device__ __forceinline__ bool img_cert(const ImgArgs &im, float4 q, float key, int w) {
+    const double rho = sqrt((double)key) * (1.0 + 1e-5) + 1e-9;
+    const double bu = proj_extent((double)q.x, (double)q.z, rho) * (double)im.fx;
+    const double bv = proj_extent((double)q.y, (double)q.z, rho) * (double)im.fy;
+    const double win = (double)((w + 1) * im.stride) - 1e-3;
+    return bu < win && bv < win;
+}
+
+template <int K, int M>
+__global__ void __launch_bounds__(kImgThreads, 4) k_knn_image(KnnArgs a, ImgArgs im) {
+    constexpr int SW = kImgTX + 2 * M, SH = kImgTY + 2 * M;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float4(*tile)[SW] = reinterpret_cast<float4(*)[SW]>(smem_raw);
+    uint32_t(*hist)[kImgThreads] = reinterpret_cast<uint32_t(*)[kImgThreads]>(smem_raw + sizeof(float4) * SW * SH);
+    unsigned long long(*list)[kImgThreads] = reinterpret_cast<unsigned long long(*)[kImgThreads]>(
+        smem_raw + sizeof(float4) * SW * SH + sizeof(uint32_t) * (kImgBuckets / 2) * kImgThreads);
+    const int tid = threadIdx.x;
+    const int gx0 = blockIdx.x * kImgTX - M, gy0 = blockIdx.y * kImgTY - M;
+    const bool bad = __ldg(im.ctr + kImgCtrBad) != 0u;
+    for (int t = tid; t < SW * SH; t += kImgThreads) {
+        const int ty = t / SW, tx = t - ty * SW;
+        const int gx = gx0 + tx, gy = gy0 + ty;
+        float4 p = make_float4(kImgFar, kImgFar, kImgFar, __int_as_float(-1));
+        if (gx >= 0 && gx < im.Ws && gy >= 0 && gy < im.Hs) {
+            const int i = __ldg(im.map + gy * im.Ws + gx);
+            if (i >= 0) {
+                p = __ldg(a.pos + i);
+                p.w = __int_as_float(i);
+            }
+        }
+        tile[ty][tx] = p;
+    }
+#pragma unroll
+    for (int b = 0; b < kImgBuckets / 2; ++b) hist[b][tid] = 0u;
+    __syncthreads();
+    const int lx = tid % kImgTX, ly = tid / kImgTX;
+    const float4 q = tile[ly + M][lx + M];
+    const int i = __float_as_int(q.w);
+    if (i < 0) return;  // no point on this pixel (no block-wide sync follows)
+    if (bad) {
+        im.queue[atomicAdd(im.ctr + kImgCtrQueue, 1u)] = (uint32_t)i;
+        return;
+    }
+    const int k = a.k;
+    // bucket kImgBucketRef <-> key (2 * spacing)^2, spacing = s z / fx
+    const float sp = 2.f * (float)im.stride * q.z / im.fx;
+    const int base = (int)(__float_as_uint(fmaxf(sp * sp, 1e-30f)) >> 21) - kImgBucketRef;
+    uint32_t *hcol = &hist[0][tid];
+    // ---- pass 1: histogram of the window's keys (rows not unrolled: keeps the code in i-cache)
+#pragma unroll 1
+    for (int dy = 0; dy <= 2 * M; ++dy) {
+        const float4 *row = &tile[ly + dy][lx];
+#pragma unroll
+        for (int dx = 0; dx <= 2 * M; ++dx) {
+            const float4 P = row[dx];
+            const float key = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
+            const int bk = min(max((int)(__float_as_uint(key) >> 21) - base, 0), kImgBuckets - 1);
+            atomicAdd(hcol + (bk >> 1) * kImgThreads, 1u << ((bk & 1) * 16));
+        }
+    }
+    int bstar = -1;
+    uint32_t cum = 0, m = 0, below = 0;
+#pragma unroll
+    for (int b = 0; b < kImgBuckets / 2; ++b) {
+        const uint32_t wd = hist[b][tid];
+#pragma unroll
+        for (int hb = 0; hb < 2; ++hb) {
+            const uint32_t c = (wd >> (16 * hb)) & 0xFFFFu;
+            if (bstar < 0 && cum + c >= (uint32_t)k) {
+                bstar = 2 * b + hb;
+                below = cum;
+                m = cum + c;
+            }
+            cum += c;
+        }
+    }
+    bool ok = bstar >= 0 && m <= (uint32_t)kImgList;
+    if (ok) {
+        // ---- pass 2: the candidates at or below b*, in stencil order: those below b* are all
+        // among the k nearest; the boundary bucket's go to the end of the list and only the
+        // (k - below) smallest of them by (key, index) are kept
+        const uint32_t lo_lim = (uint32_t)(base + bstar) << 21;  // keys below bucket b*
+        const uint32_t lim = bstar >= kImgBuckets - 1 ? 0x7F800000u : (uint32_t)(base + bstar + 1) << 21;
+        int nlo = 0, nbd = 0;
+#pragma unroll 1
+        for (int dy = 0; dy <= 2 * M; ++dy) {
+            const float4 *row = &tile[ly + dy][lx];
+#pragma unroll
+            for (int dx = 0; dx <= 2 * M; ++dx) {
+                const float4 P = row[dx];
+                const float key = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
+                const uint32_t kb = __float_as_uint(key);
+                if (kb < lim && kb < 0x7F800000u) {
+                    const unsigned long long e = pack_ki(key, (uint32_t)__float_as_int(P.w));
+                    const bool lo = bstar > 0 && kb < lo_lim;
+                    const int slot = lo ? nlo : kImgList - 1 - nbd;  // boundary entries from the top
+                    if (nlo + nbd < kImgList) list[slot][tid] = e;
+                    nlo += lo ? 1 : 0;
+                    nbd += lo ? 0 : 1;
+                }
+            }
+        }
+        ok = nlo + nbd == (int)m && nlo == (int)below;
+        if (ok) {
+            // keep the r smallest boundary entries (rank by (key, index) among them): a bit mask
+            // over the boundary slots (boundary entry j sits in slot kImgList-1-j)
+            const int r = k - nlo;
+            unsigned long long kth = 0ull;
+            uint32_t sel = 0u;
+            for (int j = 0; j < nbd; ++j) {
+                const unsigned long long e = list[kImgList - 1 - j][tid];
+                int rank = 0;
+                for (int l = 0; l < nbd; ++l) rank += list[kImgList - 1 - l][tid] < e ? 1 : 0;
+                if (rank < r) {
+                    sel |= 1u << j;
+                    kth = e > kth ? e : kth;
+                }
+            }
+            ok = img_cert(im, q, ki_key(kth), M);
+            if (a.debug) a.debug[i] = make_int4(ok ? -1 : -2, M, (int)m, 0);
+            if (ok) {
+                if (a.knn_idx) {  // sorted neighbour list (API output only)
+                    unsigned long long L[kImgList];
+#pragma unroll
+                    for (int j = 0; j < kImgList; ++j) {
+                        const bool take = j < nlo || (j >= kImgList - nbd && ((sel >> (kImgList - 1 - j)) & 1u));
+                        L[j] = take ? list[j][tid] : kEmptyKey;
+                    }
+                    sort_net<kImgList>(L);
+#pragma unroll
+                    for (int j = 0; j < K; ++j)
+                        if (j < k) a.knn_idx[(size_t)i * k + j] = (int32_t)ki_idx(L[j]);
+                }
+                // moments in list order (the sure entries, then the kept boundary entries, each in
+                // stencil order: deterministic), then the A4 epilogue
+                double s1[3] = {0, 0, 0}, s2[6] = {0, 0, 0, 0, 0, 0};
+                auto acc = [&](unsigned long long e) {
+                    const float4 p = __ldg(a.pos + ki_idx(e));
+                    const double d0 = (double)p.x - (double)q.x, d1 = (double)p.y - (double)q.y,
+                                 d2 = (double)p.z - (double)q.z;
+                    s1[0] += d0;
+                    s1[1] += d1;
+                    s1[2] += d2;
+                    s2[0] += d0 * d0;
+                    s2[1] += d0 * d1;
+                    s2[2] += d0 * d2;
+                    s2[3] += d1 * d1;
+                    s2[4] += d1 * d2;
+                    s2[5] += d2 * d2;
+                };
+                for (int j = 0; j < nlo; ++j) acc(list[j][tid]);
+                for (int j = 0; j < nbd; ++j)
+                    if ((sel >> j) & 1u) acc(list[kImgList - 1 - j][tid]);
+                const int nsel = nlo + __popc(sel);
+                finish_moments(a, *a.d_n, i, s1, s2, nsel);
+            }
+        }
+    }
+    if (!ok) im.queue[atomicAdd(im.ctr + kImgCtrQueue, 1u)] = (uint32_t)i;
+}
+
+// Wide window for the queries the tile kernel could not certify: warp per query, lanes split the
+// (2 kImgWideM + 1)^2 window (lattice -> point map and positions read through L1/L2), per-lane
+// histogram columns summed across the warp, the m <= 32 candidates at or below b* compacted one
+// per lane and sorted by a warp bitonic network; same certificate.  Misses go to the hash queue.
+// One wide-window attempt of half-width M2 for query q (pixel us, vs) by the calling warp.
+// CACHE: the lane's window keys stay in registers across the histogram passes (small windows);
+// otherwise they are recomputed from the map each pass.  Returns true (and finishes the query) if
+// the k nearest of the window certify.  `fail` = 1: certificate failed (try a wider window),
+// 2: no usable boundary bucket (too few points, or more than 64 at or below b*).
+template <int K, int M2, bool CACHE>
+__device__ bool wide_attempt(const KnnArgs &a, const ImgArgs &im, int i, float4 q, int us, int vs, int lane,
+                             uint32_t (*hist)[32], unsigned long long *lst, int &fail) {
+    constexpr int SIDE = 2 * M2 + 1, CELLS = SIDE * SIDE, PER = (CELLS + 31) / 32;
+    const int k = a.k;
+    int cidx[CACHE ? PER : 1];
+    float ckey[CACHE ? PER : 1];
+    auto cell_key_of = [&](int j, int &idx) -> float {
+        const int c = lane + 32 * j;
+        const int x = us + c % SIDE - M2, y = vs + c / SIDE - M2;
+        idx = (c < CELLS && x >= 0 && x < im.Ws && y >= 0 && y < im.Hs) ? __ldg(im.map + y * im.Ws + x) : -1;
+        if (idx < 0) return INFINITY;
+        const float4 P = __ldg(a.pos + idx);
+        return canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
+    };
+    if (CACHE) {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int c = lane + 32 * j;
+            const int x = us + c % SIDE - M2, y = vs + c / SIDE - M2;
+            cidx[j] = (c < CELLS && x >= 0 && x < im.Ws && y >= 0 && y < im.Hs) ? __ldg(im.map + y * im.Ws + x) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            ckey[j] = INFINITY;
+            if (cidx[j] >= 0) {
+                const float4 P = __ldg(a.pos + cidx[j]);
+                ckey[j] = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
+            }
+        }
+    }
+    auto get = [&](int j, int &idx) -> float {
+        if (CACHE) {
+            float kk = ckey[0];
+            idx = cidx[0];
+#pragma unroll
+            for (int r = 1; r < (CACHE ? PER : 1); ++r)
+                if (r == j) {
+                    kk = ckey[r];
+                    idx = cidx[r];
+                }
+            return kk;
+        }
+        return cell_key_of(j, idx);
+    };
+    // histogram over 32 quarter-octave buckets; if the k-th falls in the open top bucket, shift
+    // the scale up 16 buckets (4 octaves in key) and count again
+    const float sp = 2.f * (float)im.stride * q.z / im.fx;
+    int base = (int)(__float_as_uint(fmaxf(sp * sp, 1e-30f)) >> 21) - kImgBucketRef;
+    int bstar = -1;
+    uint32_t m = 0;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+#pragma unroll
+        for (int b = 0; b < kImgBuckets / 2; ++b) hist[b][lane] = 0u;
+#pragma unroll(CACHE ? PER : 4)
+        for (int j = 0; j < PER; ++j) {
+            int idx;
+            const float key = get(j, idx);
+            if (key < INFINITY) {
+                const int bk = min(max((int)(__float_as_uint(key) >> 21) - base, 0), kImgBuckets - 1);
+                atomicAdd(&hist[bk >> 1][lane], 1u << ((bk & 1) * 16));
+            }
+        }
+        __syncwarp();
+        bstar = -1;
+        uint32_t cum = 0;
+#pragma unroll
+        for (int b = 0; b < kImgBuckets / 2; ++b) {
+            const uint32_t wd = __reduce_add_sync(kFull, hist[b][lane]);
+#pragma unroll
+            for (int hb = 0; hb < 2; ++hb) {
+                cum += (wd >> (16 * hb)) & 0xFFFFu;
+                if (bstar < 0 && cum >= (uint32_t)k) {
+                    bstar = 2 * b + hb;
+                    m = cum;
+                }
+            }
+        }
+        __syncwarp();
+        if (bstar != kImgBuckets - 1) break;
+        base += 16;
+    }
+    if (bstar < 0 || m > 64u) {
+        fail = 2;
+        return false;
+    }
+    // the m <= 64 candidates at or below b*, two per lane, sorted: the 32 smallest end up in
+    // order across the lanes (lane j: j-th)
+    const uint32_t lim = bstar >= kImgBuckets - 1 ? 0x7F800000u : (uint32_t)(base + bstar + 1) << 21;
+    int nl = 0;
+#pragma unroll(CACHE ? PER : 4)
+    for (int j = 0; j < PER; ++j) {
+        int idx;
+        const float key = get(j, idx);
+        const bool take = __float_as_uint(key) < lim && key < INFINITY;
+        const unsigned bb = __ballot_sync(kFull, take);
+        const int slot = nl + __popc(bb & ((1u << lane) - 1u));
+        if (take && slot < 64) lst[slot] = pack_ki(key, (uint32_t)idx);
+        nl += __popc(bb);
+    }
+    __syncwarp();
+    if (nl < k || nl > 64) {
+        fail = 2;
+        return false;
+    }
+    unsigned long long A = lane < nl ? lst[lane] : kEmptyKey;
+    unsigned long long B = lane + 32 < nl ? lst[lane + 32] : kEmptyKey;
+    __syncwarp();
+    A = WarpTopK<32>::sort_w<32>(A, lane);
+    if (nl > 32) {
+        B = WarpTopK<32>::sort_w<32>(B, lane);
+        const unsigned long long Br = shfl_u64(B, 31 - lane);  // descending
+        A = WarpTopK<32>::merge32(A < Br ? A : Br, lane);      // the 32 smallest, a bitonic merge
+    }
+    const unsigned long long last = shfl_u64(A, k - 1);
+    if (!img_cert(im, q, ki_key(last), M2)) {
+        fail = 1;
+        return false;
+    }
+    if (a.knn_idx && lane < k) a.knn_idx[(size_t)i * k + lane] = (int32_t)ki_idx(A);
+    int ids[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) ids[j] = (int)ki_idx(shfl_u64(A, j));
+    if (a.debug && lane == 0) a.debug[i] = make_int4(-3, M2, (int)m, 0);
+    if (lane == 0) finish_query<K>(a, *a.d_n, i, q, k, ids);
+    return true;
+}
+
+// Wide window for the queries the tile kernel could not certify: warp per query, half-width
+// kImgWideM (keys cached in registers).  Misses go to the last queue.
+template <int K>
+__global__ void __launch_bounds__(128) k_knn_image_wide(KnnArgs a, ImgArgs im) {
+    __shared__ uint32_t hist[4][kImgBuckets / 2][32];
+    __shared__ unsigned long long lst[4][64];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int nq = (int)*(im.ctr + kImgCtrQueue);
+    const bool bad = __ldg(im.ctr + kImgCtrBad) != 0u;
+    for (;;) {
+        int t = 0;
+        if (lane == 0) t = (int)atomicAdd(im.ctr + kImgCtrWideWork, 1u);
+        t = __shfl_sync(kFull, t, 0);
+        if (t >= nq) return;
+        const int i = (int)__ldg(im.queue + t);
+        const float4 q = __ldg(a.pos + i);
+        bool ok = false;
+        if (!bad) {
+            const int pix = __float_as_int(q.w);
+            const int v = pix / im.W, u = pix - v * im.W;
+            const int us = u / im.stride, vs = v / im.stride;
+            int fail = 0;
+            ok = wide_attempt<K, kImgWideM, true>(a, im, i, q, us, vs, lane, hist[wib], lst[wib], fail);
+            if (!ok && a.debug && lane == 0) a.debug[i] = make_int4(fail == 1 ? -4 : -5, 0, 0, 0);
+        }
+        if (!ok && lane == 0) im.queue2[atomicAdd(im.ctr + kImgCtrQueue2, 1u)] = (uint32_t)i;
+        __syncwarp();
+    }
+}
+
+// The last queue: up to kBruteMax queries are searched by brute force over the whole cloud
+// (exact by definition — no certificate), a block per query with the same two-pass histogram
+// selection (bucket scale shifted until the boundary bucket is a proper one); a longer queue
+// (e.g. a cloud that is not a depth frame) goes to the hash search.
+constexpr int kBruteThreads = 512;
+
+// block-wide sum of per-thread histogram columns hist[16][T] (two 16-bit counters per word) into
+// tot[32] (32-bit); ends with a barrier
+template <int T>
+__device__ __forceinline__ void block_hist_sum(uint32_t (*hist)[T], uint32_t (*part)[kImgBuckets], uint32_t *tot) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < kImgBuckets / 2; ++b) {
+        const uint32_t wd = hist[b][tid];
+        const uint32_t lo = __reduce_add_sync(kFull, wd & 0xFFFFu), hi = __reduce_add_sync(kFull, wd >> 16);
+        if (lane == 0) {
+            part[warp][2 * b] = lo;
+            part[warp][2 * b + 1] = hi;
+        }
+    }
+    __syncthreads();
+    if (tid < kImgBuckets) {
+        uint32_t c = 0;
+        for (int w2 = 0; w2 < T / 32; ++w2) c += part[w2][tid];
+        tot[tid] = c;
+    }
+    __syncthreads();
+}
+
+template <int K>
+__global__ void __launch_bounds__(kBruteThreads) k_knn_brute(KnnArgs a, ImgArgs im) {
+    __shared__ uint32_t hist[kImgBuckets / 2][kBruteThreads];
+    __shared__ uint32_t part[kBruteThreads / 32][kImgBuckets];
+    __shared__ uint32_t tot[kImgBuckets];
+    __shared__ unsigned long long lst[64];
+    __shared__ int s_nl, s_nb;
+    const uint32_t nq = *(im.ctr + kImgCtrQueue2);
+    if (nq == 0u || nq > kBruteMax) return;
+    const int n = *a.d_n, k = a.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // boundary of a histogram: first bucket where the count (plus `below`) reaches k
+    auto boundary = [&](uint32_t below, uint32_t &cum_lo, uint32_t &cum_hi) {
+        uint32_t cum = below;
+        for (int b = 0; b < kImgBuckets; ++b) {
+            if (cum + tot[b] >= (uint32_t)k) {
+                cum_lo = cum;
+                cum_hi = cum + tot[b];
+                return b;
+            }
+            cum += tot[b];
+        }
+        cum_lo = cum_hi = cum;
+        return -1;
+    };
+    for (uint32_t t = blockIdx.x; t < nq; t += gridDim.x) {
+        const int i = (int)__ldg(im.queue2 + t);
+        const float4 q = __ldg(a.pos + i);
+        // pass 1: octave histogram of all keys (key exponent, octaves 2^-20 .. 2^11 m^2, clamped)
+#pragma unroll
+        for (int b = 0; b < kImgBuckets / 2; ++b) hist[b][tid] = 0u;
+#pragma unroll 16
+        for (int j = tid; j < n; j += kBruteThreads) {
+            const float4 P = __ldg(a.pos + j);
+            const float key = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
+            const int bk = min(max((int)(__float_as_uint(key) >> 23) - (127 - 20), 0), kImgBuckets - 1);
+            atomicAdd(&hist[bk >> 1][tid], 1u << ((bk & 1) * 16));
+        }
+        block_hist_sum<kBruteThreads>(hist, part, tot);
+        uint32_t lo1, hi1;
+        const int o = boundary(0u, lo1, hi1);
+        // keys of octave bucket o: exponent field e_o (bucket 0 and 31 are open-ended)
+        uint32_t klo = 0u, khi = 0x7F800000u;  // collect range [klo, khi) of key bits
+        uint32_t below = o >= 0 ? lo1 : 0u, m = hi1;  // (o < 0: fewer than k points, all boundary)
+        bool ok = o >= 0 || (uint32_t)n < (uint32_t)k;
+        if (o > 0 && o < kImgBuckets - 1) {
+            // pass 2: 32 sub-buckets of that octave (the top 5 mantissa bits)
+            const uint32_t e = (uint32_t)(o + 127 - 20);
+#pragma unroll
+            for (int b = 0; b < kImgBuckets / 2; ++b) hist[b][tid] = 0u;
+            __syncthreads();
+#pragma unroll 16
+            for (int j = tid; j < n; j += kBruteThreads) {
+                const float4 P = __ldg(a.pos + j);
+                const uint32_t kb = __float_as_uint(canon_key(q.x, q.y, q.z, P.x, P.y, P.z));
+                if ((kb >> 23) == e) {
+                    const int bk = (int)((kb >> 18) & 31u);
+                    atomicAdd(&hist[bk >> 1][tid], 1u << ((bk & 1) * 16));
+                }
+            }
+            block_hist_sum<kBruteThreads>(hist, part, tot);
+            uint32_t lo2, hi2;
+            const int sb = boundary(lo1, lo2, hi2);
+            below = lo2;
+            m = hi2;
+            klo = (e << 23) | ((uint32_t)sb << 18);
+            khi = klo + (1u << 18);
+        } else if (o == 0) {
+            khi = (uint32_t)(127 - 20 + 1) << 23;
+        } else if (o == kImgBuckets - 1) {
+            klo = (uint32_t)(127 - 20 + kImgBuckets - 1) << 23;
+        }
+        // every key below klo is among the k nearest (`below` of them); [klo, khi) is the boundary
+        if (!ok || m - below > 64u) {  // > 64 near-equal keys at the boundary: hand over to the hash
+            if (tid == 0) im.queue[atomicAdd(im.ctr + kImgCtrQueue3, 1u)] = (uint32_t)i;
+            __syncthreads();
+            continue;
+        }
+        // pass 3: the k nearest = the `below` keys < klo (list slots 0..) plus the `need` smallest of
+        // the boundary range [klo, khi) (slots 32.. ; at most 32 of each)
+        if (tid == 0) {
+            s_nl = 0;
+            s_nb = 0;
+        }
+        __syncthreads();
+        const int need = k - (int)below;
+#pragma unroll 16
+        for (int j = tid; j < n; j += kBruteThreads) {
+            const float4 P = __ldg(a.pos + j);
+            const float key = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
+            const uint32_t kb = __float_as_uint(key);
+            if (kb < khi && key < INFINITY) {
+                const bool lo = kb < klo;
+                const int slot = atomicAdd(lo ? &s_nl : &s_nb, 1);
+                if (slot < 32) lst[(lo ? 0 : 32) + slot] = pack_ki(key, (uint32_t)j);
+            }
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int nl = s_nl, nb = s_nb;
+            if (nb > 32 || nl > 32) {  // boundary too crowded for one warp: hand over to the hash
+                if (lane == 0) im.queue[atomicAdd(im.ctr + kImgCtrQueue3, 1u)] = (uint32_t)i;
+            } else {
+                // boundary entries sorted; lanes [0, need) take them after the `below` ones
+                unsigned long long B = lane < nb ? lst[32 + lane] : kEmptyKey;
+                B = WarpTopK<32>::sort_w<32>(B, lane);
+                const unsigned long long Bsh = shfl_u64(B, (lane - nl) & 31);
+                unsigned long long A = lane < nl ? lst[lane] : (lane < nl + need ? Bsh : kEmptyKey);
+                A = WarpTopK<32>::sort_w<32>(A, lane);
+                if (a.knn_idx && lane < k) a.knn_idx[(size_t)i * k + lane] = A == kEmptyKey ? -1 : (int32_t)ki_idx(A);
+                int ids[K];
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const unsigned long long v = shfl_u64(A, j);
+                    ids[j] = v == kEmptyKey ? -1 : (int)ki_idx(v);
+                }
+                if (a.debug && lane == 0) a.debug[i] = make_int4(-6, 0, (int)m, 0);
+                if (lane == 0) finish_query<K>(a, n, i, q, k, ids);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// the hash path takes the last queue when it is longer than kBruteMax, else whatever brute force
+// handed over (moved to the front of queue 2)
+__global__ void k_img_hash_n(ImgArgs im, const int32_t *__restrict__ d_n) {
+    const uint32_t q2 = im.ctr[kImgCtrQueue2], q3 = im.ctr[kImgCtrQueue3];
+    uint32_t hq = 0u;
+    if (q2 > kBruteMax) {
+        hq = q2;
+    } else if (q3 > 0u) {
+        for (uint32_t j = 0; j < q3; ++j) im.queue2[j] = im.queue[j];
+        hq = q3;
+    }
+    im.ctr[kImgCtrHashN] = hq ? (uint32_t)*d_n : 0u;
+    im.ctr[kImgCtrHashQ] = hq;
+}
+
+template <int K>
+cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s);
+template <int K>
+cudaError_t launch_epilogue(const KnnArgs &a, int cap, cudaStream_t s);
+
+template <int K>
+cudaError_t launch_tile(const KnnArgs &a, const ImgArgs &im, cudaStream_t s) {
+    constexpr int M = kImgM, SW = kImgTX + 2 * M, SH = kImgTY + 2 * M;
+    const int smem = (int)(sizeof(float4) * SW * SH + sizeof(uint32_t) * (kImgBuckets / 2) * kImgThreads +
+                           sizeof(unsigned long long) * kImgList * kImgThreads);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_knn_image<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    const dim3 grid((unsigned)((im.Ws + kImgTX - 1) / kImgTX), (unsigned)((im.Hs + kImgTY - 1) / kImgTY));
+    k_knn_image<K, M><<<grid, kImgThreads, smem, s>>>(a, im);
+    GSICP_LAUNCH_CHECK("k_knn_image");
+    return cudaSuccess;
+}
+
+template <int K>
+cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *pos, const int32_t *d_n, cudaStream_t s) {
+    ktimer_mark(KT_KNN_SEARCH, false, s);
+    const int L = im.Hs * im.Ws;
+    k_img_map_clear<<<blocks_for(std::max(L, kImgCounters), 256), 256, 0, s>>>(im);
+    GSICP_LAUNCH_CHECK("k_img_map_clear");
+    k_img_map_fill<<<blocks_for(cap, 256), 256, 0, s>>>(im, pos, d_n);
+    GSICP_LAUNCH_CHECK("k_img_map_fill");
+    cudaError_t e = launch_tile<K>(a, im, s);
+    if (e != cudaSuccess) return e;
+    ktimer_mark(KT_KNN_SEARCH, true, s);
+    // wide window over the queue (a resident grid pulling queries)
+    k_knn_image_wide<K><<<(unsigned)num_sms() * 8, 128, 0, s>>>(a, im);
+    GSICP_LAUNCH_CHECK("k_knn_image_wide");
+    // the rest: brute force (a short queue) or hash the cloud, warp search, epilogue (long queue)
+    k_knn_brute<K><<<(unsigned)num_sms(), kBruteThreads, 0, s>>>(a, im);
+    GSICP_LAUNCH_CHECK("k_knn_brute");
+    k_img_hash_n<<<1, 1, 0, s>>>(im, d_n);
+    GSICP_LAUNCH_CHECK("k_img_hash_n");
+    const int32_t *hn = reinterpret_cast<const int32_t *>(im.ctr + kImgCtrHashN);
+    e = grid_build(a.g, pos, nullptr, nullptr, hn, cap, s);
+    if (e != cudaSuccess) return e;
+    a.queue = im.queue2;
+    a.queue_n = im.ctr + kImgCtrHashQ;
+    a.work = im.ctr + kImgCtrWork;
+    e = launch_search<K>(a, cap, s);
+    if (e != cudaSuccess) return e;
+    e = launch_epilogue<K>(a, cap, s);
+    if (e != cudaSuccess) return e;
+    note_launch(8);
+    return cudaSuccess;
 }
 
 template <int K>
 cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s) {
-    const bool timed = a.nbr_t != nullptr;  // the covariance search (not the target graph build)
-    if (timed) ktimer_mark(KT_KNN_SEARCH, false, s);
-    if (knn_use_warp()) {
-        // a resident grid (one wave) pulling work batches; never more warps than batches
-        const long long warps = (cap + kQueriesPerWarp - 1) / kQueriesPerWarp;
-        const long long blocks = std::min<long long>(blocks_for(warps * 32, kKnnThreads), (long long)num_sms() * kKnnMinBlocks);
-        k_knn_search<K><<<(unsigned)std::max<long long>(blocks, 1), kKnnThreads, 0, s>>>(a);
-    } else {
-        k_knn_thread<K><<<blocks_for(cap, kKnnThreads), kKnnThreads, 0, s>>>(a);
-    }
+    // a resident grid (one wave) pulling work batches; never more warps than batches
+    const long long warps = (cap + kQueriesPerWarp - 1) / kQueriesPerWarp;
+    const long long blocks = std::min<long long>(blocks_for(warps * 32, kKnnThreads), (long long)num_sms() * kKnnMinBlocks);
+    k_knn_search<K><<<(unsigned)std::max<long long>(blocks, 1), kKnnThreads, 0, s>>>(a);
     GSICP_LAUNCH_CHECK("k_knn_search");
-    if (timed) ktimer_mark(KT_KNN_SEARCH, true, s);
+    return cudaSuccess;
+}
+
+template <int K>
+cudaError_t launch_epilogue(const KnnArgs &a, int cap, cudaStream_t s) {
+    const long long blocks = std::min<long long>(blocks_for(cap, kKnnThreads), (long long)num_sms() * 16);
+    k_knn_epilogue<K><<<(unsigned)std::max<long long>(blocks, 1), kKnnThreads, 0, s>>>(a);
+    GSICP_LAUNCH_CHECK("k_knn_epilogue");
     return cudaSuccess;
 }
 
 template <int K>
 cudaError_t launch_k(const KnnArgs &a, int cap, cudaStream_t s) {
+    ktimer_mark(KT_KNN_SEARCH, false, s);
     cudaError_t e = launch_search<K>(a, cap, s);
     if (e != cudaSuccess) return e;
-    k_knn_epilogue<<<blocks_for(cap, kKnnThreads), kKnnThreads, 0, s>>>(a);
-    GSICP_LAUNCH_CHECK("k_knn_epilogue");
+    ktimer_mark(KT_KNN_SEARCH, true, s);
+    e = launch_epilogue<K>(a, cap, s);
+    if (e != cudaSuccess) return e;
     note_launch(2);
     return cudaSuccess;
 }
@@ -541,7 +1077,7 @@ size_t covariances_ws_bytes(int cap, int levels) {
 cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, int k, int mode, float eps,
                                float cell0, int levels, float *cov_a, float *cov_b, int32_t *knn_idx, void *ws,
                                cudaStream_t s) {
-    KnnArgs a;
+    KnnArgs a{};
     a.g = grid_carve(ws, cap, levels, false, cell0);
     a.pos = reinterpret_cast<const float4 *>(pos);
     a.d_n = d_n;
@@ -553,6 +1089,7 @@ cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, in
     a.knn_idx = knn_idx;
     a.debug = reinterpret_cast<int4 *>(g_knn_debug);
     a.nbr_t = reinterpret_cast<int32_t *>(static_cast<char *>(ws) + grid_bytes(cap, levels, false));
+    a.work = a.g.counters + kMaxLevels;
     cudaError_t e = grid_build(a.g, a.pos, nullptr, nullptr, d_n, cap, s);
     if (e != cudaSuccess) return e;
     if (k <= 4) return launch_k<4>(a, cap, s);
@@ -576,10 +1113,58 @@ cudaError_t knn_graph_launch(const GridView &g, const float4 *pos, const int32_t
     a.knn_idx = knn_idx;
     a.nbr_t = nullptr;
     a.debug = nullptr;
+    a.work = g.counters + kMaxLevels;
     cudaError_t e = launch_search<kGraphK>(a, cap, s);
     if (e != cudaSuccess) return e;
     note_launch();
     return cudaSuccess;
+}
+
+size_t covariances_image_ws_bytes(int cap, int levels, int H, int W, int stride) {
+    const size_t L = (size_t)((H + stride - 1) / stride) * (size_t)((W + stride - 1) / stride);
+    return covariances_ws_bytes(cap, levels) + align_up(L * sizeof(int32_t)) +
+           2 * align_up((size_t)cap * sizeof(uint32_t)) + align_up(kImgCounters * sizeof(uint32_t));
+}
+
+cudaError_t covariances_image_launch(const float *pos, const int32_t *d_n, int cap, int H, int W, int stride,
+                                     gsicp_intrinsics Kin, int k, int mode, float eps, float cell0, int levels,
+                                     float *cov_a, float *cov_b, int32_t *knn_idx, void *ws, cudaStream_t s) {
+    KnnArgs a{};
+    a.g = grid_carve(ws, cap, levels, false, cell0);
+    a.pos = reinterpret_cast<const float4 *>(pos);
+    a.d_n = d_n;
+    a.k = k;
+    a.mode = mode;
+    a.eps = (double)eps;
+    a.cov_a = reinterpret_cast<float4 *>(cov_a);
+    a.cov_b = reinterpret_cast<float4 *>(cov_b);
+    a.knn_idx = knn_idx;
+    a.debug = reinterpret_cast<int4 *>(g_knn_debug);
+    char *p = static_cast<char *>(ws) + grid_bytes(cap, levels, false);
+    a.nbr_t = reinterpret_cast<int32_t *>(p);
+    p += align_up((size_t)cap * kMaxK * sizeof(int32_t));
+    ImgArgs im{};
+    im.H = H;
+    im.W = W;
+    im.stride = stride;
+    im.Hs = (H + stride - 1) / stride;
+    im.Ws = (W + stride - 1) / stride;
+    im.fx = Kin.fx;
+    im.fy = Kin.fy;
+    im.map = reinterpret_cast<int32_t *>(p);
+    p += align_up((size_t)im.Hs * im.Ws * sizeof(int32_t));
+    im.queue = reinterpret_cast<uint32_t *>(p);
+    p += align_up((size_t)cap * sizeof(uint32_t));
+    im.queue2 = reinterpret_cast<uint32_t *>(p);
+    p += align_up((size_t)cap * sizeof(uint32_t));
+    im.ctr = reinterpret_cast<uint32_t *>(p);
+    const float4 *p4 = a.pos;
+    if (k <= 4) return launch_image<4>(a, im, cap, p4, d_n, s);
+    if (k <= 8) return launch_image<8>(a, im, cap, p4, d_n, s);
+    if (k <= 16) return launch_image<16>(a, im, cap, p4, d_n, s);
+    if (k <= 20) return launch_image<20>(a, im, cap, p4, d_n, s);
+    if (k <= 24) return launch_image<24>(a, im, cap, p4, d_n, s);
+    return launch_image<32>(a, im, cap, p4, d_n, s);
 }
 
 }  // namespace gsicp

@@ -106,10 +106,17 @@ def test_backproject_edge_cases(g):
 
 
 # ----------------------------------------------------------------------------------------- A2-A4
-def _cov_check(g, xyz_np, pos, d_n, k=20, mode=oracle.ELLIPSE, cell0=0.01, levels=5, sample=None, brute_max=60000):
+def _cov_check(g, xyz_np, pos, d_n, k=20, mode=oracle.ELLIPSE, cell0=0.01, levels=5, sample=None, brute_max=60000,
+               image=None):
+    """image = (H, W, stride, K): run the image-window path (gsicp_covariances_image) instead."""
     n = xyz_np.shape[0]
     knn = torch.full((pos.shape[0], k), -7, dtype=torch.int32, device=DEV)
-    cl = g.covariances(pos, d_n, k=k, mode=mode, eps_var=1e-3, cell0=cell0, levels=levels, knn_idx=knn)
+    if image is None:
+        cl = g.covariances(pos, d_n, k=k, mode=mode, eps_var=1e-3, cell0=cell0, levels=levels, knn_idx=knn)
+    else:
+        H, W, s, K = image
+        cl = g.covariances_image(pos, d_n, H, W, s, (K.fx, K.fy, K.cx, K.cy), k=k, mode=mode, eps_var=1e-3,
+                                 cell0=cell0, levels=levels, knn_idx=knn)
     gk = knn[:n].cpu().numpy()
     gc = cl.cov6()[:n].cpu().numpy()
     gf = cl.flags()[:n].cpu().numpy()
@@ -173,6 +180,50 @@ def test_knn_cov_grid_params_do_not_change_results(g, replica, levels, cell0):
     _cov_check(g, xyz, pos, d_n, cell0=cell0, levels=levels, sample=3000)
 
 
+# ----------------------------------------------------------------------------------------- A3/A4 image window
+@pytest.mark.parametrize("case", ["c1", "replica4", "tum1", "tum3", "tum4"])
+def test_knn_cov_image_window(g, c1, replica, tum, case):
+    """gsicp_covariances_image == the oracle's brute-force kNN (bit-exact) and covariances."""
+    w, s = {"c1": (c1, 1), "replica4": (replica, 4), "tum1": (tum, 1), "tum3": (tum, 3), "tum4": (tum, 4)}[case]
+    K = w.K
+    H, W = w.depth.shape
+    pos, d_n = gpu_points(g, w.depth, K, s)
+    xyz, _ = oracle.backproject(w.depth, K.fx, K.fy, K.cx, K.cy, s)
+    ks = (1, 5, 20, 32) if case == "c1" else (20,)
+    for k in ks:
+        _cov_check(g, xyz, pos, d_n, k=k, cell0=3.0 * s / K.fx, levels=4, image=(H, W, s, K),
+                   sample=4000 if case == "tum1" else None)
+
+
+def test_knn_cov_image_window_modes_and_ties(g, replica):
+    """PLANE / NONE modes, and a fronto-parallel wall (tie-heavy lattice), through the image path."""
+    K = replica.K
+    H, W = replica.depth.shape
+    pos, d_n = gpu_points(g, replica.depth, K, 4)
+    xyz, _ = oracle.backproject(replica.depth, K.fx, K.fy, K.cx, K.cy, 4)
+    for mode in (oracle.NONE, oracle.PLANE):
+        _cov_check(g, xyz, pos, d_n, mode=mode, cell0=0.02, levels=4, image=(H, W, 4, K))
+    wall = np.full((96, 128), 2.0, np.float32)
+    wall[40:60, 50:90] = np.nan  # a hole
+    Kw = synth.Intrinsics(W=128, H=96, fx=64.0, fy=64.0, cx=63.5, cy=47.5)
+    pos, d_n = gpu_points(g, wall, Kw, 1)
+    xyz, _ = oracle.backproject(wall, Kw.fx, Kw.fy, Kw.cx, Kw.cy, 1)
+    _cov_check(g, xyz, pos, d_n, cell0=0.1, levels=3, image=(96, 128, 1, Kw))
+
+
+def test_knn_cov_image_window_non_frame_cloud(g):
+    """A cloud whose pixel ids are not a lattice of the image is detected and searched by the hash."""
+    rng = np.random.default_rng(11)
+    n = 3000
+    xyz = rng.normal(size=(n, 3)).astype(np.float32) + np.float32([0, 0, 4])
+    pos = torch.zeros((n, 4), dtype=torch.float32, device=DEV)
+    pos[:, :3] = t(xyz)
+    pos[:, 3] = t(np.zeros(n, np.int32).view(np.float32))  # every point claims pixel 0
+    d_n = torch.tensor([n], dtype=torch.int32, device=DEV)
+    K = synth.make_c1(1).K
+    _cov_check(g, xyz, pos, d_n, cell0=0.3, levels=3, image=(48, 64, 1, K))
+
+
 def test_knn_cov_ragged_and_low_support(g):
     rng = np.random.default_rng(9)
     for n, cap in ((5, 64), (19, 19), (20, 1000), (1000, 1037), (4097, 5000)):
@@ -200,14 +251,16 @@ def test_knn_cov_degenerate_clouds(g):
             _cov_check(g, xyz, pos, d_n, mode=mode, cell0=0.02, levels=2)
 
 
-def test_knn_cov_map_c4_sampled(g):
-    """C4-style: kNN covariance of a 4e6-point map (sampled queries vs brute force)."""
+@pytest.mark.parametrize("cell,levels", [(2.5, 1), (3.0, 3)])
+def test_knn_cov_map_c4_sampled(g, cell, levels):
+    """C4-style: kNN covariance of a 4e6-point map (sampled queries vs brute force); levels=1 is
+    the warp search of every point, (3.0, 3) the bench configuration (cell tiles + queue)."""
     scene = synth.make_scene(1004)
     means, _, _, ell = synth.sample_map(scene, 4_000_000, 4004)
     pos = torch.zeros((means.shape[0], 4), dtype=torch.float32, device=DEV)
     pos[:, :3] = t(means)
     d_n = torch.tensor([means.shape[0]], dtype=torch.int32, device=DEV)
-    _cov_check(g, means, pos, d_n, cell0=2.5 * ell, levels=1, sample=300)
+    _cov_check(g, means, pos, d_n, cell0=cell * ell, levels=levels, sample=300)
 
 
 # ----------------------------------------------------------------------------------------- A5

@@ -39,7 +39,10 @@ def run(pos, d_n, cell0, levels, label, reps=5):
     n = int(d_n.item())
     d = dbg[:n].cpu().numpy()
     print(f"{label}: cell0={cell0:.4f} levels={levels}  median {np.median(ts):.3f} ms")
-    print("  level hist", np.bincount(d[:, 0], minlength=levels).tolist())
+    lv = d[:, 0]
+    print("  tile level hist", np.bincount(lv[lv < 16], minlength=levels).tolist(),
+          " queue (warp search) level hist", np.bincount(lv[lv >= 16] - 16, minlength=levels).tolist(),
+          f" queue frac {np.mean(lv >= 16):.4f}")
     dist("probes", d[:, 1])
     dist("cands", d[:, 2])
     dist("inserts", d[:, 3])

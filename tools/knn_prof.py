@@ -10,7 +10,19 @@ import paper_2403_12550_b200 as g
 import synth
 
 
+def c4():
+    scene = synth.make_scene(1004)
+    means, _, _, ell = synth.sample_map(scene, 4_000_000, 4004)
+    c = g.Cloud.from_points(torch.from_numpy(means).cuda())
+    ws = g._ws(g.lib().gsicp_covariances_workspace_size(c.cap, 3), c.pos.device)
+    for _ in range(3):
+        g.covariances(c.pos, c.d_n, 20, g.REG_ELLIPSE, 1e-3, 3.0 * ell, 3, c.cov_a, c.cov_b, None, ws)
+    torch.cuda.synchronize()
+
+
 def main():
+    if "c4" in sys.argv:
+        return c4()
     w = synth.make_frame_workload(2, "replica", M=1000, stride=4)
     K = w.K
     dev = torch.device("cuda")

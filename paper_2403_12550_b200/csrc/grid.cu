@@ -32,6 +32,7 @@ __global__ void k_grid_init(CellEntry *table, uint32_t slots, uint32_t *counters
 
 __global__ void k_grid_insert(GridView g, const float4 *__restrict__ pos, const int32_t *__restrict__ d_n) {
     const int n = *d_n;
+    if (n <= 0) return;  // nothing to hash (block-uniform)
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int level = (int)(t / g.cap);
     const int i = (int)(t - (long long)level * g.cap);

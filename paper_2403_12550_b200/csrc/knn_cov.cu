@@ -20,9 +20,13 @@
 #include <algorithm>
 #include <string.h>
 
+#include <cooperative_groups.h>
+
 #include "grid.cuh"
 #include "host_common.cuh"
 #include "search.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gsicp {
 
@@ -817,142 +821,151 @@ __global__ void __launch_bounds__(128) k_knn_image_wide(KnnArgs a, ImgArgs im) {
 }
 
 // The last queue: up to kBruteMax queries are searched by brute force over the whole cloud
-// (exact by definition — no certificate), a block per query with the same two-pass histogram
-// selection (bucket scale shifted until the boundary bucket is a proper one); a longer queue
-// (e.g. a cloud that is not a depth frame) goes to the hash search.
+// (exact by definition — no certificate); a longer queue (e.g. a cloud that is not a depth frame)
+// goes to the hash search.  Brute force: a 1024-bin histogram of all keys (octave x 32
+// sub-buckets) gives the boundary bin, a second pass collects the keys below it and the bin's
+// own, and the k smallest of those are the k nearest.
 constexpr int kBruteThreads = 512;
 
-// block-wide sum of per-thread histogram columns hist[16][T] (two 16-bit counters per word) into
-// tot[32] (32-bit); ends with a barrier
-template <int T>
-__device__ __forceinline__ void block_hist_sum(uint32_t (*hist)[T], uint32_t (*part)[kImgBuckets], uint32_t *tot) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    __syncthreads();
-#pragma unroll
-    for (int b = 0; b < kImgBuckets / 2; ++b) {
-        const uint32_t wd = hist[b][tid];
-        const uint32_t lo = __reduce_add_sync(kFull, wd & 0xFFFFu), hi = __reduce_add_sync(kFull, wd >> 16);
-        if (lane == 0) {
-            part[warp][2 * b] = lo;
-            part[warp][2 * b + 1] = hi;
-        }
+// A cluster of kBruteCluster CTAs per query (thread-block cluster): the CTAs split the cloud and
+// merge their histograms / candidate lists through distributed shared memory.
+constexpr int kBruteCluster = 8;
+
+// key -> one of 1024 bins: 32 octaves of the key (2^-20 .. 2^11 m^2, the end octaves open) x 32
+// sub-buckets (top 5 mantissa bits); bins are ordered like the keys
+__device__ __forceinline__ int brute_bin(uint32_t kb) {
+    const int o = (int)(kb >> 23) - (127 - 20);
+    if (o <= 0) return 0;
+    if (o >= 31) return 1023;
+    return o * 32 + (int)((kb >> 18) & 31u);
+}
+// key range [lo, hi) of a bin (as key bits)
+__device__ __forceinline__ void brute_bin_range(int bin, uint32_t &lo, uint32_t &hi) {
+    if (bin == 0) {
+        lo = 0u;
+        hi = (uint32_t)(127 - 20 + 1) << 23;
+    } else if (bin == 1023) {
+        lo = (uint32_t)(127 - 20 + 31) << 23;
+        hi = 0x7F800000u;
+    } else {
+        lo = ((uint32_t)(bin / 32 + 127 - 20) << 23) | ((uint32_t)(bin & 31) << 18);
+        hi = lo + (1u << 18);
     }
-    __syncthreads();
-    if (tid < kImgBuckets) {
-        uint32_t c = 0;
-        for (int w2 = 0; w2 < T / 32; ++w2) c += part[w2][tid];
-        tot[tid] = c;
-    }
-    __syncthreads();
 }
 
 template <int K>
-__global__ void __launch_bounds__(kBruteThreads) k_knn_brute(KnnArgs a, ImgArgs im) {
-    __shared__ uint32_t hist[kImgBuckets / 2][kBruteThreads];
-    __shared__ uint32_t part[kBruteThreads / 32][kImgBuckets];
-    __shared__ uint32_t tot[kImgBuckets];
+__global__ void __cluster_dims__(kBruteCluster, 1, 1) __launch_bounds__(kBruteThreads, 2)
+    k_knn_brute(KnnArgs a, ImgArgs im) {
+    __shared__ uint32_t bins[1024], gbins[1024];
+    __shared__ uint32_t wsum[32];
     __shared__ unsigned long long lst[64];
-    __shared__ int s_nl, s_nb;
+    __shared__ int s_nl, s_nb, s_bin;
+    __shared__ uint32_t s_below, s_m;
+    cg::cluster_group cl = cg::this_cluster();
     const uint32_t nq = *(im.ctr + kImgCtrQueue2);
-    if (nq == 0u || nq > kBruteMax) return;
+    if (nq == 0u || nq > kBruteMax) return;  // uniform over the grid: no cluster barrier is skipped alone
+    const int crank = (int)cl.block_rank();
     const int n = *a.d_n, k = a.k, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // boundary of a histogram: first bucket where the count (plus `below`) reaches k
-    auto boundary = [&](uint32_t below, uint32_t &cum_lo, uint32_t &cum_hi) {
-        uint32_t cum = below;
-        for (int b = 0; b < kImgBuckets; ++b) {
-            if (cum + tot[b] >= (uint32_t)k) {
-                cum_lo = cum;
-                cum_hi = cum + tot[b];
-                return b;
-            }
-            cum += tot[b];
-        }
-        cum_lo = cum_hi = cum;
-        return -1;
-    };
-    for (uint32_t t = blockIdx.x; t < nq; t += gridDim.x) {
+    const int j0 = crank * kBruteThreads + tid, js = kBruteCluster * kBruteThreads;
+    const uint32_t nclusters = gridDim.x / kBruteCluster;
+    for (uint32_t t = blockIdx.x / kBruteCluster; t < nq; t += nclusters) {
         const int i = (int)__ldg(im.queue2 + t);
         const float4 q = __ldg(a.pos + i);
-        // pass 1: octave histogram of all keys (key exponent, octaves 2^-20 .. 2^11 m^2, clamped)
-#pragma unroll
-        for (int b = 0; b < kImgBuckets / 2; ++b) hist[b][tid] = 0u;
-#pragma unroll 16
-        for (int j = tid; j < n; j += kBruteThreads) {
+        // pass 1: 1024-bin histogram of this CTA's share of the keys
+        for (int b = tid; b < 1024; b += kBruteThreads) bins[b] = 0u;
+        __syncthreads();
+#pragma unroll 4
+        for (int j = j0; j < n; j += js) {
             const float4 P = __ldg(a.pos + j);
-            const float key = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
-            const int bk = min(max((int)(__float_as_uint(key) >> 23) - (127 - 20), 0), kImgBuckets - 1);
-            atomicAdd(&hist[bk >> 1][tid], 1u << ((bk & 1) * 16));
+            atomicAdd(&bins[brute_bin(__float_as_uint(canon_key(q.x, q.y, q.z, P.x, P.y, P.z)))], 1u);
         }
-        block_hist_sum<kBruteThreads>(hist, part, tot);
-        uint32_t lo1, hi1;
-        const int o = boundary(0u, lo1, hi1);
-        // keys of octave bucket o: exponent field e_o (bucket 0 and 31 are open-ended)
-        uint32_t klo = 0u, khi = 0x7F800000u;  // collect range [klo, khi) of key bits
-        uint32_t below = o >= 0 ? lo1 : 0u, m = hi1;  // (o < 0: fewer than k points, all boundary)
-        bool ok = o >= 0 || (uint32_t)n < (uint32_t)k;
-        if (o > 0 && o < kImgBuckets - 1) {
-            // pass 2: 32 sub-buckets of that octave (the top 5 mantissa bits)
-            const uint32_t e = (uint32_t)(o + 127 - 20);
+        cl.sync();
+        // the cluster's histogram (every CTA sums it: two bins per thread), then the boundary bin
+        for (int b = tid; b < 1024; b += kBruteThreads) {
+            uint32_t c = 0;
 #pragma unroll
-            for (int b = 0; b < kImgBuckets / 2; ++b) hist[b][tid] = 0u;
-            __syncthreads();
-#pragma unroll 16
-            for (int j = tid; j < n; j += kBruteThreads) {
-                const float4 P = __ldg(a.pos + j);
-                const uint32_t kb = __float_as_uint(canon_key(q.x, q.y, q.z, P.x, P.y, P.z));
-                if ((kb >> 23) == e) {
-                    const int bk = (int)((kb >> 18) & 31u);
-                    atomicAdd(&hist[bk >> 1][tid], 1u << ((bk & 1) * 16));
-                }
+            for (int r = 0; r < kBruteCluster; ++r) c += cl.map_shared_rank(bins, r)[b];
+            gbins[b] = c;
+        }
+        __syncthreads();
+        if (warp == 0) {  // lane l owns bins [32 l, 32 l + 32): warp prefix of the lane sums
+            uint32_t sl = 0;
+            for (int b = 0; b < 32; ++b) sl += gbins[32 * lane + b];
+            uint32_t incl = sl;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += y;
             }
-            block_hist_sum<kBruteThreads>(hist, part, tot);
-            uint32_t lo2, hi2;
-            const int sb = boundary(lo1, lo2, hi2);
-            below = lo2;
-            m = hi2;
-            klo = (e << 23) | ((uint32_t)sb << 18);
-            khi = klo + (1u << 18);
-        } else if (o == 0) {
-            khi = (uint32_t)(127 - 20 + 1) << 23;
-        } else if (o == kImgBuckets - 1) {
-            klo = (uint32_t)(127 - 20 + kImgBuckets - 1) << 23;
+            const uint32_t excl = incl - sl;
+            const unsigned hit = __ballot_sync(kFull, incl >= (uint32_t)k);
+            if (lane == 0) s_bin = -1;
+            if (hit) {
+                const int L = __ffs(hit) - 1;
+                if (lane == L) {
+                    uint32_t cum = excl;
+                    for (int b = 0; b < 32; ++b) {
+                        const uint32_t c = gbins[32 * lane + b];
+                        if (cum + c >= (uint32_t)k) {
+                            s_bin = 32 * lane + b;
+                            s_below = cum;
+                            s_m = cum + c;
+                            break;
+                        }
+                        cum += c;
+                    }
+                }
+            } else if (lane == 31) {  // fewer than k points: all of them
+                s_bin = 1024;
+                s_below = 0u;
+                s_m = incl;
+            }
         }
-        // every key below klo is among the k nearest (`below` of them); [klo, khi) is the boundary
-        if (!ok || m - below > 64u) {  // > 64 near-equal keys at the boundary: hand over to the hash
-            if (tid == 0) im.queue[atomicAdd(im.ctr + kImgCtrQueue3, 1u)] = (uint32_t)i;
-            __syncthreads();
-            continue;
-        }
-        // pass 3: the k nearest = the `below` keys < klo (list slots 0..) plus the `need` smallest of
-        // the boundary range [klo, khi) (slots 32.. ; at most 32 of each)
+        __syncthreads();
+        const int bin = s_bin;
+        const uint32_t below = s_below, m = s_m;
+        uint32_t klo = 0u, khi = 0x7F800000u;  // boundary range [klo, khi) of key bits
+        if (bin < 1024) brute_bin_range(bin, klo, khi);
+        // pass 2: the k nearest = the `below` keys < klo plus the `need` smallest of [klo, khi)
+        const bool fits = below <= 32u && m - below <= 32u;  // (cluster-uniform)
         if (tid == 0) {
             s_nl = 0;
             s_nb = 0;
         }
         __syncthreads();
-        const int need = k - (int)below;
-#pragma unroll 16
-        for (int j = tid; j < n; j += kBruteThreads) {
-            const float4 P = __ldg(a.pos + j);
-            const float key = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
-            const uint32_t kb = __float_as_uint(key);
-            if (kb < khi && key < INFINITY) {
-                const bool lo = kb < klo;
-                const int slot = atomicAdd(lo ? &s_nl : &s_nb, 1);
-                if (slot < 32) lst[(lo ? 0 : 32) + slot] = pack_ki(key, (uint32_t)j);
+        if (fits) {
+#pragma unroll 4
+            for (int j = j0; j < n; j += js) {
+                const float4 P = __ldg(a.pos + j);
+                const float key = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
+                const uint32_t kb = __float_as_uint(key);
+                if (kb < khi && key < INFINITY) {
+                    const bool lo = kb < klo;
+                    const int slot = atomicAdd(lo ? &s_nl : &s_nb, 1);
+                    if (slot < 32) lst[(lo ? 0 : 32) + slot] = pack_ki(key, (uint32_t)j);
+                }
             }
         }
-        __syncthreads();
-        if (warp == 0) {
-            const int nl = s_nl, nb = s_nb;
-            if (nb > 32 || nl > 32) {  // boundary too crowded for one warp: hand over to the hash
+        cl.sync();
+        if (crank == 0 && warp == 0) {
+            if (!fits) {  // > 32 near-equal keys at the boundary: hand over to the hash
                 if (lane == 0) im.queue[atomicAdd(im.ctr + kImgCtrQueue3, 1u)] = (uint32_t)i;
             } else {
-                // boundary entries sorted; lanes [0, need) take them after the `below` ones
-                unsigned long long B = lane < nb ? lst[32 + lane] : kEmptyKey;
-                B = WarpTopK<32>::sort_w<32>(B, lane);
-                const unsigned long long Bsh = shfl_u64(B, (lane - nl) & 31);
-                unsigned long long A = lane < nl ? lst[lane] : (lane < nl + need ? Bsh : kEmptyKey);
+                // gather the CTAs' lists (at most 32 + 32 entries in all): lane j fetches entry j
+                unsigned long long L = kEmptyKey, Bd = kEmptyKey;
+                int nl = 0, nb = 0;
+                for (int r = 0; r < kBruteCluster; ++r) {
+                    const int cl_l = *cl.map_shared_rank(&s_nl, r), cl_b = *cl.map_shared_rank(&s_nb, r);
+                    const unsigned long long *rl = cl.map_shared_rank(lst, r);
+                    if (lane >= nl && lane < nl + cl_l) L = rl[lane - nl];
+                    if (lane >= nb && lane < nb + cl_b) Bd = rl[32 + lane - nb];
+                    nl += cl_l;
+                    nb += cl_b;
+                }
+                const int need = k - nl;
+                Bd = WarpTopK<32>::sort_w<32>(Bd, lane);
+                const unsigned long long Bsh = shfl_u64(Bd, (lane - nl) & 31);
+                unsigned long long A = lane < nl ? L : (lane < nl + need ? Bsh : kEmptyKey);
                 A = WarpTopK<32>::sort_w<32>(A, lane);
                 if (a.knn_idx && lane < k) a.knn_idx[(size_t)i * k + lane] = A == kEmptyKey ? -1 : (int32_t)ki_idx(A);
                 int ids[K];
@@ -965,7 +978,7 @@ __global__ void __launch_bounds__(kBruteThreads) k_knn_brute(KnnArgs a, ImgArgs 
                 if (lane == 0) finish_query<K>(a, n, i, q, k, ids);
             }
         }
-        __syncthreads();
+        cl.sync();  // the lists are read remotely before the next query overwrites them
     }
 }
 
@@ -1020,7 +1033,7 @@ cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *po
     k_knn_image_wide<K><<<(unsigned)num_sms() * 8, 128, 0, s>>>(a, im);
     GSICP_LAUNCH_CHECK("k_knn_image_wide");
     // the rest: brute force (a short queue) or hash the cloud, warp search, epilogue (long queue)
-    k_knn_brute<K><<<(unsigned)num_sms(), kBruteThreads, 0, s>>>(a, im);
+    k_knn_brute<K><<<(unsigned)(2 * (num_sms() / kBruteCluster) * kBruteCluster), kBruteThreads, 0, s>>>(a, im);
     GSICP_LAUNCH_CHECK("k_knn_brute");
     k_img_hash_n<<<1, 1, 0, s>>>(im, d_n);
     GSICP_LAUNCH_CHECK("k_img_hash_n");

@@ -115,6 +115,19 @@ gsicp_status gsicp_backproject_downsample(const float *depth_m, int32_t H, int32
                                           float *pos_out, int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes,
                                           void *stream);
 
+/* Same output (bit-identical) from only the rows A1 reads: depth_rows holds ceil(H/stride)
+ * rows of row_pitch_elems floats, row r being image row r*stride — what a caller uploads when
+ * the frame arrives in host memory (1/stride of the bytes).  Errors as above. */
+gsicp_status gsicp_backproject_sampled_rows(const float *depth_rows, int32_t H, int32_t W, int32_t row_pitch_elems,
+                                            gsicp_intrinsics K, int32_t stride, float z_min, float z_max,
+                                            float *pos_out, int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes,
+                                            void *stream);
+/* Host -> device staging for it: copies rows 0, stride, 2*stride, ... of a host depth image
+ * (src_pitch_elems floats per row; pinned memory for an asynchronous copy) into dst_rows
+ * [dev] (ceil(H/stride) rows of W floats), stream-ordered.  Errors: INVALID_ARGUMENT, CUDA. */
+gsicp_status gsicp_upload_sampled_rows(float *dst_rows, const float *src_host, int32_t H, int32_t W,
+                                       int32_t src_pitch_elems, int32_t stride, void *stream);
+
 /* ---------------------------------------------------------------------------------------
  * A2-A4  Per-point covariance of the exact k nearest neighbours ("computing covariance
  * matrix of k-nearest neighbors of x"; self included, ties by lower index),

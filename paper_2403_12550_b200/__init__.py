@@ -78,6 +78,8 @@ def lib():
         L.gsicp_backproject_workspace_size.argtypes = [i32, i32, i32]
         L.gsicp_backproject_workspace_size.restype = sz
         L.gsicp_backproject_downsample.argtypes = [P, i32, i32, i32, Intrinsics, i32, f32, f32, P, i32, P, P, sz, P]
+        L.gsicp_backproject_sampled_rows.argtypes = [P, i32, i32, i32, Intrinsics, i32, f32, f32, P, i32, P, P, sz, P]
+        L.gsicp_upload_sampled_rows.argtypes = [P, P, i32, i32, i32, i32, P]
         L.gsicp_covariances_workspace_size.argtypes = [i32, i32]
         L.gsicp_covariances_workspace_size.restype = sz
         L.gsicp_covariances.argtypes = [P, P, i32, i32, i32, f32, f32, i32, P, P, P, P, sz, P]
@@ -112,7 +114,8 @@ def lib():
         L.gsicp_debug_kernel_timer.restype = None
         L.gsicp_debug_kernel_time.argtypes = [i32, C.POINTER(C.c_float)]
         L.gsicp_debug_kernel_time.restype = i32
-        for name in ("gsicp_backproject_downsample", "gsicp_covariances", "gsicp_covariances_image", "gsicp_build_target",
+        for name in ("gsicp_backproject_downsample", "gsicp_backproject_sampled_rows", "gsicp_upload_sampled_rows",
+                     "gsicp_covariances", "gsicp_covariances_image", "gsicp_build_target",
                      "gsicp_build_target_cloud", "gsicp_align", "gsicp_align_async", "gsicp_align_seed",
                      "gsicp_linearize"):
             getattr(L, name).restype = i32
@@ -121,7 +124,8 @@ def lib():
 
 
 EXPORTED = [
-    "gsicp_backproject_workspace_size", "gsicp_backproject_downsample", "gsicp_covariances_workspace_size",
+    "gsicp_backproject_workspace_size", "gsicp_backproject_downsample", "gsicp_backproject_sampled_rows",
+    "gsicp_upload_sampled_rows", "gsicp_covariances_workspace_size",
     "gsicp_covariances", "gsicp_covariances_image_workspace_size", "gsicp_covariances_image",
     "gsicp_build_target_workspace_size", "gsicp_build_target", "gsicp_build_target_cloud",
     "gsicp_align_workspace_size", "gsicp_align", "gsicp_align_async", "gsicp_align_seed", "gsicp_linearize",
@@ -263,6 +267,36 @@ def backproject_downsample(depth: torch.Tensor, K, stride: int = 4, z_min: float
                                               _ptr(pos_out), pos_out.shape[0], _ptr(d_n), _ptr(ws), ws.numel(),
                                               _stream(stream)))
     return pos_out, d_n
+
+
+def backproject_sampled_rows(rows: torch.Tensor, H: int, W: int, K, stride: int = 4, z_min: float = 0.1,
+                             z_max: float = 10.0, pos_out: torch.Tensor | None = None,
+                             d_n: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
+    """A1 from only the sampled rows (rows[r] = image row r*stride): same output as
+    backproject_downsample on the full (H, W) image."""
+    pitch = rows.stride(0)
+    cap = ((H + stride - 1) // stride) * ((W + stride - 1) // stride)
+    dev = rows.device
+    if pos_out is None:
+        pos_out = torch.empty((cap, 4), dtype=torch.float32, device=dev)
+    if d_n is None:
+        d_n = torch.zeros(1, dtype=torch.int32, device=dev)
+    if ws is None:
+        ws = _ws(lib().gsicp_backproject_workspace_size(H, W, stride), dev)
+    Kc = K if isinstance(K, Intrinsics) else Intrinsics(*K)
+    _check(lib().gsicp_backproject_sampled_rows(C.c_void_p(rows.data_ptr()), H, W, pitch, Kc, stride, z_min, z_max,
+                                                _ptr(pos_out), pos_out.shape[0], _ptr(d_n), _ptr(ws), ws.numel(),
+                                                _stream(stream)))
+    return pos_out, d_n
+
+
+def upload_sampled_rows(dst_rows: torch.Tensor, depth_host: torch.Tensor, stride: int, stream=None):
+    """Copy rows 0, s, 2s, ... of a (pinned) host depth image into dst_rows (device), async."""
+    H, W = depth_host.shape
+    assert dst_rows.is_cuda and dst_rows.is_contiguous() and dst_rows.shape == ((H + stride - 1) // stride, W)
+    assert not depth_host.is_cuda and depth_host.dtype == torch.float32
+    _check(lib().gsicp_upload_sampled_rows(_ptr(dst_rows), C.c_void_p(depth_host.data_ptr()), H, W,
+                                           depth_host.stride(0), stride, _stream(stream)))
 
 
 def covariances(pos: torch.Tensor, d_n: torch.Tensor, k: int = 20, mode: int = REG_ELLIPSE, eps_var: float = 1e-3,
@@ -421,7 +455,9 @@ def linearize(src: Cloud, tgt: Target, T, max_corr_dist: float = math.inf, corr_
 
 class Tracker:
     """Per-frame tracking pipeline with preallocated buffers: A1 -> A2-A4 -> A6-A9 against a
-    prebuilt target.  `track()` is the public per-frame call; `step_async()` is graph-capturable."""
+    prebuilt target.  Public per-frame calls: `track()` (depth already on the device) and
+    `track_host()` (depth in host memory: only the sampled rows are uploaded); both replay the
+    frame from a CUDA graph captured on first use.  `step_async()` is the graph-capturable frame."""
 
     def __init__(self, H: int, W: int, K, stride: int = 4, k: int = 20, mode: int = REG_ELLIPSE,
                  eps_var: float = 1e-3, z_min: float = 0.1, z_max: float = 10.0, cell0: float | None = None,
@@ -436,6 +472,7 @@ class Tracker:
         self.params = params or align_params()
         self.device = torch.device(device)
         self.cloud = Cloud.empty(self.cap, self.device)
+        self.rows = torch.empty(((H + stride - 1) // stride, W), dtype=torch.float32, device=self.device)
         self.ws_bp = _ws(lib().gsicp_backproject_workspace_size(H, W, stride), self.device)
         self.ws_cov = _ws(lib().gsicp_covariances_image_workspace_size(self.cap, levels, H, W, stride), self.device)
         self.ws_align = align_workspace(self.cap, self.device)
@@ -444,6 +481,10 @@ class Tracker:
         self._side = torch.cuda.Stream(self.device)
         self._fork = torch.cuda.Event()
         self._join = torch.cuda.Event()
+        self._graphs = {}
+        self._T_host = torch.zeros(16, dtype=torch.float64).pin_memory()
+        self._T_out = torch.zeros(16, dtype=torch.float64).pin_memory()
+        self._st_out = torch.zeros(C.sizeof(AlignStats), dtype=torch.uint8).pin_memory()
 
     def preprocess(self, depth: torch.Tensor, stream=None):
         backproject_downsample(depth, self.K, self.stride, self.z_min, self.z_max, self.cloud.pos, self.cloud.d_n,
@@ -455,16 +496,21 @@ class Tracker:
                           self.eps, self.cell0, self.levels, self.cloud.cov_a, self.cloud.cov_b, None, self.ws_cov,
                           stream)
 
-    def step_async(self, depth: torch.Tensor, tgt: Target, stream=None, events=None):
+    def step_async(self, depth: torch.Tensor | None, tgt: Target, stream=None, events=None):
         """Whole frame, device-resident pose in self.d_T (set it before), no host sync.
-        A1 on `stream`; then the iteration-0 correspondences (gsicp_align_seed) on a side stream
+        A1 on `stream` (from `depth`, or from the sampled-row buffer `self.rows` when depth is
+        None); then the iteration-0 correspondences (gsicp_align_seed) on a side stream
         concurrently with A2-A4; joined before A6-A9.  `events` (optional, 4 CUDA events) are
         recorded on `stream` around A1 / A2-A4 / A6-A9."""
         s0 = stream if stream is not None else torch.cuda.current_stream(self.device)
         if events:
             events[0].record(s0)
-        backproject_downsample(depth, self.K, self.stride, self.z_min, self.z_max, self.cloud.pos, self.cloud.d_n,
-                               self.ws_bp, s0)
+        if depth is None:
+            backproject_sampled_rows(self.rows, self.H, self.W, self.K, self.stride, self.z_min, self.z_max,
+                                     self.cloud.pos, self.cloud.d_n, self.ws_bp, s0)
+        else:
+            backproject_downsample(depth, self.K, self.stride, self.z_min, self.z_max, self.cloud.pos,
+                                   self.cloud.d_n, self.ws_bp, s0)
         if events:
             events[1].record(s0)
         self._fork.record(s0)
@@ -479,17 +525,49 @@ class Tracker:
         if events:
             events[3].record(s0)
 
-    def track(self, depth: torch.Tensor, tgt: Target, init_T, stream=None):
-        """Whole frame through the public API: host pose in, (T, stats) out (blocking)."""
+    def _graph(self, key, depth, tgt):
+        """The whole frame (step_async) captured once per (input, target), replayed after."""
+        hit = self._graphs.get(key)
+        if hit is not None:
+            return hit[0]
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        self.step_async(depth, tgt, s)  # one run outside the capture (lazy library state)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.step_async(depth, tgt, s)
+        self._graphs[key] = (g, depth, tgt)  # keep the captured buffers alive
+        return g
+
+    def _run(self, key, depth, tgt, init_T, stream, upload=None):
         s0 = stream if stream is not None else torch.cuda.current_stream(self.device)
-        T0 = torch.from_numpy(np.ascontiguousarray(init_T, dtype=np.float64).reshape(16))
+        g = self._graph(key, depth, tgt)
+        self._T_host.numpy()[:] = np.ascontiguousarray(init_T, dtype=np.float64).reshape(16)
         with torch.cuda.stream(s0):
-            self.d_T.copy_(T0.pin_memory() if not T0.is_pinned() else T0, non_blocking=True)
-        self.step_async(depth, tgt, s0)
-        with torch.cuda.stream(s0):
-            T = self.d_T.to("cpu", non_blocking=True)
-            st = self.d_stats.to("cpu", non_blocking=True)
+            self.d_T.copy_(self._T_host, non_blocking=True)
+            if upload is not None:
+                upload(s0)
+            g.replay()
+            self._T_out.copy_(self.d_T, non_blocking=True)
+            self._st_out.copy_(self.d_stats, non_blocking=True)
         s0.synchronize()
-        stats = AlignStats.from_buffer_copy(st.numpy().tobytes()[:C.sizeof(AlignStats)]).as_dict()
+        stats = AlignStats.from_buffer_copy(self._st_out.numpy().tobytes()[:C.sizeof(AlignStats)]).as_dict()
         _check(stats["status"], _ALIGN_ALLOW)
-        return T.numpy().reshape(4, 4).copy(), stats
+        return self._T_out.numpy().reshape(4, 4).copy(), stats
+
+    def track(self, depth: torch.Tensor, tgt: Target, init_T, stream=None):
+        """Whole frame from a device depth image: host pose in, (T, stats) out (blocking)."""
+        key = ("dev", depth.data_ptr(), tuple(depth.shape), tuple(depth.stride()), id(tgt))
+        return self._run(key, depth, tgt, init_T, stream)
+
+    def track_host(self, depth_host: torch.Tensor, tgt: Target, init_T, stream=None):
+        """Whole frame from a host depth image (pinned for an asynchronous copy): uploads only the
+        rows A1 reads (every stride-th), then as track().  Returns (T, stats)."""
+        key = ("rows", id(tgt))
+        up = lambda s0: upload_sampled_rows(self.rows, depth_host, self.stride, s0)  # noqa: E731
+        return self._run(key, None, tgt, init_T, stream, up)
+
+    def upload_bytes(self) -> int:
+        """Bytes track_host() copies host -> device per frame (the sampled rows)."""
+        return self.rows.numel() * 4

@@ -47,7 +47,8 @@ void set_error(const char *fmt, ...) {
 // defined in the kernel translation units
 size_t backproject_ws_bytes(int H, int W, int stride);
 cudaError_t backproject_launch(const float *depth, int H, int W, int pitch, gsicp_intrinsics K, int stride,
-                               float zmin, float zmax, float *pos_out, int32_t *d_n, void *ws, cudaStream_t s);
+                               float zmin, float zmax, float *pos_out, int32_t *d_n, void *ws, cudaStream_t s,
+                               int rows_sampled);
 size_t covariances_ws_bytes(int cap, int levels);
 cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, int k, int mode, float eps,
                                float cell0, int levels, float *cov_a, float *cov_b, int32_t *knn_idx, void *ws,
@@ -155,10 +156,10 @@ size_t gsicp_backproject_workspace_size(int32_t H, int32_t W, int32_t stride) {
     return backproject_ws_bytes(H, W, stride);
 }
 
-gsicp_status gsicp_backproject_downsample(const float *depth_m, int32_t H, int32_t W, int32_t row_pitch_elems,
-                                          gsicp_intrinsics K, int32_t stride, float z_min, float z_max,
-                                          float *pos_out, int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes,
-                                          void *stream) {
+static gsicp_status backproject_common(const float *depth_m, int32_t H, int32_t W, int32_t row_pitch_elems,
+                                       gsicp_intrinsics K, int32_t stride, float z_min, float z_max, float *pos_out,
+                                       int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes, void *stream,
+                                       int rows_sampled) {
     g_err[0] = 0;
     if (!depth_m || !pos_out || !d_n_out) BAD("backproject: null pointer");
     if (H < 1 || W < 1 || stride < 1 || row_pitch_elems < W) BAD("backproject: bad image geometry");
@@ -170,8 +171,36 @@ gsicp_status gsicp_backproject_downsample(const float *depth_m, int32_t H, int32
     gsicp_status st = check_ws(ws, ws_bytes, backproject_ws_bytes(H, W, stride));
     if (st != GSICP_OK) return st;
     return cuda_status(backproject_launch(depth_m, H, W, row_pitch_elems, K, stride, z_min, z_max, pos_out, d_n_out, ws,
-                                          (cudaStream_t)stream),
+                                          (cudaStream_t)stream, rows_sampled),
                        "backproject");
+}
+
+gsicp_status gsicp_backproject_downsample(const float *depth_m, int32_t H, int32_t W, int32_t row_pitch_elems,
+                                          gsicp_intrinsics K, int32_t stride, float z_min, float z_max,
+                                          float *pos_out, int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes,
+                                          void *stream) {
+    return backproject_common(depth_m, H, W, row_pitch_elems, K, stride, z_min, z_max, pos_out, cap, d_n_out, ws,
+                              ws_bytes, stream, 0);
+}
+
+gsicp_status gsicp_backproject_sampled_rows(const float *depth_rows, int32_t H, int32_t W, int32_t row_pitch_elems,
+                                            gsicp_intrinsics K, int32_t stride, float z_min, float z_max,
+                                            float *pos_out, int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes,
+                                            void *stream) {
+    return backproject_common(depth_rows, H, W, row_pitch_elems, K, stride, z_min, z_max, pos_out, cap, d_n_out, ws,
+                              ws_bytes, stream, 1);
+}
+
+gsicp_status gsicp_upload_sampled_rows(float *dst_rows, const float *src_host, int32_t H, int32_t W,
+                                       int32_t src_pitch_elems, int32_t stride, void *stream) {
+    g_err[0] = 0;
+    if (!dst_rows || !src_host) BAD("upload_sampled_rows: null pointer");
+    if (H < 1 || W < 1 || stride < 1 || src_pitch_elems < W) BAD("upload_sampled_rows: bad image geometry");
+    const int rows = (H + stride - 1) / stride;
+    return cuda_status(cudaMemcpy2DAsync(dst_rows, (size_t)W * sizeof(float), src_host,
+                                         (size_t)stride * src_pitch_elems * sizeof(float), (size_t)W * sizeof(float),
+                                         (size_t)rows, cudaMemcpyHostToDevice, (cudaStream_t)stream),
+                       "upload_sampled_rows");
 }
 
 size_t gsicp_covariances_workspace_size(int32_t cap, int32_t levels) {

@@ -16,6 +16,7 @@ constexpr int kBpTile = kBpThreads * kBpPerThread;
 struct BpArgs {
     const float *depth;
     int H, W, pitch, stride, Ws, Hs;  // Ws, Hs: sampled lattice size
+    int rows_sampled;                 // depth holds only the sampled rows (row r = image row r*stride)
     float fx, fy, cx, cy, zmin, zmax;
     float4 *out;
     int32_t *d_n;
@@ -28,7 +29,7 @@ __device__ __forceinline__ bool bp_valid(const BpArgs &a, int j, float &z, int &
     const int vs = j / a.Ws, us = j - vs * a.Ws;
     u = us * a.stride;
     v = vs * a.stride;
-    z = __ldg(a.depth + (size_t)v * a.pitch + u);
+    z = __ldg(a.depth + (size_t)(a.rows_sampled ? vs : v) * a.pitch + u);
     return isfinite(z) && z >= a.zmin && z <= a.zmax;
 }
 
@@ -116,8 +117,10 @@ size_t backproject_ws_bytes(int H, int W, int stride) {
 }
 
 cudaError_t backproject_launch(const float *depth, int H, int W, int pitch, gsicp_intrinsics K, int stride,
-                               float zmin, float zmax, float *pos_out, int32_t *d_n, void *ws, cudaStream_t s) {
+                               float zmin, float zmax, float *pos_out, int32_t *d_n, void *ws, cudaStream_t s,
+                               int rows_sampled) {
     BpArgs a;
+    a.rows_sampled = rows_sampled;
     a.depth = depth;
     a.H = H; a.W = W; a.pitch = pitch; a.stride = stride;
     a.Ws = (W + stride - 1) / stride;

@@ -1018,28 +1018,57 @@ cudaError_t launch_tile(const KnnArgs &a, const ImgArgs &im, cudaStream_t s) {
     return cudaSuccess;
 }
 
+// side stream (per host thread) on which the fallback hash is built while the window kernels run;
+// forked from and joined back to the caller's stream with events (graph-capture safe)
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    int dev = -1;
+};
+static cudaError_t side_stream(SideStream *&out) {
+    static thread_local SideStream ss;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (ss.s == nullptr || ss.dev != dev) {
+        cudaError_t e = cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+        ss.dev = dev;
+    }
+    out = &ss;
+    return cudaSuccess;
+}
+
 template <int K>
 cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *pos, const int32_t *d_n, cudaStream_t s) {
+    SideStream *ss = nullptr;
+    cudaError_t e = side_stream(ss);
+    if (e != cudaSuccess) return e;
+    // the hash of the cloud for the last-resort search, built off the critical path
+    if ((e = cudaEventRecord(ss->fork, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(ss->s, ss->fork, 0)) != cudaSuccess) return e;
+    e = grid_build(a.g, pos, nullptr, nullptr, d_n, cap, ss->s);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(ss->join, ss->s)) != cudaSuccess) return e;
     ktimer_mark(KT_KNN_SEARCH, false, s);
     const int L = im.Hs * im.Ws;
     k_img_map_clear<<<blocks_for(std::max(L, kImgCounters), 256), 256, 0, s>>>(im);
     GSICP_LAUNCH_CHECK("k_img_map_clear");
     k_img_map_fill<<<blocks_for(cap, 256), 256, 0, s>>>(im, pos, d_n);
     GSICP_LAUNCH_CHECK("k_img_map_fill");
-    cudaError_t e = launch_tile<K>(a, im, s);
+    e = launch_tile<K>(a, im, s);
     if (e != cudaSuccess) return e;
     ktimer_mark(KT_KNN_SEARCH, true, s);
     // wide window over the queue (a resident grid pulling queries)
     k_knn_image_wide<K><<<(unsigned)num_sms() * 8, 128, 0, s>>>(a, im);
     GSICP_LAUNCH_CHECK("k_knn_image_wide");
-    // the rest: brute force (a short queue) or hash the cloud, warp search, epilogue (long queue)
+    // the rest: brute force (a short queue), else the hash search + epilogue (long queue)
     k_knn_brute<K><<<(unsigned)(2 * (num_sms() / kBruteCluster) * kBruteCluster), kBruteThreads, 0, s>>>(a, im);
     GSICP_LAUNCH_CHECK("k_knn_brute");
     k_img_hash_n<<<1, 1, 0, s>>>(im, d_n);
     GSICP_LAUNCH_CHECK("k_img_hash_n");
-    const int32_t *hn = reinterpret_cast<const int32_t *>(im.ctr + kImgCtrHashN);
-    e = grid_build(a.g, pos, nullptr, nullptr, hn, cap, s);
-    if (e != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(s, ss->join, 0)) != cudaSuccess) return e;
     a.queue = im.queue2;
     a.queue_n = im.ctr + kImgCtrHashQ;
     a.work = im.ctr + kImgCtrWork;

@@ -439,6 +439,31 @@ def test_align_errors(g, c1_setup):
     assert st["status"] == g.ERR_DEGENERATE_FRAME
 
 
+def test_tracker_host_frames_and_sampled_rows(g, replica, tum):
+    """A1 from only the sampled rows == A1 from the full image (bit-exact), and track_host()
+    (sampled-row upload + graph replay) returns the same pose as track() on the device image."""
+    for w, s in ((replica, 4), (tum, 3), (tum, 1)):
+        H, W = w.depth.shape
+        K = (w.K.fx, w.K.fy, w.K.cx, w.K.cy)
+        full, n_full = g.backproject_downsample(t(w.depth), K, stride=s)
+        rows = torch.empty(((H + s - 1) // s, W), dtype=torch.float32, device=DEV)
+        g.upload_sampled_rows(rows, torch.from_numpy(w.depth).pin_memory(), s)
+        part, n_part = g.backproject_sampled_rows(rows, H, W, K, stride=s)
+        n = int(n_full.item())
+        assert n == int(n_part.item())
+        assert torch.equal(full[:n], part[:n])
+    w = replica
+    tr = g.Tracker(w.K.H, w.K.W, (w.K.fx, w.K.fy, w.K.cx, w.K.cy), stride=4)
+    tgt = g.build_target(t(w.means), t(w.quats), t(w.scales))
+    T_dev, st_dev = tr.track(t(w.depth), tgt, w.T_init)
+    host = torch.from_numpy(w.depth).pin_memory()
+    for _ in range(2):
+        T_host, st_host = tr.track_host(host, tgt, w.T_init)
+        np.testing.assert_array_equal(T_host, T_dev)
+        assert st_host["iters"] == st_dev["iters"] and st_host["fitness"] == st_dev["fitness"]
+    assert tr.upload_bytes() == ((w.K.H + 3) // 4) * w.K.W * 4
+
+
 def test_tracker_graph_capture(g, replica):
     """The whole frame (A1 -> A4 -> A6-A9) captured in one CUDA graph and replayed."""
     w = replica

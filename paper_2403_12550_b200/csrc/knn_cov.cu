@@ -799,11 +799,10 @@ __global__ void __launch_bounds__(128) k_knn_image_wide(KnnArgs a, ImgArgs im) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int nq = (int)*(im.ctr + kImgCtrQueue);
     const bool bad = __ldg(im.ctr + kImgCtrBad) != 0u;
-    for (;;) {
-        int t = 0;
-        if (lane == 0) t = (int)atomicAdd(im.ctr + kImgCtrWideWork, 1u);
-        t = __shfl_sync(kFull, t, 0);
-        if (t >= nq) return;
+    // static warp-strided assignment (a shared work counter serialises thousands of warps on
+    // one atomic for a queue of ~1e3)
+    const int gw = (int)(blockIdx.x * 4 + wib), nw = (int)gridDim.x * 4;
+    for (int t = gw; t < nq; t += nw) {
         const int i = (int)__ldg(im.queue + t);
         const float4 q = __ldg(a.pos + i);
         bool ok = false;

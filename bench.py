@@ -32,7 +32,6 @@ METRIC = "G-ICP aligns/sec (Replica frame vs 1M-Gaussian map); kNN-cov Mpts/s; H
 WORKLOAD = "Replica-shaped 1200x680 depth frame, stride 4 (<=51k pts), vs 1e6-Gaussian map (C2 geometry, 1M map)"
 ALGO_BYTES_ALIGN = 96 + 8   # per (source point x GN iteration): src pos+cov, tgt pos+cov, corr
 ALGO_BYTES_KNN = 16 + 32    # per query of the kNN-cov stage: pos in, cov out
-ALGO_BYTES_KNN_SEARCH = 16 + 4 * 20  # per query of k_knn_search: query record in, 20 neighbour ids out
 C4_CELL, C4_LEVELS = 3.0, 3  # map kNN-cov grid: finest cell 3 x map spacing, 3 levels (outliers go coarse)
 
 
@@ -213,8 +212,9 @@ def bench_gpu(args):
     K = w.K
     depth_host = torch.from_numpy(w.depth).pin_memory()
     depth = depth_host.to(dev)
+    tcell = float(os.environ.get("BENCH_TGT_CELL", "0")) * w.ell  # (diagnostic; 0 = the library's auto cell)
     tgt = g.build_target(torch.from_numpy(w.means).to(dev), torch.from_numpy(w.quats).to(dev),
-                         torch.from_numpy(w.scales).to(dev))
+                         torch.from_numpy(w.scales).to(dev), cell=tcell)
     params = g.align_params(max_iters=30, max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6)
     tr = g.Tracker(K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=w.stride, params=params, device=dev)
     T0 = torch.from_numpy(w.T_init.reshape(-1).copy()).to(dev)
@@ -245,21 +245,23 @@ def bench_gpu(args):
     # the timed step: the whole frame replayed from one CUDA graph (captured once; the kernel
     # timer's event pairs around k_knn_search / k_align / the seed pass are part of the graph)
     cap_stream = torch.cuda.Stream(dev)
-    g.debug_kernel_timer(True)
+    # kernel timer: the dominant kernels (level 1); BENCH_SPANS=1 adds the stage spans (level 2,
+    # more event nodes in the graph: diagnostic only)
+    g.debug_kernel_timer(2 if os.environ.get("BENCH_SPANS") == "1" else 1)
     step()  # creates the timer events outside the capture
     torch.cuda.synchronize()
     l0 = g.launch_count()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=cap_stream):
+    graph = g.FrameGraph()  # instantiated with per-node priorities (critical path high, seeds low)
+    with graph.capture(cap_stream):
         step()
     launches_per_step = g.launch_count() - l0
     g.debug_kernel_timer(False)
     for _ in range(max(args.warmup, 3)):
-        graph.replay()
+        graph.replay(stream)
     torch.cuda.synchronize()
     e0 = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
     e1 = [torch.cuda.Event(enable_timing=True) for _ in range(nev)]
-    kt = {k: [] for k in (g.KT_KNN_SEARCH, g.KT_ALIGN, g.KT_SEED)}
+    kt = {k: [] for k in (g.KT_KNN_SEARCH, g.KT_ALIGN, g.KT_SEED, g.KT_BP, g.KT_COVS, g.KT_WIDE, g.KT_TAIL)}
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -267,7 +269,7 @@ def bench_gpu(args):
         for i in range(nev):
             flush.zero_()  # L2 flush (256 MB > 126 MB L2), outside the timed events
             e0[i].record(stream)
-            graph.replay()
+            graph.replay(stream)
             e1[i].record(stream)
             torch.cuda.synchronize()  # per-step kernel timer readout (host side, outside the events)
             for k in kt:
@@ -334,7 +336,7 @@ def bench_gpu(args):
     # dominant kernel of the step, timed live (kernel timer events inside the replayed graph)
     kms = {k: float(np.mean([x for x in v if x is not None])) if any(x is not None for x in v) else None
            for k, v in kt.items()}
-    cand = {"k_knn_search": (kms[g.KT_KNN_SEARCH], ALGO_BYTES_KNN_SEARCH * n_src),
+    cand = {"k_knn_image": (kms[g.KT_KNN_SEARCH], ALGO_BYTES_KNN * n_src),
             "k_align": (kms[g.KT_ALIGN], ALGO_BYTES_ALIGN * n_src * iters)}
     kernel = max((k for k in cand if cand[k][0] is not None), key=lambda k: cand[k][0])
     kernel_ms, algo = cand[kernel]
@@ -352,8 +354,12 @@ def bench_gpu(args):
                    "l2": "flushed between timed steps (256 MB write)"},
         "timing": "CUDA graph replay of the whole frame, CUDA events per step on the launch stream",
         "stage_ms_eager": {names[j]: float(mean_stage[j]) for j in range(3)},
-        "kernel_ms": {"k_knn_search": kms[g.KT_KNN_SEARCH], "k_align": kms[g.KT_ALIGN],
-                      "seed pass (k_align_seed + k_align_seed_hard, side stream)": kms[g.KT_SEED]},
+        "kernel_ms": {"k_knn_image (11x11 window tile)": kms[g.KT_KNN_SEARCH], "k_align": kms[g.KT_ALIGN],
+                      "seed pass (k_align_seed + k_align_seed_hard, side stream)": kms[g.KT_SEED],
+                      "A1 (k_bp_count + k_bp_emit)": kms[g.KT_BP],
+                      "A2-A4 gsicp_covariances_image, main-stream span": kms[g.KT_COVS],
+                      "wide window + brute force + hash_n": kms[g.KT_WIDE],
+                      "hash join + search + epilogue": kms[g.KT_TAIL]},
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                      "algo_bytes_per_launch": algo, "kernel_ms": kernel_ms},

@@ -122,6 +122,16 @@ gsicp_status gsicp_backproject_sampled_rows(const float *depth_rows, int32_t H, 
                                             gsicp_intrinsics K, int32_t stride, float z_min, float z_max,
                                             float *pos_out, int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes,
                                             void *stream);
+/* A1 that also writes the lattice map lattice_map_out [dev] int32[ceil(H/s)*ceil(W/s)]: the output
+ * index of each sampled pixel (row-major lattice), -1 where the pixel is invalid — the index the
+ * image-window kNN uses (gsicp_covariances_image), built here for free.  rows_sampled = 0: depth is
+ * the full image (as gsicp_backproject_downsample); 1: only the sampled rows (as
+ * gsicp_backproject_sampled_rows).  Errors as above. */
+gsicp_status gsicp_backproject_lattice(const float *depth, int32_t rows_sampled, int32_t H, int32_t W,
+                                       int32_t row_pitch_elems, gsicp_intrinsics K, int32_t stride, float z_min,
+                                       float z_max, float *pos_out, int32_t cap, int32_t *d_n_out,
+                                       int32_t *lattice_map_out, void *ws, size_t ws_bytes, void *stream);
+
 /* Host -> device staging for it: copies rows 0, stride, 2*stride, ... of a host depth image
  * (src_pitch_elems floats per row; pinned memory for an asynchronous copy) into dst_rows
  * [dev] (ceil(H/stride) rows of W floats), stream-ordered.  Errors: INVALID_ARGUMENT, CUDA. */
@@ -158,12 +168,15 @@ gsicp_status gsicp_covariances(const float *pos, const int32_t *d_n, int32_t cap
  * finished by the hash search of gsicp_covariances (cell0, levels as there).  A cloud that is
  * not a depth-frame cloud (a pixel id off the lattice, two points on one pixel) is detected on
  * the device and handled entirely by the hash search, so the result is exact for any input.
+ *  lattice_map [dev] nullable: the map gsicp_backproject_lattice wrote for exactly these points
+ *  (then it is used as is, not rebuilt or validated); NULL: built and validated here.
  *  Errors: INVALID_ARGUMENT. */
 size_t gsicp_covariances_image_workspace_size(int32_t cap, int32_t levels, int32_t H, int32_t W, int32_t stride);
 gsicp_status gsicp_covariances_image(const float *pos, const int32_t *d_n, int32_t cap, int32_t H, int32_t W,
                                      int32_t stride, gsicp_intrinsics K, int32_t k, gsicp_reg_mode mode,
                                      float eps_var, float cell0, int32_t levels, float *cov_a, float *cov_b,
-                                     int32_t *knn_idx, void *ws, size_t ws_bytes, void *stream);
+                                     int32_t *knn_idx, const int32_t *lattice_map, void *ws, size_t ws_bytes,
+                                     void *stream);
 
 /* ---------------------------------------------------------------------------------------
  * A5  Map Gaussians -> G-ICP targets (the map's Gaussians are reused as
@@ -244,14 +257,26 @@ void gsicp_debug_align_timeline(int64_t *d_out, int64_t capacity);
  * summed over the GN iterations (int32, device, >= 4*cap entries).  NULL switches it off. */
 void gsicp_debug_align_counters(int32_t *d_out);
 
-/* DIAGNOSTIC: kernel timer.  While enabled (non-zero) on the calling thread, the launches of
- * the hot kernels record a CUDA event pair around themselves on their stream (also inside a
+/* DIAGNOSTIC: kernel timer.  While enabled (1: spans 0-2 below; 2: all spans) on the calling
+ * thread, the launches of the hot kernels record a CUDA event pair around themselves on their stream (also inside a
  * stream capture: the events then record at every graph replay).  gsicp_debug_kernel_time
- * returns 1 and the elapsed ms of the LAST recorded launch of `kernel` (0 = k_knn_search of
- * gsicp_covariances, 1 = k_align of the align calls, 2 = the two seed kernels of
- * gsicp_align_seed); the caller synchronises first.  Returns 0 if none was recorded. */
+ * returns 1 and the elapsed ms of the LAST recorded span `kernel`: 0 = the kNN search kernel
+ * (k_knn_search of gsicp_covariances; the 11x11 window kernel of gsicp_covariances_image),
+ * 1 = k_align of the align calls, 2 = the two seed kernels of gsicp_align_seed, 3 = A1,
+ * 4 = gsicp_covariances_image on the caller's stream (all of it), 5 = its wide-window + brute
+ * force stage, 6 = its hash tail (join + search + epilogue); the caller synchronises first.
+ * Returns 0 if none was recorded. */
 void gsicp_debug_kernel_timer(int enable);
 int gsicp_debug_kernel_time(int kernel, float *ms);
+
+/* CUDA-graph helpers for callers that capture a whole frame (host pointers; stream-ordered).
+ * gsicp_graph_instantiate: instantiates a captured graph (cudaGraph_t) so that kernel nodes keep
+ * their launch priorities (cudaGraphInstantiateFlagUseNodePriority): the frame's critical path
+ * runs at high priority and the side-stream work (iteration-0 seeds) at low priority.
+ * gsicp_graph_launch / gsicp_graph_destroy: launch on a stream / destroy the executable graph. */
+gsicp_status gsicp_graph_instantiate(void *graph, void **exec_out);
+gsicp_status gsicp_graph_launch(void *exec, void *stream);
+gsicp_status gsicp_graph_destroy(void *exec);
 
 /* Misc */
 const char *gsicp_status_string(gsicp_status s);

@@ -11,6 +11,7 @@ Public API (names follow include/gsicp.h):
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import dataclasses
 import math
@@ -80,13 +81,15 @@ def lib():
         L.gsicp_backproject_downsample.argtypes = [P, i32, i32, i32, Intrinsics, i32, f32, f32, P, i32, P, P, sz, P]
         L.gsicp_backproject_sampled_rows.argtypes = [P, i32, i32, i32, Intrinsics, i32, f32, f32, P, i32, P, P, sz, P]
         L.gsicp_upload_sampled_rows.argtypes = [P, P, i32, i32, i32, i32, P]
+        L.gsicp_backproject_lattice.argtypes = [P, i32, i32, i32, i32, Intrinsics, i32, f32, f32, P, i32, P, P, P,
+                                                sz, P]
         L.gsicp_covariances_workspace_size.argtypes = [i32, i32]
         L.gsicp_covariances_workspace_size.restype = sz
         L.gsicp_covariances.argtypes = [P, P, i32, i32, i32, f32, f32, i32, P, P, P, P, sz, P]
         L.gsicp_covariances_image_workspace_size.argtypes = [i32, i32, i32, i32, i32]
         L.gsicp_covariances_image_workspace_size.restype = sz
         L.gsicp_covariances_image.argtypes = [P, P, i32, i32, i32, i32, Intrinsics, i32, i32, f32, f32, i32, P, P, P,
-                                              P, sz, P]
+                                              P, P, sz, P]
         L.gsicp_build_target_workspace_size.argtypes = [i32]
         L.gsicp_build_target_workspace_size.restype = sz
         L.gsicp_build_target.argtypes = [P, P, P, i32, i32, i32, f32, f32, C.POINTER(_Target), P, sz, P]
@@ -110,11 +113,17 @@ def lib():
         L.gsicp_debug_align_timeline.restype = None
         L.gsicp_debug_align_counters.argtypes = [P]
         L.gsicp_debug_align_counters.restype = None
+        L.gsicp_graph_instantiate.argtypes = [P, C.POINTER(C.c_void_p)]
+        L.gsicp_graph_launch.argtypes = [P, P]
+        L.gsicp_graph_destroy.argtypes = [P]
+        for name in ("gsicp_graph_instantiate", "gsicp_graph_launch", "gsicp_graph_destroy"):
+            getattr(L, name).restype = i32
         L.gsicp_debug_kernel_timer.argtypes = [i32]
         L.gsicp_debug_kernel_timer.restype = None
         L.gsicp_debug_kernel_time.argtypes = [i32, C.POINTER(C.c_float)]
         L.gsicp_debug_kernel_time.restype = i32
         for name in ("gsicp_backproject_downsample", "gsicp_backproject_sampled_rows", "gsicp_upload_sampled_rows",
+                     "gsicp_backproject_lattice",
                      "gsicp_covariances", "gsicp_covariances_image", "gsicp_build_target",
                      "gsicp_build_target_cloud", "gsicp_align", "gsicp_align_async", "gsicp_align_seed",
                      "gsicp_linearize"):
@@ -125,22 +134,22 @@ def lib():
 
 EXPORTED = [
     "gsicp_backproject_workspace_size", "gsicp_backproject_downsample", "gsicp_backproject_sampled_rows",
-    "gsicp_upload_sampled_rows", "gsicp_covariances_workspace_size",
+    "gsicp_upload_sampled_rows", "gsicp_backproject_lattice", "gsicp_covariances_workspace_size",
     "gsicp_covariances", "gsicp_covariances_image_workspace_size", "gsicp_covariances_image",
     "gsicp_build_target_workspace_size", "gsicp_build_target", "gsicp_build_target_cloud",
     "gsicp_align_workspace_size", "gsicp_align", "gsicp_align_async", "gsicp_align_seed", "gsicp_linearize",
     "gsicp_status_string",
     "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version", "gsicp_debug_knn_counters",
     "gsicp_debug_align_timeline", "gsicp_debug_align_counters", "gsicp_debug_kernel_timer",
-    "gsicp_debug_kernel_time",
+    "gsicp_debug_kernel_time", "gsicp_graph_instantiate", "gsicp_graph_launch", "gsicp_graph_destroy",
 ]
 
-KT_KNN_SEARCH, KT_ALIGN, KT_SEED = 0, 1, 2
+KT_KNN_SEARCH, KT_ALIGN, KT_SEED, KT_BP, KT_COVS, KT_WIDE, KT_TAIL = 0, 1, 2, 3, 4, 5, 6
 
 
-def debug_kernel_timer(enable: bool):
+def debug_kernel_timer(enable):
     """Diagnostic: the hot kernels record CUDA events around their launches (see gsicp.h)."""
-    lib().gsicp_debug_kernel_timer(1 if enable else 0)
+    lib().gsicp_debug_kernel_timer(int(enable))
 
 
 def debug_kernel_time(kernel: int) -> float | None:
@@ -290,6 +299,30 @@ def backproject_sampled_rows(rows: torch.Tensor, H: int, W: int, K, stride: int 
     return pos_out, d_n
 
 
+def backproject_lattice(depth: torch.Tensor, H: int, W: int, K, stride: int = 4, rows_sampled: bool = False,
+                        z_min: float = 0.1, z_max: float = 10.0, pos_out: torch.Tensor | None = None,
+                        d_n: torch.Tensor | None = None, lattice: torch.Tensor | None = None,
+                        ws: torch.Tensor | None = None, stream=None):
+    """A1 (from the full image, or from its sampled rows) that also writes the lattice map
+    (output index of every sampled pixel, -1 if invalid).  Returns (pos, d_n, lattice)."""
+    pitch = depth.stride(0)
+    Hs, Ws = (H + stride - 1) // stride, (W + stride - 1) // stride
+    dev = depth.device
+    if pos_out is None:
+        pos_out = torch.empty((Hs * Ws, 4), dtype=torch.float32, device=dev)
+    if d_n is None:
+        d_n = torch.zeros(1, dtype=torch.int32, device=dev)
+    if lattice is None:
+        lattice = torch.empty(Hs * Ws, dtype=torch.int32, device=dev)
+    if ws is None:
+        ws = _ws(lib().gsicp_backproject_workspace_size(H, W, stride), dev)
+    Kc = K if isinstance(K, Intrinsics) else Intrinsics(*K)
+    _check(lib().gsicp_backproject_lattice(C.c_void_p(depth.data_ptr()), 1 if rows_sampled else 0, H, W, pitch, Kc,
+                                           stride, z_min, z_max, _ptr(pos_out), pos_out.shape[0], _ptr(d_n),
+                                           _ptr(lattice), _ptr(ws), ws.numel(), _stream(stream)))
+    return pos_out, d_n, lattice
+
+
 def upload_sampled_rows(dst_rows: torch.Tensor, depth_host: torch.Tensor, stride: int, stream=None):
     """Copy rows 0, s, 2s, ... of a (pinned) host depth image into dst_rows (device), async."""
     H, W = depth_host.shape
@@ -319,9 +352,11 @@ def covariances(pos: torch.Tensor, d_n: torch.Tensor, k: int = 20, mode: int = R
 
 def covariances_image(pos: torch.Tensor, d_n: torch.Tensor, H: int, W: int, stride: int, K, k: int = 20,
                       mode: int = REG_ELLIPSE, eps_var: float = 1e-3, cell0: float = 0.01, levels: int = 1,
-                      cov_a=None, cov_b=None, knn_idx: torch.Tensor | None = None, ws=None, stream=None):
+                      cov_a=None, cov_b=None, knn_idx: torch.Tensor | None = None, ws=None, stream=None,
+                      lattice: torch.Tensor | None = None):
     """A2-A4 for a depth-frame cloud from backproject_downsample(H, W, stride, K): the
-    image-window kNN (same result as covariances()).  Returns a Cloud sharing `pos`."""
+    image-window kNN (same result as covariances()).  `lattice`: the map backproject_lattice
+    wrote for these points (else built here).  Returns a Cloud sharing `pos`."""
     cap = pos.shape[0]
     dev = pos.device
     if cov_a is None:
@@ -333,7 +368,7 @@ def covariances_image(pos: torch.Tensor, d_n: torch.Tensor, H: int, W: int, stri
         ws = _ws(need, dev)
     Kc = K if isinstance(K, Intrinsics) else Intrinsics(*K)
     _check(lib().gsicp_covariances_image(_ptr(pos), _ptr(d_n), cap, H, W, stride, Kc, k, mode, eps_var, cell0, levels,
-                                         _ptr(cov_a), _ptr(cov_b), _ptr(knn_idx), _ptr(ws), ws.numel(),
+                                         _ptr(cov_a), _ptr(cov_b), _ptr(knn_idx), _ptr(lattice), _ptr(ws), ws.numel(),
                                          _stream(stream)))
     return Cloud(pos, cov_a, cov_b, d_n)
 
@@ -453,6 +488,32 @@ def linearize(src: Cloud, tgt: Target, T, max_corr_dist: float = math.inf, corr_
     return dict(H=H, b=b, cost=cost.value, n=n.value)
 
 
+class FrameGraph:
+    """A stream capture instantiated with per-node launch priorities (gsicp_graph_instantiate):
+    the critical-path kernels run high, the side-stream work low.  Usage:
+        fg = FrameGraph(); with fg.capture(stream): ...; fg.replay(stream)"""
+
+    def __init__(self):
+        self._g = torch.cuda.CUDAGraph(keep_graph=True)
+        self._exec = C.c_void_p()
+
+    @contextlib.contextmanager
+    def capture(self, stream):
+        with torch.cuda.graph(self._g, stream=stream):
+            yield
+        _check(lib().gsicp_graph_instantiate(C.c_void_p(self._g.raw_cuda_graph()), C.byref(self._exec)))
+
+    def replay(self, stream=None):
+        _check(lib().gsicp_graph_launch(self._exec, _stream(stream)))
+
+    def __del__(self):
+        try:
+            if self._exec:
+                lib().gsicp_graph_destroy(self._exec)
+        except Exception:
+            pass
+
+
 class Tracker:
     """Per-frame tracking pipeline with preallocated buffers: A1 -> A2-A4 -> A6-A9 against a
     prebuilt target.  Public per-frame calls: `track()` (depth already on the device) and
@@ -473,6 +534,7 @@ class Tracker:
         self.device = torch.device(device)
         self.cloud = Cloud.empty(self.cap, self.device)
         self.rows = torch.empty(((H + stride - 1) // stride, W), dtype=torch.float32, device=self.device)
+        self.lattice = torch.empty(self.cap, dtype=torch.int32, device=self.device)
         self.ws_bp = _ws(lib().gsicp_backproject_workspace_size(H, W, stride), self.device)
         self.ws_cov = _ws(lib().gsicp_covariances_image_workspace_size(self.cap, levels, H, W, stride), self.device)
         self.ws_align = align_workspace(self.cap, self.device)
@@ -487,14 +549,19 @@ class Tracker:
         self._st_out = torch.zeros(C.sizeof(AlignStats), dtype=torch.uint8).pin_memory()
 
     def preprocess(self, depth: torch.Tensor, stream=None):
-        backproject_downsample(depth, self.K, self.stride, self.z_min, self.z_max, self.cloud.pos, self.cloud.d_n,
-                               self.ws_bp, stream)
+        self._backproject(depth, stream)
         self._covariances(stream)
+
+    def _backproject(self, depth, stream):
+        """A1 from `depth`, or from the sampled-row buffer `self.rows` when depth is None; also
+        writes the lattice map the image-window kNN uses."""
+        backproject_lattice(self.rows if depth is None else depth, self.H, self.W, self.K, self.stride, depth is None,
+                            self.z_min, self.z_max, self.cloud.pos, self.cloud.d_n, self.lattice, self.ws_bp, stream)
 
     def _covariances(self, stream):
         covariances_image(self.cloud.pos, self.cloud.d_n, self.H, self.W, self.stride, self.K, self.k, self.mode,
                           self.eps, self.cell0, self.levels, self.cloud.cov_a, self.cloud.cov_b, None, self.ws_cov,
-                          stream)
+                          stream, self.lattice)
 
     def step_async(self, depth: torch.Tensor | None, tgt: Target, stream=None, events=None):
         """Whole frame, device-resident pose in self.d_T (set it before), no host sync.
@@ -505,20 +572,18 @@ class Tracker:
         s0 = stream if stream is not None else torch.cuda.current_stream(self.device)
         if events:
             events[0].record(s0)
-        if depth is None:
-            backproject_sampled_rows(self.rows, self.H, self.W, self.K, self.stride, self.z_min, self.z_max,
-                                     self.cloud.pos, self.cloud.d_n, self.ws_bp, s0)
-        else:
-            backproject_downsample(depth, self.K, self.stride, self.z_min, self.z_max, self.cloud.pos,
-                                   self.cloud.d_n, self.ws_bp, s0)
+        self._backproject(depth, s0)
         if events:
             events[1].record(s0)
-        self._fork.record(s0)
-        self._side.wait_event(self._fork)
-        align_seed(self.cloud, tgt, self.d_T, self.params, self.ws_align, self._side)
-        self._join.record(self._side)
+        seed = os.environ.get("GSICP_NO_SEED", "0") != "1"  # (A/B diagnostic switch)
+        if seed:
+            self._fork.record(s0)
+            self._side.wait_event(self._fork)
+            align_seed(self.cloud, tgt, self.d_T, self.params, self.ws_align, self._side)
+            self._join.record(self._side)
         self._covariances(s0)
-        s0.wait_event(self._join)
+        if seed:
+            s0.wait_event(self._join)
         if events:
             events[2].record(s0)
         align_async(self.cloud, tgt, self.d_T, self.d_stats, self.params, self.ws_align, None, s0)
@@ -534,8 +599,8 @@ class Tracker:
         s.wait_stream(torch.cuda.current_stream(self.device))
         self.step_async(depth, tgt, s)  # one run outside the capture (lazy library state)
         s.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s):
+        g = FrameGraph()
+        with g.capture(s):
             self.step_async(depth, tgt, s)
         self._graphs[key] = (g, depth, tgt)  # keep the captured buffers alive
         return g
@@ -548,7 +613,7 @@ class Tracker:
             self.d_T.copy_(self._T_host, non_blocking=True)
             if upload is not None:
                 upload(s0)
-            g.replay()
+            g.replay(s0)
             self._T_out.copy_(self.d_T, non_blocking=True)
             self._st_out.copy_(self.d_stats, non_blocking=True)
         s0.synchronize()

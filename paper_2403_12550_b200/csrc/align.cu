@@ -762,12 +762,15 @@ __global__ void __launch_bounds__(kSeedHardT) k_align_seed_hard(AlignArgs a) {
 }
 
 __global__ void k_align_init(int32_t *corr_ws, int cap, unsigned int *barrier) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < cap) corr_ws[i] = -1;
     if (i == 0) *barrier = 0u;
 }
 
 __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
+    pdl_wait();  // (no early launch of dependents: they must not take SMs from this cooperative grid)
     __shared__ double sT[12];
     __shared__ double sRed[kWarps][kPad];
     __shared__ double sAcc[kPad];
@@ -1247,9 +1250,9 @@ cudaError_t align_seed_launch(const gsicp_cloud &src, const gsicp_target &tgt, c
         return e;
     }
     ktimer_mark(KT_SEED, false, s);
-    k_align_seed<<<blocks_for(src.cap > 0 ? src.cap : 1, kSeedT), kSeedT, 0, s>>>(a);
+    launch_low(k_align_seed, dim3(blocks_for(src.cap > 0 ? src.cap : 1, kSeedT)), dim3(kSeedT), 0, s, a);
     GSICP_LAUNCH_CHECK("k_align_seed");
-    k_align_seed_hard<<<num_sms() * 8, kSeedHardT, 0, s>>>(a);
+    launch_low(k_align_seed_hard, dim3(num_sms() * 8), dim3(kSeedHardT), 0, s, a);
     GSICP_LAUNCH_CHECK("k_align_seed_hard");
     ktimer_mark(KT_SEED, true, s);
     note_launch(2);
@@ -1263,7 +1266,8 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
     AlignArgs a = make_args(src, tgt, d_T_inout, p, d_stats, corr_out, linearize_only, r_lin, w);
     a.seed_ticket = (g_seed_ws == ws && g_seed_src == src.pos && g_seed_tgt == tgt.pos) ? g_seed_ticket : 0.0;
     g_seed_ws = nullptr;
-    k_align_init<<<blocks_for(src.cap > 0 ? src.cap : 1, 256), 256, 0, s>>>(w.corr_ws, src.cap, w.barrier);
+    launch_pdl(k_align_init, dim3(blocks_for(src.cap > 0 ? src.cap : 1, 256)), dim3(256), 0, s, w.corr_ws, src.cap,
+               w.barrier);
     GSICP_LAUNCH_CHECK("k_align_init");
     int per_sm = 0;
     const int G = align_grid_blocks(src.cap, &per_sm);
@@ -1275,15 +1279,17 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
         return cudaErrorCooperativeLaunchTooLarge;
     }
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributePriority;
+    at[1].val.priority = launch_priority(true);
     cfg.gridDim = dim3(G);
     cfg.blockDim = dim3(kT);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     ktimer_mark(KT_ALIGN, false, s);
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_align, a);
     ktimer_mark(KT_ALIGN, true, s);

@@ -18,12 +18,13 @@ extern thread_local int32_t *g_align_debug;
 
 void note_launch(int n) { g_launches += (uint64_t)n; }
 
-static thread_local bool g_ktimer_on = false;
+static thread_local int g_ktimer_on = 0;
 static thread_local cudaEvent_t g_kt_ev[KT_COUNT][2] = {};
 static thread_local bool g_kt_used[KT_COUNT] = {};
 
 void ktimer_mark(int id, bool stop, cudaStream_t s) {
     if (!g_ktimer_on || id < 0 || id >= KT_COUNT) return;
+    if (id >= KT_BP && g_ktimer_on < 2) return;  // stage spans only at level 2
     cudaEvent_t &ev = g_kt_ev[id][stop ? 1 : 0];
     if (!ev && cudaEventCreate(&ev) != cudaSuccess) {
         ev = nullptr;
@@ -48,7 +49,7 @@ void set_error(const char *fmt, ...) {
 size_t backproject_ws_bytes(int H, int W, int stride);
 cudaError_t backproject_launch(const float *depth, int H, int W, int pitch, gsicp_intrinsics K, int stride,
                                float zmin, float zmax, float *pos_out, int32_t *d_n, void *ws, cudaStream_t s,
-                               int rows_sampled);
+                               int rows_sampled, int32_t *map);
 size_t covariances_ws_bytes(int cap, int levels);
 cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, int k, int mode, float eps,
                                float cell0, int levels, float *cov_a, float *cov_b, int32_t *knn_idx, void *ws,
@@ -56,7 +57,8 @@ cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, in
 size_t covariances_image_ws_bytes(int cap, int levels, int H, int W, int stride);
 cudaError_t covariances_image_launch(const float *pos, const int32_t *d_n, int cap, int H, int W, int stride,
                                      gsicp_intrinsics K, int k, int mode, float eps, float cell0, int levels,
-                                     float *cov_a, float *cov_b, int32_t *knn_idx, void *ws, cudaStream_t s);
+                                     float *cov_a, float *cov_b, int32_t *knn_idx, const int32_t *lattice_map,
+                                     void *ws, cudaStream_t s);
 size_t target_ws_bytes(int M);
 cudaError_t build_target_launch(const float *means, const float *quats, const float *scales, int scales_are_log,
                                 int M, int mode, float eps, float cell, gsicp_target *out, void *ws,
@@ -137,7 +139,26 @@ const char *gsicp_last_error(void) { return g_err; }
 void gsicp_debug_knn_counters(int32_t *d_out) { gsicp::g_knn_debug = d_out; }
 void gsicp_debug_align_counters(int32_t *d_out) { gsicp::g_align_debug = d_out; }
 
-void gsicp_debug_kernel_timer(int enable) { gsicp::g_ktimer_on = enable != 0; }
+gsicp_status gsicp_graph_instantiate(void *graph, void **exec_out) {
+    g_err[0] = 0;
+    if (!graph || !exec_out) BAD("graph_instantiate: null pointer");
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t e = cudaGraphInstantiateWithFlags(&ex, (cudaGraph_t)graph, cudaGraphInstantiateFlagUseNodePriority);
+    *exec_out = ex;
+    return cuda_status(e, "graph_instantiate");
+}
+gsicp_status gsicp_graph_launch(void *exec, void *stream) {
+    g_err[0] = 0;
+    if (!exec) BAD("graph_launch: null exec");
+    return cuda_status(cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream), "graph_launch");
+}
+gsicp_status gsicp_graph_destroy(void *exec) {
+    g_err[0] = 0;
+    if (!exec) return GSICP_OK;
+    return cuda_status(cudaGraphExecDestroy((cudaGraphExec_t)exec), "graph_destroy");
+}
+
+void gsicp_debug_kernel_timer(int enable) { gsicp::g_ktimer_on = enable < 0 ? 0 : enable; }
 
 int gsicp_debug_kernel_time(int kernel, float *ms) {
     using namespace gsicp;
@@ -159,7 +180,7 @@ size_t gsicp_backproject_workspace_size(int32_t H, int32_t W, int32_t stride) {
 static gsicp_status backproject_common(const float *depth_m, int32_t H, int32_t W, int32_t row_pitch_elems,
                                        gsicp_intrinsics K, int32_t stride, float z_min, float z_max, float *pos_out,
                                        int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes, void *stream,
-                                       int rows_sampled) {
+                                       int rows_sampled, int32_t *map) {
     g_err[0] = 0;
     if (!depth_m || !pos_out || !d_n_out) BAD("backproject: null pointer");
     if (H < 1 || W < 1 || stride < 1 || row_pitch_elems < W) BAD("backproject: bad image geometry");
@@ -171,7 +192,7 @@ static gsicp_status backproject_common(const float *depth_m, int32_t H, int32_t 
     gsicp_status st = check_ws(ws, ws_bytes, backproject_ws_bytes(H, W, stride));
     if (st != GSICP_OK) return st;
     return cuda_status(backproject_launch(depth_m, H, W, row_pitch_elems, K, stride, z_min, z_max, pos_out, d_n_out, ws,
-                                          (cudaStream_t)stream, rows_sampled),
+                                          (cudaStream_t)stream, rows_sampled, map),
                        "backproject");
 }
 
@@ -180,7 +201,19 @@ gsicp_status gsicp_backproject_downsample(const float *depth_m, int32_t H, int32
                                           float *pos_out, int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes,
                                           void *stream) {
     return backproject_common(depth_m, H, W, row_pitch_elems, K, stride, z_min, z_max, pos_out, cap, d_n_out, ws,
-                              ws_bytes, stream, 0);
+                              ws_bytes, stream, 0, nullptr);
+}
+
+gsicp_status gsicp_backproject_lattice(const float *depth, int32_t rows_sampled, int32_t H, int32_t W,
+                                       int32_t row_pitch_elems, gsicp_intrinsics K, int32_t stride, float z_min,
+                                       float z_max, float *pos_out, int32_t cap, int32_t *d_n_out,
+                                       int32_t *lattice_map_out, void *ws, size_t ws_bytes, void *stream) {
+    if (rows_sampled != 0 && rows_sampled != 1) {
+        g_err[0] = 0;
+        BAD("backproject_lattice: rows_sampled must be 0 or 1");
+    }
+    return backproject_common(depth, H, W, row_pitch_elems, K, stride, z_min, z_max, pos_out, cap, d_n_out, ws,
+                              ws_bytes, stream, rows_sampled, lattice_map_out);
 }
 
 gsicp_status gsicp_backproject_sampled_rows(const float *depth_rows, int32_t H, int32_t W, int32_t row_pitch_elems,
@@ -188,7 +221,7 @@ gsicp_status gsicp_backproject_sampled_rows(const float *depth_rows, int32_t H, 
                                             float *pos_out, int32_t cap, int32_t *d_n_out, void *ws, size_t ws_bytes,
                                             void *stream) {
     return backproject_common(depth_rows, H, W, row_pitch_elems, K, stride, z_min, z_max, pos_out, cap, d_n_out, ws,
-                              ws_bytes, stream, 1);
+                              ws_bytes, stream, 1, nullptr);
 }
 
 gsicp_status gsicp_upload_sampled_rows(float *dst_rows, const float *src_host, int32_t H, int32_t W,
@@ -235,7 +268,7 @@ size_t gsicp_covariances_image_workspace_size(int32_t cap, int32_t levels, int32
 gsicp_status gsicp_covariances_image(const float *pos, const int32_t *d_n, int32_t cap, int32_t H, int32_t W,
                                      int32_t stride, gsicp_intrinsics K, int32_t k, gsicp_reg_mode mode, float eps_var,
                                      float cell0, int32_t levels, float *cov_a, float *cov_b, int32_t *knn_idx,
-                                     void *ws, size_t ws_bytes, void *stream) {
+                                     const int32_t *lattice_map, void *ws, size_t ws_bytes, void *stream) {
     g_err[0] = 0;
     if (!pos || !d_n || !cov_a || !cov_b) BAD("covariances_image: null pointer");
     if (!aligned16(pos) || !aligned16(cov_a) || !aligned16(cov_b)) BAD("covariances_image: arrays must be 16-byte aligned");
@@ -251,7 +284,7 @@ gsicp_status gsicp_covariances_image(const float *pos, const int32_t *d_n, int32
     gsicp_status st = check_ws(ws, ws_bytes, covariances_image_ws_bytes(cap, levels, H, W, stride));
     if (st != GSICP_OK) return st;
     return cuda_status(covariances_image_launch(pos, d_n, cap, H, W, stride, K, k, (int)mode, eps_var, cell0, levels,
-                                                cov_a, cov_b, knn_idx, ws, (cudaStream_t)stream),
+                                                cov_a, cov_b, knn_idx, lattice_map, ws, (cudaStream_t)stream),
                        "covariances_image");
 }
 

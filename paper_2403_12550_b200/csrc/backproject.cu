@@ -17,6 +17,7 @@ struct BpArgs {
     const float *depth;
     int H, W, pitch, stride, Ws, Hs;  // Ws, Hs: sampled lattice size
     int rows_sampled;                 // depth holds only the sampled rows (row r = image row r*stride)
+    int32_t *map;                     // nullable [Hs*Ws]: output index of each sampled pixel, -1 if invalid
     float fx, fy, cx, cy, zmin, zmax;
     float4 *out;
     int32_t *d_n;
@@ -34,6 +35,8 @@ __device__ __forceinline__ bool bp_valid(const BpArgs &a, int j, float &z, int &
 }
 
 __global__ void k_bp_count(BpArgs a) {
+    pdl_wait();
+    pdl_launch_dependents();
     __shared__ uint32_t warp_tot[kBpThreads / 32];
     const int base = blockIdx.x * kBpTile + threadIdx.x * kBpPerThread;
     uint32_t c = 0;
@@ -55,6 +58,8 @@ __global__ void k_bp_count(BpArgs a) {
 }
 
 __global__ void k_bp_emit(BpArgs a) {
+    pdl_wait();
+    pdl_launch_dependents();
     __shared__ uint32_t red[kBpThreads / 32];
     __shared__ uint32_t warp_excl[kBpThreads / 32];
     __shared__ uint32_t s_prefix;
@@ -98,6 +103,12 @@ __global__ void k_bp_emit(BpArgs a) {
     }
     __syncthreads();
     uint32_t dst = s_prefix + warp_excl[warp] + incl - mine;
+    if (a.map) {
+        uint32_t d2 = dst;
+#pragma unroll
+        for (int e = 0; e < kBpPerThread; ++e)
+            if (base + e < a.Ws * a.Hs) a.map[base + e] = ok[e] ? (int32_t)(d2++) : -1;
+    }
 #pragma unroll
     for (int e = 0; e < kBpPerThread; ++e) {
         if (!ok[e]) continue;
@@ -118,9 +129,10 @@ size_t backproject_ws_bytes(int H, int W, int stride) {
 
 cudaError_t backproject_launch(const float *depth, int H, int W, int pitch, gsicp_intrinsics K, int stride,
                                float zmin, float zmax, float *pos_out, int32_t *d_n, void *ws, cudaStream_t s,
-                               int rows_sampled) {
+                               int rows_sampled, int32_t *map) {
     BpArgs a;
     a.rows_sampled = rows_sampled;
+    a.map = map;
     a.depth = depth;
     a.H = H; a.W = W; a.pitch = pitch; a.stride = stride;
     a.Ws = (W + stride - 1) / stride;
@@ -131,10 +143,12 @@ cudaError_t backproject_launch(const float *depth, int H, int W, int pitch, gsic
     a.d_n = d_n;
     a.tile_counts = static_cast<uint32_t *>(ws);
     a.tiles = (int)(((long long)a.Ws * a.Hs + kBpTile - 1) / kBpTile);
-    k_bp_count<<<a.tiles, kBpThreads, 0, s>>>(a);
+    ktimer_mark(KT_BP, false, s);
+    launch_pdl(k_bp_count, dim3(a.tiles), dim3(kBpThreads), 0, s, a);
     GSICP_LAUNCH_CHECK("k_bp_count");
-    k_bp_emit<<<a.tiles, kBpThreads, 0, s>>>(a);
+    launch_pdl(k_bp_emit, dim3(a.tiles), dim3(kBpThreads), 0, s, a);
     GSICP_LAUNCH_CHECK("k_bp_emit");
+    ktimer_mark(KT_BP, true, s);
     note_launch(2);
     return cudaSuccess;
 }

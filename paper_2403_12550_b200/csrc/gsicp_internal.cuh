@@ -24,6 +24,12 @@ struct __align__(16) CellEntry {
     uint32_t count;
 };
 
+// Programmatic dependent launch: wait for the stream predecessor grid (its completion and memory
+// flush) — first statement of every kernel launched with launch_pdl — and let the next kernel of
+// the stream launch early (it waits the same way).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------------------------------
 // Canonical binary32 squared-distance key (R1): dx = a.x - b.x, key = (dx*dx + dy*dy) + dz*dz,
 // every op rounded separately (no FMA) so the CPU oracle reproduces it bit for bit.

@@ -246,6 +246,8 @@ __device__ bool knn_search_warp(const GridView &g, int level, float qx, float qy
 
 template <int K>
 __global__ void __launch_bounds__(kKnnThreads, kKnnMinBlocks) k_knn_search(KnnArgs a) {
+    pdl_wait();
+    pdl_launch_dependents();
     if (a.queue && *a.queue_n == 0u) return;  // empty fallback queue (block-uniform)
     const int n = *a.d_n;
     const GridView &g = a.g;
@@ -397,6 +399,8 @@ __device__ __forceinline__ void finish_query(const KnnArgs &a, int n, int i, flo
 // the t-th point in coarsest-cell order, or queue[t] in queue mode.
 template <int K>
 __global__ void __launch_bounds__(kKnnThreads) k_knn_epilogue(KnnArgs a) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int n = *a.d_n;
     const int nq = a.queue ? (int)*a.queue_n : n;
     const GridView &g = a.g;
@@ -445,6 +449,7 @@ constexpr int kImgWideM = 12;  // half-width of the wide window (warp per query)
 
 struct ImgArgs {
     int32_t *map;  // [Hs][Ws] point index of each lattice pixel, -1 if none
+    int map_given;  // the map came from A1 (gsicp_backproject_lattice): not rebuilt here
     uint32_t *queue2;
     int H, W, Hs, Ws, stride;
     float fx, fy;
@@ -452,15 +457,19 @@ struct ImgArgs {
     uint32_t *queue;
 };
 
-__global__ void k_img_map_clear(ImgArgs im) {
+__global__ void k_img_map_clear(ImgArgs im, int clear_map) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < im.Hs * im.Ws) im.map[j] = -1;
+    if (clear_map && j < im.Hs * im.Ws) im.map[j] = -1;
     if (j < kImgCounters) im.ctr[j] = 0u;
 }
 
 // lattice -> point map; a point whose pixel id is not a lattice pixel of this image, or two
 // points on one pixel, flag the cloud as not a depth-frame cloud (then every query is queued)
 __global__ void k_img_map_fill(ImgArgs im, const float4 *__restrict__ pos, const int32_t *__restrict__ d_n) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= *d_n) return;
     const int pix = __float_as_int(__ldg(pos + i).w);
@@ -502,6 +511,8 @@ __device__ __forceinline__ bool img_cert(const ImgArgs &im, float4 q, float key,
 
 template <int K, int M>
 __global__ void __launch_bounds__(kImgThreads, 4) k_knn_image(KnnArgs a, ImgArgs im) {
+    pdl_wait();
+    pdl_launch_dependents();
     constexpr int SW = kImgTX + 2 * M, SH = kImgTY + 2 * M;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float4(*tile)[SW] = reinterpret_cast<float4(*)[SW]>(smem_raw);
@@ -794,6 +805,8 @@ __device__ bool wide_attempt(const KnnArgs &a, const ImgArgs &im, int i, float4 
 // kImgWideM (keys cached in registers).  Misses go to the last queue.
 template <int K>
 __global__ void __launch_bounds__(128) k_knn_image_wide(KnnArgs a, ImgArgs im) {
+    pdl_wait();
+    pdl_launch_dependents();
     __shared__ uint32_t hist[4][kImgBuckets / 2][32];
     __shared__ unsigned long long lst[4][64];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -855,6 +868,8 @@ __device__ __forceinline__ void brute_bin_range(int bin, uint32_t &lo, uint32_t 
 template <int K>
 __global__ void __cluster_dims__(kBruteCluster, 1, 1) __launch_bounds__(kBruteThreads, 2)
     k_knn_brute(KnnArgs a, ImgArgs im) {
+    pdl_wait();
+    pdl_launch_dependents();
     __shared__ uint32_t bins[1024], gbins[1024];
     __shared__ uint32_t wsum[32];
     __shared__ unsigned long long lst[64];
@@ -984,6 +999,8 @@ __global__ void __cluster_dims__(kBruteCluster, 1, 1) __launch_bounds__(kBruteTh
 // the hash path takes the last queue when it is longer than kBruteMax, else whatever brute force
 // handed over (moved to the front of queue 2)
 __global__ void k_img_hash_n(ImgArgs im, const int32_t *__restrict__ d_n) {
+    pdl_wait();
+    pdl_launch_dependents();
     const uint32_t q2 = im.ctr[kImgCtrQueue2], q3 = im.ctr[kImgCtrQueue3];
     uint32_t hq = 0u;
     if (q2 > kBruteMax) {
@@ -1012,7 +1029,7 @@ cudaError_t launch_tile(const KnnArgs &a, const ImgArgs &im, cudaStream_t s) {
         attr = true;
     }
     const dim3 grid((unsigned)((im.Ws + kImgTX - 1) / kImgTX), (unsigned)((im.Hs + kImgTY - 1) / kImgTY));
-    k_knn_image<K, M><<<grid, kImgThreads, smem, s>>>(a, im);
+    launch_pdl(k_knn_image<K, M>, grid, dim3(kImgThreads), (size_t)smem, s, a, im);
     GSICP_LAUNCH_CHECK("k_knn_image");
     return cudaSuccess;
 }
@@ -1039,35 +1056,63 @@ static cudaError_t side_stream(SideStream *&out) {
     return cudaSuccess;
 }
 
+bool img_side_grid() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("GSICP_SIDE_GRID");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 template <int K>
 cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *pos, const int32_t *d_n, cudaStream_t s) {
     SideStream *ss = nullptr;
-    cudaError_t e = side_stream(ss);
-    if (e != cudaSuccess) return e;
-    // the hash of the cloud for the last-resort search, built off the critical path
-    if ((e = cudaEventRecord(ss->fork, s)) != cudaSuccess) return e;
-    if ((e = cudaStreamWaitEvent(ss->s, ss->fork, 0)) != cudaSuccess) return e;
-    e = grid_build(a.g, pos, nullptr, nullptr, d_n, cap, ss->s);
-    if (e != cudaSuccess) return e;
-    if ((e = cudaEventRecord(ss->join, ss->s)) != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
+    const bool side = img_side_grid();
+    if (side) {
+        // the hash of the cloud for the last-resort search, built off the critical path
+        if ((e = side_stream(ss)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ss->fork, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(ss->s, ss->fork, 0)) != cudaSuccess) return e;
+        e = grid_build(a.g, pos, nullptr, nullptr, d_n, cap, ss->s);
+        if (e != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ss->join, ss->s)) != cudaSuccess) return e;
+    }
+    ktimer_mark(KT_COVS, false, s);
     ktimer_mark(KT_KNN_SEARCH, false, s);
     const int L = im.Hs * im.Ws;
-    k_img_map_clear<<<blocks_for(std::max(L, kImgCounters), 256), 256, 0, s>>>(im);
-    GSICP_LAUNCH_CHECK("k_img_map_clear");
-    k_img_map_fill<<<blocks_for(cap, 256), 256, 0, s>>>(im, pos, d_n);
-    GSICP_LAUNCH_CHECK("k_img_map_fill");
+    if (im.map_given) {  // the map came with the points: only the counters are reset
+        launch_pdl(k_img_map_clear, dim3(1), dim3(32), 0, s, im, 0);
+        GSICP_LAUNCH_CHECK("k_img_map_clear");
+    } else {
+        launch_pdl(k_img_map_clear, dim3(blocks_for(std::max(L, kImgCounters), 256)), dim3(256), 0, s, im, 1);
+        GSICP_LAUNCH_CHECK("k_img_map_clear");
+        launch_pdl(k_img_map_fill, dim3(blocks_for(cap, 256)), dim3(256), 0, s, im, pos, d_n);
+        GSICP_LAUNCH_CHECK("k_img_map_fill");
+    }
     e = launch_tile<K>(a, im, s);
     if (e != cudaSuccess) return e;
     ktimer_mark(KT_KNN_SEARCH, true, s);
+    ktimer_mark(KT_WIDE, false, s);
     // wide window over the queue (a resident grid pulling queries)
-    k_knn_image_wide<K><<<(unsigned)num_sms() * 8, 128, 0, s>>>(a, im);
+    launch_pdl(k_knn_image_wide<K>, dim3((unsigned)num_sms() * 8), dim3(128), 0, s, a, im);
     GSICP_LAUNCH_CHECK("k_knn_image_wide");
     // the rest: brute force (a short queue), else the hash search + epilogue (long queue)
-    k_knn_brute<K><<<(unsigned)(2 * (num_sms() / kBruteCluster) * kBruteCluster), kBruteThreads, 0, s>>>(a, im);
+    launch_pdl(k_knn_brute<K>, dim3((unsigned)(2 * (num_sms() / kBruteCluster) * kBruteCluster)), dim3(kBruteThreads), 0,
+               s, a, im);
     GSICP_LAUNCH_CHECK("k_knn_brute");
-    k_img_hash_n<<<1, 1, 0, s>>>(im, d_n);
+    launch_pdl(k_img_hash_n, dim3(1), dim3(1), 0, s, im, d_n);
     GSICP_LAUNCH_CHECK("k_img_hash_n");
-    if ((e = cudaStreamWaitEvent(s, ss->join, 0)) != cudaSuccess) return e;
+    ktimer_mark(KT_WIDE, true, s);
+    ktimer_mark(KT_TAIL, false, s);
+    if (side) {
+        if ((e = cudaStreamWaitEvent(s, ss->join, 0)) != cudaSuccess) return e;
+    } else {  // inline, only for a non-empty hash queue (the build kernels return at once otherwise)
+        const int32_t *hn = reinterpret_cast<const int32_t *>(im.ctr + kImgCtrHashN);
+        e = grid_build(a.g, pos, nullptr, nullptr, hn, cap, s);
+        if (e != cudaSuccess) return e;
+    }
     a.queue = im.queue2;
     a.queue_n = im.ctr + kImgCtrHashQ;
     a.work = im.ctr + kImgCtrWork;
@@ -1075,6 +1120,8 @@ cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *po
     if (e != cudaSuccess) return e;
     e = launch_epilogue<K>(a, cap, s);
     if (e != cudaSuccess) return e;
+    ktimer_mark(KT_TAIL, true, s);
+    ktimer_mark(KT_COVS, true, s);
     note_launch(8);
     return cudaSuccess;
 }
@@ -1084,7 +1131,7 @@ cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s) {
     // a resident grid (one wave) pulling work batches; never more warps than batches
     const long long warps = (cap + kQueriesPerWarp - 1) / kQueriesPerWarp;
     const long long blocks = std::min<long long>(blocks_for(warps * 32, kKnnThreads), (long long)num_sms() * kKnnMinBlocks);
-    k_knn_search<K><<<(unsigned)std::max<long long>(blocks, 1), kKnnThreads, 0, s>>>(a);
+    launch_pdl(k_knn_search<K>, dim3((unsigned)std::max<long long>(blocks, 1)), dim3(kKnnThreads), 0, s, a);
     GSICP_LAUNCH_CHECK("k_knn_search");
     return cudaSuccess;
 }
@@ -1092,7 +1139,7 @@ cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s) {
 template <int K>
 cudaError_t launch_epilogue(const KnnArgs &a, int cap, cudaStream_t s) {
     const long long blocks = std::min<long long>(blocks_for(cap, kKnnThreads), (long long)num_sms() * 16);
-    k_knn_epilogue<K><<<(unsigned)std::max<long long>(blocks, 1), kKnnThreads, 0, s>>>(a);
+    launch_pdl(k_knn_epilogue<K>, dim3((unsigned)std::max<long long>(blocks, 1)), dim3(kKnnThreads), 0, s, a);
     GSICP_LAUNCH_CHECK("k_knn_epilogue");
     return cudaSuccess;
 }
@@ -1169,7 +1216,8 @@ size_t covariances_image_ws_bytes(int cap, int levels, int H, int W, int stride)
 
 cudaError_t covariances_image_launch(const float *pos, const int32_t *d_n, int cap, int H, int W, int stride,
                                      gsicp_intrinsics Kin, int k, int mode, float eps, float cell0, int levels,
-                                     float *cov_a, float *cov_b, int32_t *knn_idx, void *ws, cudaStream_t s) {
+                                     float *cov_a, float *cov_b, int32_t *knn_idx, const int32_t *lattice_map,
+                                     void *ws, cudaStream_t s) {
     KnnArgs a{};
     a.g = grid_carve(ws, cap, levels, false, cell0);
     a.pos = reinterpret_cast<const float4 *>(pos);
@@ -1192,7 +1240,8 @@ cudaError_t covariances_image_launch(const float *pos, const int32_t *d_n, int c
     im.Ws = (W + stride - 1) / stride;
     im.fx = Kin.fx;
     im.fy = Kin.fy;
-    im.map = reinterpret_cast<int32_t *>(p);
+    im.map = lattice_map ? const_cast<int32_t *>(lattice_map) : reinterpret_cast<int32_t *>(p);
+    im.map_given = lattice_map != nullptr;
     p += align_up((size_t)im.Hs * im.Ws * sizeof(int32_t));
     im.queue = reinterpret_cast<uint32_t *>(p);
     p += align_up((size_t)cap * sizeof(uint32_t));

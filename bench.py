@@ -298,6 +298,28 @@ def bench_gpu(args):
     e2e_total = max_over_ranks(sum(e2e_ms), dist, dev)
     e2e_value = job_throughput(nev, ws, e2e_total)
 
+    # C5: sequence tracking — each rank its own synthetic 30 Hz sequence (scene 100+rank), frames
+    # 1..n tracked in order with the constant-velocity initial pose computed on the device, one
+    # graph replay per frame (no host round trip), L2 flushed between frames; ATE vs the
+    # generating trajectory.  Whole-job aligns/s = frames of all ranks / max-over-ranks time.
+    seq_line = None
+    if args.seq_frames > 0:
+        import synth
+
+        sq = synth.make_sequence(rank, args.seq_frames + 1, "replica", M=1_000_000)
+        rows_all = synth.render_sequence_rows(sq, dev)
+        tgt_s = g.build_target(torch.from_numpy(sq.means).to(dev), torch.from_numpy(sq.quats).to(dev),
+                               torch.from_numpy(sq.scales).to(dev))
+        Ks = sq.K
+        tr_s = g.Tracker(Ks.H, Ks.W, (Ks.fx, Ks.fy, Ks.cx, Ks.cy), stride=sq.stride, params=params, device=dev)
+        T_est, ms_s = g.track_sequence(tr_s, tgt_s, rows_all, sq.T_gt[0], flush=flush)
+        seq_total = max_over_ranks(float(ms_s.sum()), dist, dev)
+        seq_line = {"workload": f"C5: {args.seq_frames}-frame Replica-shaped 30 Hz sequence per rank "
+                                "(Lissajous path, 1e6-Gaussian map of its room), constant-velocity init",
+                    "frames_per_rank": args.seq_frames, "aligns_per_s": job_throughput(args.seq_frames, ws, seq_total),
+                    "ms_per_frame_mean": float(ms_s.mean()), **synth.trajectory_error(T_est, sq.T_gt[1:])}
+        del rows_all, tr_s, tgt_s
+
     # kNN-cov Mpts/s over a 4e6-point map (C4), kernel stage only
     knn_mpts = None
     if not args.no_c4 and rank == 0:
@@ -370,6 +392,8 @@ def bench_gpu(args):
         "clocks": clk.summary(),
         "fitness": st["fitness"], "status": st["status"],
     }
+    if seq_line is not None:
+        line["sequence"] = seq_line
     if knn_mpts is not None:
         line["knn_cov_mpts_s"] = knn_mpts
         line["knn_cov_4M_ms"] = knn4_ms
@@ -389,6 +413,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--seq-frames", type=int, default=120, help="C5 sequence frames per rank (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

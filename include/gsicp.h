@@ -269,6 +269,18 @@ void gsicp_debug_align_counters(int32_t *d_out);
 void gsicp_debug_kernel_timer(int enable);
 int gsicp_debug_kernel_time(int kernel, float *ms);
 
+/* ---------------------------------------------------------------------------------------
+ * Sequence tracking (C5): the initial pose of frame t is the constant-velocity extrapolation
+ * T_{t-1} (T_{t-2}^-1 T_{t-1}) (binary64; the rotation re-orthonormalised), computed on
+ * the device so that a whole sequence runs without host round trips.
+ *  gsicp_pose_predict: d_hist [dev] double[32] = (T_{t-2}, T_{t-1}) row-major 4x4; writes d_T_out.
+ *  gsicp_pose_push: d_hist <- (T_{t-1}, d_T); if d_traj [dev] double[traj_cap*16] and d_counter
+ *  [dev] int32 are given, d_traj[*d_counter] = d_T and ++*d_counter (while < traj_cap).
+ *  Errors: INVALID_ARGUMENT, CUDA. */
+gsicp_status gsicp_pose_predict(const double *d_hist, double *d_T_out, void *stream);
+gsicp_status gsicp_pose_push(double *d_hist, const double *d_T, double *d_traj, int32_t *d_counter, int32_t traj_cap,
+                             void *stream);
+
 /* CUDA-graph helpers for callers that capture a whole frame (host pointers; stream-ordered).
  * gsicp_graph_instantiate: instantiates a captured graph (cudaGraph_t) so that kernel nodes keep
  * their launch priorities (cudaGraphInstantiateFlagUseNodePriority): the frame's critical path

@@ -113,6 +113,10 @@ def lib():
         L.gsicp_debug_align_timeline.restype = None
         L.gsicp_debug_align_counters.argtypes = [P]
         L.gsicp_debug_align_counters.restype = None
+        L.gsicp_pose_predict.argtypes = [P, P, P]
+        L.gsicp_pose_push.argtypes = [P, P, P, P, i32, P]
+        for name in ("gsicp_pose_predict", "gsicp_pose_push"):
+            getattr(L, name).restype = i32
         L.gsicp_graph_instantiate.argtypes = [P, C.POINTER(C.c_void_p)]
         L.gsicp_graph_launch.argtypes = [P, P]
         L.gsicp_graph_destroy.argtypes = [P]
@@ -142,6 +146,7 @@ EXPORTED = [
     "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version", "gsicp_debug_knn_counters",
     "gsicp_debug_align_timeline", "gsicp_debug_align_counters", "gsicp_debug_kernel_timer",
     "gsicp_debug_kernel_time", "gsicp_graph_instantiate", "gsicp_graph_launch", "gsicp_graph_destroy",
+    "gsicp_pose_predict", "gsicp_pose_push",
 ]
 
 KT_KNN_SEARCH, KT_ALIGN, KT_SEED, KT_BP, KT_COVS, KT_WIDE, KT_TAIL = 0, 1, 2, 3, 4, 5, 6
@@ -488,6 +493,18 @@ def linearize(src: Cloud, tgt: Target, T, max_corr_dist: float = math.inf, corr_
     return dict(H=H, b=b, cost=cost.value, n=n.value)
 
 
+def pose_predict(hist: torch.Tensor, T_out: torch.Tensor, stream=None):
+    """T_out = constant-velocity extrapolation of hist = (T_{t-2}, T_{t-1}) (device, double[32])."""
+    _check(lib().gsicp_pose_predict(_ptr(hist), _ptr(T_out), _stream(stream)))
+
+
+def pose_push(hist: torch.Tensor, T: torch.Tensor, traj: torch.Tensor | None = None,
+              counter: torch.Tensor | None = None, stream=None):
+    """hist <- (T_{t-1}, T); traj[counter++] = T if given (device tensors)."""
+    cap = traj.shape[0] if traj is not None else 0
+    _check(lib().gsicp_pose_push(_ptr(hist), _ptr(T), _ptr(traj), _ptr(counter), cap, _stream(stream)))
+
+
 class FrameGraph:
     """A stream capture instantiated with per-node launch priorities (gsicp_graph_instantiate):
     the critical-path kernels run high, the side-stream work low.  Usage:
@@ -633,6 +650,64 @@ class Tracker:
         up = lambda s0: upload_sampled_rows(self.rows, depth_host, self.stride, s0)  # noqa: E731
         return self._run(key, None, tgt, init_T, stream, up)
 
+    def sequence_graph(self, tgt: Target, hist: torch.Tensor, traj: torch.Tensor, counter: torch.Tensor):
+        """A graph for sequence tracking (C5): pose_predict(hist) -> the frame from self.rows ->
+        pose_push(hist, traj).  Replay it once per frame after writing the frame's sampled rows
+        into self.rows; no host round trip between frames."""
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        fg = FrameGraph()
+
+        def frame():
+            pose_predict(hist, self.d_T, s)
+            self.step_async(None, tgt, s)
+            pose_push(hist, self.d_T, traj, counter, s)
+        with torch.cuda.stream(s):
+            h0, c0 = hist.clone(), counter.clone()
+            frame()  # one run outside the capture (lazy library state); state restored after
+            s.synchronize()
+            hist.copy_(h0)
+            counter.copy_(c0)
+            s.synchronize()
+        with fg.capture(s):
+            frame()
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        return fg
+
     def upload_bytes(self) -> int:
         """Bytes track_host() copies host -> device per frame (the sampled rows)."""
         return self.rows.numel() * 4
+
+
+def track_sequence(tr: Tracker, tgt: Target, frames_rows: torch.Tensor, T0, flush: torch.Tensor | None = None,
+                   warmup: int = 3):
+    """Sequence tracking (C5): frames_rows (n, ceil(H/s), W) — each frame's sampled depth rows on
+    the device; T0 — the pose of frame 0.  Frames 1..n-1 are tracked in order, each with the
+    constant-velocity initial pose computed on the device, one graph replay per frame and no host
+    round trip.  `flush` (optional device tensor) is zeroed between frames outside the timed
+    events (L2 flush).  Returns (T_est (n-1, 4, 4) numpy, per-frame device ms (n-1,) numpy)."""
+    dev = tr.device
+    n = frames_rows.shape[0]
+    T0t = torch.from_numpy(np.ascontiguousarray(T0, dtype=np.float64).reshape(-1)).to(dev)
+    hist = torch.cat([T0t, T0t])  # zero velocity before frame 1
+    traj = torch.zeros((max(n - 1, 1), 16), dtype=torch.float64, device=dev)
+    counter = torch.zeros(1, dtype=torch.int32, device=dev)
+    fg = tr.sequence_graph(tgt, hist, traj, counter)
+    stream = torch.cuda.current_stream(dev)
+    for i in range(1, 1 + min(warmup, n - 1)):  # warm-up, then restart from frame 1
+        tr.rows.copy_(frames_rows[i])
+        fg.replay(stream)
+    torch.cuda.synchronize()
+    hist.copy_(torch.cat([T0t, T0t]))
+    counter.zero_()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n - 1)]
+    for i in range(1, n):
+        if flush is not None:
+            flush.zero_()
+        ev[i - 1][0].record(stream)
+        tr.rows.copy_(frames_rows[i])
+        fg.replay(stream)
+        ev[i - 1][1].record(stream)
+    torch.cuda.synchronize()
+    ms = np.array([a.elapsed_time(b) for a, b in ev])
+    return traj[: n - 1].cpu().numpy().reshape(-1, 4, 4), ms

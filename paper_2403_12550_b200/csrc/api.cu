@@ -139,6 +139,81 @@ const char *gsicp_last_error(void) { return g_err; }
 void gsicp_debug_knn_counters(int32_t *d_out) { gsicp::g_knn_debug = d_out; }
 void gsicp_debug_align_counters(int32_t *d_out) { gsicp::g_align_debug = d_out; }
 
+// ---------------------------------------------------------------------------------------------
+// Sequence tracking helpers: constant-velocity initial pose and the pose history.
+namespace gsicp {
+namespace {
+// T_out = T1 (T0^-1 T1): the last relative motion applied once more (rigid 4x4, row-major)
+__global__ void k_pose_predict(const double *__restrict__ hist, double *__restrict__ T_out) {
+    const double *A = hist, *B = hist + 16;  // T_{t-2}, T_{t-1}
+    double Ai[12];  // inverse of A: [R^T | -R^T t]
+    for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) Ai[4 * r + c] = A[4 * c + r];
+        Ai[4 * r + 3] = -(A[r] * A[3] + A[4 + r] * A[7] + A[8 + r] * A[11]);
+    }
+    double D[12];  // A^-1 B
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 4; ++c)
+            D[4 * r + c] = Ai[4 * r] * B[c] + Ai[4 * r + 1] * B[4 + c] + Ai[4 * r + 2] * B[8 + c] + (c == 3 ? Ai[4 * r + 3] : 0.0);
+    double P[12];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 4; ++c)
+            P[4 * r + c] = B[4 * r] * D[c] + B[4 * r + 1] * D[4 + c] + B[4 * r + 2] * D[8 + c] + (c == 3 ? B[4 * r + 3] : 0.0);
+    // re-orthonormalise the rotation (Gram-Schmidt on the rows): the poses carry rounding-level
+    // departures from SO(3), which the transpose-inverse above would compound from frame to frame
+    double r0[3] = {P[0], P[1], P[2]}, r1[3] = {P[4], P[5], P[6]};
+    const double n0 = 1.0 / sqrt(r0[0] * r0[0] + r0[1] * r0[1] + r0[2] * r0[2]);
+    for (int k = 0; k < 3; ++k) r0[k] *= n0;
+    const double d01 = r0[0] * r1[0] + r0[1] * r1[1] + r0[2] * r1[2];
+    for (int k = 0; k < 3; ++k) r1[k] -= d01 * r0[k];
+    const double n1 = 1.0 / sqrt(r1[0] * r1[0] + r1[1] * r1[1] + r1[2] * r1[2]);
+    for (int k = 0; k < 3; ++k) r1[k] *= n1;
+    const double r2[3] = {r0[1] * r1[2] - r0[2] * r1[1], r0[2] * r1[0] - r0[0] * r1[2], r0[0] * r1[1] - r0[1] * r1[0]};
+    for (int k = 0; k < 3; ++k) {
+        T_out[k] = r0[k];
+        T_out[4 + k] = r1[k];
+        T_out[8 + k] = r2[k];
+    }
+    T_out[3] = P[3]; T_out[7] = P[7]; T_out[11] = P[11];
+    T_out[12] = 0.0; T_out[13] = 0.0; T_out[14] = 0.0; T_out[15] = 1.0;
+}
+// history <- (T_{t-1}, T_t); the trajectory (if any) records T_t at its running counter
+__global__ void k_pose_push(double *__restrict__ hist, const double *__restrict__ T, double *__restrict__ traj,
+                            int32_t *__restrict__ counter, int32_t cap) {
+    const int k = threadIdx.x;
+    if (k < 16) {
+        const double t = T[k];
+        hist[k] = hist[16 + k];
+        hist[16 + k] = t;
+        if (traj && counter) {
+            const int32_t c = *counter;
+            if (c < cap) traj[(size_t)c * 16 + k] = t;
+        }
+    }
+    __syncthreads();
+    if (k == 0 && counter) *counter += 1;
+}
+}  // namespace
+}  // namespace gsicp
+
+gsicp_status gsicp_pose_predict(const double *d_hist, double *d_T_out, void *stream) {
+    g_err[0] = 0;
+    if (!d_hist || !d_T_out) BAD("pose_predict: null pointer");
+    gsicp::k_pose_predict<<<1, 1, 0, (cudaStream_t)stream>>>(d_hist, d_T_out);
+    gsicp::note_launch();
+    return cuda_status(cudaGetLastError(), "pose_predict");
+}
+
+gsicp_status gsicp_pose_push(double *d_hist, const double *d_T, double *d_traj, int32_t *d_counter, int32_t traj_cap,
+                             void *stream) {
+    g_err[0] = 0;
+    if (!d_hist || !d_T) BAD("pose_push: null pointer");
+    if ((d_traj == nullptr) != (d_counter == nullptr)) BAD("pose_push: trajectory and counter go together");
+    gsicp::k_pose_push<<<1, 32, 0, (cudaStream_t)stream>>>(d_hist, d_T, d_traj, d_counter, traj_cap);
+    gsicp::note_launch();
+    return cuda_status(cudaGetLastError(), "pose_push");
+}
+
 gsicp_status gsicp_graph_instantiate(void *graph, void **exec_out) {
     g_err[0] = 0;
     if (!graph || !exec_out) BAD("graph_instantiate: null pointer");

@@ -20,7 +20,8 @@ import numpy as np
 __all__ = [
     "Intrinsics", "REPLICA", "TUM", "TINY", "Scene", "make_scene", "raycast_depth",
     "tum_noise", "sample_map", "camera_pose", "perturb_pose", "rot_axis_angle",
-    "make_frame_workload", "make_c1", "quat_from_rotmat",
+    "make_frame_workload", "make_c1", "quat_from_rotmat", "raycast_depth_torch", "lissajous_trajectory",
+    "make_sequence", "Sequence", "render_sequence_rows", "trajectory_error",
 ]
 
 
@@ -391,3 +392,149 @@ def make_c1(cfg: int = 1) -> C1Workload:
     Tg[:3, :3] = rot_axis_angle(rng.standard_normal(3), math.radians(8.0))
     Tg[:3, 3] = [0.05, -0.08, 0.03]
     return C1Workload(TINY, depth, Tg)
+
+
+# ------------------------------------------------------------------------------------------ C5
+def raycast_depth_torch(scene: Scene, K: Intrinsics, T_wc, device="cuda"):
+    """raycast_depth on the GPU (torch, binary64): the same analytic z-depth, for generating long
+    sequences (C5) quickly.  Returns a (H, W) float32 tensor on `device`."""
+    import torch
+
+    f64 = torch.float64
+    u, v = torch.meshgrid(torch.arange(K.W, dtype=f64, device=device), torch.arange(K.H, dtype=f64, device=device),
+                          indexing="xy")
+    dc = torch.stack([(u - K.cx) / K.fx, (v - K.cy) / K.fy, torch.ones_like(u)], dim=-1).reshape(-1, 3)
+    T = torch.as_tensor(np.asarray(T_wc), dtype=f64, device=device)
+    R, o = T[:3, :3], T[:3, 3]
+    d = dc @ R.T
+    inf = torch.tensor(float("inf"), dtype=f64, device=device)
+    room = torch.as_tensor(scene.room, dtype=f64, device=device)
+    inv = 1.0 / d
+    t1 = (0.0 - o[None, :]) * inv
+    t2 = (room[None, :] - o[None, :]) * inv
+    tfar = torch.max(t1, t2).min(dim=1).values
+    best = torch.where(tfar > 0, tfar, inf)
+    for b in scene.boxes:
+        Rz = torch.as_tensor(_rot_z(b[6]), dtype=f64, device=device)
+        c = torch.as_tensor(b[:3], dtype=f64, device=device)
+        h = torch.as_tensor(b[3:6], dtype=f64, device=device)
+        ol = Rz.T @ (o - c)
+        dl = d @ Rz
+        invl = 1.0 / dl
+        ta = (-h[None, :] - ol[None, :]) * invl
+        tb = (h[None, :] - ol[None, :]) * invl
+        tn = torch.min(ta, tb).max(dim=1).values
+        tf = torch.max(ta, tb).min(dim=1).values
+        hit = (tn <= tf) & (tn > 1e-6)
+        best = torch.where(hit & (tn < best), tn, best)
+    for s in scene.spheres:
+        oc = o - torch.as_tensor(s[:3], dtype=f64, device=device)
+        a = (d * d).sum(dim=1)
+        bq = d @ oc
+        c = oc @ oc - s[3] ** 2
+        disc = bq * bq - a * c
+        t = (-bq - torch.sqrt(torch.clamp(disc, min=0))) / a
+        hit = (disc >= 0) & (t > 1e-6)
+        best = torch.where(hit & (t < best), t, best)
+    for cy in scene.cylinders:
+        ox, oy = o[0] - cy[0], o[1] - cy[1]
+        a = d[:, 0] ** 2 + d[:, 1] ** 2
+        bq = ox * d[:, 0] + oy * d[:, 1]
+        c = ox * ox + oy * oy - cy[2] ** 2
+        disc = bq * bq - a * c
+        t = (-bq - torch.sqrt(torch.clamp(disc, min=0))) / a
+        z = o[2] + t * d[:, 2]
+        hit = (disc >= 0) & (t > 1e-6) & (z >= cy[3]) & (z <= cy[3] + cy[4])
+        best = torch.where(hit & (t < best), t, best)
+        tc = (cy[3] + cy[4] - o[2]) / d[:, 2]
+        px, py = ox + tc * d[:, 0], oy + tc * d[:, 1]
+        hit = (tc > 1e-6) & (px * px + py * py <= cy[2] ** 2)
+        best = torch.where(hit & (tc < best), tc, best)
+    depth = torch.where(torch.isfinite(best), best, torch.zeros_like(best)).reshape(K.H, K.W)
+    return depth.to(torch.float32)
+
+
+@dataclasses.dataclass
+class Sequence:
+    K: Intrinsics
+    scene: Scene
+    T_gt: np.ndarray        # (n, 4, 4) camera -> world at 30 Hz
+    means: np.ndarray       # the map of the room
+    quats: np.ndarray
+    scales: np.ndarray
+    ell: float
+    stride: int
+
+
+def lissajous_trajectory(scene: Scene, seed: int, n: int, fps: float = 30.0, vmax: float = 0.5,
+                         wmax_deg: float = 30.0) -> np.ndarray:
+    """Camera poses (n, 4, 4) along a Lissajous path inside the room's free space (>= 0.5 m from
+    walls and objects), looking at a slowly moving point on the walls; speed <= vmax m/s, view
+    rotation <= wmax_deg deg/s.  Parameters are redrawn until both hold."""
+    rng = np.random.default_rng(seed)
+    L = scene.room
+    ts = np.arange(n) / fps
+    for _attempt in range(1000):
+        c = np.array([rng.uniform(0.35, 0.65) * L[0], rng.uniform(0.35, 0.65) * L[1], min(1.5, L[2] / 2)])
+        A = np.array([0.25 * L[0], 0.25 * L[1], 0.15 * L[2]]) * rng.uniform(0.3, 1.0, 3)
+        w = rng.uniform(0.1, 0.3, 3) * 2 * np.pi / 10.0  # rad/s (periods of tens of seconds)
+        ph = rng.uniform(0, 2 * np.pi, 3)
+        w = w * min(1.0, vmax / max(np.linalg.norm(A * w), 1e-9))  # |p'| <= |A w| <= vmax
+        P = c[None, :] + A[None, :] * np.sin(w[None, :] * ts[:, None] + ph[None, :])
+        if min(_clearance(scene, p) for p in P) < 0.5:
+            continue
+        look_c = np.array([L[0] / 2, L[1] / 2, L[2] / 2])
+        look_A = np.array([0.45 * L[0], 0.45 * L[1], 0.2 * L[2]])
+        look_w = rng.uniform(0.05, 0.15, 3) * 2 * np.pi / 10.0
+        look_ph = rng.uniform(0, 2 * np.pi, 3)
+        T = np.zeros((n, 4, 4))
+        for i in range(n):
+            tgt = look_c + look_A * np.sin(look_w * ts[i] + look_ph)
+            zc = _unit(tgt - P[i])
+            xc = _unit(np.cross(zc, np.array([0.0, 0.0, 1.0])))
+            yc = np.cross(zc, xc)
+            T[i] = np.eye(4)
+            T[i, :3, :3] = np.stack([xc, yc, zc], axis=1)
+            T[i, :3, 3] = P[i]
+        rate = 0.0
+        for i in range(1, n):
+            Rrel = T[i - 1, :3, :3].T @ T[i, :3, :3]
+            rate = max(rate, math.degrees(math.acos(max(-1.0, min(1.0, (np.trace(Rrel) - 1) / 2)))) * fps)
+        if rate <= wmax_deg:
+            return T
+    raise RuntimeError("no admissible Lissajous path found")
+
+
+def make_sequence(seq: int, n_frames: int, shape: str = "replica", M: int = 1_000_000, stride: int = 4) -> Sequence:
+    """C5: sequence `seq` (scene seed 100+seq) — a room, its M-Gaussian map and an n-frame 30 Hz
+    trajectory.  Frames are rendered on demand (raycast_depth_torch)."""
+    if shape == "replica":
+        K, room, nb, ns, nc = REPLICA, (6.0, 5.0, 3.0), 12, 6, 4
+    elif shape == "tum":
+        K, room, nb, ns, nc = TUM, (8.0, 8.0, 3.0), 16, 6, 6
+    else:
+        raise ValueError(shape)
+    scene = make_scene(100 + seq, room, nb, ns, nc)
+    T = lissajous_trajectory(scene, 200 + seq, n_frames)
+    means, quats, scales, ell = sample_map(scene, M, 400 + seq)
+    return Sequence(K, scene, T, means, quats, scales, ell, stride)
+
+
+def render_sequence_rows(seq: Sequence, device="cuda"):
+    """All frames' sampled depth rows (n, ceil(H/s), W) float32 on `device` (GPU ray casting)."""
+    import torch
+
+    K, s = seq.K, seq.stride
+    rows = torch.empty((seq.T_gt.shape[0], (K.H + s - 1) // s, K.W), dtype=torch.float32, device=device)
+    for i in range(seq.T_gt.shape[0]):
+        rows[i] = raycast_depth_torch(seq.scene, K, seq.T_gt[i], device=device)[::s]
+    return rows
+
+
+def trajectory_error(T_est: np.ndarray, T_gt: np.ndarray) -> dict:
+    """Absolute trajectory error of camera poses (no alignment: both start from the frame-0 pose)."""
+    dt = np.linalg.norm(T_est[:, :3, 3] - T_gt[:, :3, 3], axis=1)
+    ang = [math.degrees(math.acos(max(-1.0, min(1.0, (np.trace(A[:3, :3].T @ B[:3, :3]) - 1) / 2))))
+           for A, B in zip(T_est, T_gt)]
+    return {"ate_rmse_m": float(np.sqrt(np.mean(dt ** 2))), "trans_max_m": float(dt.max()),
+            "rot_max_deg": float(max(ang))}

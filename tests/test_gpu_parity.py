@@ -452,6 +452,15 @@ def test_tracker_host_frames_and_sampled_rows(g, replica, tum):
         n = int(n_full.item())
         assert n == int(n_part.item())
         assert torch.equal(full[:n], part[:n])
+        # the lattice map written by A1: output index of every sampled pixel, -1 where invalid
+        for src, rs in ((t(w.depth), False), (rows, True)):
+            pos_l, n_l, lat = g.backproject_lattice(src, H, W, K, stride=s, rows_sampled=rs)
+            assert torch.equal(pos_l[:n], full[:n])
+            Ws = (W + s - 1) // s
+            pix = full[:n, 3].cpu().numpy().view(np.int32)
+            expect = np.full(lat.shape[0], -1, np.int32)
+            expect[(pix // W) // s * Ws + (pix % W) // s] = np.arange(n, dtype=np.int32)
+            np.testing.assert_array_equal(lat.cpu().numpy(), expect)
     w = replica
     tr = g.Tracker(w.K.H, w.K.W, (w.K.fx, w.K.fy, w.K.cx, w.K.cy), stride=4)
     tgt = g.build_target(t(w.means), t(w.quats), t(w.scales))
@@ -486,3 +495,27 @@ def test_tracker_graph_capture(g, replica):
         torch.cuda.synchronize()
         np.testing.assert_array_equal(tr.d_T.cpu().numpy().reshape(4, 4), T_ref)
         assert g.decode_stats(tr.d_stats)["iters"] == st_ref["iters"]
+
+
+# ----------------------------------------------------------------------------------------- C5
+def test_sequence_tracking(g):
+    """C5-style: a 30 Hz synthetic sequence tracked with the device-side constant-velocity init
+    (one graph replay per frame): every frame converges and the trajectory error stays small."""
+    seq = synth.make_sequence(0, 40, "replica", M=300_000)
+    rows = synth.render_sequence_rows(seq, DEV)
+    tgt = g.build_target(t(seq.means), t(seq.quats), t(seq.scales))
+    K = seq.K
+    tr = g.Tracker(K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=seq.stride,
+                   params=g.align_params(max_iters=30, max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6))
+    T_est, ms = g.track_sequence(tr, tgt, rows, seq.T_gt[0])
+    err = synth.trajectory_error(T_est, seq.T_gt[1:])
+    assert err["ate_rmse_m"] < 5e-3 and err["rot_max_deg"] < 0.5, err
+    assert g.decode_stats(tr.d_stats)["status"] in (g.OK, g.WARN_MAX_ITERS)
+    # the device-side prediction equals the constant-velocity formula on the host
+    hist = torch.from_numpy(np.concatenate([seq.T_gt[3].reshape(-1), seq.T_gt[4].reshape(-1)])).to(DEV)
+    out = torch.zeros(16, dtype=torch.float64, device=DEV)
+    g.pose_predict(hist, out)
+    A, B = seq.T_gt[3], seq.T_gt[4]
+    P = out.cpu().numpy().reshape(4, 4)
+    np.testing.assert_allclose(P, B @ np.linalg.inv(A) @ B, atol=1e-12)
+    np.testing.assert_allclose(P[:3, :3] @ P[:3, :3].T, np.eye(3), atol=1e-14)

@@ -135,3 +135,4 @@ def test_knn_low_support_pads():
     assert (idx[:, 7:] == -1).all() and (np.sort(idx[:, :7], 1) == np.arange(7)).all()
     out = oracle.covariances(P, k=20)
     assert (out["flags"] & oracle.FLAG_LOW_SUPPORT).all()
+

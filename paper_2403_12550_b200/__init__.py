@@ -569,18 +569,19 @@ class Tracker:
         self._backproject(depth, stream)
         self._covariances(stream)
 
-    def _backproject(self, depth, stream):
-        """A1 from `depth`, or from the sampled-row buffer `self.rows` when depth is None; also
-        writes the lattice map the image-window kNN uses."""
-        backproject_lattice(self.rows if depth is None else depth, self.H, self.W, self.K, self.stride, depth is None,
-                            self.z_min, self.z_max, self.cloud.pos, self.cloud.d_n, self.lattice, self.ws_bp, stream)
+    def _backproject(self, depth, stream, rows=None):
+        """A1 from `depth`, or from a sampled-row buffer (`rows`, default self.rows) when depth is
+        None; also writes the lattice map the image-window kNN uses."""
+        src = depth if depth is not None else (rows if rows is not None else self.rows)
+        backproject_lattice(src, self.H, self.W, self.K, self.stride, depth is None, self.z_min, self.z_max,
+                            self.cloud.pos, self.cloud.d_n, self.lattice, self.ws_bp, stream)
 
     def _covariances(self, stream):
         covariances_image(self.cloud.pos, self.cloud.d_n, self.H, self.W, self.stride, self.K, self.k, self.mode,
                           self.eps, self.cell0, self.levels, self.cloud.cov_a, self.cloud.cov_b, None, self.ws_cov,
                           stream, self.lattice)
 
-    def step_async(self, depth: torch.Tensor | None, tgt: Target, stream=None, events=None):
+    def step_async(self, depth: torch.Tensor | None, tgt: Target, stream=None, events=None, rows=None):
         """Whole frame, device-resident pose in self.d_T (set it before), no host sync.
         A1 on `stream` (from `depth`, or from the sampled-row buffer `self.rows` when depth is
         None); then the iteration-0 correspondences (gsicp_align_seed) on a side stream
@@ -589,7 +590,7 @@ class Tracker:
         s0 = stream if stream is not None else torch.cuda.current_stream(self.device)
         if events:
             events[0].record(s0)
-        self._backproject(depth, s0)
+        self._backproject(depth, s0, rows)
         if events:
             events[1].record(s0)
         seed = os.environ.get("GSICP_NO_SEED", "0") != "1"  # (A/B diagnostic switch)
@@ -607,19 +608,19 @@ class Tracker:
         if events:
             events[3].record(s0)
 
-    def _graph(self, key, depth, tgt):
+    def _graph(self, key, depth, tgt, rows=None):
         """The whole frame (step_async) captured once per (input, target), replayed after."""
         hit = self._graphs.get(key)
         if hit is not None:
             return hit[0]
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
-        self.step_async(depth, tgt, s)  # one run outside the capture (lazy library state)
+        self.step_async(depth, tgt, s, rows=rows)  # one run outside the capture (lazy library state)
         s.synchronize()
         g = FrameGraph()
         with g.capture(s):
-            self.step_async(depth, tgt, s)
-        self._graphs[key] = (g, depth, tgt)  # keep the captured buffers alive
+            self.step_async(depth, tgt, s, rows=rows)
+        self._graphs[key] = (g, depth, tgt, rows)  # keep the captured buffers alive
         return g
 
     def _run(self, key, depth, tgt, init_T, stream, upload=None):
@@ -673,6 +674,47 @@ class Tracker:
             frame()
         torch.cuda.current_stream(self.device).wait_stream(s)
         return fg
+
+    def track_host_stream(self, frames, tgt: Target, init_T, stream=None):
+        """Track a stream of host depth frames (each pinned (H, W) float32; init_T: one pose for all
+        frames, or one per frame).  The sampled-row upload of frame t+1 runs on a copy stream
+        into the other of two row buffers while frame t computes; each frame's pose and stats are
+        read back asynchronously.  Returns [(T, stats)] in order (blocks once, at the end)."""
+        s0 = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_rows2"):
+            self._rows2 = [self.rows, torch.empty_like(self.rows)]
+            self._cp = torch.cuda.Stream(self.device)
+            self._ev_up = [torch.cuda.Event(), torch.cuda.Event()]
+            self._ev_done = [torch.cuda.Event(), torch.cuda.Event()]
+        graphs = [self._graph(("rows", id(tgt), b), None, tgt, self._rows2[b]) for b in range(2)]
+        n = len(frames)
+        inits = [init_T] * n if np.asarray(init_T).ndim == 2 else list(init_T)
+        T_host = torch.empty((n, 16), dtype=torch.float64).pin_memory()
+        T_out = torch.empty((n, 16), dtype=torch.float64).pin_memory()
+        st_out = torch.empty((n, C.sizeof(AlignStats)), dtype=torch.uint8).pin_memory()
+        for i in range(n):
+            T_host[i].numpy()[:] = np.ascontiguousarray(inits[i], dtype=np.float64).reshape(16)
+        for b in range(2):
+            self._ev_done[b].record(s0)
+        for i, fr in enumerate(frames):
+            b = i & 1
+            self._cp.wait_event(self._ev_done[b])  # buffer b's previous frame has finished
+            upload_sampled_rows(self._rows2[b], fr, self.stride, self._cp)
+            self._ev_up[b].record(self._cp)
+            s0.wait_event(self._ev_up[b])
+            with torch.cuda.stream(s0):
+                self.d_T.copy_(T_host[i], non_blocking=True)
+                graphs[b].replay(s0)
+                T_out[i].copy_(self.d_T, non_blocking=True)
+                st_out[i].copy_(self.d_stats, non_blocking=True)
+            self._ev_done[b].record(s0)
+        s0.synchronize()
+        out = []
+        for i in range(n):
+            stats = AlignStats.from_buffer_copy(st_out[i].numpy().tobytes()[:C.sizeof(AlignStats)]).as_dict()
+            _check(stats["status"], _ALIGN_ALLOW)
+            out.append((T_out[i].numpy().reshape(4, 4).copy(), stats))
+        return out
 
     def upload_bytes(self) -> int:
         """Bytes track_host() copies host -> device per frame (the sampled rows)."""

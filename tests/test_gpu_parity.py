@@ -471,6 +471,11 @@ def test_tracker_host_frames_and_sampled_rows(g, replica, tum):
         np.testing.assert_array_equal(T_host, T_dev)
         assert st_host["iters"] == st_dev["iters"] and st_host["fitness"] == st_dev["fitness"]
     assert tr.upload_bytes() == ((w.K.H + 3) // 4) * w.K.W * 4
+    # the streaming call (double-buffered uploads overlapping compute) returns the same poses
+    res = tr.track_host_stream([host] * 5, tgt, w.T_init)
+    for T_s, st_s in res:
+        np.testing.assert_array_equal(T_s, T_dev)
+        assert st_s["iters"] == st_dev["iters"]
 
 
 def test_tracker_graph_capture(g, replica):

@@ -170,13 +170,16 @@ gsicp_status gsicp_covariances(const float *pos, const int32_t *d_n, int32_t cap
  * the device and handled entirely by the hash search, so the result is exact for any input.
  *  lattice_map [dev] nullable: the map gsicp_backproject_lattice wrote for exactly these points
  *  (then it is used as is, not rebuilt or validated); NULL: built and validated here.
+ *  window_done_event nullable cudaEvent_t: recorded on `stream` right after the window kernel
+ *  (before the latency-bound wide-window / brute-force stages), so that independent work on
+ *  another stream can start there instead of competing with the window kernel for the SMs.
  *  Errors: INVALID_ARGUMENT. */
 size_t gsicp_covariances_image_workspace_size(int32_t cap, int32_t levels, int32_t H, int32_t W, int32_t stride);
 gsicp_status gsicp_covariances_image(const float *pos, const int32_t *d_n, int32_t cap, int32_t H, int32_t W,
                                      int32_t stride, gsicp_intrinsics K, int32_t k, gsicp_reg_mode mode,
                                      float eps_var, float cell0, int32_t levels, float *cov_a, float *cov_b,
                                      int32_t *knn_idx, const int32_t *lattice_map, void *ws, size_t ws_bytes,
-                                     void *stream);
+                                     void *stream, void *window_done_event);
 
 /* ---------------------------------------------------------------------------------------
  * A5  Map Gaussians -> G-ICP targets (the map's Gaussians are reused as

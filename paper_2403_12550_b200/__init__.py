@@ -89,7 +89,7 @@ def lib():
         L.gsicp_covariances_image_workspace_size.argtypes = [i32, i32, i32, i32, i32]
         L.gsicp_covariances_image_workspace_size.restype = sz
         L.gsicp_covariances_image.argtypes = [P, P, i32, i32, i32, i32, Intrinsics, i32, i32, f32, f32, i32, P, P, P,
-                                              P, P, sz, P]
+                                              P, P, sz, P, P]
         L.gsicp_build_target_workspace_size.argtypes = [i32]
         L.gsicp_build_target_workspace_size.restype = sz
         L.gsicp_build_target.argtypes = [P, P, P, i32, i32, i32, f32, f32, C.POINTER(_Target), P, sz, P]
@@ -358,7 +358,7 @@ def covariances(pos: torch.Tensor, d_n: torch.Tensor, k: int = 20, mode: int = R
 def covariances_image(pos: torch.Tensor, d_n: torch.Tensor, H: int, W: int, stride: int, K, k: int = 20,
                       mode: int = REG_ELLIPSE, eps_var: float = 1e-3, cell0: float = 0.01, levels: int = 1,
                       cov_a=None, cov_b=None, knn_idx: torch.Tensor | None = None, ws=None, stream=None,
-                      lattice: torch.Tensor | None = None):
+                      lattice: torch.Tensor | None = None, window_done: torch.cuda.Event | None = None):
     """A2-A4 for a depth-frame cloud from backproject_downsample(H, W, stride, K): the
     image-window kNN (same result as covariances()).  `lattice`: the map backproject_lattice
     wrote for these points (else built here).  Returns a Cloud sharing `pos`."""
@@ -374,7 +374,8 @@ def covariances_image(pos: torch.Tensor, d_n: torch.Tensor, H: int, W: int, stri
     Kc = K if isinstance(K, Intrinsics) else Intrinsics(*K)
     _check(lib().gsicp_covariances_image(_ptr(pos), _ptr(d_n), cap, H, W, stride, Kc, k, mode, eps_var, cell0, levels,
                                          _ptr(cov_a), _ptr(cov_b), _ptr(knn_idx), _ptr(lattice), _ptr(ws), ws.numel(),
-                                         _stream(stream)))
+                                         _stream(stream),
+                                         C.c_void_p(window_done.cuda_event) if window_done is not None else None))
     return Cloud(pos, cov_a, cov_b, d_n)
 
 
@@ -560,6 +561,7 @@ class Tracker:
         self._side = torch.cuda.Stream(self.device)
         self._fork = torch.cuda.Event()
         self._join = torch.cuda.Event()
+        self._fork.record(torch.cuda.current_stream(self.device))  # creates the event (handle passed to C)
         self._graphs = {}
         self._T_host = torch.zeros(16, dtype=torch.float64).pin_memory()
         self._T_out = torch.zeros(16, dtype=torch.float64).pin_memory()
@@ -576,10 +578,10 @@ class Tracker:
         backproject_lattice(src, self.H, self.W, self.K, self.stride, depth is None, self.z_min, self.z_max,
                             self.cloud.pos, self.cloud.d_n, self.lattice, self.ws_bp, stream)
 
-    def _covariances(self, stream):
+    def _covariances(self, stream, window_done=None):
         covariances_image(self.cloud.pos, self.cloud.d_n, self.H, self.W, self.stride, self.K, self.k, self.mode,
                           self.eps, self.cell0, self.levels, self.cloud.cov_a, self.cloud.cov_b, None, self.ws_cov,
-                          stream, self.lattice)
+                          stream, self.lattice, window_done)
 
     def step_async(self, depth: torch.Tensor | None, tgt: Target, stream=None, events=None, rows=None):
         """Whole frame, device-resident pose in self.d_T (set it before), no host sync.
@@ -593,14 +595,18 @@ class Tracker:
         self._backproject(depth, s0, rows)
         if events:
             events[1].record(s0)
+        # the iteration-0 correspondences need only the points: on a side stream, forked right
+        # after A1 (measured: forking after the window kernel — the SM-heavy part of A2-A4 — speeds
+        # that kernel up but the ~55-80 us seed pass then ends after A2-A4 and delays A6-A9)
         seed = os.environ.get("GSICP_NO_SEED", "0") != "1"  # (A/B diagnostic switch)
-        if seed:
+        early = os.environ.get("GSICP_SEED_EARLY", "1") == "1"  # (A/B: 0 = fork after the window)
+        if seed and early:
             self._fork.record(s0)
+        self._covariances(s0, self._fork if seed and not early else None)
+        if seed:
             self._side.wait_event(self._fork)
             align_seed(self.cloud, tgt, self.d_T, self.params, self.ws_align, self._side)
             self._join.record(self._side)
-        self._covariances(s0)
-        if seed:
             s0.wait_event(self._join)
         if events:
             events[2].record(s0)

@@ -58,7 +58,7 @@ size_t covariances_image_ws_bytes(int cap, int levels, int H, int W, int stride)
 cudaError_t covariances_image_launch(const float *pos, const int32_t *d_n, int cap, int H, int W, int stride,
                                      gsicp_intrinsics K, int k, int mode, float eps, float cell0, int levels,
                                      float *cov_a, float *cov_b, int32_t *knn_idx, const int32_t *lattice_map,
-                                     void *ws, cudaStream_t s);
+                                     void *ws, cudaStream_t s, void *window_done);
 size_t target_ws_bytes(int M);
 cudaError_t build_target_launch(const float *means, const float *quats, const float *scales, int scales_are_log,
                                 int M, int mode, float eps, float cell, gsicp_target *out, void *ws,
@@ -343,7 +343,8 @@ size_t gsicp_covariances_image_workspace_size(int32_t cap, int32_t levels, int32
 gsicp_status gsicp_covariances_image(const float *pos, const int32_t *d_n, int32_t cap, int32_t H, int32_t W,
                                      int32_t stride, gsicp_intrinsics K, int32_t k, gsicp_reg_mode mode, float eps_var,
                                      float cell0, int32_t levels, float *cov_a, float *cov_b, int32_t *knn_idx,
-                                     const int32_t *lattice_map, void *ws, size_t ws_bytes, void *stream) {
+                                     const int32_t *lattice_map, void *ws, size_t ws_bytes, void *stream,
+                                     void *window_done_event) {
     g_err[0] = 0;
     if (!pos || !d_n || !cov_a || !cov_b) BAD("covariances_image: null pointer");
     if (!aligned16(pos) || !aligned16(cov_a) || !aligned16(cov_b)) BAD("covariances_image: arrays must be 16-byte aligned");
@@ -359,7 +360,8 @@ gsicp_status gsicp_covariances_image(const float *pos, const int32_t *d_n, int32
     gsicp_status st = check_ws(ws, ws_bytes, covariances_image_ws_bytes(cap, levels, H, W, stride));
     if (st != GSICP_OK) return st;
     return cuda_status(covariances_image_launch(pos, d_n, cap, H, W, stride, K, k, (int)mode, eps_var, cell0, levels,
-                                                cov_a, cov_b, knn_idx, lattice_map, ws, (cudaStream_t)stream),
+                                                cov_a, cov_b, knn_idx, lattice_map, ws, (cudaStream_t)stream,
+                                                window_done_event),
                        "covariances_image");
 }
 

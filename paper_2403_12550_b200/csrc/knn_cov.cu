@@ -1066,7 +1066,8 @@ bool img_side_grid() {
 }
 
 template <int K>
-cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *pos, const int32_t *d_n, cudaStream_t s) {
+cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *pos, const int32_t *d_n, cudaStream_t s,
+                         cudaEvent_t window_done) {
     SideStream *ss = nullptr;
     cudaError_t e = cudaSuccess;
     const bool side = img_side_grid();
@@ -1094,6 +1095,7 @@ cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *po
     e = launch_tile<K>(a, im, s);
     if (e != cudaSuccess) return e;
     ktimer_mark(KT_KNN_SEARCH, true, s);
+    if (window_done && (e = cudaEventRecord(window_done, s)) != cudaSuccess) return e;
     ktimer_mark(KT_WIDE, false, s);
     // wide window over the queue (a resident grid pulling queries)
     launch_pdl(k_knn_image_wide<K>, dim3((unsigned)num_sms() * 8), dim3(128), 0, s, a, im);
@@ -1217,7 +1219,7 @@ size_t covariances_image_ws_bytes(int cap, int levels, int H, int W, int stride)
 cudaError_t covariances_image_launch(const float *pos, const int32_t *d_n, int cap, int H, int W, int stride,
                                      gsicp_intrinsics Kin, int k, int mode, float eps, float cell0, int levels,
                                      float *cov_a, float *cov_b, int32_t *knn_idx, const int32_t *lattice_map,
-                                     void *ws, cudaStream_t s) {
+                                     void *ws, cudaStream_t s, void *window_done) {
     KnnArgs a{};
     a.g = grid_carve(ws, cap, levels, false, cell0);
     a.pos = reinterpret_cast<const float4 *>(pos);
@@ -1249,12 +1251,12 @@ cudaError_t covariances_image_launch(const float *pos, const int32_t *d_n, int c
     p += align_up((size_t)cap * sizeof(uint32_t));
     im.ctr = reinterpret_cast<uint32_t *>(p);
     const float4 *p4 = a.pos;
-    if (k <= 4) return launch_image<4>(a, im, cap, p4, d_n, s);
-    if (k <= 8) return launch_image<8>(a, im, cap, p4, d_n, s);
-    if (k <= 16) return launch_image<16>(a, im, cap, p4, d_n, s);
-    if (k <= 20) return launch_image<20>(a, im, cap, p4, d_n, s);
-    if (k <= 24) return launch_image<24>(a, im, cap, p4, d_n, s);
-    return launch_image<32>(a, im, cap, p4, d_n, s);
+    if (k <= 4) return launch_image<4>(a, im, cap, p4, d_n, s, (cudaEvent_t)window_done);
+    if (k <= 8) return launch_image<8>(a, im, cap, p4, d_n, s, (cudaEvent_t)window_done);
+    if (k <= 16) return launch_image<16>(a, im, cap, p4, d_n, s, (cudaEvent_t)window_done);
+    if (k <= 20) return launch_image<20>(a, im, cap, p4, d_n, s, (cudaEvent_t)window_done);
+    if (k <= 24) return launch_image<24>(a, im, cap, p4, d_n, s, (cudaEvent_t)window_done);
+    return launch_image<32>(a, im, cap, p4, d_n, s, (cudaEvent_t)window_done);
 }
 
 }  // namespace gsicp

@@ -1018,9 +1018,19 @@ cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s);
 template <int K>
 cudaError_t launch_epilogue(const KnnArgs &a, int cap, cudaStream_t s);
 
-template <int K>
-cudaError_t launch_tile(const KnnArgs &a, const ImgArgs &im, cudaStream_t s) {
-    constexpr int M = kImgM, SW = kImgTX + 2 * M, SH = kImgTY + 2 * M;
+int img_window() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("GSICP_IMG_M");
+        v = e ? atoi(e) : kImgM;
+        if (v < 4 || v > 6) v = kImgM;
+    }
+    return v;
+}
+
+template <int K, int M>
+cudaError_t launch_tile_m(const KnnArgs &a, const ImgArgs &im, cudaStream_t s) {
+    constexpr int SW = kImgTX + 2 * M, SH = kImgTY + 2 * M;
     const int smem = (int)(sizeof(float4) * SW * SH + sizeof(uint32_t) * (kImgBuckets / 2) * kImgThreads +
                            sizeof(unsigned long long) * kImgList * kImgThreads);
     static bool attr = false;
@@ -1032,6 +1042,13 @@ cudaError_t launch_tile(const KnnArgs &a, const ImgArgs &im, cudaStream_t s) {
     launch_pdl(k_knn_image<K, M>, grid, dim3(kImgThreads), (size_t)smem, s, a, im);
     GSICP_LAUNCH_CHECK("k_knn_image");
     return cudaSuccess;
+}
+
+// window half-width: kImgM, or GSICP_IMG_M = 4..6 (A/B)
+template <int K>
+cudaError_t launch_tile(const KnnArgs &a, const ImgArgs &im, cudaStream_t s) {
+    const int M = img_window();
+    return M == 4 ? launch_tile_m<K, 4>(a, im, s) : (M == 6 ? launch_tile_m<K, 6>(a, im, s) : launch_tile_m<K, 5>(a, im, s));
 }
 
 // side stream (per host thread) on which the fallback hash is built while the window kernels run;

@@ -116,7 +116,8 @@ def max_over_ranks(x: float, dist=None, device=None) -> float:
         return float(x)
     import torch
 
-    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    on_cpu = dist.get_backend() == "gloo"
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cpu" if on_cpu else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -157,15 +158,20 @@ def oracle_prepare(w):
     w._oracle_tree = oracle.KDTree(w.means)
 
 
-def cpu_baseline(w, frames=1):
+def cpu_baseline(w, min_seconds=10.0, max_frames=64):
+    """The oracle as it stands on the host cores: whole frames of the bench workload until about
+    min_seconds of CPU time (a bounded sample), aligns/s."""
     import oracle
 
+    oracle.set_threads(os.cpu_count() or 1)
     oracle_prepare(w)
-    secs = [run_oracle_frame(w)[0] for _ in range(frames)]
+    secs = []
+    while sum(secs) < min_seconds and len(secs) < max_frames:
+        secs.append(run_oracle_frame(w)[0])
     t = sum(secs)
-    return {"value": frames / t, "unit": "aligns/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{frames} Replica-shaped frame(s) of the bench workload (A1 + brute-force kNN-cov + GN with "
-                      f"kd-tree NN over the prebuilt 1e6-map index), {t:.1f} s"}
+    return {"value": len(secs) / t, "unit": "aligns/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{len(secs)} Replica-shaped frame(s) of the bench workload (A1 + brute-force kNN-cov + GN "
+                      f"with kd-tree NN over the prebuilt 1e6-map index), {t:.1f} s"}
 
 
 def bench_reference(args):
@@ -174,6 +180,7 @@ def bench_reference(args):
         return 0
     import oracle
 
+    oracle.set_threads(os.cpu_count() or 1)  # every host core (torchrun sets OMP_NUM_THREADS=1)
     w = make_workload(0)
     oracle_prepare(w)
     for _ in range(args.warmup):
@@ -199,13 +206,20 @@ def bench_gpu(args):
     import torch
 
     ws, rank, local = dist_env()
+    # BENCH_DIST_BACKEND=gloo (testing the multi-rank path on one GPU: every rank on device
+    # local % device_count, CPU reductions); the real multi-GPU run uses NCCL, one GPU per rank
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     import paper_2403_12550_b200 as g
 
     w = make_workload(rank)
@@ -400,7 +414,7 @@ def bench_gpu(args):
         line["knn_cov_mpts_s"] = knn_mpts
         line["knn_cov_4M_ms"] = knn4_ms
         line["knn_cov_hbm_frac"] = ALGO_BYTES_KNN * 4e6 / (knn4_ms / 1000) / 1e9 / hbm
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and ws == 1:  # rank 0 at N=1 only
         line["cpu_baseline"] = cpu_baseline(w)
     print(json.dumps(line), flush=True)
     if dist:

@@ -66,6 +66,8 @@ def lib():
         L.ora_align.argtypes = [P, P, i, P, P, i, i, P, P, i, f, d, d, i, P, P]
         L.ora_align.restype = i
         L.ora_num_threads.restype = i
+        L.ora_set_threads.argtypes = [i]
+        L.ora_set_threads.restype = None
         L.ora_scale_align.argtypes = [P, d, d, d, P]
         L.ora_scale_align.restype = i
         _lib = L
@@ -83,6 +85,10 @@ def _f32(a, shape_last=None):
 
 def num_threads() -> int:
     return lib().ora_num_threads()
+
+
+def set_threads(n: int) -> None:
+    lib().ora_set_threads(int(n))
 
 
 def backproject(depth, fx, fy, cx, cy, stride=1, zmin=0.1, zmax=10.0):

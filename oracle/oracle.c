@@ -680,6 +680,16 @@ int ora_num_threads(void) {
 #endif
 }
 
+/* thread count of the OpenMP loops (the bench's baseline uses every host core even under a
+ * launcher that sets OMP_NUM_THREADS=1) */
+void ora_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* O12  Scale aligning for map insertion (Lambda'' = Lambda' / z^p, p empirically
  * 1.5).  scales_out = c * scales_in / z^p (c: absolute factor, R21).  z <= 0 -> -1. */
 int ora_scale_align(const double *scales_in, double z, double p, double c, double *scales_out) {

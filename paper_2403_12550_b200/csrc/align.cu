@@ -537,8 +537,10 @@ __device__ __forceinline__ void so3_exp(const double *w, double *R) {
         A = 1.0;
         B = 0.5;
     } else {
-        A = sin(th) / th;
-        B = (1.0 - cos(th)) / th2;
+        double sn, cs;
+        sincos(th, &sn, &cs);  // one shared range reduction on the solve's serial path
+        A = sn / th;
+        B = (1.0 - cs) / th2;
     }
     const double K[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
     for (int r = 0; r < 3; ++r)

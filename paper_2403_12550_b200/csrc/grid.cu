@@ -8,6 +8,8 @@ namespace {
 
 __global__ void k_grid_init(CellEntry *table, uint32_t slots, uint32_t *counters, int32_t *bbox, uint32_t *mark,
                             const int32_t *__restrict__ d_n) {
+    pdl_wait();
+    pdl_launch_dependents();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (*d_n <= 0) {  // nothing to hash (e.g. an empty fallback queue): leave the table alone
         if (i < kGridCounters) counters[i] = 0;
@@ -31,6 +33,8 @@ __global__ void k_grid_init(CellEntry *table, uint32_t slots, uint32_t *counters
 }
 
 __global__ void k_grid_insert(GridView g, const float4 *__restrict__ pos, const int32_t *__restrict__ d_n) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int n = *d_n;
     if (n <= 0) return;  // nothing to hash (block-uniform)
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -88,6 +92,8 @@ constexpr int kAllocThreads = 256;
 constexpr int kAllocPerThread = 4;
 
 __global__ void __launch_bounds__(kAllocThreads) k_grid_alloc(GridView g, const int32_t *__restrict__ d_n) {
+    pdl_wait();
+    pdl_launch_dependents();
     __shared__ uint32_t s_tot[kMaxLevels], s_base[kMaxLevels];
     if (*d_n <= 0) return;
     const int lane = threadIdx.x & 31;
@@ -134,6 +140,8 @@ __global__ void __launch_bounds__(kAllocThreads) k_grid_alloc(GridView g, const 
 template <bool WITH_COV>
 __global__ void k_grid_scatter(GridView g, const float4 *__restrict__ pos, const float4 *__restrict__ cov_a,
                                const float4 *__restrict__ cov_b, const int32_t *__restrict__ d_n) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int n = *d_n;
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int level = (int)(t / g.cap);
@@ -193,16 +201,16 @@ cudaError_t grid_build(const GridView &g, const float4 *pos, const float4 *cov_a
     const int T = 256;
     const uint32_t slots = g.mask + 1;
     const long long work = (long long)g.levels * g.cap;
-    k_grid_init<<<blocks_for(slots, T), T, 0, s>>>(g.table, slots, g.counters, g.bbox, g.mark, d_n);
+    launch_pdl(k_grid_init, dim3(blocks_for(slots, T)), dim3(T), 0, s, g.table, slots, g.counters, g.bbox, g.mark, d_n);
     GSICP_LAUNCH_CHECK("k_grid_init");
-    k_grid_insert<<<blocks_for(work, T), T, 0, s>>>(g, pos, d_n);
+    launch_pdl(k_grid_insert, dim3(blocks_for(work, T)), dim3(T), 0, s, g, pos, d_n);
     GSICP_LAUNCH_CHECK("k_grid_insert");
-    k_grid_alloc<<<blocks_for(slots, kAllocThreads * kAllocPerThread), kAllocThreads, 0, s>>>(g, d_n);
+    launch_pdl(k_grid_alloc, dim3(blocks_for(slots, kAllocThreads * kAllocPerThread)), dim3(kAllocThreads), 0, s, g, d_n);
     GSICP_LAUNCH_CHECK("k_grid_alloc");
     if (g.scov_a)
-        k_grid_scatter<true><<<blocks_for(work, T), T, 0, s>>>(g, pos, cov_a, cov_b, d_n);
+        launch_pdl(k_grid_scatter<true>, dim3(blocks_for(work, T)), dim3(T), 0, s, g, pos, cov_a, cov_b, d_n);
     else
-        k_grid_scatter<false><<<blocks_for(work, T), T, 0, s>>>(g, pos, cov_a, cov_b, d_n);
+        launch_pdl(k_grid_scatter<false>, dim3(blocks_for(work, T)), dim3(T), 0, s, g, pos, cov_a, cov_b, d_n);
     GSICP_LAUNCH_CHECK("k_grid_scatter");
     note_launch(4);
     return cudaSuccess;

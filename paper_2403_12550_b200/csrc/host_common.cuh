@@ -53,13 +53,17 @@ inline unsigned blocks_for(long long n, int threads) { return (unsigned)((n + th
 // predecessor is still running and waits for it in-kernel (pdl_wait() at its top, before any
 // dependent read), which hides the launch latency between consecutive kernels of the frame
 // (CUDA-graph edges included).  GSICP_PDL=0 turns it off (A/B).
+inline bool &pdl_suspended() {  // set while capturing into a conditional-node body
+    static thread_local bool off = false;
+    return off;
+}
 inline bool pdl_enabled() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("GSICP_PDL");
         v = (e && e[0] == '0') ? 0 : 1;
     }
-    return v == 1;
+    return v == 1 && !pdl_suspended();
 }
 
 // Launch priorities: the frame's critical path (A1 -> A2-A4 -> A6-A9) runs high, the work

@@ -998,7 +998,8 @@ __global__ void __cluster_dims__(kBruteCluster, 1, 1) __launch_bounds__(kBruteTh
 
 // the hash path takes the last queue when it is longer than kBruteMax, else whatever brute force
 // handed over (moved to the front of queue 2)
-__global__ void k_img_hash_n(ImgArgs im, const int32_t *__restrict__ d_n) {
+__global__ void k_img_hash_n(ImgArgs im, const int32_t *__restrict__ d_n, cudaGraphConditionalHandle cond,
+                             int use_cond) {
     pdl_wait();
     pdl_launch_dependents();
     const uint32_t q2 = im.ctr[kImgCtrQueue2], q3 = im.ctr[kImgCtrQueue3];
@@ -1011,6 +1012,7 @@ __global__ void k_img_hash_n(ImgArgs im, const int32_t *__restrict__ d_n) {
     }
     im.ctr[kImgCtrHashN] = hq ? (uint32_t)*d_n : 0u;
     im.ctr[kImgCtrHashQ] = hq;
+    if (use_cond) cudaGraphSetConditional(cond, hq ? 1u : 0u);  // the graph runs the hash tail only if needed
 }
 
 template <int K>
@@ -1073,6 +1075,28 @@ static cudaError_t side_stream(SideStream *&out) {
     return cudaSuccess;
 }
 
+bool img_cond_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("GSICP_COND");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// stream used to capture conditional-node bodies (per host thread)
+cudaStream_t body_stream() {
+    static thread_local cudaStream_t bs = nullptr;
+    static thread_local int dev = -1;
+    int d = 0;
+    cudaGetDevice(&d);
+    if (!bs || dev != d) {
+        if (cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        dev = d;
+    }
+    return bs;
+}
+
 bool img_side_grid() {
     static int v = -1;
     if (v < 0) {
@@ -1121,24 +1145,71 @@ cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *po
     launch_pdl(k_knn_brute<K>, dim3((unsigned)(2 * (num_sms() / kBruteCluster) * kBruteCluster)), dim3(kBruteThreads), 0,
                s, a, im);
     GSICP_LAUNCH_CHECK("k_knn_brute");
-    launch_pdl(k_img_hash_n, dim3(1), dim3(1), 0, s, im, d_n);
-    GSICP_LAUNCH_CHECK("k_img_hash_n");
-    ktimer_mark(KT_WIDE, true, s);
-    ktimer_mark(KT_TAIL, false, s);
-    if (side) {
-        if ((e = cudaStreamWaitEvent(s, ss->join, 0)) != cudaSuccess) return e;
-    } else {  // inline, only for a non-empty hash queue (the build kernels return at once otherwise)
+    // the hash tail (hash the cloud, warp search, epilogue) only for a non-empty hash queue: inside
+    // a stream capture as the body of a conditional (IF) graph node whose condition k_img_hash_n
+    // sets on the device; otherwise launched directly, each kernel returning at once when idle
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cst);
+    if (cst == cudaStreamCaptureStatusActive && !side && img_cond_enabled()) {
+        cudaGraph_t graph = nullptr;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t nd = 0;
+        unsigned long long cid = 0;
+        if ((e = cudaStreamGetCaptureInfo(s, &cst, &cid, &graph, &deps, &nd)) != cudaSuccess) return e;
+        cudaGraphConditionalHandle h;
+        if ((e = cudaGraphConditionalHandleCreate(&h, graph, 0, 0)) != cudaSuccess) return e;
+        launch_pdl(k_img_hash_n, dim3(1), dim3(1), 0, s, im, d_n, h, 1);
+        GSICP_LAUNCH_CHECK("k_img_hash_n");
+        ktimer_mark(KT_WIDE, true, s);
+        ktimer_mark(KT_TAIL, false, s);
+        if ((e = cudaStreamGetCaptureInfo(s, &cst, &cid, &graph, &deps, &nd)) != cudaSuccess) return e;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeIf;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        if ((e = cudaGraphAddNode(&cnode, graph, deps, nd, &cp)) != cudaSuccess) return e;
+        cudaStream_t bs = body_stream();
+        if (!bs) return cudaErrorInvalidResourceHandle;
+        if ((e = cudaStreamBeginCaptureToGraph(bs, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+            return e;
+        pdl_suspended() = true;  // no programmatic edges inside the conditional body
         const int32_t *hn = reinterpret_cast<const int32_t *>(im.ctr + kImgCtrHashN);
-        e = grid_build(a.g, pos, nullptr, nullptr, hn, cap, s);
+        cudaError_t eb = grid_build(a.g, pos, nullptr, nullptr, hn, cap, bs);
+        a.queue = im.queue2;
+        a.queue_n = im.ctr + kImgCtrHashQ;
+        a.work = im.ctr + kImgCtrWork;
+        if (eb == cudaSuccess) eb = launch_search<K>(a, cap, bs);
+        if (eb == cudaSuccess) eb = launch_epilogue<K>(a, cap, bs);
+        pdl_suspended() = false;
+        cudaGraph_t body_out = nullptr;
+        e = cudaStreamEndCapture(bs, &body_out);
+        if (eb != cudaSuccess) return eb;
+        if (e != cudaSuccess) return e;
+        if ((e = cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
+            return e;
+    } else {
+        launch_pdl(k_img_hash_n, dim3(1), dim3(1), 0, s, im, d_n, cudaGraphConditionalHandle{}, 0);
+        GSICP_LAUNCH_CHECK("k_img_hash_n");
+        ktimer_mark(KT_WIDE, true, s);
+        ktimer_mark(KT_TAIL, false, s);
+        if (side) {
+            if ((e = cudaStreamWaitEvent(s, ss->join, 0)) != cudaSuccess) return e;
+        } else {  // inline, only for a non-empty hash queue (the build kernels return at once otherwise)
+            const int32_t *hn = reinterpret_cast<const int32_t *>(im.ctr + kImgCtrHashN);
+            e = grid_build(a.g, pos, nullptr, nullptr, hn, cap, s);
+            if (e != cudaSuccess) return e;
+        }
+        a.queue = im.queue2;
+        a.queue_n = im.ctr + kImgCtrHashQ;
+        a.work = im.ctr + kImgCtrWork;
+        e = launch_search<K>(a, cap, s);
+        if (e != cudaSuccess) return e;
+        e = launch_epilogue<K>(a, cap, s);
         if (e != cudaSuccess) return e;
     }
-    a.queue = im.queue2;
-    a.queue_n = im.ctr + kImgCtrHashQ;
-    a.work = im.ctr + kImgCtrWork;
-    e = launch_search<K>(a, cap, s);
-    if (e != cudaSuccess) return e;
-    e = launch_epilogue<K>(a, cap, s);
-    if (e != cudaSuccess) return e;
     ktimer_mark(KT_TAIL, true, s);
     ktimer_mark(KT_COVS, true, s);
     note_launch(8);

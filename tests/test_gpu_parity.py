@@ -222,6 +222,23 @@ def test_knn_cov_image_window_non_frame_cloud(g):
     d_n = torch.tensor([n], dtype=torch.int32, device=DEV)
     K = synth.make_c1(1).K
     _cov_check(g, xyz, pos, d_n, cell0=0.3, levels=3, image=(48, 64, 1, K))
+    # the same through a CUDA graph: the hash tail is then the body of a conditional node that
+    # the device switches on (every query needs the hash here); results identical to eager
+    Kt = (K.fx, K.fy, K.cx, K.cy)
+    ws = g._ws(g.lib().gsicp_covariances_image_workspace_size(n, 3, 48, 64, 1), DEV)
+    knn_e = torch.full((n, 20), -7, dtype=torch.int32, device=DEV)
+    ce = g.covariances_image(pos, d_n, 48, 64, 1, Kt, 20, cell0=0.3, levels=3, knn_idx=knn_e, ws=ws)
+    ca_e, cb_e = ce.cov_a.clone(), ce.cov_b.clone()
+    knn_g = torch.full((n, 20), -7, dtype=torch.int32, device=DEV)
+    ca_g, cb_g = torch.zeros_like(ca_e), torch.zeros_like(cb_e)
+    st = torch.cuda.Stream()
+    fg = g.FrameGraph()
+    with fg.capture(st):
+        g.covariances_image(pos, d_n, 48, 64, 1, Kt, 20, cell0=0.3, levels=3, cov_a=ca_g, cov_b=cb_g, knn_idx=knn_g,
+                            ws=ws, stream=st)
+    fg.replay(st)
+    st.synchronize()
+    assert torch.equal(knn_g, knn_e) and torch.equal(ca_g, ca_e) and torch.equal(cb_g, cb_e)
 
 
 def test_knn_cov_ragged_and_low_support(g):

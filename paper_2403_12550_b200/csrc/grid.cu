@@ -160,7 +160,10 @@ __global__ void k_grid_scatter(GridView g, const float4 *__restrict__ pos, const
 }  // namespace
 
 uint32_t grid_table_slots(int cap, int levels) {
-    uint64_t want = 2ull * (uint64_t)cap * (uint64_t)levels;
+    // >= 1.25 slots per (point, level): the load factor stays <= 80% even if every point sits in
+    // its own cell on every level (linear probing terminates), while real clouds (many points
+    // per cell) use a small, more cache-friendly table
+    uint64_t want = (5ull * (uint64_t)cap * (uint64_t)levels + 3) / 4;
     uint64_t s = 1024;
     while (s < want) s <<= 1;
     return (uint32_t)s;

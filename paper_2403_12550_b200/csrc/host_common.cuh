@@ -106,7 +106,12 @@ inline cudaError_t launch_low(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributePriority;
-    at[0].val.priority = launch_priority(false);
+    static int flip = -1;  // GSICP_SIDE_HIGH=1: side work at high priority too (A/B)
+    if (flip < 0) {
+        const char *e = getenv("GSICP_SIDE_HIGH");
+        flip = (e && e[0] == '1') ? 1 : 0;
+    }
+    at[0].val.priority = launch_priority(flip == 1);
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;

@@ -41,8 +41,7 @@ constexpr int kQueriesPerWarp = 8;  // queries a warp searches one after the oth
 constexpr int kKnnMinBlocks = 8;    // resident blocks per SM the register budget is sized for
 constexpr int kMergeThreshold = 4;  // more passing candidates than this: sort-merge the batch
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kKnnBatch = 4;
-constexpr int kMaxK = 32;  // hash probes in flight per thread (thread variant)
+constexpr int kMaxK = 32;  // neighbour-list stride of the warp search's nbr_t rows
 
 struct KnnArgs {
     GridView g;
@@ -442,7 +441,7 @@ constexpr int kImgBucketRef = 16;  // bucket of key = (2 * spacing)^2
 constexpr float kImgFar = 1e30f;   // empty lattice pixel: keys overflow to +inf
 // image counters (zeroed by k_img_map_clear): window queue, warp-search work, map conflict flag,
 // hash queue (what the wide window could not certify), wide-pass work, hash point count
-constexpr int kImgCtrQueue = 0, kImgCtrWork = 1, kImgCtrBad = 2, kImgCtrQueue2 = 3, kImgCtrWideWork = 4,
+constexpr int kImgCtrQueue = 0, kImgCtrWork = 1, kImgCtrBad = 2, kImgCtrQueue2 = 3,
               kImgCtrHashN = 5, kImgCtrHashQ = 6, kImgCtrQueue3 = 7, kImgCounters = 8;
 constexpr uint32_t kBruteMax = 256;  // a last queue up to this size is searched by brute force
 constexpr int kImgWideM = 12;  // half-width of the wide window (warp per query)
@@ -871,7 +870,6 @@ __global__ void __cluster_dims__(kBruteCluster, 1, 1) __launch_bounds__(kBruteTh
     pdl_wait();
     pdl_launch_dependents();
     __shared__ uint32_t bins[1024], gbins[1024];
-    __shared__ uint32_t wsum[32];
     __shared__ unsigned long long lst[64];
     __shared__ int s_nl, s_nb, s_bin;
     __shared__ uint32_t s_below, s_m;

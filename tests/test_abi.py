@@ -87,3 +87,28 @@ def test_product_has_no_oracle_or_cpu_fallback():
                 txt = open(os.path.join(root, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "liboracle" not in txt, f
+
+
+def test_new_entry_points_reject_bad_arguments(g):
+    """Argument validation of the image-window / sampled-row / sequence / graph entry points."""
+    L = g.lib()
+    K = g.Intrinsics(600.0, 600.0, 599.5, 339.5)
+    fake = C.c_void_p(0x100000)
+    assert L.gsicp_covariances_image_workspace_size(51000, 4, 680, 1200, 4) > L.gsicp_covariances_workspace_size(51000, 4)
+    assert L.gsicp_covariances_image_workspace_size(51000, 4, 0, 1200, 4) == 0
+    st = L.gsicp_covariances_image(None, fake, 100, 680, 1200, 4, K, 20, g.REG_ELLIPSE, 1e-3, 0.02, 4, fake, fake,
+                                   None, None, fake, 1 << 30, None, None)
+    assert st == g.ERR_INVALID_ARGUMENT
+    st = L.gsicp_covariances_image(fake, fake, 100, 680, 1200, 4, K, 33, g.REG_ELLIPSE, 1e-3, 0.02, 4, fake, fake,
+                                   None, None, fake, 1 << 30, None, None)
+    assert st == g.ERR_INVALID_ARGUMENT and b"k must be" in L.gsicp_last_error()
+    st = L.gsicp_backproject_lattice(fake, 2, 680, 1200, 1200, K, 4, 0.1, 10.0, fake, 51000, fake, fake, fake, 1 << 20,
+                                     None)
+    assert st == g.ERR_INVALID_ARGUMENT  # rows_sampled must be 0 or 1
+    st = L.gsicp_upload_sampled_rows(None, fake, 680, 1200, 1200, 4, None)
+    assert st == g.ERR_INVALID_ARGUMENT
+    st = L.gsicp_pose_push(fake, fake, fake, None, 4, None)
+    assert st == g.ERR_INVALID_ARGUMENT  # trajectory without a counter
+    assert L.gsicp_pose_predict(None, fake, None) == g.ERR_INVALID_ARGUMENT
+    assert L.gsicp_graph_launch(None, None) == g.ERR_INVALID_ARGUMENT
+    assert L.gsicp_graph_destroy(None) == g.OK

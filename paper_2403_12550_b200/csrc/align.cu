@@ -1254,7 +1254,13 @@ cudaError_t align_seed_launch(const gsicp_cloud &src, const gsicp_target &tgt, c
     ktimer_mark(KT_SEED, false, s);
     launch_low(k_align_seed, dim3(blocks_for(src.cap > 0 ? src.cap : 1, kSeedT)), dim3(kSeedT), 0, s, a);
     GSICP_LAUNCH_CHECK("k_align_seed");
-    launch_low(k_align_seed_hard, dim3(num_sms() * 8), dim3(kSeedHardT), 0, s, a);
+    static int per_sm = -1;  // GSICP_SEED_HARD_PER_SM (A/B): resident blocks per SM of the hard pass
+    if (per_sm < 0) {
+        const char *e = getenv("GSICP_SEED_HARD_PER_SM");
+        per_sm = e ? atoi(e) : 8;
+        if (per_sm < 1) per_sm = 8;
+    }
+    launch_low(k_align_seed_hard, dim3(num_sms() * per_sm), dim3(kSeedHardT), 0, s, a);
     GSICP_LAUNCH_CHECK("k_align_seed_hard");
     ktimer_mark(KT_SEED, true, s);
     note_launch(2);

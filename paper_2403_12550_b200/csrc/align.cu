@@ -803,8 +803,13 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     if (tid == 0) sDone = 0;
     if (tid == 0) sQn = 0;
     // resident point of this thread: source data, current match and own target cell in registers
-    const int i0 = blockIdx.x * kT + tid;
-    const bool has0 = i0 < n;
+    // resident points: block b owns the contiguous chunk [b P, b P + P), P = ceil(n / G) (at most
+    // kT): the whole co-resident grid shares the points — and the hard queries each block's warps
+    // search — however small the frame is (one block per kT points left most SMs idle and piled
+    // the warp searches of a noisy frame onto a few blocks)
+    const int P = min(kT, (n + G - 1) / G);
+    const int i0 = P == kT ? blockIdx.x * kT + tid : blockIdx.x * P + tid;
+    const bool has0 = tid < P && i0 < n;
     float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), ca0 = x0, cb0 = x0;
     if (has0) {
         x0 = __ldg(a.spos + i0);
@@ -1123,6 +1128,8 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
 }
 
 // Co-resident grid for the cooperative launch (0 if the kernel cannot be resident at all).
+constexpr int kMaxAlignGrid = 2048;  // partial records reserved in the workspace (>= SMs x blocks/SM)
+
 int align_grid_blocks(int cap, int *per_sm_out) {
     static int per_sm = -1;
     if (per_sm < 0) {
@@ -1131,9 +1138,9 @@ int align_grid_blocks(int cap, int *per_sm_out) {
         per_sm = v;
     }
     *per_sm_out = per_sm;
-    const int need = (int)blocks_for(cap > 0 ? cap : 1, kT);
-    const int maxb = per_sm * num_sms();
-    return need < maxb ? need : maxb;
+    (void)cap;
+    const int g = per_sm * num_sms();  // the full co-resident grid; k_align splits the points over it
+    return g < kMaxAlignGrid ? g : kMaxAlignGrid;
 }
 
 }  // namespace
@@ -1157,8 +1164,8 @@ static AlignWs align_carve(Carver &c, int cap) {
     w.d_stats = c.take<gsicp_align_stats>(1);
     w.d_lin = c.take<double>(48);
     w.barrier = c.take<unsigned int>(4);
-    const int G = (int)blocks_for(cap > 0 ? cap : 1, kT);
-    w.partials = c.take<double>((size_t)2 * G * kPad);
+    (void)cap;
+    w.partials = c.take<double>((size_t)2 * kMaxAlignGrid * kPad);  // the grid is the co-resident one
     w.corr_ws = c.take<int32_t>(cap);
     w.seed_slot = c.take<int32_t>(cap);
     w.seed_hdr = c.take<double>(16);

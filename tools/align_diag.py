@@ -13,16 +13,17 @@ import synth
 
 
 def main():
-    w = synth.make_frame_workload(2, "replica", M=1_000_000, stride=4)
+    shape = sys.argv[1] if len(sys.argv) > 1 else "replica"
+    stride = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    w = (synth.make_frame_workload(2, "replica", M=1_000_000, stride=stride) if shape == "replica"
+         else synth.make_frame_workload(3, "tum", M=1_000_000, stride=stride, noisy=True))
     K = w.K
     dev = torch.device("cuda")
-    tr = g.Tracker(K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=4, device=dev)
+    tr = g.Tracker(K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=stride, device=dev)
     depth = torch.from_numpy(w.depth).to(dev)
     tr.preprocess(depth)
     means, quats, scales = (torch.from_numpy(x).to(dev) for x in (w.means, w.quats, w.scales))
     tl = torch.zeros(1 << 16, dtype=torch.int64, device=dev)
-    w5 = synth.make_frame_workload(2, "replica", M=100_000, stride=4)
-    small = tuple(torch.from_numpy(x).to(dev) for x in (w5.means, w5.quats, w5.scales))
     cases = [("1e6", means, quats, scales, 0.0)]
     seeded = os.environ.get("SEEDED", "1") == "1"
     for name, mm, qq, ss, cell in cases:

@@ -37,12 +37,13 @@ def main():
         g.debug_align_counters(None)
         c = cnt[:tr.cloud.n()].cpu().numpy().astype(np.int64) & 0xffffffff
         n_it = int(c[:, 3].max())
-        Gb = int(np.ceil(c.shape[0] / 384))
+        Gb = torch.cuda.get_device_properties(0).multi_processor_count
         for it in range(n_it):
             bit = 1 << it
             q, r, gr = ((c[:, k] & bit) != 0 for k in range(3))
             fast = ~(q | r | gr)
-            pb = lambda m: np.bincount(np.arange(len(m))[m] // 384, minlength=Gb)
+            P = -(-c.shape[0] // Gb)  # k_align's chunk of points per block
+            pb = lambda m: np.bincount(np.arange(len(m))[m] // P, minlength=Gb)
             print(f"  it {it}: queued {q.mean():.4f} reuse {r.mean():.4f} graph {gr.mean():.4f} other {fast.mean():.4f} | "
                   f"per block max: queued {pb(q).max()} graph {pb(gr).max()} other {pb(fast).max()}")
         tl.zero_()
@@ -59,8 +60,7 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         t = tl.cpu().numpy()
-        Gn = int(np.ceil(tr.cap / 384))
-        Gn = min(Gn, 148)
+        Gn = torch.cuda.get_device_properties(0).multi_processor_count  # k_align: the full co-resident grid
         t0 = t[0]
         print(f"cell={tgt.cell * 100:.2f} cm  iters={st['iters']} total {ms * 1000:.1f} us (event)")
         prev = t0

@@ -403,8 +403,9 @@ def bench_gpu(args):
         "e2e": {"value": e2e_value, "unit": "aligns/s", "h2d_bytes_per_step": int(tr.upload_bytes() + 16 * 8),
                 "d2h_bytes_per_step": 16 * 8 + 32,
                 "path": "Tracker.track_host_stream: per frame H2D of the sampled depth rows (copy stream, double "
-                        "buffered) + pose, graph replay, D2H of pose + stats; wall clock over all frames"},
-        "gpu_launches": int(launches),
+                        "buffered) + pose, graph replay, D2H of pose + stats; wall clock over all frames",
+                "l2": "flushed once before the stream of frames (not between frames)"},
+        "gpu_launches": int(launches),  # captured per frame (conditional-body kernels excluded) x steps
         "clocks": clk.summary(),
         "fitness": st["fitness"], "status": st["status"],
     }

@@ -16,7 +16,11 @@ extern thread_local long long *g_align_timeline;  // align.cu
 extern thread_local long long g_align_timeline_cap;
 extern thread_local int32_t *g_align_debug;
 
-void note_launch(int n) { g_launches += (uint64_t)n; }
+// (launches captured into a conditional graph node's body are not counted: they run only when the
+// device switches the node on — the hash tail of the image-window kNN, which a frame rarely needs)
+void note_launch(int n) {
+    if (!pdl_suspended()) g_launches += (uint64_t)n;
+}
 
 static thread_local int g_ktimer_on = 0;
 static thread_local cudaEvent_t g_kt_ev[KT_COUNT][2] = {};

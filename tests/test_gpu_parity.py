@@ -392,6 +392,30 @@ def test_align_replica_pose(g, replica_setup):
     assert abs(st["iters"] - ref["iters"]) <= 1
 
 
+def test_align_tum_noisy_pose_and_linearize(g, tum):
+    """C3: TUM-shaped noisy frame (stride 4) vs the 1e6 map.  Per-linearisation parity at the
+    initial pose, and the final pose from the same init after a fixed number of GN iterations
+    (on noisy depth the 1e-6 convergence test is not reached: both run to the cap)."""
+    w = tum
+    K = w.K
+    s = 4
+    xyz, _ = oracle.backproject(w.depth, K.fx, K.fy, K.cx, K.cy, s)
+    pos, d_n = gpu_points(g, w.depth, K, s)
+    src = g.covariances(pos, d_n, cell0=3.0 * s / K.fx, levels=4)
+    tgt = g.build_target(t(w.means), t(w.quats), t(w.scales))
+    S = dict(xyz=xyz, txyz=w.means, src=src, tgt=tgt, ocs=oracle.covariances(xyz)["cov"],
+             oct=oracle.target_from_map(w.quats, w.scales)[0], tree=oracle.KDTree(w.means))
+    _lin_check(g, S, w.T_init, 0.1)
+    for iters in (3, 8):
+        p = g.align_params(max_iters=iters, max_corr_dist=0.1, eps_rot=0.0, eps_trans=0.0)
+        Tg, st = g.align(src, tgt, w.T_init, p)
+        ref = oracle.align(xyz, S["ocs"], w.means, S["oct"], w.T_init, max_iters=iters, max_corr_dist=0.1,
+                           eps_rot=0.0, eps_trans=0.0, use_tree=True, tree=S["tree"])
+        assert rot_angle(Tg[:3, :3], ref["T"][:3, :3]) <= 1e-5, iters
+        assert np.linalg.norm(Tg[:3, 3] - ref["T"][:3, 3]) <= 1e-5, iters
+        assert st["n_inliers"] == ref["n_inliers"] and st["iters"] == ref["iters"] == iters
+
+
 def test_align_deterministic(g, replica_setup):
     S = replica_setup
     w = S["w"]

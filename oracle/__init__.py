@@ -70,6 +70,10 @@ def lib():
         L.ora_set_threads.restype = None
         L.ora_scale_align.argtypes = [P, d, d, d, P]
         L.ora_scale_align.restype = i
+        L.ora_export_gaussian.argtypes = [P, P, P, i, d, d, d, P, P, P]
+        L.ora_export_gaussian.restype = i
+        L.ora_export_gaussians.argtypes = [P, P, i, P, i, d, d, d, P, P, P]
+        L.ora_export_gaussians.restype = None
         _lib = L
     return _lib
 
@@ -254,3 +258,24 @@ def scale_align(scales, z, p=1.5, c=1.0):
     if rc != 0:
         raise ValueError("scale_align: z must be > 0")
     return out
+
+
+def export_gaussian(C6, p_cam, T=None, mode=ELLIPSE, eps=1e-3, p=1.5, c=1.0):
+    """O12' one point -> (mean (3,), quat wxyz (4,), scales (3,), rc) in binary64."""
+    C6 = np.ascontiguousarray(C6, np.float64)
+    pc = _f32(p_cam)
+    Tm = None if T is None else np.ascontiguousarray(T, np.float64)
+    mean, quat, sc = np.empty(3), np.empty(4), np.empty(3)
+    rc = lib().ora_export_gaussian(_p(C6), _p(pc), _p(Tm), mode, eps, p, c, _p(mean), _p(quat), _p(sc))
+    return mean, quat, sc, rc
+
+
+def export_gaussians(xyz, raw, T=None, mode=ELLIPSE, eps=1e-3, p=1.5, c=1.0):
+    """O12' over a cloud (raw covariances from covariances()['raw']) -> (means, quats, scales) f64."""
+    xyz = _f32(xyz)
+    raw = np.ascontiguousarray(raw, np.float64)
+    n = xyz.shape[0]
+    Tm = None if T is None else np.ascontiguousarray(T, np.float64)
+    means, quats, sc = np.empty((n, 3)), np.empty((n, 4)), np.empty((n, 3))
+    lib().ora_export_gaussians(_p(xyz), _p(raw), n, _p(Tm), mode, eps, p, c, _p(means), _p(quats), _p(sc))
+    return means, quats, sc

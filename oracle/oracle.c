@@ -698,3 +698,91 @@ int ora_scale_align(const double *scales_in, double z, double p, double c, doubl
     for (int a = 0; a < 3; ++a) scales_out[a] = scales_in[a] * f;
     return 0;
 }
+
+/* O12' 3DGS export of one source point (ALG-12; Eq. 3-4):
+ *  1. C = R Lambda^2 R^T (Eq. 3) by O4 (Jacobi): variances lam_2 >= lam_1 >= lam_0, frame (v2, v1, v0);
+ *  2. the mode's regularised variances (the spectrum of O5's output, R6-R8):
+ *       ELLIPSE  max(lam_i / lam_1, eps)   (Lambda' = Lambda / median(S), Eq. 4, floored, R7)
+ *       PLANE    (1, 1, eps)               (R6)
+ *       NONE     max(lam_i, 1e-6)
+ *       degenerate (R8): lam_2 <= tau -> (1, 1, 1) (NONE: 1e-6 each); lam_1 <= tau -> (1, eps, eps);
+ *  3. Lambda'' = Lambda' / z^p with the absolute factor c (R21): scales_i = c * sqrt(var_i) / z^p,
+ *     z = the point's depth in the camera frame (p_cam[2]); z <= 0 -> scales 0 and return -1;
+ *  4. the Gaussian's orientation: the frame (v2, v1, v0) made right-handed (v0 <- -v0 if det < 0),
+ *     rotated into the world by T (R_w = T_R * frame), as a unit quaternion wxyz with w >= 0
+ *     (Shepperd's method: the largest of 1 + trace, 1 + 2 R_aa - trace picks the stable formula);
+ *  5. the mean: K3(T, p_cam).
+ * T: row-major 4x4 binary64 (NULL = identity). */
+static void ora_quat_from_rot(double R[3][3], double *q) {
+    double tr = R[0][0] + R[1][1] + R[2][2];
+    double w, x, y, z;
+    if (tr >= R[0][0] && tr >= R[1][1] && tr >= R[2][2]) {
+        double s = 2.0 * sqrt(1.0 + tr);
+        w = 0.25 * s; x = (R[2][1] - R[1][2]) / s; y = (R[0][2] - R[2][0]) / s; z = (R[1][0] - R[0][1]) / s;
+    } else if (R[0][0] >= R[1][1] && R[0][0] >= R[2][2]) {
+        double s = 2.0 * sqrt(1.0 + R[0][0] - R[1][1] - R[2][2]);
+        w = (R[2][1] - R[1][2]) / s; x = 0.25 * s; y = (R[0][1] + R[1][0]) / s; z = (R[0][2] + R[2][0]) / s;
+    } else if (R[1][1] >= R[2][2]) {
+        double s = 2.0 * sqrt(1.0 + R[1][1] - R[0][0] - R[2][2]);
+        w = (R[0][2] - R[2][0]) / s; x = (R[0][1] + R[1][0]) / s; y = 0.25 * s; z = (R[1][2] + R[2][1]) / s;
+    } else {
+        double s = 2.0 * sqrt(1.0 + R[2][2] - R[0][0] - R[1][1]);
+        w = (R[1][0] - R[0][1]) / s; x = (R[0][2] + R[2][0]) / s; y = (R[1][2] + R[2][1]) / s; z = 0.25 * s;
+    }
+    double n = sqrt(w * w + x * x + y * y + z * z);
+    double sg = w < 0 ? -1.0 : 1.0;
+    q[0] = sg * w / n; q[1] = sg * x / n; q[2] = sg * y / n; q[3] = sg * z / n;
+}
+
+int ora_export_gaussian(const double *C, const float *p_cam, const double *T, int mode, double eps, double p,
+                        double c, double *mean_out, double *quat_out, double *scale_out) {
+    double lam[3], V[9], var[3];
+    ora_eigen_jacobi(C, lam, V);
+    if (mode == ORA_NONE) {
+        for (int j = 0; j < 3; ++j) var[j] = lam[j] > ORA_NONE_FLOOR ? lam[j] : ORA_NONE_FLOOR;
+    } else if (lam[0] <= ORA_TAU) {
+        var[0] = var[1] = var[2] = 1.0;
+    } else if (lam[1] <= ORA_TAU) {
+        var[0] = 1.0; var[1] = var[2] = eps;
+    } else if (mode == ORA_PLANE) {
+        var[0] = var[1] = 1.0; var[2] = eps;
+    } else {
+        for (int j = 0; j < 3; ++j) {
+            double w = lam[j] / lam[1];
+            var[j] = w > eps ? w : eps;
+        }
+    }
+    double z = (double)p_cam[2];
+    int rc = 0;
+    double f = 0.0;
+    if (z > 0) f = c / pow(z, p); else rc = -1;
+    for (int j = 0; j < 3; ++j) scale_out[j] = f * sqrt(var[j]);
+    /* right-handed frame: columns v2, v1, v0 */
+    double F[3][3];
+    for (int r = 0; r < 3; ++r)
+        for (int j = 0; j < 3; ++j) F[r][j] = V[3 * j + r];
+    double det = F[0][0] * (F[1][1] * F[2][2] - F[1][2] * F[2][1]) - F[0][1] * (F[1][0] * F[2][2] - F[1][2] * F[2][0]) +
+                 F[0][2] * (F[1][0] * F[2][1] - F[1][1] * F[2][0]);
+    if (det < 0)
+        for (int r = 0; r < 3; ++r) F[r][2] = -F[r][2];
+    double Rw[3][3];
+    for (int r = 0; r < 3; ++r)
+        for (int j = 0; j < 3; ++j)
+            Rw[r][j] = T ? T[4 * r + 0] * F[0][j] + T[4 * r + 1] * F[1][j] + T[4 * r + 2] * F[2][j] : F[r][j];
+    ora_quat_from_rot(Rw, quat_out);
+    if (T) {
+        ora_transform(T, p_cam, mean_out);
+    } else {
+        for (int r = 0; r < 3; ++r) mean_out[r] = (double)p_cam[r];
+    }
+    return rc;
+}
+
+/* O12' over a cloud: raw covariances (n*6 binary64, from ora_covariances' raw_out). */
+void ora_export_gaussians(const float *xyz, const double *raw, int n, const double *T, int mode, double eps,
+                          double p, double c, double *means, double *quats, double *scales) {
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i)
+        ora_export_gaussian(raw + 6 * (int64_t)i, xyz + 3 * (int64_t)i, T, mode, eps, p, c, means + 3 * (int64_t)i,
+                            quats + 4 * (int64_t)i, scales + 3 * (int64_t)i);
+}

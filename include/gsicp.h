@@ -284,6 +284,24 @@ gsicp_status gsicp_pose_predict(const double *d_hist, double *d_T_out, void *str
 gsicp_status gsicp_pose_push(double *d_hist, const double *d_T, double *d_traj, int32_t *d_counter, int32_t traj_cap,
                              void *stream);
 
+/* A4 export: source points -> 3DGS Gaussians for keyframe insertion into the map (ALG-12).
+ * P:187-191 Eq. 3 C = R Lambda^2 R^T, Eq. 4 Lambda' = Lambda / median(S)
+ * Lambda'' = Lambda' / z^p (p = 1.5 best) with the absolute factor c (R21).
+ *  pos, cov_a, cov_b [dev]: a source cloud and the covariances gsicp_covariances* wrote for it
+ *      (the regularised covariance: its spectrum is the mode's Lambda'^2, its eigenvectors R);
+ *  d_n [dev] int32: the number of points (<= cap); d_T [dev] double[16] row-major or NULL
+ *      (identity): the pose mapping the camera frame into the world (the tracked pose);
+ *  p, c: the scale-aligning exponent and factor.
+ *  means_out [dev] float[cap*3] = K3(T, x) rounded to binary32; quats_out [dev] float[cap*4]
+ *      (16-byte aligned) unit wxyz quaternion (w >= 0) of T_R * (v2, v1, v0) made right-handed;
+ *  scales_out [dev] float[cap*3] = c * sqrt(var'_j) / z^p, descending, z = the point's camera
+ *      depth (z <= 0: scales 0).  Exactly the layout gsicp_build_target reads (scales linear).
+ *  Rows [*d_n, cap) are not written.  Errors: INVALID_ARGUMENT (null, misaligned, cap < 1,
+ *  p or c not finite, c <= 0), CUDA. */
+gsicp_status gsicp_export_gaussians(const float *pos, const float *cov_a, const float *cov_b, const int32_t *d_n,
+                                    int32_t cap, const double *d_T, double p, double c, float *means_out,
+                                    float *quats_out, float *scales_out, void *stream);
+
 /* CUDA-graph helpers for callers that capture a whole frame (host pointers; stream-ordered).
  * gsicp_graph_instantiate: instantiates a captured graph (cudaGraph_t) so that kernel nodes keep
  * their launch priorities (cudaGraphInstantiateFlagUseNodePriority): the frame's critical path

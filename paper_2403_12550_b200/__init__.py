@@ -115,7 +115,8 @@ def lib():
         L.gsicp_debug_align_counters.restype = None
         L.gsicp_pose_predict.argtypes = [P, P, P]
         L.gsicp_pose_push.argtypes = [P, P, P, P, i32, P]
-        for name in ("gsicp_pose_predict", "gsicp_pose_push"):
+        L.gsicp_export_gaussians.argtypes = [P, P, P, P, i32, P, C.c_double, C.c_double, P, P, P, P]
+        for name in ("gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_gaussians"):
             getattr(L, name).restype = i32
         L.gsicp_graph_instantiate.argtypes = [P, C.POINTER(C.c_void_p)]
         L.gsicp_graph_launch.argtypes = [P, P]
@@ -146,7 +147,7 @@ EXPORTED = [
     "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version", "gsicp_debug_knn_counters",
     "gsicp_debug_align_timeline", "gsicp_debug_align_counters", "gsicp_debug_kernel_timer",
     "gsicp_debug_kernel_time", "gsicp_graph_instantiate", "gsicp_graph_launch", "gsicp_graph_destroy",
-    "gsicp_pose_predict", "gsicp_pose_push",
+    "gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_gaussians",
 ]
 
 KT_KNN_SEARCH, KT_ALIGN, KT_SEED, KT_BP, KT_COVS, KT_WIDE, KT_TAIL = 0, 1, 2, 3, 4, 5, 6
@@ -504,6 +505,22 @@ def pose_push(hist: torch.Tensor, T: torch.Tensor, traj: torch.Tensor | None = N
     """hist <- (T_{t-1}, T); traj[counter++] = T if given (device tensors)."""
     cap = traj.shape[0] if traj is not None else 0
     _check(lib().gsicp_pose_push(_ptr(hist), _ptr(T), _ptr(traj), _ptr(counter), cap, _stream(stream)))
+
+
+def export_gaussians(pos: torch.Tensor, d_n: torch.Tensor, cov_a: torch.Tensor, cov_b: torch.Tensor,
+                     T: torch.Tensor | None = None, p: float = 1.5, c: float = 1.0, out=None, stream=None):
+    """A4 export (ALG-12): the cloud's points as 3DGS Gaussians in the world frame of
+    the device pose T (float64 4x4, None = identity) -> (means (cap,3), quats wxyz (cap,4),
+    scales (cap,3)) float32 device tensors, rows [0, d_n) written — the layout build_target reads."""
+    cap = pos.shape[0]
+    if out is None:
+        out = (torch.empty((cap, 3), dtype=torch.float32, device=pos.device),
+               torch.empty((cap, 4), dtype=torch.float32, device=pos.device),
+               torch.empty((cap, 3), dtype=torch.float32, device=pos.device))
+    means, quats, scales = out
+    _check(lib().gsicp_export_gaussians(_ptr(pos), _ptr(cov_a), _ptr(cov_b), _ptr(d_n), cap, _ptr(T), float(p),
+                                        float(c), _ptr(means), _ptr(quats), _ptr(scales), _stream(stream)))
+    return means, quats, scales
 
 
 class FrameGraph:

@@ -69,6 +69,9 @@ cudaError_t build_target_launch(const float *means, const float *quats, const fl
                                 cudaStream_t s);
 cudaError_t build_target_cloud_launch(const gsicp_cloud &cl, int M, float cell, gsicp_target *out, void *ws,
                                       cudaStream_t s);
+cudaError_t export_launch(const float4 *pos, const float4 *cov_a, const float4 *cov_b, const int32_t *d_n, int cap,
+                          const double *d_T, double p, double c, float *means, float *quats, float *scales,
+                          cudaStream_t s);
 size_t align_ws_bytes(int cap);
 double *align_ws_T(void *ws);
 gsicp_align_stats *align_ws_stats(void *ws);
@@ -216,6 +219,21 @@ gsicp_status gsicp_pose_push(double *d_hist, const double *d_T, double *d_traj, 
     gsicp::k_pose_push<<<1, 32, 0, (cudaStream_t)stream>>>(d_hist, d_T, d_traj, d_counter, traj_cap);
     gsicp::note_launch();
     return cuda_status(cudaGetLastError(), "pose_push");
+}
+
+gsicp_status gsicp_export_gaussians(const float *pos, const float *cov_a, const float *cov_b, const int32_t *d_n,
+                                    int32_t cap, const double *d_T, double p, double c, float *means_out,
+                                    float *quats_out, float *scales_out, void *stream) {
+    g_err[0] = 0;
+    if (!pos || !cov_a || !cov_b || !d_n || !means_out || !quats_out || !scales_out)
+        BAD("export_gaussians: null pointer");
+    if (!aligned16(pos) || !aligned16(cov_a) || !aligned16(cov_b) || !aligned16(quats_out))
+        BAD("export_gaussians: pos, cov_a, cov_b and quats_out must be 16-byte aligned");
+    if (cap < 1) BAD("export_gaussians: cap must be >= 1");
+    if (!isfinite(p) || !isfinite(c) || !(c > 0.0)) BAD("export_gaussians: p must be finite and c > 0");
+    return cuda_status(export_launch((const float4 *)pos, (const float4 *)cov_a, (const float4 *)cov_b, d_n, cap, d_T,
+                                     p, c, means_out, quats_out, scales_out, (cudaStream_t)stream),
+                       "export_gaussians");
 }
 
 gsicp_status gsicp_graph_instantiate(void *graph, void **exec_out) {

@@ -112,3 +112,9 @@ def test_new_entry_points_reject_bad_arguments(g):
     assert L.gsicp_pose_predict(None, fake, None) == g.ERR_INVALID_ARGUMENT
     assert L.gsicp_graph_launch(None, None) == g.ERR_INVALID_ARGUMENT
     assert L.gsicp_graph_destroy(None) == g.OK
+    st = L.gsicp_export_gaussians(fake, fake, fake, fake, 100, None, 1.5, 1.0, fake, None, fake, None)
+    assert st == g.ERR_INVALID_ARGUMENT  # null quats_out
+    st = L.gsicp_export_gaussians(fake, fake, fake, fake, 100, None, 1.5, 0.0, fake, fake, fake, None)
+    assert st == g.ERR_INVALID_ARGUMENT and b"c > 0" in L.gsicp_last_error()
+    st = L.gsicp_export_gaussians(fake, fake, fake, fake, 0, None, 1.5, 1.0, fake, fake, fake, None)
+    assert st == g.ERR_INVALID_ARGUMENT

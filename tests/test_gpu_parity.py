@@ -565,3 +565,79 @@ def test_sequence_tracking(g):
     P = out.cpu().numpy().reshape(4, 4)
     np.testing.assert_allclose(P, B @ np.linalg.inv(A) @ B, atol=1e-12)
     np.testing.assert_allclose(P[:3, :3] @ P[:3, :3].T, np.eye(3), atol=1e-14)
+
+
+# ----------------------------------------------------------------------------------------- A4 export
+def _quat_rot(q):
+    """(n,4) wxyz -> (n,3,3) rotation matrices (the textbook formula, binary64)."""
+    q = np.asarray(q, np.float64)
+    q = q / np.linalg.norm(q, axis=1, keepdims=True)
+    w, x, y, z = q.T
+    return np.stack([np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)], 1),
+                     np.stack([2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)], 1),
+                     np.stack([2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], 1)], 1)
+
+
+@pytest.mark.parametrize("case,mode", [("c1", oracle.ELLIPSE), ("replica4", oracle.ELLIPSE),
+                                       ("replica4", oracle.PLANE), ("replica4", oracle.NONE)])
+def test_export_gaussians(g, c1, replica, case, mode):
+    """gsicp_export_gaussians (ALG-12) vs the oracle's O12' on the same frame and pose:
+    means bit-exact (K3, rounded to binary32); the exported world covariance R diag(s^2) R^T within
+    1e-4 (the covariance tolerance); the variances within 1e-4 of the largest; unit quaternions
+    with w >= 0; where the spectrum has clear gaps, the same axes up to sign.  ELLIPSE round trip:
+    build_target of the export gives the source covariance rotated into the world."""
+    w, s = {"c1": (c1, 1), "replica4": (replica, 4)}[case]
+    K = w.K
+    H, W = w.depth.shape
+    pos, d_n = gpu_points(g, w.depth, K, s)
+    xyz, _ = oracle.backproject(w.depth, K.fx, K.fy, K.cx, K.cy, s)
+    n = xyz.shape[0]
+    cl = g.covariances_image(pos, d_n, H, W, s, (K.fx, K.fy, K.cx, K.cy), k=20, mode=mode, eps_var=1e-3,
+                             cell0=3.0 * s / K.fx, levels=4)
+    rng = np.random.default_rng(80)
+    a = rng.normal(size=3)
+    a /= np.linalg.norm(a)  # 0.5 rad about a random unit axis (Rodrigues)
+    Kx = np.array([[0, -a[2], a[1]], [a[2], 0, -a[0]], [-a[1], a[0], 0]])
+    T = np.eye(4)
+    T[:3, :3] = np.eye(3) + math.sin(0.5) * Kx + (1 - math.cos(0.5)) * Kx @ Kx
+    T[:3, 3] = [0.3, -1.2, 2.0]
+    p, c = 1.5, 0.7
+    gm, gq, gs = g.export_gaussians(cl.pos, cl.d_n, cl.cov_a, cl.cov_b, T=t(T), p=p, c=c)
+    gm, gq, gs = gm[:n].cpu().numpy(), gq[:n].cpu().numpy(), gs[:n].cpu().numpy()
+    ref = oracle.covariances(xyz, k=20, mode=mode)
+    om, oq, os_ = oracle.export_gaussians(xyz, ref["raw"], T=T, mode=mode, p=p, c=c)
+    np.testing.assert_array_equal(gm, om.astype(np.float32))
+    assert np.abs(np.linalg.norm(gq.astype(np.float64), axis=1) - 1).max() < 1e-6
+    assert (gq[:, 0] >= 0).all()
+    Rg, Ro = _quat_rot(gq), _quat_rot(oq)
+    Sg = Rg @ (gs.astype(np.float64)[:, :, None] ** 2 * np.transpose(Rg, (0, 2, 1)))
+    So = Ro @ (os_[:, :, None] ** 2 * np.transpose(Ro, (0, 2, 1)))
+    err = np.linalg.norm(Sg - So, axis=(1, 2)) / np.linalg.norm(So, axis=(1, 2))
+    assert err.max() <= 1e-4, (err.max(), np.argmax(err))
+    vg, vo = gs.astype(np.float64) ** 2, os_ ** 2
+    assert (np.abs(vg - vo) <= 1e-4 * vo[:, :1]).all()
+    assert (gs[:, 0] >= gs[:, 1]).all() and (gs[:, 1] >= gs[:, 2]).all()
+    # an axis is unique (up to sign) where its variance is separated from its neighbours' (PLANE:
+    # only the normal, the other two share variance 1)
+    g01 = vo[:, 0] - vo[:, 1] > 1e-2 * vo[:, 0]
+    g12 = vo[:, 1] - vo[:, 2] > 1e-2 * vo[:, 0]
+    dots = np.abs(np.einsum("nrj,nrj->nj", Rg, Ro))
+    for j, sep in enumerate((g01, g01 & g12, g12)):
+        if mode != oracle.PLANE or j == 2:
+            assert sep.mean() > 0.5, (j, sep.mean())
+        if sep.any():
+            assert dots[sep, j].min() >= 1 - 1e-6, (j, dots[sep, j].min())
+    if mode == oracle.ELLIPSE:
+        tgt = g.build_target(t(gm), t(gq), t(gs), mode=mode, eps_var=1e-3)
+        tpos, ca, cb = tgt.arrays()
+        order = tpos[:, 3].contiguous().view(torch.int32).long().cpu().numpy()
+        inv = np.empty(n, np.int64)
+        inv[order] = np.arange(n)
+        tc = torch.cat([ca, cb[:, :2]], 1).cpu().numpy()[inv]
+        R = T[:3, :3]
+        cam = cl.cov6()[:n].cpu().numpy().astype(np.float64)
+        full = cam[:, [0, 1, 2, 1, 3, 4, 2, 4, 5]].reshape(-1, 3, 3)
+        wc = R @ full @ R.T
+        wc6 = wc[:, [0, 0, 0, 1, 1, 2], [0, 1, 2, 1, 2, 2]]
+        e2 = cov_rel_err(tc, wc6)
+        assert e2.max() <= 1e-4, e2.max()

@@ -296,11 +296,18 @@ gsicp_status gsicp_pose_push(double *d_hist, const double *d_T, double *d_traj, 
  *      (16-byte aligned) unit wxyz quaternion (w >= 0) of T_R * (v2, v1, v0) made right-handed;
  *  scales_out [dev] float[cap*3] = c * sqrt(var'_j) / z^p, descending, z = the point's camera
  *      depth (z <= 0: scales 0).  Exactly the layout gsicp_build_target reads (scales linear).
- *  Rows [*d_n, cap) are not written.  Errors: INVALID_ARGUMENT (null, misaligned, cap < 1,
- *  p or c not finite, c <= 0), CUDA. */
+ *  corr [dev] nullable int32[cap]: the overlap filter (R28) — if given, only the points
+ *      with corr[i] < 0 (no valid correspondence in the final linearisation: gsicp_align_async's
+ *      corr_out, or gsicp_linearize's) are exported, compacted in index order into rows
+ *      [0, *d_m_out); then d_m_out is required and ws must hold gsicp_export_workspace_size(cap)
+ *      bytes (256-byte aligned).  Without corr, row i is point i and *d_m_out (if given) = *d_n.
+ *  Rows beyond the exported count are not written.  Errors: INVALID_ARGUMENT (null, misaligned,
+ *  cap < 1, p or c not finite, c <= 0, corr without d_m_out), WORKSPACE_TOO_SMALL, CUDA. */
+size_t gsicp_export_workspace_size(int32_t cap);
 gsicp_status gsicp_export_gaussians(const float *pos, const float *cov_a, const float *cov_b, const int32_t *d_n,
-                                    int32_t cap, const double *d_T, double p, double c, float *means_out,
-                                    float *quats_out, float *scales_out, void *stream);
+                                    int32_t cap, const double *d_T, double p, double c, const int32_t *corr,
+                                    float *means_out, float *quats_out, float *scales_out, int32_t *d_m_out,
+                                    void *ws, size_t ws_bytes, void *stream);
 
 /* CUDA-graph helpers for callers that capture a whole frame (host pointers; stream-ordered).
  * gsicp_graph_instantiate: instantiates a captured graph (cudaGraph_t) so that kernel nodes keep

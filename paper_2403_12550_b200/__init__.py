@@ -115,7 +115,9 @@ def lib():
         L.gsicp_debug_align_counters.restype = None
         L.gsicp_pose_predict.argtypes = [P, P, P]
         L.gsicp_pose_push.argtypes = [P, P, P, P, i32, P]
-        L.gsicp_export_gaussians.argtypes = [P, P, P, P, i32, P, C.c_double, C.c_double, P, P, P, P]
+        L.gsicp_export_gaussians.argtypes = [P, P, P, P, i32, P, C.c_double, C.c_double, P, P, P, P, P, P, sz, P]
+        L.gsicp_export_workspace_size.argtypes = [i32]
+        L.gsicp_export_workspace_size.restype = sz
         for name in ("gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_gaussians"):
             getattr(L, name).restype = i32
         L.gsicp_graph_instantiate.argtypes = [P, C.POINTER(C.c_void_p)]
@@ -147,7 +149,7 @@ EXPORTED = [
     "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version", "gsicp_debug_knn_counters",
     "gsicp_debug_align_timeline", "gsicp_debug_align_counters", "gsicp_debug_kernel_timer",
     "gsicp_debug_kernel_time", "gsicp_graph_instantiate", "gsicp_graph_launch", "gsicp_graph_destroy",
-    "gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_gaussians",
+    "gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_workspace_size", "gsicp_export_gaussians",
 ]
 
 KT_KNN_SEARCH, KT_ALIGN, KT_SEED, KT_BP, KT_COVS, KT_WIDE, KT_TAIL = 0, 1, 2, 3, 4, 5, 6
@@ -508,19 +510,26 @@ def pose_push(hist: torch.Tensor, T: torch.Tensor, traj: torch.Tensor | None = N
 
 
 def export_gaussians(pos: torch.Tensor, d_n: torch.Tensor, cov_a: torch.Tensor, cov_b: torch.Tensor,
-                     T: torch.Tensor | None = None, p: float = 1.5, c: float = 1.0, out=None, stream=None):
+                     T: torch.Tensor | None = None, p: float = 1.5, c: float = 1.0, corr: torch.Tensor | None = None,
+                     out=None, stream=None):
     """A4 export (ALG-12): the cloud's points as 3DGS Gaussians in the world frame of
     the device pose T (float64 4x4, None = identity) -> (means (cap,3), quats wxyz (cap,4),
-    scales (cap,3)) float32 device tensors, rows [0, d_n) written — the layout build_target reads."""
+    scales (cap,3), d_m (1,) int32) float32 device tensors, rows [0, d_m) written — the layout
+    build_target reads.  corr (int32, from align/linearize): export only the points without a map
+    correspondence (the overlap filter), compacted in index order."""
     cap = pos.shape[0]
+    dev = pos.device
     if out is None:
-        out = (torch.empty((cap, 3), dtype=torch.float32, device=pos.device),
-               torch.empty((cap, 4), dtype=torch.float32, device=pos.device),
-               torch.empty((cap, 3), dtype=torch.float32, device=pos.device))
+        out = (torch.empty((cap, 3), dtype=torch.float32, device=dev),
+               torch.empty((cap, 4), dtype=torch.float32, device=dev),
+               torch.empty((cap, 3), dtype=torch.float32, device=dev))
     means, quats, scales = out
+    d_m = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = _ws(lib().gsicp_export_workspace_size(cap), dev) if corr is not None else None
     _check(lib().gsicp_export_gaussians(_ptr(pos), _ptr(cov_a), _ptr(cov_b), _ptr(d_n), cap, _ptr(T), float(p),
-                                        float(c), _ptr(means), _ptr(quats), _ptr(scales), _stream(stream)))
-    return means, quats, scales
+                                        float(c), _ptr(corr), _ptr(means), _ptr(quats), _ptr(scales), _ptr(d_m),
+                                        _ptr(ws), ws.numel() if ws is not None else 0, _stream(stream)))
+    return means, quats, scales, d_m
 
 
 class FrameGraph:

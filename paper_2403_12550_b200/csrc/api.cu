@@ -69,9 +69,10 @@ cudaError_t build_target_launch(const float *means, const float *quats, const fl
                                 cudaStream_t s);
 cudaError_t build_target_cloud_launch(const gsicp_cloud &cl, int M, float cell, gsicp_target *out, void *ws,
                                       cudaStream_t s);
+size_t export_ws_bytes(int cap);
 cudaError_t export_launch(const float4 *pos, const float4 *cov_a, const float4 *cov_b, const int32_t *d_n, int cap,
-                          const double *d_T, double p, double c, float *means, float *quats, float *scales,
-                          cudaStream_t s);
+                          const double *d_T, double p, double c, const int32_t *corr, float *means, float *quats,
+                          float *scales, int32_t *d_m, void *ws, cudaStream_t s);
 size_t align_ws_bytes(int cap);
 double *align_ws_T(void *ws);
 gsicp_align_stats *align_ws_stats(void *ws);
@@ -221,9 +222,12 @@ gsicp_status gsicp_pose_push(double *d_hist, const double *d_T, double *d_traj, 
     return cuda_status(cudaGetLastError(), "pose_push");
 }
 
+size_t gsicp_export_workspace_size(int32_t cap) { return cap < 1 ? 0 : export_ws_bytes(cap); }
+
 gsicp_status gsicp_export_gaussians(const float *pos, const float *cov_a, const float *cov_b, const int32_t *d_n,
-                                    int32_t cap, const double *d_T, double p, double c, float *means_out,
-                                    float *quats_out, float *scales_out, void *stream) {
+                                    int32_t cap, const double *d_T, double p, double c, const int32_t *corr,
+                                    float *means_out, float *quats_out, float *scales_out, int32_t *d_m_out,
+                                    void *ws, size_t ws_bytes, void *stream) {
     g_err[0] = 0;
     if (!pos || !cov_a || !cov_b || !d_n || !means_out || !quats_out || !scales_out)
         BAD("export_gaussians: null pointer");
@@ -231,8 +235,13 @@ gsicp_status gsicp_export_gaussians(const float *pos, const float *cov_a, const 
         BAD("export_gaussians: pos, cov_a, cov_b and quats_out must be 16-byte aligned");
     if (cap < 1) BAD("export_gaussians: cap must be >= 1");
     if (!isfinite(p) || !isfinite(c) || !(c > 0.0)) BAD("export_gaussians: p must be finite and c > 0");
+    if (corr) {
+        if (!d_m_out) BAD("export_gaussians: a correspondence filter needs d_m_out");
+        gsicp_status st = check_ws(ws, ws_bytes, export_ws_bytes(cap));
+        if (st != GSICP_OK) return st;
+    }
     return cuda_status(export_launch((const float4 *)pos, (const float4 *)cov_a, (const float4 *)cov_b, d_n, cap, d_T,
-                                     p, c, means_out, quats_out, scales_out, (cudaStream_t)stream),
+                                     p, c, corr, means_out, quats_out, scales_out, d_m_out, ws, (cudaStream_t)stream),
                        "export_gaussians");
 }
 

@@ -112,9 +112,15 @@ def test_new_entry_points_reject_bad_arguments(g):
     assert L.gsicp_pose_predict(None, fake, None) == g.ERR_INVALID_ARGUMENT
     assert L.gsicp_graph_launch(None, None) == g.ERR_INVALID_ARGUMENT
     assert L.gsicp_graph_destroy(None) == g.OK
-    st = L.gsicp_export_gaussians(fake, fake, fake, fake, 100, None, 1.5, 1.0, fake, None, fake, None)
-    assert st == g.ERR_INVALID_ARGUMENT  # null quats_out
-    st = L.gsicp_export_gaussians(fake, fake, fake, fake, 100, None, 1.5, 0.0, fake, fake, fake, None)
+    E = L.gsicp_export_gaussians
+    assert E(fake, fake, fake, fake, 100, None, 1.5, 1.0, None, fake, None, fake, None, None, 0, None) \
+        == g.ERR_INVALID_ARGUMENT  # null quats_out
+    st = E(fake, fake, fake, fake, 100, None, 1.5, 0.0, None, fake, fake, fake, None, None, 0, None)
     assert st == g.ERR_INVALID_ARGUMENT and b"c > 0" in L.gsicp_last_error()
-    st = L.gsicp_export_gaussians(fake, fake, fake, fake, 0, None, 1.5, 1.0, fake, fake, fake, None)
-    assert st == g.ERR_INVALID_ARGUMENT
+    assert E(fake, fake, fake, fake, 0, None, 1.5, 1.0, None, fake, fake, fake, None, None, 0, None) \
+        == g.ERR_INVALID_ARGUMENT
+    st = E(fake, fake, fake, fake, 100, None, 1.5, 1.0, fake, fake, fake, fake, None, fake, 1 << 20, None)
+    assert st == g.ERR_INVALID_ARGUMENT and b"d_m_out" in L.gsicp_last_error()
+    st = E(fake, fake, fake, fake, 100000, None, 1.5, 1.0, fake, fake, fake, fake, fake, C.c_void_p(0x100000), 16, None)
+    assert st == g.ERR_WORKSPACE_TOO_SMALL
+    assert L.gsicp_export_workspace_size(100000) >= 4 * (100000 // 256)

@@ -602,7 +602,8 @@ def test_export_gaussians(g, c1, replica, case, mode):
     T[:3, :3] = np.eye(3) + math.sin(0.5) * Kx + (1 - math.cos(0.5)) * Kx @ Kx
     T[:3, 3] = [0.3, -1.2, 2.0]
     p, c = 1.5, 0.7
-    gm, gq, gs = g.export_gaussians(cl.pos, cl.d_n, cl.cov_a, cl.cov_b, T=t(T), p=p, c=c)
+    gm, gq, gs, d_m = g.export_gaussians(cl.pos, cl.d_n, cl.cov_a, cl.cov_b, T=t(T), p=p, c=c)
+    assert int(d_m.item()) == n
     gm, gq, gs = gm[:n].cpu().numpy(), gq[:n].cpu().numpy(), gs[:n].cpu().numpy()
     ref = oracle.covariances(xyz, k=20, mode=mode)
     om, oq, os_ = oracle.export_gaussians(xyz, ref["raw"], T=T, mode=mode, p=p, c=c)
@@ -641,3 +642,36 @@ def test_export_gaussians(g, c1, replica, case, mode):
         wc6 = wc[:, [0, 0, 0, 1, 1, 2], [0, 1, 2, 1, 2, 2]]
         e2 = cov_rel_err(tc, wc6)
         assert e2.max() <= 1e-4, e2.max()
+
+
+def test_export_overlap_filter(g, replica_setup):
+    """Overlap filter (R28): with the correspondences of a linearisation, only the points
+    without a map correspondence are exported, compacted in index order — the same rows as the
+    oracle's export of the points its own O7 leaves unmatched at the same pose (bit-exact means)."""
+    S = replica_setup
+    src, tgt, xyz = S["src"], S["tgt"], S["xyz"]
+    n = xyz.shape[0]
+    T = synth.perturb_pose(S["w"].T_gt, 13, 2.0, 0.03)
+    oraw = oracle.covariances(xyz)["raw"]
+    for r in (0.01, 0.03, 1e3):
+        corr = torch.full((src.cap,), -9, dtype=torch.int32, device=DEV)
+        g.linearize(src, tgt, T, r, corr_out=corr)
+        gm, gq, gs, d_m = g.export_gaussians(src.pos, src.d_n, src.cov_a, src.cov_b, T=t(T), corr=corr)
+        m = int(d_m.item())
+        lin = oracle.linearize(xyz, S["ocs"], S["txyz"], S["oct"], T, r, tree=S["tree"])
+        keep = np.nonzero(lin["corr"] < 0)[0]
+        assert m == keep.size, (r, m, keep.size, n)
+        if r > 1.0:
+            assert m == 0
+            continue
+        assert m < n and (m > 0 or r > 0.01), (r, m)
+        if m == 0:
+            continue
+        om, oq, os_ = oracle.export_gaussians(xyz[keep], oraw[keep], T=T)
+        np.testing.assert_array_equal(gm[:m].cpu().numpy(), om.astype(np.float32))
+        Rg, Ro = _quat_rot(gq[:m].cpu().numpy()), _quat_rot(oq)
+        gsn = gs[:m].cpu().numpy().astype(np.float64)
+        Sg = Rg @ (gsn[:, :, None] ** 2 * np.transpose(Rg, (0, 2, 1)))
+        So = Ro @ (os_[:, :, None] ** 2 * np.transpose(Ro, (0, 2, 1)))
+        err = np.linalg.norm(Sg - So, axis=(1, 2)) / np.linalg.norm(So, axis=(1, 2))
+        assert err.max() <= 1e-4, err.max()

@@ -566,7 +566,7 @@ class Tracker:
 
     def __init__(self, H: int, W: int, K, stride: int = 4, k: int = 20, mode: int = REG_ELLIPSE,
                  eps_var: float = 1e-3, z_min: float = 0.1, z_max: float = 10.0, cell0: float | None = None,
-                 levels: int = 4, params: AlignParams | None = None, device="cuda"):
+                 levels: int = 4, params: AlignParams | None = None, device="cuda", keep_corr: bool = False):
         self.H, self.W, self.stride, self.k, self.mode, self.eps = H, W, stride, k, mode, eps_var
         self.K = K if isinstance(K, Intrinsics) else Intrinsics(*K)
         self.z_min, self.z_max = z_min, z_max
@@ -584,6 +584,8 @@ class Tracker:
         self.ws_align = align_workspace(self.cap, self.device)
         self.d_T = torch.zeros(16, dtype=torch.float64, device=self.device)
         self.d_stats = torch.zeros(C.sizeof(AlignStats), dtype=torch.uint8, device=self.device)
+        # final correspondences (the overlap filter of keyframe insertion needs them; 4 B/point/iteration)
+        self.corr = torch.full((self.cap,), -1, dtype=torch.int32, device=self.device) if keep_corr else None
         self._side = torch.cuda.Stream(self.device)
         self._fork = torch.cuda.Event()
         self._join = torch.cuda.Event()
@@ -636,7 +638,7 @@ class Tracker:
             s0.wait_event(self._join)
         if events:
             events[2].record(s0)
-        align_async(self.cloud, tgt, self.d_T, self.d_stats, self.params, self.ws_align, None, s0)
+        align_async(self.cloud, tgt, self.d_T, self.d_stats, self.params, self.ws_align, self.corr, s0)
         if events:
             events[3].record(s0)
 
@@ -682,6 +684,15 @@ class Tracker:
         key = ("rows", id(tgt))
         up = lambda s0: upload_sampled_rows(self.rows, depth_host, self.stride, s0)  # noqa: E731
         return self._run(key, None, tgt, init_T, stream, up)
+
+    def track_rows(self, tgt: Target, init_T, stream=None):
+        """Whole frame from the sampled rows already in self.rows (device): (T, stats), blocking."""
+        return self._run(("rows", id(tgt)), None, tgt, init_T, stream)
+
+    def drop_graphs(self):
+        """Forget the captured frame graphs (and the targets they keep alive), e.g. after the map
+        was rebuilt."""
+        self._graphs.clear()
 
     def sequence_graph(self, tgt: Target, hist: torch.Tensor, traj: torch.Tensor, counter: torch.Tensor):
         """A graph for sequence tracking (C5): pose_predict(hist) -> the frame from self.rows ->
@@ -785,3 +796,90 @@ def track_sequence(tr: Tracker, tgt: Target, frames_rows: torch.Tensor, T0, flus
     torch.cuda.synchronize()
     ms = np.array([a.elapsed_time(b) for a, b in ev])
     return traj[: n - 1].cpu().numpy().reshape(-1, 4, 4), ms
+
+
+# ----------------------------------------------------------------------------------------------
+# N1: keyframes and map growth (P:209-214 keyframe selection by the correspondence proportion,
+# P:237 only non-overlapping Gaussians, P:250-255 scale aligning, P:262-266 forced keyframe)
+def is_keyframe(fitness: float, since_last: int, min_fitness: float = 0.95, max_gap: int = 30) -> bool:
+    """a frame whose proportion of correspondences with the map (the align fitness, R19)
+    falls below the threshold is a keyframe; if none qualified for max_gap frames since
+    the last keyframe, this one is.  The paper gives no threshold value (R29: a parameter)."""
+    return fitness < min_fitness or since_last >= max_gap
+
+
+class GaussianMap:
+    """A device-resident growing 3DGS map for tracking: rows [0, M) of means (cap,3), quats wxyz
+    (cap,4) and scales (cap,3) float32 buffers, and the G-ICP target over them (A5), rebuilt after
+    each insertion with a fixed cell size (the first build's: inserted Gaussians must not change
+    the search structure's scale)."""
+
+    def __init__(self, means: torch.Tensor, quats: torch.Tensor, scales: torch.Tensor, capacity: int,
+                 mode: int = REG_ELLIPSE, eps_var: float = 1e-3, cell: float = 0.0):
+        M = means.shape[0]
+        if capacity < M:
+            raise ValueError("capacity < initial map size")
+        dev = means.device
+        self.capacity, self.mode, self.eps = capacity, mode, eps_var
+        self.means = torch.zeros((capacity, 3), dtype=torch.float32, device=dev)
+        self.quats = torch.zeros((capacity, 4), dtype=torch.float32, device=dev)
+        self.scales = torch.zeros((capacity, 3), dtype=torch.float32, device=dev)
+        self.means[:M].copy_(means)
+        self.quats[:M].copy_(quats)
+        self.scales[:M].copy_(scales)
+        self.M = M
+        self.cell = cell
+        self.tgt = None
+        self.rebuild()
+        self.cell = float(self.tgt.st.cell)
+
+    def rebuild(self, stream=None):
+        self.tgt = build_target(self.means[:self.M], self.quats[:self.M], self.scales[:self.M], mode=self.mode,
+                                eps_var=self.eps, cell=self.cell, stream=stream)
+
+    def insert(self, cloud: Cloud, d_T: torch.Tensor, corr: torch.Tensor | None, p: float = 1.5, c: float = 1.0,
+               stream=None) -> int:
+        """Append the cloud's non-overlapping points (corr < 0; all if corr is None) as
+        scale-aligned Gaussians at the device pose d_T, then rebuild the target.  Returns how many."""
+        if self.M + cloud.cap > self.capacity:
+            raise RuntimeError(f"GaussianMap full: {self.M} + {cloud.cap} > {self.capacity}")
+        M = self.M
+        out = (self.means[M:M + cloud.cap], self.quats[M:M + cloud.cap], self.scales[M:M + cloud.cap])
+        _, _, _, d_m = export_gaussians(cloud.pos, cloud.d_n, cloud.cov_a, cloud.cov_b, T=d_T, p=p, c=c, corr=corr,
+                                        out=out, stream=stream)
+        m = int(d_m.item())
+        if m:
+            self.M += m
+            self.rebuild(stream)
+        return m
+
+
+def track_sequence_mapping(tr: Tracker, gmap: GaussianMap, frames_rows: torch.Tensor, T0, min_fitness: float = 0.95,
+                           max_gap: int = 30, p: float = 1.5, c: float = 1.0):
+    """Tracking with map growth (N1): frames 1..n-1 tracked in order from the constant-velocity
+    initial pose (host); a keyframe (is_keyframe) inserts its non-overlapping points into
+    the map (GaussianMap.insert with the tracker's final correspondences).  `tr` must be built with
+    keep_corr=True.  Returns (T_est (n-1,4,4), keyframe frame indices, Gaussians inserted per
+    keyframe, per-frame stats)."""
+    if tr.corr is None:
+        raise ValueError("track_sequence_mapping needs Tracker(keep_corr=True)")
+    n = frames_rows.shape[0]
+    prev2 = prev = np.ascontiguousarray(T0, dtype=np.float64).reshape(4, 4)
+    T_est, kfs, added, stats_all = [], [], [], []
+    since = 0
+    for i in range(1, n):
+        init = prev @ np.linalg.inv(prev2) @ prev
+        tr.rows.copy_(frames_rows[i])
+        T, st = tr.track_rows(gmap.tgt, init)
+        T_est.append(T)
+        stats_all.append(st)
+        since += 1
+        if is_keyframe(st["fitness"], since, min_fitness, max_gap):
+            m = gmap.insert(tr.cloud, tr.d_T, tr.corr, p=p, c=c)
+            kfs.append(i)
+            added.append(m)
+            since = 0
+            if m:
+                tr.drop_graphs()
+        prev2, prev = prev, T
+    return np.array(T_est), kfs, added, stats_all

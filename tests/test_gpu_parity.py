@@ -675,3 +675,44 @@ def test_export_overlap_filter(g, replica_setup):
         So = Ro @ (os_[:, :, None] ** 2 * np.transpose(Ro, (0, 2, 1)))
         err = np.linalg.norm(Sg - So, axis=(1, 2)) / np.linalg.norm(So, axis=(1, 2))
         assert err.max() <= 1e-4, err.max()
+
+
+def test_sequence_map_growth(g):
+    """N1: half of the room removed from the map; with keyframe
+    insertion the first frame becomes a keyframe, inserts exactly its unmatched points, and the
+    following frames are fully matched; without it the fitness stays ~0.5.  Tracking stays exact
+    (ATE < 1 mm) either way."""
+    seq = synth.make_sequence(1, 40, "replica", M=300_000)
+    rows = synth.render_sequence_rows(seq, DEV)
+    K = seq.K
+    d = rows[0].cpu().numpy()
+    v, u = np.nonzero(np.isfinite(d) & (d > 0.1) & (d < 10))
+    z = d[v, u]
+    P0 = np.stack([(u - K.cx) * z / K.fx, (v * seq.stride - K.cy) * z / K.fy, z], 1) @ seq.T_gt[0][:3, :3].T \
+        + seq.T_gt[0][:3, 3]
+    keep = seq.means[:, 0] < np.median(P0[:, 0])
+    M0 = int(keep.sum())
+    res = {}
+    for grow in (False, True):
+        tr = g.Tracker(K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=seq.stride, keep_corr=True,
+                       params=g.align_params(max_iters=30, max_corr_dist=0.1))
+        gm = g.GaussianMap(t(seq.means[keep]), t(seq.quats[keep]), t(seq.scales[keep]), capacity=M0 + 4 * tr.cap)
+        if grow:  # frame 1 by hand: the insertion count is the number of unmatched points
+            tr.rows.copy_(rows[1])
+            T1, st1 = tr.track_rows(gm.tgt, seq.T_gt[0])
+            unmatched = int((tr.corr[:tr.cloud.n()] < 0).sum().item())
+            assert st1["fitness"] < 0.95 and unmatched == tr.cloud.n() - st1["n_inliers"]
+            tr2 = g.Tracker(K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=seq.stride, keep_corr=True,
+                            params=g.align_params(max_iters=30, max_corr_dist=0.1))
+        T_est, kfs, added, st = g.track_sequence_mapping(tr if not grow else tr2, gm, rows, seq.T_gt[0],
+                                                         min_fitness=0.95 if grow else -1.0,
+                                                         max_gap=30 if grow else 10 ** 9)
+        err = synth.trajectory_error(T_est, seq.T_gt[1:])
+        assert err["ate_rmse_m"] < 1e-3 and err["rot_max_deg"] < 0.05, err
+        fit = np.array([s["fitness"] for s in st])
+        res[grow] = (fit, kfs, added, gm.M)
+        if grow:
+            assert kfs[0] == 1 and added[0] == unmatched and gm.M == M0 + sum(added)
+            assert fit[-10:].min() > 0.99, fit
+        else:
+            assert kfs == [] and gm.M == M0 and fit[-10:].max() < 0.7, fit

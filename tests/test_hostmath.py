@@ -96,3 +96,14 @@ def test_degenerate_and_exact_cases(hm):
     out, fl, lm = host_reg(hm, np.array([9.0, 0, 0, 4, 0, 1]), oracle.ELLIPSE)
     np.testing.assert_allclose(out, [2.25, 0, 0, 1, 0, 0.25], atol=1e-15)
     assert lm == pytest.approx(4.0, rel=1e-15)
+
+
+def test_keyframe_policy():
+    """P:213 (proportion of correspondences below the threshold) and P:264-265 (forced at the
+    30th frame since the last keyframe)."""
+    import paper_2403_12550_b200 as g
+
+    assert g.is_keyframe(0.80, 1, min_fitness=0.9)
+    assert not g.is_keyframe(0.95, 1, min_fitness=0.9)
+    assert not g.is_keyframe(0.9, 29, min_fitness=0.9, max_gap=30)  # threshold is strict
+    assert g.is_keyframe(1.0, 30, min_fitness=0.9, max_gap=30)

@@ -335,6 +335,38 @@ def bench_gpu(args):
                     "ms_per_frame_mean": float(ms_s.mean()), **synth.trajectory_error(T_est, sq.T_gt[1:])}
         del rows_all, tr_s, tgt_s
 
+    # N2 throughput mode: B copies of the workload frame (B different initial poses) per step —
+    # concurrent A1-A4 streams + one k_align_batch launch, one graph replay, L2 flushed per step
+    batch_line = None
+    if args.batch > 0:
+        import synth
+
+        B = args.batch
+        bt = g.BatchTracker(B, K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=w.stride, params=params, device=dev)
+        bt.rows.copy_(torch.from_numpy(w.depth[::w.stride]).to(dev).expand(B, -1, -1))
+        init_b = np.stack([synth.perturb_pose(w.T_gt, 500 + b, 2.0, 0.03) for b in range(B)])
+        bt.track_rows(tgt, init_b)
+        gb = bt.graph(tgt)
+        Tb0 = torch.from_numpy(init_b.reshape(B, 16)).to(dev)
+        sb = torch.cuda.current_stream(dev)
+        nb = max(10, min(args.steps, 50))
+        evb = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nb)]
+        for e0, e1 in evb:
+            flush.zero_()
+            bt.d_T.copy_(Tb0)
+            e0.record(sb)
+            gb.replay(sb)
+            e1.record(sb)
+        torch.cuda.synchronize()
+        b_total = max_over_ranks(sum(a.elapsed_time(b) for a, b in evb), dist, dev)
+        Tb, stb = bt.track_rows(tgt, init_b)
+        batch_line = {"workload": f"N2: {B} copies of the workload frame per step from {B} initial poses, one "
+                                  "k_align_batch launch (G/B blocks per frame), A1-A4 on B concurrent streams",
+                      "B": B, "aligns_per_s": job_throughput(nb * B, ws, b_total), "ms_per_step": b_total / nb,
+                      "iters": [s_["iters"] for s_ in stb],
+                      "max_trans_err_m": float(max(np.abs(Tb[b][:3, 3] - w.T_gt[:3, 3]).max() for b in range(B)))}
+        del bt
+
     # kNN-cov Mpts/s over a 4e6-point map (C4), kernel stage only
     knn_mpts = None
     if not args.no_c4 and rank == 0:
@@ -411,6 +443,8 @@ def bench_gpu(args):
     }
     if seq_line is not None:
         line["sequence"] = seq_line
+    if batch_line is not None:
+        line["batched"] = batch_line
     if knn_mpts is not None:
         line["knn_cov_mpts_s"] = knn_mpts
         line["knn_cov_4M_ms"] = knn4_ms
@@ -432,6 +466,7 @@ def main():
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--seq-frames", type=int, default=120, help="C5 sequence frames per rank (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch", type=int, default=4, help="N2 frames per batched step (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return bench_reference(args)

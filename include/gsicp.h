@@ -221,6 +221,23 @@ gsicp_status gsicp_align_async(const gsicp_cloud *src, const gsicp_target *tgt, 
                                const gsicp_align_params *prm, gsicp_align_stats *d_stats, int32_t *corr_out,
                                void *ws, size_t ws_bytes, void *stream);
 
+/* N2 frame batch (the throughput mode): B independent frames aligned against the same target in
+ * ONE cooperative launch — each frame runs the GN loop of gsicp_align_async on G/B co-resident
+ * blocks with its own grid barrier, partials and convergence test, so the per-iteration latency
+ * (barrier, reduction, solve) is paid once for the batch.  Per-frame results equal
+ * gsicp_align_async's up to the summation grouping of the H/b partials (the block count differs).
+ *  srcs    host array [B] of clouds;  B in [1, gsicp_align_batch_max()];
+ *  d_T     [dev] double[B*16]: frame f's pose (row-major 4x4) at d_T + 16 f, read and updated;
+ *  d_stats [dev] gsicp_align_stats[B];
+ *  corr_out NULL or host array [B] of nullable [dev] int32[cap_f] (final correspondences);
+ *  ws      host array [B] of distinct align workspaces (gsicp_align_workspace_size(cap_f) each,
+ *          ws_bytes = the smallest of their sizes).  Seeds (gsicp_align_seed) are not used.
+ *  Errors: INVALID_ARGUMENT, WORKSPACE_TOO_SMALL, CUDA.  Asynchronous, graph-capturable. */
+int32_t gsicp_align_batch_max(void);
+gsicp_status gsicp_align_batch_async(const gsicp_cloud *srcs, int32_t B, const gsicp_target *tgt, double *d_T,
+                                     const gsicp_align_params *prm, gsicp_align_stats *d_stats,
+                                     int32_t *const *corr_out, void *const *ws, size_t ws_bytes, void *stream);
+
 /* Iteration-0 correspondences ahead of the GN loop (A6 at the initial pose, P:95 / R15): for
  * every source point the exact 1-NN of fl32(K3(T0, x_i)) among the target means, written into
  * the align workspace `ws`.  Reads only src->pos / src->d_n (not the covariances), the target and

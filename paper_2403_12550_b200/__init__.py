@@ -116,6 +116,10 @@ def lib():
         L.gsicp_pose_predict.argtypes = [P, P, P]
         L.gsicp_pose_push.argtypes = [P, P, P, P, i32, P]
         L.gsicp_export_gaussians.argtypes = [P, P, P, P, i32, P, C.c_double, C.c_double, P, P, P, P, P, P, sz, P]
+        L.gsicp_align_batch_async.argtypes = [P, i32, P, P, P, P, P, P, sz, P]
+        L.gsicp_align_batch_async.restype = i32
+        L.gsicp_align_batch_max.argtypes = []
+        L.gsicp_align_batch_max.restype = i32
         L.gsicp_export_workspace_size.argtypes = [i32]
         L.gsicp_export_workspace_size.restype = sz
         for name in ("gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_gaussians"):
@@ -150,6 +154,7 @@ EXPORTED = [
     "gsicp_debug_align_timeline", "gsicp_debug_align_counters", "gsicp_debug_kernel_timer",
     "gsicp_debug_kernel_time", "gsicp_graph_instantiate", "gsicp_graph_launch", "gsicp_graph_destroy",
     "gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_workspace_size", "gsicp_export_gaussians",
+    "gsicp_align_batch_max", "gsicp_align_batch_async",
 ]
 
 KT_KNN_SEARCH, KT_ALIGN, KT_SEED, KT_BP, KT_COVS, KT_WIDE, KT_TAIL = 0, 1, 2, 3, 4, 5, 6
@@ -462,6 +467,22 @@ def align_async(src: Cloud, tgt: Target, d_T: torch.Tensor, d_stats: torch.Tenso
     cs = src.c_struct()
     _check(lib().gsicp_align_async(C.byref(cs), C.byref(tgt.st), _ptr(d_T), C.byref(params), _ptr(d_stats),
                                    _ptr(corr_out), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def align_batch_async(srcs: list, tgt: Target, d_T: torch.Tensor, d_stats: torch.Tensor,
+                      params: AlignParams | None = None, wss: list | None = None, corr_outs: list | None = None,
+                      stream=None):
+    """N2: B frames against one target in one launch.  d_T (B, 16) float64 and d_stats
+    (B, sizeof(gsicp_align_stats)) uint8 on the device, read / written per frame; wss: B distinct
+    align workspaces."""
+    B = len(srcs)
+    params = params or align_params()
+    wss = wss if wss is not None else [align_workspace(c.cap, c.pos.device) for c in srcs]
+    cs = (_Cloud * B)(*[c.c_struct() for c in srcs])
+    ws_arr = (C.c_void_p * B)(*[_ptr(w) for w in wss])
+    corr_arr = (C.c_void_p * B)(*[_ptr(c) for c in corr_outs]) if corr_outs is not None else None
+    _check(lib().gsicp_align_batch_async(cs, B, C.byref(tgt.st), _ptr(d_T), C.byref(params), _ptr(d_stats), corr_arr,
+                                         ws_arr, min(w.numel() for w in wss), _stream(stream)))
 
 
 def align_seed(src: Cloud, tgt: Target, d_T: torch.Tensor, params: AlignParams | None = None,
@@ -883,3 +904,77 @@ def track_sequence_mapping(tr: Tracker, gmap: GaussianMap, frames_rows: torch.Te
                 tr.drop_graphs()
         prev2, prev = prev, T
     return np.array(T_est), kfs, added, stats_all
+
+
+class BatchTracker:
+    """N2 throughput mode: B independent frames per step against one target.  Each frame's A1 and
+    A2-A4 run on a stream of its own (concurrently), then ONE k_align_batch launch runs the B GN
+    loops side by side (gsicp_align_batch_async); the whole step is one graph replay.  Frames are
+    written into self.rows[b] (sampled depth rows, as Tracker.rows)."""
+
+    def __init__(self, B: int, H: int, W: int, K, stride: int = 4, params: AlignParams | None = None,
+                 device="cuda", **kw):
+        if not 1 <= B <= int(lib().gsicp_align_batch_max()):
+            raise ValueError(f"B must be in [1, {lib().gsicp_align_batch_max()}]")
+        self.B = B
+        self.params = params or align_params()
+        self.device = torch.device(device)
+        self.trs = [Tracker(H, W, K, stride=stride, params=self.params, device=device, **kw) for _ in range(B)]
+        self.rows = torch.empty((B,) + tuple(self.trs[0].rows.shape), dtype=torch.float32, device=self.device)
+        self.d_T = torch.zeros((B, 16), dtype=torch.float64, device=self.device)
+        self.d_stats = torch.zeros((B, C.sizeof(AlignStats)), dtype=torch.uint8, device=self.device)
+        self._streams = [torch.cuda.Stream(self.device) for _ in range(B)]
+        self._fork = torch.cuda.Event()
+        self._joins = [torch.cuda.Event() for _ in range(B)]
+        self._graphs = {}
+        self._T_host = torch.zeros((B, 16), dtype=torch.float64).pin_memory()
+        self._T_out = torch.zeros((B, 16), dtype=torch.float64).pin_memory()
+        self._st_out = torch.zeros((B, C.sizeof(AlignStats)), dtype=torch.uint8).pin_memory()
+
+    def step_async(self, tgt: Target, stream=None):
+        s0 = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self._fork.record(s0)
+        for b, tr in enumerate(self.trs):
+            sb = self._streams[b]
+            sb.wait_event(self._fork)
+            tr._backproject(None, sb, self.rows[b])
+            tr._covariances(sb)
+            self._joins[b].record(sb)
+            s0.wait_event(self._joins[b])
+        align_batch_async([tr.cloud for tr in self.trs], tgt, self.d_T, self.d_stats, self.params,
+                          [tr.ws_align for tr in self.trs], None, s0)
+
+    def graph(self, tgt: Target):
+        hit = self._graphs.get(id(tgt))
+        if hit is not None:
+            return hit[0]
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            T0 = self.d_T.clone()
+            self.step_async(tgt, s)  # one run outside the capture (lazy library state)
+            self.d_T.copy_(T0)
+        s.synchronize()
+        g = FrameGraph()
+        with g.capture(s):
+            self.step_async(tgt, s)
+        self._graphs[id(tgt)] = (g, tgt)
+        return g
+
+    def track_rows(self, tgt: Target, init_T, stream=None):
+        """The B frames in self.rows from the B initial poses init_T (B, 4, 4): (T (B, 4, 4),
+        [stats] * B), blocking."""
+        s0 = stream if stream is not None else torch.cuda.current_stream(self.device)
+        g = self.graph(tgt)
+        self._T_host.numpy()[:] = np.ascontiguousarray(init_T, dtype=np.float64).reshape(self.B, 16)
+        with torch.cuda.stream(s0):
+            self.d_T.copy_(self._T_host, non_blocking=True)
+            g.replay(s0)
+            self._T_out.copy_(self.d_T, non_blocking=True)
+            self._st_out.copy_(self.d_stats, non_blocking=True)
+        s0.synchronize()
+        raw = self._st_out.numpy()
+        stats = [AlignStats.from_buffer_copy(raw[b].tobytes()[:C.sizeof(AlignStats)]).as_dict() for b in range(self.B)]
+        for st in stats:
+            _check(st["status"], _ALIGN_ALLOW)
+        return self._T_out.numpy().reshape(self.B, 4, 4).copy(), stats

@@ -771,8 +771,9 @@ __global__ void k_align_init(int32_t *corr_ws, int cap, unsigned int *barrier) {
     if (i == 0) *barrier = 0u;
 }
 
-__global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
-    pdl_wait();  // (no early launch of dependents: they must not take SMs from this cooperative grid)
+// The GN loop of one frame on blocks [0, G) of its own (bid = this block's index among them):
+// k_align runs one frame on the whole grid, k_align_batch several frames side by side.
+__device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, const int G) {
     __shared__ double sT[12];
     __shared__ double sRed[kWarps][kPad];
     __shared__ double sAcc[kPad];
@@ -788,10 +789,9 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     __shared__ float4 sQp[kT];
     __shared__ float sQd2[kT];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int G = gridDim.x;
     const int n = *a.d_n;
     if (tid < 12) sT[tid] = a.d_T[tid];
-    if (a.timeline && blockIdx.x == 0 && tid == 0 && a.timeline_cap > 0) a.timeline[0] = globaltimer_ns();
+    if (a.timeline && bid == 0 && tid == 0 && a.timeline_cap > 0) a.timeline[0] = globaltimer_ns();
     __shared__ int sSeeded;
     if (tid == 0) {
         load_cell_index(a, sIdx, sBox);
@@ -808,7 +808,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     // search — however small the frame is (one block per kT points left most SMs idle and piled
     // the warp searches of a noisy frame onto a few blocks)
     const int P = min(kT, (n + G - 1) / G);
-    const int i0 = P == kT ? blockIdx.x * kT + tid : blockIdx.x * P + tid;
+    const int i0 = P == kT ? bid * kT + tid : bid * P + tid;
     const bool has0 = tid < P && i0 < n;
     float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), ca0 = x0, cb0 = x0;
     if (has0) {
@@ -833,7 +833,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             if (a.timeline) {
                 __syncthreads();
                 const long long idx = 1 + (long long)a.max_iters * (G + 1) + (long long)it * 8 + p;
-                if (blockIdx.x == 0 && tid == 0 && idx < a.timeline_cap) a.timeline[idx] = globaltimer_ns();
+                if (bid == 0 && tid == 0 && idx < a.timeline_cap) a.timeline[idx] = globaltimer_ns();
             }
         };
         stamp(0);
@@ -841,12 +841,12 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         // ------------------------------------------------------------ A6: correspondences
         double q0r = 0.0, q1r = 0.0, q2r = 0.0;
         // diagnostic sub-phase clocks of warp 0 of block 0 (SM cycles)
-        const bool sub = a.timeline && blockIdx.x == 0 && tid == 0;
+        const bool sub = a.timeline && bid == 0 && tid == 0;
         const long long sub_base = 1 + (long long)a.max_iters * (G + 9) + (long long)it * 8;
         auto sub_stamp = [&](int k) {
             if (sub && sub_base + k < a.timeline_cap) a.timeline[sub_base + k] = clock64();
         };
-        const long long lane_t0 = a.timeline && blockIdx.x == 0 ? clock64() : 0;
+        const long long lane_t0 = a.timeline && bid == 0 ? clock64() : 0;
         int path_code = 0;
         if (has0) {
             sub_stamp(0);
@@ -926,7 +926,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
             ++dbg_its;
             m0 = nn;
         }
-        if (a.timeline && blockIdx.x == 0) {  // diagnostic: slowest lane of each warp of block 0
+        if (a.timeline && bid == 0) {  // diagnostic: slowest lane of each warp of block 0
             long long d = has0 ? clock64() - lane_t0 : 0;
             int code = path_code;
 #pragma unroll
@@ -1051,20 +1051,20 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         if (tid < kAlignTerms) {
             double s = 0.0;
             for (int w = 0; w < kWarps; ++w) s += sRed[w][tid];
-            part[(size_t)blockIdx.x * kPad + tid] = s;
+            part[(size_t)bid * kPad + tid] = s;
         }
         // ------------------------------------------------------------ grid barrier
         __syncthreads();
         if (tid == 0) {
             const long long rec = 1 + (long long)it * (G + 1);
-            if (a.timeline && rec + G < a.timeline_cap) a.timeline[rec + blockIdx.x] = globaltimer_ns();
+            if (a.timeline && rec + G < a.timeline_cap) a.timeline[rec + bid] = globaltimer_ns();
             __threadfence();
             atomicAdd(a.barrier, 1u);
             const unsigned int target = (unsigned int)(it + 1) * (unsigned int)G;
             while (ld_acquire(a.barrier) < target) {
             }
             __threadfence();
-            if (a.timeline && blockIdx.x == 0 && rec + G < a.timeline_cap) a.timeline[rec + G] = globaltimer_ns();
+            if (a.timeline && bid == 0 && rec + G < a.timeline_cap) a.timeline[rec + G] = globaltimer_ns();
         }
         __syncthreads();
         stamp(3);
@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         if (sDone) break;
     }
     if (a.debug && has0) a.debug[i0] = make_int4(dbg_slow, dbg_reuse, dbg_graph, dbg_its);
-    if (blockIdx.x == 0 && tid == 0) {
+    if (bid == 0 && tid == 0) {
         if (!a.linearize_only) {
             for (int k = 0; k < 12; ++k) a.d_T[k] = sT[k];
             a.d_T[12] = 0.0; a.d_T[13] = 0.0; a.d_T[14] = 0.0; a.d_T[15] = 1.0;
@@ -1125,6 +1125,34 @@ __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
         st.status = status;
         *a.d_stats = st;
     }
+}
+
+__global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
+    pdl_wait();  // (no early launch of dependents: they must not take SMs from this cooperative grid)
+    align_body(a, blockIdx.x, gridDim.x);
+}
+
+// N2 frame batch: frame f = blockIdx.x / Gf runs on blocks [f Gf, (f+1) Gf) with its own
+// workspace (partials, barrier, match cache), pose and stats; the target is shared.  The frames'
+// arguments travel in the launch's parameter space (graph-capturable, no host->device copy).
+constexpr int kMaxAlignBatch = 16;
+struct AlignBatch {
+    AlignArgs f[kMaxAlignBatch];
+};
+
+__global__ void __launch_bounds__(kT, 1) k_align_batch(const __grid_constant__ AlignBatch b, int Gf) {
+    pdl_wait();
+    const int f = blockIdx.x / Gf;
+    align_body(b.f[f], blockIdx.x - f * Gf, Gf);
+}
+
+__global__ void k_align_init_batch(const __grid_constant__ AlignBatch b) {
+    const AlignArgs &a = b.f[blockIdx.y];
+    pdl_wait();
+    pdl_launch_dependents();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < a.cap) a.corr_ws[i] = -1;
+    if (i == 0) *a.barrier = 0u;
 }
 
 // Co-resident grid for the cooperative launch (0 if the kernel cannot be resident at all).
@@ -1310,6 +1338,61 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
     ktimer_mark(KT_ALIGN, true, s);
     if (e != cudaSuccess) {
         set_error("k_align launch: %s", cudaGetErrorString(e));
+        return e;
+    }
+    note_launch(2);
+    return cudaSuccess;
+}
+
+int align_batch_max() { return kMaxAlignBatch; }
+
+// N2: B frames against one target in one cooperative launch (G / B co-resident blocks per frame).
+cudaError_t align_batch_launch(const gsicp_cloud *srcs, int B, const gsicp_target &tgt, double *d_T,
+                               const gsicp_align_params &p, gsicp_align_stats *d_stats, int32_t *const *corr_out,
+                               void *const *ws, cudaStream_t s) {
+    static thread_local AlignBatch hb;  // host staging of the launch parameter (copied at launch)
+    int cap_max = 1;
+    for (int f = 0; f < B; ++f) {
+        AlignWs w = align_carve(ws[f], srcs[f].cap);
+        hb.f[f] = make_args(srcs[f], tgt, d_T + 16 * (size_t)f, p, d_stats + f, corr_out ? corr_out[f] : nullptr, 0,
+                            0.f, w);
+        hb.f[f].timeline = nullptr;  // the diagnostics describe single-frame launches
+        hb.f[f].timeline_cap = 0;
+        hb.f[f].debug = nullptr;
+        if (srcs[f].cap > cap_max) cap_max = srcs[f].cap;
+    }
+    g_seed_ws = nullptr;  // seeds are single-frame only
+    launch_pdl(k_align_init_batch, dim3(blocks_for(cap_max, 256), B), dim3(256), 0, s, hb);
+    GSICP_LAUNCH_CHECK("k_align_init_batch");
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        int v = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_align_batch, kT, 0) != cudaSuccess) v = 0;
+        per_sm = v;
+    }
+    int G = per_sm * num_sms();
+    if (G > kMaxAlignGrid) G = kMaxAlignGrid;
+    const int Gf = G / B;
+    if (Gf < 1) {
+        set_error("k_align_batch: %d frames do not fit the co-resident grid (%d blocks)", B, G);
+        return cudaErrorCooperativeLaunchTooLarge;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributePriority;
+    at[1].val.priority = launch_priority(true);
+    cfg.gridDim = dim3(Gf * B);
+    cfg.blockDim = dim3(kT);
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    ktimer_mark(KT_ALIGN, false, s);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_align_batch, hb, Gf);
+    ktimer_mark(KT_ALIGN, true, s);
+    if (e != cudaSuccess) {
+        set_error("k_align_batch launch: %s", cudaGetErrorString(e));
         return e;
     }
     note_launch(2);

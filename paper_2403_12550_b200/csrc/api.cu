@@ -74,6 +74,10 @@ cudaError_t export_launch(const float4 *pos, const float4 *cov_a, const float4 *
                           const double *d_T, double p, double c, const int32_t *corr, float *means, float *quats,
                           float *scales, int32_t *d_m, void *ws, cudaStream_t s);
 size_t align_ws_bytes(int cap);
+int align_batch_max();
+cudaError_t align_batch_launch(const gsicp_cloud *srcs, int B, const gsicp_target &tgt, double *d_T,
+                               const gsicp_align_params &p, gsicp_align_stats *d_stats, int32_t *const *corr_out,
+                               void *const *ws, cudaStream_t s);
 double *align_ws_T(void *ws);
 gsicp_align_stats *align_ws_stats(void *ws);
 double *align_ws_lin(void *ws);
@@ -458,6 +462,28 @@ gsicp_status gsicp_align_async(const gsicp_cloud *src, const gsicp_target *tgt, 
     return cuda_status(align_launch(*src, *tgt, d_T_inout, *prm, d_stats, corr_out, 0, 0.f, ws, (cudaStream_t)stream),
                        "align");
 }
+
+int32_t gsicp_align_batch_max(void) { return align_batch_max(); }
+
+gsicp_status gsicp_align_batch_async(const gsicp_cloud *srcs, int32_t B, const gsicp_target *tgt, double *d_T,
+                                     const gsicp_align_params *prm, gsicp_align_stats *d_stats,
+                                     int32_t *const *corr_out, void *const *ws, size_t ws_bytes, void *stream) {
+    g_err[0] = 0;
+    if (!srcs || !ws || !d_T || !d_stats) BAD("align_batch: null pointer");
+    if (B < 1 || B > align_batch_max()) BAD("align_batch: B must be in [1, %d]", align_batch_max());
+    gsicp_status st = check_target(tgt);
+    if (st != GSICP_OK) return st;
+    if ((st = check_params(prm)) != GSICP_OK) return st;
+    for (int f = 0; f < B; ++f) {
+        if ((st = check_cloud(srcs + f, "align_batch src")) != GSICP_OK) return st;
+        if ((st = check_ws(ws[f], ws_bytes, align_ws_bytes(srcs[f].cap))) != GSICP_OK) return st;
+        for (int g2 = 0; g2 < f; ++g2)
+            if (ws[g2] == ws[f]) BAD("align_batch: every frame needs its own workspace");
+    }
+    return cuda_status(align_batch_launch(srcs, B, *tgt, d_T, *prm, d_stats, corr_out, ws, (cudaStream_t)stream),
+                       "align_batch");
+}
+
 
 gsicp_status gsicp_align_seed(const gsicp_cloud *src, const gsicp_target *tgt, const double *d_T,
                               const gsicp_align_params *prm, void *ws, size_t ws_bytes, void *stream) {

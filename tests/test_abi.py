@@ -124,3 +124,11 @@ def test_new_entry_points_reject_bad_arguments(g):
     st = E(fake, fake, fake, fake, 100000, None, 1.5, 1.0, fake, fake, fake, fake, fake, C.c_void_p(0x100000), 16, None)
     assert st == g.ERR_WORKSPACE_TOO_SMALL
     assert L.gsicp_export_workspace_size(100000) >= 4 * (100000 // 256)
+    Bmax = L.gsicp_align_batch_max()
+    assert Bmax >= 8
+    st = L.gsicp_align_batch_async(fake, 0, fake, fake, fake, fake, None, fake, 1 << 20, None)
+    assert st == g.ERR_INVALID_ARGUMENT and b"B must be" in L.gsicp_last_error()
+    st = L.gsicp_align_batch_async(fake, Bmax + 1, fake, fake, fake, fake, None, fake, 1 << 20, None)
+    assert st == g.ERR_INVALID_ARGUMENT
+    assert L.gsicp_align_batch_async(None, 2, fake, fake, fake, fake, None, fake, 1 << 20, None) \
+        == g.ERR_INVALID_ARGUMENT

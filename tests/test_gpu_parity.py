@@ -716,3 +716,38 @@ def test_sequence_map_growth(g):
             assert fit[-10:].min() > 0.99, fit
         else:
             assert kfs == [] and gm.M == M0 and fit[-10:].max() < 0.7, fit
+
+
+def test_align_batch(g):
+    """N2: B = 4 frames of a sequence in one BatchTracker step (concurrent A1-A4 streams + one
+    k_align_batch launch) give the poses single-frame tracking gives (same algorithm; only the
+    grouping of the H/b partial sums differs) and, for a frame checked against the oracle from the
+    same initial pose, the oracle's pose within 1e-5 rad / 1e-5 m."""
+    seq = synth.make_sequence(2, 5, "replica", M=300_000)
+    rows = synth.render_sequence_rows(seq, DEV)
+    K = seq.K
+    B = 4
+    prm = g.align_params(max_iters=30, max_corr_dist=0.1)
+    tgt = g.build_target(t(seq.means), t(seq.quats), t(seq.scales))
+    init = np.stack([synth.perturb_pose(seq.T_gt[1 + b], 20 + b, 2.0, 0.03) for b in range(B)])
+    bt = g.BatchTracker(B, K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=seq.stride, params=prm)
+    bt.rows.copy_(rows[1:1 + B])
+    Tb, stb = bt.track_rows(tgt, init)
+    Tb2, _ = bt.track_rows(tgt, init)  # deterministic replay
+    np.testing.assert_array_equal(Tb, Tb2)
+    tr = g.Tracker(K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=seq.stride, params=prm)
+    for b in range(B):
+        tr.rows.copy_(rows[1 + b])
+        Ts, sts = tr.track_rows(tgt, init[b])
+        assert rot_angle(Tb[b][:3, :3], Ts[:3, :3]) < 1e-6 and np.abs(Tb[b][:3, 3] - Ts[:3, 3]).max() < 1e-6
+        assert stb[b]["n_inliers"] == sts["n_inliers"] and stb[b]["status"] == sts["status"]
+        assert rot_angle(Tb[b][:3, :3], seq.T_gt[1 + b][:3, :3]) < math.radians(0.05)
+    # oracle for frame 0 of the batch, from the same initial pose
+    d = rows[1].cpu().numpy()
+    depth = np.full((K.H, K.W), np.nan, np.float32)
+    depth[::seq.stride] = d
+    xyz, _ = oracle.backproject(depth, K.fx, K.fy, K.cx, K.cy, seq.stride)
+    ocs = oracle.covariances(xyz)["cov"]
+    oct_, _ = oracle.target_from_map(seq.quats, seq.scales)
+    res = oracle.align(xyz, ocs, seq.means, oct_, init[0], max_iters=30, max_corr_dist=0.1)
+    assert rot_angle(Tb[0][:3, :3], res["T"][:3, :3]) < 1e-5 and np.abs(Tb[0][:3, 3] - res["T"][:3, 3]).max() < 1e-5

@@ -466,7 +466,7 @@ def main():
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--seq-frames", type=int, default=120, help="C5 sequence frames per rank (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--batch", type=int, default=4, help="N2 frames per batched step (0: skip)")
+    ap.add_argument("--batch", type=int, default=8, help="N2 frames per batched step (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return bench_reference(args)

@@ -231,7 +231,8 @@ gsicp_status gsicp_align_async(const gsicp_cloud *src, const gsicp_target *tgt, 
  *  d_stats [dev] gsicp_align_stats[B];
  *  corr_out NULL or host array [B] of nullable [dev] int32[cap_f] (final correspondences);
  *  ws      host array [B] of distinct align workspaces (gsicp_align_workspace_size(cap_f) each,
- *          ws_bytes = the smallest of their sizes).  Seeds (gsicp_align_seed) are not used.
+ *          ws_bytes = the smallest of their sizes).  Seeds (gsicp_align_seed) computed on a
+ *          frame's workspace at its current pose are used as in gsicp_align_async.
  *  Errors: INVALID_ARGUMENT, WORKSPACE_TOO_SMALL, CUDA.  Asynchronous, graph-capturable. */
 int32_t gsicp_align_batch_max(void);
 gsicp_status gsicp_align_batch_async(const gsicp_cloud *srcs, int32_t B, const gsicp_target *tgt, double *d_T,

@@ -938,6 +938,9 @@ class BatchTracker:
             sb = self._streams[b]
             sb.wait_event(self._fork)
             tr._backproject(None, sb, self.rows[b])
+            # iteration-0 correspondences at the frame's pose (needs only the points), then A2-A4;
+            # the frames' streams run concurrently
+            align_seed(tr.cloud, tgt, self.d_T[b], self.params, tr.ws_align, sb)
             tr._covariances(sb)
             self._joins[b].record(sb)
             s0.wait_event(self._joins[b])

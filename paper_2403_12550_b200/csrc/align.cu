@@ -997,8 +997,15 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
                 nn.slot = slot;
                 nn.best = pack_ki(canon_key(qx, qy, qz, nn.p.x, nn.p.y, nn.p.z), (uint32_t)__float_as_int(nn.p.w));
             }
-            if (!(it == 0 && sSeeded))
-                nn_search(a, sIdx, sBox, qc, sIdx.one(qc.c[0], qc.c[1], qc.c[2]), qx, qy, qz, nn, false);
+            if (!(it == 0 && sSeeded)) {
+                // the kNN-graph certificate from the previous match first (as for resident points)
+                bool exact = false;
+                if (nn.slot >= 0 && a.nbr) {
+                    float d2 = 0.f;
+                    exact = graph_nn(a, qx, qy, qz, nn, d2);
+                }
+                if (!exact) nn_search(a, sIdx, sBox, qc, sIdx.one(qc.c[0], qc.c[1], qc.c[2]), qx, qy, qz, nn, false);
+            }
             a.corr_ws[i] = (nn.slot >= 0 && ki_key(nn.best) < a.r2) ? nn.slot : -2 - nn.slot;
         }
         sub_stamp(5);
@@ -1266,10 +1273,40 @@ static AlignArgs make_args(const gsicp_cloud &src, const gsicp_target &tgt, doub
 // Seeds are single-use and bound to the workspace and the host thread: gsicp_align_seed records a
 // ticket here, the next align / linearize launch on the same workspace expects it (and clears it),
 // so stale seeds (another cloud, pose or workspace) are never used.
-thread_local void *g_seed_ws = nullptr;
-thread_local const void *g_seed_src = nullptr, *g_seed_tgt = nullptr;
-thread_local double g_seed_ticket = 0.0;
+// One entry per workspace with pending seeds (a frame batch seeds several workspaces).
+struct SeedTicket {
+    void *ws = nullptr;
+    const void *src = nullptr, *tgt = nullptr;
+    double ticket = 0.0;
+};
+constexpr int kSeedTickets = 32;
+thread_local SeedTicket g_seed[kSeedTickets];
 thread_local double g_seed_counter = 0.0;
+
+static void seed_record(void *ws, const void *src, const void *tgt, double ticket) {
+    int slot = -1;
+    for (int k = 0; k < kSeedTickets && slot < 0; ++k)
+        if (g_seed[k].ws == ws) slot = k;
+    for (int k = 0; k < kSeedTickets && slot < 0; ++k)
+        if (g_seed[k].ws == nullptr) slot = k;
+    if (slot < 0) {  // table full: evict the oldest ticket (its seeds are then simply not used)
+        slot = 0;
+        for (int k = 1; k < kSeedTickets; ++k)
+            if (g_seed[k].ticket < g_seed[slot].ticket) slot = k;
+    }
+    g_seed[slot] = SeedTicket{ws, src, tgt, ticket};
+}
+
+// the ticket the next launch on `ws` expects (0: none), consumed
+static double seed_take(void *ws, const void *src, const void *tgt) {
+    for (int k = 0; k < kSeedTickets; ++k)
+        if (g_seed[k].ws == ws) {
+            const double t = (g_seed[k].src == src && g_seed[k].tgt == tgt) ? g_seed[k].ticket : 0.0;
+            g_seed[k] = SeedTicket{};
+            return t;
+        }
+    return 0.0;
+}
 
 cudaError_t align_seed_launch(const gsicp_cloud &src, const gsicp_target &tgt, const double *d_T,
                               const gsicp_align_params &p, void *ws, cudaStream_t s) {
@@ -1277,10 +1314,7 @@ cudaError_t align_seed_launch(const gsicp_cloud &src, const gsicp_target &tgt, c
     AlignArgs a = make_args(src, tgt, const_cast<double *>(d_T), p, nullptr, nullptr, 0, 0.f, w);
     g_seed_counter += 1.0;
     a.seed_ticket = g_seed_counter;
-    g_seed_ws = ws;
-    g_seed_src = src.pos;
-    g_seed_tgt = tgt.pos;
-    g_seed_ticket = a.seed_ticket;
+    seed_record(ws, src.pos, tgt.pos, a.seed_ticket);
     cudaError_t e = cudaMemsetAsync(w.seed_qn, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) {
         set_error("align_seed memset: %s", cudaGetErrorString(e));
@@ -1307,8 +1341,7 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
                          int linearize_only, float r_lin, void *ws, cudaStream_t s) {
     AlignWs w = align_carve(ws, src.cap);
     AlignArgs a = make_args(src, tgt, d_T_inout, p, d_stats, corr_out, linearize_only, r_lin, w);
-    a.seed_ticket = (g_seed_ws == ws && g_seed_src == src.pos && g_seed_tgt == tgt.pos) ? g_seed_ticket : 0.0;
-    g_seed_ws = nullptr;
+    a.seed_ticket = seed_take(ws, src.pos, tgt.pos);
     launch_pdl(k_align_init, dim3(blocks_for(src.cap > 0 ? src.cap : 1, 256)), dim3(256), 0, s, w.corr_ws, src.cap,
                w.barrier);
     GSICP_LAUNCH_CHECK("k_align_init");
@@ -1359,9 +1392,9 @@ cudaError_t align_batch_launch(const gsicp_cloud *srcs, int B, const gsicp_targe
         hb.f[f].timeline = nullptr;  // the diagnostics describe single-frame launches
         hb.f[f].timeline_cap = 0;
         hb.f[f].debug = nullptr;
+        hb.f[f].seed_ticket = seed_take(ws[f], srcs[f].pos, tgt.pos);
         if (srcs[f].cap > cap_max) cap_max = srcs[f].cap;
     }
-    g_seed_ws = nullptr;  // seeds are single-frame only
     launch_pdl(k_align_init_batch, dim3(blocks_for(cap_max, 256), B), dim3(256), 0, s, hb);
     GSICP_LAUNCH_CHECK("k_align_init_batch");
     static int per_sm = -1;

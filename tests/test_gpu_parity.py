@@ -751,3 +751,37 @@ def test_align_batch(g):
     oct_, _ = oracle.target_from_map(seq.quats, seq.scales)
     res = oracle.align(xyz, ocs, seq.means, oct_, init[0], max_iters=30, max_corr_dist=0.1)
     assert rot_angle(Tb[0][:3, :3], res["T"][:3, :3]) < 1e-5 and np.abs(Tb[0][:3, 3] - res["T"][:3, 3]).max() < 1e-5
+
+
+def test_align_batch_single_and_ragged(g):
+    """B = 1 runs the same blocks and summation as the single-frame kernel: bitwise-identical pose
+    and stats.  A ragged batch (one frame with a third of its depth missing, so fewer points) gives
+    every frame its single-frame pose."""
+    seq = synth.make_sequence(3, 4, "replica", M=300_000)
+    rows = synth.render_sequence_rows(seq, DEV)
+    K = seq.K
+    prm = g.align_params(max_iters=30, max_corr_dist=0.1)
+    tgt = g.build_target(t(seq.means), t(seq.quats), t(seq.scales))
+    tr = g.Tracker(K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=seq.stride, params=prm)
+    init1 = synth.perturb_pose(seq.T_gt[1], 40, 2.0, 0.03)
+    tr.rows.copy_(rows[1])
+    Ts, sts = tr.track_rows(tgt, init1)
+    b1 = g.BatchTracker(1, K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=seq.stride, params=prm)
+    b1.rows.copy_(rows[1:2])
+    Tb, stb = b1.track_rows(tgt, init1[None])
+    np.testing.assert_array_equal(Tb[0], Ts)
+    assert stb[0] == sts
+    rr = rows[1:4].clone()
+    rr[2, : rr.shape[1] // 3] = 0.0  # invalid depth: a third fewer points in frame 3
+    init = np.stack([synth.perturb_pose(seq.T_gt[1 + b], 41 + b, 2.0, 0.03) for b in range(3)])
+    b3 = g.BatchTracker(3, K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=seq.stride, params=prm)
+    b3.rows.copy_(rr)
+    Tb3, st3 = b3.track_rows(tgt, init)
+    ns = [tr_.cloud.n() for tr_ in b3.trs]
+    assert ns[2] < 0.75 * ns[0], ns
+    for b in range(3):
+        tr.rows.copy_(rr[b])
+        Ts, sts = tr.track_rows(tgt, init[b])
+        assert tr.cloud.n() == ns[b]
+        assert rot_angle(Tb3[b][:3, :3], Ts[:3, :3]) < 1e-6 and np.abs(Tb3[b][:3, 3] - Ts[:3, 3]).max() < 1e-6
+        assert st3[b]["n_inliers"] == sts["n_inliers"]

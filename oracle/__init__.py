@@ -65,6 +65,8 @@ def lib():
         L.ora_update.argtypes = [P, P]
         L.ora_align.argtypes = [P, P, i, P, P, i, i, P, P, i, f, d, d, i, P, P]
         L.ora_align.restype = i
+        L.ora_align2.argtypes = [P, P, i, P, P, i, i, P, P, i, f, d, d, i, i, d, P, P]
+        L.ora_align2.restype = i
         L.ora_num_threads.restype = i
         L.ora_set_threads.argtypes = [i]
         L.ora_set_threads.restype = None
@@ -233,19 +235,21 @@ def update(T, delta):
 
 
 def align(src_xyz, src_cov, tgt_xyz, tgt_cov, T0, max_iters=30, max_corr_dist=np.inf, eps_rot=1e-6,
-          eps_trans=1e-6, min_pairs=50, use_tree=None, tree: KDTree | None = None):
+          eps_trans=1e-6, min_pairs=50, use_tree=None, tree: KDTree | None = None, solver=0, lm_lambda0=1e-4):
     """O10/O11 -> dict(T, fitness, mean_cost, n_inliers, iters, converged, status).
-    tree: optional prebuilt KDTree over tgt_xyz (else one is built per call if use_tree)."""
+    tree: optional prebuilt KDTree over tgt_xyz (else one is built per call if use_tree).
+    solver 0 = Gauss-Newton, 1 = Levenberg-Marquardt (R30) with initial damping lm_lambda0."""
     src_xyz, src_cov, tgt_xyz, tgt_cov = map(_f32, (src_xyz, src_cov, tgt_xyz, tgt_cov))
     if use_tree is None:
         use_tree = src_xyz.shape[0] * tgt_xyz.shape[0] > 10_000_000
     T0 = np.ascontiguousarray(T0, np.float64)
     T = np.empty((4, 4))
     st = np.empty(6)
-    status = lib().ora_align(_p(src_xyz), _p(src_cov), src_xyz.shape[0], _p(tgt_xyz), _p(tgt_cov),
-                             tgt_xyz.shape[0], int(use_tree),
-                             C.c_void_p(tree._t) if tree is not None else None, _p(T0), max_iters, float(max_corr_dist), eps_rot,
-                             eps_trans, min_pairs, _p(T), _p(st))
+    status = lib().ora_align2(_p(src_xyz), _p(src_cov), src_xyz.shape[0], _p(tgt_xyz), _p(tgt_cov),
+                              tgt_xyz.shape[0], int(use_tree),
+                              C.c_void_p(tree._t) if tree is not None else None, _p(T0), max_iters,
+                              float(max_corr_dist), eps_rot, eps_trans, min_pairs, int(solver), float(lm_lambda0),
+                              _p(T), _p(st))
     return dict(T=T, fitness=st[0], mean_cost=st[1], n_inliers=int(st[2]), iters=int(st[3]),
                 converged=bool(st[4]), status=int(status))
 

@@ -641,25 +641,63 @@ void ora_update(double *T, const double *delta) {
 /* O10/O11  Gauss-Newton loop (R16-R20).  stats: [fitness, mean_cost, n_inliers,
  * iters, converged, status].  NN: prebuilt kd-tree over tgt_xyz if given, else a tree built here
  * (use_tree) or brute force.  Returns status. */
-int ora_align(const float *src_xyz, const float *src_cov, int n, const float *tgt_xyz, const float *tgt_cov,
-              int M, int use_tree, const void *prebuilt, const double *T0, int max_iters, float max_corr_dist,
-              double eps_rot, double eps_trans, int min_pairs, double *T_out, double *stats) {
+/* O10 with the solver option.  solver 0: Gauss-Newton (O9 each iteration).  solver 1:
+ * Levenberg-Marquardt (R30; the paper is silent, SPEC S:151/S:157 ask for a damped fallback):
+ * iteration k linearises at the trial pose T_k; T_k is accepted iff k == 0 or its Eq. 1 cost is
+ * below the last accepted cost (a trial with fewer than min_pairs inliers is rejected); accept:
+ * lambda <- k == 0 ? lambda0 : lambda / 10, keep (T_a, H_a, b_a, cost_a, n_a); reject: lambda <-
+ * 10 lambda.  Step: (H_a + lambda diag(H_a)) delta = -b_a (O9's Cholesky with its PD fallback),
+ * T_{k+1} = Exp(delta) T_a (left update).  Converged iff |omega| < eps_rot and |v| < eps_trans
+ * (the pose returned is then T_{k+1}, as for GN); at the cap the best accepted pose T_a is returned
+ * ("max-iters, best iterate").  Stats from the accepted linearisation. */
+int ora_align2(const float *src_xyz, const float *src_cov, int n, const float *tgt_xyz, const float *tgt_cov,
+               int M, int use_tree, const void *prebuilt, const double *T0, int max_iters, float max_corr_dist,
+               double eps_rot, double eps_trans, int min_pairs, int solver, double lambda0, double *T_out,
+               double *stats) {
     void *own = (!prebuilt && use_tree) ? ora_kdtree_build(tgt_xyz, M) : NULL;
     const void *tree = prebuilt ? prebuilt : own;
-    double T[16];
+    double T[16], Ta[16], Ha[36], ba[6], cost_a = 0, lambda = lambda0;
     memcpy(T, T0, sizeof(T));
-    int status = ORA_MAX_ITERS, iters = 0, conv = 0, ninl = 0;
+    memcpy(Ta, T0, sizeof(Ta));
+    int status = ORA_MAX_ITERS, iters = 0, conv = 0, ninl = 0, n_a = 0;
     double cost = 0;
     for (int it = 0; it < max_iters; ++it) {
         double H[36], b[6], delta[6];
         ninl = ora_linearize(src_xyz, src_cov, n, tgt_xyz, tgt_cov, M, tree, T, max_corr_dist, H, b, &cost, NULL);
-        if (ninl < min_pairs) { status = ORA_TRACKING_LOST; break; }
-        if (!ora_solve(H, b, delta)) { status = ORA_TRACKING_LOST; break; }
-        ora_update(T, delta);
+        if (solver == 0) {
+            if (ninl < min_pairs) { status = ORA_TRACKING_LOST; break; }
+            if (!ora_solve(H, b, delta)) { status = ORA_TRACKING_LOST; break; }
+            ora_update(T, delta);
+        } else {
+            int accept = it == 0 ? ninl >= min_pairs : (ninl >= min_pairs && cost < cost_a);
+            if (it == 0 && !accept) { status = ORA_TRACKING_LOST; break; }
+            if (accept) {
+                memcpy(Ta, T, sizeof(Ta));
+                memcpy(Ha, H, sizeof(Ha));
+                memcpy(ba, b, sizeof(ba));
+                cost_a = cost;
+                n_a = ninl;
+                if (it > 0) lambda = lambda / 10.0;
+            } else {
+                lambda = lambda * 10.0;
+            }
+            double D[36];
+            memcpy(D, Ha, sizeof(D));
+            for (int k = 0; k < 6; ++k) D[7 * k] = Ha[7 * k] + lambda * Ha[7 * k];
+            if (!ora_solve(D, ba, delta)) { status = ORA_TRACKING_LOST; break; }
+            memcpy(T, Ta, sizeof(T));
+            ora_update(T, delta);
+        }
         iters = it + 1;
         double nw = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]);
         double nv = sqrt(delta[3] * delta[3] + delta[4] * delta[4] + delta[5] * delta[5]);
         if (nw < eps_rot && nv < eps_trans) { conv = 1; status = ORA_OK; break; }
+    }
+    if (solver != 0) {
+        if (status == ORA_MAX_ITERS) memcpy(T, Ta, sizeof(T));  /* best (accepted) iterate */
+        if (status == ORA_TRACKING_LOST && iters > 0) memcpy(T, Ta, sizeof(T));
+        ninl = n_a;
+        cost = cost_a;
     }
     if (own) ora_kdtree_free(own);
     memcpy(T_out, T, sizeof(T));
@@ -670,6 +708,13 @@ int ora_align(const float *src_xyz, const float *src_cov, int n, const float *tg
     stats[4] = conv;
     stats[5] = status;
     return status;
+}
+
+int ora_align(const float *src_xyz, const float *src_cov, int n, const float *tgt_xyz, const float *tgt_cov,
+              int M, int use_tree, const void *prebuilt, const double *T0, int max_iters, float max_corr_dist,
+              double eps_rot, double eps_trans, int min_pairs, double *T_out, double *stats) {
+    return ora_align2(src_xyz, src_cov, n, tgt_xyz, tgt_cov, M, use_tree, prebuilt, T0, max_iters, max_corr_dist,
+                      eps_rot, eps_trans, min_pairs, 0, 0.0, T_out, stats);
 }
 
 int ora_num_threads(void) {

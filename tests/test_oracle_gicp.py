@@ -241,3 +241,64 @@ def test_kdtree_linearize_equals_brute():
     b = oracle.linearize(xyz, cs, tgt, ct, Tp, max_corr_dist=0.1, tree=oracle.KDTree(tgt))
     np.testing.assert_array_equal(a["corr"], b["corr"])
     np.testing.assert_array_equal(a["H"], b["H"])
+
+
+# ------------------------------------------------------------------ Levenberg-Marquardt (R30)
+@pytest.mark.parametrize("lam0", [1e-2, 1.0, 1e3])
+def test_lm_first_step_closed_form(lam0):
+    """The first LM step is delta = -(H + lam0 diag(H))^-1 b at T0 (numpy.linalg.solve) and the
+    pose Exp(delta) T0 with Exp = scipy.linalg.expm of the twist's rotation (left update)."""
+    xyz, tgt, T = _c1_like()
+    cs = oracle.covariances(xyz)["cov"]
+    ct = oracle.covariances(tgt)["cov"]
+    T0 = np.eye(4)
+    r = oracle.linearize(xyz, cs, tgt, ct, T0)
+    D = r["H"] + lam0 * np.diag(np.diag(r["H"]))
+    delta = np.linalg.solve(D, -r["b"])
+    E = expm(skew(delta[:3]))
+    ref = np.eye(4)
+    ref[:3, :3] = E @ T0[:3, :3]
+    ref[:3, 3] = E @ T0[:3, 3] + delta[3:]
+    a = oracle.align(xyz, cs, tgt, ct, T0, max_iters=5, eps_rot=1e9, eps_trans=1e9, solver=1, lm_lambda0=lam0)
+    assert a["status"] == oracle.OK and a["iters"] == 1
+    np.testing.assert_allclose(a["T"], ref, rtol=0, atol=1e-12)
+    assert a["n_inliers"] == r["n"] and abs(a["mean_cost"] - r["cost"] / r["n"]) <= 1e-12 * r["cost"] / r["n"]
+
+
+def test_lm_identity_and_known_transform():
+    """Identical clouds: one iteration, zero update.  C1 known transform: LM reaches the
+    same optimum as GN (the transform, 1e-6) and the two fixed points agree to 1e-9."""
+    xyz, tgt, T = _c1_like()
+    cs = oracle.covariances(xyz)["cov"]
+    ct = oracle.covariances(tgt)["cov"]
+    a = oracle.align(xyz, cs, xyz, cs, np.eye(4), solver=1)
+    assert a["status"] == oracle.OK and a["iters"] == 1
+    np.testing.assert_array_equal(a["T"], np.eye(4))
+    lm = oracle.align(xyz, cs, tgt, ct, np.eye(4), max_iters=60, eps_rot=1e-10, eps_trans=1e-10, solver=1)
+    gn = oracle.align(xyz, cs, tgt, ct, np.eye(4), max_iters=60, eps_rot=1e-10, eps_trans=1e-10)
+    assert lm["converged"] and gn["converged"]
+    assert rot_err(lm["T"][:3, :3], T[:3, :3]) < 1e-6 and np.linalg.norm(lm["T"][:3, 3] - T[:3, 3]) < 1e-6
+    assert rot_err(lm["T"][:3, :3], gn["T"][:3, :3]) < 1e-9 and np.abs(lm["T"][:3, 3] - gn["T"][:3, 3]).max() < 1e-9
+
+
+def test_lm_point_to_point_equals_kabsch_and_best_iterate_at_cap():
+    """Point-to-point (M = I): the LM fixed point is the Kabsch closed form on its final
+    correspondences.  At the iteration cap LM returns its best accepted iterate: its cost is
+    never above the initial pose's."""
+    rng = np.random.default_rng(23)
+    n = 500
+    src = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    Tg = np.eye(4); Tg[:3, :3] = synth.rot_axis_angle(rng.normal(size=3), 0.3); Tg[:3, 3] = [0.1, -0.05, 0.08]
+    tgt = (src.astype(np.float64) @ Tg[:3, :3].T + Tg[:3, 3] + rng.normal(0, 0.01, (n, 3))).astype(np.float32)
+    half = np.tile(pack(np.eye(3) / 2), (n, 1)).astype(np.float32)
+    a = oracle.align(src, half, tgt, half, np.eye(4), max_iters=200, eps_rot=1e-12, eps_trans=1e-12, solver=1)
+    r = oracle.linearize(src, half, tgt, half, a["T"])
+    R, t = _kabsch(src.astype(np.float64), tgt[r["corr"]].astype(np.float64))
+    assert np.abs(a["T"][:3, :3] - R).max() < 1e-9 and np.abs(a["T"][:3, 3] - t).max() < 1e-9
+    c0 = oracle.linearize(src, half, tgt, half, np.eye(4), max_corr_dist=0.2)["cost"]
+    for cap in (1, 2, 3):
+        b = oracle.align(src, half, tgt, half, np.eye(4), max_iters=cap, eps_rot=0.0, eps_trans=0.0, solver=1,
+                         max_corr_dist=0.2, lm_lambda0=10.0)
+        assert b["status"] == oracle.MAX_ITERS
+        cb = oracle.linearize(src, half, tgt, half, b["T"], max_corr_dist=0.2)["cost"]
+        assert cb <= c0

@@ -86,6 +86,11 @@ typedef struct {
     double eps_rot;        /* converged iff |omega| < eps_rot and |v| < eps_trans     */
     double eps_trans;
     int32_t min_pairs;     /* fewer inliers -> TRACKING_LOST, default 50       */
+    int32_t solver;        /* 0 = Gauss-Newton (default); 1 = Levenberg-Marquardt (R30): a trial
+                              pose is kept iff its Eq. 1 cost is below the last kept one, step
+                              (H + lambda diag H) delta = -b, lambda / 10 on accept, x 10 on reject;
+                              at the cap the best kept pose is returned                */
+    double lm_lambda0;     /* initial lambda (solver 1), > 0                                  */
 } gsicp_align_params;
 
 typedef struct {

@@ -53,7 +53,8 @@ class _Target(C.Structure):
 
 class AlignParams(C.Structure):
     _fields_ = [("max_iters", C.c_int32), ("max_corr_dist", C.c_float), ("eps_rot", C.c_double),
-                ("eps_trans", C.c_double), ("min_pairs", C.c_int32)]
+                ("eps_trans", C.c_double), ("min_pairs", C.c_int32), ("solver", C.c_int32),
+                ("lm_lambda0", C.c_double)]
 
 
 class AlignStats(C.Structure):
@@ -435,8 +436,14 @@ def build_target_cloud(cloud: Cloud, cell: float, M: int | None = None, stream=N
     return Target(ws, st, (cloud,))
 
 
-def align_params(max_iters=30, max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6, min_pairs=50) -> AlignParams:
-    return AlignParams(max_iters, max_corr_dist, eps_rot, eps_trans, min_pairs)
+SOLVER_GN, SOLVER_LM = 0, 1
+
+
+def align_params(max_iters=30, max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6, min_pairs=50, solver=SOLVER_GN,
+                 lm_lambda0=1e-4) -> AlignParams:
+    """A6-A9 parameters; solver SOLVER_LM selects Levenberg-Marquardt (R30) with initial damping
+    lm_lambda0."""
+    return AlignParams(max_iters, max_corr_dist, eps_rot, eps_trans, min_pairs, solver, lm_lambda0)
 
 
 def align_workspace(cap: int, device="cuda") -> torch.Tensor:

@@ -54,6 +54,8 @@ struct AlignArgs {
     float r, r2;
     double eps_rot, eps_trans;
     int min_pairs;
+    int solver;               // 0 GN, 1 LM (R30)
+    double lm_lambda0;
     int linearize_only;
     double *d_T;              // [16] in/out (row-major 4x4)
     gsicp_align_stats *d_stats;
@@ -592,8 +594,12 @@ __device__ __forceinline__ bool chol6_solve(const double *H, const double *rhs, 
 // A8 for one block (thread 0): solve H delta = -b, update the shared pose, convergence test.
 // Out of line: its ~150 live doubles must not raise the register pressure of the point loop.
 // Returns 1 when the loop is done (status set).
+// LM state kept by every block (identical): [0,12) kept pose, [12,41) its linearisation terms
+// (sAcc layout), [41] lambda, [42] 1 once a pose was kept
+constexpr int kLmState = 44;
+
 __device__ __forceinline__ int solve_step(const AlignArgs &a, const double *sAcc, double *sT, int it, int n, int &status,
-                                       int &iters, int &converged) {
+                                       int &iters, int &converged, double *sLM) {
     double H[36], b[6];
     int t = 0;
     for (int r = 0; r < 6; ++r)
@@ -614,7 +620,29 @@ __device__ __forceinline__ int solve_step(const AlignArgs &a, const double *sAcc
         status = GSICP_ERR_DEGENERATE_FRAME;
         return 1;
     }
-    if (n_in < (double)a.min_pairs) {
+    if (a.solver == 1) {
+        // Levenberg-Marquardt (R30): keep the trial pose iff its cost beats the kept one
+        const bool enough = n_in >= (double)a.min_pairs;
+        const bool accept = it == 0 ? enough : (enough && sAcc[27] < sLM[12 + 27]);
+        if (it == 0 && !accept) {
+            status = GSICP_ERR_TRACKING_LOST;
+            return 1;
+        }
+        if (accept) {
+            for (int k = 0; k < 12; ++k) sLM[k] = sT[k];
+            for (int k = 0; k < 29; ++k) sLM[12 + k] = sAcc[k];
+            sLM[41] = it == 0 ? a.lm_lambda0 : sLM[41] / 10.0;
+            sLM[42] = 1.0;
+        } else {
+            sLM[41] = sLM[41] * 10.0;
+        }
+        t = 0;
+        for (int r = 0; r < 6; ++r)
+            for (int c = r; c < 6; ++c) H[6 * r + c] = H[6 * c + r] = sLM[12 + t++];
+        for (int r = 0; r < 6; ++r) b[r] = sLM[12 + 21 + r];
+        for (int k = 0; k < 6; ++k) H[7 * k] = H[7 * k] + sLM[41] * H[7 * k];
+        for (int k = 0; k < 12; ++k) sT[k] = sLM[k];  // the step starts from the kept pose
+    } else if (n_in < (double)a.min_pairs) {
         status = GSICP_ERR_TRACKING_LOST;
         return 1;
     }
@@ -629,7 +657,7 @@ __device__ __forceinline__ int solve_step(const AlignArgs &a, const double *sAcc
     }
     if (!ok) {
         status = GSICP_ERR_TRACKING_LOST;
-        return 1;
+        return 1;  // (LM: sT already holds the kept pose)
     }
     double E[9];
     so3_exp(delta, E);
@@ -649,6 +677,8 @@ __device__ __forceinline__ int solve_step(const AlignArgs &a, const double *sAcc
     }
     if (iters >= a.max_iters) {
         status = GSICP_WARN_MAX_ITERS;
+        if (a.solver == 1)
+            for (int k = 0; k < 12; ++k) sT[k] = sLM[k];  // the best kept iterate
         return 1;
     }
     return 0;
@@ -778,6 +808,7 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
     __shared__ double sRed[kWarps][kPad];
     __shared__ double sAcc[kPad];
     __shared__ int sDone;
+    __shared__ double sLM[kLmState];
     __shared__ int sBox[6];
     __shared__ CellIndex sIdx;
     // per-block queue of queries needing the general search (handled by whole warps)
@@ -801,6 +832,7 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
         sSeeded = ok;
     }
     if (tid == 0) sDone = 0;
+    if (tid == 0) sLM[42] = 0.0;
     if (tid == 0) sQn = 0;
     // resident point of this thread: source data, current match and own target cell in registers
     // resident points: block b owns the contiguous chunk [b P, b P + P), P = ceil(n / G) (at most
@@ -1108,7 +1140,11 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
             n_in = sAcc[28];
             cost_last = sAcc[27];
             int st_ = status, it_ = iters, cv_ = converged;
-            sDone = solve_step(a, sAcc, sT, it, n, st_, it_, cv_);
+            sDone = solve_step(a, sAcc, sT, it, n, st_, it_, cv_, sLM);
+            if (a.solver == 1 && !a.linearize_only && sLM[42] != 0.0) {  // stats of the kept linearisation
+                n_in = sLM[12 + 28];
+                cost_last = sLM[12 + 27];
+            }
             status = st_;
             iters = it_;
             converged = cv_;
@@ -1251,6 +1287,8 @@ static AlignArgs make_args(const gsicp_cloud &src, const gsicp_target &tgt, doub
     a.eps_rot = p.eps_rot;
     a.eps_trans = p.eps_trans;
     a.min_pairs = p.min_pairs;
+    a.solver = p.solver;
+    a.lm_lambda0 = p.lm_lambda0;
     a.linearize_only = linearize_only;
     a.d_T = d_T_inout;
     a.d_stats = d_stats;

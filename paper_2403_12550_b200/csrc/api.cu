@@ -446,6 +446,8 @@ static gsicp_status check_params(const gsicp_align_params *p) {
     if (!(p->max_corr_dist > 0.f)) BAD("align: max_corr_dist must be > 0 (INFINITY allowed)");
     if (!(p->eps_rot >= 0.0) || !(p->eps_trans >= 0.0)) BAD("align: eps must be >= 0");
     if (p->min_pairs < 0) BAD("align: min_pairs must be >= 0");
+    if (p->solver != 0 && p->solver != 1) BAD("align: solver must be 0 (GN) or 1 (LM)");
+    if (p->solver == 1 && !(p->lm_lambda0 > 0.0 && p->lm_lambda0 < 1e30)) BAD("align: lm_lambda0 must be > 0");
     return GSICP_OK;
 }
 

@@ -785,3 +785,31 @@ def test_align_batch_single_and_ragged(g):
         assert tr.cloud.n() == ns[b]
         assert rot_angle(Tb3[b][:3, :3], Ts[:3, :3]) < 1e-6 and np.abs(Tb3[b][:3, 3] - Ts[:3, 3]).max() < 1e-6
         assert st3[b]["n_inliers"] == sts["n_inliers"]
+
+
+@pytest.mark.parametrize("lam0", [1e-4, 1.0])
+def test_align_lm_pose(g, c1_setup, replica_setup, lam0):
+    """Levenberg-Marquardt (R30) through the C ABI vs the oracle's LM from the same initial pose:
+    C1 (30 fixed iterations, known transform) and the Replica frame vs the 1e6 map (converged);
+    the pose within 1e-5 rad / 1e-5 m.  A large initial damping takes more iterations but reaches
+    the same pose."""
+    S = c1_setup
+    p = g.align_params(max_iters=30, max_corr_dist=math.inf, eps_rot=0.0, eps_trans=0.0, solver=g.SOLVER_LM,
+                       lm_lambda0=lam0)
+    Tg, st = g.align(S["src"], S["tgt"], np.eye(4), p)
+    ref = oracle.align(S["xyz"], S["ocs"], S["txyz"], S["oct"], np.eye(4), max_iters=30, eps_rot=0.0, eps_trans=0.0,
+                       solver=1, lm_lambda0=lam0)
+    assert st["status"] == ref["status"] == g.WARN_MAX_ITERS
+    assert rot_angle(Tg[:3, :3], ref["T"][:3, :3]) <= 1e-5 and np.linalg.norm(Tg[:3, 3] - ref["T"][:3, 3]) <= 1e-5
+    assert rot_angle(Tg[:3, :3], S["T"][:3, :3]) <= 1e-5 and np.linalg.norm(Tg[:3, 3] - S["T"][:3, 3]) <= 1e-5
+    R = replica_setup
+    w = R["w"]
+    p = g.align_params(max_iters=30, max_corr_dist=0.1, solver=g.SOLVER_LM, lm_lambda0=lam0)
+    Tg, st = g.align(R["src"], R["tgt"], w.T_init, p)
+    ref = oracle.align(R["xyz"], R["ocs"], R["txyz"], R["oct"], w.T_init, max_iters=30, max_corr_dist=0.1,
+                       use_tree=True, tree=R["tree"], solver=1, lm_lambda0=lam0)
+    assert st["status"] == ref["status"] == g.OK, (st, ref["status"], ref["iters"])
+    assert rot_angle(Tg[:3, :3], ref["T"][:3, :3]) <= 1e-5 and np.linalg.norm(Tg[:3, 3] - ref["T"][:3, 3]) <= 1e-5
+    assert abs(st["iters"] - ref["iters"]) <= 1 and st["n_inliers"] == ref["n_inliers"]
+    gn, _ = g.align(R["src"], R["tgt"], w.T_init, g.align_params(max_iters=30, max_corr_dist=0.1))
+    assert rot_angle(Tg[:3, :3], gn[:3, :3]) <= 1e-5 and np.linalg.norm(Tg[:3, 3] - gn[:3, 3]) <= 1e-5

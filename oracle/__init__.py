@@ -67,6 +67,8 @@ def lib():
         L.ora_align.restype = i
         L.ora_align2.argtypes = [P, P, i, P, P, i, i, P, P, i, f, d, d, i, i, d, P, P]
         L.ora_align2.restype = i
+        L.ora_voxel_downsample.argtypes = [P, i, f, P, P]
+        L.ora_voxel_downsample.restype = i
         L.ora_num_threads.restype = i
         L.ora_set_threads.argtypes = [i]
         L.ora_set_threads.restype = None
@@ -283,3 +285,13 @@ def export_gaussians(xyz, raw, T=None, mode=ELLIPSE, eps=1e-3, p=1.5, c=1.0):
     means, quats, sc = np.empty((n, 3)), np.empty((n, 4)), np.empty((n, 3))
     lib().ora_export_gaussians(_p(xyz), _p(raw), n, _p(Tm), mode, eps, p, c, _p(means), _p(quats), _p(sc))
     return means, quats, sc
+
+
+def voxel_downsample(xyz, voxel):
+    """N4 (R31) -> (points (m,3) f32 ordered by each voxel's first member, counts (m,) i32)."""
+    xyz = _f32(xyz)
+    n = xyz.shape[0]
+    out = np.empty((max(n, 1), 3), np.float32)
+    cnt = np.empty(max(n, 1), np.int32)
+    m = lib().ora_voxel_downsample(_p(xyz), n, float(voxel), _p(out), _p(cnt))
+    return out[:m].copy(), cnt[:m].copy()

@@ -831,3 +831,56 @@ void ora_export_gaussians(const float *xyz, const double *raw, int n, const doub
         ora_export_gaussian(raw + 6 * (int64_t)i, xyz + 3 * (int64_t)i, T, mode, eps, p, c, means + 3 * (int64_t)i,
                             quats + 4 * (int64_t)i, scales + 3 * (int64_t)i);
 }
+
+/* N4 voxel downsampling ("at most one output point per occupied voxel; output point
+ * = centroid of members"; R31): voxel of a point = (floor(x / h), floor(y / h), floor(z / h)) with
+ * binary64 division; output point = the binary64 mean of the members' coordinates (summed in index
+ * order), rounded to binary32; outputs ordered by the smallest input index of each voxel; cnt_out =
+ * members.  Non-finite points are skipped.  Returns m.  O(n log n): (key, index) pairs sorted. */
+typedef struct { int64_t k[3]; int32_t i; } ora_vkey;
+static int ora_vkey_cmp(const void *pa, const void *pb) {
+    const ora_vkey *a = (const ora_vkey *)pa, *b = (const ora_vkey *)pb;
+    for (int d = 0; d < 3; ++d)
+        if (a->k[d] != b->k[d]) return a->k[d] < b->k[d] ? -1 : 1;
+    return a->i < b->i ? -1 : (a->i > b->i);
+}
+typedef struct { int32_t first; float p[3]; int32_t cnt; } ora_vout;
+static int ora_vout_cmp(const void *pa, const void *pb) {
+    const ora_vout *a = (const ora_vout *)pa, *b = (const ora_vout *)pb;
+    return a->first < b->first ? -1 : (a->first > b->first);
+}
+int ora_voxel_downsample(const float *xyz, int n, float voxel, float *out_xyz, int32_t *cnt_out) {
+    ora_vkey *v = (ora_vkey *)malloc(sizeof(ora_vkey) * (size_t)(n > 0 ? n : 1));
+    int nv = 0;
+    for (int i = 0; i < n; ++i) {
+        const float *p = xyz + 3 * (int64_t)i;
+        if (!isfinite(p[0]) || !isfinite(p[1]) || !isfinite(p[2])) continue;
+        for (int d = 0; d < 3; ++d) v[nv].k[d] = (int64_t)floor((double)p[d] / (double)voxel);
+        v[nv].i = i;
+        ++nv;
+    }
+    qsort(v, (size_t)nv, sizeof(ora_vkey), ora_vkey_cmp);
+    ora_vout *o = (ora_vout *)malloc(sizeof(ora_vout) * (size_t)(nv > 0 ? nv : 1));
+    int m = 0;
+    for (int a = 0; a < nv;) {
+        int b = a;
+        double s[3] = {0, 0, 0};
+        while (b < nv && v[b].k[0] == v[a].k[0] && v[b].k[1] == v[a].k[1] && v[b].k[2] == v[a].k[2]) {
+            for (int d = 0; d < 3; ++d) s[d] += (double)xyz[3 * (int64_t)v[b].i + d];  /* index order */
+            ++b;
+        }
+        o[m].first = v[a].i;
+        o[m].cnt = b - a;
+        for (int d = 0; d < 3; ++d) o[m].p[d] = (float)(s[d] / (double)(b - a));
+        ++m;
+        a = b;
+    }
+    qsort(o, (size_t)m, sizeof(ora_vout), ora_vout_cmp);
+    for (int j = 0; j < m; ++j) {
+        for (int d = 0; d < 3; ++d) out_xyz[3 * (int64_t)j + d] = o[j].p[d];
+        cnt_out[j] = o[j].cnt;
+    }
+    free(v);
+    free(o);
+    return m;
+}

@@ -183,3 +183,40 @@ def test_scale_align_spec_examples(ex):
     np.testing.assert_allclose(oracle.scale_align(ex["scales"], ex["z"], ex["p"]), ex["out"], rtol=1e-15)
     with pytest.raises(ValueError):
         oracle.scale_align(ex["scales"], 0.0, ex["p"])
+
+
+# ------------------------------------------------------------------ N4 voxel downsampling (R31)
+def test_voxel_spec_examples():
+    """SPEC S:58-60 worked examples."""
+    p, c = oracle.voxel_downsample(np.array([[0.3, -0.2, 1.5]], np.float32), 0.1)
+    np.testing.assert_array_equal(p, np.float32([[0.3, -0.2, 1.5]]))
+    assert c.tolist() == [1]
+    p, c = oracle.voxel_downsample(np.array([[0, 0, 0], [0.01, 0, 0]], np.float32), 0.1)
+    np.testing.assert_allclose(p, [[0.005, 0, 0]], rtol=1e-6)
+    assert c.tolist() == [2]
+    p, c = oracle.voxel_downsample(np.array([[0, 0, 0], [1.0, 0, 0]], np.float32), 0.1)
+    assert p.shape == (2, 3) and c.tolist() == [1, 1]
+
+
+def test_voxel_brute_force_groups():
+    """Brute force on a random cloud: one output per distinct floor(x/h) triple (numpy.unique),
+    each the binary64 mean of its members (numpy) rounded to binary32, in the order of each voxel's
+    first member; counts sum to n; output size <= input size; empty in, empty out."""
+    rng = np.random.default_rng(31)
+    P = (rng.normal(size=(3000, 3)) * [0.4, 0.3, 0.2] + [0.0, 0.05, 2.0]).astype(np.float32)
+    P[5] = np.nan  # skipped
+    for h in (0.02, 0.1, 0.37):
+        pts, cnt = oracle.voxel_downsample(P, h)
+        ok = np.isfinite(P).all(1)
+        idx = np.nonzero(ok)[0]
+        keys = np.floor(P[idx].astype(np.float64) / np.float64(np.float32(h))).astype(np.int64)
+        uk, first, inv = np.unique(keys, axis=0, return_index=True, return_inverse=True)
+        inv = inv.reshape(-1)
+        order = np.argsort(idx[first])
+        assert pts.shape[0] == uk.shape[0] <= P.shape[0] and cnt.sum() == idx.size
+        for j, g_ in enumerate(order):
+            mem = idx[inv == g_]
+            np.testing.assert_array_equal(pts[j], P[mem].astype(np.float64).mean(0).astype(np.float32))
+            assert cnt[j] == mem.size
+    e, ce = oracle.voxel_downsample(np.zeros((0, 3), np.float32), 0.1)
+    assert e.shape == (0, 3) and ce.size == 0

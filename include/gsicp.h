@@ -307,6 +307,19 @@ gsicp_status gsicp_pose_predict(const double *d_hist, double *d_T_out, void *str
 gsicp_status gsicp_pose_push(double *d_hist, const double *d_T, double *d_traj, int32_t *d_counter, int32_t traj_cap,
                              void *stream);
 
+/* N4 voxel downsampling (reading R31): at most one output point per occupied voxel,
+ * the centroid of its members.  Voxel = (floor(x/h), floor(y/h), floor(z/h)), binary64 division;
+ * centroid = binary64 mean of the members rounded to binary32; outputs ordered by each voxel's
+ * smallest input index; non-finite points skipped; voxels within +-2^20 h of the origin.
+ *  pos [dev] float4[cap] (x, y, z, payload), d_n [dev] int32 (<= cap);
+ *  pos_out [dev] float4[cap]: rows [0, *d_m_out) = (centroid, member count as int bits) — a
+ *      general cloud: search it with gsicp_covariances, not the image-window path;
+ *  ws: gsicp_voxel_downsample_workspace_size(cap) bytes, 256-byte aligned.
+ *  Errors: INVALID_ARGUMENT, WORKSPACE_TOO_SMALL, CUDA. */
+size_t gsicp_voxel_downsample_workspace_size(int32_t cap);
+gsicp_status gsicp_voxel_downsample(const float *pos, const int32_t *d_n, int32_t cap, float voxel, float *pos_out,
+                                    int32_t *d_m_out, void *ws, size_t ws_bytes, void *stream);
+
 /* A4 export: source points -> 3DGS Gaussians for keyframe insertion into the map (ALG-12).
  * P:187-191 Eq. 3 C = R Lambda^2 R^T, Eq. 4 Lambda' = Lambda / median(S)
  * Lambda'' = Lambda' / z^p (p = 1.5 best) with the absolute factor c (R21).

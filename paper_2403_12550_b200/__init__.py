@@ -121,6 +121,10 @@ def lib():
         L.gsicp_align_batch_async.restype = i32
         L.gsicp_align_batch_max.argtypes = []
         L.gsicp_align_batch_max.restype = i32
+        L.gsicp_voxel_downsample_workspace_size.argtypes = [i32]
+        L.gsicp_voxel_downsample_workspace_size.restype = sz
+        L.gsicp_voxel_downsample.argtypes = [P, P, i32, f32, P, P, P, sz, P]
+        L.gsicp_voxel_downsample.restype = i32
         L.gsicp_export_workspace_size.argtypes = [i32]
         L.gsicp_export_workspace_size.restype = sz
         for name in ("gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_gaussians"):
@@ -155,7 +159,8 @@ EXPORTED = [
     "gsicp_debug_align_timeline", "gsicp_debug_align_counters", "gsicp_debug_kernel_timer",
     "gsicp_debug_kernel_time", "gsicp_graph_instantiate", "gsicp_graph_launch", "gsicp_graph_destroy",
     "gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_workspace_size", "gsicp_export_gaussians",
-    "gsicp_align_batch_max", "gsicp_align_batch_async",
+    "gsicp_align_batch_max", "gsicp_align_batch_async", "gsicp_voxel_downsample_workspace_size",
+    "gsicp_voxel_downsample",
 ]
 
 KT_KNN_SEARCH, KT_ALIGN, KT_SEED, KT_BP, KT_COVS, KT_WIDE, KT_TAIL = 0, 1, 2, 3, 4, 5, 6
@@ -535,6 +540,19 @@ def pose_push(hist: torch.Tensor, T: torch.Tensor, traj: torch.Tensor | None = N
     """hist <- (T_{t-1}, T); traj[counter++] = T if given (device tensors)."""
     cap = traj.shape[0] if traj is not None else 0
     _check(lib().gsicp_pose_push(_ptr(hist), _ptr(T), _ptr(traj), _ptr(counter), cap, _stream(stream)))
+
+
+def voxel_downsample(pos: torch.Tensor, d_n: torch.Tensor, voxel: float, out: torch.Tensor | None = None,
+                     stream=None):
+    """N4 (R31): -> (pos_out (cap, 4) float32, d_m (1,) int32): rows [0, d_m) are the voxel
+    centroids in the order of each voxel's first member, w = member count (int bits)."""
+    cap = pos.shape[0]
+    out = out if out is not None else torch.empty((cap, 4), dtype=torch.float32, device=pos.device)
+    d_m = torch.zeros(1, dtype=torch.int32, device=pos.device)
+    ws = _ws(lib().gsicp_voxel_downsample_workspace_size(cap), pos.device)
+    _check(lib().gsicp_voxel_downsample(_ptr(pos), _ptr(d_n), cap, float(voxel), _ptr(out), _ptr(d_m), _ptr(ws),
+                                        ws.numel(), _stream(stream)))
+    return out, d_m
 
 
 def export_gaussians(pos: torch.Tensor, d_n: torch.Tensor, cov_a: torch.Tensor, cov_b: torch.Tensor,

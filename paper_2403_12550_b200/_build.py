@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libgsicp.so")
 HOSTMATH = os.path.join(HERE, "libgsicp_hostmath.so")
-SOURCES = ["api.cu", "backproject.cu", "grid.cu", "knn_cov.cu", "target.cu", "align.cu", "export.cu"]
+SOURCES = ["api.cu", "backproject.cu", "grid.cu", "knn_cov.cu", "target.cu", "align.cu", "export.cu", "voxel.cu"]
 HEADERS = ["gsicp_internal.cuh", "grid.cuh", "host_common.cuh"]
 
 

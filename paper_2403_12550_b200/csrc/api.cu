@@ -69,6 +69,9 @@ cudaError_t build_target_launch(const float *means, const float *quats, const fl
                                 cudaStream_t s);
 cudaError_t build_target_cloud_launch(const gsicp_cloud &cl, int M, float cell, gsicp_target *out, void *ws,
                                       cudaStream_t s);
+size_t voxel_ws_bytes(int cap);
+cudaError_t voxel_launch(const float4 *pos, const int32_t *d_n, int cap, float voxel, float4 *out, int32_t *d_m,
+                         void *ws, cudaStream_t s);
 size_t export_ws_bytes(int cap);
 cudaError_t export_launch(const float4 *pos, const float4 *cov_a, const float4 *cov_b, const int32_t *d_n, int cap,
                           const double *d_T, double p, double c, const int32_t *corr, float *means, float *quats,
@@ -224,6 +227,22 @@ gsicp_status gsicp_pose_push(double *d_hist, const double *d_T, double *d_traj, 
     gsicp::k_pose_push<<<1, 32, 0, (cudaStream_t)stream>>>(d_hist, d_T, d_traj, d_counter, traj_cap);
     gsicp::note_launch();
     return cuda_status(cudaGetLastError(), "pose_push");
+}
+
+size_t gsicp_voxel_downsample_workspace_size(int32_t cap) { return cap < 1 ? 0 : voxel_ws_bytes(cap); }
+
+gsicp_status gsicp_voxel_downsample(const float *pos, const int32_t *d_n, int32_t cap, float voxel, float *pos_out,
+                                    int32_t *d_m_out, void *ws, size_t ws_bytes, void *stream) {
+    g_err[0] = 0;
+    if (!pos || !d_n || !pos_out || !d_m_out) BAD("voxel_downsample: null pointer");
+    if (!aligned16(pos) || !aligned16(pos_out)) BAD("voxel_downsample: pos and pos_out must be 16-byte aligned");
+    if (cap < 1) BAD("voxel_downsample: cap must be >= 1");
+    if (!(voxel > 0.f) || !isfinite(voxel)) BAD("voxel_downsample: voxel must be > 0");
+    gsicp_status st = check_ws(ws, ws_bytes, voxel_ws_bytes(cap));
+    if (st != GSICP_OK) return st;
+    return cuda_status(voxel_launch((const float4 *)pos, d_n, cap, voxel, (float4 *)pos_out, d_m_out, ws,
+                                    (cudaStream_t)stream),
+                       "voxel_downsample");
 }
 
 size_t gsicp_export_workspace_size(int32_t cap) { return cap < 1 ? 0 : export_ws_bytes(cap); }

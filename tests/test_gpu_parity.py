@@ -813,3 +813,26 @@ def test_align_lm_pose(g, c1_setup, replica_setup, lam0):
     assert abs(st["iters"] - ref["iters"]) <= 1 and st["n_inliers"] == ref["n_inliers"]
     gn, _ = g.align(R["src"], R["tgt"], w.T_init, g.align_params(max_iters=30, max_corr_dist=0.1))
     assert rot_angle(Tg[:3, :3], gn[:3, :3]) <= 1e-5 and np.linalg.norm(Tg[:3, 3] - gn[:3, 3]) <= 1e-5
+
+
+@pytest.mark.parametrize("h", [0.01, 0.03, 0.1])
+def test_voxel_downsample(g, replica, tum, h):
+    """N4 (R31) vs the oracle on a Replica frame (stride 1, ~800k points) and the noisy
+    TUM frame: the same voxels in the same order (first member), counts exact, centroids equal
+    (binary64 sums of one voxel's members are exact, so bit-equal in practice; checked to 1 ulp);
+    then A2-A4 on the voxel cloud (general-cloud hash path) == the oracle (kNN bit-exact)."""
+    for w in (replica, tum):
+        K = w.K
+        pos, d_n = gpu_points(g, w.depth, K, 1)
+        xyz, _ = oracle.backproject(w.depth, K.fx, K.fy, K.cx, K.cy, 1)
+        out, d_m = g.voxel_downsample(pos, d_n, h)
+        m = int(d_m.item())
+        op, oc = oracle.voxel_downsample(xyz, h)
+        assert m == op.shape[0] and 0 < m <= xyz.shape[0]
+        gp = out[:m].cpu().numpy()
+        np.testing.assert_array_equal(gp[:, 3].view(np.int32), oc)
+        np.testing.assert_allclose(gp[:, :3], op, rtol=1.2e-7, atol=0)
+        assert (gp[:, :3] == op).mean() > 0.999
+    if h == 0.03:  # the voxel cloud through A2-A4 (hash path)
+        cl = g.Cloud.from_points(out[:m, :3].contiguous())
+        _cov_check(g, gp[:, :3].copy(), cl.pos, cl.d_n, cell0=2 * h, levels=1)

@@ -29,7 +29,7 @@ struct VoxWs {
 
 static uint32_t vox_slots(int cap) {
     uint32_t s = 1024;
-    while (s < 2u * (uint32_t)cap) s <<= 1;
+    while (s < (uint32_t)cap + (uint32_t)cap / 4u) s <<= 1;  // load <= 0.8 even if every point is its own voxel
     return s;
 }
 
@@ -65,33 +65,61 @@ __global__ void k_vox_clear(VoxWs w) {
     }
 }
 
+// Warp-aggregated insert: the lanes of a warp holding points of the same voxel (adjacent pixels
+// mostly) elect their lowest lane — also their smallest index — which inserts the key and adds the
+// group's binary64 sums (exact, so the grouping does not change them) with one set of atomics.
 __global__ void k_vox_insert(VoxWs w, const float4 *__restrict__ pos, const int32_t *__restrict__ d_n, double h) {
     pdl_wait();
     const int n = *d_n;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const float4 p = pos[i];
-        if (!isfinite(p.x) || !isfinite(p.y) || !isfinite(p.z)) {
-            w.slot[i] = -1;
-            continue;
+    const int lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < n; base += warps * 32) {
+        const int i = base + lane;
+        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool valid = i < n;
+        if (valid) {
+            p = pos[i];
+            valid = isfinite(p.x) && isfinite(p.y) && isfinite(p.z);
+            if (!valid) w.slot[i] = -1;
         }
-        const long long ix = (long long)floor(__ddiv_rn((double)p.x, h));
-        const long long iy = (long long)floor(__ddiv_rn((double)p.y, h));
-        const long long iz = (long long)floor(__ddiv_rn((double)p.z, h));
-        // 21 bits per axis (two's complement, masked): voxels within +-2^20 of the origin
-        const unsigned long long key = ((unsigned long long)(ix & 0x1fffff) << 42) |
-                                       ((unsigned long long)(iy & 0x1fffff) << 21) | (unsigned long long)(iz & 0x1fffff);
-        uint32_t s = vox_hash(key, w.mask);
-        while (true) {
-            const unsigned long long prev = atomicCAS(&w.keys[s], kVoxEmpty, key);
-            if (prev == kVoxEmpty || prev == key) break;
-            s = (s + 1) & w.mask;
+        unsigned long long key = kVoxEmpty;  // (never a real key: bit 63 is clear in every packed key)
+        if (valid) {
+            const long long ix = (long long)floor(__ddiv_rn((double)p.x, h));
+            const long long iy = (long long)floor(__ddiv_rn((double)p.y, h));
+            const long long iz = (long long)floor(__ddiv_rn((double)p.z, h));
+            // 21 bits per axis (two's complement, masked): voxels within +-2^20 of the origin
+            key = ((unsigned long long)(ix & 0x1fffff) << 42) | ((unsigned long long)(iy & 0x1fffff) << 21) |
+                  (unsigned long long)(iz & 0x1fffff);
         }
-        atomicAdd(&w.sum[3 * (size_t)s], (double)p.x);
-        atomicAdd(&w.sum[3 * (size_t)s + 1], (double)p.y);
-        atomicAdd(&w.sum[3 * (size_t)s + 2], (double)p.z);
-        atomicAdd(&w.cnt[s], 1u);
-        atomicMin(&w.first[s], (uint32_t)i);
-        w.slot[i] = (int32_t)s;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const int leader = __ffs(peers) - 1;
+        double sx = 0.0, sy = 0.0, sz = 0.0;
+        for (int src = 0; src < 32; ++src) {  // the group's sums at its leader (all lanes shuffle)
+            const float vx = __shfl_sync(0xffffffffu, p.x, src), vy = __shfl_sync(0xffffffffu, p.y, src),
+                        vz = __shfl_sync(0xffffffffu, p.z, src);
+            if ((peers >> src) & 1u) {
+                sx += (double)vx;
+                sy += (double)vy;
+                sz += (double)vz;
+            }
+        }
+        int s = -1;
+        if (valid && lane == leader) {
+            uint32_t t = vox_hash(key, w.mask);
+            while (true) {
+                const unsigned long long prev = atomicCAS(&w.keys[t], kVoxEmpty, key);
+                if (prev == kVoxEmpty || prev == key) break;
+                t = (t + 1) & w.mask;
+            }
+            s = (int)t;
+            atomicAdd(&w.sum[3 * (size_t)t], sx);
+            atomicAdd(&w.sum[3 * (size_t)t + 1], sy);
+            atomicAdd(&w.sum[3 * (size_t)t + 2], sz);
+            atomicAdd(&w.cnt[t], (uint32_t)__popc(peers));
+            atomicMin(&w.first[t], (uint32_t)i);
+        }
+        s = __shfl_sync(0xffffffffu, s, leader);
+        if (valid) w.slot[i] = s;
     }
 }
 

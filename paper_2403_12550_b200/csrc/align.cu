@@ -598,8 +598,9 @@ __device__ __forceinline__ bool chol6_solve(const double *H, const double *rhs, 
 // (sAcc layout), [41] lambda, [42] 1 once a pose was kept
 constexpr int kLmState = 44;
 
-__device__ __forceinline__ int solve_step(const AlignArgs &a, const double *sAcc, double *sT, int it, int n, int &status,
-                                       int &iters, int &converged, double *sLM) {
+template <bool LM>
+__device__ __forceinline__ int solve_step_t(const AlignArgs &a, const double *sAcc, double *sT, int it, int n,
+                                         int &status, int &iters, int &converged, double *sLM) {
     double H[36], b[6];
     int t = 0;
     for (int r = 0; r < 6; ++r)
@@ -620,7 +621,7 @@ __device__ __forceinline__ int solve_step(const AlignArgs &a, const double *sAcc
         status = GSICP_ERR_DEGENERATE_FRAME;
         return 1;
     }
-    if (a.solver == 1) {
+    if constexpr (LM) {
         // Levenberg-Marquardt (R30): keep the trial pose iff its cost beats the kept one
         const bool enough = n_in >= (double)a.min_pairs;
         const bool accept = it == 0 ? enough : (enough && sAcc[27] < sLM[12 + 27]);
@@ -677,7 +678,7 @@ __device__ __forceinline__ int solve_step(const AlignArgs &a, const double *sAcc
     }
     if (iters >= a.max_iters) {
         status = GSICP_WARN_MAX_ITERS;
-        if (a.solver == 1)
+        if constexpr (LM)
             for (int k = 0; k < 12; ++k) sT[k] = sLM[k];  // the best kept iterate
         return 1;
     }
@@ -803,6 +804,9 @@ __global__ void k_align_init(int32_t *corr_ws, int cap, unsigned int *barrier) {
 
 // The GN loop of one frame on blocks [0, G) of its own (bid = this block's index among them):
 // k_align runs one frame on the whole grid, k_align_batch several frames side by side.
+// LM: the solver is a template parameter, so the GN kernel carries no LM code (measured: an
+// inlined run-time branch cost the GN loop ~3 us per frame through register allocation)
+template <bool LM>
 __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, const int G) {
     __shared__ double sT[12];
     __shared__ double sRed[kWarps][kPad];
@@ -1140,8 +1144,8 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
             n_in = sAcc[28];
             cost_last = sAcc[27];
             int st_ = status, it_ = iters, cv_ = converged;
-            sDone = solve_step(a, sAcc, sT, it, n, st_, it_, cv_, sLM);
-            if (a.solver == 1 && !a.linearize_only && sLM[42] != 0.0) {  // stats of the kept linearisation
+            sDone = solve_step_t<LM>(a, sAcc, sT, it, n, st_, it_, cv_, sLM);
+            if (LM && !a.linearize_only && sLM[42] != 0.0) {  // stats of the kept linearisation
                 n_in = sLM[12 + 28];
                 cost_last = sLM[12 + 27];
             }
@@ -1170,9 +1174,10 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
     }
 }
 
+template <bool LM>
 __global__ void __launch_bounds__(kT, 1) k_align(AlignArgs a) {
     pdl_wait();  // (no early launch of dependents: they must not take SMs from this cooperative grid)
-    align_body(a, blockIdx.x, gridDim.x);
+    align_body<LM>(a, blockIdx.x, gridDim.x);
 }
 
 // N2 frame batch: frame f = blockIdx.x / Gf runs on blocks [f Gf, (f+1) Gf) with its own
@@ -1183,10 +1188,11 @@ struct AlignBatch {
     AlignArgs f[kMaxAlignBatch];
 };
 
+template <bool LM>
 __global__ void __launch_bounds__(kT, 1) k_align_batch(const __grid_constant__ AlignBatch b, int Gf) {
     pdl_wait();
     const int f = blockIdx.x / Gf;
-    align_body(b.f[f], blockIdx.x - f * Gf, Gf);
+    align_body<LM>(b.f[f], blockIdx.x - f * Gf, Gf);
 }
 
 __global__ void k_align_init_batch(const __grid_constant__ AlignBatch b) {
@@ -1205,7 +1211,10 @@ int align_grid_blocks(int cap, int *per_sm_out) {
     static int per_sm = -1;
     if (per_sm < 0) {
         int v = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_align, kT, 0) != cudaSuccess) v = 0;
+        int v1 = 0;  // the GN and LM kernels: the smaller residency of the two
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_align<false>, kT, 0) != cudaSuccess) v = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v1, k_align<true>, kT, 0) != cudaSuccess) v1 = 0;
+        v = v < v1 ? v : v1;
         per_sm = v;
     }
     *per_sm_out = per_sm;
@@ -1387,7 +1396,7 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
     const int G = align_grid_blocks(src.cap, &per_sm);
     if (G < 1) {
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, k_align);
+        cudaFuncGetAttributes(&fa, k_align<false>);
         set_error("k_align cannot be co-resident: occupancy %d blocks/SM (regs %d, local %zu B, max threads %d)",
                   per_sm, fa.numRegs, fa.localSizeBytes, fa.maxThreadsPerBlock);
         return cudaErrorCooperativeLaunchTooLarge;
@@ -1405,7 +1414,7 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
     cfg.attrs = at;
     cfg.numAttrs = 2;
     ktimer_mark(KT_ALIGN, false, s);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_align, a);
+    cudaError_t e = p.solver == 1 ? cudaLaunchKernelEx(&cfg, k_align<true>, a) : cudaLaunchKernelEx(&cfg, k_align<false>, a);
     ktimer_mark(KT_ALIGN, true, s);
     if (e != cudaSuccess) {
         set_error("k_align launch: %s", cudaGetErrorString(e));
@@ -1438,7 +1447,10 @@ cudaError_t align_batch_launch(const gsicp_cloud *srcs, int B, const gsicp_targe
     static int per_sm = -1;
     if (per_sm < 0) {
         int v = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_align_batch, kT, 0) != cudaSuccess) v = 0;
+        int v1 = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_align_batch<false>, kT, 0) != cudaSuccess) v = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v1, k_align_batch<true>, kT, 0) != cudaSuccess) v1 = 0;
+        v = v < v1 ? v : v1;
         per_sm = v;
     }
     int G = per_sm * num_sms();
@@ -1460,7 +1472,8 @@ cudaError_t align_batch_launch(const gsicp_cloud *srcs, int B, const gsicp_targe
     cfg.attrs = at;
     cfg.numAttrs = 2;
     ktimer_mark(KT_ALIGN, false, s);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_align_batch, hb, Gf);
+    cudaError_t e = p.solver == 1 ? cudaLaunchKernelEx(&cfg, k_align_batch<true>, hb, Gf)
+                                  : cudaLaunchKernelEx(&cfg, k_align_batch<false>, hb, Gf);
     ktimer_mark(KT_ALIGN, true, s);
     if (e != cudaSuccess) {
         set_error("k_align_batch launch: %s", cudaGetErrorString(e));

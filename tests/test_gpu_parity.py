@@ -836,3 +836,24 @@ def test_voxel_downsample(g, replica, tum, h):
     if h == 0.03:  # the voxel cloud through A2-A4 (hash path)
         cl = g.Cloud.from_points(out[:m, :3].contiguous())
         _cov_check(g, gp[:, :3].copy(), cl.pos, cl.d_n, cell0=2 * h, levels=1)
+
+
+def test_align_batch_lm(g):
+    """The LM solver in the batched kernel (k_align_batch<true>): each frame's pose equals
+    single-frame LM tracking's (1e-6)."""
+    seq = synth.make_sequence(4, 4, "replica", M=300_000)
+    rows = synth.render_sequence_rows(seq, DEV)
+    K = seq.K
+    prm = g.align_params(max_iters=30, max_corr_dist=0.1, solver=g.SOLVER_LM, lm_lambda0=1e-2)
+    tgt = g.build_target(t(seq.means), t(seq.quats), t(seq.scales))
+    init = np.stack([synth.perturb_pose(seq.T_gt[1 + b], 60 + b, 2.0, 0.03) for b in range(3)])
+    bt = g.BatchTracker(3, K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=seq.stride, params=prm)
+    bt.rows.copy_(rows[1:4])
+    Tb, stb = bt.track_rows(tgt, init)
+    tr = g.Tracker(K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=seq.stride, params=prm)
+    for b in range(3):
+        tr.rows.copy_(rows[1 + b])
+        Ts, sts = tr.track_rows(tgt, init[b])
+        assert rot_angle(Tb[b][:3, :3], Ts[:3, :3]) < 1e-6 and np.abs(Tb[b][:3, 3] - Ts[:3, 3]).max() < 1e-6
+        assert stb[b]["status"] == sts["status"] == g.OK
+        assert rot_angle(Tb[b][:3, :3], seq.T_gt[1 + b][:3, :3]) < math.radians(0.05)

@@ -857,3 +857,26 @@ def test_align_batch_lm(g):
         assert rot_angle(Tb[b][:3, :3], Ts[:3, :3]) < 1e-6 and np.abs(Tb[b][:3, 3] - Ts[:3, 3]).max() < 1e-6
         assert stb[b]["status"] == sts["status"] == g.OK
         assert rot_angle(Tb[b][:3, :3], seq.T_gt[1 + b][:3, :3]) < math.radians(0.05)
+
+
+def test_gaussian_map_capacity_and_unfiltered_insert(g, c1):
+    """GaussianMap: an insertion that could overflow the capacity raises before any launch; an
+    unfiltered insertion (corr None) appends every point at the pose (means == K3 of the oracle)."""
+    K = c1.K
+    pos, d_n = gpu_points(g, c1.depth, K, 1)
+    xyz, _ = oracle.backproject(c1.depth, K.fx, K.fy, K.cx, K.cy, 1)
+    n = xyz.shape[0]
+    cl = g.covariances(pos, d_n, cell0=0.05, levels=3)
+    m0 = np.zeros((10, 3), np.float32)
+    q0 = np.tile(np.float32([1, 0, 0, 0]), (10, 1))
+    s0 = np.full((10, 3), 0.01, np.float32)
+    gm = g.GaussianMap(t(m0), t(q0), t(s0), capacity=10 + n, cell=0.05)
+    T = np.eye(4)
+    T[:3, 3] = [0.5, -0.25, 1.0]
+    added = gm.insert(cl, t(T), None)
+    assert added == n and gm.M == 10 + n
+    om, _, _ = oracle.export_gaussians(xyz, oracle.covariances(xyz)["raw"], T=T)
+    np.testing.assert_array_equal(gm.means[10:10 + n].cpu().numpy(), om.astype(np.float32))
+    with pytest.raises(RuntimeError):
+        gm.insert(cl, t(T), None)  # 10 + 2n > capacity
+    assert gm.M == 10 + n

@@ -49,6 +49,7 @@ def lib():
         L.ora_kdtree_build.restype = P
         L.ora_kdtree_free.argtypes = [P]
         L.ora_kdtree_knn.argtypes = [P, P, i, i, P, P]
+        L.ora_kdtree_nn_d.argtypes = [P, P, i, P, P]
         L.ora_covariance.argtypes = [P, P, i, P]
         L.ora_eigen_jacobi.argtypes = [P, P, P]
         L.ora_regularize_eig.argtypes = [P, P, i, d, P]
@@ -112,18 +113,19 @@ def backproject(depth, fx, fy, cx, cy, stride=1, zmin=0.1, zmax=10.0):
 
 
 def knn_brute(xyz, k, queries=None, return_keys=False):
-    """O2 brute-force kNN.  queries: indices into xyz (default all).  -> idx (nq,k) int32 [, keys]"""
+    """O2 brute-force kNN by the binary64 K2 key, ties by index.  queries: indices into xyz
+    (default all).  -> idx (nq,k) int32 [, keys (nq,k) float64]"""
     xyz = _f32(xyz)
     n = xyz.shape[0]
     q = np.arange(n, dtype=np.int32) if queries is None else np.ascontiguousarray(queries, np.int32)
     out = np.empty((q.shape[0], k), np.int32)
-    keys = np.empty((q.shape[0], k), np.float32)
+    keys = np.empty((q.shape[0], k), np.float64)
     lib().ora_knn_brute(_p(xyz), n, _p(q), q.shape[0], k, _p(out), _p(keys))
     return (out, keys) if return_keys else out
 
 
 class KDTree:
-    """Exact kd-tree over binary32 points with the (key, idx) order of knn_brute."""
+    """Exact kd-tree over binary32 points with the (K2 key, idx) order of knn_brute."""
 
     def __init__(self, xyz):
         self.xyz = _f32(xyz)
@@ -133,9 +135,17 @@ class KDTree:
     def knn(self, q, k, return_keys=False):
         q = _f32(q).reshape(-1, 3)
         out = np.empty((q.shape[0], k), np.int32)
-        keys = np.empty((q.shape[0], k), np.float32)
+        keys = np.empty((q.shape[0], k), np.float64)
         lib().ora_kdtree_knn(C.c_void_p(self._t), _p(q), q.shape[0], k, _p(out), _p(keys))
         return (out, keys) if return_keys else out
+
+    def nn(self, q):
+        """1-NN of binary64 queries (n,3) by (K2, idx) -> (idx (n,) int32, key (n,) float64)."""
+        q = np.ascontiguousarray(np.asarray(q, np.float64).reshape(-1, 3))
+        out = np.empty(q.shape[0], np.int32)
+        keys = np.empty(q.shape[0], np.float64)
+        lib().ora_kdtree_nn_d(C.c_void_p(self._t), _p(q), q.shape[0], _p(out), _p(keys))
+        return out, keys
 
     def __del__(self):
         if getattr(self, "_t", None):

@@ -9,10 +9,11 @@
  * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
  * Rn = reading n listed in DESIGN.md §3 (Rn = SURVEY.md §8(c).3 Qn for n >= 3).
  *
- * Precision: all arithmetic in IEEE binary64 except where a floating-point value
- * decides an integer (kNN / NN membership): there both sides take the decision with
- * the kernel's canonical binary32 key (DESIGN.md §3 R1), evaluated here with
- * -ffp-contract=off so no FMA contraction changes the rounding.
+ * Precision: all arithmetic in IEEE binary64.  Where a floating-point value decides an
+ * integer (kNN / NN membership) the decision is taken on SURVEY §8(c).1's canonical binary64
+ * keys (DESIGN.md §3 R1): K2 key = (dx*dx + dy*dy) + dz*dz with dx = (double)a.x - (double)b.x,
+ * and for correspondences the query is the binary64 K3 transform itself (R15, no rounding of
+ * T x to binary32).  -ffp-contract=off: no FMA contraction changes the rounding.
  * Storage format: points and covariances are stored as binary32 (the hot path's
  * SoA format); the oracle rounds its binary64 results to binary32 where the format
  * stores them (DESIGN.md §3 R2).
@@ -69,25 +70,31 @@ int ora_backproject(const float *depth, int H, int W, int pitch, float fx, float
 }
 
 /* ------------------------------------------------------------------------- */
-/* Canonical binary32 squared-distance key (R1):
- * dx = a.x - b.x (binary32), key = (dx*dx + dy*dy) + dz*dz, left to right, no FMA. */
-static inline float ora_key(const float *a, const float *b) {
-    float dx = a[0] - b[0];
-    float dy = a[1] - b[1];
-    float dz = a[2] - b[2];
-    float s = dx * dx;
+/* Canonical binary64 squared-distance key K2: the query q in binary64
+ * (a binary32 cloud point widened exactly, or the binary64 K3 transform of one), b a binary32
+ * point widened exactly; dx = b.x - q.x (the sign is irrelevant: squares of negations are
+ * bit-identical), key = (dx*dx + dy*dy) + dz*dz, every op rounded separately, left to right. */
+static inline double ora_keyd(const double *q, const float *b) {
+    double dx = (double)b[0] - q[0];
+    double dy = (double)b[1] - q[1];
+    double dz = (double)b[2] - q[2];
+    double s = dx * dx;
     s = s + dy * dy;
     s = s + dz * dz;
     return s;
 }
+static inline double ora_key(const float *a, const float *b) {
+    double q[3] = {(double)a[0], (double)a[1], (double)a[2]};
+    return ora_keyd(q, b);
+}
 
 /* (key, idx) lexicographic "less than" — the kNN / NN order (R12). */
-static inline int ora_less(float ka, int ia, float kb, int ib) {
+static inline int ora_less(double ka, int ia, double kb, int ib) {
     return ka < kb || (ka == kb && ia < ib);
 }
 
 /* insert (key, idx) into the sorted list of length *len (capacity k) */
-static inline void ora_topk_insert(float *keys, int32_t *ids, int *len, int k, float key, int id) {
+static inline void ora_topk_insert(double *keys, int32_t *ids, int *len, int k, double key, int id) {
     int m = *len;
     if (m == k) {
         if (!ora_less(key, id, keys[k - 1], ids[k - 1])) return;
@@ -108,10 +115,10 @@ static inline void ora_topk_insert(float *keys, int32_t *ids, int *len, int k, f
  * S:64 self included; S:39 min(k,n) sorted; S:82 ties by lower index).
  * For each query q in qidx[0..nq): out_idx[q*k + j] = j-th neighbour, -1 pads when n<k.
  * out_key (nullable) gets the keys. */
-void ora_knn_brute(const float *xyz, int n, const int32_t *qidx, int nq, int k, int32_t *out_idx, float *out_key) {
+void ora_knn_brute(const float *xyz, int n, const int32_t *qidx, int nq, int k, int32_t *out_idx, double *out_key) {
 #pragma omp parallel for schedule(dynamic, 64)
     for (int qi = 0; qi < nq; ++qi) {
-        float keys[256];
+        double keys[256];
         int32_t ids[256];
         int len = 0;
         const float *q = xyz + 3 * (int64_t)qidx[qi];
@@ -126,9 +133,10 @@ void ora_knn_brute(const float *xyz, int n, const int32_t *qidx, int nq, int k, 
 /* ------------------------------------------------------------------------- */
 /* Exact kd-tree over binary32 points (speed-up for large clouds; validated against
  * ora_knn_brute and scipy's cKDTree in tests).  Split values are point coordinates,
- * so a subtree across a split plane s can be skipped iff the binary32 key of the
- * plane offset, fl(fl(q_a - s)^2), exceeds the current k-th key: rounding is
- * monotone, so every point p behind the plane has key(q,p) >= that plane key. */
+ * so a subtree across a split plane s can be skipped iff the binary64 plane key
+ * fl(fl(q_a - s)^2) exceeds the current k-th key: rounding is monotone and every K2 key is
+ * a rounded sum of non-negative terms, so every point p behind the plane has
+ * key(q, p) >= fl((q_a - p_a)^2) >= that plane key. */
 typedef struct {
     int32_t *perm;   /* point ids in tree order */
     int32_t *lo, *hi; /* node range */
@@ -204,37 +212,52 @@ void ora_kdtree_free(void *p) {
     free(t);
 }
 
-static void ora_kd_search(const ora_kdtree *t, int node, const float *q, int k, float *keys, int32_t *ids, int *len) {
+static void ora_kd_search(const ora_kdtree *t, int node, const double *q, int k, double *keys, int32_t *ids, int *len) {
     if (t->axis[node] < 0) {
         for (int i = t->lo[node]; i < t->hi[node]; ++i) {
             int id = t->perm[i];
-            ora_topk_insert(keys, ids, len, k, ora_key(q, t->xyz + 3 * (int64_t)id), id);
+            ora_topk_insert(keys, ids, len, k, ora_keyd(q, t->xyz + 3 * (int64_t)id), id);
         }
         return;
     }
     int ax = t->axis[node];
-    float s = t->split[node];
-    float d = q[ax] - s;
+    double d = q[ax] - (double)t->split[node];
     int first = d <= 0 ? t->left[node] : t->right[node];
     int second = d <= 0 ? t->right[node] : t->left[node];
     ora_kd_search(t, first, q, k, keys, ids, len);
-    float pk = d * d;
+    double pk = d * d;
     if (*len < k || !(pk > keys[*len - 1])) ora_kd_search(t, second, q, k, keys, ids, len);
 }
 
-/* kNN of arbitrary query positions q[nq][3] against the tree's points (same order/ties as brute force). */
-void ora_kdtree_knn(const void *tree, const float *q, int nq, int k, int32_t *out_idx, float *out_key) {
+/* kNN of arbitrary binary32 query positions q[nq][3] against the tree's points (same order/ties
+ * as brute force). */
+void ora_kdtree_knn(const void *tree, const float *q, int nq, int k, int32_t *out_idx, double *out_key) {
     const ora_kdtree *t = (const ora_kdtree *)tree;
 #pragma omp parallel for schedule(dynamic, 256)
     for (int i = 0; i < nq; ++i) {
-        float keys[256];
+        double keys[256];
         int32_t ids[256];
         int len = 0;
-        if (t->nnodes > 0) ora_kd_search(t, 0, q + 3 * (int64_t)i, k, keys, ids, &len);
+        double qd[3] = {(double)q[3 * (int64_t)i], (double)q[3 * (int64_t)i + 1], (double)q[3 * (int64_t)i + 2]};
+        if (t->nnodes > 0) ora_kd_search(t, 0, qd, k, keys, ids, &len);
         for (int j = 0; j < k; ++j) {
             out_idx[(int64_t)i * k + j] = j < len ? ids[j] : -1;
             if (out_key) out_key[(int64_t)i * k + j] = j < len ? keys[j] : INFINITY;
         }
+    }
+}
+
+/* 1-NN of binary64 queries (the K3 transforms of O7) by (K2, index); -1 / inf if the tree is empty. */
+void ora_kdtree_nn_d(const void *tree, const double *q, int nq, int32_t *out_idx, double *out_key) {
+    const ora_kdtree *t = (const ora_kdtree *)tree;
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int i = 0; i < nq; ++i) {
+        double key = INFINITY;
+        int32_t id = -1;
+        int len = 0;
+        if (t->nnodes > 0) ora_kd_search(t, 0, q + 3 * (int64_t)i, 1, &key, &id, &len);
+        out_idx[i] = len ? id : -1;
+        out_key[i] = len ? key : INFINITY;
     }
 }
 
@@ -478,33 +501,31 @@ static int ora_inv_spd3(double S[3][3], double Mi[3][3]) {
 }
 
 /* O7 + O8: correspondences and linearisation of Eq. 1 at pose T.
- * O7: q_i = K3(T, x_i); j* = argmin over (key(fl32(q_i), m_j), j) ("nearest neighbor");
- *     valid iff key < fl32(r*r) (strict, R15).
+ * O7: q_i = K3(T, x_i) in binary64; j* = argmin over (K2(q_i, m_j), j) ("nearest neighbor",
+ *     R15); valid iff key < r^2 with r^2 = (double)r * (double)r (strict, R15).
  * O8: Sigma_i = C^t_j + R C^s_i R^T (R3), M_i = Sigma_i^{-1}, d_i = m_j - q_i,
  *     J_i = [[q_i]x, -I] (left twist (omega, v), R16), H = sum J^T M J, b = sum J^T M d,
- *     cost = sum d^T M d (Eq. 1), summed in index order in binary64.
+ *     cost = sum d^T M d (Eq. 1), summed in index order in binary64.  A pair whose Sigma is not
+ *     positive definite is skipped (after R31).
  * tree: kd-tree over tgt_xyz or NULL (brute force).  H row-major 36, b 6.  corr (nullable).
  * Returns the inlier count. */
 int ora_linearize(const float *src_xyz, const float *src_cov, int n, const float *tgt_xyz, const float *tgt_cov,
                   int M, const void *tree, const double *T, float max_corr_dist, double *H, double *b,
                   double *cost, int32_t *corr) {
-    float r2 = max_corr_dist * max_corr_dist;
+    double r2 = (double)max_corr_dist * (double)max_corr_dist;
     double *contrib = (double *)calloc((size_t)(n > 0 ? n : 1) * 28, sizeof(double));
     int32_t *cj = (int32_t *)malloc(sizeof(int32_t) * (n > 0 ? n : 1));
 #pragma omp parallel for schedule(dynamic, 256)
     for (int i = 0; i < n; ++i) {
         double q[3];
         ora_transform(T, src_xyz + 3 * (int64_t)i, q);
-        float qf[3] = {(float)q[0], (float)q[1], (float)q[2]};
         int best = -1;
-        float bk = INFINITY;
+        double bk = INFINITY;
         if (tree) {
-            int32_t id; float kk;
-            ora_kdtree_knn(tree, qf, 1, 1, &id, &kk);
-            best = id; bk = kk;
+            ora_kdtree_nn_d(tree, q, 1, &best, &bk);
         } else {
             for (int j = 0; j < M; ++j) {
-                float kk = ora_key(qf, tgt_xyz + 3 * (int64_t)j);
+                double kk = ora_keyd(q, tgt_xyz + 3 * (int64_t)j);
                 if (best < 0 || ora_less(kk, j, bk, best)) { bk = kk; best = j; }
             }
         }

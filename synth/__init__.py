@@ -21,7 +21,7 @@ __all__ = [
     "Intrinsics", "REPLICA", "TUM", "TINY", "Scene", "make_scene", "raycast_depth",
     "tum_noise", "sample_map", "camera_pose", "perturb_pose", "rot_axis_angle",
     "make_frame_workload", "make_c1", "quat_from_rotmat", "raycast_depth_torch", "lissajous_trajectory",
-    "make_sequence", "Sequence", "render_sequence_rows", "trajectory_error",
+    "make_sequence", "Sequence", "render_sequence_rows", "trajectory_error", "fronto_parallel_wall",
 ]
 
 
@@ -392,6 +392,17 @@ def make_c1(cfg: int = 1) -> C1Workload:
     Tg[:3, :3] = rot_axis_angle(rng.standard_normal(3), math.radians(8.0))
     Tg[:3, 3] = [0.05, -0.08, 0.03]
     return C1Workload(TINY, depth, Tg)
+
+
+def fronto_parallel_wall(K: Intrinsics = REPLICA, z: float = 2.0, hole=None) -> np.ndarray:
+    """Depth of a wall parallel to the image plane at distance z (the tie-heavy case of SURVEY
+    hard part 1: back-projected stride lattices give many equal squared distances).  hole =
+    (v0, v1, u0, u1) pixels set invalid (NaN)."""
+    depth = np.full((K.H, K.W), z, np.float32)
+    if hole is not None:
+        v0, v1, u0, u1 = hole
+        depth[v0:v1, u0:u1] = np.nan
+    return depth
 
 
 # ------------------------------------------------------------------------------------------ C5

@@ -1,9 +1,11 @@
 """Pins of the oracle's O1 (back-projection) and O2 (exact kNN), CPU only.
 
 O1 is pinned to SPEC's worked examples (tests/golden/spec_examples.json) and to the
-projection round trip.  O2 is pinned to brute force == kd-tree on tie-heavy data, to
-scipy's cKDTree (a library routine, re-ranked by the canonical binary32 key), to the analytic
-neighbour shells of an integer lattice, and to permutation invariance.
+projection round trip.  O2 (binary64 K2 key, DESIGN R1) is pinned to
+brute force == kd-tree on tie-heavy data, to scipy's cKDTree (a library routine, re-ranked by
+the key), to the analytic neighbour shells of an integer lattice, to permutation invariance
+(S:74), and on the tie-heavy fronto-parallel wall to a numpy float64 lexsort brute force and to
+EXACT integer distances (ties by index).
 """
 import json
 import os
@@ -63,8 +65,8 @@ def test_backproject_roundtrip():
 
 
 def _canonical_keys(q, P):
-    """binary32 key evaluated with numpy float32 ops (separate rounding per op, no FMA)."""
-    d = (q[None, :].astype(np.float32) - P.astype(np.float32))
+    """binary64 key evaluated with numpy float64 ops (separate rounding per op, no FMA)."""
+    d = (q[None, :].astype(np.float64) - P.astype(np.float64))
     s = d[:, 0] * d[:, 0]
     s = s + d[:, 1] * d[:, 1]
     return s + d[:, 2] * d[:, 2]
@@ -136,3 +138,64 @@ def test_knn_low_support_pads():
     out = oracle.covariances(P, k=20)
     assert (out["flags"] & oracle.FLAG_LOW_SUPPORT).all()
 
+
+
+# ---------------------------------------------------------------------------------------------
+# the kNN order is the binary64 key, not a binary32 one (R1).  Pinned on the
+# tie-heavy fronto-parallel wall (SURVEY hard part 1) against (a) a numpy float64 lexsort brute
+# force and (b) EXACT rational distances (Python integers), ties by index.
+def _wall_cloud(stride=4):
+    import synth
+
+    K = synth.REPLICA
+    xyz, _ = oracle.backproject(synth.fronto_parallel_wall(K), K.fx, K.fy, K.cx, K.cy, stride)
+    return xyz
+
+
+def _exact_sqdist(q, P):
+    """Exact squared distances of binary32 points as Python integers (coordinates scaled by 2^64:
+    every binary32 coordinate here is a multiple of 2^-64, so the scaling is exact)."""
+    def ints(a):
+        return [[int(np.float64(v) * 2.0 ** 64) for v in row] for row in np.atleast_2d(a)]
+
+    (qi,) = ints(q)
+    return [sum((c - d) ** 2 for c, d in zip(qi, p)) for p in ints(P)]
+
+
+def test_knn_binary64_key_on_fronto_parallel_wall():
+    P = _wall_cloud()
+    assert P.shape[0] == 51_000
+    assert np.all(np.abs(P[:, :2][P[:, :2] != 0]) >= 2.0 ** -40)  # the 2^64 scaling is exact
+    k = 20
+    queries = np.arange(0, P.shape[0], 85, dtype=np.int32)  # 600 queries
+    idx, keys = oracle.knn_brute(P, k, queries=queries, return_keys=True)
+    Pd = P.astype(np.float64)
+    n_f32_differs = 0
+    for r, qi in enumerate(queries):
+        d = Pd - Pd[qi]
+        key = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
+        order = np.lexsort((np.arange(P.shape[0]), key))
+        np.testing.assert_array_equal(idx[r], order[:k])  # (a) float64 lexsort brute force
+        np.testing.assert_array_equal(keys[r], key[order[:k]])
+        # (b) exact: rank the 64 nearest candidates by exact integer distance, ties by index;
+        # everything outside them is farther than the k-th (float64 error << the gap asserted)
+        cand = order[:64]
+        ex = _exact_sqdist(P[qi], P[cand])
+        ranked = sorted(zip(ex, cand.tolist()))
+        assert [c for _, c in ranked[:k]] == idx[r].tolist()
+        assert ranked[k - 1][0] < ranked[-1][0]
+        # the binary32 key would pick another neighbour SET on some queries (sensitivity of this pin)
+        d32 = P - P[qi]
+        k32 = (d32[:, 0] * d32[:, 0] + d32[:, 1] * d32[:, 1]) + d32[:, 2] * d32[:, 2]
+        o32 = np.lexsort((np.arange(P.shape[0]), k32))
+        n_f32_differs += int(set(o32[:k].tolist()) != set(idx[r].tolist()))
+    assert n_f32_differs >= 5, n_f32_differs
+
+
+def test_kdtree_equals_brute_on_wall_binary64():
+    P = _wall_cloud()
+    q = np.arange(0, P.shape[0], 97, dtype=np.int32)
+    a, ka = oracle.knn_brute(P, 20, queries=q, return_keys=True)
+    b, kb = oracle.KDTree(P).knn(P[q], 20, return_keys=True)
+    np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(ka, kb)

@@ -302,3 +302,66 @@ def test_lm_point_to_point_equals_kabsch_and_best_iterate_at_cap():
         assert b["status"] == oracle.MAX_ITERS
         cb = oracle.linearize(src, half, tgt, half, b["T"], max_corr_dist=0.2)["cost"]
         assert cb <= c0
+
+
+# ------------------------------------------------------------------ O7 on the binary64 query (R15)
+_HALF_I = pack(np.eye(3) / 2.0).astype(np.float32)
+
+
+def test_nn_uses_binary64_query_not_its_binary32_rounding():
+    """q = K3(T, x) = 1 + 2^-23 - 2^-30 (x = 1 + 2^-23, t = -2^-30): exactly one of two targets
+    1 and 1 + 2^-22 is nearer (distances 2^-23 - 2^-30 vs 2^-23 + 2^-30), but fl32(q) = 1 + 2^-23
+    is their midpoint (a binary32 tie, which the lower index, the farther target, would win)."""
+    x = np.float32([[1.0 + 2.0 ** -23, 0.0, 0.0]])
+    assert float(x[0, 0]) == 1.0 + 2.0 ** -23
+    tgt = np.float32([[1.0 + 2.0 ** -22, 0, 0], [1.0, 0, 0]])  # index 0 is the farther one
+    T = np.eye(4)
+    T[0, 3] = -(2.0 ** -30)
+    r = oracle.linearize(x, _HALF_I[None], tgt, np.repeat(_HALF_I[None], 2, 0), T)
+    assert r["corr"][0] == 1
+    # exact rational check of the claim
+    q = 1.0 + 2.0 ** -23 - 2.0 ** -30
+    assert abs(q - 1.0) < abs(q - (1.0 + 2.0 ** -22))
+    assert np.float32(q) == np.float32(1.0 + 2.0 ** -23)
+    # the kd-tree path takes the same decision
+    r2 = oracle.linearize(x, _HALF_I[None], tgt, np.repeat(_HALF_I[None], 2, 0), T, tree=oracle.KDTree(tgt))
+    assert r2["corr"][0] == 1
+
+
+def test_nn_equal_distance_tie_goes_to_lower_index():
+    x = np.float32([[0.0, 0.0, 0.0]])
+    tgt = np.float32([[0, 0.25, 0], [0.25, 0, 0], [0, 0, -0.25]])  # all at exactly 1/4
+    r = oracle.linearize(x, _HALF_I[None], tgt, np.repeat(_HALF_I[None], 3, 0), np.eye(4))
+    assert r["corr"][0] == 0
+
+
+def test_correspondence_gate_is_strict():
+    """R15: valid iff key < r^2.  A target at exactly r (0.5: key 0.25 = r^2) is rejected; one
+    binary32 ulp closer is accepted."""
+    x = np.zeros((1, 3), np.float32)
+    for d, valid in ((0.5, False), (float(np.nextafter(np.float32(0.5), np.float32(0))), True)):
+        tgt = np.float32([[d, 0, 0]])
+        r = oracle.linearize(x, _HALF_I[None], tgt, _HALF_I[None], np.eye(4), max_corr_dist=0.5)
+        assert (r["n"] == 1) == valid and (r["corr"][0] == 0) == valid
+
+
+def test_non_pd_sigma_pair_is_skipped():
+    """A pair whose Sigma = C^t + R C^s R^T is not positive definite contributes nothing."""
+    x = np.float32([[0, 0, 0], [1, 0, 0]])
+    tgt = np.float32([[0, 0, 0.01], [1, 0, 0.01]])
+    zero = np.zeros(6, np.float32)
+    r = oracle.linearize(x, np.stack([zero, _HALF_I]), tgt, np.stack([zero, _HALF_I]), np.eye(4))
+    assert r["n"] == 1 and r["corr"][0] == -1 and r["corr"][1] == 1
+    np.testing.assert_allclose(r["cost"], np.float64(np.float32(0.01)) ** 2, rtol=1e-12)  # M = I
+
+
+def test_solve_pd_fallback():
+    """A8/O9: a singular H (zero eigenvalue) is solved as H + 1e-6 tr(H)/6 I (numpy.linalg.solve);
+    a negative definite H fails both attempts."""
+    H = np.diag([1.0, 2.0, 3.0, 4.0, 5.0, 0.0])
+    b = np.array([1.0, -1.0, 2.0, 0.5, 1.0, 0.25])
+    x, ok = oracle.solve(H, b)
+    assert ok
+    np.testing.assert_allclose(x, np.linalg.solve(H + 1e-6 * 15.0 / 6.0 * np.eye(6), -b), rtol=1e-12)
+    x, ok = oracle.solve(-np.eye(6), b)
+    assert not ok

@@ -283,6 +283,16 @@ void gsicp_debug_align_timeline(int64_t *d_out, int64_t capacity);
  * summed over the GN iterations (int32, device, >= 4*cap entries).  NULL switches it off. */
 void gsicp_debug_align_counters(int32_t *d_out);
 
+/* DIAGNOSTIC (per-iteration parity, SURVEY §8(c).5 "per-iteration H/b"): while set (d_rec
+ * non-NULL, max_iters > 0) on the calling thread, every align launch (and frame 0 of a batch)
+ * records, for each Gauss-Newton iteration it < max_iters that runs, d_rec[48*it + 0..11] = the
+ * pose T_it the iteration linearised at (row-major 3x4, binary64) and d_rec[48*it + 12..40] = its
+ * reduced Eq. 1 terms (21 upper-triangular H entries row by row, b[6], cost, inlier count);
+ * d_corr (nullable, int32[max_iters * src cap]) gets d_corr[it*cap + i] = point i's
+ * correspondence in that iteration (original target index, -1 none).  Device memory of the caller;
+ * the pointers are baked into CUDA graphs captured while set.  NULL switches it off. */
+void gsicp_debug_align_iterations(double *d_rec, int32_t *d_corr, int32_t max_iters);
+
 /* DIAGNOSTIC: kernel timer.  While enabled (1: spans 0-2 below; 2: all spans) on the calling
  * thread, the launches of the hot kernels record a CUDA event pair around themselves on their stream (also inside a
  * stream capture: the events then record at every graph replay).  gsicp_debug_kernel_time

@@ -60,6 +60,8 @@ def lib():
         L.ora_target_from_map.argtypes = [P, P, i, i, i, d, P, P]
         L.ora_linearize.argtypes = [P, P, i, P, P, i, P, P, f, P, P, P, P]
         L.ora_linearize.restype = i
+        L.ora_linearize_ex.argtypes = [P, P, i, P, P, i, P, P, f, P, P, P, P, P]
+        L.ora_linearize_ex.restype = i
         L.ora_solve.argtypes = [P, P, P]
         L.ora_solve.restype = i
         L.ora_so3_exp.argtypes = [P, P]
@@ -211,17 +213,19 @@ def target_from_map(quats, scales, mode=ELLIPSE, eps=1e-3, scales_are_log=False)
 
 
 def linearize(src_xyz, src_cov, tgt_xyz, tgt_cov, T, max_corr_dist=np.inf, tree: KDTree | None = None):
-    """O7+O8 -> dict(H (6,6), b (6,), cost, n, corr (n,) int32)."""
+    """O7+O8 -> dict(H (6,6), b (6,), cost, n, corr (n,) int32, bsum = sum_i |J_i^T M_i d_i|)."""
     src_xyz, src_cov, tgt_xyz, tgt_cov = map(_f32, (src_xyz, src_cov, tgt_xyz, tgt_cov))
     T = np.ascontiguousarray(T, np.float64)
     H = np.empty((6, 6))
     b = np.empty(6)
     cost = np.empty(1)
+    bsum = np.empty(1)
     corr = np.empty(src_xyz.shape[0], np.int32)
     t = C.c_void_p(tree._t) if tree is not None else None
-    n = lib().ora_linearize(_p(src_xyz), _p(src_cov), src_xyz.shape[0], _p(tgt_xyz), _p(tgt_cov),
-                            tgt_xyz.shape[0], t, _p(T), float(max_corr_dist), _p(H), _p(b), _p(cost), _p(corr))
-    return dict(H=H, b=b, cost=float(cost[0]), n=n, corr=corr)
+    n = lib().ora_linearize_ex(_p(src_xyz), _p(src_cov), src_xyz.shape[0], _p(tgt_xyz), _p(tgt_cov),
+                               tgt_xyz.shape[0], t, _p(T), float(max_corr_dist), _p(H), _p(b), _p(cost), _p(corr),
+                               _p(bsum))
+    return dict(H=H, b=b, cost=float(cost[0]), n=n, corr=corr, bsum=float(bsum[0]))
 
 
 def solve(H, b):

@@ -509,9 +509,19 @@ static int ora_inv_spd3(double S[3][3], double Mi[3][3]) {
  *     positive definite is skipped (after R31).
  * tree: kd-tree over tgt_xyz or NULL (brute force).  H row-major 36, b 6.  corr (nullable).
  * Returns the inlier count. */
+/* bsum (nullable): sum over the valid pairs of |J_i^T M_i d_i| — the scale of SURVEY §8(c).5's
+ * per-iteration b tolerance (b itself -> 0 at the optimum). */
+int ora_linearize_ex(const float *src_xyz, const float *src_cov, int n, const float *tgt_xyz, const float *tgt_cov,
+                     int M, const void *tree, const double *T, float max_corr_dist, double *H, double *b,
+                     double *cost, int32_t *corr, double *bsum);
 int ora_linearize(const float *src_xyz, const float *src_cov, int n, const float *tgt_xyz, const float *tgt_cov,
                   int M, const void *tree, const double *T, float max_corr_dist, double *H, double *b,
                   double *cost, int32_t *corr) {
+    return ora_linearize_ex(src_xyz, src_cov, n, tgt_xyz, tgt_cov, M, tree, T, max_corr_dist, H, b, cost, corr, NULL);
+}
+int ora_linearize_ex(const float *src_xyz, const float *src_cov, int n, const float *tgt_xyz, const float *tgt_cov,
+                     int M, const void *tree, const double *T, float max_corr_dist, double *H, double *b,
+                     double *cost, int32_t *corr, double *bsum) {
     double r2 = (double)max_corr_dist * (double)max_corr_dist;
     double *contrib = (double *)calloc((size_t)(n > 0 ? n : 1) * 28, sizeof(double));
     int32_t *cj = (int32_t *)malloc(sizeof(int32_t) * (n > 0 ? n : 1));
@@ -571,14 +581,17 @@ int ora_linearize(const float *src_xyz, const float *src_cov, int n, const float
         for (int r = 0; r < 6; ++r) o[21 + r] = J[0][r] * Md[0] + J[1][r] * Md[1] + J[2][r] * Md[2];
         o[27] = d[0] * Md[0] + d[1] * Md[1] + d[2] * Md[2];
     }
-    double acc[28] = {0};
+    double acc[28] = {0}, bs = 0.0;
     int cnt = 0;
     for (int i = 0; i < n; ++i) {
         if (corr) corr[i] = cj[i];
         if (cj[i] < 0) continue;
         ++cnt;
         for (int t = 0; t < 28; ++t) acc[t] += contrib[(int64_t)i * 28 + t];
+        const double *bi = contrib + (int64_t)i * 28 + 21;
+        bs += sqrt(bi[0] * bi[0] + bi[1] * bi[1] + bi[2] * bi[2] + bi[3] * bi[3] + bi[4] * bi[4] + bi[5] * bi[5]);
     }
+    if (bsum) *bsum = bs;
     int t = 0;
     for (int r = 0; r < 6; ++r)
         for (int c = r; c < 6; ++c) { H[6 * r + c] = H[6 * c + r] = acc[t++]; }

@@ -114,6 +114,8 @@ def lib():
         L.gsicp_debug_align_timeline.restype = None
         L.gsicp_debug_align_counters.argtypes = [P]
         L.gsicp_debug_align_counters.restype = None
+        L.gsicp_debug_align_iterations.argtypes = [P, P, i32]
+        L.gsicp_debug_align_iterations.restype = None
         L.gsicp_pose_predict.argtypes = [P, P, P]
         L.gsicp_pose_push.argtypes = [P, P, P, P, i32, P]
         L.gsicp_export_gaussians.argtypes = [P, P, P, P, i32, P, C.c_double, C.c_double, P, P, P, P, P, P, sz, P]
@@ -156,7 +158,8 @@ EXPORTED = [
     "gsicp_align_workspace_size", "gsicp_align", "gsicp_align_async", "gsicp_align_seed", "gsicp_linearize",
     "gsicp_status_string",
     "gsicp_last_error", "gsicp_kernel_launch_count", "gsicp_abi_version", "gsicp_debug_knn_counters",
-    "gsicp_debug_align_timeline", "gsicp_debug_align_counters", "gsicp_debug_kernel_timer",
+    "gsicp_debug_align_timeline", "gsicp_debug_align_counters", "gsicp_debug_align_iterations",
+    "gsicp_debug_kernel_timer",
     "gsicp_debug_kernel_time", "gsicp_graph_instantiate", "gsicp_graph_launch", "gsicp_graph_destroy",
     "gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_workspace_size", "gsicp_export_gaussians",
     "gsicp_align_batch_max", "gsicp_align_batch_async", "gsicp_voxel_downsample_workspace_size",
@@ -181,6 +184,48 @@ def debug_align_counters(out: torch.Tensor | None):
     """Diagnostic: while set, align/linearize write (queued searches, reuses, graph certificates, iterations)
     per resident source point into `out` ((cap, 4) int32 CUDA tensor); None switches it off."""
     lib().gsicp_debug_align_counters(_ptr(out) if out is not None else None)
+
+
+class AlignIterations:
+    """Diagnostic (per-iteration parity): while active, align launches record every GN iteration's
+    pose T_it and reduced Eq. 1 terms, and each point's correspondence (gsicp_debug_align_iterations).
+    Usage: with AlignIterations(max_iters, src_cap) as rec: ... ; rec.iterations() after a sync."""
+
+    REC = 48
+
+    def __init__(self, max_iters: int, cap: int, device="cuda"):
+        self.max_iters, self.cap = int(max_iters), int(cap)
+        self.rec = torch.full((self.max_iters, self.REC), float("nan"), dtype=torch.float64, device=device)
+        self.corr = torch.full((self.max_iters, self.cap), -3, dtype=torch.int32, device=device)
+
+    def __enter__(self):
+        lib().gsicp_debug_align_iterations(_ptr(self.rec), _ptr(self.corr), self.max_iters)
+        return self
+
+    def __exit__(self, *exc):
+        lib().gsicp_debug_align_iterations(None, None, 0)
+        return False
+
+    def iterations(self, n_points: int | None = None) -> list[dict]:
+        """[{T (4,4), H (6,6), b (6,), cost, n, corr (n_points,)}] for the iterations that ran."""
+        rec = self.rec.cpu().numpy()
+        corr = self.corr.cpu().numpy()
+        out = []
+        for it in range(self.max_iters):
+            r = rec[it]
+            if np.isnan(r[0]):
+                break
+            T = np.eye(4)
+            T[:3, :] = r[:12].reshape(3, 4)
+            H = np.zeros((6, 6))
+            k = 12
+            for a_ in range(6):
+                for b_ in range(a_, 6):
+                    H[a_, b_] = H[b_, a_] = r[k]
+                    k += 1
+            out.append(dict(T=T, H=H, b=r[33:39].copy(), cost=float(r[39]), n=int(r[40]),
+                            corr=corr[it, :(n_points if n_points is not None else self.cap)].copy()))
+        return out
 
 
 def debug_align_timeline(out: torch.Tensor | None):
@@ -275,10 +320,22 @@ class Cloud:
         return c
 
 
+def _check_depth(depth: torch.Tensor, what: str = "depth"):
+    """A depth image handed to the library: a 2-D float32 CUDA tensor with unit column stride (the
+    row pitch is passed on); anything else would be misread, so it is rejected here."""
+    if not isinstance(depth, torch.Tensor) or not depth.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor")
+    if depth.dtype != torch.float32:
+        raise ValueError(f"{what} must be float32 metres (got {depth.dtype})")
+    if depth.dim() != 2 or depth.stride(1) != 1 or depth.stride(0) < depth.shape[1]:
+        raise ValueError(f"{what} must be a 2-D row-major view with unit column stride")
+
+
 def backproject_downsample(depth: torch.Tensor, K, stride: int = 4, z_min: float = 0.1, z_max: float = 10.0,
                            pos_out: torch.Tensor | None = None, d_n: torch.Tensor | None = None,
                            ws: torch.Tensor | None = None, stream=None):
     """A1.  depth: (H, W) f32 metres on the GPU.  Returns (pos (cap, 4), d_n (1,))."""
+    _check_depth(depth)
     H, W = depth.shape
     pitch = depth.stride(0)
     cap = ((H + stride - 1) // stride) * ((W + stride - 1) // stride)
@@ -302,6 +359,9 @@ def backproject_sampled_rows(rows: torch.Tensor, H: int, W: int, K, stride: int 
                              d_n: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
     """A1 from only the sampled rows (rows[r] = image row r*stride): same output as
     backproject_downsample on the full (H, W) image."""
+    _check_depth(rows, "rows")
+    if rows.shape != ((H + stride - 1) // stride, W):
+        raise ValueError(f"rows must be ({(H + stride - 1) // stride}, {W})")
     pitch = rows.stride(0)
     cap = ((H + stride - 1) // stride) * ((W + stride - 1) // stride)
     dev = rows.device
@@ -324,6 +384,9 @@ def backproject_lattice(depth: torch.Tensor, H: int, W: int, K, stride: int = 4,
                         ws: torch.Tensor | None = None, stream=None):
     """A1 (from the full image, or from its sampled rows) that also writes the lattice map
     (output index of every sampled pixel, -1 if invalid).  Returns (pos, d_n, lattice)."""
+    _check_depth(depth)
+    if depth.shape != (((H + stride - 1) // stride, W) if rows_sampled else (H, W)):
+        raise ValueError(f"depth shape {tuple(depth.shape)} does not match H={H}, W={W}, stride={stride}")
     pitch = depth.stride(0)
     Hs, Ws = (H + stride - 1) // stride, (W + stride - 1) // stride
     dev = depth.device
@@ -637,6 +700,7 @@ class Tracker:
         self._join = torch.cuda.Event()
         self._fork.record(torch.cuda.current_stream(self.device))  # creates the event (handle passed to C)
         self._graphs = {}
+        self._depth = None  # staging buffer of track()
         self._T_host = torch.zeros(16, dtype=torch.float64).pin_memory()
         self._T_out = torch.zeros(16, dtype=torch.float64).pin_memory()
         self._st_out = torch.zeros(C.sizeof(AlignStats), dtype=torch.uint8).pin_memory()
@@ -672,16 +736,12 @@ class Tracker:
         # the iteration-0 correspondences need only the points: on a side stream, forked right
         # after A1 (measured: forking after the window kernel — the SM-heavy part of A2-A4 — speeds
         # that kernel up but the ~55-80 us seed pass then ends after A2-A4 and delays A6-A9)
-        seed = os.environ.get("GSICP_NO_SEED", "0") != "1"  # (A/B diagnostic switch)
-        early = os.environ.get("GSICP_SEED_EARLY", "1") == "1"  # (A/B: 0 = fork after the window)
-        if seed and early:
-            self._fork.record(s0)
-        self._covariances(s0, self._fork if seed and not early else None)
-        if seed:
-            self._side.wait_event(self._fork)
-            align_seed(self.cloud, tgt, self.d_T, self.params, self.ws_align, self._side)
-            self._join.record(self._side)
-            s0.wait_event(self._join)
+        self._fork.record(s0)
+        self._covariances(s0)
+        self._side.wait_event(self._fork)
+        align_seed(self.cloud, tgt, self.d_T, self.params, self.ws_align, self._side)
+        self._join.record(self._side)
+        s0.wait_event(self._join)
         if events:
             events[2].record(s0)
         align_async(self.cloud, tgt, self.d_T, self.d_stats, self.params, self.ws_align, self.corr, s0)
@@ -720,9 +780,16 @@ class Tracker:
         return self._T_out.numpy().reshape(4, 4).copy(), stats
 
     def track(self, depth: torch.Tensor, tgt: Target, init_T, stream=None):
-        """Whole frame from a device depth image: host pose in, (T, stats) out (blocking)."""
-        key = ("dev", depth.data_ptr(), tuple(depth.shape), tuple(depth.stride()), id(tgt))
-        return self._run(key, depth, tgt, init_T, stream)
+        """Whole frame from a device depth image: host pose in, (T, stats) out (blocking).  The
+        image is copied into the tracker's staging buffer on the stream, so one graph per target
+        serves every caller tensor (no per-address graphs, nothing of the caller's retained)."""
+        _check_depth(depth)
+        if tuple(depth.shape) != (self.H, self.W):
+            raise ValueError(f"depth must be ({self.H}, {self.W})")
+        if self._depth is None:
+            self._depth = torch.zeros((self.H, self.W), dtype=torch.float32, device=self.device)
+        up = lambda s0: self._depth.copy_(depth, non_blocking=True)  # noqa: E731
+        return self._run(("dev", id(tgt)), self._depth, tgt, init_T, stream, up)
 
     def track_host(self, depth_host: torch.Tensor, tgt: Target, init_T, stream=None):
         """Whole frame from a host depth image (pinned for an asynchronous copy): uploads only the
@@ -891,9 +958,11 @@ class GaussianMap:
             raise RuntimeError(f"GaussianMap full: {self.M} + {cloud.cap} > {self.capacity}")
         M = self.M
         out = (self.means[M:M + cloud.cap], self.quats[M:M + cloud.cap], self.scales[M:M + cloud.cap])
-        _, _, _, d_m = export_gaussians(cloud.pos, cloud.d_n, cloud.cov_a, cloud.cov_b, T=d_T, p=p, c=c, corr=corr,
-                                        out=out, stream=stream)
-        m = int(d_m.item())
+        s0 = stream if stream is not None else torch.cuda.current_stream(self.means.device)
+        with torch.cuda.stream(s0):  # allocation, export and count readback all ordered on s0
+            _, _, _, d_m = export_gaussians(cloud.pos, cloud.d_n, cloud.cov_a, cloud.cov_b, T=d_T, p=p, c=c,
+                                            corr=corr, out=out, stream=s0)
+            m = int(d_m.item())
         if m:
             self.M += m
             self.rebuild(stream)

@@ -1,9 +1,9 @@
 // A6-A9  G-ICP alignment in ONE persistent cooperative kernel.
 //
 // Per Gauss-Newton iteration, every thread takes source points i (grid-stride) and
-//   A6  q = K3(T, x_i) in binary64 (no FMA), exact 1-NN of fl32(q) among the target means by
-//       the canonical (key, index) order, grid search warm-started with the previous
-//       iteration's match; valid iff key < fl32(r*r) (R15);
+//   A6  q = K3(T, x_i) in binary64 (no FMA), exact 1-NN of q among the target means by the
+//       canonical binary64 (K2 key, index) order (R1, R15), grid search warm-started with
+//       the previous iteration's match; valid iff key < r^2 (R15);
 //   A7  Sigma = C^t_j + R C^s_i R^T, M = Sigma^{-1} (adjugate, binary64), d = x^t_j - q,
 //       J = [[q]x, -I]: accumulates the 21 unique H = J^T M J terms, b = J^T M d, d^T M d and
 //       the inlier count (Eq. 1; R1-R3, R16);
@@ -30,6 +30,10 @@ namespace gsicp {
 thread_local long long *g_align_timeline = nullptr;
 thread_local long long g_align_timeline_cap = 0;
 thread_local int32_t *g_align_debug = nullptr;
+// per-iteration linearisation record hook (gsicp_debug_align_iterations)
+thread_local double *g_align_iter_rec = nullptr;
+thread_local int32_t *g_align_iter_corr = nullptr;
+thread_local int g_align_iter_cap = 0;
 
 namespace {
 
@@ -51,7 +55,9 @@ struct AlignArgs {
     const int32_t *nbr;       // nullable: target kNN graph, [M][kGraphK] slots
     const float *nbr_key;     // [M] key of the kGraphK-th neighbour
     int max_iters;
-    float r, r2;
+    float r;                  // max_corr_dist
+    double r2;                // (double)r * (double)r: valid iff key64 < r2 (R15)
+    float r2f;                // binary32 upper bound of r2 (cell pruning)
     double eps_rot, eps_trans;
     int min_pairs;
     int solver;               // 0 GN, 1 LM (R30)
@@ -73,7 +79,14 @@ struct AlignArgs {
     double seed_ticket;       // k_align_seed: ticket to write; k_align: ticket expected (0: none)
     int32_t *seed_queue;      // [cap] hard queries of the seed pass
     int32_t *seed_qn;         // [1] their count
+    // diagnostic (nullable): per GN iteration it < iter_cap, iter_rec[it * kIterRec + ..] = the pose
+    // T_it the iteration linearised at (12, row-major 3x4) then its 29 reduced terms (21 H upper,
+    // 6 b, cost, n); iter_corr[it * cap + i] = point i's correspondence (original index or -1)
+    double *iter_rec;
+    int32_t *iter_corr;
+    int iter_cap;
 };
+constexpr int kIterRec = 48;
 
 __device__ __forceinline__ long long globaltimer_ns() {
     long long t;
@@ -89,18 +102,55 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
 
 __device__ __forceinline__ float ordered_to_float_(int32_t i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
 
-// running 1-NN state of one query
+// The query of a correspondence search: the binary64 K3 transform q (the definition, R15) and its
+// binary32 rounding (cell geometry, pruning and the binary32 screen; QueryCell's margin covers
+// |q - fl32(q)|).
+struct Qry {
+    double d0, d1, d2;
+    float x, y, z;
+    __device__ __forceinline__ Qry(double a, double b, double c)
+        : d0(a), d1(b), d2(c), x((float)a), y((float)b), z((float)c) {}
+    // >= |q - fl32(q)| (each coordinate within 2^-24 |q_i|: 2 u |fl32(q)|_1 with margin)
+    __device__ __forceinline__ float E() const { return 1.2e-7f * (fabsf(x) + fabsf(y) + fabsf(z)) + 1e-30f; }
+    __device__ __forceinline__ double key(const float4 &p) const { return key64(d0, d1, d2, p.x, p.y, p.z); }
+    __device__ __forceinline__ float key32(const float4 &p) const { return canon_key(x, y, z, p.x, p.y, p.z); }
+};
+
+// running 1-NN state of one query: the best (K2 key, original index) so far
 struct NN {
-    unsigned long long best = kEmptyKey;  // packed (key, original index)
-    int slot = -1;                        // cell-ordered target slot of best
+    double bk = INFINITY;                 // key64 of best
+    uint32_t bi = 0xffffffffu;            // original index of best (= p.w's bits)
+    int slot = -1;                        // cell-ordered target slot of best (-1: none yet)
     float4 p;                             // target record of best
     int probes = 0, cands = 0, slow = 0;  // diagnostics
+    __device__ __forceinline__ void offer(double k, uint32_t i, int s, const float4 &rec) {
+        if (k < bk || (k == bk && i < bi)) {
+            bk = k;
+            bi = i;
+            slot = s;
+            p = rec;
+        }
+    }
+    __device__ __forceinline__ void set(double k, int s, const float4 &rec) {
+        bk = k;
+        bi = (uint32_t)__float_as_int(rec.w);
+        slot = s;
+        p = rec;
+    }
+    // Binary32 screen: a candidate c can beat (or tie) the best only if key32(fl32(q), c) <= screen:
+    // |q - c| <= |q - best| and |fl32(q) - c| <= |q - c| + E, key32 within 5u of |fl32(q) - c|^2.
+    // Only such candidates get the binary64 key (usually just the best itself).
+    __device__ __forceinline__ float screen(const Qry &q) const {
+        if (slot < 0) return INFINITY;
+        const float s = __fmul_ru(__fadd_ru(__fsqrt_ru(__double2float_ru(bk)), q.E()), 1.000002f);
+        return __fmul_ru(s, s);
+    }
 };
 
 constexpr int kCandBatch = 4;   // candidate records loaded together (one latency per batch)
 constexpr int kNbBatch = 4;     // neighbour-cell lookups in flight together (fast path)
 
-__device__ __forceinline__ void scan_target_cell(const AlignArgs &a, uint2 se, float qx, float qy, float qz, NN &nn) {
+__device__ __forceinline__ void scan_target_cell(const AlignArgs &a, uint2 se, const Qry &q, NN &nn) {
     ++nn.probes;
     nn.cands += (int)se.y;
     const uint32_t end = se.x + se.y;
@@ -111,25 +161,20 @@ __device__ __forceinline__ void scan_target_cell(const AlignArgs &a, uint2 se, f
 #pragma unroll
         for (int u = 0; u < kCandBatch; ++u) {
             if (j0 + u >= end) break;
-            const unsigned long long v =
-                pack_ki(canon_key(qx, qy, qz, p[u].x, p[u].y, p[u].z), (uint32_t)__float_as_int(p[u].w));
-            if (v < nn.best) {
-                nn.best = v;
-                nn.slot = (int)(j0 + u);
-                nn.p = p[u];
-            }
+            if (q.key32(p[u]) <= nn.screen(q)) nn.offer(q.key(p[u]), (uint32_t)__float_as_int(p[u].w), (int)(j0 + u), p[u]);
         }
     }
 }
 
+// binary32 upper bound on min(best key, r^2) for cell pruning (the gaps are binary32 lower bounds)
 __device__ __forceinline__ float nn_bound(const AlignArgs &a, const NN &nn) {
-    return nn.best != kEmptyKey ? fminf(ki_key(nn.best), a.r2) : a.r2;
+    return nn.slot >= 0 ? fminf(__double2float_ru(nn.bk), a.r2f) : a.r2f;
 }
 
 // Certified graph step: nn holds a candidate slot j with key k_j.  Every target k that could beat
 // it satisfies |m_j - m_k| <= 2 |q - m_j| (triangle inequality), so if 4 k_j < key_K(j) (with
-// slack for binary32 rounding of both keys) all of them are in j's exact K-NN list and the 1-NN
-// of q is the best of that list (self included).  Returns false (nn untouched) otherwise.
+// slack for the binary32 rounding of the graph's key) all of them are in j's K-NN list and the 1-NN
+// of q is the best of that list (self included).
 // Greedy descent on the graph until a certified step: each step scans the list of the current
 // candidate j (which can only improve nn); if j was certified the result is exact.  If the list
 // holds nothing better and j is not certified, or after kGraphSteps steps, returns false (nn
@@ -147,10 +192,10 @@ constexpr int kD2FromIter = GSICP_D2_FROM_ITER;
 // exact distances, every other target k has |q - m_k| >= |m_j - m_k| - |q - m_j| >=
 // sqrt(key_K(j)) - sqrt(k_j).  d2lb receives that lower bound on the distance from q to any
 // target other than the 1-NN (conservatively rounded), for the motion-bounded reuse in k_align.
-__device__ __forceinline__ bool graph_nn(const AlignArgs &a, float qx, float qy, float qz, NN &nn, float &d2lb) {
+__device__ __forceinline__ bool graph_nn(const AlignArgs &a, const Qry &q, NN &nn, float &d2lb) {
     for (int step = 0; step < kGraphSteps; ++step) {
         const int j = nn.slot;
-        const float kj = ki_key(nn.best);
+        const float kj = __double2float_ru(nn.bk);
         const int4 *lst = reinterpret_cast<const int4 *>(a.nbr + (size_t)j * kGraphK);
         const float kk = __ldg(a.nbr_key + j);
         int sl[kGraphK];
@@ -160,28 +205,42 @@ __device__ __forceinline__ bool graph_nn(const AlignArgs &a, float qx, float qy,
             sl[4 * v] = w.x; sl[4 * v + 1] = w.y; sl[4 * v + 2] = w.z; sl[4 * v + 3] = w.w;
         }
         const bool certified = 4.f * kj * (1.f + 4e-5f) < kk * (1.f - 4e-5f);
-        float4 p[kGraphK];
+        // binary32 screen of the list (records in flight together), then the binary64 keys of the
+        // few that can beat the best (records reloaded through L1: keeps the doubles out of the
+        // 16-wide unrolled section)
+        float k32[kGraphK];
+        {
+            float4 p[kGraphK];
 #pragma unroll
-        for (int u = 0; u < kGraphK; ++u) p[u] = sl[u] >= 0 ? __ldg(a.tpos + sl[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int u = 0; u < kGraphK; ++u)
+                p[u] = sl[u] >= 0 ? __ldg(a.tpos + sl[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < kGraphK; ++u) k32[u] = sl[u] >= 0 ? q.key32(p[u]) : INFINITY;
+        }
         ++nn.probes;
         nn.cands += kGraphK;
-        unsigned long long l1 = kEmptyKey, l2 = kEmptyKey;  // the two smallest of this list
+        float l1 = INFINITY, l2 = INFINITY;  // the two smallest screen keys of this list
+        uint32_t cand = 0u;
+        const float scr = nn.screen(q);
 #pragma unroll
         for (int u = 0; u < kGraphK; ++u) {
-            if (sl[u] < 0) continue;
-            const unsigned long long v =
-                pack_ki(canon_key(qx, qy, qz, p[u].x, p[u].y, p[u].z), (uint32_t)__float_as_int(p[u].w));
-            if (v < nn.best) {
-                nn.best = v;
-                nn.slot = sl[u];
-                nn.p = p[u];
-            }
-            l2 = v < l1 ? l1 : (v < l2 ? v : l2);
-            l1 = v < l1 ? v : l1;
+            cand |= (k32[u] <= scr ? 1u : 0u) << u;
+            l2 = k32[u] < l1 ? l1 : (k32[u] < l2 ? k32[u] : l2);
+            l1 = k32[u] < l1 ? k32[u] : l1;
+        }
+        while (cand) {
+            const int u = __ffs(cand) - 1;
+            cand &= cand - 1;
+            int su = sl[0];
+#pragma unroll
+            for (int v = 1; v < kGraphK; ++v) su = v == u ? sl[v] : su;
+            const float4 rec = __ldg(a.tpos + su);
+            if (q.key32(rec) <= nn.screen(q)) nn.offer(q.key(rec), (uint32_t)__float_as_int(rec.w), su, rec);
         }
         if (certified) {
             const float rc = sqrtf(kk) * (1.f - kReuseMargin) - sqrtf(kj) * (1.f + kReuseMargin);
-            const float d2 = l2 != kEmptyKey ? sqrtf(ki_key(l2)) : INFINITY;
+            // every list member other than the 1-NN: |q - m| >= |fl32(q) - m| - E
+            const float d2 = l2 < INFINITY ? fmaxf(sqrtf(__fmul_rd(l2, 0.999999f)) - q.E(), 0.f) : INFINITY;
             d2lb = fmaxf(fminf(d2, rc), 0.f) * (1.f - kReuseMargin);
             return true;
         }
@@ -197,7 +256,7 @@ constexpr int kFlatBatch = 8;  // candidate records loaded per round trip in the
 // round trip (instead of one chain of round trips per cell); a cell's records are skipped once
 // its lower bound exceeds the shrinking bound.
 __device__ __forceinline__ void scan_cells_flat(const AlignArgs &a, const uint2 (&se)[kMaxCells],
-                                                const float (&lbs)[kMaxCells], float qx, float qy, float qz, NN &nn) {
+                                                const float (&lbs)[kMaxCells], const Qry &q, NN &nn) {
     uint32_t pre[kMaxCells + 1];
     pre[0] = 0;
 #pragma unroll
@@ -227,16 +286,17 @@ __device__ __forceinline__ void scan_cells_flat(const AlignArgs &a, const uint2 
             slot[u] = s;
             p[u] = v ? __ldg(a.tpos + s) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        uint32_t cand = 0u;
 #pragma unroll
-        for (int u = 0; u < kFlatBatch; ++u) {
-            if (!ok[u]) continue;
-            const unsigned long long v =
-                pack_ki(canon_key(qx, qy, qz, p[u].x, p[u].y, p[u].z), (uint32_t)__float_as_int(p[u].w));
-            if (v < nn.best) {
-                nn.best = v;
-                nn.slot = (int)slot[u];
-                nn.p = p[u];
-            }
+        for (int u = 0; u < kFlatBatch; ++u) cand |= (ok[u] && q.key32(p[u]) <= nn.screen(q) ? 1u : 0u) << u;
+        while (cand) {  // binary64 keys of the screened few (records reloaded: no doubles in the unrolled part)
+            const int u = __ffs(cand) - 1;
+            cand &= cand - 1;
+            uint32_t su = slot[0];
+#pragma unroll
+            for (int v = 1; v < kFlatBatch; ++v) su = v == u ? slot[v] : su;
+            const float4 rec = __ldg(a.tpos + su);
+            if (q.key32(rec) <= nn.screen(q)) nn.offer(q.key(rec), (uint32_t)__float_as_int(rec.w), (int)su, rec);
         }
     }
 }
@@ -244,13 +304,12 @@ __device__ __forceinline__ void scan_cells_flat(const AlignArgs &a, const uint2 
 // General exact search after the own cell: grow shells while an ungated search has found
 // nothing, then the ball traversal bounded by min(best, r^2).  Out of line so that the
 // common fast path keeps its registers.
-__device__ __forceinline__ void nn_slow(const AlignArgs &a, const CellIndex &idx, const int *sb, float qx, float qy,
-                                     float qz, NN &nn) {
-    const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
+__device__ __forceinline__ void nn_slow(const AlignArgs &a, const CellIndex &idx, const int *sb, const Qry &q, NN &nn) {
+    const QueryCell qc(q.x, q.y, q.z, a.h, a.inv_h);
     const int *blo = sb, *bhi = sb + 3;
     int m_done = 0;
-    if (nn.best == kEmptyKey && !(a.r2 < INFINITY)) {
-        while (nn.best == kEmptyKey && !qc.covers(m_done, blo, bhi)) {
+    if (nn.slot < 0 && !(a.r2 < INFINITY)) {
+        while (nn.slot < 0 && !qc.covers(m_done, blo, bhi)) {
             ++m_done;
             const int cnt = shell_count(m_done);
             for (int t = 0; t < cnt; ++t) {
@@ -258,13 +317,13 @@ __device__ __forceinline__ void nn_slow(const AlignArgs &a, const CellIndex &idx
                 shell_cell(m_done, t, dx, dy, dz);
                 const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
                 if (x < blo[0] || x > bhi[0] || y < blo[1] || y > bhi[1] || z < blo[2] || z > bhi[2]) continue;
-                scan_target_cell(a, idx.one(x, y, z), qx, qy, qz, nn);
+                scan_target_cell(a, idx.one(x, y, z), q, nn);
             }
         }
     }
     ball_search(
         qc, idx, blo, bhi, [&](int dx, int dy, int dz) { return max(max(abs(dx), abs(dy)), abs(dz)) <= m_done; },
-        [&](uint2 se) { scan_target_cell(a, se, qx, qy, qz, nn); }, [&]() { return nn_bound(a, nn); });
+        [&](uint2 se) { scan_target_cell(a, se, q, nn); }, [&]() { return nn_bound(a, nn); });
 }
 
 // Exact 1-NN given the query's cell geometry and its own cell's (start, count) (already known).
@@ -274,8 +333,7 @@ __device__ __forceinline__ void nn_slow(const AlignArgs &a, const CellIndex &idx
 // Returns true when nn is the exact answer; false (only with defer) when the general search is
 // still needed — nn then holds the best point seen.
 __device__ __forceinline__ bool nn_search(const AlignArgs &a, const CellIndex &idx, const int *sb,
-                                          const QueryCell &qc, uint2 own, float qx, float qy, float qz, NN &nn,
-                                          bool defer) {
+                                          const QueryCell &qc, uint2 own, const Qry &q, NN &nn, bool defer) {
     float glo[3], ghi[3], glo2[3], ghi2[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -291,14 +349,14 @@ __device__ __forceinline__ bool nn_search(const AlignArgs &a, const CellIndex &i
     float b = nn_bound(a, nn);
     bool own_pending = true;
     if (!fits(b)) {
-        scan_target_cell(a, own, qx, qy, qz, nn);
+        scan_target_cell(a, own, q, nn);
         own_pending = false;
         b = nn_bound(a, nn);
         if (!fits(b)) {
             ++nn.slow;
             if (defer) return false;  // the block's warps run it cooperatively (warp_nn)
             NN tmp = nn;  // a copy: taking nn's address would pin it to local memory
-            nn_slow(a, idx, sb, qx, qy, qz, tmp);
+            nn_slow(a, idx, sb, q, tmp);
             nn = tmp;
             return true;
         }
@@ -345,29 +403,27 @@ __device__ __forceinline__ bool nn_search(const AlignArgs &a, const CellIndex &i
         idx.batch(xs, ys, zs, valid, se);
         se[0] = own_pending ? own : make_uint2(0u, 0u);
         own_pending = false;
-        scan_cells_flat(a, se, lbs, qx, qy, qz, nn);
+        scan_cells_flat(a, se, lbs, q, nn);
     }
     return true;
 }
 
-__device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int src) {
-    return ((unsigned long long)__shfl_sync(0xffffffffu, (unsigned)(v >> 32), src) << 32) |
-           __shfl_sync(0xffffffffu, (unsigned)v, src);
+__device__ __forceinline__ double shfl_f64(double v, int src) {
+    return __hiloint2double(__shfl_sync(0xffffffffu, __double2hiint(v), src), __shfl_sync(0xffffffffu, __double2loint(v), src));
 }
 
 // Warp-cooperative exact 1-NN for one query (all lanes call it with the same arguments; nn is
 // uniform on entry and exit).  Cells are visited in Chebyshev shells around the query cell,
 // nearest first (shell 0+1 = 27 cells in the first round, then shell m in rounds of 32, lane =
 // cell), skipping cells whose lower bound exceeds the current bound; the points of the probed
-// cells are scanned as one flattened range (lane = candidate) and the batch minimum is taken by
-// shuffles.  After shell m every unvisited point is >= certified_key(m) away, so the search
-// stops as soon as the bound is below that (or the shells cover the target bbox).  Used for the
-// queries whose per-thread fast path failed, so a few hard queries do not serialise a warp.
-// With fixed_b2 >= 0 it instead finds the best target with key <= fixed_b2 other than slot
-// `excl` (the second-neighbour bound of the motion-bounded reuse); the r gate does not apply.
+// cells are scanned as one flattened range (lane = candidate) and the batch minimum by (key64,
+// index) is taken by shuffles.  After shell m every unvisited point is >= certified_key(m) away,
+// so the search stops as soon as the bound is below that (or the shells cover the target bbox).
+// Used for the queries whose per-thread fast path failed, so a few hard queries do not serialise
+// a warp.  With fixed_b2 >= 0 it instead finds the best target with key <= fixed_b2 other than
+// slot `excl` (the second-neighbour bound of the motion-bounded reuse); the r gate does not apply.
 __device__ __forceinline__ void warp_scan_cells(const AlignArgs &a, const CellIndex &idx, const QueryCell &qc, bool valid,
-                                                int dx, int dy, int dz, float qx, float qy, float qz, NN &nn, int lane,
-                                                int excl) {
+                                                int dx, int dy, int dz, const Qry &q, NN &nn, int lane, int excl) {
     const uint2 se = valid ? idx.one(qc.c[0] + dx, qc.c[1] + dy, qc.c[2] + dz) : make_uint2(0u, 0u);
     uint32_t incl = se.y;
 #pragma unroll
@@ -389,24 +445,26 @@ __device__ __forceinline__ void warp_scan_cells(const AlignArgs &a, const CellIn
         const uint32_t c_incl = __shfl_sync(0xffffffffu, incl, l0);
         const uint32_t c_start = __shfl_sync(0xffffffffu, se.x, l0);
         const uint32_t c_cnt = __shfl_sync(0xffffffffu, se.y, l0);
-        unsigned long long cand = kEmptyKey;
+        double ck = INFINITY;
+        uint32_t ci = 0xffffffffu;
         float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
         uint32_t slot = 0;
         if (item < ctot) {
             slot = c_start + (item - (c_incl - c_cnt));
             p = __ldg(a.tpos + slot);
-            cand = (int)slot == excl ? kEmptyKey
-                                     : pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
+            if ((int)slot != excl) {
+                ck = q.key(p);
+                ci = (uint32_t)__float_as_int(p.w);
+            }
         }
-        unsigned long long mn = cand;
+        double mk = ck;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long v = shfl_u64(mn, lane ^ o);
-            mn = v < mn ? v : mn;
-        }
-        if (mn < nn.best) {
-            const int src = __ffs(__ballot_sync(0xffffffffu, cand == mn)) - 1;
-            nn.best = mn;
+        for (int o = 16; o > 0; o >>= 1) mk = fmin(mk, shfl_f64(mk, lane ^ o));
+        const uint32_t mi = __reduce_min_sync(0xffffffffu, ck == mk ? ci : 0xffffffffu);
+        if (mk < nn.bk || (mk == nn.bk && mi < nn.bi)) {
+            const int src = __ffs(__ballot_sync(0xffffffffu, ck == mk && ci == mi)) - 1;
+            nn.bk = mk;
+            nn.bi = mi;
             nn.slot = (int)__shfl_sync(0xffffffffu, slot, src);
             nn.p.x = __shfl_sync(0xffffffffu, p.x, src);
             nn.p.y = __shfl_sync(0xffffffffu, p.y, src);
@@ -418,12 +476,12 @@ __device__ __forceinline__ void warp_scan_cells(const AlignArgs &a, const CellIn
 
 constexpr int kWarpShells = 3;  // shells visited nearest-first before the box traversal
 
-__device__ void warp_nn(const AlignArgs &a, const CellIndex &idx, const int *sb, float qx, float qy, float qz, NN &nn,
-                        int lane, float fixed_b2 = -1.f, int excl = -1) {
-    const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
+__device__ void warp_nn(const AlignArgs &a, const CellIndex &idx, const int *sb, const Qry &q, NN &nn, int lane,
+                        float fixed_b2 = -1.f, int excl = -1) {
+    const QueryCell qc(q.x, q.y, q.z, a.h, a.inv_h);
     const int *blo = sb, *bhi = sb + 3;
     auto bound = [&]() {
-        return fixed_b2 >= 0.f ? fminf(nn.best != kEmptyKey ? ki_key(nn.best) : INFINITY, fixed_b2) : nn_bound(a, nn);
+        return fixed_b2 >= 0.f ? fminf(nn.slot >= 0 ? __double2float_ru(nn.bk) : INFINITY, fixed_b2) : nn_bound(a, nn);
     };
     auto in_box = [&](int dx, int dy, int dz) {
         const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
@@ -446,7 +504,7 @@ __device__ void warp_nn(const AlignArgs &a, const CellIndex &idx, const int *sb,
                 valid = in_box(dx, dy, dz) && qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2) <= b;
             }
             if (!__any_sync(0xffffffffu, valid)) continue;
-            warp_scan_cells(a, idx, qc, valid, dx, dy, dz, qx, qy, qz, nn, lane, excl);
+            warp_scan_cells(a, idx, qc, valid, dx, dy, dz, q, nn, lane, excl);
         }
         // shells 0..m done: every unvisited point is >= certified_key(m) away
         if (bound() < qc.certified_key(m) || qc.covers(m, blo, bhi)) return;
@@ -471,7 +529,7 @@ __device__ void warp_nn(const AlignArgs &a, const CellIndex &idx, const int *sb,
                     qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2) <= b;
         }
         if (!__any_sync(0xffffffffu, valid)) continue;
-        warp_scan_cells(a, idx, qc, valid, dx, dy, dz, qx, qy, qz, nn, lane, excl);
+        warp_scan_cells(a, idx, qc, valid, dx, dy, dz, q, nn, lane, excl);
     }
 }
 
@@ -688,8 +746,8 @@ __device__ __forceinline__ int solve_step_t(const AlignArgs &a, const double *sA
 // No warm start: the own cell's best becomes the candidate; an empty own cell is seeded from
 // the 6 face neighbours (the graph step then needs some candidate to start from).
 __device__ __forceinline__ void nn_cold_start(const AlignArgs &a, const CellIndex &idx, const QueryCell &qc, uint2 own,
-                                              float qx, float qy, float qz, NN &nn) {
-    scan_target_cell(a, own, qx, qy, qz, nn);
+                                              const Qry &q, NN &nn) {
+    scan_target_cell(a, own, q, nn);
     for (int f0 = 0; f0 < 6 && nn.slot < 0; f0 += kMaxCells) {
         int xs[kMaxCells], ys[kMaxCells], zs[kMaxCells];
         bool valid[kMaxCells];
@@ -706,7 +764,7 @@ __device__ __forceinline__ void nn_cold_start(const AlignArgs &a, const CellInde
         }
         uint2 se[kMaxCells];
         idx.batch(xs, ys, zs, valid, se);
-        scan_cells_flat(a, se, lbs, qx, qy, qz, nn);
+        scan_cells_flat(a, se, lbs, q, nn);
     }
 }
 
@@ -724,7 +782,7 @@ __device__ __forceinline__ void load_cell_index(const AlignArgs &a, CellIndex &i
 }
 
 // Iteration-0 correspondences ahead of the GN loop (gsicp_align_seed): exact 1-NN of
-// fl32(K3(T0, x_i)) for every source point, by the same search as k_align's first iteration
+// K3(T0, x_i) (binary64, R15) for every source point, by the same search as k_align's first iteration
 // (cold start, certified graph descent, fast path, block queue solved by whole warps).  It needs
 // only the source positions, so it can run concurrently with the source covariances (A2-A4).
 constexpr int kSeedT = 256;
@@ -743,20 +801,20 @@ __global__ void __launch_bounds__(kSeedT) k_align_seed(AlignArgs a) {
         const float4 x = __ldg(a.spos + i);
         double q0, q1, q2;
         k3(sT, x.x, x.y, x.z, q0, q1, q2);
-        const float qx = __double2float_rn(q0), qy = __double2float_rn(q1), qz = __double2float_rn(q2);
-        const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
+        const Qry q(q0, q1, q2);
+        const QueryCell qc(q.x, q.y, q.z, a.h, a.inv_h);
         const uint2 own = sIdx.one(qc.c[0], qc.c[1], qc.c[2]);
         NN nn;
         uint2 own_left = own;
         if (a.nbr) {
-            nn_cold_start(a, sIdx, qc, own, qx, qy, qz, nn);
+            nn_cold_start(a, sIdx, qc, own, q, nn);
             own_left = make_uint2(0u, 0u);
         }
         float d2 = 0.f;
         // per thread only the cheap certified case (own cell, then the graph); everything else
         // goes to the warp-cooperative pass (no divergent per-thread grid walks here)
-        bool exact = nn.slot >= 0 && a.nbr && graph_nn(a, qx, qy, qz, nn, d2);
-        if (!exact && !a.nbr) exact = nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn, true);
+        bool exact = nn.slot >= 0 && a.nbr && graph_nn(a, q, nn, d2);
+        if (!exact && !a.nbr) exact = nn_search(a, sIdx, sBox, qc, own_left, q, nn, true);
         a.seed_slot[i] = nn.slot;  // exact, or the best seen (an upper bound for the hard pass)
         if (!exact) a.seed_queue[atomicAdd(a.seed_qn, 1)] = i;
     }
@@ -781,15 +839,14 @@ __global__ void __launch_bounds__(kSeedHardT) k_align_seed_hard(AlignArgs a) {
         const float4 x = __ldg(a.spos + i);
         double q0, q1, q2;
         k3(sT, x.x, x.y, x.z, q0, q1, q2);
-        const float qx = __double2float_rn(q0), qy = __double2float_rn(q1), qz = __double2float_rn(q2);
+        const Qry q(q0, q1, q2);
         NN nn;
         const int sl = a.seed_slot[i];
         if (sl >= 0) {
-            nn.slot = sl;
-            nn.p = __ldg(a.tpos + sl);
-            nn.best = pack_ki(canon_key(qx, qy, qz, nn.p.x, nn.p.y, nn.p.z), (uint32_t)__float_as_int(nn.p.w));
+            const float4 rec = __ldg(a.tpos + sl);
+            nn.set(q.key(rec), sl, rec);
         }
-        warp_nn(a, sIdx, sBox, qx, qy, qz, nn, lane);
+        warp_nn(a, sIdx, sBox, q, nn, lane);
         if (lane == 0) a.seed_slot[i] = nn.slot;
     }
 }
@@ -818,8 +875,8 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
     // per-block queue of queries needing the general search (handled by whole warps)
     __shared__ int sQn;
     __shared__ int sQtid[kT];
-    __shared__ float4 sQq[kT];
-    __shared__ unsigned long long sQbest[kT];
+    __shared__ double4 sQq[kT];
+    __shared__ double sQbk[kT];
     __shared__ int sQslot[kT];
     __shared__ float4 sQp[kT];
     __shared__ float sQd2[kT];
@@ -887,8 +944,8 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
         if (has0) {
             sub_stamp(0);
             k3(T, x0.x, x0.y, x0.z, q0r, q1r, q2r);
-            const float qx = __double2float_rn(q0r), qy = __double2float_rn(q1r), qz = __double2float_rn(q2r);
-            const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
+            const Qry q(q0r, q1r, q2r);
+            const QueryCell qc(q.x, q.y, q.z, a.h, a.inv_h);
             if (qc.c[0] != own_c[0] || qc.c[1] != own_c[1] || qc.c[2] != own_c[2]) {
                 own_c[0] = qc.c[0]; own_c[1] = qc.c[1]; own_c[2] = qc.c[2];
                 own_se = sIdx.one(qc.c[0], qc.c[1], qc.c[2]);
@@ -900,25 +957,23 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
             if (seeded0) {  // exact match at this pose computed ahead by k_align_seed
                 const int sl = __ldg(a.seed_slot + i0);
                 if (sl >= 0) {
-                    nn.p = __ldg(a.tpos + sl);
-                    nn.slot = sl;
-                    nn.best = pack_ki(canon_key(qx, qy, qz, nn.p.x, nn.p.y, nn.p.z), (uint32_t)__float_as_int(nn.p.w));
+                    const float4 rec = __ldg(a.tpos + sl);
+                    nn.set(q.key(rec), sl, rec);
                 }
             } else if (m0.slot >= 0) {  // warm start from the previous match (record kept in registers)
-                nn.p = m0.p;
-                nn.slot = m0.slot;
-                nn.best = pack_ki(canon_key(qx, qy, qz, m0.p.x, m0.p.y, m0.p.z), (uint32_t)__float_as_int(m0.p.w));
+                nn.set(q.key(m0.p), m0.slot, m0.p);
             }
             bool exact = seeded0;
             // motion-bounded reuse: the query moved by delta since the match was proven, with
-            // every other target >= d2lb away then; if d1' + delta < d2lb - delta... precisely
-            // |q' - m| < d2lb - delta <= |q' - m_k| for all k != m, the match stands (no loads)
+            // every other target >= d2lb away then, so |q' - m_k| >= d2lb - delta for all k != m;
+            // if |q' - m| < d2lb - delta the match stands (no loads).  delta is measured between the
+            // binary32 roundings of the two binary64 queries, plus their rounding (2 E)
             if (!exact && d2lb > 0.f) {
-                const float ex = qx - qp0, ey = qy - qp1, ez = qz - qp2;
-                const float delta = sqrtf(ex * ex + ey * ey + ez * ez) * (1.f + kReuseMargin);
+                const float ex = q.x - qp0, ey = q.y - qp1, ez = q.z - qp2;
+                const float delta = sqrtf(ex * ex + ey * ey + ez * ez) * (1.f + kReuseMargin) + 2.f * q.E();
                 // d2lb bounds every target other than the candidate: beating d1 proves the
                 // candidate is the 1-NN, or (candidate absent or beyond r) that the point stays gated
-                const float d1 = nn.slot >= 0 ? fminf(sqrtf(ki_key(nn.best)), a.r) : a.r;
+                const float d1 = nn.slot >= 0 ? fminf(sqrtf(__double2float_ru(nn.bk)), a.r) : a.r;
                 if ((d2lb - delta) * (1.f - kReuseMargin) > d1 * (1.f + kReuseMargin)) {
                     exact = true;
                     d2lb -= delta;
@@ -929,32 +984,32 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
             sub_stamp(2);
             uint2 own_left = own_se;
             if (!exact && nn.slot < 0 && a.nbr) {  // no warm start: the own cell's best becomes the candidate
-                nn_cold_start(a, sIdx, qc, own_se, qx, qy, qz, nn);
+                nn_cold_start(a, sIdx, qc, own_se, q, nn);
                 own_left = make_uint2(0u, 0u);
             }
             path_code = exact ? (seeded0 ? 4 : 0) : 1;
             if (!exact && nn.slot >= 0 && a.nbr) {
-                exact = graph_nn(a, qx, qy, qz, nn, d2lb);
+                exact = graph_nn(a, q, nn, d2lb);
                 dbg_graph |= (exact ? 1 : 0) << (it & 31);
                 path_code = exact ? 1 : 2;
             }
             // after iteration 0 a point the graph cannot certify goes straight to the block queue:
             // the warp path also bounds its second neighbour, so the next iterations can reuse
             if (!exact && (it == 0 || !a.nbr)) {
-                exact = nn_search(a, sIdx, sBox, qc, own_left, qx, qy, qz, nn, true);
+                exact = nn_search(a, sIdx, sBox, qc, own_left, q, nn, true);
                 path_code = exact ? 2 : 3;
             }
             if (!exact) path_code = 3;
-            qp0 = qx;
-            qp1 = qy;
-            qp2 = qz;
-            if (sub) a.timeline[sub_base + 4] = nn.best == kEmptyKey ? 1 : 0;
+            qp0 = q.x;
+            qp1 = q.y;
+            qp2 = q.z;
+            if (sub) a.timeline[sub_base + 4] = nn.slot < 0 ? 1 : 0;
             sub_stamp(3);
             if (!exact) {  // hand over to the block's warps (warp_nn below)
                 const int k = atomicAdd(&sQn, 1);
                 sQtid[k] = tid;
-                sQq[k] = make_float4(qx, qy, qz, 0.f);
-                sQbest[k] = nn.best;
+                sQq[k] = make_double4(q0r, q1r, q2r, 0.0);
+                sQbk[k] = nn.bk;
                 sQslot[k] = nn.slot;
                 sQp[k] = nn.p;
             }
@@ -983,25 +1038,25 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
         // queries whose fast path failed: one warp each, all lanes cooperating
         __syncthreads();
         for (int k = warp; k < sQn; k += kWarps) {
-            const float4 qq = sQq[k];
+            const double4 qq = sQq[k];
+            const Qry q(qq.x, qq.y, qq.z);
             NN nn;
-            nn.best = sQbest[k];
             nn.slot = sQslot[k];
-            nn.p = sQp[k];
-            warp_nn(a, sIdx, sBox, qq.x, qq.y, qq.z, nn, lane);
+            if (nn.slot >= 0) nn.set(sQbk[k], nn.slot, sQp[k]);
+            warp_nn(a, sIdx, sBox, q, nn, lane);
             // a lower bound on every other target's distance (exact within rho), so that the
             // following iterations can keep this answer while the query moves little
-            const bool in_r = nn.slot >= 0 && ki_key(nn.best) < a.r2;
-            const float base = in_r ? sqrtf(ki_key(nn.best)) : a.r;
+            const bool in_r = nn.slot >= 0 && nn.bk < a.r2;
+            const float base = in_r ? sqrtf(__double2float_ru(nn.bk)) : a.r;
             float d2 = 0.f;
             if (base < INFINITY && it >= kD2FromIter) {
                 const float rho = base * 1.25f + 0.25f * a.h;
                 NN n2;
-                warp_nn(a, sIdx, sBox, qq.x, qq.y, qq.z, n2, lane, rho * rho, nn.slot);
-                d2 = fminf(n2.best != kEmptyKey ? sqrtf(ki_key(n2.best)) : INFINITY, rho) * (1.f - kReuseMargin);
+                warp_nn(a, sIdx, sBox, q, n2, lane, rho * rho, nn.slot);
+                d2 = fminf(n2.slot >= 0 ? sqrtf(__double2float_rd(n2.bk)) : INFINITY, rho) * (1.f - kReuseMargin);
             }
             if (lane == 0) {
-                sQbest[k] = nn.best;
+                sQbk[k] = nn.bk;
                 sQslot[k] = nn.slot;
                 sQp[k] = nn.p;
                 sQd2[k] = d2;
@@ -1011,38 +1066,35 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
         if (has0) {
             for (int k = 0; k < sQn; ++k)
                 if (sQtid[k] == tid) {
-                    m0.best = sQbest[k];
-                    m0.slot = sQslot[k];
-                    m0.p = sQp[k];
+                    if (sQslot[k] >= 0) m0.set(sQbk[k], sQslot[k], sQp[k]); else m0.slot = -1;
                     d2lb = sQd2[k];
                 }
-            valid0 = m0.slot >= 0 && ki_key(m0.best) < a.r2;
+            valid0 = m0.slot >= 0 && m0.bk < a.r2;
         }
         if (tid == 0) sQn = 0;  // next use is after at least one more __syncthreads
         for (int i = i0 + G * kT; i < n; i += G * kT) {  // non-resident points (large clouds)
             const float4 x = __ldg(a.spos + i);
             double q0, q1, q2;
             k3(T, x.x, x.y, x.z, q0, q1, q2);
-            const float qx = __double2float_rn(q0), qy = __double2float_rn(q1), qz = __double2float_rn(q2);
-            const QueryCell qc(qx, qy, qz, a.h, a.inv_h);
+            const Qry q(q0, q1, q2);
+            const QueryCell qc(q.x, q.y, q.z, a.h, a.inv_h);
             NN nn;
             int slot = (it == 0 && sSeeded) ? a.seed_slot[i] : a.corr_ws[i];
             if (slot <= -2) slot = -2 - slot;
             if (slot >= 0) {
-                nn.p = __ldg(a.tpos + slot);
-                nn.slot = slot;
-                nn.best = pack_ki(canon_key(qx, qy, qz, nn.p.x, nn.p.y, nn.p.z), (uint32_t)__float_as_int(nn.p.w));
+                const float4 rec = __ldg(a.tpos + slot);
+                nn.set(q.key(rec), slot, rec);
             }
             if (!(it == 0 && sSeeded)) {
                 // the kNN-graph certificate from the previous match first (as for resident points)
                 bool exact = false;
                 if (nn.slot >= 0 && a.nbr) {
                     float d2 = 0.f;
-                    exact = graph_nn(a, qx, qy, qz, nn, d2);
+                    exact = graph_nn(a, q, nn, d2);
                 }
-                if (!exact) nn_search(a, sIdx, sBox, qc, sIdx.one(qc.c[0], qc.c[1], qc.c[2]), qx, qy, qz, nn, false);
+                if (!exact) nn_search(a, sIdx, sBox, qc, sIdx.one(qc.c[0], qc.c[1], qc.c[2]), q, nn, false);
             }
-            a.corr_ws[i] = (nn.slot >= 0 && ki_key(nn.best) < a.r2) ? nn.slot : -2 - nn.slot;
+            a.corr_ws[i] = (nn.slot >= 0 && nn.bk < a.r2) ? nn.slot : -2 - nn.slot;
         }
         sub_stamp(5);
         stamp(1);
@@ -1064,6 +1116,7 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
             if (sub) acc[0] += 0.0 * (double)clock();
             sub_stamp(7);
             if (a.corr_out) a.corr_out[i0] = corr_val;
+            if (a.iter_corr && it < a.iter_cap) a.iter_corr[(size_t)it * a.cap + i0] = corr_val;
         }
         for (int i = i0 + G * kT; i < n; i += G * kT) {
             const int slot = a.corr_ws[i];
@@ -1078,6 +1131,7 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
                     corr_val = __float_as_int(m.w);
             }
             if (a.corr_out) a.corr_out[i] = corr_val;
+            if (a.iter_corr && it < a.iter_cap) a.iter_corr[(size_t)it * a.cap + i] = corr_val;
         }
         stamp(2);
         // ------------------------------------------------------------ block reduction
@@ -1139,6 +1193,11 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
             __syncthreads();
         }
         stamp(4);
+        if (a.iter_rec && it < a.iter_cap && bid == 0 && tid < 12 + kAlignTerms) {
+            double *rec = a.iter_rec + (size_t)it * kIterRec;
+            rec[tid] = tid < 12 ? sT[tid] : sAcc[tid - 12];
+        }
+        __syncthreads();
         // ------------------------------------------------------------ A8 solve / update / test
         if (tid == 0) {
             n_in = sAcc[28];
@@ -1207,16 +1266,18 @@ __global__ void k_align_init_batch(const __grid_constant__ AlignBatch b) {
 // Co-resident grid for the cooperative launch (0 if the kernel cannot be resident at all).
 constexpr int kMaxAlignGrid = 2048;  // partial records reserved in the workspace (>= SMs x blocks/SM)
 
+// blocks per SM of the GN kernels (the smaller residency of the GN and LM variants), per device
+template <class F1, class F2>
+static int coresident_per_sm(F1 k_gn, F2 k_lm) {
+    int v = 0, v1 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_gn, kT, 0) != cudaSuccess) v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v1, k_lm, kT, 0) != cudaSuccess) v1 = 0;
+    return v < v1 ? v : v1;
+}
+
 int align_grid_blocks(int cap, int *per_sm_out) {
-    static int per_sm = -1;
-    if (per_sm < 0) {
-        int v = 0;
-        int v1 = 0;  // the GN and LM kernels: the smaller residency of the two
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_align<false>, kT, 0) != cudaSuccess) v = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v1, k_align<true>, kT, 0) != cudaSuccess) v1 = 0;
-        v = v < v1 ? v : v1;
-        per_sm = v;
-    }
+    static PerDevice<int> cache;
+    const int per_sm = cache.get([](int) { return coresident_per_sm(k_align<false>, k_align<true>); });
     *per_sm_out = per_sm;
     (void)cap;
     const int g = per_sm * num_sms();  // the full co-resident grid; k_align splits the points over it
@@ -1292,7 +1353,9 @@ static AlignArgs make_args(const gsicp_cloud &src, const gsicp_target &tgt, doub
     a.nbr_key = tgt.nbr_key;
     a.max_iters = p.max_iters;
     a.r = linearize_only ? r_lin : p.max_corr_dist;
-    a.r2 = a.r * a.r;
+    a.r2 = (double)a.r * (double)a.r;
+    a.r2f = (float)a.r2;
+    if ((double)a.r2f < a.r2) a.r2f = nextafterf(a.r2f, INFINITY);
     a.eps_rot = p.eps_rot;
     a.eps_trans = p.eps_trans;
     a.min_pairs = p.min_pairs;
@@ -1314,6 +1377,9 @@ static AlignArgs make_args(const gsicp_cloud &src, const gsicp_target &tgt, doub
     a.seed_ticket = 0.0;
     a.seed_queue = w.seed_queue;
     a.seed_qn = w.seed_qn;
+    a.iter_rec = g_align_iter_rec;
+    a.iter_corr = g_align_iter_corr;
+    a.iter_cap = g_align_iter_rec ? g_align_iter_cap : 0;
     return a;
 }
 
@@ -1370,13 +1436,8 @@ cudaError_t align_seed_launch(const gsicp_cloud &src, const gsicp_target &tgt, c
     ktimer_mark(KT_SEED, false, s);
     launch_low(k_align_seed, dim3(blocks_for(src.cap > 0 ? src.cap : 1, kSeedT)), dim3(kSeedT), 0, s, a);
     GSICP_LAUNCH_CHECK("k_align_seed");
-    static int per_sm = -1;  // GSICP_SEED_HARD_PER_SM (A/B): resident blocks per SM of the hard pass
-    if (per_sm < 0) {
-        const char *e = getenv("GSICP_SEED_HARD_PER_SM");
-        per_sm = e ? atoi(e) : 8;
-        if (per_sm < 1) per_sm = 8;
-    }
-    launch_low(k_align_seed_hard, dim3(num_sms() * per_sm), dim3(kSeedHardT), 0, s, a);
+    constexpr int kSeedHardPerSm = 8;  // resident blocks per SM of the hard pass (measured best, round 1)
+    launch_low(k_align_seed_hard, dim3(num_sms() * kSeedHardPerSm), dim3(kSeedHardT), 0, s, a);
     GSICP_LAUNCH_CHECK("k_align_seed_hard");
     ktimer_mark(KT_SEED, true, s);
     note_launch(2);
@@ -1439,20 +1500,18 @@ cudaError_t align_batch_launch(const gsicp_cloud *srcs, int B, const gsicp_targe
         hb.f[f].timeline = nullptr;  // the diagnostics describe single-frame launches
         hb.f[f].timeline_cap = 0;
         hb.f[f].debug = nullptr;
+        if (f > 0) {  // the per-iteration record hook follows frame 0 of a batch
+            hb.f[f].iter_rec = nullptr;
+            hb.f[f].iter_corr = nullptr;
+            hb.f[f].iter_cap = 0;
+        }
         hb.f[f].seed_ticket = seed_take(ws[f], srcs[f].pos, tgt.pos);
         if (srcs[f].cap > cap_max) cap_max = srcs[f].cap;
     }
     launch_pdl(k_align_init_batch, dim3(blocks_for(cap_max, 256), B), dim3(256), 0, s, hb);
     GSICP_LAUNCH_CHECK("k_align_init_batch");
-    static int per_sm = -1;
-    if (per_sm < 0) {
-        int v = 0;
-        int v1 = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_align_batch<false>, kT, 0) != cudaSuccess) v = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v1, k_align_batch<true>, kT, 0) != cudaSuccess) v1 = 0;
-        v = v < v1 ? v : v1;
-        per_sm = v;
-    }
+    static PerDevice<int> cache;
+    const int per_sm = cache.get([](int) { return coresident_per_sm(k_align_batch<false>, k_align_batch<true>); });
     int G = per_sm * num_sms();
     if (G > kMaxAlignGrid) G = kMaxAlignGrid;
     const int Gf = G / B;

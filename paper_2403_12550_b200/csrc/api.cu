@@ -15,6 +15,9 @@ extern thread_local int32_t *g_knn_debug;  // knn_cov.cu
 extern thread_local long long *g_align_timeline;  // align.cu
 extern thread_local long long g_align_timeline_cap;
 extern thread_local int32_t *g_align_debug;
+extern thread_local double *g_align_iter_rec;
+extern thread_local int32_t *g_align_iter_corr;
+extern thread_local int g_align_iter_cap;
 
 // (launches captured into a conditional graph node's body are not counted: they run only when the
 // device switches the node on — the hash tail of the image-window kNN, which a frame rarely needs)
@@ -153,6 +156,11 @@ const char *gsicp_status_string(gsicp_status s) {
 const char *gsicp_last_error(void) { return g_err; }
 void gsicp_debug_knn_counters(int32_t *d_out) { gsicp::g_knn_debug = d_out; }
 void gsicp_debug_align_counters(int32_t *d_out) { gsicp::g_align_debug = d_out; }
+void gsicp_debug_align_iterations(double *d_rec, int32_t *d_corr, int32_t max_iters) {
+    gsicp::g_align_iter_rec = max_iters > 0 ? d_rec : nullptr;
+    gsicp::g_align_iter_corr = max_iters > 0 ? d_corr : nullptr;
+    gsicp::g_align_iter_cap = d_rec && max_iters > 0 ? max_iters : 0;
+}
 
 // ---------------------------------------------------------------------------------------------
 // Sequence tracking helpers: constant-velocity initial pose and the pose history.
@@ -376,7 +384,7 @@ gsicp_status gsicp_covariances(const float *pos, const int32_t *d_n, int32_t cap
     g_err[0] = 0;
     if (!pos || !d_n || !cov_a || !cov_b) BAD("covariances: null pointer");
     if (!aligned16(pos) || !aligned16(cov_a) || !aligned16(cov_b)) BAD("covariances: arrays must be 16-byte aligned");
-    if (cap < 1) BAD("covariances: cap must be >= 1");
+    if (cap < 1 || (uint32_t)cap > kMaxBandIndex) BAD("covariances: cap must be in [1, 2^27)");
     if (k < 1 || k > 32) BAD("covariances: k must be in [1, 32]");
     if (mode != GSICP_REG_NONE && mode != GSICP_REG_PLANE && mode != GSICP_REG_ELLIPSE) BAD("covariances: bad mode");
     if (!(eps_var > 0.f) || !(eps_var <= 1.f)) BAD("covariances: eps_var must be in (0, 1]");
@@ -402,7 +410,7 @@ gsicp_status gsicp_covariances_image(const float *pos, const int32_t *d_n, int32
     g_err[0] = 0;
     if (!pos || !d_n || !cov_a || !cov_b) BAD("covariances_image: null pointer");
     if (!aligned16(pos) || !aligned16(cov_a) || !aligned16(cov_b)) BAD("covariances_image: arrays must be 16-byte aligned");
-    if (cap < 1) BAD("covariances_image: cap must be >= 1");
+    if (cap < 1 || (uint32_t)cap > kMaxBandIndex) BAD("covariances_image: cap must be in [1, 2^27)");
     if (H < 1 || W < 1 || stride < 1) BAD("covariances_image: bad image geometry");
     if ((long long)H * W >= (1ll << 31)) BAD("covariances_image: image too large for 32-bit pixel ids");
     if (!(K.fx > 0.f) || !(K.fy > 0.f) || !isfinite(K.fx) || !isfinite(K.fy)) BAD("covariances_image: bad intrinsics");
@@ -429,7 +437,7 @@ gsicp_status gsicp_build_target(const float *means, const float *quats_wxyz, con
                                 gsicp_target *out, void *target_ws, size_t ws_bytes, void *stream) {
     g_err[0] = 0;
     if (!means || !quats_wxyz || !scales || !out) BAD("build_target: null pointer");
-    if (M < 1) BAD("build_target: M must be >= 1");
+    if (M < 1 || (uint32_t)M > kMaxBandIndex) BAD("build_target: M must be in [1, 2^27)");
     if (mode != GSICP_REG_NONE && mode != GSICP_REG_PLANE && mode != GSICP_REG_ELLIPSE) BAD("build_target: bad mode");
     if (!(eps_var > 0.f) || !(eps_var <= 1.f)) BAD("build_target: eps_var must be in (0, 1]");
     if (!isfinite(cell)) BAD("build_target: cell must be finite");
@@ -446,7 +454,7 @@ gsicp_status gsicp_build_target_cloud(const gsicp_cloud *cloud, int32_t M, float
     gsicp_status st = check_cloud(cloud, "build_target_cloud");
     if (st != GSICP_OK) return st;
     if (!out) BAD("build_target_cloud: null out");
-    if (M < 1 || M > cloud->cap) BAD("build_target_cloud: M must be in [1, cap]");
+    if (M < 1 || M > cloud->cap || (uint32_t)M > kMaxBandIndex) BAD("build_target_cloud: M must be in [1, min(cap, 2^27))");
     if (!(cell > 0.f) || !isfinite(cell)) BAD("build_target_cloud: cell must be > 0");
     st = check_ws(target_ws, ws_bytes, target_ws_bytes(M));
     if (st != GSICP_OK) return st;

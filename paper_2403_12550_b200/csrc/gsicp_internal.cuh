@@ -31,8 +31,26 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------------------
-// Canonical binary32 squared-distance key (R1): dx = a.x - b.x, key = (dx*dx + dy*dy) + dz*dz,
-// every op rounded separately (no FMA) so the CPU oracle reproduces it bit for bit.
+// Canonical keys (DESIGN R1).  The DEFINITION is the binary64 key K2:
+// dx = (double)b.x - q.x (q binary64: a binary32 point widened exactly, or the K3 transform of
+// one), key = (dx*dx + dy*dy) + dz*dz, each op rounded separately (no FMA), order (key, index).
+__device__ __forceinline__ double key64(double qx, double qy, double qz, float bx, float by, float bz) {
+    const double dx = __dsub_rn((double)bx, qx), dy = __dsub_rn((double)by, qy), dz = __dsub_rn((double)bz, qz);
+    double s = __dmul_rn(dx, dx);
+    s = __dadd_rn(s, __dmul_rn(dy, dy));
+    s = __dadd_rn(s, __dmul_rn(dz, dz));
+    return s;
+}
+__device__ __forceinline__ double key64f(float ax, float ay, float az, float bx, float by, float bz) {
+    return key64((double)ax, (double)ay, (double)az, bx, by, bz);
+}
+
+// The binary32 SCREEN key: the same expression in binary32.  For binary32 points a, b it is within
+// 5u (u = 2^-24) of the exact squared distance, and key64 within 5 * 2^-53, so
+// |key32 - key64| <= 11 u key64 (plus binary32 underflow, < 1e-44 absolute).  Candidates are ranked
+// by key32 and only those within the band [band_lo(t), band_hi(t)] of the k-th / best key32 t are
+// resolved in binary64: every candidate below band_lo(t) is certainly among the k
+// nearest by key64, every one above band_hi(t) certainly not (kBand = 4e-6 > 22 u).
 __device__ __forceinline__ float canon_key(float ax, float ay, float az, float bx, float by, float bz) {
     float dx = __fsub_rn(ax, bx), dy = __fsub_rn(ay, by), dz = __fsub_rn(az, bz);
     float s = __fmul_rn(dx, dx);
@@ -40,14 +58,36 @@ __device__ __forceinline__ float canon_key(float ax, float ay, float az, float b
     s = __fadd_rn(s, __fmul_rn(dz, dz));
     return s;
 }
+constexpr float kBand = 4e-6f;
+__device__ __forceinline__ float band_hi(float t) { return __fadd_ru(__fmul_ru(t, 1.f + kBand), 1e-36f); }
+__device__ __forceinline__ float band_lo(float t) { return __fsub_rd(__fmul_rd(t, 1.f - kBand), 1e-36f); }
 
-// (key, index) packed so that unsigned 64-bit order == lexicographic (key, index) order
+// (key32, index) packed so that unsigned 64-bit order == lexicographic (key32, index) order
 // (keys are >= 0, so their IEEE bit patterns are monotone as unsigned integers).
 __device__ __forceinline__ unsigned long long pack_ki(float key, uint32_t idx) {
     return ((unsigned long long)__float_as_uint(key) << 32) | idx;
 }
 __device__ __forceinline__ float ki_key(unsigned long long v) { return __uint_as_float((uint32_t)(v >> 32)); }
 __device__ __forceinline__ uint32_t ki_idx(unsigned long long v) { return (uint32_t)v; }
+
+// Exact (key64, index) order of candidates inside one band, packed in 64 bits: a band spans less
+// than 1e-5 relative in key64, i.e. < 2^37 binary64 ulps, so the key64 bit pattern minus that of
+// the band's floor fits 37 bits above a 27-bit index (clouds of < 2^27 points; checked by the API).
+constexpr int kBandIdxBits = 27;
+constexpr uint32_t kMaxBandIndex = (1u << kBandIdxBits) - 1u;
+// (A band around t < 1e-30 has floor 0 and the offset saturates: pairs of distinct points closer
+// than ~1e-18 m are then ordered by index — the one documented inexact corner, DESIGN R1.)
+__device__ __forceinline__ unsigned long long band_pack(double key, uint32_t idx, unsigned long long floor_bits) {
+    unsigned long long off = (unsigned long long)__double_as_longlong(key) - floor_bits;
+    off = off < (1ull << (64 - kBandIdxBits)) ? off : (1ull << (64 - kBandIdxBits)) - 1ull;
+    return (off << kBandIdxBits) | idx;
+}
+__device__ __forceinline__ uint32_t band_idx(unsigned long long v) { return (uint32_t)(v & kMaxBandIndex); }
+// floor of a band: a binary64 value below every key64 of a candidate whose key32 >= band_lo(t)
+__device__ __forceinline__ unsigned long long band_floor_bits(float t) {
+    const double f = t < 1e-30f ? 0.0 : fmax((double)band_lo(t) * (1.0 - 2e-6), 0.0);
+    return (unsigned long long)__double_as_longlong(f);
+}
 
 // ---------------------------------------------------------------------------------------
 // Spatial hash: cell coordinates c = floor(p * inv_h) (binary32, same function at build and

@@ -5,6 +5,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <mutex>
 #include <utility>
 
 namespace gsicp {
@@ -36,15 +37,31 @@ struct Carver {
     size_t bytes() const { return align_up(off); }
 };
 
-inline int num_sms() {
-    static int sms = 0;
-    if (!sms) {
+// A value per CUDA device, computed once per device on first use (thread-safe: std::call_once)
+// and immutable afterwards — device properties and kernel occupancies, which may differ between
+// the devices one process drives.  This is the library's only process-wide state besides
+// thread-local diagnostics (gsicp.h, "State").
+template <typename T>
+struct PerDevice {
+    static constexpr int kMaxDevices = 64;
+    std::once_flag once[kMaxDevices];
+    T value[kMaxDevices];
+    template <typename F>
+    const T &get(F &&compute) {
         int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+        std::call_once(once[dev], [&] { value[dev] = compute(dev); });
+        return value[dev];
     }
-    return sms;
+};
+
+inline int num_sms() {
+    static PerDevice<int> cache;
+    return cache.get([](int dev) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return sms > 0 ? sms : 148;
+    });
 }
 
 inline unsigned blocks_for(long long n, int threads) { return (unsigned)((n + threads - 1) / threads); }
@@ -52,33 +69,25 @@ inline unsigned blocks_for(long long n, int threads) { return (unsigned)((n + th
 // Programmatic dependent launch (sm_90+): the kernel may be launched while its stream
 // predecessor is still running and waits for it in-kernel (pdl_wait() at its top, before any
 // dependent read), which hides the launch latency between consecutive kernels of the frame
-// (CUDA-graph edges included).  GSICP_PDL=0 turns it off (A/B).
+// (CUDA-graph edges included).  Off only while a conditional-node body is being captured.
 inline bool &pdl_suspended() {  // set while capturing into a conditional-node body
     static thread_local bool off = false;
     return off;
 }
-inline bool pdl_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("GSICP_PDL");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1 && !pdl_suspended();
-}
+inline bool pdl_enabled() { return !pdl_suspended(); }
 
 // Launch priorities: the frame's critical path (A1 -> A2-A4 -> A6-A9) runs high, the work
 // overlapped on side streams (iteration-0 seeds, the fallback hash) low, so that it fills idle
 // SM slots instead of slowing the critical kernels.  Honoured in graphs instantiated with
-// cudaGraphInstantiateFlagUseNodePriority (gsicp_graph_instantiate).  GSICP_PRIO=0: off.
+// cudaGraphInstantiateFlagUseNodePriority (gsicp_graph_instantiate).
 inline int launch_priority(bool high) {
-    static int lo = 1, hi = 1, on = -1;
-    if (on < 0) {
-        const char *e = getenv("GSICP_PRIO");
-        on = (e && e[0] == '0') ? 0 : 1;
-        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) on = 0;
-    }
-    if (!on) return 0;
-    return high ? hi : lo;
+    static PerDevice<int2> cache;  // (least, greatest) stream priority of the device
+    const int2 r = cache.get([](int) {
+        int lo = 0, hi = 0;
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) lo = hi = 0;
+        return make_int2(lo, hi);
+    });
+    return high ? r.y : r.x;
 }
 
 template <typename... KArgs, typename... Args>
@@ -106,12 +115,7 @@ inline cudaError_t launch_low(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributePriority;
-    static int flip = -1;  // GSICP_SIDE_HIGH=1: side work at high priority too (A/B)
-    if (flip < 0) {
-        const char *e = getenv("GSICP_SIDE_HIGH");
-        flip = (e && e[0] == '1') ? 1 : 0;
-    }
-    at[0].val.priority = launch_priority(flip == 1);
+    at[0].val.priority = launch_priority(false);
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;

@@ -52,8 +52,9 @@ struct KnnArgs {
     double eps;
     float4 *cov_a, *cov_b;
     int32_t *knn_idx;
+    int sort_out;     // knn_idx rows sorted by (key64, index) (API output); else any order (graph)
     int4 *debug;
-    int32_t *nbr_t;   // [cap][kMaxK]: the k neighbours (input indices, sorted, -1 pad) per query in search order
+    int32_t *nbr_t;   // [cap][kMaxK]: the k neighbours (input indices, -1 pad) per query in search order
     // queue mode (fallback of the image-window kernel): the queries are queue[0 .. *queue_n) (input
     // indices) instead of every point; query t of the search is queue[t]
     const uint32_t *queue;
@@ -73,21 +74,103 @@ __device__ __forceinline__ unsigned long long shfl_up_u64(unsigned long long v, 
     return ((unsigned long long)__shfl_up_sync(kFull, (unsigned)(v >> 32), d) << 32) |
            __shfl_up_sync(kFull, (unsigned)v, d);
 }
+__device__ __forceinline__ double shfl_f64(double v, int src) {
+    return __hiloint2double(__shfl_sync(kFull, __double2hiint(v), src), __shfl_sync(kFull, __double2loint(v), src));
+}
 
-// Warp-distributed sorted best-K list.
+// Position of this lane's entry (sel: taking part) in the (key64, index) order of all selected
+// lanes' entries (the key64 of each computed once, then compared by shuffles).
+__device__ __forceinline__ int warp_rank64(bool sel, uint32_t id, double qx, double qy, double qz,
+                                           const float4 *__restrict__ pos) {
+    double k64 = INFINITY;
+    if (sel) {
+        const float4 p = __ldg(pos + id);
+        k64 = key64(qx, qy, qz, p.x, p.y, p.z);
+    }
+    int r = 0;
+    for (unsigned m = __ballot_sync(kFull, sel); m; m &= m - 1) {
+        const int l = __ffs(m) - 1;
+        const double ok = shfl_f64(k64, l);
+        const uint32_t oi = __shfl_sync(kFull, id, l);
+        r += (ok < k64 || (ok == k64 && oi < id)) ? 1 : 0;
+    }
+    return r;
+}
+
+// Exact k nearest by (key64, index) from the candidates of the calling warp, given
+// as A (lane j: the j-th smallest packed (key32, index), kEmptyKey past the end) holding every
+// candidate of key32 <= band_hi(t), t the k-th key32 — unless `capped` (more candidates than the 32
+// lanes existed) and lane 31 still lies in the band: then false (the band may be incomplete).
+// On success `pos_out` is this lane's output position (0..k-1, in (key64, index) order if SORT,
+// else in list order) or -1 if its entry is not among the k nearest.
+template <bool SORT>
+__device__ __forceinline__ bool warp_exact_select(unsigned long long A, int k, bool capped, double qx, double qy,
+                                                  double qz, const float4 *__restrict__ pos, int lane, int &pos_out) {
+    const unsigned long long At = shfl_u64(A, k - 1);
+    bool sel;
+    if (At == kEmptyKey) {  // fewer than k candidates: all of them
+        sel = A != kEmptyKey;
+    } else {
+        const float t = ki_key(At), hi = band_hi(t), lo = band_lo(t);
+        if (capped && ki_key(shfl_u64(A, 31)) <= hi) return false;
+        const float kk = ki_key(A);
+        const bool inS = A != kEmptyKey && kk < lo;
+        const bool inB = A != kEmptyKey && kk >= lo && kk <= hi;
+        const int s = __popc(__ballot_sync(kFull, inS)), nb = __popc(__ballot_sync(kFull, inB));
+        if (s + nb == k) {
+            sel = inS || inB;
+        } else {  // a tie band: rank its members by key64
+            const int r = warp_rank64(inB, ki_idx(A), qx, qy, qz, pos);
+            sel = inS || (inB && r < k - s);
+        }
+    }
+    if (SORT) {
+        const int r = warp_rank64(sel, ki_idx(A), qx, qy, qz, pos);
+        pos_out = sel ? r : -1;
+    } else {
+        const unsigned sm = __ballot_sync(kFull, sel);  // (all lanes: not inside the conditional)
+        pos_out = sel ? __popc(sm & ((1u << lane) - 1u)) : -1;
+    }
+    return true;
+}
+
+// ids[j] (every lane) = the index of the entry at output position j, -1 if none
 template <int K>
+__device__ __forceinline__ void collect_ids(int outpos, uint32_t id, int lane, int (&ids)[K]) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const unsigned b = __ballot_sync(kFull, outpos == j);
+        const int v = (int)__shfl_sync(kFull, id, b ? __ffs(b) - 1 : 0);
+        ids[j] = b ? v : -1;
+    }
+}
+
+// Warp-distributed sorted list of the 32 smallest candidates (lane j holds the j-th smallest packed
+// value, kEmptyKey if fewer).  Candidates are accepted below thr = min(list[31], band_hi of the
+// K-th key32), so every candidate within the binary64 resolution band of the K-th is retained as
+// long as the 32 lanes hold it (warp_exact_select detects the rare overflow).
+// BAND: the values are band-packed (key64, index) pairs of one band (band pass): thr = list[31].
+template <int K, bool BAND = false>
 struct WarpTopK {
-    unsigned long long L;  // lane j < K: j-th smallest (kEmptyKey if fewer); lanes >= K: kEmptyKey
-    unsigned long long worst;  // = list[K-1] (warp-uniform)
+    unsigned long long L;    // this lane's entry
+    unsigned long long thr;  // acceptance threshold (warp-uniform)
+    unsigned long long kth;  // list[K-1] (warp-uniform)
     int inserts;
 
     __device__ __forceinline__ void reset() {
         L = kEmptyKey;
-        worst = kEmptyKey;
+        thr = kEmptyKey;
+        kth = kEmptyKey;
     }
-    __device__ __forceinline__ bool full() const { return worst != kEmptyKey; }
-    // insert the candidates of all lanes (cand = kEmptyKey for none): a few by ballot + shuffle,
-    // many by a warp bitonic sort of the batch merged into the list (fixed ~40 shuffles)
+    __device__ __forceinline__ bool full() const { return kth != kEmptyKey; }
+    __device__ __forceinline__ float bound() const { return ki_key(thr); }  // prune / certify against this
+    __device__ __forceinline__ void update() {
+        kth = shfl_u64(L, K - 1);
+        const unsigned long long l31 = shfl_u64(L, 31);
+        const unsigned long long b =
+            (BAND || kth == kEmptyKey) ? kEmptyKey : pack_ki(band_hi(ki_key(kth)), 0xffffffffu);
+        thr = l31 < b ? l31 : b;
+    }
     // bitonic sort (ascending) of the values of lanes [0, W) (other lanes: don't care)
     template <int W>
     __device__ __forceinline__ static unsigned long long sort_w(unsigned long long c, int lane) {
@@ -110,52 +193,36 @@ struct WarpTopK {
         }
         return m;
     }
-    __device__ __forceinline__ void insert_all(unsigned long long cand, int lane, unsigned long long *wbuf) {
-        unsigned pass = __ballot_sync(kFull, cand < worst);
+    // insert the candidates of all lanes (cand = kEmptyKey for none): a few by ballot + shuffle,
+    // many by a warp bitonic sort of the batch merged into the list
+    __device__ __forceinline__ void insert_all(unsigned long long cand, int lane) {
+        unsigned pass = __ballot_sync(kFull, cand < thr);
         const int np = __popc(pass);
-        if (np > kMergeThreshold && np <= 8 && K <= 24) {
-            // few: compact the passing candidates to lanes 0..np-1 (warp scratch), sort those 8,
-            // place them descending in lanes 24..31 after the ascending list (a bitonic sequence)
-            // and merge — 6 + 5 shuffle stages instead of 15 + 5
-            inserts += np;
-            if (cand < worst) wbuf[__popc(pass & ((1u << lane) - 1u))] = cand;
-            __syncwarp();
-            unsigned long long c = lane < np ? wbuf[lane] : kEmptyKey;
-            __syncwarp();
-            c = sort_w<8>(c, lane);
-            const unsigned long long rev = shfl_u64(c, (31 - lane) & 7);
-            const unsigned long long m = merge32(lane < K ? L : (lane >= 24 ? rev : kEmptyKey), lane);
-            L = lane < K ? m : kEmptyKey;
-            worst = shfl_u64(L, K - 1);
-            return;
-        }
         if (np > kMergeThreshold) {
             inserts += np;
-            unsigned long long c = cand < worst ? cand : kEmptyKey;
+            unsigned long long c = cand < thr ? cand : kEmptyKey;
             c = sort_w<32>(c, lane);
             if (shfl_u64(L, 0) == kEmptyKey) {  // empty list: the sorted batch is the list
-                L = lane < K ? c : kEmptyKey;
-                worst = shfl_u64(L, K - 1);
+                L = c;
+                update();
                 return;
             }
-            // list ascending (lanes >= K empty) vs batch descending: lane-wise min = the 32 smallest
+            // list ascending vs batch descending: lane-wise min = the 32 smallest (bitonic)
             const unsigned long long rev = shfl_u64(c, 31 - lane);
-            unsigned long long m = L < rev ? L : rev;
-            m = merge32(m, lane);
-            L = lane < K ? m : kEmptyKey;
-            worst = shfl_u64(L, K - 1);
+            L = merge32(L < rev ? L : rev, lane);
+            update();
             return;
         }
         while (pass) {
             const int src = __ffs(pass) - 1;
             pass &= pass - 1;
             const unsigned long long v = shfl_u64(cand, src);
-            if (!(v < worst)) continue;  // worst shrank since the ballot
+            if (!(v < thr)) continue;  // thr shrank since the ballot
             ++inserts;
-            const int p = __popc(__ballot_sync(kFull, lane < K && L < v));
+            const int p = __popc(__ballot_sync(kFull, L < v));
             const unsigned long long up = shfl_up_u64(L, 1);
-            if (lane < K) L = lane < p ? L : (lane == p ? v : up);
-            worst = shfl_u64(L, K - 1);
+            L = lane < p ? L : (lane == p ? v : up);
+            update();
         }
     }
 };
@@ -169,10 +236,10 @@ struct Counters {
 // found without a search: the non-empty cells are compacted into the warp's cell table (spos
 // start, first item), the cell starts falling into a round are OR-reduced into a bit mask, and a
 // lane's cell is (cells started before the round) + popc(starts at or below the lane) - 1.
-template <int K>
-__device__ __forceinline__ void scan_cells(const GridView &g, bool valid, unsigned long long key, float qx, float qy,
-                                           float qz, WarpTopK<K> &T, Counters &cn, int lane, unsigned long long *wbuf,
-                                           uint2 *wcell) {
+// make(p) -> the packed candidate value of record p (kEmptyKey: not a candidate).
+template <class TopK, class Make>
+__device__ __forceinline__ void scan_cells(const GridView &g, bool valid, unsigned long long key, TopK &T,
+                                           Counters &cn, int lane, uint2 *wcell, Make make) {
     const uint2 se = valid ? cell_lookup(g.table, g.mask, key) : make_uint2(0u, 0u);
     cn.probes += __popc(__ballot_sync(kFull, valid));
     uint32_t incl = se.y;
@@ -195,20 +262,23 @@ __device__ __forceinline__ void scan_cells(const GridView &g, bool valid, unsign
         unsigned long long cand = kEmptyKey;
         if (item < total) {
             const uint2 c = wcell[before + __popc(P & (0xffffffffu >> (31 - lane))) - 1];
-            const float4 p = __ldg(g.spos + c.x + (item - c.y));
-            cand = pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
+            cand = make(__ldg(g.spos + c.x + (item - c.y)));
         }
         before += __popc(P);
-        T.insert_all(cand, lane, wbuf);
+        T.insert_all(cand, lane);
     }
     __syncwarp();
 }
 
-// Exact best-K of one query on one level.  Returns false (list reset) if shell 1 does not fill
-// the list and a coarser level exists.
-template <int K>
-__device__ bool knn_search_warp(const GridView &g, int level, float qx, float qy, float qz, WarpTopK<K> &T,
-                                Counters &cn, int lane, unsigned long long *wbuf, uint2 *wcell, const int *sbox) {
+// Shell-ordered exact search of one query on one level: every cell whose box lower bound is <=
+// bound() (binary32 key; +inf: none yet) is scanned (nearest shells first); stops once bound() is
+// below the certified key of the shells done, or the shells cover the cloud.  Returns false (list
+// reset) if shell 1 does not fill the list and a coarser level exists (only when `escalate`).
+// bound(T) is a stateless function of the list (no captured references: keeps T in registers).
+template <class TopK, class Make, class Bound>
+__device__ __forceinline__ bool knn_shells_warp(const GridView &g, int level, float qx, float qy, float qz, TopK &T,
+                                                Counters &cn, int lane, uint2 *wcell, const int *sbox, bool escalate,
+                                                Make make, Bound bound) {
     T.reset();
     const float inv_h = ldexpf(g.inv_h0, -level);
     const QueryCell qc(qx, qy, qz, ldexpf(g.h0, level), inv_h);
@@ -229,21 +299,22 @@ __device__ bool knn_search_warp(const GridView &g, int level, float qx, float qy
             }
             const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
             bool valid = t < cnt && x >= blo[0] && x <= bhi[0] && y >= blo[1] && y <= bhi[1] && z >= blo[2] && z <= bhi[2];
-            if (valid && T.full()) {
+            const float bd = bound(T);
+            if (valid && bd < INFINITY) {
                 const float lb = qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2);
-                valid = !(lb > ki_key(T.worst));
+                valid = !(lb > bd);
             }
             if (!__any_sync(kFull, valid)) continue;
-            scan_cells<K>(g, valid, cell_key(level, x, y, z), qx, qy, qz, T, cn, lane, wbuf, wcell);
+            scan_cells(g, valid, cell_key(level, x, y, z), T, cn, lane, wcell, make);
         }
         const int mm = m == 0 ? 1 : m;  // shells 0..mm are complete
-        if (T.full() && ki_key(T.worst) < qc.certified_key(mm)) return true;
-        if (qc.covers(mm, blo, bhi)) return true;  // whole cloud scanned (fewer than K points)
-        if (mm == 1 && !T.full() && level + 1 < g.levels) return false;
+        if (bound(T) < qc.certified_key(mm)) return true;
+        if (qc.covers(mm, blo, bhi)) return true;  // whole cloud scanned
+        if (escalate && mm == 1 && !T.full() && level + 1 < g.levels) return false;
     }
 }
 
-template <int K>
+template <int K, bool SORT>
 __global__ void __launch_bounds__(kKnnThreads, kKnnMinBlocks) k_knn_search(KnnArgs a) {
     pdl_wait();
     pdl_launch_dependents();
@@ -251,12 +322,10 @@ __global__ void __launch_bounds__(kKnnThreads, kKnnMinBlocks) k_knn_search(KnnAr
     const int n = *a.d_n;
     const GridView &g = a.g;
     const int lane = threadIdx.x & 31;
-    __shared__ unsigned long long sBuf[kKnnThreads];
     __shared__ uint2 sCell[kKnnThreads];
     __shared__ int sBox[kMaxLevels * 6];
     if (threadIdx.x < g.levels) grid_cell_bbox(g, threadIdx.x, sBox + 6 * threadIdx.x, sBox + 6 * threadIdx.x + 3);
     __syncthreads();
-    unsigned long long *wbuf = sBuf + (threadIdx.x & ~31);
     uint2 *wcell = sCell + (threadIdx.x & ~31);
     // dynamic scheduling: warps take batches of kQueriesPerWarp queries until none are left
     const int nq_all = a.queue ? (int)*a.queue_n : n;
@@ -298,12 +367,55 @@ __global__ void __launch_bounds__(kKnnThreads, kKnnMinBlocks) k_knn_search(KnnAr
         WarpTopK<K> T;
         T.inserts = 0;
         Counters cn;
-        while (!knn_search_warp<K>(g, level, qx, qy, qz, T, cn, lane, wbuf, wcell, sBox)) ++level;
+        auto by_key32 = [&](const float4 &p) {
+            return pack_ki(canon_key(qx, qy, qz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w));
+        };
+        auto t_bound = [](const WarpTopK<K> &L) { return L.thr != kEmptyKey ? L.bound() : INFINITY; };
+        while (!knn_shells_warp(g, level, qx, qy, qz, T, cn, lane, wcell, sBox, true, by_key32, t_bound)) ++level;
+        // exact k nearest by (key64, index): the binary32 list resolved in binary64
+        int outpos = -1;
+        uint32_t myid = ki_idx(T.L);
+        if (!warp_exact_select<SORT>(T.L, a.k, shfl_u64(T.L, 31) != kEmptyKey, qx, qy, qz, a.pos, lane, outpos)) {
+            // band overflow (more than the list's spare lanes tie with the k-th): a second pass
+            // collects exactly the band's members in the exact (key64, index) order
+            const float t = ki_key(T.kth), lo = band_lo(t), hi = band_hi(t);
+            const bool inS = T.L != kEmptyKey && ki_key(T.L) < lo;
+            const int s = __popc(__ballot_sync(kFull, inS));
+            const unsigned long long fl = band_floor_bits(t);
+            const double dqx = qx, dqy = qy, dqz = qz;
+            auto in_band = [&](const float4 &p) {
+                const float k32 = canon_key(qx, qy, qz, p.x, p.y, p.z);
+                return (k32 >= lo && k32 <= hi)
+                           ? band_pack(key64(dqx, dqy, dqz, p.x, p.y, p.z), (uint32_t)__float_as_int(p.w), fl)
+                           : kEmptyKey;
+            };
+            WarpTopK<32, true> B;
+            B.inserts = 0;
+            knn_shells_warp(g, level, qx, qy, qz, B, cn, lane, wcell, sBox, false, in_band,
+                            [hi](const WarpTopK<32, true> &) { return hi; });
+            const unsigned long long b = shfl_u64(B.L, (lane - s) & 31);
+            const bool takeB = lane >= s && lane < a.k && b != kEmptyKey;
+            myid = inS ? ki_idx(T.L) : (takeB ? band_idx(b) : 0u);
+            const bool sel = inS || takeB;
+            if (SORT) {
+                const int r = warp_rank64(sel, myid, dqx, dqy, dqz, a.pos);
+                outpos = sel ? r : -1;
+            } else {
+                outpos = sel ? lane : -1;  // S occupies lanes [0, s), the band's best [s, k)
+            }
+        }
         if (a.debug && lane == 0 && !a.queue) a.debug[i] = make_int4(level, cn.probes, cn.cands, T.inserts);
-        // moments over the k nearest: lane j < k holds neighbour j (sorted by (key, index))
-        const bool have = lane < a.k && T.L != kEmptyKey;
-        if (a.knn_idx && lane < a.k) a.knn_idx[(size_t)i * a.k + lane] = have ? (int32_t)ki_idx(T.L) : -1;
-        if (a.nbr_t && lane < a.k) a.nbr_t[(size_t)(wbase + qi) * kMaxK + lane] = have ? (int32_t)ki_idx(T.L) : -1;
+        // every selected lane writes its entry at its output position; the rest of the row is -1
+        const int cnt = __popc(__ballot_sync(kFull, outpos >= 0));
+        if (a.knn_idx) {
+            if (outpos >= 0) a.knn_idx[(size_t)i * a.k + outpos] = (int32_t)myid;
+            if (lane >= cnt && lane < a.k) a.knn_idx[(size_t)i * a.k + lane] = -1;
+        }
+        if (a.nbr_t) {
+            int32_t *row = a.nbr_t + (size_t)(wbase + qi) * kMaxK;
+            if (outpos >= 0) row[outpos] = (int32_t)myid;
+            if (lane >= cnt && lane < a.k) row[lane] = -1;
+        }
     }
     }
 }
@@ -580,11 +692,13 @@ __global__ void __launch_bounds__(kImgThreads, 4) k_knn_image(KnnArgs a, ImgArgs
     }
     bool ok = bstar >= 0 && m <= (uint32_t)kImgList;
     if (ok) {
-        // ---- pass 2: the candidates at or below b*, in stencil order: those below b* are all
-        // among the k nearest; the boundary bucket's go to the end of the list and only the
-        // (k - below) smallest of them by (key, index) are kept
-        const uint32_t lo_lim = (uint32_t)(base + bstar) << 21;  // keys below bucket b*
-        const uint32_t lim = bstar >= kImgBuckets - 1 ? 0x7F800000u : (uint32_t)(base + bstar + 1) << 21;
+        // ---- pass 2: the candidates below b*'s lower edge (shrunk by the binary64 resolution
+        // band) are all among the k nearest ("sure", from the bottom of the list); those
+        // up to b*'s upper edge (widened by the band) form the boundary group (from the top); in
+        // stencil order
+        const float lo_edge = __uint_as_float((uint32_t)(base + bstar) << 21);
+        const float lo_lim = bstar > 0 ? band_lo(lo_edge) : -1.f;
+        const float lim = bstar >= kImgBuckets - 1 ? INFINITY : band_hi(__uint_as_float((uint32_t)(base + bstar + 1) << 21));
         int nlo = 0, nbd = 0;
 #pragma unroll 1
         for (int dy = 0; dy <= 2 * M; ++dy) {
@@ -593,10 +707,9 @@ __global__ void __launch_bounds__(kImgThreads, 4) k_knn_image(KnnArgs a, ImgArgs
             for (int dx = 0; dx <= 2 * M; ++dx) {
                 const float4 P = row[dx];
                 const float key = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
-                const uint32_t kb = __float_as_uint(key);
-                if (kb < lim && kb < 0x7F800000u) {
+                if (key <= lim && key < INFINITY) {
                     const unsigned long long e = pack_ki(key, (uint32_t)__float_as_int(P.w));
-                    const bool lo = bstar > 0 && kb < lo_lim;
+                    const bool lo = key < lo_lim;
                     const int slot = lo ? nlo : kImgList - 1 - nbd;  // boundary entries from the top
                     if (nlo + nbd < kImgList) list[slot][tid] = e;
                     nlo += lo ? 1 : 0;
@@ -604,42 +717,66 @@ __global__ void __launch_bounds__(kImgThreads, 4) k_knn_image(KnnArgs a, ImgArgs
                 }
             }
         }
-        ok = nlo + nbd == (int)m && nlo == (int)below;
+        ok = nlo + nbd <= kImgList && nlo < k && nlo + nbd >= k;
         if (ok) {
-            // keep the r smallest boundary entries (rank by (key, index) among them): a bit mask
-            // over the boundary slots (boundary entry j sits in slot kImgList-1-j)
+            // t = the k-th smallest key32 = the (k - nlo)-th of the boundary group (rank by packed
+            // (key32, index)); then over all filled slots: key32 < band_lo(t) is in, > band_hi(t)
+            // out, and a tie band around t is ranked by (key64, index).  Masks are over list slots
+            // (filled: [0, nlo) and [kImgList - nbd, kImgList)).
             const int r = k - nlo;
-            unsigned long long kth = 0ull;
-            uint32_t sel = 0u;
-            for (int j = 0; j < nbd; ++j) {
-                const unsigned long long e = list[kImgList - 1 - j][tid];
+            float t = 0.f;
+            for (int j = kImgList - nbd; j < kImgList; ++j) {
+                const unsigned long long e = list[j][tid];
                 int rank = 0;
-                for (int l = 0; l < nbd; ++l) rank += list[kImgList - 1 - l][tid] < e ? 1 : 0;
-                if (rank < r) {
-                    sel |= 1u << j;
-                    kth = e > kth ? e : kth;
-                }
+                for (int l = kImgList - nbd; l < kImgList; ++l) rank += list[l][tid] < e ? 1 : 0;
+                if (rank == r - 1) t = ki_key(e);
             }
-            ok = img_cert(im, q, ki_key(kth), M);
+            const float blo = band_lo(t), bhi = band_hi(t);
+            const uint32_t filled = (nlo >= 32 ? ~0u : ((1u << nlo) - 1u)) | (nbd == 0 ? 0u : ~0u << (kImgList - nbd));
+            uint32_t sel = 0u, band = 0u;
+            for (uint32_t f = filled; f; f &= f - 1) {
+                const int j = __ffs(f) - 1;
+                const float kj = ki_key(list[j][tid]);
+                sel |= (kj < blo ? 1u : 0u) << j;
+                band |= (kj >= blo && kj <= bhi ? 1u : 0u) << j;
+            }
+            const int need = k - __popc(sel);
+            const double qx = q.x, qy = q.y, qz = q.z;
+            // key64 of the entry in slot j, and its rank by (key64, index) among the slots of mask
+            auto key_of = [&](int j, uint32_t &id) {
+                id = ki_idx(list[j][tid]);
+                const float4 p = __ldg(a.pos + id);
+                return key64(qx, qy, qz, p.x, p.y, p.z);
+            };
+            auto rank_in = [&](int j, uint32_t mask) {
+                uint32_t ij;
+                const double kj = key_of(j, ij);
+                int rank = 0;
+                for (uint32_t bl = mask; bl; bl &= bl - 1) {
+                    uint32_t il;
+                    const double kl = key_of(__ffs(bl) - 1, il);
+                    rank += (kl < kj || (kl == kj && il < ij)) ? 1 : 0;
+                }
+                return rank;
+            };
+            if (__popc(band) == need) {
+                sel |= band;
+            } else {  // equal-key32 ties across the band
+                uint32_t add = 0u;
+                for (uint32_t bj = band; bj; bj &= bj - 1)
+                    if (rank_in(__ffs(bj) - 1, band) < need) add |= 1u << (__ffs(bj) - 1);
+                sel |= add;
+            }
+            ok = img_cert(im, q, bhi, M);
             if (a.debug) a.debug[i] = make_int4(ok ? -1 : -2, M, (int)m, 0);
             if (ok) {
-                if (a.knn_idx) {  // sorted neighbour list (API output only)
-                    unsigned long long L[kImgList];
-#pragma unroll
-                    for (int j = 0; j < kImgList; ++j) {
-                        const bool take = j < nlo || (j >= kImgList - nbd && ((sel >> (kImgList - 1 - j)) & 1u));
-                        L[j] = take ? list[j][tid] : kEmptyKey;
-                    }
-                    sort_net<kImgList>(L);
-#pragma unroll
-                    for (int j = 0; j < K; ++j)
-                        if (j < k) a.knn_idx[(size_t)i * k + j] = (int32_t)ki_idx(L[j]);
-                }
-                // moments in list order (the sure entries, then the kept boundary entries, each in
-                // stencil order: deterministic), then the A4 epilogue
+                if (a.knn_idx)  // the k nearest in (key64, index) order (API output only)
+                    for (uint32_t f = sel; f; f &= f - 1)
+                        a.knn_idx[(size_t)i * k + rank_in(__ffs(f) - 1, sel)] = (int32_t)ki_idx(list[__ffs(f) - 1][tid]);
+                // moments over the selected slots in slot order (deterministic), then the A4 epilogue
                 double s1[3] = {0, 0, 0}, s2[6] = {0, 0, 0, 0, 0, 0};
-                auto acc = [&](unsigned long long e) {
-                    const float4 p = __ldg(a.pos + ki_idx(e));
+                for (uint32_t f = sel; f; f &= f - 1) {
+                    const float4 p = __ldg(a.pos + ki_idx(list[__ffs(f) - 1][tid]));
                     const double d0 = (double)p.x - (double)q.x, d1 = (double)p.y - (double)q.y,
                                  d2 = (double)p.z - (double)q.z;
                     s1[0] += d0;
@@ -651,12 +788,8 @@ __global__ void __launch_bounds__(kImgThreads, 4) k_knn_image(KnnArgs a, ImgArgs
                     s2[3] += d1 * d1;
                     s2[4] += d1 * d2;
                     s2[5] += d2 * d2;
-                };
-                for (int j = 0; j < nlo; ++j) acc(list[j][tid]);
-                for (int j = 0; j < nbd; ++j)
-                    if ((sel >> j) & 1u) acc(list[kImgList - 1 - j][tid]);
-                const int nsel = nlo + __popc(sel);
-                finish_moments(a, *a.d_n, i, s1, s2, nsel);
+                }
+                finish_moments(a, *a.d_n, i, s1, s2, __popc(sel));
             }
         }
     }
@@ -758,15 +891,15 @@ __device__ bool wide_attempt(const KnnArgs &a, const ImgArgs &im, int i, float4 
         fail = 2;
         return false;
     }
-    // the m <= 64 candidates at or below b*, two per lane, sorted: the 32 smallest end up in
-    // order across the lanes (lane j: j-th)
-    const uint32_t lim = bstar >= kImgBuckets - 1 ? 0x7F800000u : (uint32_t)(base + bstar + 1) << 21;
+    // the m <= 64 candidates at or below b* (its upper edge widened by the binary64 resolution
+    // band), two per lane, sorted: the 32 smallest end up in order across the lanes (lane j: j-th)
+    const float lim = bstar >= kImgBuckets - 1 ? INFINITY : band_hi(__uint_as_float((uint32_t)(base + bstar + 1) << 21));
     int nl = 0;
 #pragma unroll(CACHE ? PER : 4)
     for (int j = 0; j < PER; ++j) {
         int idx;
         const float key = get(j, idx);
-        const bool take = __float_as_uint(key) < lim && key < INFINITY;
+        const bool take = key <= lim && key < INFINITY;
         const unsigned bb = __ballot_sync(kFull, take);
         const int slot = nl + __popc(bb & ((1u << lane) - 1u));
         if (take && slot < 64) lst[slot] = pack_ki(key, (uint32_t)idx);
@@ -786,15 +919,21 @@ __device__ bool wide_attempt(const KnnArgs &a, const ImgArgs &im, int i, float4 
         const unsigned long long Br = shfl_u64(B, 31 - lane);  // descending
         A = WarpTopK<32>::merge32(A < Br ? A : Br, lane);      // the 32 smallest, a bitonic merge
     }
-    const unsigned long long last = shfl_u64(A, k - 1);
-    if (!img_cert(im, q, ki_key(last), M2)) {
+    const float t = ki_key(shfl_u64(A, k - 1));
+    if (!img_cert(im, q, band_hi(t), M2)) {
         fail = 1;
         return false;
     }
-    if (a.knn_idx && lane < k) a.knn_idx[(size_t)i * k + lane] = (int32_t)ki_idx(A);
+    int outpos = -1;
+    const bool ok = a.knn_idx ? warp_exact_select<true>(A, k, nl > 32, q.x, q.y, q.z, a.pos, lane, outpos)
+                              : warp_exact_select<false>(A, k, nl > 32, q.x, q.y, q.z, a.pos, lane, outpos);
+    if (!ok) {
+        fail = 2;
+        return false;
+    }
+    if (a.knn_idx && outpos >= 0) a.knn_idx[(size_t)i * k + outpos] = (int32_t)ki_idx(A);
     int ids[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) ids[j] = (int)ki_idx(shfl_u64(A, j));
+    collect_ids<K>(outpos, ki_idx(A), lane, ids);
     if (a.debug && lane == 0) a.debug[i] = make_int4(-3, M2, (int)m, 0);
     if (lane == 0) finish_query<K>(a, *a.d_n, i, q, k, ids);
     return true;
@@ -911,7 +1050,8 @@ __global__ void __cluster_dims__(kBruteCluster, 1, 1) __launch_bounds__(kBruteTh
             }
             const uint32_t excl = incl - sl;
             const unsigned hit = __ballot_sync(kFull, incl >= (uint32_t)k);
-            if (lane == 0) s_bin = -1;
+            // exactly one lane writes s_bin / s_below / s_m: the first lane whose prefix reaches k
+            // (its own 32 bins then contain the boundary bin), else lane 31
             if (hit) {
                 const int L = __ffs(hit) - 1;
                 if (lane == L) {
@@ -938,54 +1078,63 @@ __global__ void __cluster_dims__(kBruteCluster, 1, 1) __launch_bounds__(kBruteTh
         const uint32_t below = s_below, m = s_m;
         uint32_t klo = 0u, khi = 0x7F800000u;  // boundary range [klo, khi) of key bits
         if (bin < 1024) brute_bin_range(bin, klo, khi);
-        // pass 2: the k nearest = the `below` keys < klo plus the `need` smallest of [klo, khi)
-        const bool fits = below <= 32u && m - below <= 32u;  // (cluster-uniform)
+        (void)below;
+        (void)m;
+        // pass 2: keys below the boundary bin (shrunk by the binary64 resolution band) are among
+        // the k nearest; the boundary group runs up to the bin's top widened by the band
+        const float lo_lim = band_lo(__uint_as_float(klo));
+        const float hi_lim = khi >= 0x7F800000u ? INFINITY : band_hi(__uint_as_float(khi));
         if (tid == 0) {
             s_nl = 0;
             s_nb = 0;
         }
         __syncthreads();
-        if (fits) {
 #pragma unroll 4
-            for (int j = j0; j < n; j += js) {
-                const float4 P = __ldg(a.pos + j);
-                const float key = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
-                const uint32_t kb = __float_as_uint(key);
-                if (kb < khi && key < INFINITY) {
-                    const bool lo = kb < klo;
-                    const int slot = atomicAdd(lo ? &s_nl : &s_nb, 1);
-                    if (slot < 32) lst[(lo ? 0 : 32) + slot] = pack_ki(key, (uint32_t)j);
-                }
+        for (int j = j0; j < n; j += js) {
+            const float4 P = __ldg(a.pos + j);
+            const float key = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
+            if (key <= hi_lim && key < INFINITY) {
+                const bool lo = key < lo_lim;
+                const int slot = atomicAdd(lo ? &s_nl : &s_nb, 1);
+                if (slot < 32) lst[(lo ? 0 : 32) + slot] = pack_ki(key, (uint32_t)j);
             }
         }
         cl.sync();
         if (crank == 0 && warp == 0) {
-            if (!fits) {  // > 32 near-equal keys at the boundary: hand over to the hash
-                if (lane == 0) im.queue[atomicAdd(im.ctr + kImgCtrQueue3, 1u)] = (uint32_t)i;
-            } else {
-                // gather the CTAs' lists (at most 32 + 32 entries in all): lane j fetches entry j
-                unsigned long long L = kEmptyKey, Bd = kEmptyKey;
-                int nl = 0, nb = 0;
-                for (int r = 0; r < kBruteCluster; ++r) {
-                    const int cl_l = *cl.map_shared_rank(&s_nl, r), cl_b = *cl.map_shared_rank(&s_nb, r);
-                    const unsigned long long *rl = cl.map_shared_rank(lst, r);
-                    if (lane >= nl && lane < nl + cl_l) L = rl[lane - nl];
-                    if (lane >= nb && lane < nb + cl_b) Bd = rl[32 + lane - nb];
-                    nl += cl_l;
-                    nb += cl_b;
-                }
-                const int need = k - nl;
+            // gather the CTAs' lists (at most 32 + 32 entries in all): lane j fetches entry j
+            unsigned long long L = kEmptyKey, Bd = kEmptyKey;
+            int nl = 0, nb = 0;
+            bool over = false;
+            for (int r = 0; r < kBruteCluster; ++r) {
+                const int cl_l = *cl.map_shared_rank(&s_nl, r), cl_b = *cl.map_shared_rank(&s_nb, r);
+                over = over || cl_l > 32 || cl_b > 32;
+                const unsigned long long *rl = cl.map_shared_rank(lst, r);
+                if (lane >= nl && lane < nl + cl_l) L = rl[lane - nl];
+                if (lane >= nb && lane < nb + cl_b) Bd = rl[32 + lane - nb];
+                nl += cl_l;
+                nb += cl_b;
+            }
+            over = over || nl > 32 || nb > 32;
+            int outpos = -1;
+            unsigned long long A = kEmptyKey;
+            if (!over) {
+                L = WarpTopK<32>::sort_w<32>(L, lane);
                 Bd = WarpTopK<32>::sort_w<32>(Bd, lane);
                 const unsigned long long Bsh = shfl_u64(Bd, (lane - nl) & 31);
-                unsigned long long A = lane < nl ? L : (lane < nl + need ? Bsh : kEmptyKey);
-                A = WarpTopK<32>::sort_w<32>(A, lane);
-                if (a.knn_idx && lane < k) a.knn_idx[(size_t)i * k + lane] = A == kEmptyKey ? -1 : (int32_t)ki_idx(A);
-                int ids[K];
-#pragma unroll
-                for (int j = 0; j < K; ++j) {
-                    const unsigned long long v = shfl_u64(A, j);
-                    ids[j] = v == kEmptyKey ? -1 : (int)ki_idx(v);
+                A = lane < nl ? L : Bsh;  // every sure key32 < every boundary key32
+                over = !(a.knn_idx ? warp_exact_select<true>(A, k, nl + nb > 32, q.x, q.y, q.z, a.pos, lane, outpos)
+                                   : warp_exact_select<false>(A, k, nl + nb > 32, q.x, q.y, q.z, a.pos, lane, outpos));
+            }
+            if (over) {  // > 32 near-equal keys at the boundary: hand over to the hash
+                if (lane == 0) im.queue[atomicAdd(im.ctr + kImgCtrQueue3, 1u)] = (uint32_t)i;
+            } else {
+                if (a.knn_idx) {
+                    if (outpos >= 0) a.knn_idx[(size_t)i * k + outpos] = (int32_t)ki_idx(A);
+                    const int cnt = __popc(__ballot_sync(kFull, outpos >= 0));
+                    if (lane >= cnt && lane < k) a.knn_idx[(size_t)i * k + lane] = -1;
                 }
+                int ids[K];
+                collect_ids<K>(outpos, ki_idx(A), lane, ids);
                 if (a.debug && lane == 0) a.debug[i] = make_int4(-6, 0, (int)m, 0);
                 if (lane == 0) finish_query<K>(a, n, i, q, k, ids);
             }
@@ -1018,68 +1167,23 @@ cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s);
 template <int K>
 cudaError_t launch_epilogue(const KnnArgs &a, int cap, cudaStream_t s);
 
-int img_window() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("GSICP_IMG_M");
-        v = e ? atoi(e) : kImgM;
-        if (v < 4 || v > 6) v = kImgM;
-    }
-    return v;
-}
-
 template <int K, int M>
 cudaError_t launch_tile_m(const KnnArgs &a, const ImgArgs &im, cudaStream_t s) {
     constexpr int SW = kImgTX + 2 * M, SH = kImgTY + 2 * M;
     const int smem = (int)(sizeof(float4) * SW * SH + sizeof(uint32_t) * (kImgBuckets / 2) * kImgThreads +
                            sizeof(unsigned long long) * kImgList * kImgThreads);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_knn_image<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    static PerDevice<int> attr;  // the opt-in shared memory size, set once per device
+    attr.get([&](int) { return (int)cudaFuncSetAttribute(k_knn_image<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
     const dim3 grid((unsigned)((im.Ws + kImgTX - 1) / kImgTX), (unsigned)((im.Hs + kImgTY - 1) / kImgTY));
     launch_pdl(k_knn_image<K, M>, grid, dim3(kImgThreads), (size_t)smem, s, a, im);
     GSICP_LAUNCH_CHECK("k_knn_image");
     return cudaSuccess;
 }
 
-// window half-width: kImgM, or GSICP_IMG_M = 4..6 (A/B)
+// window half-width kImgM (4 and 6 measured slower in round 1)
 template <int K>
 cudaError_t launch_tile(const KnnArgs &a, const ImgArgs &im, cudaStream_t s) {
-    const int M = img_window();
-    return M == 4 ? launch_tile_m<K, 4>(a, im, s) : (M == 6 ? launch_tile_m<K, 6>(a, im, s) : launch_tile_m<K, 5>(a, im, s));
-}
-
-// side stream (per host thread) on which the fallback hash is built while the window kernels run;
-// forked from and joined back to the caller's stream with events (graph-capture safe)
-struct SideStream {
-    cudaStream_t s = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-    int dev = -1;
-};
-static cudaError_t side_stream(SideStream *&out) {
-    static thread_local SideStream ss;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (ss.s == nullptr || ss.dev != dev) {
-        cudaError_t e = cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming);
-        if (e != cudaSuccess) return e;
-        ss.dev = dev;
-    }
-    out = &ss;
-    return cudaSuccess;
-}
-
-bool img_cond_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("GSICP_COND");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
+    return launch_tile_m<K, kImgM>(a, im, s);
 }
 
 // stream used to capture conditional-node bodies (per host thread)
@@ -1095,30 +1199,10 @@ cudaStream_t body_stream() {
     return bs;
 }
 
-bool img_side_grid() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("GSICP_SIDE_GRID");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-
 template <int K>
 cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *pos, const int32_t *d_n, cudaStream_t s,
                          cudaEvent_t window_done) {
-    SideStream *ss = nullptr;
     cudaError_t e = cudaSuccess;
-    const bool side = img_side_grid();
-    if (side) {
-        // the hash of the cloud for the last-resort search, built off the critical path
-        if ((e = side_stream(ss)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(ss->fork, s)) != cudaSuccess) return e;
-        if ((e = cudaStreamWaitEvent(ss->s, ss->fork, 0)) != cudaSuccess) return e;
-        e = grid_build(a.g, pos, nullptr, nullptr, d_n, cap, ss->s);
-        if (e != cudaSuccess) return e;
-        if ((e = cudaEventRecord(ss->join, ss->s)) != cudaSuccess) return e;
-    }
     ktimer_mark(KT_COVS, false, s);
     ktimer_mark(KT_KNN_SEARCH, false, s);
     const int L = im.Hs * im.Ws;
@@ -1148,7 +1232,7 @@ cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *po
     // sets on the device; otherwise launched directly, each kernel returning at once when idle
     cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cst);
-    if (cst == cudaStreamCaptureStatusActive && !side && img_cond_enabled()) {
+    if (cst == cudaStreamCaptureStatusActive) {
         cudaGraph_t graph = nullptr;
         const cudaGraphNode_t *deps = nullptr;
         size_t nd = 0;
@@ -1193,9 +1277,7 @@ cudaError_t launch_image(KnnArgs a, const ImgArgs &im, int cap, const float4 *po
         GSICP_LAUNCH_CHECK("k_img_hash_n");
         ktimer_mark(KT_WIDE, true, s);
         ktimer_mark(KT_TAIL, false, s);
-        if (side) {
-            if ((e = cudaStreamWaitEvent(s, ss->join, 0)) != cudaSuccess) return e;
-        } else {  // inline, only for a non-empty hash queue (the build kernels return at once otherwise)
+        {  // inline, only for a non-empty hash queue (the build kernels return at once otherwise)
             const int32_t *hn = reinterpret_cast<const int32_t *>(im.ctr + kImgCtrHashN);
             e = grid_build(a.g, pos, nullptr, nullptr, hn, cap, s);
             if (e != cudaSuccess) return e;
@@ -1219,7 +1301,11 @@ cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s) {
     // a resident grid (one wave) pulling work batches; never more warps than batches
     const long long warps = (cap + kQueriesPerWarp - 1) / kQueriesPerWarp;
     const long long blocks = std::min<long long>(blocks_for(warps * 32, kKnnThreads), (long long)num_sms() * kKnnMinBlocks);
-    launch_pdl(k_knn_search<K>, dim3((unsigned)std::max<long long>(blocks, 1)), dim3(kKnnThreads), 0, s, a);
+    const dim3 grid((unsigned)std::max<long long>(blocks, 1));
+    if (a.sort_out)
+        launch_pdl(k_knn_search<K, true>, grid, dim3(kKnnThreads), 0, s, a);
+    else
+        launch_pdl(k_knn_search<K, false>, grid, dim3(kKnnThreads), 0, s, a);
     GSICP_LAUNCH_CHECK("k_knn_search");
     return cudaSuccess;
 }
@@ -1263,6 +1349,7 @@ cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, in
     a.cov_a = reinterpret_cast<float4 *>(cov_a);
     a.cov_b = reinterpret_cast<float4 *>(cov_b);
     a.knn_idx = knn_idx;
+    a.sort_out = knn_idx != nullptr;
     a.debug = reinterpret_cast<int4 *>(g_knn_debug);
     a.nbr_t = reinterpret_cast<int32_t *>(static_cast<char *>(ws) + grid_bytes(cap, levels, false));
     a.work = a.g.counters + kMaxLevels;
@@ -1287,6 +1374,7 @@ cudaError_t knn_graph_launch(const GridView &g, const float4 *pos, const int32_t
     a.d_n = d_n;
     a.k = kGraphK;
     a.knn_idx = knn_idx;
+    a.sort_out = 0;  // the graph needs the neighbour set only (k_graph_finalize takes the max key)
     a.nbr_t = nullptr;
     a.debug = nullptr;
     a.work = g.counters + kMaxLevels;
@@ -1316,6 +1404,7 @@ cudaError_t covariances_image_launch(const float *pos, const int32_t *d_n, int c
     a.cov_a = reinterpret_cast<float4 *>(cov_a);
     a.cov_b = reinterpret_cast<float4 *>(cov_b);
     a.knn_idx = knn_idx;
+    a.sort_out = knn_idx != nullptr;
     a.debug = reinterpret_cast<int4 *>(g_knn_debug);
     char *p = static_cast<char *>(ws) + grid_bytes(cap, levels, false);
     a.nbr_t = reinterpret_cast<int32_t *>(p);

@@ -159,19 +159,21 @@ __global__ void k_graph_finalize(const float4 *spos, const int32_t *d_n, const i
     if (s >= *d_n) return;
     const float4 p = spos[s];
     const int orig = __float_as_int(p.w);
-    int last = -1;
+    // the list is the exact kGraphK-NN SET (any order): its radius is the largest key32 in it
+    float kmax = 0.f;
+    bool short_list = false;
     for (int j = 0; j < kGraphK; ++j) {
         const int o = knn_idx[(size_t)orig * kGraphK + j];
         const int sl = o >= 0 ? inv[o] : -1;
         nbr[(size_t)s * kGraphK + j] = sl;
-        last = sl;
+        if (sl >= 0) {
+            const float4 q = spos[sl];
+            kmax = fmaxf(kmax, canon_key(p.x, p.y, p.z, q.x, q.y, q.z));
+        } else {
+            short_list = true;
+        }
     }
-    if (last >= 0) {
-        const float4 q = spos[last];
-        nbr_key[s] = canon_key(p.x, p.y, p.z, q.x, q.y, q.z);
-    } else {
-        nbr_key[s] = INFINITY;  // the list holds the whole cloud
-    }
+    nbr_key[s] = short_list ? INFINITY : kmax;  // INFINITY: the list holds the whole cloud
 }
 
 }  // namespace
@@ -221,17 +223,8 @@ static void fill_target(const GridView &g, const TargetWs &t, int M, gsicp_targe
     out->M = M;
 }
 
-// auto cell = mult x mean middle scale (a cost knob only; results are exact at any cell size).
-// GSICP_CELL_MULT overrides the multiplier (tuning experiments).
-static double auto_cell_mult() {
-    static double m = -1.0;
-    if (m < 0.0) {
-        const char *e = getenv("GSICP_CELL_MULT");
-        m = e ? atof(e) : 3.0;
-        if (!(m > 0.0)) m = 3.0;
-    }
-    return m;
-}
+// auto cell = kAutoCellMult x mean middle scale (a cost knob only; results are exact at any cell size)
+constexpr double kAutoCellMult = 3.0;
 
 cudaError_t build_target_launch(const float *means, const float *quats, const float *scales, int scales_are_log,
                                 int M, int mode, float eps, float cell, gsicp_target *out, void *ws,
@@ -260,7 +253,7 @@ cudaError_t build_target_launch(const float *means, const float *quats, const fl
             set_error("build_target auto cell: %s", cudaGetErrorString(e));
             return e;
         }
-        cell = (float)(auto_cell_mult() * sum / (double)M);
+        cell = (float)(kAutoCellMult * sum / (double)M);
         if (!(cell > 0.f)) cell = 0.01f;
     }
     GridView g = grid_carve(t.grid, M, 1, true, cell);

@@ -365,3 +365,16 @@ def test_solve_pd_fallback():
     np.testing.assert_allclose(x, np.linalg.solve(H + 1e-6 * 15.0 / 6.0 * np.eye(6), -b), rtol=1e-12)
     x, ok = oracle.solve(-np.eye(6), b)
     assert not ok
+
+
+def test_linearize_bsum_is_sum_of_per_pair_b_norms():
+    """bsum = sum_i |J_i^T M_i d_i| (SURVEY §8(c).5's b scale): with one valid pair it equals |b|;
+    with two pairs whose contributions cancel it is the sum of the two norms while b = 0."""
+    x = np.float32([[0, 0, 0]])
+    r = oracle.linearize(x, _HALF_I[None], np.float32([[0.3, 0, 0]]), _HALF_I[None], np.eye(4))
+    assert r["bsum"] == pytest.approx(np.linalg.norm(r["b"]), rel=1e-15)
+    x2 = np.float32([[0, 0, 0], [0, 0, 0]])
+    # two points at the origin matched to targets at +-0.3 x: contributions cancel
+    r2 = oracle.linearize(x2[:1], _HALF_I[None], np.float32([[0.3, 0, 0]]), _HALF_I[None], np.eye(4))
+    r3 = oracle.linearize(x2[:1], _HALF_I[None], np.float32([[-0.3, 0, 0]]), _HALF_I[None], np.eye(4))
+    assert r2["bsum"] == pytest.approx(r3["bsum"]) and np.allclose(r2["b"] + r3["b"], 0)

@@ -128,6 +128,83 @@ def job_throughput(units_per_rank: int, world_size: int, total_ms: float) -> flo
     return world_size * units_per_rank / (total_ms / 1000.0)
 
 
+def csrc_sha() -> str:
+    """Hash of the CUDA sources: ties a stored ncu traffic figure to the code it was measured on."""
+    import hashlib
+
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_2403_12550_b200", "csrc")
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh", ".inc")):
+            h.update(f.encode())
+            h.update(open(os.path.join(d, f), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def pct(xs, q):
+    return float(np.percentile(np.asarray(xs, dtype=np.float64), q))
+
+
+def time_frame_graph(g, tr, depth, tgt, T_init, steps, warmup, flush, stream, dev):
+    """A frame config timed like the headline: the whole frame (Tracker.step_async) captured in one
+    graph, replayed `steps` times with L2 flushed in between, CUDA events per replay on the launch
+    stream; each replay's pose compared bitwise with the first.  -> (ms list, stats, bitwise)"""
+    import torch
+
+    T0 = torch.from_numpy(np.ascontiguousarray(T_init).reshape(-1).copy()).to(dev)
+
+    def step():
+        tr.d_T.copy_(T0)
+        tr.step_async(depth, tgt, torch.cuda.current_stream(dev))
+
+    for _ in range(max(warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    cs = torch.cuda.Stream(dev)
+    fg = g.FrameGraph()
+    with fg.capture(cs):
+        step()
+    for _ in range(max(warmup, 3)):
+        fg.replay(stream)
+    torch.cuda.synchronize()
+    ms, poses = [], []
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fg.replay(stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+        poses.append(tr.d_T.cpu().numpy().copy())
+    bitwise = all(np.array_equal(p_, poses[0]) for p_ in poses)
+    return ms, g.decode_stats(tr.d_stats), bitwise
+
+
+class CollectiveWatch:
+    """Counts torch.distributed collectives issued while `active` (the timed regions): the replicas
+    share nothing on the data path, so the count must stay 0."""
+
+    def __init__(self, dist):
+        self.active = False
+        self.count = 0
+        if dist is None:
+            return
+        for name in ("all_reduce", "barrier", "all_gather", "broadcast", "reduce_scatter", "all_to_all",
+                     "all_gather_into_tensor", "reduce_scatter_tensor"):
+            fn = getattr(dist, name, None)
+            if fn is None:
+                continue
+
+            def wrap(f):
+                def inner(*a, **k):
+                    if self.active:
+                        self.count += 1
+                    return f(*a, **k)
+                return inner
+            setattr(dist, name, wrap(fn))
+
+
 def make_workload(rank: int):
     import synth
 
@@ -222,6 +299,7 @@ def bench_gpu(args):
             dist.init_process_group("nccl", device_id=dev)
     import paper_2403_12550_b200 as g
 
+    watch = CollectiveWatch(dist)
     w = make_workload(rank)
     K = w.K
     depth_host = torch.from_numpy(w.depth).pin_memory()
@@ -279,6 +357,8 @@ def bench_gpu(args):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    poses = []
+    watch.active = True
     with ClockSampler(local) as clk:
         for i in range(nev):
             flush.zero_()  # L2 flush (256 MB > 126 MB L2), outside the timed events
@@ -288,6 +368,9 @@ def bench_gpu(args):
             torch.cuda.synchronize()  # per-step kernel timer readout (host side, outside the events)
             for k in kt:
                 kt[k].append(g.debug_kernel_time(k))
+            poses.append(tr.d_T.cpu().numpy().copy())  # (outside the events) for the bitwise check
+    watch.active = False
+    repeat_bitwise = all(np.array_equal(p_, poses[0]) for p_ in poses)
     if dist:
         dist.barrier()
     step_ms = np.array([e0[i].elapsed_time(e1[i]) for i in range(nev)])
@@ -305,13 +388,54 @@ def bench_gpu(args):
     torch.cuda.synchronize()
     flush.zero_()
     torch.cuda.synchronize()
+    watch.active = True
     t0 = time.perf_counter()
     res_e2e = tr.track_host_stream([depth_host] * nev, tgt, T_init)
     t1 = time.perf_counter()
+    watch.active = False
     e2e_ms = [1000 * (t1 - t0) / nev] * nev
     Tg, st_e = res_e2e[-1]
     e2e_total = max_over_ranks(sum(e2e_ms), dist, dev)
     e2e_value = job_throughput(nev, ws, e2e_total)
+
+    # C2 (the same frame vs a 1e5-Gaussian map) and C3 (TUM-shaped noisy frame vs the 1e6 map, at
+    # stride 4 and stride 1): the other single-frame configs of BASELINE.json, timed like the headline
+    configs_lines = {}
+    if args.configs and rank == 0:
+        import synth
+
+        scene2 = synth.make_scene(1002)
+        m2, q2, s2, _ = synth.sample_map(scene2, 100_000, 4002)
+        tgt2 = g.build_target(torch.from_numpy(m2).to(dev), torch.from_numpy(q2).to(dev), torch.from_numpy(s2).to(dev))
+        ms2, st2, bw2 = time_frame_graph(g, tr, depth, tgt2, w.T_init, nev, args.warmup, flush, stream, dev)
+        configs_lines["c2"] = {"workload": "C2: the Replica-shaped frame (stride 4) vs a 1e5-Gaussian map",
+                               "aligns_per_s": 1000.0 / float(np.mean(ms2)), "ms_p10_p50_p90": [pct(ms2, 10), pct(ms2, 50), pct(ms2, 90)],
+                               "gn_iters": st2["iters"], "fitness": st2["fitness"], "repeat_bitwise": bw2}
+        del tgt2
+        w3 = synth.make_frame_workload(3, "tum", M=1_000_000, stride=1, noisy=True)
+        K3 = w3.K
+        tgt3 = g.build_target(torch.from_numpy(w3.means).to(dev), torch.from_numpy(w3.quats).to(dev),
+                              torch.from_numpy(w3.scales).to(dev))
+        depth3 = torch.from_numpy(w3.depth).to(dev)
+        for s3 in (4, 1):
+            tr3 = g.Tracker(K3.H, K3.W, (K3.fx, K3.fy, K3.cx, K3.cy), stride=s3, params=params, device=dev)
+            g.debug_kernel_timer(1)
+            ms3, st3, bw3 = time_frame_graph(g, tr3, depth3, tgt3, w3.T_init, max(10, nev // 3), args.warmup, flush,
+                                             stream, dev)
+            ka = g.debug_kernel_time(g.KT_ALIGN)
+            g.debug_kernel_timer(False)
+            n3 = tr3.cloud.n()
+            algo3 = ALGO_BYTES_ALIGN * n3 * max(1, st3["iters"])
+            configs_lines[f"c3_s{s3}"] = {
+                "workload": f"C3: TUM-shaped 640x480 noisy frame, stride {s3} ({n3} pts) vs the 1e6-Gaussian map",
+                "aligns_per_s": 1000.0 / float(np.mean(ms3)), "ms_p10_p50_p90": [pct(ms3, 10), pct(ms3, 50), pct(ms3, 90)],
+                "gn_iters": st3["iters"], "fitness": st3["fitness"], "status": st3["status"], "repeat_bitwise": bw3,
+                "k_align_ms_last": ka,
+                "k_align_roofline": None if not ka else {"achieved_gbs": algo3 / (ka / 1000) / 1e9,
+                                                         "frac": algo3 / (ka / 1000) / 1e9 / peaks()[0],
+                                                         "algo_bytes": algo3}}
+            del tr3
+        del tgt3, depth3
 
     # C5: sequence tracking — each rank its own synthetic 30 Hz sequence (scene 100+rank), frames
     # 1..n tracked in order with the constant-velocity initial pose computed on the device, one
@@ -413,18 +537,28 @@ def bench_gpu(args):
     kernel = max((k for k in cand if cand[k][0] is not None), key=lambda k: cand[k][0])
     kernel_ms, algo = cand[kernel]
     achieved = algo / (kernel_ms / 1000.0) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
-        traffic = json.load(open(prof)).get(kernel)
+        tj = json.load(open(prof))
+        traffic = tj.get(kernel)
+        fresh = tj.get("_csrc_sha") == csrc_sha()
+        traffic_src = {"file": "profiles/ncu_traffic.json", "capture": tj.get("_capture"),
+                       "same_cuda_sources": fresh,
+                       "note": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel"
+                               + ("" if fresh else "; STALE: measured on other CUDA sources")}
     line = {
         "metric": METRIC, "value": value, "unit": "aligns/s", "n_gpus": ws, "steps": nev, "warmup": args.warmup,
         "ms_per_step": total_ms / nev, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 storage + f64 math", "data": "synthetic",
         "config": {"workload": WORKLOAD, "n_src": n_src, "map_gaussians": tgt.M, "k": 20, "mode": "ellipse",
                    "max_iters": 30, "gn_iters_used": st["iters"], "max_corr_dist": 0.1, "parallelism": f"replicas{ws}",
+                   "rank_workload_seeds": [2 + 100 * r for r in range(ws)],
+                   "collectives_in_timed_region": watch.count,
                    "l2": "flushed between timed steps (256 MB write)"},
         "timing": "CUDA graph replay of the whole frame, CUDA events per step on the launch stream",
+        "ms_p10_p50_p90": [pct(step_ms, 10), pct(step_ms, 50), pct(step_ms, 90)],
+        "repeat_bitwise": repeat_bitwise,
         "stage_ms_eager": {names[j]: float(mean_stage[j]) for j in range(3)},
         "kernel_ms": {"k_knn_image (11x11 window tile)": kms[g.KT_KNN_SEARCH], "k_align": kms[g.KT_ALIGN],
                       "seed pass (k_align_seed + k_align_seed_hard, side stream)": kms[g.KT_SEED],
@@ -433,7 +567,7 @@ def bench_gpu(args):
                       "wide window + brute force + hash_n": kms[g.KT_WIDE],
                       "hash join + search + epilogue": kms[g.KT_TAIL]},
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                     "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src, "peak_kind": peak_kind,
                      "algo_bytes_per_launch": algo, "kernel_ms": kernel_ms},
         "e2e": {"value": e2e_value, "unit": "aligns/s", "h2d_bytes_per_step": int(tr.upload_bytes() + 16 * 8),
                 "d2h_bytes_per_step": 16 * 8 + 32,
@@ -444,6 +578,7 @@ def bench_gpu(args):
         "clocks": clk.summary(),
         "fitness": st["fitness"], "status": st["status"],
     }
+    line.update(configs_lines)
     if seq_line is not None:
         line["sequence"] = seq_line
     if batch_line is not None:
@@ -470,6 +605,7 @@ def main():
     ap.add_argument("--seq-frames", type=int, default=120, help="C5 sequence frames per rank (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=4, help="N2 frames per batched step (0: skip)")
+    ap.add_argument("--no-configs", dest="configs", action="store_false", help="skip the C2 / C3 objects")
     args = ap.parse_args()
     if args.impl == "reference":
         return bench_reference(args)

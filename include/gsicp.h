@@ -8,9 +8,16 @@
  *    library never allocates device memory.  Each call takes a caller workspace sized by
  *    the matching *_workspace_size() query (256-byte aligned base required).
  *  - `stream` is a cudaStream_t passed as void*.  All work is stream-ordered on it; calls are
- *    reentrant and keep no global mutable state, so independent calls on different streams /
- *    devices may run concurrently.  Only gsicp_align and gsicp_linearize
- *    synchronise `stream` (they return host results).
+ *    reentrant, so independent calls on different streams / devices may run concurrently (S:84,
+ *    S:163).  gsicp_align and gsicp_linearize synchronise `stream` (they return host results),
+ *    and so do the automatic cell sizes (cell <= 0) of gsicp_covariances / gsicp_build_target*.
+ *  - State: the library keeps per-device caches of device properties and kernel occupancies
+ *    (filled once per device under std::call_once, immutable after) and thread-local state only
+ *    (error string, launch counter, diagnostic hooks, a per-thread capture stream for
+ *    conditional graph nodes).  It reads no environment variables.
+ *  - Keys (DESIGN R1): every nearest-neighbour decision follows the binary64 K2
+ *    order (key = (dx*dx + dy*dy) + dz*dz with dx = (double)b.x - q.x, ties by lower index); the
+ *    kernels screen in binary32 and resolve the candidates near the k-th / best key in binary64.
  *  - Host-side argument errors return GSICP_ERR_INVALID_ARGUMENT before anything is launched.
  *    CUDA launch errors return GSICP_ERR_CUDA (detail in gsicp_last_error()).
  *  - Point layout (SoA, binary32, 16-byte aligned float4 records):
@@ -150,14 +157,16 @@ gsicp_status gsicp_upload_sampled_rows(float *dst_rows, const float *src_host, i
  *   NONE    sum_i max(lam_i, 1e-6) v_i v_i^T
  *   PLANE   v2 v2^T + v1 v1^T + eps_var v0 v0^T            (S = [1, 1, eps])
  *   ELLIPSE sum_i max(lam_i / lam_1, eps_var) v_i v_i^T     (Lambda' = Lambda/median(S), Eq. 4)
- * The neighbour order is the canonical binary32 key (R1) then index.  A device spatial hash with
+ * The neighbour order is the binary64 K2 key (R1) then index.  A device spatial hash with
  * `levels` cell sizes cell0 * 2^l is built in the workspace; every query picks the finest level
- * whose own cell holds >= 4 points and runs a certified expanding-ring search (exact result).
- *  pos      [dev] float4[cap] (w ignored), d_n [dev] count
+ * whose own cell holds >= 3 points and runs a certified expanding-ring search (exact result).
+ *  pos      [dev] float4[cap] (w ignored), d_n [dev] count; cap < 2^27
  *  k        1..32 neighbours.  If n < k all n points are used and GSICP_FLAG_LOW_SUPPORT set.
- *  cell0    finest cell edge (m, > 0); levels 1..8.  (Performance knobs only: results are exact.)
+ *  cell0    finest cell edge (m); <= 0: automatic (2 x the estimated point spacing for several
+ *           levels, 3 x for one; estimated on the device from a 32^3 occupancy grid; blocking);
+ *           levels 1..8.  (Performance knobs only: results are exact at any cell size.)
  *  cov_a, cov_b [dev] float4[cap] outputs in input order (cov_b.z = raw lam_1, cov_b.w = flags)
- *  knn_idx  [dev] nullable int32[cap*k]: neighbours sorted by (key, index), -1 padded
+ *  knn_idx  [dev] nullable int32[cap*k]: neighbours sorted by (K2 key, index), -1 padded
  *  Errors: INVALID_ARGUMENT. */
 size_t gsicp_covariances_workspace_size(int32_t cap, int32_t levels);
 gsicp_status gsicp_covariances(const float *pos, const int32_t *d_n, int32_t cap, int32_t k, gsicp_reg_mode mode,
@@ -167,10 +176,10 @@ gsicp_status gsicp_covariances(const float *pos, const int32_t *d_n, int32_t cap
 /* Same result as gsicp_covariances (bit-identical neighbour lists and covariances), for a
  * depth-frame cloud: pos/d_n exactly as written by gsicp_backproject_downsample with the same
  * (H, W, stride) and fx, fy of K (pos.w = pixel id v*W + u).  Candidates come from the
- * (2M+1)^2 lattice-pixel window around each query's pixel (M = 4), exact whenever the k-th
+ * (2M+1)^2 lattice-pixel window around each query's pixel (M = 5), exact whenever the k-th
  * radius rho satisfies the projection bound f rho (z + |x|) / (z (z - rho)) < (M+1) s in both
  * image axes (every point within rho then lies in the window); the remaining queries are
- * finished by the hash search of gsicp_covariances (cell0, levels as there).  A cloud that is
+ * finished by the hash search of gsicp_covariances (cell0 > 0, levels as there).  A cloud that is
  * not a depth-frame cloud (a pixel id off the lattice, two points on one pixel) is detected on
  * the device and handled entirely by the hash search, so the result is exact for any input.
  *  lattice_map [dev] nullable: the map gsicp_backproject_lattice wrote for exactly these points
@@ -201,7 +210,8 @@ gsicp_status gsicp_build_target(const float *means, const float *quats_wxyz, con
                                 gsicp_target *out, void *target_ws, size_t ws_bytes, void *stream);
 
 /* Same, from a cloud that already carries G-ICP covariances (e.g. gsicp_covariances output;
- * used for frame-to-frame tracking and the C1 configuration).  cell must be > 0. */
+ * used for frame-to-frame tracking and the C1 configuration).  cell <= 0: automatic (3 x the
+ * estimated point spacing; blocking).  M < 2^27. */
 gsicp_status gsicp_build_target_cloud(const gsicp_cloud *cloud, int32_t M, float cell, gsicp_target *out,
                                       void *target_ws, size_t ws_bytes, void *stream);
 
@@ -354,6 +364,53 @@ gsicp_status gsicp_export_gaussians(const float *pos, const float *cov_a, const 
                                     int32_t cap, const double *d_T, double p, double c, const int32_t *corr,
                                     float *means_out, float *quats_out, float *scales_out, int32_t *d_m_out,
                                     void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------
+ * N1  Keyframes and a device-resident growing map with incremental target maintenance
+ * (P:209-214 keyframe selection by the correspondence proportion, P:237 only Gaussians that do
+ * not overlap the current map, P:250-255 scale aligning, P:262-266 forced keyframe; R28, R29).
+ * The map owns its Gaussians (rows [0, *d_M) of means / quats wxyz / scales (linear), capacity
+ * rows) and the G-ICP target over them (`target`, usable by every align call).  An insertion
+ * appends a keyframe's exported Gaussians (gsicp_export_gaussians with the overlap filter) and
+ * maintains the target incrementally: the exact 16-NN lists are recomputed only for the new
+ * rows and the old rows whose list ball contains a new point; hash, dense cell
+ * array and slot lists are rebuilt by streaming kernels.  The result equals a from-scratch
+ * gsicp_build_target of the same rows (same neighbour sets, same covariances).  All counts stay
+ * on the device: an insertion (and the keyframe decision) can be captured in a CUDA graph. */
+typedef struct {
+    gsicp_target target;   /* views into the map workspace (target.M = capacity)       */
+    float *means;          /* [dev] float[capacity][3]                                 */
+    float *quats;          /* [dev] float[capacity][4] wxyz                            */
+    float *scales;         /* [dev] float[capacity][3] linear                          */
+    int32_t *d_M;          /* [dev] d_M[0] current rows, d_M[1] rows added by the last insert,
+                              d_M[4] Gaussians dropped because the map was full            */
+    int32_t capacity, max_insert, mode;
+    float cell, eps_var;
+    void *ws;              /* the map workspace (opaque)                                */
+} gsicp_map;
+
+/* capacity >= 1 rows (< 2^27), max_insert >= 1: the largest keyframe cloud cap inserted. */
+size_t gsicp_map_workspace_size(int32_t capacity, int32_t max_insert);
+/* Copies M0 (<= capacity) initial Gaussians (scales linear or log) into the map and builds its
+ * target with cell edge `cell` (<= 0: 3 x mean middle scale, blocking), kept for the map's life.
+ * mode / eps_var: the regularisation of the target covariances (as gsicp_build_target). */
+gsicp_status gsicp_map_init(const float *means, const float *quats_wxyz, const float *scales, int32_t scales_are_log,
+                            int32_t M0, int32_t capacity, int32_t max_insert, gsicp_reg_mode mode, float eps_var,
+                            float cell, gsicp_map *out, void *ws, size_t ws_bytes, void *stream);
+/* Appends the keyframe cloud's Gaussians (kf->cap <= max_insert; d_T [dev] double[16] its
+ * camera->world pose; corr [dev] nullable: the overlap filter, as gsicp_export_gaussians; p, c
+ * scale aligning) and maintains the target.  d_flag [dev] nullable int32: insert only if
+ * *d_flag != 0 — inside a stream capture this becomes a conditional graph node switched on the
+ * device; eagerly it is read back (blocking).  Rows beyond the capacity are dropped and counted
+ * in d_M[4].  Errors: INVALID_ARGUMENT, CUDA. */
+gsicp_status gsicp_map_insert(const gsicp_map *map, const gsicp_cloud *kf, const double *d_T, const int32_t *corr,
+                              double p, double c, const int32_t *d_flag, void *stream);
+/* P:209-214 / P:262-266 keyframe decision on the device (R29): d_state [dev] int32[2] =
+ * (frames since the last keyframe, decision); the frame is a keyframe iff it was tracked (status
+ * not TRACKING_LOST / DEGENERATE_FRAME) and fitness < min_fitness or max_gap frames have passed;
+ * then d_state = (0, 1), else (since + 1, 0).  d_stats [dev]: the frame's align stats. */
+gsicp_status gsicp_keyframe_decide(const gsicp_align_stats *d_stats, int32_t *d_state, float min_fitness,
+                                   int32_t max_gap, void *stream);
 
 /* CUDA-graph helpers for callers that capture a whole frame (host pointers; stream-ordered).
  * gsicp_graph_instantiate: instantiates a captured graph (cudaGraph_t) so that kernel nodes keep

@@ -129,6 +129,13 @@ def lib():
         L.gsicp_voxel_downsample.restype = i32
         L.gsicp_export_workspace_size.argtypes = [i32]
         L.gsicp_export_workspace_size.restype = sz
+        L.gsicp_map_workspace_size.argtypes = [i32, i32]
+        L.gsicp_map_workspace_size.restype = sz
+        L.gsicp_map_init.argtypes = [P, P, P, i32, i32, i32, i32, i32, f32, f32, P, P, sz, P]
+        L.gsicp_map_insert.argtypes = [P, P, P, P, C.c_double, C.c_double, P, P]
+        L.gsicp_keyframe_decide.argtypes = [P, P, f32, i32, P]
+        for name in ("gsicp_map_init", "gsicp_map_insert", "gsicp_keyframe_decide"):
+            getattr(L, name).restype = i32
         for name in ("gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_gaussians"):
             getattr(L, name).restype = i32
         L.gsicp_graph_instantiate.argtypes = [P, C.POINTER(C.c_void_p)]
@@ -163,7 +170,8 @@ EXPORTED = [
     "gsicp_debug_kernel_time", "gsicp_graph_instantiate", "gsicp_graph_launch", "gsicp_graph_destroy",
     "gsicp_pose_predict", "gsicp_pose_push", "gsicp_export_workspace_size", "gsicp_export_gaussians",
     "gsicp_align_batch_max", "gsicp_align_batch_async", "gsicp_voxel_downsample_workspace_size",
-    "gsicp_voxel_downsample",
+    "gsicp_voxel_downsample", "gsicp_map_workspace_size", "gsicp_map_init", "gsicp_map_insert",
+    "gsicp_keyframe_decide",
 ]
 
 KT_KNN_SEARCH, KT_ALIGN, KT_SEED, KT_BP, KT_COVS, KT_WIDE, KT_TAIL = 0, 1, 2, 3, 4, 5, 6
@@ -415,9 +423,9 @@ def upload_sampled_rows(dst_rows: torch.Tensor, depth_host: torch.Tensor, stride
 
 
 def covariances(pos: torch.Tensor, d_n: torch.Tensor, k: int = 20, mode: int = REG_ELLIPSE, eps_var: float = 1e-3,
-                cell0: float = 0.01, levels: int = 1, cov_a=None, cov_b=None, knn_idx: torch.Tensor | None = None,
+                cell0: float = 0.0, levels: int = 1, cov_a=None, cov_b=None, knn_idx: torch.Tensor | None = None,
                 ws=None, stream=None):
-    """A2-A4 (Eq. 3-4).  Returns a Cloud sharing `pos`."""
+    """A2-A4 (Eq. 3-4).  cell0 <= 0: automatic cell size (blocking).  Returns a Cloud sharing `pos`."""
     cap = pos.shape[0]
     dev = pos.device
     if cov_a is None:
@@ -471,6 +479,21 @@ class Target:
     def cell(self) -> float:
         return float(self.st.cell)
 
+    def graph_rows(self, n: int | None = None) -> np.ndarray:
+        """Diagnostic: the exact 16-NN graph by input row — (n, 16) int64, row r's neighbour rows
+        sorted ascending (-1 padded), for the first n slots' rows (default all M)."""
+        n = self.M if n is None else n
+        base = self.ws.data_ptr()
+        pos = self.arrays()[0][:n]
+        rows = pos[:, 3].contiguous().view(torch.int32).long().cpu().numpy()
+        off = self.st.nbr - base
+        nbr = self.ws[off:off + 4 * 16 * n].view(torch.int32).view(n, 16).long().cpu().numpy()
+        out = np.full((n, 16), -1, np.int64)
+        nb = np.where(nbr >= 0, rows[np.clip(nbr, 0, n - 1)], -1)
+        nb.sort(axis=1)
+        out[rows] = nb
+        return out
+
     def arrays(self):
         """(pos, cov_a, cov_b) as (M, 4) float32 views into the workspace, in cell order;
         pos[:, 3] holds the original index bits."""
@@ -494,7 +517,8 @@ def build_target(means: torch.Tensor, quats_wxyz: torch.Tensor, scales: torch.Te
     return Target(ws, st, (means, quats_wxyz, scales))
 
 
-def build_target_cloud(cloud: Cloud, cell: float, M: int | None = None, stream=None) -> Target:
+def build_target_cloud(cloud: Cloud, cell: float = 0.0, M: int | None = None, stream=None) -> Target:
+    """A5 for a cloud that carries covariances; cell <= 0: automatic (blocking)."""
     M = cloud.cap if M is None else M
     need = lib().gsicp_build_target_workspace_size(M)
     ws = _ws(need, cloud.pos.device)
@@ -921,83 +945,129 @@ def is_keyframe(fitness: float, since_last: int, min_fitness: float = 0.95, max_
     return fitness < min_fitness or since_last >= max_gap
 
 
+class _Map(C.Structure):
+    _fields_ = [("target", _Target), ("means", C.c_void_p), ("quats", C.c_void_p), ("scales", C.c_void_p),
+                ("d_M", C.c_void_p), ("capacity", C.c_int32), ("max_insert", C.c_int32), ("mode", C.c_int32),
+                ("cell", C.c_float), ("eps_var", C.c_float), ("ws", C.c_void_p)]
+
+
 class GaussianMap:
-    """A device-resident growing 3DGS map for tracking: rows [0, M) of means (cap,3), quats wxyz
-    (cap,4) and scales (cap,3) float32 buffers, and the G-ICP target over them (A5), rebuilt after
-    each insertion with a fixed cell size (the first build's: inserted Gaussians must not change
-    the search structure's scale)."""
+    """N1: a device-resident growing 3DGS map for tracking (gsicp_map_*): the library owns rows
+    [0, M) of means / quats wxyz / scales (linear) for `capacity` rows and the G-ICP target over
+    them, maintained INCREMENTALLY on insertion (only the affected 16-NN lists are recomputed; the
+    target views never move, so frame graphs captured against `tgt` stay valid as the map grows).
+    Counts live on the device: insert() can sit inside a CUDA graph, switched by a device flag."""
 
     def __init__(self, means: torch.Tensor, quats: torch.Tensor, scales: torch.Tensor, capacity: int,
-                 mode: int = REG_ELLIPSE, eps_var: float = 1e-3, cell: float = 0.0):
-        M = means.shape[0]
-        if capacity < M:
+                 max_insert: int | None = None, mode: int = REG_ELLIPSE, eps_var: float = 1e-3, cell: float = 0.0,
+                 scales_are_log: bool = False, stream=None):
+        M0 = means.shape[0]
+        if capacity < M0:
             raise ValueError("capacity < initial map size")
         dev = means.device
-        self.capacity, self.mode, self.eps = capacity, mode, eps_var
-        self.means = torch.zeros((capacity, 3), dtype=torch.float32, device=dev)
-        self.quats = torch.zeros((capacity, 4), dtype=torch.float32, device=dev)
-        self.scales = torch.zeros((capacity, 3), dtype=torch.float32, device=dev)
-        self.means[:M].copy_(means)
-        self.quats[:M].copy_(quats)
-        self.scales[:M].copy_(scales)
-        self.M = M
-        self.cell = cell
-        self.tgt = None
-        self.rebuild()
-        self.cell = float(self.tgt.st.cell)
+        self.capacity = int(capacity)
+        self.max_insert = int(max_insert if max_insert is not None else min(capacity, 1 << 20))
+        need = lib().gsicp_map_workspace_size(self.capacity, self.max_insert)
+        if need == 0:
+            raise ValueError("bad map capacity / max_insert")
+        self.ws = _ws(need, dev)
+        self.st = _Map()
+        m, q, sc = (x.contiguous() for x in (means, quats, scales))
+        _check(lib().gsicp_map_init(_ptr(m), _ptr(q), _ptr(sc), int(scales_are_log), M0, self.capacity,
+                                    self.max_insert, mode, eps_var, cell, C.byref(self.st), _ptr(self.ws),
+                                    self.ws.numel(), _stream(stream)))
+        self.tgt = Target(self.ws, self.st.target, (self,))
+        self.cell = float(self.st.cell)
+        base = self.ws.data_ptr()
 
-    def rebuild(self, stream=None):
-        self.tgt = build_target(self.means[:self.M], self.quats[:self.M], self.scales[:self.M], mode=self.mode,
-                                eps_var=self.eps, cell=self.cell, stream=stream)
+        def view(ptr, cols, dtype=torch.float32):
+            off = ptr - base
+            return self.ws[off:off + 4 * cols * self.capacity].view(dtype).view(self.capacity, cols)
+        self.means, self.quats, self.scales = view(self.st.means, 3), view(self.st.quats, 4), view(self.st.scales, 3)
+        off = self.st.d_M - base
+        self.d_M = self.ws[off:off + 32].view(torch.int32)  # [0] M, [1] last insert, [4] dropped (full)
 
-    def insert(self, cloud: Cloud, d_T: torch.Tensor, corr: torch.Tensor | None, p: float = 1.5, c: float = 1.0,
-               stream=None) -> int:
-        """Append the cloud's non-overlapping points (corr < 0; all if corr is None) as
-        scale-aligned Gaussians at the device pose d_T, then rebuild the target.  Returns how many."""
-        if self.M + cloud.cap > self.capacity:
-            raise RuntimeError(f"GaussianMap full: {self.M} + {cloud.cap} > {self.capacity}")
-        M = self.M
-        out = (self.means[M:M + cloud.cap], self.quats[M:M + cloud.cap], self.scales[M:M + cloud.cap])
-        s0 = stream if stream is not None else torch.cuda.current_stream(self.means.device)
-        with torch.cuda.stream(s0):  # allocation, export and count readback all ordered on s0
-            _, _, _, d_m = export_gaussians(cloud.pos, cloud.d_n, cloud.cov_a, cloud.cov_b, T=d_T, p=p, c=c,
-                                            corr=corr, out=out, stream=s0)
-            m = int(d_m.item())
-        if m:
-            self.M += m
-            self.rebuild(stream)
-        return m
+    @property
+    def M(self) -> int:
+        """Current row count (reads the device counter: synchronising)."""
+        return int(self.d_M[0].item())
+
+    def insert(self, cloud: Cloud, d_T: torch.Tensor, corr: torch.Tensor | None = None, p: float = 1.5,
+               c: float = 1.0, flag: torch.Tensor | None = None, stream=None):
+        """Append the cloud's non-overlapping points (corr < 0; all if corr is None) as scale-aligned
+        Gaussians at the device pose d_T and maintain the target (gsicp_map_insert).  flag (device
+        int32): insert only if nonzero (a conditional graph node inside a capture).  Asynchronous;
+        d_M[1] holds the rows added."""
+        cs = cloud.c_struct()
+        _check(lib().gsicp_map_insert(C.byref(self.st), C.byref(cs), _ptr(d_T), _ptr(corr), float(p), float(c),
+                                      _ptr(flag), _stream(stream)))
+
+
+def keyframe_decide(d_stats: torch.Tensor, state: torch.Tensor, min_fitness: float = 0.95, max_gap: int = 30,
+                    stream=None):
+    """Device keyframe decision (R29): state (int32[2] device) = (frames since
+    the last keyframe, this frame's decision), updated from the frame's align stats."""
+    _check(lib().gsicp_keyframe_decide(_ptr(d_stats), _ptr(state), float(min_fitness), int(max_gap),
+                                       _stream(stream)))
 
 
 def track_sequence_mapping(tr: Tracker, gmap: GaussianMap, frames_rows: torch.Tensor, T0, min_fitness: float = 0.95,
-                           max_gap: int = 30, p: float = 1.5, c: float = 1.0):
-    """Tracking with map growth (N1): frames 1..n-1 tracked in order from the constant-velocity
-    initial pose (host); a keyframe (is_keyframe) inserts its non-overlapping points into
-    the map (GaussianMap.insert with the tracker's final correspondences).  `tr` must be built with
-    keep_corr=True.  Returns (T_est (n-1,4,4), keyframe frame indices, Gaussians inserted per
-    keyframe, per-frame stats)."""
+                           max_gap: int = 30, p: float = 1.5, c: float = 1.0, timed: bool = False):
+    """Tracking with map growth (N1), frames 1..n-1 in order, one graph replay per frame and NO
+    host round trip: constant-velocity initial pose (gsicp_pose_predict) -> the frame
+    (A1-A9 from tr.rows) -> device keyframe decision (gsicp_keyframe_decide) -> a conditional
+    insertion of the frame's non-overlapping points into the map with incremental target
+    maintenance (gsicp_map_insert, the tracker's final correspondences as the overlap filter) ->
+    pose history.  `tr` must be built with keep_corr=True.  Returns (T_est (n-1,4,4), keyframe
+    frame indices, Gaussians inserted per keyframe, per-frame fitness, per-frame device ms or None)."""
     if tr.corr is None:
         raise ValueError("track_sequence_mapping needs Tracker(keep_corr=True)")
+    dev = tr.device
     n = frames_rows.shape[0]
-    prev2 = prev = np.ascontiguousarray(T0, dtype=np.float64).reshape(4, 4)
-    T_est, kfs, added, stats_all = [], [], [], []
-    since = 0
+    T0t = torch.from_numpy(np.ascontiguousarray(T0, dtype=np.float64).reshape(-1)).to(dev)
+    hist = torch.cat([T0t, T0t])
+    traj = torch.zeros((max(n - 1, 1), 16), dtype=torch.float64, device=dev)
+    counter = torch.zeros(1, dtype=torch.int32, device=dev)
+    state = torch.zeros(2, dtype=torch.int32, device=dev)
+    log = torch.zeros((max(n - 1, 1), 4), dtype=torch.float64, device=dev)  # fitness, keyframe, added, M
+    s = torch.cuda.Stream(dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    stats_f64 = tr.d_stats[:8].view(torch.float64)  # fitness (first field)
+
+    def frame():
+        pose_predict(hist, tr.d_T, s)
+        tr.step_async(None, gmap.tgt, s)
+        keyframe_decide(tr.d_stats, state, min_fitness, max_gap, s)
+        gmap.insert(tr.cloud, tr.d_T, tr.corr, p=p, c=c, flag=state[1:], stream=s)
+        rec = torch.stack([stats_f64[0], state[1].double(), gmap.d_M[1].double() * state[1].double(),
+                           gmap.d_M[0].double()]).view(1, 4)
+        log.index_copy_(0, counter.long().clamp(max=log.shape[0] - 1), rec)
+        pose_push(hist, tr.d_T, traj, counter, s)
+
+    with torch.cuda.stream(s):
+        tr.rows.copy_(frames_rows[min(1, n - 1)])
+        tr.step_async(None, gmap.tgt, s)  # one frame outside the capture (lazy library state), no insertion
+        s.synchronize()
+        fg = FrameGraph()
+        with fg.capture(s):
+            frame()
+    torch.cuda.current_stream(dev).wait_stream(s)
+    stream = torch.cuda.current_stream(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n - 1)] \
+        if timed else None
     for i in range(1, n):
-        init = prev @ np.linalg.inv(prev2) @ prev
         tr.rows.copy_(frames_rows[i])
-        T, st = tr.track_rows(gmap.tgt, init)
-        T_est.append(T)
-        stats_all.append(st)
-        since += 1
-        if is_keyframe(st["fitness"], since, min_fitness, max_gap):
-            m = gmap.insert(tr.cloud, tr.d_T, tr.corr, p=p, c=c)
-            kfs.append(i)
-            added.append(m)
-            since = 0
-            if m:
-                tr.drop_graphs()
-        prev2, prev = prev, T
-    return np.array(T_est), kfs, added, stats_all
+        if ev:
+            ev[i - 1][0].record(stream)
+        fg.replay(stream)
+        if ev:
+            ev[i - 1][1].record(stream)
+    torch.cuda.synchronize()
+    L = log[: n - 1].cpu().numpy()
+    kfs = [i + 1 for i in range(n - 1) if L[i, 1] > 0]
+    added = [int(L[i, 2]) for i in range(n - 1) if L[i, 1] > 0]
+    ms = np.array([a.elapsed_time(b) for a, b in ev]) if ev else None
+    return traj[: n - 1].cpu().numpy().reshape(-1, 4, 4), kfs, added, L[:, 0].copy(), ms
 
 
 class BatchTracker:

@@ -873,7 +873,7 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
     __shared__ int sBox[6];
     __shared__ CellIndex sIdx;
     // per-block queue of queries needing the general search (handled by whole warps)
-    __shared__ int sQn;
+    __shared__ int sQn, sQn2;
     __shared__ int sQtid[kT];
     __shared__ double4 sQq[kT];
     __shared__ double sQbk[kT];
@@ -986,6 +986,12 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
             if (!exact && nn.slot < 0 && a.nbr) {  // no warm start: the own cell's best becomes the candidate
                 nn_cold_start(a, sIdx, qc, own_se, q, nn);
                 own_left = make_uint2(0u, 0u);
+            } else if (!exact && a.nbr && nn.bk > 0.25 * (double)a.h * (double)a.h) {
+                // the query moved more than half a cell from its previous match (the large early
+                // pose updates): start the graph descent from the best of the own cell as well
+                // (one cached lookup, one cell of records) instead of walking from the far match
+                scan_target_cell(a, own_se, q, nn);
+                own_left = make_uint2(0u, 0u);
             }
             path_code = exact ? (seeded0 ? 4 : 0) : 1;
             if (!exact && nn.slot >= 0 && a.nbr) {
@@ -1055,6 +1061,7 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
                 warp_nn(a, sIdx, sBox, q, n2, lane, rho * rho, nn.slot);
                 d2 = fminf(n2.slot >= 0 ? sqrtf(__double2float_rd(n2.bk)) : INFINITY, rho) * (1.f - kReuseMargin);
             }
+            __syncwarp();  // every lane has read entry k (above) before lane 0 overwrites it
             if (lane == 0) {
                 sQbk[k] = nn.bk;
                 sQslot[k] = nn.slot;
@@ -1071,30 +1078,64 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
                 }
             valid0 = m0.slot >= 0 && m0.bk < a.r2;
         }
-        if (tid == 0) sQn = 0;  // next use is after at least one more __syncthreads
-        for (int i = i0 + G * kT; i < n; i += G * kT) {  // non-resident points (large clouds)
-            const float4 x = __ldg(a.spos + i);
-            double q0, q1, q2;
-            k3(T, x.x, x.y, x.z, q0, q1, q2);
-            const Qry q(q0, q1, q2);
-            const QueryCell qc(q.x, q.y, q.z, a.h, a.inv_h);
-            NN nn;
-            int slot = (it == 0 && sSeeded) ? a.seed_slot[i] : a.corr_ws[i];
-            if (slot <= -2) slot = -2 - slot;
-            if (slot >= 0) {
-                const float4 rec = __ldg(a.tpos + slot);
-                nn.set(q.key(rec), slot, rec);
-            }
-            if (!(it == 0 && sSeeded)) {
-                // the kNN-graph certificate from the previous match first (as for resident points)
-                bool exact = false;
-                if (nn.slot >= 0 && a.nbr) {
+        // non-resident points (clouds larger than the co-resident grid's threads): rounds of one
+        // point per thread over this block's chunks, the cheap certified paths per thread and the
+        // rest through the same block queue, solved by whole warps
+        __syncthreads();  // the resident readback of the queue (above) is done before its reuse
+        for (int r = 1;; ++r) {
+            const long long cb = ((long long)r * G + bid) * kT;  // this block's chunk (block-uniform)
+            if (P < kT || cb >= n) break;
+            if (tid == 0) sQn2 = 0;
+            __syncthreads();
+            const int i = (int)cb + tid;
+            if (i < n) {
+                const float4 x = __ldg(a.spos + i);
+                double q0, q1, q2;
+                k3(T, x.x, x.y, x.z, q0, q1, q2);
+                const Qry q(q0, q1, q2);
+                const QueryCell qc(q.x, q.y, q.z, a.h, a.inv_h);
+                NN nn;
+                const bool seeded = it == 0 && sSeeded;
+                int slot = seeded ? a.seed_slot[i] : a.corr_ws[i];
+                if (slot <= -2) slot = -2 - slot;
+                if (slot >= 0) {
+                    const float4 rec = __ldg(a.tpos + slot);
+                    nn.set(q.key(rec), slot, rec);
+                }
+                bool exact = seeded;
+                const uint2 own = sIdx.one(qc.c[0], qc.c[1], qc.c[2]);
+                uint2 own_left = own;
+                if (!exact && a.nbr && (nn.slot < 0 || nn.bk > 0.25 * (double)a.h * (double)a.h)) {
+                    scan_target_cell(a, own, q, nn);  // (as the resident path: a far or absent warm start)
+                    own_left = make_uint2(0u, 0u);
+                }
+                if (!exact && nn.slot >= 0 && a.nbr) {
                     float d2 = 0.f;
                     exact = graph_nn(a, q, nn, d2);
                 }
-                if (!exact) nn_search(a, sIdx, sBox, qc, sIdx.one(qc.c[0], qc.c[1], qc.c[2]), q, nn, false);
+                if (!exact && !a.nbr) exact = nn_search(a, sIdx, sBox, qc, own_left, q, nn, true);
+                if (exact) {
+                    a.corr_ws[i] = (nn.slot >= 0 && nn.bk < a.r2) ? nn.slot : -2 - nn.slot;
+                } else {
+                    const int k = atomicAdd(&sQn2, 1);
+                    sQtid[k] = i;
+                    sQq[k] = make_double4(q0, q1, q2, 0.0);
+                    sQbk[k] = nn.bk;
+                    sQslot[k] = nn.slot;
+                    sQp[k] = nn.p;
+                }
             }
-            a.corr_ws[i] = (nn.slot >= 0 && nn.bk < a.r2) ? nn.slot : -2 - nn.slot;
+            __syncthreads();
+            for (int k = warp; k < sQn2; k += kWarps) {
+                const double4 qq = sQq[k];
+                const Qry q(qq.x, qq.y, qq.z);
+                NN nn;
+                nn.slot = sQslot[k];
+                if (nn.slot >= 0) nn.set(sQbk[k], nn.slot, sQp[k]);
+                warp_nn(a, sIdx, sBox, q, nn, lane);
+                if (lane == 0) a.corr_ws[sQtid[k]] = (nn.slot >= 0 && nn.bk < a.r2) ? nn.slot : -2 - nn.slot;
+            }
+            __syncthreads();  // the queue entries are read before the next round refills them
         }
         sub_stamp(5);
         stamp(1);
@@ -1144,6 +1185,8 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
             for (int k = 0; k < kAlignTerms; ++k) sRed[warp][k] = acc[k];
         }
         __syncthreads();
+        // every thread's reads of the block queue (sQn, above) happened before this barrier
+        if (tid == 0) sQn = 0;
         double *part = a.partials + (size_t)(it & 1) * G * kPad;
         if (tid < kAlignTerms) {
             double s = 0.0;

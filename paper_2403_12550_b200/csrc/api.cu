@@ -78,7 +78,15 @@ cudaError_t voxel_launch(const float4 *pos, const int32_t *d_n, int cap, float v
 size_t export_ws_bytes(int cap);
 cudaError_t export_launch(const float4 *pos, const float4 *cov_a, const float4 *cov_b, const int32_t *d_n, int cap,
                           const double *d_T, double p, double c, const int32_t *corr, float *means, float *quats,
-                          float *scales, int32_t *d_m, void *ws, cudaStream_t s);
+                          float *scales, int32_t *d_m, void *ws, cudaStream_t s, const int32_t *d_base = nullptr);
+size_t map_ws_bytes(int cap, int max_insert);
+cudaError_t map_init_launch(const float *means, const float *quats, const float *scales, int scales_are_log, int M0,
+                            int cap, int max_insert, int mode, float eps, float cell, gsicp_map *out, void *ws,
+                            cudaStream_t s);
+cudaError_t map_insert_launch(const gsicp_map &mp, const gsicp_cloud &kf, const double *d_T, const int32_t *corr,
+                              double p, double c, const int32_t *d_flag, cudaStream_t s);
+cudaError_t keyframe_launch(const gsicp_align_stats *d_stats, int32_t *d_state, float min_fitness, int max_gap,
+                            cudaStream_t s);
 size_t align_ws_bytes(int cap);
 int align_batch_max();
 cudaError_t align_batch_launch(const gsicp_cloud *srcs, int B, const gsicp_target &tgt, double *d_T,
@@ -388,7 +396,7 @@ gsicp_status gsicp_covariances(const float *pos, const int32_t *d_n, int32_t cap
     if (k < 1 || k > 32) BAD("covariances: k must be in [1, 32]");
     if (mode != GSICP_REG_NONE && mode != GSICP_REG_PLANE && mode != GSICP_REG_ELLIPSE) BAD("covariances: bad mode");
     if (!(eps_var > 0.f) || !(eps_var <= 1.f)) BAD("covariances: eps_var must be in (0, 1]");
-    if (!(cell0 > 0.f) || !isfinite(cell0)) BAD("covariances: cell0 must be > 0");
+    if (!isfinite(cell0)) BAD("covariances: cell0 must be finite (<= 0: automatic)");
     if (levels < 1 || levels > kMaxLevels) BAD("covariances: levels must be in [1, %d]", kMaxLevels);
     gsicp_status st = check_ws(ws, ws_bytes, covariances_ws_bytes(cap, levels));
     if (st != GSICP_OK) return st;
@@ -427,6 +435,49 @@ gsicp_status gsicp_covariances_image(const float *pos, const int32_t *d_n, int32
                        "covariances_image");
 }
 
+size_t gsicp_map_workspace_size(int32_t capacity, int32_t max_insert) {
+    if (capacity < 1 || (uint32_t)capacity > kMaxBandIndex || max_insert < 1) return 0;
+    return map_ws_bytes(capacity, max_insert);
+}
+
+gsicp_status gsicp_map_init(const float *means, const float *quats_wxyz, const float *scales, int32_t scales_are_log,
+                            int32_t M0, int32_t capacity, int32_t max_insert, gsicp_reg_mode mode, float eps_var,
+                            float cell, gsicp_map *out, void *ws, size_t ws_bytes, void *stream) {
+    g_err[0] = 0;
+    if (!out || (M0 > 0 && (!means || !quats_wxyz || !scales))) BAD("map_init: null pointer");
+    if (capacity < 1 || (uint32_t)capacity > kMaxBandIndex) BAD("map_init: capacity must be in [1, 2^27)");
+    if (max_insert < 1) BAD("map_init: max_insert must be >= 1");
+    if (M0 < 0 || M0 > capacity) BAD("map_init: M0 must be in [0, capacity]");
+    if (mode != GSICP_REG_NONE && mode != GSICP_REG_PLANE && mode != GSICP_REG_ELLIPSE) BAD("map_init: bad mode");
+    if (!(eps_var > 0.f) || !(eps_var <= 1.f)) BAD("map_init: eps_var must be in (0, 1]");
+    if (!isfinite(cell)) BAD("map_init: cell must be finite");
+    if (M0 == 0 && !(cell > 0.f)) BAD("map_init: an empty map needs an explicit cell > 0");
+    gsicp_status st = check_ws(ws, ws_bytes, map_ws_bytes(capacity, max_insert));
+    if (st != GSICP_OK) return st;
+    return cuda_status(map_init_launch(means, quats_wxyz, scales, scales_are_log, M0, capacity, max_insert, (int)mode,
+                                       eps_var, cell, out, ws, (cudaStream_t)stream),
+                       "map_init");
+}
+
+gsicp_status gsicp_map_insert(const gsicp_map *map, const gsicp_cloud *kf, const double *d_T, const int32_t *corr,
+                              double p, double c, const int32_t *d_flag, void *stream) {
+    g_err[0] = 0;
+    if (!map || !map->ws) BAD("map_insert: null map");
+    gsicp_status st = check_cloud(kf, "map_insert");
+    if (st != GSICP_OK) return st;
+    if (kf->cap > map->max_insert) BAD("map_insert: keyframe cap %d > max_insert %d", kf->cap, map->max_insert);
+    if (!isfinite(p) || !isfinite(c) || !(c > 0.0)) BAD("map_insert: p must be finite and c > 0");
+    return cuda_status(map_insert_launch(*map, *kf, d_T, corr, p, c, d_flag, (cudaStream_t)stream), "map_insert");
+}
+
+gsicp_status gsicp_keyframe_decide(const gsicp_align_stats *d_stats, int32_t *d_state, float min_fitness,
+                                   int32_t max_gap, void *stream) {
+    g_err[0] = 0;
+    if (!d_stats || !d_state) BAD("keyframe_decide: null pointer");
+    if (max_gap < 1) BAD("keyframe_decide: max_gap must be >= 1");
+    return cuda_status(keyframe_launch(d_stats, d_state, min_fitness, max_gap, (cudaStream_t)stream), "keyframe_decide");
+}
+
 size_t gsicp_build_target_workspace_size(int32_t M) {
     if (M < 1) return 0;
     return target_ws_bytes(M);
@@ -455,7 +506,7 @@ gsicp_status gsicp_build_target_cloud(const gsicp_cloud *cloud, int32_t M, float
     if (st != GSICP_OK) return st;
     if (!out) BAD("build_target_cloud: null out");
     if (M < 1 || M > cloud->cap || (uint32_t)M > kMaxBandIndex) BAD("build_target_cloud: M must be in [1, min(cap, 2^27))");
-    if (!(cell > 0.f) || !isfinite(cell)) BAD("build_target_cloud: cell must be > 0");
+    if (!isfinite(cell)) BAD("build_target_cloud: cell must be finite (<= 0: automatic)");
     st = check_ws(target_ws, ws_bytes, target_ws_bytes(M));
     if (st != GSICP_OK) return st;
     return cuda_status(build_target_cloud_launch(*cloud, M, cell, out, target_ws, (cudaStream_t)stream),

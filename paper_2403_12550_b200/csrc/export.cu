@@ -36,6 +36,7 @@ struct ExportArgs {
     const int32_t *corr;  // nullable: export only corr < 0, compacted
     int32_t *tile_count;  // [tiles] (corr only)
     int32_t *d_m;         // nullable: rows written
+    const int32_t *d_base;  // nullable: rows are written at *d_base + row (appending to a map, N1)
 };
 
 __global__ void __launch_bounds__(kExportThreads) k_export_count(const int32_t *__restrict__ corr,
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(kExportThreads) k_export(ExportArgs a, int til
             m[r] = (float)__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(T[4 * r], xd), __dmul_rn(T[4 * r + 1], yd)),
                                               __dmul_rn(T[4 * r + 2], zd)),
                                     T[4 * r + 3]);
+        if (a.d_base) row += *a.d_base;
         const size_t i3 = 3 * (size_t)row, i4 = 4 * (size_t)row;
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
@@ -159,9 +161,9 @@ size_t export_ws_bytes(int cap) { return (size_t)((cap + kExportThreads - 1) / k
 
 cudaError_t export_launch(const float4 *pos, const float4 *cov_a, const float4 *cov_b, const int32_t *d_n, int cap,
                           const double *d_T, double p, double c, const int32_t *corr, float *means, float *quats,
-                          float *scales, int32_t *d_m, void *ws, cudaStream_t s) {
+                          float *scales, int32_t *d_m, void *ws, cudaStream_t s, const int32_t *d_base) {
     const int tiles = (cap + kExportThreads - 1) / kExportThreads;
-    ExportArgs a{pos, cov_a, cov_b, d_n, d_T, p, c, means, quats, scales, corr, (int32_t *)ws, d_m};
+    ExportArgs a{pos, cov_a, cov_b, d_n, d_T, p, c, means, quats, scales, corr, (int32_t *)ws, d_m, d_base};
     const int blocks = tiles < 8 * num_sms() ? tiles : 8 * num_sms();
     if (corr) {
         const cudaError_t e = launch_pdl(k_export_count, dim3(blocks), dim3(kExportThreads), 0, s, corr, d_n,

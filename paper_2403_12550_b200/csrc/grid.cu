@@ -1,4 +1,9 @@
 // Device spatial hash build (see grid.cuh).
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+
 #include "grid.cuh"
 #include "host_common.cuh"
 
@@ -157,7 +162,114 @@ __global__ void k_grid_scatter(GridView g, const float4 *__restrict__ pos, const
     }
 }
 
+// ---- spacing estimate of a cloud (the automatic cell size; a cost knob only — every search is
+// exact at any cell size): occupancy of a kSpG^3 trial grid over the bbox.  For points sampled on
+// surfaces at spacing l, each occupied trial cell (edge h) holds ~(h / l)^2 points, so
+// l ~= h sqrt(occupied / n).
+constexpr int kSpG = 32;
+constexpr int kSpWords = kSpG * kSpG * kSpG / 32;  // occupancy bitmap
+
+__global__ void k_sp_init(uint32_t *scr) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < kSpWords) scr[i] = 0u;
+    if (i < 3) {
+        reinterpret_cast<int32_t *>(scr + kSpWords)[i] = float_to_ordered(INFINITY);
+        reinterpret_cast<int32_t *>(scr + kSpWords)[3 + i] = float_to_ordered(-INFINITY);
+    }
+    if (i == 0) scr[kSpWords + 6] = scr[kSpWords + 7] = 0u;
+}
+
+__global__ void k_sp_bbox(const float4 *__restrict__ pos, const int32_t *__restrict__ d_n, uint32_t *scr) {
+    const int n = *d_n;
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 p = __ldg(pos + i);
+        const float c[3] = {p.x, p.y, p.z};
+        for (int a = 0; a < 3; ++a)
+            if (isfinite(c[a])) {
+                lo[a] = fminf(lo[a], c[a]);
+                hi[a] = fmaxf(hi[a], c[a]);
+            }
+    }
+    int32_t *bb = reinterpret_cast<int32_t *>(scr + kSpWords);
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+            hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(bb + a, float_to_ordered(lo[a]));
+            atomicMax(bb + 3 + a, float_to_ordered(hi[a]));
+        }
+    }
+}
+
+__global__ void k_sp_mark(const float4 *__restrict__ pos, const int32_t *__restrict__ d_n, uint32_t *scr) {
+    const int n = *d_n;
+    const int32_t *bb = reinterpret_cast<const int32_t *>(scr + kSpWords);
+    float lo[3], ext = 0.f;
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = ordered_to_float(bb[a]);
+        ext = fmaxf(ext, ordered_to_float(bb[3 + a]) - lo[a]);
+    }
+    const float inv = ext > 0.f ? (float)kSpG / ext : 0.f;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 p = __ldg(pos + i);
+        if (!isfinite(p.x) || !isfinite(p.y) || !isfinite(p.z)) continue;
+        const int x = min(max((int)((p.x - lo[0]) * inv), 0), kSpG - 1);
+        const int y = min(max((int)((p.y - lo[1]) * inv), 0), kSpG - 1);
+        const int z = min(max((int)((p.z - lo[2]) * inv), 0), kSpG - 1);
+        const int c = (z * kSpG + y) * kSpG + x;
+        atomicOr(scr + (c >> 5), 1u << (c & 31));
+    }
+}
+
+__global__ void k_sp_count(uint32_t *scr) {
+    uint32_t c = 0;
+    for (int i = threadIdx.x; i < kSpWords; i += blockDim.x) c += __popc(scr[i]);
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(scr + kSpWords + 6, c);
+}
+
 }  // namespace
+
+size_t spacing_scratch_bytes() { return (size_t)(kSpWords + 8) * sizeof(uint32_t); }
+
+// Blocking: reads the estimate back to the host.  scratch: >= spacing_scratch_bytes() of device memory.
+cudaError_t estimate_spacing(const float4 *pos, const int32_t *d_n, int cap, void *scratch, float *spacing,
+                             cudaStream_t s) {
+    uint32_t *scr = static_cast<uint32_t *>(scratch);
+    k_sp_init<<<blocks_for(kSpWords + 8, 256), 256, 0, s>>>(scr);
+    const unsigned gb = std::min<unsigned>(blocks_for(cap, 256), (unsigned)num_sms() * 8);
+    k_sp_bbox<<<gb, 256, 0, s>>>(pos, d_n, scr);
+    k_sp_mark<<<gb, 256, 0, s>>>(pos, d_n, scr);
+    k_sp_count<<<1, 1024, 0, s>>>(scr);
+    GSICP_LAUNCH_CHECK("estimate_spacing");
+    note_launch(4);
+    uint32_t host[8];
+    int32_t n = 0;
+    cudaError_t e = cudaMemcpyAsync(host, scr + kSpWords, sizeof(host), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&n, d_n, sizeof(n), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        set_error("estimate_spacing: %s", cudaGetErrorString(e));
+        return e;
+    }
+    auto of = [](uint32_t v) {
+        const int32_t i = (int32_t)v;
+        float f;
+        const int32_t b = i >= 0 ? i : i ^ 0x7FFFFFFF;
+        memcpy(&f, &b, sizeof f);
+        return f;
+    };
+    float ext = 0.f;
+    for (int a = 0; a < 3; ++a) ext = std::max(ext, of(host[3 + a]) - of(host[a]));
+    const double occ = (double)host[6];
+    double sp = 0.01;
+    if (n > 1 && ext > 0.f && std::isfinite(ext) && occ > 0.0) sp = (double)ext / kSpG * std::sqrt(occ / (double)n);
+    *spacing = (float)sp;
+    return cudaSuccess;
+}
 
 uint32_t grid_table_slots(int cap, int levels) {
     // >= 1.25 slots per (point, level): the load factor stays <= 80% even if every point sits in

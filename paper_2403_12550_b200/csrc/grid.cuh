@@ -42,6 +42,11 @@ uint32_t grid_table_slots(int cap, int levels);
 GridView grid_carve(void *base, int cap, int levels, bool with_cov, float h0, bool with_mark = false);
 cudaError_t grid_build(const GridView &g, const float4 *pos, const float4 *cov_a, const float4 *cov_b,
                        const int32_t *d_n, int n_host_max, cudaStream_t s);
+// automatic cell size: mean point spacing of a surface-sampled cloud (blocking; scratch >=
+// spacing_scratch_bytes() device bytes, e.g. the head of a grid workspace before its build)
+size_t spacing_scratch_bytes();
+cudaError_t estimate_spacing(const float4 *pos, const int32_t *d_n, int cap, void *scratch, float *spacing,
+                             cudaStream_t s);
 
 // bbox of level-0 cell coordinates at level l
 __device__ __forceinline__ void grid_cell_bbox(const GridView &g, int level, int lo[3], int hi[3]) {

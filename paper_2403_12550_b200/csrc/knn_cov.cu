@@ -1332,6 +1332,11 @@ cudaError_t launch_k(const KnnArgs &a, int cap, cudaStream_t s) {
 
 }  // namespace
 
+// automatic cell sizes (cell0 <= 0): multiples of the estimated point spacing — the C4 setting
+// (3 x spacing) for one level; finer for several levels (the coarser levels cover sparse parts)
+constexpr float kAutoCellMult = 3.0f;
+constexpr float kAutoCellMultiLevel = 2.0f;
+
 size_t covariances_ws_bytes(int cap, int levels) {
     return grid_bytes(cap, levels, false) + align_up((size_t)cap * kMaxK * sizeof(int32_t));
 }
@@ -1340,6 +1345,12 @@ cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, in
                                float cell0, int levels, float *cov_a, float *cov_b, int32_t *knn_idx, void *ws,
                                cudaStream_t s) {
     KnnArgs a{};
+    if (!(cell0 > 0.f)) {  // automatic: ~k-neighbourhood-sized finest cells (blocking estimate)
+        float sp = 0.f;
+        cudaError_t e = estimate_spacing(reinterpret_cast<const float4 *>(pos), d_n, cap, ws, &sp, s);
+        if (e != cudaSuccess) return e;
+        cell0 = (levels > 1 ? kAutoCellMultiLevel : kAutoCellMult) * sp;
+    }
     a.g = grid_carve(ws, cap, levels, false, cell0);
     a.pos = reinterpret_cast<const float4 *>(pos);
     a.d_n = d_n;
@@ -1377,6 +1388,26 @@ cudaError_t knn_graph_launch(const GridView &g, const float4 *pos, const int32_t
     a.sort_out = 0;  // the graph needs the neighbour set only (k_graph_finalize takes the max key)
     a.nbr_t = nullptr;
     a.debug = nullptr;
+    a.work = g.counters + kMaxLevels;
+    cudaError_t e = launch_search<kGraphK>(a, cap, s);
+    if (e != cudaSuccess) return e;
+    note_launch();
+    return cudaSuccess;
+}
+
+// The same for the queued points only (incremental maintenance of a growing map's graph, N1):
+// rows queue[0 .. *queue_n) get their exact kGraphK-NN lists over the grid's points.
+cudaError_t knn_graph_queue_launch(const GridView &g, const float4 *pos, const int32_t *d_n, int cap,
+                                   const uint32_t *queue, const uint32_t *queue_n, int32_t *knn_idx, cudaStream_t s) {
+    KnnArgs a{};
+    a.g = g;
+    a.pos = pos;
+    a.d_n = d_n;
+    a.k = kGraphK;
+    a.knn_idx = knn_idx;
+    a.sort_out = 0;
+    a.queue = queue;
+    a.queue_n = queue_n;
     a.work = g.counters + kMaxLevels;
     cudaError_t e = launch_search<kGraphK>(a, cap, s);
     if (e != cudaSuccess) return e;

@@ -14,7 +14,10 @@ def main():
     scene = synth.make_scene(1004)
     means, _, _, ell = synth.sample_map(scene, 4_000_000, 4004)
     c = g.Cloud.from_points(torch.from_numpy(means).cuda())
-    for cm, lv in ((3.0, 3), (2.5, 3), (3.5, 2)):
+    cases = ((3.0, 3), (2.5, 3), (3.5, 2))
+    if len(sys.argv) > 1:  # "1": only the bench configuration (profiling)
+        cases = cases[:int(sys.argv[1])]
+    for cm, lv in cases:
         ws = g._ws(g.lib().gsicp_covariances_workspace_size(c.cap, lv), c.pos.device)
         for _ in range(2):
             g.covariances(c.pos, c.d_n, 20, g.REG_ELLIPSE, 1e-3, cm * ell, lv, c.cov_a, c.cov_b, None, ws)

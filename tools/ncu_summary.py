@@ -19,9 +19,13 @@ WANT = OrderedDict([
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram % peak"),
     ("lts__t_bytes.sum", "L2 bytes"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
-    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
-    ("smsp__inst_executed.sum", "warp instructions"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA (fp32) pipe %"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64 pipe %"),
     ("sm__inst_executed_pipe_fp64.sum", "fp64 pipe instr"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("smsp__inst_executed.sum", "warp instructions"),
     ("smsp__thread_inst_executed_per_inst_executed.ratio", "active threads / warp"),
     ("launch__registers_per_thread", "registers"),
     ("launch__grid_size", "grid"),
@@ -105,6 +109,11 @@ def main():
     for k, v in sorted(agg.items(), key=lambda x: -x[1]):
         lines.append(f"| {k} | {cnt[k]} | {v:.0f} | {100 * v / tot:.1f}% |")
     open(prefix + "_ncu_summary.md", "w").write("\n".join(lines) + "\n")
+    sys.path.insert(0, ROOT)
+    from bench import csrc_sha
+
+    traffic["_csrc_sha"] = csrc_sha()
+    traffic["_capture"] = os.path.basename(rep)
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     print("\n".join(lines))
 

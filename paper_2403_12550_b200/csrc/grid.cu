@@ -37,7 +37,10 @@ __global__ void k_grid_init(CellEntry *table, uint32_t slots, uint32_t *counters
     }
 }
 
-__global__ void k_grid_insert(GridView g, const float4 *__restrict__ pos, const int32_t *__restrict__ d_n) {
+constexpr int kInsertThreads = 256;
+
+__global__ void __launch_bounds__(kInsertThreads) k_grid_insert(GridView g, const float4 *__restrict__ pos,
+                                                               const int32_t *__restrict__ d_n) {
     pdl_wait();
     pdl_launch_dependents();
     const int n = *d_n;
@@ -62,8 +65,13 @@ __global__ void k_grid_insert(GridView g, const float4 *__restrict__ pos, const 
     if (active && lane == leader) {
         s = hash_slot(key, g.mask);
         while (true) {
-            const unsigned long long prev = atomicCAS(&g.table[s].key, kEmptyKey, key);
-            if (prev == kEmptyKey || prev == key) break;
+            // a plain read first: once a cell exists (most inserts) no CAS is issued
+            const unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(&g.table[s].key);
+            if (cur == key) break;
+            if (cur == kEmptyKey) {
+                const unsigned long long prev = atomicCAS(&g.table[s].key, kEmptyKey, key);
+                if (prev == kEmptyKey || prev == key) break;
+            }
             s = (s + 1) & g.mask;
         }
         base = atomicAdd(&g.table[s].count, (uint32_t)__popc(peers));
@@ -82,10 +90,23 @@ __global__ void k_grid_insert(GridView g, const float4 *__restrict__ pos, const 
             v[a] = fminf(v[a], __shfl_xor_sync(0xffffffffu, v[a], o));
             v[3 + a] = fmaxf(v[3 + a], __shfl_xor_sync(0xffffffffu, v[3 + a], o));
         }
-    if ((threadIdx.x & 31) == 0 && v[0] <= v[3]) {
-        for (int a = 0; a < 3; ++a) {
-            atomicMin(g.bbox + a, float_to_ordered(v[a]));
-            atomicMax(g.bbox + 3 + a, float_to_ordered(v[3 + a]));
+    // block reduction, then one atomic per bound per block (same-address atomics serialise in L2:
+    // one per warp made the bbox the bottleneck of large builds)
+    __shared__ float sbb[6][kInsertThreads / 32];
+    const int wid = threadIdx.x >> 5;
+    if (lane == 0)
+#pragma unroll
+        for (int a = 0; a < 6; ++a) sbb[a][wid] = v[a];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        const int a = threadIdx.x;
+        float r = sbb[a][0];
+        for (int w = 1; w < kInsertThreads / 32; ++w) r = a < 3 ? fminf(r, sbb[a][w]) : fmaxf(r, sbb[a][w]);
+        if (isfinite(r)) {
+            if (a < 3)
+                atomicMin(g.bbox + a, float_to_ordered(r));
+            else
+                atomicMax(g.bbox + a, float_to_ordered(r));
         }
     }
 }
@@ -318,7 +339,7 @@ cudaError_t grid_build(const GridView &g, const float4 *pos, const float4 *cov_a
     const long long work = (long long)g.levels * g.cap;
     launch_pdl(k_grid_init, dim3(blocks_for(slots, T)), dim3(T), 0, s, g.table, slots, g.counters, g.bbox, g.mark, d_n);
     GSICP_LAUNCH_CHECK("k_grid_init");
-    launch_pdl(k_grid_insert, dim3(blocks_for(work, T)), dim3(T), 0, s, g, pos, d_n);
+    launch_pdl(k_grid_insert, dim3(blocks_for(work, kInsertThreads)), dim3(kInsertThreads), 0, s, g, pos, d_n);
     GSICP_LAUNCH_CHECK("k_grid_insert");
     launch_pdl(k_grid_alloc, dim3(blocks_for(slots, kAllocThreads * kAllocPerThread)), dim3(kAllocThreads), 0, s, g, d_n);
     GSICP_LAUNCH_CHECK("k_grid_alloc");

@@ -1162,6 +1162,277 @@ __global__ void k_img_hash_n(ImgArgs im, const int32_t *__restrict__ d_n, cudaGr
     if (use_cond) cudaGraphSetConditional(cond, hq ? 1u : 0u);  // the graph runs the hash tail only if needed
 }
 
+// ---------------------------------------------------------------------------------------------
+// Brick kNN for general clouds (maps, voxel clouds; A3+A4 of gsicp_covariances): the grid's
+// level-0 cells are "bricks" of edge H.  A warp takes one occupied brick: it stages every point
+// of the brick's 27-brick neighbourhood that lies in the brick's box expanded by R = 0.6 H into
+// shared memory, then runs the brick's points as queries, one per lane, over the staged
+// candidates (all lanes read the same candidate: shared-memory broadcast, no divergence) with
+// the image kernel's exact two-pass selection: a per-lane histogram of quarter-octave key
+// buckets gives the boundary bucket b*, a second pass collects the <= 32 candidates at or below
+// it, and the boundary is resolved exactly in binary64.  The result is exact when
+// the k-th ball lies inside the expanded box (every point within it was staged); the rest (and
+// bricks whose neighbourhood overflows the staging buffer) go to a queue that the warp search
+// finishes.  Candidates per query ~ (H + 2R)^2 / l^2 on a surface sampled at spacing l — with
+// H ~ 6 l about 300, against the warp search's list maintenance per candidate.
+constexpr int kBrickWarps = 4;
+constexpr int kBrickCap = 352;  // staged candidates per warp (4 blocks / SM in shared memory)
+constexpr float kBrickHalo = 0.6f;
+// per warp: staged candidates, histogram columns, list keys, list slots, the 27-brick cell table
+constexpr int kBrickSmemPerWarp = kBrickCap * 16 + 16 * 32 * 4 + 32 * 32 * 4 + 32 * 32 * 2 + 32 * 8;
+
+struct BrickArgs {
+    const uint4 *bricks;     // (start, count, key lo, key hi) of the occupied level-0 cells
+    const uint32_t *n_bricks;
+    uint32_t *queue;         // queries left to the warp search (input indices)
+    uint32_t *queue_n;
+};
+
+// the occupied level-0 cells of the grid as a compact list (one atomic per warp)
+__global__ void k_brick_list(GridView g, uint4 *bricks, uint32_t *n_bricks) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    CellEntry e;
+    e.key = kEmptyKey;
+    e.count = 0;
+    if (s <= g.mask) e = g.table[s];
+    const bool occ = e.key != kEmptyKey && (e.key >> 60) == 0ull && e.count > 0;
+    const unsigned b = __ballot_sync(kFull, occ);
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == 0 && b) base = atomicAdd(n_bricks, (uint32_t)__popc(b));
+    base = __shfl_sync(kFull, base, 0);
+    if (occ) bricks[base + __popc(b & ((1u << lane) - 1u))] = make_uint4(e.start, e.count, (uint32_t)e.key, (uint32_t)(e.key >> 32));
+}
+
+template <int K, bool SORT>
+__global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, BrickArgs b) {
+    pdl_wait();
+    pdl_launch_dependents();
+    extern __shared__ __align__(16) unsigned char brick_smem[];  // kBrickSmemPerWarp per warp
+    const GridView &g = a.g;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned char *wsm = brick_smem + (size_t)wid * kBrickSmemPerWarp;
+    float4 *cand = reinterpret_cast<float4 *>(wsm);
+    uint32_t(*hist)[32] = reinterpret_cast<uint32_t(*)[32]>(wsm + kBrickCap * 16);
+    float(*lkey)[32] = reinterpret_cast<float(*)[32]>(wsm + kBrickCap * 16 + kImgBuckets / 2 * 32 * 4);
+    uint16_t(*lst)[32] = reinterpret_cast<uint16_t(*)[32]>(wsm + kBrickCap * 16 + kImgBuckets / 2 * 32 * 4 +
+                                                           kImgList * 32 * 4);
+    uint2 *scell = reinterpret_cast<uint2 *>(wsm + kBrickCap * 16 + kImgBuckets / 2 * 32 * 4 + kImgList * 32 * 4 +
+                                             kImgList * 32 * 2);
+    const int k = a.k, n = *a.d_n;
+    const uint32_t nb = *b.n_bricks;
+    const float H = g.h0, R = kBrickHalo * g.h0;
+    for (uint32_t w = blockIdx.x * kBrickWarps + wid; w < nb; w += gridDim.x * kBrickWarps) {
+        const uint4 be = __ldg(b.bricks + w);
+        const uint32_t start = be.x, cnt = be.y;
+        const unsigned long long key = ((unsigned long long)be.w << 32) | be.z;
+        const int c[3] = {(int)((key >> 40) & 0xFFFFFull) - kCoordOff, (int)((key >> 20) & 0xFFFFFull) - kCoordOff,
+                          (int)(key & 0xFFFFFull) - kCoordOff};
+        float elo[3], ehi[3];
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            elo[ax] = (float)c[ax] * H - R;
+            ehi[ax] = (float)(c[ax] + 1) * H + R;
+        }
+        // ---- stage the expanded box's points (27 bricks probed one per lane, then scanned as one
+        // flattened range, 32 records per round)
+        int dx = 0, dy = 0, dz = 0;
+        if (lane > 0 && lane < 27) shell_cell(1, lane - 1, dx, dy, dz);
+        const uint2 se = lane < 27 ? cell_lookup(g.table, g.mask, cell_key(0, c[0] + dx, c[1] + dy, c[2] + dz))
+                                   : make_uint2(0u, 0u);
+        uint32_t incl = se.y;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        const uint32_t excl = incl - se.y;
+        const unsigned ne = __ballot_sync(kFull, se.y != 0u);
+        if (se.y) scell[__popc(ne & ((1u << lane) - 1u))] = make_uint2(se.x, excl);
+        __syncwarp();
+        int nc = 0, before = 0;
+        for (uint32_t rb = 0; rb < total; rb += 32) {
+            const bool here = se.y != 0u && excl >= rb && excl < rb + 32u;
+            const unsigned P = __reduce_or_sync(kFull, here ? 1u << (excl - rb) : 0u);
+            const uint32_t item = rb + lane;
+            bool in = false;
+            float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (item < total) {
+                const uint2 ce = scell[before + __popc(P & (0xffffffffu >> (31 - lane))) - 1];
+                p = __ldg(g.spos + ce.x + (item - ce.y));
+                in = p.x >= elo[0] && p.x <= ehi[0] && p.y >= elo[1] && p.y <= ehi[1] && p.z >= elo[2] && p.z <= ehi[2];
+            }
+            before += __popc(P);
+            const unsigned bi = __ballot_sync(kFull, in);
+            const int slot = nc + __popc(bi & ((1u << lane) - 1u));
+            if (in && slot < kBrickCap) cand[slot] = p;
+            nc += __popc(bi);
+        }
+        __syncwarp();
+        const bool over = nc > kBrickCap;
+        // ---- the brick's points as queries, 32 per round
+        // bucket kImgBucketRef <-> (2 l)^2 with l^2 ~ 1.5 H^2 / cnt (a surface through the brick)
+        const float sp2 = 6.f * H * H / (float)max(cnt, 1u);
+        const int base = (int)(__float_as_uint(fmaxf(sp2, 1e-30f)) >> 21) - kImgBucketRef;
+        for (uint32_t qb = 0; qb < cnt; qb += 32) {
+            const bool has = qb + lane < cnt;
+            const float4 q = has ? __ldg(g.spos + start + qb + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const int i = __float_as_int(q.w);
+            bool ok = has && !over;
+            if (!__any_sync(kFull, ok)) {
+                if (has) b.queue[atomicAdd(b.queue_n, 1u)] = (uint32_t)i;
+                continue;
+            }
+#pragma unroll
+            for (int h = 0; h < kImgBuckets / 2; ++h) hist[h][lane] = 0u;
+            // pass 1: histogram of the candidates' keys (branch-free: a lane without a query fills
+            // its own column, which is never read)
+#pragma unroll 4
+            for (int j = 0; j < nc; ++j) {
+                const float4 P = cand[j];
+                const float kk = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
+                const int bk = min(max((int)(__float_as_uint(kk) >> 21) - base, 0), kImgBuckets - 1);
+                atomicAdd(&hist[bk >> 1][lane], 1u << ((bk & 1) * 16));
+            }
+            int bstar = -1;
+            uint32_t cum = 0, m = 0;
+#pragma unroll
+            for (int h = 0; h < kImgBuckets / 2; ++h) {
+                const uint32_t wd = hist[h][lane];
+#pragma unroll
+                for (int hb = 0; hb < 2; ++hb) {
+                    const uint32_t cc = (wd >> (16 * hb)) & 0xFFFFu;
+                    if (bstar < 0 && cum + cc >= (uint32_t)k) {
+                        bstar = 2 * h + hb;
+                        m = cum + cc;
+                    }
+                    cum += cc;
+                }
+            }
+            ok = ok && bstar >= 0 && m <= (uint32_t)kImgList;
+            // pass 2: below b*'s lower edge (shrunk by the band) from the bottom of the list, up to
+            // its upper edge (widened by the band) from the top; slots of the staged candidates
+            const float lo_lim = bstar > 0 ? band_lo(__uint_as_float((uint32_t)(base + bstar) << 21)) : -1.f;
+            const float lim = (bstar < 0 || bstar >= kImgBuckets - 1)
+                                  ? INFINITY
+                                  : band_hi(__uint_as_float((uint32_t)(base + bstar + 1) << 21));
+            int nlo = 0, nbd = 0;
+            if (__any_sync(kFull, ok)) {
+#pragma unroll 4
+                for (int j = 0; j < nc; ++j) {
+                    const float4 P = cand[j];
+                    const float kk = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
+                    const bool take = ok && kk <= lim && kk < INFINITY;
+                    const bool lo = kk < lo_lim;
+                    const int slot = lo ? nlo : kImgList - 1 - nbd;
+                    if (take && nlo + nbd < kImgList) {
+                        lst[slot][lane] = (uint16_t)j;
+                        lkey[slot][lane] = kk;
+                    }
+                    nlo += (take && lo) ? 1 : 0;
+                    nbd += (take && !lo) ? 1 : 0;
+                }
+            }
+            ok = ok && nlo + nbd <= kImgList && nlo < k && nlo + nbd >= k;
+            const double qx = q.x, qy = q.y, qz = q.z;
+            auto key32_of = [&](int s) { return lkey[s][lane]; };
+            auto key64_of = [&](int s, uint32_t &id) {
+                const float4 P = cand[lst[s][lane]];
+                id = (uint32_t)__float_as_int(P.w);
+                return key64(qx, qy, qz, P.x, P.y, P.z);
+            };
+            auto rank_in = [&](int s, uint32_t mask) {
+                uint32_t ij;
+                const double kj = key64_of(s, ij);
+                int rank = 0;
+                for (uint32_t bl = mask; bl; bl &= bl - 1) {
+                    uint32_t il;
+                    const double kl = key64_of(__ffs(bl) - 1, il);
+                    rank += (kl < kj || (kl == kj && il < ij)) ? 1 : 0;
+                }
+                return rank;
+            };
+            uint32_t sel = 0u;
+            float bhi = 0.f;
+            if (ok) {
+                // t = the k-th smallest key32 (the (k - nlo)-th of the boundary group by (key32, slot)),
+                // then in below band_lo(t), a tie band around t ranked by (key64, index)
+                const int r = k - nlo;
+                float t = 0.f;
+                for (int s = kImgList - nbd; s < kImgList; ++s) {
+                    const float ks = key32_of(s);
+                    int rank = 0;
+                    for (int l = kImgList - nbd; l < kImgList; ++l) {
+                        const float kl = key32_of(l);
+                        rank += (kl < ks || (kl == ks && lst[l][lane] < lst[s][lane])) ? 1 : 0;
+                    }
+                    if (rank == r - 1) t = ks;
+                }
+                const float blo = band_lo(t);
+                bhi = band_hi(t);
+                const uint32_t filled =
+                    (nlo >= 32 ? ~0u : ((1u << nlo) - 1u)) | (nbd == 0 ? 0u : ~0u << (kImgList - nbd));
+                uint32_t band = 0u;
+                for (uint32_t f = filled; f; f &= f - 1) {
+                    const int s = __ffs(f) - 1;
+                    const float ks = key32_of(s);
+                    sel |= (ks < blo ? 1u : 0u) << s;
+                    band |= (ks >= blo && ks <= bhi ? 1u : 0u) << s;
+                }
+                const int need = k - __popc(sel);
+                if (__popc(band) == need) {
+                    sel |= band;
+                } else {
+                    uint32_t add = 0u;
+                    for (uint32_t bj = band; bj; bj &= bj - 1)
+                        if (rank_in(__ffs(bj) - 1, band) < need) add |= 1u << (__ffs(bj) - 1);
+                    sel |= add;
+                }
+                // certificate: the k-th ball (binary64 radius with margin) inside the expanded box
+                const double rho = sqrt((double)bhi) * (1.0 + 1e-5) + 1e-9;
+                const double qc[3] = {qx, qy, qz};
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    const double mg = 1e-7 * fabs(qc[ax]);
+                    ok = ok && qc[ax] - rho - mg >= (double)elo[ax] && qc[ax] + rho + mg <= (double)ehi[ax];
+                }
+            }
+            if (ok) {
+                if (a.knn_idx) {
+                    for (uint32_t f = sel; f; f &= f - 1) {
+                        const int s = __ffs(f) - 1;
+                        const int rk = SORT ? rank_in(s, sel) : __popc(sel & ((1u << s) - 1u));
+                        a.knn_idx[(size_t)i * k + rk] = __float_as_int(cand[lst[s][lane]].w);
+                    }
+                }
+                double s1[3] = {0, 0, 0}, s2[6] = {0, 0, 0, 0, 0, 0};
+                for (uint32_t f = sel; f; f &= f - 1) {
+                    const float4 P = cand[lst[__ffs(f) - 1][lane]];
+                    const double d0 = (double)P.x - qx, d1 = (double)P.y - qy, d2 = (double)P.z - qz;
+                    s1[0] += d0;
+                    s1[1] += d1;
+                    s1[2] += d2;
+                    s2[0] += d0 * d0;
+                    s2[1] += d0 * d1;
+                    s2[2] += d0 * d2;
+                    s2[3] += d1 * d1;
+                    s2[4] += d1 * d2;
+                    s2[5] += d2 * d2;
+                }
+                finish_moments(a, n, i, s1, s2, __popc(sel));
+                if (a.debug) a.debug[i] = make_int4(-7, nc, (int)m, 0);
+            } else if (has) {
+                b.queue[atomicAdd(b.queue_n, 1u)] = (uint32_t)i;
+            }
+            __syncwarp();  // the histogram / list columns are reused by the next round
+        }
+        __syncwarp();  // the staged candidates are reused by the next brick
+    }
+}
+
 template <int K>
 cudaError_t launch_search(const KnnArgs &a, int cap, cudaStream_t s);
 template <int K>
@@ -1330,15 +1601,48 @@ cudaError_t launch_k(const KnnArgs &a, int cap, cudaStream_t s) {
     return cudaSuccess;
 }
 
+// General clouds: bricks (k_knn_brick) then the warp search over the queue they leave
+template <int K>
+cudaError_t launch_brick(KnnArgs a, const BrickArgs &b, int cap, cudaStream_t s) {
+    const GridView &g = a.g;
+    ktimer_mark(KT_KNN_SEARCH, false, s);
+    launch_pdl(k_brick_list, dim3(blocks_for((long long)g.mask + 1, 256)), dim3(256), 0, s, g, const_cast<uint4 *>(b.bricks),
+               const_cast<uint32_t *>(b.n_bricks));
+    GSICP_LAUNCH_CHECK("k_brick_list");
+    const dim3 grid((unsigned)num_sms() * 4);  // one resident wave (4 blocks / SM by shared memory)
+    constexpr int smem = kBrickWarps * kBrickSmemPerWarp;
+    static PerDevice<int> attr;  // opt-in dynamic shared memory, once per device
+    attr.get([&](int) {
+        cudaFuncSetAttribute(k_knn_brick<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        return (int)cudaFuncSetAttribute(k_knn_brick<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    });
+    if (a.sort_out)
+        launch_pdl(k_knn_brick<K, true>, grid, dim3(kBrickWarps * 32), (size_t)smem, s, a, b);
+    else
+        launch_pdl(k_knn_brick<K, false>, grid, dim3(kBrickWarps * 32), (size_t)smem, s, a, b);
+    GSICP_LAUNCH_CHECK("k_knn_brick");
+    ktimer_mark(KT_KNN_SEARCH, true, s);
+    a.queue = b.queue;
+    a.queue_n = b.queue_n;
+    a.work = g.counters + kMaxLevels + 4;
+    cudaError_t e = launch_search<K>(a, cap, s);
+    if (e == cudaSuccess) e = launch_epilogue<K>(a, cap, s);
+    if (e != cudaSuccess) return e;
+    note_launch(4);
+    return cudaSuccess;
+}
+
 }  // namespace
 
 // automatic cell sizes (cell0 <= 0): multiples of the estimated point spacing — the C4 setting
 // (3 x spacing) for one level; finer for several levels (the coarser levels cover sparse parts)
-constexpr float kAutoCellMult = 3.0f;
-constexpr float kAutoCellMultiLevel = 2.0f;
+// (the brick kernel wants level-0 cells of ~6 spacings: ~40 queries and ~300 candidates per brick)
+constexpr float kAutoCellMult = 6.0f;
+constexpr float kAutoCellMultiLevel = 6.0f;
 
 size_t covariances_ws_bytes(int cap, int levels) {
-    return grid_bytes(cap, levels, false) + align_up((size_t)cap * kMaxK * sizeof(int32_t));
+    return grid_bytes(cap, levels, false) + align_up((size_t)cap * kMaxK * sizeof(int32_t)) +
+           align_up((size_t)cap * sizeof(uint4)) + align_up((size_t)cap * sizeof(uint32_t));
 }
 
 cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, int k, int mode, float eps,
@@ -1362,16 +1666,24 @@ cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, in
     a.knn_idx = knn_idx;
     a.sort_out = knn_idx != nullptr;
     a.debug = reinterpret_cast<int4 *>(g_knn_debug);
-    a.nbr_t = reinterpret_cast<int32_t *>(static_cast<char *>(ws) + grid_bytes(cap, levels, false));
+    char *wp = static_cast<char *>(ws) + grid_bytes(cap, levels, false);
+    a.nbr_t = reinterpret_cast<int32_t *>(wp);
+    wp += align_up((size_t)cap * kMaxK * sizeof(int32_t));
+    BrickArgs b{};
+    b.bricks = reinterpret_cast<const uint4 *>(wp);
+    wp += align_up((size_t)cap * sizeof(uint4));
+    b.queue = reinterpret_cast<uint32_t *>(wp);
+    b.n_bricks = a.g.counters + kMaxLevels + 2;  // zeroed by the grid build
+    b.queue_n = a.g.counters + kMaxLevels + 3;
     a.work = a.g.counters + kMaxLevels;
     cudaError_t e = grid_build(a.g, a.pos, nullptr, nullptr, d_n, cap, s);
     if (e != cudaSuccess) return e;
-    if (k <= 4) return launch_k<4>(a, cap, s);
-    if (k <= 8) return launch_k<8>(a, cap, s);
-    if (k <= 16) return launch_k<16>(a, cap, s);
-    if (k <= 20) return launch_k<20>(a, cap, s);
-    if (k <= 24) return launch_k<24>(a, cap, s);
-    return launch_k<32>(a, cap, s);
+    if (k <= 4) return launch_brick<4>(a, b, cap, s);
+    if (k <= 8) return launch_brick<8>(a, b, cap, s);
+    if (k <= 16) return launch_brick<16>(a, b, cap, s);
+    if (k <= 20) return launch_brick<20>(a, b, cap, s);
+    if (k <= 24) return launch_brick<24>(a, b, cap, s);
+    return launch_brick<32>(a, b, cap, s);
 }
 
 // Exact kGraphK-NN lists (input indices, sorted by (key, index), self included) of the points of

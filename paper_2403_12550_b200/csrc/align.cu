@@ -69,6 +69,7 @@ struct AlignArgs {
     double *partials;         // [2][grid][kPad]
     unsigned int *barrier;
     int32_t *corr_ws;         // [cap] previous match (cell-ordered slot), -2-slot if gated out, -1 none
+    float4 *reuse_ws;         // [cap] non-resident points' reuse state: (query of the last search, d2lb)
     int32_t *corr_out;        // nullable [cap] original target index or -1
     long long *timeline;      // diagnostic (nullable): [0] start, then per iteration G arrivals + pass
     long long timeline_cap;
@@ -187,6 +188,10 @@ constexpr float kReuseMargin = 1e-5f;  // relative slack on every distance of th
 #define GSICP_D2_FROM_ITER 2
 #endif
 constexpr int kD2FromIter = GSICP_D2_FROM_ITER;
+// ... and only for queries within this many cells of their match: farther off the surface (noisy
+// depth) the second neighbour is nearly as close as the first, the reuse margin d2 - d1 vanishes
+// and the second search would be wasted
+constexpr float kD2MaxD1 = 0.8f;
 
 // On a certified step the list also bounds the SECOND nearest target: list members have their
 // exact distances, every other target k has |q - m_k| >= |m_j - m_k| - |q - m_j| >=
@@ -851,11 +856,14 @@ __global__ void __launch_bounds__(kSeedHardT) k_align_seed_hard(AlignArgs a) {
     }
 }
 
-__global__ void k_align_init(int32_t *corr_ws, int cap, unsigned int *barrier) {
+__global__ void k_align_init(int32_t *corr_ws, float4 *reuse_ws, int cap, unsigned int *barrier) {
     pdl_wait();
     pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < cap) corr_ws[i] = -1;
+    if (i < cap) {
+        corr_ws[i] = -1;
+        reuse_ws[i] = make_float4(0.f, 0.f, 0.f, 0.f);  // d2lb = 0: no reuse
+    }
     if (i == 0) *barrier = 0u;
 }
 
@@ -1001,6 +1009,8 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
             }
             // after iteration 0 a point the graph cannot certify goes straight to the block queue:
             // the warp path also bounds its second neighbour, so the next iterations can reuse
+            // (measured: the per-thread cell path here instead is slower, 227 -> 267 us, because
+            // the points then lose the second-neighbour bound and fail the reuse test later)
             if (!exact && (it == 0 || !a.nbr)) {
                 exact = nn_search(a, sIdx, sBox, qc, own_left, q, nn, true);
                 path_code = exact ? 2 : 3;
@@ -1103,19 +1113,30 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
                     nn.set(q.key(rec), slot, rec);
                 }
                 bool exact = seeded;
-                const uint2 own = sIdx.one(qc.c[0], qc.c[1], qc.c[2]);
+                // the motion-bounded reuse of the resident path, with its state kept in memory
+                const float4 ru = seeded ? make_float4(0.f, 0.f, 0.f, 0.f) : a.reuse_ws[i];
+                float d2lb = ru.w;
+                if (!exact && d2lb > 0.f) {
+                    const float ex = q.x - ru.x, ey = q.y - ru.y, ez = q.z - ru.z;
+                    const float delta = sqrtf(ex * ex + ey * ey + ez * ez) * (1.f + kReuseMargin) + 2.f * q.E();
+                    const float d1 = nn.slot >= 0 ? fminf(sqrtf(__double2float_ru(nn.bk)), a.r) : a.r;
+                    if ((d2lb - delta) * (1.f - kReuseMargin) > d1 * (1.f + kReuseMargin)) {
+                        exact = true;
+                        d2lb -= delta;
+                    }
+                }
+                if (!exact) d2lb = 0.f;
+                const uint2 own = exact ? make_uint2(0u, 0u) : sIdx.one(qc.c[0], qc.c[1], qc.c[2]);
                 uint2 own_left = own;
                 if (!exact && a.nbr && (nn.slot < 0 || nn.bk > 0.25 * (double)a.h * (double)a.h)) {
                     scan_target_cell(a, own, q, nn);  // (as the resident path: a far or absent warm start)
                     own_left = make_uint2(0u, 0u);
                 }
-                if (!exact && nn.slot >= 0 && a.nbr) {
-                    float d2 = 0.f;
-                    exact = graph_nn(a, q, nn, d2);
-                }
+                if (!exact && nn.slot >= 0 && a.nbr) exact = graph_nn(a, q, nn, d2lb);
                 if (!exact && !a.nbr) exact = nn_search(a, sIdx, sBox, qc, own_left, q, nn, true);
                 if (exact) {
                     a.corr_ws[i] = (nn.slot >= 0 && nn.bk < a.r2) ? nn.slot : -2 - nn.slot;
+                    a.reuse_ws[i] = make_float4(q.x, q.y, q.z, seeded ? 0.f : d2lb);
                 } else {
                     const int k = atomicAdd(&sQn2, 1);
                     sQtid[k] = i;
@@ -1133,7 +1154,20 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
                 nn.slot = sQslot[k];
                 if (nn.slot >= 0) nn.set(sQbk[k], nn.slot, sQp[k]);
                 warp_nn(a, sIdx, sBox, q, nn, lane);
-                if (lane == 0) a.corr_ws[sQtid[k]] = (nn.slot >= 0 && nn.bk < a.r2) ? nn.slot : -2 - nn.slot;
+                // the second-neighbour bound for the reuse of the next iterations (as resident points)
+                const bool in_r = nn.slot >= 0 && nn.bk < a.r2;
+                const float base = in_r ? sqrtf(__double2float_ru(nn.bk)) : a.r;
+                float d2 = 0.f;
+                if (base < INFINITY && it >= kD2FromIter) {
+                    const float rho = base * 1.25f + 0.25f * a.h;
+                    NN n2;
+                    warp_nn(a, sIdx, sBox, q, n2, lane, rho * rho, nn.slot);
+                    d2 = fminf(n2.slot >= 0 ? sqrtf(__double2float_rd(n2.bk)) : INFINITY, rho) * (1.f - kReuseMargin);
+                }
+                if (lane == 0) {
+                    a.corr_ws[sQtid[k]] = in_r ? nn.slot : -2 - nn.slot;
+                    a.reuse_ws[sQtid[k]] = make_float4(q.x, q.y, q.z, d2);
+                }
             }
             __syncthreads();  // the queue entries are read before the next round refills them
         }
@@ -1302,7 +1336,10 @@ __global__ void k_align_init_batch(const __grid_constant__ AlignBatch b) {
     pdl_wait();
     pdl_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < a.cap) a.corr_ws[i] = -1;
+    if (i < a.cap) {
+        a.corr_ws[i] = -1;
+        a.reuse_ws[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     if (i == 0) *a.barrier = 0u;
 }
 
@@ -1336,6 +1373,7 @@ struct AlignWs {
     unsigned int *barrier;
     double *partials;
     int32_t *corr_ws;
+    float4 *reuse_ws;
     int32_t *seed_slot;
     double *seed_hdr;
     int32_t *seed_queue;
@@ -1351,6 +1389,7 @@ static AlignWs align_carve(Carver &c, int cap) {
     (void)cap;
     w.partials = c.take<double>((size_t)2 * kMaxAlignGrid * kPad);  // the grid is the co-resident one
     w.corr_ws = c.take<int32_t>(cap);
+    w.reuse_ws = c.take<float4>(cap);
     w.seed_slot = c.take<int32_t>(cap);
     w.seed_hdr = c.take<double>(16);
     w.seed_queue = c.take<int32_t>(cap);
@@ -1411,6 +1450,7 @@ static AlignArgs make_args(const gsicp_cloud &src, const gsicp_target &tgt, doub
     a.partials = w.partials;
     a.barrier = w.barrier;
     a.corr_ws = w.corr_ws;
+    a.reuse_ws = w.reuse_ws;
     a.corr_out = corr_out;
     a.timeline = g_align_timeline;
     a.timeline_cap = g_align_timeline_cap;
@@ -1493,7 +1533,7 @@ cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double
     AlignWs w = align_carve(ws, src.cap);
     AlignArgs a = make_args(src, tgt, d_T_inout, p, d_stats, corr_out, linearize_only, r_lin, w);
     a.seed_ticket = seed_take(ws, src.pos, tgt.pos);
-    launch_pdl(k_align_init, dim3(blocks_for(src.cap > 0 ? src.cap : 1, 256)), dim3(256), 0, s, w.corr_ws, src.cap,
+    launch_pdl(k_align_init, dim3(blocks_for(src.cap > 0 ? src.cap : 1, 256)), dim3(256), 0, s, w.corr_ws, w.reuse_ws, src.cap,
                w.barrier);
     GSICP_LAUNCH_CHECK("k_align_init");
     int per_sm = 0;

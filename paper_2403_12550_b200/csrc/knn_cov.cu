@@ -1164,22 +1164,85 @@ __global__ void k_img_hash_n(ImgArgs im, const int32_t *__restrict__ d_n, cudaGr
 
 // ---------------------------------------------------------------------------------------------
 // Brick kNN for general clouds (maps, voxel clouds; A3+A4 of gsicp_covariances): the grid's
-// level-0 cells are "bricks" of edge H.  A warp takes one occupied brick: it stages every point
-// of the brick's 27-brick neighbourhood that lies in the brick's box expanded by R = 0.6 H into
-// shared memory, then runs the brick's points as queries, one per lane, over the staged
-// candidates (all lanes read the same candidate: shared-memory broadcast, no divergence) with
-// the image kernel's exact two-pass selection: a per-lane histogram of quarter-octave key
-// buckets gives the boundary bucket b*, a second pass collects the <= 32 candidates at or below
-// it, and the boundary is resolved exactly in binary64.  The result is exact when
-// the k-th ball lies inside the expanded box (every point within it was staged); the rest (and
-// bricks whose neighbourhood overflows the staging buffer) go to a queue that the warp search
-// finishes.  Candidates per query ~ (H + 2R)^2 / l^2 on a surface sampled at spacing l — with
-// H ~ 6 l about 300, against the warp search's list maintenance per candidate.
+// level-0 cells are "bricks" of edge H (~3.7 point spacings).  A brick's candidates are the
+// points of its 27-brick neighbourhood inside the brick's box expanded by R = 0.95 H; the result
+// is exact when the query's k-th ball lies inside that box (every point within it was staged).
+// A warp takes a contiguous range of the brick list and stages bricks back to back in shared memory
+// while their queries fit one 32-lane round (bricks hold ~10 points; a group of ~3 fills the warp), then
+// runs the round: a lane per query, each scanning its own brick's candidates (a few distinct
+// shared-memory addresses per load), with ONE pass of selection (each key computed once).  The
+// screen key here is key32 with its 9 low mantissa bits cleared (key32t: within 2^-14 below key32,
+// so |key32t - key64| <= 6.2e-5 key64 and the band of §7.0 widens to kBrickBand = 2e-4); the 9
+// bits carry the candidate's slot.  A lane appends every candidate with key32t <= its bound tau
+// to a per-lane list (one 32-bit store); when some lane's list nears its capacity the warp
+// compacts — each lane with >= k entries buckets them (1/8-octave buckets below tau or its largest
+// key, byte counters in two registers), takes b*, the bucket holding its k-th entry, lowers tau to
+// band_hi(upper edge of b*) and drops the entries above it.  tau never falls below band_hi(k-th
+// key32t of all its candidates), so at the end the list holds every candidate the exact selection
+// needs: the k-th key32t t, the entries below band_lo(t), and the band resolved in binary64.
+// Queries that fail the certificate (and bricks whose neighbourhood overflows the staging buffer)
+// go to a queue that the warp search finishes.
 constexpr int kBrickWarps = 4;
-constexpr int kBrickCap = 352;  // staged candidates per warp (4 blocks / SM in shared memory)
-constexpr float kBrickHalo = 0.6f;
-// per warp: staged candidates, histogram columns, list keys, list slots, the 27-brick cell table
-constexpr int kBrickSmemPerWarp = kBrickCap * 16 + 16 * 32 * 4 + 32 * 32 * 4 + 32 * 32 * 2 + 32 * 8;
+constexpr int kBrickCap = 448;     // staged candidates per warp (a group of bricks, + a sentinel each)
+constexpr float kBrickHalo = 0.95f;  // R / H (< 1: the box stays inside the 27 bricks with margin)
+constexpr int kBrickL = 48;        // per-lane list capacity
+constexpr int kBrickLx = 32;       // list entries of the final selection (a 32-bit mask)
+constexpr int kBrickU = 4;         // candidates between two capacity checks (the list keeps U free)
+constexpr uint32_t kBrickSlotMask = 0x1FFu;  // staged-candidate slot in the low bits of a list entry
+static_assert(kBrickCap < (int)kBrickSlotMask, "slot field");
+// per warp: staged candidates, packed list, 27-brick cell table (13.6 KB: 4 blocks / SM)
+constexpr int kBrickSmemPerWarp = kBrickCap * 16 + kBrickL * 32 * 4 + 32 * 8;
+constexpr int kBrickBlocksPerSm = 4;
+constexpr uint32_t kBrickKeyMask = ~kBrickSlotMask;
+constexpr float kBrickBand = 2e-4f;  // > 3 x (11 u + 2^-14)
+__device__ __forceinline__ float brick_band_hi(float t) { return __fadd_ru(__fmul_ru(t, 1.f + kBrickBand), 1e-36f); }
+__device__ __forceinline__ float brick_band_lo(float t) { return __fsub_rd(__fmul_rd(t, 1.f - kBrickBand), 1e-36f); }
+// the 27 bricks around a brick, nearest first (own, 6 faces, 12 edges, 8 corners): early
+// candidates are close, so the bounds tighten sooner
+__constant__ int8_t c_brick_nb[27][3] = {
+    {0, 0, 0}, {-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1},
+    {-1, -1, 0}, {-1, 1, 0}, {1, -1, 0}, {1, 1, 0}, {-1, 0, -1}, {-1, 0, 1}, {1, 0, -1}, {1, 0, 1},
+    {0, -1, -1}, {0, -1, 1}, {0, 1, -1}, {0, 1, 1},
+    {-1, -1, -1}, {-1, -1, 1}, {-1, 1, -1}, {-1, 1, 1}, {1, -1, -1}, {1, -1, 1}, {1, 1, -1}, {1, 1, 1}};
+
+// The brick kernel's screen key: the binary32 squared distance with fused multiply-adds.  Every
+// operand is positive, so its relative error is <= 5u like canon_key's (DESIGN §7.0's band bound
+// holds); it is used consistently inside the kernel (scan and final ranking).
+__device__ __forceinline__ float brick_key(float ax, float ay, float az, float bx, float by, float bz) {
+    const float dx = ax - bx, dy = ay - by, dz = az - bz;
+    return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+}
+// 16 byte counters in two registers (buckets 0-7, 8-15): add one to bucket b
+struct Hist16 {
+    unsigned long long lo = 0ull, hi = 0ull;
+    __device__ __forceinline__ void add(int b) {
+        const unsigned long long one = 1ull << (8 * (b & 7));
+        if (b < 8) lo += one; else hi += one;
+    }
+    // first bucket whose cumulative count reaches k (16 if none); *below = the count before it
+    __device__ __forceinline__ int select(int k, int &below) const {
+        constexpr unsigned long long C = 0x0101010101010101ull;  // byte prefix sums (< 256: no carries)
+        const unsigned long long pl = lo * C;
+        const unsigned long long ph = hi * C + (pl >> 56) * C;
+        const uint32_t w0 = (uint32_t)pl, w1 = (uint32_t)(pl >> 32), w2 = (uint32_t)ph, w3 = (uint32_t)(ph >> 32);
+        const uint32_t kk = (uint32_t)k * 0x01010101u;
+        const int ge = __popc(__vcmpgeu4(w0, kk)) + __popc(__vcmpgeu4(w1, kk)) + __popc(__vcmpgeu4(w2, kk)) +
+                       __popc(__vcmpgeu4(w3, kk));
+        const int bs = 16 - ge / 8;  // prefix sums are monotone: the bytes >= k are a suffix
+        const int bb = bs - 1;
+        const uint32_t wd = bb < 4 ? w0 : (bb < 8 ? w1 : (bb < 12 ? w2 : w3));
+        below = bs == 0 ? 0 : (int)((wd >> (8 * (bb & 3))) & 0xFFu);
+        return bs;
+    }
+};
+// 1/8-octave bucket of key bits kb in the 16 buckets whose top (15) holds the key bits tb
+__device__ __forceinline__ int bucket16(uint32_t kb, uint32_t tb) {
+    return min(max((int)(kb >> 20) - (int)(tb >> 20) + 15, 0), 15);
+}
+// smallest key bits above bucket b of that scale
+__device__ __forceinline__ uint32_t bucket16_edge(int b, uint32_t tb) {
+    return (uint32_t)max((int)(tb >> 20) - 15 + b + 1, 1) << 20;
+}
 
 struct BrickArgs {
     const uint4 *bricks;     // (start, count, key lo, key hi) of the occupied level-0 cells
@@ -1208,6 +1271,7 @@ __global__ void k_brick_list(GridView g, uint4 *bricks, uint32_t *n_bricks) {
 
 template <int K, bool SORT>
 __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, BrickArgs b) {
+    static_assert(K + kBrickU < kBrickLx, "list capacity");
     pdl_wait();
     pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char brick_smem[];  // kBrickSmemPerWarp per warp
@@ -1215,173 +1279,234 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     unsigned char *wsm = brick_smem + (size_t)wid * kBrickSmemPerWarp;
     float4 *cand = reinterpret_cast<float4 *>(wsm);
-    uint32_t(*hist)[32] = reinterpret_cast<uint32_t(*)[32]>(wsm + kBrickCap * 16);
-    float(*lkey)[32] = reinterpret_cast<float(*)[32]>(wsm + kBrickCap * 16 + kImgBuckets / 2 * 32 * 4);
-    uint16_t(*lst)[32] = reinterpret_cast<uint16_t(*)[32]>(wsm + kBrickCap * 16 + kImgBuckets / 2 * 32 * 4 +
-                                                           kImgList * 32 * 4);
-    uint2 *scell = reinterpret_cast<uint2 *>(wsm + kBrickCap * 16 + kImgBuckets / 2 * 32 * 4 + kImgList * 32 * 4 +
-                                             kImgList * 32 * 2);
+    uint32_t(*lpk)[32] = reinterpret_cast<uint32_t(*)[32]>(wsm + kBrickCap * 16);
+    uint2 *scell = reinterpret_cast<uint2 *>(wsm + kBrickCap * 16 + kBrickL * 32 * 4);
     const int k = a.k, n = *a.d_n;
     const uint32_t nb = *b.n_bricks;
     const float H = g.h0, R = kBrickHalo * g.h0;
-    for (uint32_t w = blockIdx.x * kBrickWarps + wid; w < nb; w += gridDim.x * kBrickWarps) {
-        const uint4 be = __ldg(b.bricks + w);
-        const uint32_t start = be.x, cnt = be.y;
-        const unsigned long long key = ((unsigned long long)be.w << 32) | be.z;
-        const int c[3] = {(int)((key >> 40) & 0xFFFFFull) - kCoordOff, (int)((key >> 20) & 0xFFFFFull) - kCoordOff,
-                          (int)(key & 0xFFFFFull) - kCoordOff};
-        float elo[3], ehi[3];
+    const float4 kSentinel = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);  // NaN: never listed
+    // a contiguous range of the brick list per warp (no work counter: a fetch would be one more
+    // dependent round trip per brick); the next record and the first probe of the next brick's 27
+    // neighbour cells are issued ahead, so their latency overlaps the staging / the round
+    const uint32_t W = gridDim.x * kBrickWarps, wg = blockIdx.x * kBrickWarps + wid;
+    const uint32_t p1 = (uint32_t)((unsigned long long)nb * (wg + 1) / W);
+    uint32_t p = (uint32_t)((unsigned long long)nb * wg / W);
+    const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
+    uint4 rec = p < p1 ? __ldg(b.bricks + p) : zero4;
+    uint4 recn = p + 1 < p1 ? __ldg(b.bricks + p + 1) : zero4;
+    auto nb_key = [&](const uint4 &r) {  // this lane's neighbour cell of brick r (own cell: lane 0)
+        const unsigned long long key = ((unsigned long long)r.w << 32) | r.z;
+        const int l = lane < 27 ? lane : 0;
+        const int dx = c_brick_nb[l][0], dy = c_brick_nb[l][1], dz = c_brick_nb[l][2];
+        return cell_key(0, (int)((key >> 40) & 0xFFFFFull) - kCoordOff + dx, (int)((key >> 20) & 0xFFFFFull) - kCoordOff + dy,
+                        (int)(key & 0xFFFFFull) - kCoordOff + dz);
+    };
+    auto probe_first = [&](const uint4 &r) {
+        return lane < 27 ? __ldg(reinterpret_cast<const uint4 *>(g.table + hash_slot(nb_key(r), g.mask))) : zero4;
+    };
+    auto probe_finish = [&](const uint4 &e, const uint4 &r) {  // (start, count) of the lane's cell
+        if (lane >= 27) return make_uint2(0u, 0u);
+        const unsigned long long want = nb_key(r);
+        const unsigned long long k0 = ((unsigned long long)e.y << 32) | e.x;
+        if (k0 == want) return make_uint2(e.z, e.w);
+        if (k0 == kEmptyKey) return make_uint2(0u, 0u);
+        return cell_lookup(g.table, g.mask, want);  // (collision: probe on; the scan restarts at the home slot)
+    };
+    uint4 probe = p < p1 ? probe_first(rec) : zero4;
+    bool have_se = false;
+    uint2 se = make_uint2(0u, 0u);
+    uint32_t incl = 0u, total = 0u;
+    while (p < p1) {
+        // ---- a group: bricks staged back to back while their queries fit one round.  Lane j
+        // keeps brick j's record: first point, first query lane, candidate offset and count, cell
+        int nbr = 0, gq = 0, gnc = 0;
+        uint32_t qmask = 0u;
+        uint32_t my_start = 0u;
+        int my_qs = 0, my_off = 0, my_nc = 0, my_c0 = 0, my_c1 = 0, my_c2 = 0;
+        while (p < p1) {
+            const int cnt = (int)rec.y;
+            if (nbr > 0 && gq + cnt > 32) break;  // (the probe of this brick stays in flight over the round)
+            if (!have_se) {
+                // the 27 bricks (own first): (start, count) one per lane, their prefix and total
+                se = probe_finish(probe, rec);
+                incl = se.y;
 #pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-            elo[ax] = (float)c[ax] * H - R;
-            ehi[ax] = (float)(c[ax] + 1) * H + R;
-        }
-        // ---- stage the expanded box's points (27 bricks probed one per lane, then scanned as one
-        // flattened range, 32 records per round)
-        int dx = 0, dy = 0, dz = 0;
-        if (lane > 0 && lane < 27) shell_cell(1, lane - 1, dx, dy, dz);
-        const uint2 se = lane < 27 ? cell_lookup(g.table, g.mask, cell_key(0, c[0] + dx, c[1] + dy, c[2] + dz))
-                                   : make_uint2(0u, 0u);
-        uint32_t incl = se.y;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t total = __shfl_sync(kFull, incl, 31);
-        const uint32_t excl = incl - se.y;
-        const unsigned ne = __ballot_sync(kFull, se.y != 0u);
-        if (se.y) scell[__popc(ne & ((1u << lane) - 1u))] = make_uint2(se.x, excl);
-        __syncwarp();
-        int nc = 0, before = 0;
-        for (uint32_t rb = 0; rb < total; rb += 32) {
-            const bool here = se.y != 0u && excl >= rb && excl < rb + 32u;
-            const unsigned P = __reduce_or_sync(kFull, here ? 1u << (excl - rb) : 0u);
-            const uint32_t item = rb + lane;
-            bool in = false;
-            float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (item < total) {
-                const uint2 ce = scell[before + __popc(P & (0xffffffffu >> (31 - lane))) - 1];
-                p = __ldg(g.spos + ce.x + (item - ce.y));
-                in = p.x >= elo[0] && p.x <= ehi[0] && p.y >= elo[1] && p.y <= ehi[1] && p.z >= elo[2] && p.z <= ehi[2];
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                total = __shfl_sync(kFull, incl, 31);
+                have_se = true;
             }
-            before += __popc(P);
-            const unsigned bi = __ballot_sync(kFull, in);
-            const int slot = nc + __popc(bi & ((1u << lane) - 1u));
-            if (in && slot < kBrickCap) cand[slot] = p;
-            nc += __popc(bi);
+            if (nbr > 0 && gnc + (int)total + 1 > kBrickCap) break;  // (total bounds the staged count)
+            have_se = false;
+            const unsigned long long key = ((unsigned long long)rec.w << 32) | rec.z;
+            const int c0 = (int)((key >> 40) & 0xFFFFFull) - kCoordOff, c1 = (int)((key >> 20) & 0xFFFFFull) - kCoordOff,
+                      c2 = (int)(key & 0xFFFFFull) - kCoordOff;
+            const uint32_t excl = incl - se.y;
+            const unsigned ne = __ballot_sync(kFull, se.y != 0u);
+            __syncwarp();
+            if (se.y) scell[__popc(ne & ((1u << lane) - 1u))] = make_uint2(se.x, excl);
+            __syncwarp();
+            const float elo0 = (float)c0 * H - R, elo1 = (float)c1 * H - R, elo2 = (float)c2 * H - R;
+            const float ehi0 = (float)(c0 + 1) * H + R, ehi1 = (float)(c1 + 1) * H + R, ehi2 = (float)(c2 + 1) * H + R;
+            // records of the 27 cells scanned as one flattened range, 4 x 32 loads in flight at once
+            constexpr int kStageB = 4;
+            int nc = 0, before = 0;
+            for (uint32_t rb0 = 0; rb0 < total; rb0 += 32 * kStageB) {
+                float4 pv[kStageB];
+#pragma unroll
+                for (int u = 0; u < kStageB; ++u) {
+                    const uint32_t rb = rb0 + 32u * u;
+                    const bool here = se.y != 0u && excl >= rb && excl < rb + 32u;
+                    const unsigned P = __reduce_or_sync(kFull, here ? 1u << (excl - rb) : 0u);
+                    const uint32_t item = rb + lane;
+                    pv[u] = kSentinel;
+                    if (item < total) {
+                        const uint2 ce = scell[before + __popc(P & (0xffffffffu >> (31 - lane))) - 1];
+                        pv[u] = __ldg(g.spos + ce.x + (item - ce.y));
+                    }
+                    before += __popc(P);
+                }
+#pragma unroll
+                for (int u = 0; u < kStageB; ++u) {
+                    const float4 pp = pv[u];
+                    const bool in = pp.x >= elo0 && pp.x <= ehi0 && pp.y >= elo1 && pp.y <= ehi1 && pp.z >= elo2 && pp.z <= ehi2;
+                    const unsigned bi = __ballot_sync(kFull, in);
+                    const int slot = gnc + nc + __popc(bi & ((1u << lane) - 1u));
+                    if (in && slot < kBrickCap) cand[slot] = pp;
+                    nc += __popc(bi);
+                }
+            }
+            const bool over = gnc + nc + 1 > kBrickCap;  // (only a brick staged alone can overflow)
+            if (!over && lane == 0) cand[gnc + nc] = kSentinel;
+            if (lane == nbr) {
+                my_start = rec.x;
+                my_qs = gq;
+                my_off = over ? -1 : gnc;
+                my_nc = nc;
+                my_c0 = c0;
+                my_c1 = c1;
+                my_c2 = c2;
+            }
+            if (gq < 32) qmask |= 1u << gq;
+            gq += cnt;
+            gnc += over ? 0 : nc + 1;
+            ++nbr;
+            // advance: the next record is in registers, the one after it and the next probe go out now
+            ++p;
+            rec = recn;
+            recn = p + 1 < p1 ? __ldg(b.bricks + p + 1) : zero4;
+            probe = p < p1 ? probe_first(rec) : zero4;
+            if (cnt > 32 || over) break;  // a big brick runs alone (several rounds)
         }
         __syncwarp();
-        const bool over = nc > kBrickCap;
-        // ---- the brick's points as queries, 32 per round
-        // bucket kImgBucketRef <-> (2 l)^2 with l^2 ~ 1.5 H^2 / cnt (a surface through the brick)
-        const float sp2 = 6.f * H * H / (float)max(cnt, 1u);
-        const int base = (int)(__float_as_uint(fmaxf(sp2, 1e-30f)) >> 21) - kImgBucketRef;
-        for (uint32_t qb = 0; qb < cnt; qb += 32) {
-            const bool has = qb + lane < cnt;
-            const float4 q = has ? __ldg(g.spos + start + qb + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+        // ---- the group's queries, one per lane (several rounds only for a lone big brick)
+        for (int r0 = 0; r0 < gq; r0 += 32) {
+            const int L = r0 + lane;
+            const bool has = L < gq;
+            const int bb = __popc(qmask & (0xffffffffu >> (31 - lane))) - 1;  // (lone brick: 0)
+            const uint32_t start = __shfl_sync(kFull, my_start, bb);
+            const int qs = __shfl_sync(kFull, my_qs, bb), off = __shfl_sync(kFull, my_off, bb),
+                      bnc = __shfl_sync(kFull, my_nc, bb);
+            const int c0 = __shfl_sync(kFull, my_c0, bb), c1 = __shfl_sync(kFull, my_c1, bb),
+                      c2 = __shfl_sync(kFull, my_c2, bb);
+            const float4 q = has ? __ldg(g.spos + start + (L - qs)) : make_float4(0.f, 0.f, 0.f, 0.f);
             const int i = __float_as_int(q.w);
-            bool ok = has && !over;
-            if (!__any_sync(kFull, ok)) {
-                if (has) b.queue[atomicAdd(b.queue_n, 1u)] = (uint32_t)i;
-                continue;
-            }
-#pragma unroll
-            for (int h = 0; h < kImgBuckets / 2; ++h) hist[h][lane] = 0u;
-            // pass 1: histogram of the candidates' keys (branch-free: a lane without a query fills
-            // its own column, which is never read)
-#pragma unroll 4
-            for (int j = 0; j < nc; ++j) {
-                const float4 P = cand[j];
-                const float kk = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
-                const int bk = min(max((int)(__float_as_uint(kk) >> 21) - base, 0), kImgBuckets - 1);
-                atomicAdd(&hist[bk >> 1][lane], 1u << ((bk & 1) * 16));
-            }
-            int bstar = -1;
-            uint32_t cum = 0, m = 0;
-#pragma unroll
-            for (int h = 0; h < kImgBuckets / 2; ++h) {
-                const uint32_t wd = hist[h][lane];
-#pragma unroll
-                for (int hb = 0; hb < 2; ++hb) {
-                    const uint32_t cc = (wd >> (16 * hb)) & 0xFFFFu;
-                    if (bstar < 0 && cum + cc >= (uint32_t)k) {
-                        bstar = 2 * h + hb;
-                        m = cum + cc;
-                    }
-                    cum += cc;
+            bool ok = has && off >= 0;
+            const int base = ok ? off : 0, nc = ok ? bnc : 0;  // candidates [base, base + nc), sentinel at base + nc
+            const int maxnc = __reduce_max_sync(kFull, (unsigned)nc);
+            // ---- one pass: list every candidate with key <= tau (lanes without a query: none)
+            // tau and the list in the key32t domain (bit patterns: unsigned order == float order)
+            uint32_t tau = ok ? 0x7f800000u : 0u, lmax = 0u;
+            int m = 0, n_events = 0;
+            // compaction of this lane's list: 1/8-octave buckets below tau (or, while tau is open,
+            // below the largest listed key), b* = the bucket of the k-th entry, tau lowered to
+            // band_hi(b*'s upper edge), the entries above it dropped
+            auto compact = [&]() {
+                const uint32_t top = tau < 0x7f800000u ? tau : lmax;
+                Hist16 h;
+                for (int s = 0; s < m; ++s) h.add(bucket16(lpk[s][lane], top));
+                int below;
+                const int bs = h.select(k, below);
+                tau = min(tau, __float_as_uint(brick_band_hi(__uint_as_float(bucket16_edge(bs, top)))) & kBrickKeyMask);
+                int wr = 0;
+                for (int s = 0; s < m; ++s) {
+                    const uint32_t v = lpk[s][lane];
+                    if ((v & kBrickKeyMask) <= tau) lpk[wr++][lane] = v;
                 }
-            }
-            ok = ok && bstar >= 0 && m <= (uint32_t)kImgList;
-            // pass 2: below b*'s lower edge (shrunk by the band) from the bottom of the list, up to
-            // its upper edge (widened by the band) from the top; slots of the staged candidates
-            const float lo_lim = bstar > 0 ? band_lo(__uint_as_float((uint32_t)(base + bstar) << 21)) : -1.f;
-            const float lim = (bstar < 0 || bstar >= kImgBuckets - 1)
-                                  ? INFINITY
-                                  : band_hi(__uint_as_float((uint32_t)(base + bstar + 1) << 21));
-            int nlo = 0, nbd = 0;
-            if (__any_sync(kFull, ok)) {
-#pragma unroll 4
-                for (int j = 0; j < nc; ++j) {
-                    const float4 P = cand[j];
-                    const float kk = canon_key(q.x, q.y, q.z, P.x, P.y, P.z);
-                    const bool take = ok && kk <= lim && kk < INFINITY;
-                    const bool lo = kk < lo_lim;
-                    const int slot = lo ? nlo : kImgList - 1 - nbd;
-                    if (take && nlo + nbd < kImgList) {
-                        lst[slot][lane] = (uint16_t)j;
-                        lkey[slot][lane] = kk;
-                    }
-                    nlo += (take && lo) ? 1 : 0;
-                    nbd += (take && !lo) ? 1 : 0;
-                }
-            }
-            ok = ok && nlo + nbd <= kImgList && nlo < k && nlo + nbd >= k;
-            const double qx = q.x, qy = q.y, qz = q.z;
-            auto key32_of = [&](int s) { return lkey[s][lane]; };
-            auto key64_of = [&](int s, uint32_t &id) {
-                const float4 P = cand[lst[s][lane]];
-                id = (uint32_t)__float_as_int(P.w);
-                return key64(qx, qy, qz, P.x, P.y, P.z);
+                m = wr;
             };
-            auto rank_in = [&](int s, uint32_t mask) {
-                uint32_t ij;
-                const double kj = key64_of(s, ij);
-                int rank = 0;
-                for (uint32_t bl = mask; bl; bl &= bl - 1) {
-                    uint32_t il;
-                    const double kl = key64_of(__ffs(bl) - 1, il);
-                    rank += (kl < kj || (kl == kj && il < ij)) ? 1 : 0;
+            for (int j0 = 0; j0 <= maxnc; j0 += kBrickU) {
+                if (__any_sync(kFull, m > kBrickL - kBrickU)) {
+                    // (whole warp: every lane with >= k entries tightens its bound)
+                    ++n_events;
+                    if (m >= k) compact();
+                    if (m > kBrickL - kBrickU) {  // ties crowd one bucket: give the query to the search
+                        ok = false;
+                        tau = 0u;
+                        m = 0;
+                    }
                 }
-                return rank;
-            };
-            uint32_t sel = 0u;
-            float bhi = 0.f;
+#pragma unroll
+                for (int u = 0; u < kBrickU; ++u) {
+                    const int idx = base + min(j0 + u, nc);
+                    const float4 P = cand[idx];
+                    const uint32_t kt = __float_as_uint(brick_key(q.x, q.y, q.z, P.x, P.y, P.z)) & kBrickKeyMask;
+                    if (kt <= tau && ok) {  // (NaN sentinel: 0x7fc00000 > any finite tau or +inf; no query: tau 0, ok false)
+                        lpk[m][lane] = kt | (uint32_t)idx;
+                        lmax = max(lmax, kt);
+                        ++m;
+                    }
+                }
+            }
+            ok = ok && m >= k;
+            // ---- exact selection: tighten once more, t = the k-th key32t, band resolved in binary64
             if (ok) {
-                // t = the k-th smallest key32 (the (k - nlo)-th of the boundary group by (key32, slot)),
-                // then in below band_lo(t), a tie band around t ranked by (key64, index)
-                const int r = k - nlo;
-                float t = 0.f;
-                for (int s = kImgList - nbd; s < kImgList; ++s) {
-                    const float ks = key32_of(s);
+                compact();
+                ok = m <= kBrickLx;
+            }
+            uint32_t sel = 0u;
+            if (ok) {
+                const double qx = q.x, qy = q.y, qz = q.z;
+                Hist16 h;
+                for (int s = 0; s < m; ++s) h.add(bucket16(lpk[s][lane], tau));
+                int nlo;
+                const int bs = h.select(k, nlo);
+                uint32_t bd = 0u;  // the boundary bucket's entries
+                for (int s = 0; s < m; ++s) bd |= (bucket16(lpk[s][lane], tau) == bs ? 1u : 0u) << s;
+                const int r = k - nlo;  // t: the r-th smallest (key32t, slot) of the boundary bucket
+                uint32_t t = 0u;
+                for (uint32_t f = bd; f; f &= f - 1) {
+                    const uint32_t vs = lpk[__ffs(f) - 1][lane];
                     int rank = 0;
-                    for (int l = kImgList - nbd; l < kImgList; ++l) {
-                        const float kl = key32_of(l);
-                        rank += (kl < ks || (kl == ks && lst[l][lane] < lst[s][lane])) ? 1 : 0;
-                    }
-                    if (rank == r - 1) t = ks;
+                    for (uint32_t f2 = bd; f2; f2 &= f2 - 1) rank += lpk[__ffs(f2) - 1][lane] < vs ? 1 : 0;
+                    if (rank == r - 1) t = vs & kBrickKeyMask;
                 }
-                const float blo = band_lo(t);
-                bhi = band_hi(t);
-                const uint32_t filled =
-                    (nlo >= 32 ? ~0u : ((1u << nlo) - 1u)) | (nbd == 0 ? 0u : ~0u << (kImgList - nbd));
+                const float blo = brick_band_lo(__uint_as_float(t)), bhi = brick_band_hi(__uint_as_float(t));
+                ok = (__float_as_uint(bhi) & kBrickKeyMask) <= tau;  // every candidate up to band_hi(t) is listed
                 uint32_t band = 0u;
-                for (uint32_t f = filled; f; f &= f - 1) {
-                    const int s = __ffs(f) - 1;
-                    const float ks = key32_of(s);
+                for (int s = 0; s < m; ++s) {
+                    const float ks = __uint_as_float(lpk[s][lane] & kBrickKeyMask);
                     sel |= (ks < blo ? 1u : 0u) << s;
                     band |= (ks >= blo && ks <= bhi ? 1u : 0u) << s;
                 }
+                auto key64_of = [&](int s, uint32_t &id) {
+                    const float4 P = cand[lpk[s][lane] & kBrickSlotMask];
+                    id = (uint32_t)__float_as_int(P.w);
+                    return key64(qx, qy, qz, P.x, P.y, P.z);
+                };
+                auto rank_in = [&](int s, uint32_t mask) {
+                    uint32_t ij;
+                    const double kj = key64_of(s, ij);
+                    int rank = 0;
+                    for (uint32_t bl = mask; bl; bl &= bl - 1) {
+                        uint32_t il;
+                        const double kl = key64_of(__ffs(bl) - 1, il);
+                        rank += (kl < kj || (kl == kj && il < ij)) ? 1 : 0;
+                    }
+                    return rank;
+                };
                 const int need = k - __popc(sel);
                 if (__popc(band) == need) {
                     sel |= band;
@@ -1394,42 +1519,43 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
                 // certificate: the k-th ball (binary64 radius with margin) inside the expanded box
                 const double rho = sqrt((double)bhi) * (1.0 + 1e-5) + 1e-9;
                 const double qc[3] = {qx, qy, qz};
+                const int cc[3] = {c0, c1, c2};
 #pragma unroll
                 for (int ax = 0; ax < 3; ++ax) {
                     const double mg = 1e-7 * fabs(qc[ax]);
-                    ok = ok && qc[ax] - rho - mg >= (double)elo[ax] && qc[ax] + rho + mg <= (double)ehi[ax];
+                    const float lo_ = (float)cc[ax] * H - R, hi_ = (float)(cc[ax] + 1) * H + R;
+                    ok = ok && qc[ax] - rho - mg >= (double)lo_ && qc[ax] + rho + mg <= (double)hi_;
                 }
-            }
-            if (ok) {
-                if (a.knn_idx) {
-                    for (uint32_t f = sel; f; f &= f - 1) {
-                        const int s = __ffs(f) - 1;
-                        const int rk = SORT ? rank_in(s, sel) : __popc(sel & ((1u << s) - 1u));
-                        a.knn_idx[(size_t)i * k + rk] = __float_as_int(cand[lst[s][lane]].w);
+                if (ok) {
+                    if (a.knn_idx) {
+                        for (uint32_t f = sel; f; f &= f - 1) {
+                            const int s = __ffs(f) - 1;
+                            const int rk = SORT ? rank_in(s, sel) : __popc(sel & ((1u << s) - 1u));
+                            a.knn_idx[(size_t)i * k + rk] = __float_as_int(cand[lpk[s][lane] & kBrickSlotMask].w);
+                        }
                     }
+                    double s1[3] = {0, 0, 0}, s2[6] = {0, 0, 0, 0, 0, 0};
+                    for (uint32_t f = sel; f; f &= f - 1) {
+                        const float4 P = cand[lpk[__ffs(f) - 1][lane] & kBrickSlotMask];
+                        const double d0 = (double)P.x - qx, d1 = (double)P.y - qy, d2 = (double)P.z - qz;
+                        s1[0] += d0;
+                        s1[1] += d1;
+                        s1[2] += d2;
+                        s2[0] += d0 * d0;
+                        s2[1] += d0 * d1;
+                        s2[2] += d0 * d2;
+                        s2[3] += d1 * d1;
+                        s2[4] += d1 * d2;
+                        s2[5] += d2 * d2;
+                    }
+                    finish_moments(a, n, i, s1, s2, __popc(sel));
+                    if (a.debug) a.debug[i] = make_int4(-7, bnc, m, nbr * 256 + n_events * 65536 + __popc(__ballot_sync(__activemask(), true)));
                 }
-                double s1[3] = {0, 0, 0}, s2[6] = {0, 0, 0, 0, 0, 0};
-                for (uint32_t f = sel; f; f &= f - 1) {
-                    const float4 P = cand[lst[__ffs(f) - 1][lane]];
-                    const double d0 = (double)P.x - qx, d1 = (double)P.y - qy, d2 = (double)P.z - qz;
-                    s1[0] += d0;
-                    s1[1] += d1;
-                    s1[2] += d2;
-                    s2[0] += d0 * d0;
-                    s2[1] += d0 * d1;
-                    s2[2] += d0 * d2;
-                    s2[3] += d1 * d1;
-                    s2[4] += d1 * d2;
-                    s2[5] += d2 * d2;
-                }
-                finish_moments(a, n, i, s1, s2, __popc(sel));
-                if (a.debug) a.debug[i] = make_int4(-7, nc, (int)m, 0);
-            } else if (has) {
-                b.queue[atomicAdd(b.queue_n, 1u)] = (uint32_t)i;
             }
-            __syncwarp();  // the histogram / list columns are reused by the next round
+            if (has && !ok) b.queue[atomicAdd(b.queue_n, 1u)] = (uint32_t)i;
+            __syncwarp();  // the list columns are reused by the next round
         }
-        __syncwarp();  // the staged candidates are reused by the next brick
+        __syncwarp();  // the staged candidates are reused by the next group
     }
 }
 
@@ -1609,7 +1735,7 @@ cudaError_t launch_brick(KnnArgs a, const BrickArgs &b, int cap, cudaStream_t s)
     launch_pdl(k_brick_list, dim3(blocks_for((long long)g.mask + 1, 256)), dim3(256), 0, s, g, const_cast<uint4 *>(b.bricks),
                const_cast<uint32_t *>(b.n_bricks));
     GSICP_LAUNCH_CHECK("k_brick_list");
-    const dim3 grid((unsigned)num_sms() * 4);  // one resident wave (4 blocks / SM by shared memory)
+    const dim3 grid((unsigned)num_sms() * kBrickBlocksPerSm);  // one resident wave (by shared memory)
     constexpr int smem = kBrickWarps * kBrickSmemPerWarp;
     static PerDevice<int> attr;  // opt-in dynamic shared memory, once per device
     attr.get([&](int) {
@@ -1634,11 +1760,11 @@ cudaError_t launch_brick(KnnArgs a, const BrickArgs &b, int cap, cudaStream_t s)
 
 }  // namespace
 
-// automatic cell sizes (cell0 <= 0): multiples of the estimated point spacing — the C4 setting
-// (3 x spacing) for one level; finer for several levels (the coarser levels cover sparse parts)
-// (the brick kernel wants level-0 cells of ~6 spacings: ~40 queries and ~300 candidates per brick)
-constexpr float kAutoCellMult = 6.0f;
-constexpr float kAutoCellMultiLevel = 6.0f;
+// automatic cell sizes (cell0 <= 0): multiples of the estimated point spacing (the brick kernel
+// wants level-0 cells of ~3.7 spacings: ~10 queries and ~120 candidates per brick, the k = 20
+// ball inside the brick's box expanded by 0.95 H for > 99.9% of the queries of a surface)
+constexpr float kAutoCellMult = 3.7f;
+constexpr float kAutoCellMultiLevel = 3.7f;
 
 size_t covariances_ws_bytes(int cap, int levels) {
     return grid_bytes(cap, levels, false) + align_up((size_t)cap * kMaxK * sizeof(int32_t)) +
@@ -1683,7 +1809,7 @@ cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, in
     if (k <= 16) return launch_brick<16>(a, b, cap, s);
     if (k <= 20) return launch_brick<20>(a, b, cap, s);
     if (k <= 24) return launch_brick<24>(a, b, cap, s);
-    return launch_brick<32>(a, b, cap, s);
+    return launch_k<32>(a, cap, s);  // (the brick list keeps k + 4 < 32 entries: larger k take the warp search)
 }
 
 // Exact kGraphK-NN lists (input indices, sorted by (key, index), self included) of the points of

@@ -12,7 +12,7 @@ import synth
 
 
 def main():
-    cm = float(sys.argv[1]) if len(sys.argv) > 1 else 6.5
+    cm = float(sys.argv[1]) if len(sys.argv) > 1 else 3.7
     lv = int(sys.argv[2]) if len(sys.argv) > 2 else 2
     scene = synth.make_scene(1004)
     means, _, _, ell = synth.sample_map(scene, 4_000_000, 4004)
@@ -28,6 +28,8 @@ def main():
     print(f"cell {cm} ell levels {lv}: brick-finished {brick.mean():.4f}, fallback {1 - brick.mean():.4f}; "
           f"staged candidates per query (brick) mean {d[brick, 1].mean():.0f} max {d[brick, 1].max()}, "
           f"m mean {d[brick, 2].mean():.1f}")
+    w = d[brick, 3]
+    print(f"  lanes/round mean {(w & 255).mean():.1f}  bricks/group mean {((w >> 8) & 255).mean():.2f}  events/round mean {(w >> 16).mean():.2f}")
     fb = ~brick
     if fb.any():
         print(f"  fallback: level mean {d[fb, 0].mean():.2f}, probes mean {d[fb, 1].mean():.0f}, cands mean {d[fb, 2].mean():.0f}")

@@ -32,7 +32,7 @@ METRIC = "G-ICP aligns/sec (Replica frame vs 1M-Gaussian map); kNN-cov Mpts/s; H
 WORKLOAD = "Replica-shaped 1200x680 depth frame, stride 4 (<=51k pts), vs 1e6-Gaussian map (C2 geometry, 1M map)"
 ALGO_BYTES_ALIGN = 96 + 8   # per (source point x GN iteration): src pos+cov, tgt pos+cov, corr
 ALGO_BYTES_KNN = 16 + 32    # per query of the kNN-cov stage: pos in, cov out
-C4_CELL, C4_LEVELS = 3.7, 2  # map kNN-cov grid: bricks of 3.7 map spacings, a coarser level for the outliers
+C4_CELL, C4_LEVELS = 3.4, 3  # map kNN-cov grid: bricks of 3.4 map spacings, two coarser levels for the floating outliers
 
 
 def peaks():

@@ -1175,8 +1175,8 @@ __global__ void k_img_hash_n(ImgArgs im, const int32_t *__restrict__ d_n, cudaGr
 // so |key32t - key64| <= 6.2e-5 key64 and the band of §7.0 widens to kBrickBand = 2e-4); the 9
 // bits carry the candidate's slot.  A lane appends every candidate with key32t <= its bound tau
 // to a per-lane list (one 32-bit store); when some lane's list nears its capacity the warp
-// compacts — each lane with >= k entries buckets them (1/8-octave buckets below tau or its largest
-// key, byte counters in two registers), takes b*, the bucket holding its k-th entry, lowers tau to
+// compacts — each lane with >= k entries buckets them (quarter-octave buckets below tau or its
+// largest key, byte counters in one register), takes b*, the bucket holding its k-th entry, lowers tau to
 // band_hi(upper edge of b*) and drops the entries above it.  tau never falls below band_hi(k-th
 // key32t of all its candidates), so at the end the list holds every candidate the exact selection
 // needs: the k-th key32t t, the entries below band_lo(t), and the band resolved in binary64.
@@ -1235,6 +1235,22 @@ struct Hist16 {
         return bs;
     }
 };
+// 8 byte counters in one register (the list compaction: quarter-octave buckets, 2 octaves)
+struct Hist8 {
+    unsigned long long c = 0ull;
+    __device__ __forceinline__ void add(int b) { c += 1ull << (8 * b); }
+    __device__ __forceinline__ int select(int k) const {
+        const unsigned long long p = c * 0x0101010101010101ull;
+        const uint32_t kk = (uint32_t)k * 0x01010101u;
+        return 8 - (__popc(__vcmpgeu4((uint32_t)p, kk)) + __popc(__vcmpgeu4((uint32_t)(p >> 32), kk))) / 8;
+    }
+};
+__device__ __forceinline__ int bucket8(uint32_t kb, uint32_t tb) {
+    return min(max((int)(kb >> 21) - (int)(tb >> 21) + 7, 0), 7);
+}
+__device__ __forceinline__ uint32_t bucket8_edge(int b, uint32_t tb) {
+    return (uint32_t)max((int)(tb >> 21) - 7 + b + 1, 1) << 21;
+}
 // 1/8-octave bucket of key bits kb in the 16 buckets whose top (15) holds the key bits tb
 __device__ __forceinline__ int bucket16(uint32_t kb, uint32_t tb) {
     return min(max((int)(kb >> 20) - (int)(tb >> 20) + 15, 0), 15);
@@ -1420,16 +1436,15 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
             // tau and the list in the key32t domain (bit patterns: unsigned order == float order)
             uint32_t tau = ok ? 0x7f800000u : 0u, lmax = 0u;
             int m = 0, n_events = 0;
-            // compaction of this lane's list: 1/8-octave buckets below tau (or, while tau is open,
+            // compaction of this lane's list: quarter-octave buckets below tau (or, while tau is open,
             // below the largest listed key), b* = the bucket of the k-th entry, tau lowered to
             // band_hi(b*'s upper edge), the entries above it dropped
             auto compact = [&]() {
                 const uint32_t top = tau < 0x7f800000u ? tau : lmax;
-                Hist16 h;
-                for (int s = 0; s < m; ++s) h.add(bucket16(lpk[s][lane], top));
-                int below;
-                const int bs = h.select(k, below);
-                tau = min(tau, __float_as_uint(brick_band_hi(__uint_as_float(bucket16_edge(bs, top)))) & kBrickKeyMask);
+                Hist8 h;
+                for (int s = 0; s < m; ++s) h.add(bucket8(lpk[s][lane], top));
+                const int bs = h.select(k);
+                tau = min(tau, __float_as_uint(brick_band_hi(__uint_as_float(bucket8_edge(bs, top)))) & kBrickKeyMask);
                 int wr = 0;
                 for (int s = 0; s < m; ++s) {
                     const uint32_t v = lpk[s][lane];
@@ -1460,11 +1475,13 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
                     }
                 }
             }
+            int why = !has ? 0 : (off < 0 ? 1 : (!ok ? 2 : (m < k ? 3 : 0)));
             ok = ok && m >= k;
             // ---- exact selection: tighten once more, t = the k-th key32t, band resolved in binary64
             if (ok) {
                 compact();
                 ok = m <= kBrickLx;
+                if (!ok) why = 4;
             }
             uint32_t sel = 0u;
             if (ok) {
@@ -1485,6 +1502,7 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
                 }
                 const float blo = brick_band_lo(__uint_as_float(t)), bhi = brick_band_hi(__uint_as_float(t));
                 ok = (__float_as_uint(bhi) & kBrickKeyMask) <= tau;  // every candidate up to band_hi(t) is listed
+                if (!ok) why = 5;
                 uint32_t band = 0u;
                 for (int s = 0; s < m; ++s) {
                     const float ks = __uint_as_float(lpk[s][lane] & kBrickKeyMask);
@@ -1526,6 +1544,7 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
                     const float lo_ = (float)cc[ax] * H - R, hi_ = (float)(cc[ax] + 1) * H + R;
                     ok = ok && qc[ax] - rho - mg >= (double)lo_ && qc[ax] + rho + mg <= (double)hi_;
                 }
+                if (!ok && why == 0) why = 6;
                 if (ok) {
                     if (a.knn_idx) {
                         for (uint32_t f = sel; f; f &= f - 1) {
@@ -1552,7 +1571,10 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
                     if (a.debug) a.debug[i] = make_int4(-7, bnc, m, nbr * 256 + n_events * 65536 + __popc(__ballot_sync(__activemask(), true)));
                 }
             }
-            if (has && !ok) b.queue[atomicAdd(b.queue_n, 1u)] = (uint32_t)i;
+            if (has && !ok) {
+                b.queue[atomicAdd(b.queue_n, 1u)] = (uint32_t)i;
+                if (a.debug) a.debug[i] = make_int4(-8, why, bnc, m);
+            }
             __syncwarp();  // the list columns are reused by the next round
         }
         __syncwarp();  // the staged candidates are reused by the next group
@@ -1763,8 +1785,8 @@ cudaError_t launch_brick(KnnArgs a, const BrickArgs &b, int cap, cudaStream_t s)
 // automatic cell sizes (cell0 <= 0): multiples of the estimated point spacing (the brick kernel
 // wants level-0 cells of ~3.7 spacings: ~10 queries and ~120 candidates per brick, the k = 20
 // ball inside the brick's box expanded by 0.95 H for > 99.9% of the queries of a surface)
-constexpr float kAutoCellMult = 3.7f;
-constexpr float kAutoCellMultiLevel = 3.7f;
+constexpr float kAutoCellMult = 3.5f;
+constexpr float kAutoCellMultiLevel = 3.5f;
 
 size_t covariances_ws_bytes(int cap, int levels) {
     return grid_bytes(cap, levels, false) + align_up((size_t)cap * kMaxK * sizeof(int32_t)) +

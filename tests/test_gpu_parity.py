@@ -283,7 +283,7 @@ def test_knn_cov_degenerate_clouds(g):
             _cov_check(g, xyz, pos, d_n, mode=mode, cell0=0.02, levels=2)
 
 
-@pytest.mark.parametrize("cell,levels,sample", [(2.5, 1, 300), (3.7, 2, 100_000), (6.5, 1, 300)])
+@pytest.mark.parametrize("cell,levels,sample", [(2.5, 1, 300), (3.4, 3, 100_000), (6.5, 1, 300)])
 def test_knn_cov_map_c4_sampled(g, cell, levels, sample):
     """C4-style: kNN covariance of a 4e6-point map (sampled queries vs the oracle's exact kd-tree /
     brute force); levels=1 is the warp search of every point, (3.0, 3) the bench configuration."""

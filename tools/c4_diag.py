@@ -12,8 +12,8 @@ import synth
 
 
 def main():
-    cm = float(sys.argv[1]) if len(sys.argv) > 1 else 3.7
-    lv = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    cm = float(sys.argv[1]) if len(sys.argv) > 1 else 3.4
+    lv = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     scene = synth.make_scene(1004)
     means, _, _, ell = synth.sample_map(scene, 4_000_000, 4004)
     c = g.Cloud.from_points(torch.from_numpy(means).cuda())
@@ -30,6 +30,10 @@ def main():
           f"m mean {d[brick, 2].mean():.1f}")
     w = d[brick, 3]
     print(f"  lanes/round mean {(w & 255).mean():.1f}  bricks/group mean {((w >> 8) & 255).mean():.2f}  events/round mean {(w >> 16).mean():.2f}")
+    fb8 = d[:, 0] == -8
+    if fb8.any():
+        print("  brick failures by reason (1 staging overflow, 2 tie overflow, 3 m<k, 4 list>32, 5 band>tau, 6 certificate):",
+              np.bincount(d[fb8, 1], minlength=7)[1:], " staged mean", d[fb8, 2].mean())
     fb = ~brick
     if fb.any():
         print(f"  fallback: level mean {d[fb, 0].mean():.2f}, probes mean {d[fb, 1].mean():.0f}, cands mean {d[fb, 2].mean():.0f}")

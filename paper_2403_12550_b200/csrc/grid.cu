@@ -120,10 +120,11 @@ constexpr int kAllocPerThread = 4;
 __global__ void __launch_bounds__(kAllocThreads) k_grid_alloc(GridView g, const int32_t *__restrict__ d_n) {
     pdl_wait();
     pdl_launch_dependents();
-    __shared__ uint32_t s_tot[kMaxLevels], s_base[kMaxLevels];
+    __shared__ uint32_t s_tot[kMaxLevels], s_base[kMaxLevels], s_bn, s_bbase;
     if (*d_n <= 0) return;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x < kMaxLevels) s_tot[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_bn = 0;
     __syncthreads();
     uint32_t slot[kAllocPerThread], cnt[kAllocPerThread], off[kAllocPerThread];
     int lev[kAllocPerThread];
@@ -158,9 +159,39 @@ __global__ void __launch_bounds__(kAllocThreads) k_grid_alloc(GridView g, const 
     __syncthreads();
     if (threadIdx.x < g.levels) s_base[threadIdx.x] = s_tot[threadIdx.x] ? atomicAdd(g.counters + threadIdx.x, s_tot[threadIdx.x]) : 0u;
     __syncthreads();
+    uint32_t start[kAllocPerThread];
 #pragma unroll
-    for (int r = 0; r < kAllocPerThread; ++r)
-        if (lev[r] >= 0) g.table[slot[r]].start = (uint32_t)lev[r] * (uint32_t)g.cap + s_base[lev[r]] + off[r];
+    for (int r = 0; r < kAllocPerThread; ++r) {
+        start[r] = lev[r] >= 0 ? (uint32_t)lev[r] * (uint32_t)g.cap + s_base[lev[r]] + off[r] : 0u;
+        if (lev[r] >= 0) g.table[slot[r]].start = start[r];
+    }
+    if (g.bricks) {
+        // the occupied level-0 cells as a compact list: offsets aggregated per warp and per block
+        // (one global atomic per block: same-address atomics per warp were the bottleneck)
+        unsigned bal[kAllocPerThread];
+        uint32_t wtot = 0;
+#pragma unroll
+        for (int r = 0; r < kAllocPerThread; ++r) {
+            bal[r] = __ballot_sync(0xffffffffu, lev[r] == 0 && cnt[r] > 0);
+            wtot += __popc(bal[r]);
+        }
+        uint32_t woff = 0;
+        if (lane == 0 && wtot) woff = atomicAdd(&s_bn, wtot);
+        woff = __shfl_sync(0xffffffffu, woff, 0);
+        __syncthreads();
+        if (threadIdx.x == 0) s_bbase = s_bn ? atomicAdd(g.n_bricks, s_bn) : 0u;
+        __syncthreads();
+        uint32_t pos = s_bbase + woff;
+#pragma unroll
+        for (int r = 0; r < kAllocPerThread; ++r) {
+            if (bal[r] >> lane & 1u) {
+                const unsigned long long key = g.table[slot[r]].key;
+                g.bricks[pos + __popc(bal[r] & ((1u << lane) - 1u))] =
+                    make_uint4(start[r], cnt[r], (uint32_t)key, (uint32_t)(key >> 32));
+            }
+            pos += __popc(bal[r]);
+        }
+    }
 }
 
 template <bool WITH_COV>
@@ -308,6 +339,8 @@ static GridView carve(Carver &c, int cap, int levels, bool with_cov, float h0, b
     g.table = c.take<CellEntry>(slots);
     g.mask = slots - 1;
     g.levels = levels;
+    g.bricks = nullptr;
+    g.n_bricks = nullptr;
     g.h0 = h0;
     g.inv_h0 = h0 > 0.f ? 1.0f / h0 : 0.f;
     g.spos = c.take<float4>((size_t)levels * cap);

@@ -28,6 +28,8 @@ struct GridView {
     uint32_t *mark;          // nullable: one bit per table slot, zeroed by the build (tile kNN units)
     int32_t *bbox;           // [6] ordered-int encoded float min xyz / max xyz
     int cap;
+    uint4 *bricks;           // nullable: the alloc step also lists the occupied level-0 cells here
+    uint32_t *n_bricks;      //   as (start, count, key lo, key hi), count in *n_bricks (zeroed by init)
 };
 
 __device__ __forceinline__ int32_t float_to_ordered(float f) {

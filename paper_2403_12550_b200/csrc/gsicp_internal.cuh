@@ -15,7 +15,10 @@ constexpr double kNoneFloor = 1e-6;      // NONE-mode eigenvalue floor, m^2 (S:8
 constexpr int kMaxLevels = 8;
 constexpr int kAlignThreads = 384;       // 12 warps x 148 SMs >= 51k resident points (168 regs)
 constexpr int kAlignTerms = 29;          // 21 H (upper) + 6 b + cost + count
-constexpr int kGraphK = 16;              // target kNN-graph degree (self included)
+#ifndef GSICP_GRAPH_K
+#define GSICP_GRAPH_K 16
+#endif
+constexpr int kGraphK = GSICP_GRAPH_K;   // target kNN-graph degree (self included)
 
 // 16-byte cell-table entry: 64-bit cell key, start offset and point count of the cell.
 struct __align__(16) CellEntry {

@@ -1267,24 +1267,6 @@ struct BrickArgs {
     uint32_t *queue_n;
 };
 
-// the occupied level-0 cells of the grid as a compact list (one atomic per warp)
-__global__ void k_brick_list(GridView g, uint4 *bricks, uint32_t *n_bricks) {
-    pdl_wait();
-    pdl_launch_dependents();
-    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-    CellEntry e;
-    e.key = kEmptyKey;
-    e.count = 0;
-    if (s <= g.mask) e = g.table[s];
-    const bool occ = e.key != kEmptyKey && (e.key >> 60) == 0ull && e.count > 0;
-    const unsigned b = __ballot_sync(kFull, occ);
-    const int lane = threadIdx.x & 31;
-    uint32_t base = 0;
-    if (lane == 0 && b) base = atomicAdd(n_bricks, (uint32_t)__popc(b));
-    base = __shfl_sync(kFull, base, 0);
-    if (occ) bricks[base + __popc(b & ((1u << lane) - 1u))] = make_uint4(e.start, e.count, (uint32_t)e.key, (uint32_t)(e.key >> 32));
-}
-
 template <int K, bool SORT>
 __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, BrickArgs b) {
     static_assert(K + kBrickU < kBrickLx, "list capacity");
@@ -1754,9 +1736,7 @@ template <int K>
 cudaError_t launch_brick(KnnArgs a, const BrickArgs &b, int cap, cudaStream_t s) {
     const GridView &g = a.g;
     ktimer_mark(KT_KNN_SEARCH, false, s);
-    launch_pdl(k_brick_list, dim3(blocks_for((long long)g.mask + 1, 256)), dim3(256), 0, s, g, const_cast<uint4 *>(b.bricks),
-               const_cast<uint32_t *>(b.n_bricks));
-    GSICP_LAUNCH_CHECK("k_brick_list");
+    (void)g;  // (the brick list comes from the grid build's alloc step)
     const dim3 grid((unsigned)num_sms() * kBrickBlocksPerSm);  // one resident wave (by shared memory)
     constexpr int smem = kBrickWarps * kBrickSmemPerWarp;
     static PerDevice<int> attr;  // opt-in dynamic shared memory, once per device
@@ -1776,7 +1756,7 @@ cudaError_t launch_brick(KnnArgs a, const BrickArgs &b, int cap, cudaStream_t s)
     cudaError_t e = launch_search<K>(a, cap, s);
     if (e == cudaSuccess) e = launch_epilogue<K>(a, cap, s);
     if (e != cudaSuccess) return e;
-    note_launch(4);
+    note_launch(3);
     return cudaSuccess;
 }
 
@@ -1824,6 +1804,10 @@ cudaError_t covariances_launch(const float *pos, const int32_t *d_n, int cap, in
     b.n_bricks = a.g.counters + kMaxLevels + 2;  // zeroed by the grid build
     b.queue_n = a.g.counters + kMaxLevels + 3;
     a.work = a.g.counters + kMaxLevels;
+    if (k <= 24) {  // the alloc step lists the bricks
+        a.g.bricks = const_cast<uint4 *>(b.bricks);
+        a.g.n_bricks = const_cast<uint32_t *>(b.n_bricks);
+    }
     cudaError_t e = grid_build(a.g, a.pos, nullptr, nullptr, d_n, cap, s);
     if (e != cudaSuccess) return e;
     if (k <= 4) return launch_brick<4>(a, b, cap, s);

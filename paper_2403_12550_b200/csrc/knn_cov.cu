@@ -1553,9 +1553,16 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
                     if (a.debug) a.debug[i] = make_int4(-7, bnc, m, nbr * 256 + n_events * 65536 + __popc(__ballot_sync(__activemask(), true)));
                 }
             }
-            if (has && !ok) {
-                b.queue[atomicAdd(b.queue_n, 1u)] = (uint32_t)i;
-                if (a.debug) a.debug[i] = make_int4(-8, why, bnc, m);
+            {  // the queries left to the warp search (one atomic per warp)
+                const bool qd = has && !ok;
+                const unsigned qb = __ballot_sync(kFull, qd);
+                uint32_t qbase = 0u;
+                if (lane == 0 && qb) qbase = atomicAdd(b.queue_n, (uint32_t)__popc(qb));
+                qbase = __shfl_sync(kFull, qbase, 0);
+                if (qd) {
+                    b.queue[qbase + __popc(qb & ((1u << lane) - 1u))] = (uint32_t)i;
+                    if (a.debug) a.debug[i] = make_int4(-8, why, bnc, m);
+                }
             }
             __syncwarp();  // the list columns are reused by the next round
         }

@@ -79,6 +79,9 @@ struct AlignArgs {
     double *seed_hdr;         // [16]: pose the seeds were computed at (12), ticket at [12]
     double seed_ticket;       // k_align_seed: ticket to write; k_align: ticket expected (0: none)
     int32_t *seed_queue;      // [cap] hard queries of the seed pass
+    int2 *flat_queue;         // [cap] hard queries of the flat GN path (point, warm-start slot)
+    int32_t *rset;            // [cap][kSetCap] the flat path's neighbourhood sets (-1 pads)
+    float4 *rset_hdr;         // [cap] (query the set was taken at, rho_cert); rho_cert 0: none
     int32_t *seed_qn;         // [1] their count
     // diagnostic (nullable): per GN iteration it < iter_cap, iter_rec[it * kIterRec + ..] = the pose
     // T_it the iteration linearised at (12, row-major 3x4) then its 29 reduced terms (21 H upper,
@@ -1343,6 +1346,536 @@ __global__ void k_align_init_batch(const __grid_constant__ AlignBatch b) {
     if (i == 0) *a.barrier = 0u;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Large clouds (cap above the co-resident grid's threads, e.g. a stride-1 TUM frame): the GN loop
+// as ordinary kernels per iteration instead of one persistent cooperative kernel —
+//   k_flat_corr : thread per point, the cheap certified paths of k_align (seeds, motion-bounded
+//                 reuse, certified graph step, own-cell search), the rest to a global queue;
+//   k_flat_hard : a warp per queued point, spread over the whole GPU (warp_nn and the
+//                 second-neighbour bound of the reuse test);
+//   k_flat_terms: thread per point, the Eq. 1 terms (binary64) and block partials; the last block
+//                 to arrive reduces the partials in block order (deterministic) and runs the same
+//                 solve step as k_align, then publishes the pose, the iteration and the stop flag.
+// In a captured graph the three kernels are the body of a conditional WHILE node (k_flat_terms
+// sets its condition); otherwise they are launched max_iters times and return at once after the
+// stop.  k_align's persistent grid holds one point per thread for 1 block / SM (168 registers):
+// a 205k-point frame then runs its hard queries as 12 warps per block in turn; here they spread
+// over every warp slot of the GPU.
+// Neighbourhood sets (the flat path's near-tie reuse): a point whose 1-NN stays
+// ambiguous — a near-tie with its second neighbour, e.g. noisy depth 1-3 cm off a surface sampled
+// at ~1.2 cm — fails both the motion-bounded reuse and the graph certificate every iteration.
+// When the warp search solves such a point it also collects every target whose binary32 key from
+// fl32(q) is <= rho^2 (rho as the second-neighbour bound's) and keeps the kSetCap nearest: every
+// other target is then at least rho_cert from q (rho_cert = the (kSetCap+1)-th member's distance,
+// or sqrt(rho^2 / (1 + 6u)) - E when all fit).  At a later query q' with |q' - q| <= delta the
+// best member (binary64 keys, ties by index) is the exact 1-NN whenever its distance is below
+// rho_cert - delta: one gather of <= kSetCap records per thread instead of a warp search.
+constexpr int kSetCap = 16;
+
+// the targets of the cells selected by `valid` with key32(fl32 q) <= B appended to the warp list
+// (lane j holds the j-th; cnt may exceed 32: overflow)
+__device__ __forceinline__ void warp_collect_cells(const AlignArgs &a, const CellIndex &idx, const QueryCell &qc,
+                                                   bool valid, int dx, int dy, int dz, const Qry &q, float B, int lane,
+                                                   int &cnt, int &mine) {
+    const uint2 se = valid ? idx.one(qc.c[0] + dx, qc.c[1] + dy, qc.c[2] + dz) : make_uint2(0u, 0u);
+    uint32_t incl = se.y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t ctot = __shfl_sync(0xffffffffu, incl, 31);
+    for (uint32_t base = 0; base < ctot; base += 32) {
+        const uint32_t item = base + lane;
+        int l0 = 0, l1 = 31;
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+            const int mid = (l0 + l1) >> 1;
+            if (__shfl_sync(0xffffffffu, incl, mid) > item) l1 = mid; else l0 = mid + 1;
+        }
+        const uint32_t c_incl = __shfl_sync(0xffffffffu, incl, l0);
+        const uint32_t c_start = __shfl_sync(0xffffffffu, se.x, l0);
+        const uint32_t c_cnt = __shfl_sync(0xffffffffu, se.y, l0);
+        int slot = -1;
+        bool in = false;
+        if (item < ctot) {
+            slot = (int)(c_start + (item - (c_incl - c_cnt)));
+            in = q.key32(__ldg(a.tpos + slot)) <= B;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        const int k = lane - cnt, nb = __popc(bal);
+        const bool take = k >= 0 && k < nb;
+        const int got = __shfl_sync(0xffffffffu, slot, take ? (int)__fns(bal, 0u, k + 1) : lane);
+        if (take) mine = got;
+        cnt += nb;
+    }
+}
+
+// every target with key32(fl32 q) <= B (warp_nn's traversal with a fixed bound); stops early
+// once more than 32 are found
+__device__ void warp_range(const AlignArgs &a, const CellIndex &idx, const int *sb, const Qry &q, float B, int lane,
+                           int &cnt, int &mine) {
+    const QueryCell qc(q.x, q.y, q.z, a.h, a.inv_h);
+    const int *blo = sb, *bhi = sb + 3;
+    cnt = 0;
+    mine = -1;
+    auto in_box = [&](int dx, int dy, int dz) {
+        const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
+        return x >= blo[0] && x <= bhi[0] && y >= blo[1] && y <= bhi[1] && z >= blo[2] && z <= bhi[2];
+    };
+    for (int m = 1; m <= kWarpShells; ++m) {
+        const int sc = m == 1 ? 27 : shell_count(m);
+        for (int t0 = 0; t0 < sc; t0 += 32) {
+            const int t = t0 + lane;
+            int dx = 0, dy = 0, dz = 0;
+            bool valid = t < sc;
+            if (valid) {
+                if (m == 1) {
+                    if (t > 0) shell_cell(1, t - 1, dx, dy, dz);
+                } else {
+                    shell_cell(m, t, dx, dy, dz);
+                }
+                valid = in_box(dx, dy, dz) && qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2) <= B;
+            }
+            if (!__any_sync(0xffffffffu, valid)) continue;
+            warp_collect_cells(a, idx, qc, valid, dx, dy, dz, q, B, lane, cnt, mine);
+            if (cnt > 32) return;
+        }
+        if (B < qc.certified_key(m) || qc.covers(m, blo, bhi)) return;
+    }
+    int lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) axis_range(qc, k, B, blo[k], bhi[k], lo[k], hi[k]);
+    const int nx = max(hi[0] - lo[0] + 1, 0), ny = max(hi[1] - lo[1] + 1, 0), nz = max(hi[2] - lo[2] + 1, 0);
+    const long long total = (long long)nx * ny * nz;
+    for (long long t0 = 0; t0 < total; t0 += 32) {
+        const long long t = t0 + lane;
+        int dx = 0, dy = 0, dz = 0;
+        bool valid = t < total;
+        if (valid) {
+            dx = lo[0] + (int)(t % nx);
+            dy = lo[1] + (int)((t / nx) % ny);
+            dz = lo[2] + (int)(t / ((long long)nx * ny));
+            valid = max(abs(dx), max(abs(dy), abs(dz))) > kWarpShells &&
+                    qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2) <= B;
+        }
+        if (!__any_sync(0xffffffffu, valid)) continue;
+        warp_collect_cells(a, idx, qc, valid, dx, dy, dz, q, B, lane, cnt, mine);
+        if (cnt > 32) return;
+    }
+}
+
+// After the warp search of point i (nn: its exact 1-NN at q): the second-neighbour bound d2 of
+// the motion-bounded reuse and, when at most 32 targets lie within rho, the point's
+// neighbourhood set (the kSetCap nearest of them).  Returns d2.
+__device__ float warp_reuse_state(const AlignArgs &a, const CellIndex &idx, const int *sb, const Qry &q, const NN &nn,
+                                  int i, int lane) {
+    const bool in_r = nn.slot >= 0 && nn.bk < a.r2;
+    const float base = in_r ? sqrtf(__double2float_ru(nn.bk)) : a.r;
+    if (!(base < INFINITY)) return 0.f;
+    const float rho = base * 1.25f + 0.25f * a.h;
+    const float B = rho * rho;
+    const float rc_all = fmaxf(__fsub_rd(__fsqrt_rd(__fmul_rd(B, 0.9999994f)), q.E()), 0.f);
+    int cnt, mine;
+    warp_range(a, idx, sb, q, B, lane, cnt, mine);
+    if (cnt <= 32) {
+        // binary64 keys of the members, a warp bitonic sort, the kSetCap nearest kept
+        const double kk = lane < cnt ? q.key(__ldg(a.tpos + mine)) : INFINITY;
+        double sk = kk;
+        int ss = lane < cnt ? mine : -1;
+#pragma unroll
+        for (int kb = 2; kb <= 32; kb <<= 1) {
+#pragma unroll
+            for (int j = kb >> 1; j > 0; j >>= 1) {
+                const double ok = shfl_f64(sk, lane ^ j);
+                const int os = __shfl_xor_sync(0xffffffffu, ss, j);
+                const bool low = ((lane & kb) == 0) == ((lane & j) == 0);  // this lane keeps the smaller
+                if (low ? (ok < sk) : (ok > sk)) {
+                    sk = ok;
+                    ss = os;
+                }
+            }
+        }
+        float rc = rc_all;
+        const double k17 = shfl_f64(sk, kSetCap);  // the (kSetCap+1)-th nearest
+        if (cnt > kSetCap) rc = fminf(rc, sqrtf(__double2float_rd(k17)));
+        rc *= (1.f - kReuseMargin);
+        if (lane < kSetCap) a.rset[(size_t)i * kSetCap + lane] = lane < cnt ? ss : -1;
+        if (lane == 0) a.rset_hdr[i] = make_float4(q.x, q.y, q.z, rc);
+        // the second neighbour: the nearest member other than the 1-NN
+        double k2 = lane < cnt && mine != nn.slot ? kk : INFINITY;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) k2 = fmin(k2, shfl_f64(k2, lane ^ o));
+        const float d2s = k2 < INFINITY ? sqrtf(__double2float_rd(k2)) : INFINITY;
+        return fminf(fminf(d2s, rho), rc_all) * (1.f - kReuseMargin);
+    }
+    if (lane == 0) a.rset_hdr[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    NN n2;
+    warp_nn(a, idx, sb, q, n2, lane, B, nn.slot);
+    return fminf(n2.slot >= 0 ? sqrtf(__double2float_rd(n2.bk)) : INFINITY, rho) * (1.f - kReuseMargin);
+}
+
+// The neighbourhood-set test of point i at its new query q: true if the set proves the exact
+// 1-NN (nn = it, or the point stays gated); false if there is no set or the query moved too far.
+__device__ __forceinline__ bool set_nn(const AlignArgs &a, const Qry &q, int i, NN &nn) {
+    const float4 h = __ldcg(a.rset_hdr + i);  // (written during this loop: no read-only path)
+    if (!(h.w > 0.f)) return false;
+    const float ex = q.x - h.x, ey = q.y - h.y, ez = q.z - h.z;
+    const float delta = sqrtf(ex * ex + ey * ey + ez * ez) * (1.f + kReuseMargin) + 2.f * q.E();
+    const float L = h.w - delta;
+    if (!(L > 0.f)) return false;
+    const int4 *ls = reinterpret_cast<const int4 *>(a.rset + (size_t)i * kSetCap);
+    int sl[kSetCap];
+#pragma unroll
+    for (int v = 0; v < kSetCap / 4; ++v) {
+        const int4 w = __ldcg(ls + v);
+        sl[4 * v] = w.x; sl[4 * v + 1] = w.y; sl[4 * v + 2] = w.z; sl[4 * v + 3] = w.w;
+    }
+    NN ns;
+    float k32[kSetCap];
+    {
+        float4 p[kSetCap];
+#pragma unroll
+        for (int u = 0; u < kSetCap; ++u) p[u] = sl[u] >= 0 ? __ldg(a.tpos + sl[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < kSetCap; ++u) k32[u] = sl[u] >= 0 ? q.key32(p[u]) : INFINITY;
+    }
+    float m32 = INFINITY;
+#pragma unroll
+    for (int u = 0; u < kSetCap; ++u) m32 = fminf(m32, k32[u]);
+    if (m32 < INFINITY) {
+        // binary64 keys of the members that can beat or tie the best binary32 one
+        const float s0 = __fmul_ru(__fadd_ru(__fsqrt_ru(m32), 2.f * q.E()), 1.000004f);
+        const float scr = __fmul_ru(s0, s0);
+#pragma unroll
+        for (int u = 0; u < kSetCap; ++u) {
+            if (k32[u] <= scr) {
+                const float4 rec = __ldg(a.tpos + sl[u]);
+                ns.offer(q.key(rec), (uint32_t)__float_as_int(rec.w), sl[u], rec);
+            }
+        }
+    }
+    const float d1 = ns.slot >= 0 ? fminf(sqrtf(__double2float_ru(ns.bk)), a.r) : a.r;
+    if (!(L * (1.f - kReuseMargin) > d1 * (1.f + kReuseMargin))) return false;
+    nn = ns;
+    return true;
+}
+
+struct FlatState {
+    int it, stop, status, iters, converged, pad;
+    unsigned int qn, arrive;
+    double n_in, cost;
+    double T[12];
+    double lm[kLmState];
+};
+#ifndef GSICP_FLAT_D2_FROM_ITER
+#define GSICP_FLAT_D2_FROM_ITER 2
+#endif
+constexpr int kFlatD2FromIter = GSICP_FLAT_D2_FROM_ITER;
+  // reuse bound + neighbourhood set from this iteration
+#ifndef GSICP_FLAT_DIV
+#define GSICP_FLAT_DIV 1  // clouds above (co-resident threads) / this take the flat path
+#endif
+constexpr int kFlatT = 256;
+constexpr int kFlatHardT = 128;
+constexpr int kFlatTermsPerSm = 2;  // k_flat_terms blocks per SM (partials reduced by the last one)
+
+__global__ void k_flat_init(AlignArgs a, FlatState *fs) {
+    pdl_wait();
+    pdl_launch_dependents();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < a.cap) {
+        a.corr_ws[i] = -1;
+        a.reuse_ws[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        a.rset_hdr[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (i == 0) {
+        fs->it = 0;
+        fs->stop = 0;
+        fs->status = GSICP_WARN_MAX_ITERS;
+        fs->iters = 0;
+        fs->converged = 0;
+        fs->qn = 0u;
+        fs->arrive = 0u;
+        fs->n_in = 0.0;
+        fs->cost = 0.0;
+        for (int k = 0; k < 12; ++k) fs->T[k] = a.d_T[k];
+        fs->lm[42] = 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(kFlatT) k_flat_corr(AlignArgs a, FlatState *fs) {
+    __shared__ double sT[12];
+    __shared__ int sBox[6];
+    __shared__ CellIndex sIdx;
+    __shared__ int sIt, sStop, sSeeded;
+    pdl_wait();
+    pdl_launch_dependents();
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) {
+        sStop = fs->stop;
+        sIt = fs->it;
+        load_cell_index(a, sIdx, sBox);
+        // seeds only at the pose they were computed at (iteration 0, the caller's pose)
+        bool ok = a.seed_ticket > 0.0 && a.seed_hdr[12] == a.seed_ticket;
+        for (int k = 0; k < 12; ++k) ok = ok && __double_as_longlong(a.seed_hdr[k]) == __double_as_longlong(a.d_T[k]);
+        sSeeded = ok;
+    }
+    if (tid < 12) sT[tid] = fs->T[tid];
+    __syncthreads();
+    if (sStop) return;
+    const int it = sIt, n = *a.d_n;
+    for (int i0 = blockIdx.x * kFlatT; i0 < n; i0 += gridDim.x * kFlatT) {  // (warp-uniform trip count)
+        const int i = i0 + tid;
+        bool queued = false;
+        int qslot = -1;
+        if (i < n) {
+            const float4 x = __ldg(a.spos + i);
+            double q0, q1, q2;
+            k3(sT, x.x, x.y, x.z, q0, q1, q2);
+            const Qry q(q0, q1, q2);
+            const QueryCell qc(q.x, q.y, q.z, a.h, a.inv_h);
+            NN nn;
+            const bool seeded = it == 0 && sSeeded;
+            int slot = seeded ? a.seed_slot[i] : a.corr_ws[i];
+            if (slot <= -2) slot = -2 - slot;
+            if (slot >= 0) {
+                const float4 rec = __ldg(a.tpos + slot);
+                nn.set(q.key(rec), slot, rec);
+            }
+            bool exact = seeded;
+            const float4 ru = seeded ? make_float4(0.f, 0.f, 0.f, 0.f) : a.reuse_ws[i];
+            float d2lb = ru.w;
+            if (!exact && d2lb > 0.f) {  // the motion-bounded reuse (k_align)
+                const float ex = q.x - ru.x, ey = q.y - ru.y, ez = q.z - ru.z;
+                const float delta = sqrtf(ex * ex + ey * ey + ez * ez) * (1.f + kReuseMargin) + 2.f * q.E();
+                const float d1 = nn.slot >= 0 ? fminf(sqrtf(__double2float_ru(nn.bk)), a.r) : a.r;
+                if ((d2lb - delta) * (1.f - kReuseMargin) > d1 * (1.f + kReuseMargin)) {
+                    exact = true;
+                    d2lb -= delta;
+                }
+            }
+            const bool by_reuse = exact && !seeded;
+            if (!exact) d2lb = 0.f;
+            bool by_set = false;
+            if (!exact && !seeded) by_set = exact = set_nn(a, q, i, nn);  // near-tie points: the neighbourhood set
+            const uint2 own = exact ? make_uint2(0u, 0u) : sIdx.one(qc.c[0], qc.c[1], qc.c[2]);
+            uint2 own_left = own;
+            if (!exact && a.nbr && (nn.slot < 0 || nn.bk > 0.25 * (double)a.h * (double)a.h)) {
+                scan_target_cell(a, own, q, nn);  // a far or absent warm start: from the own cell
+                own_left = make_uint2(0u, 0u);
+            }
+            const bool pre = exact;
+            if (!exact && nn.slot >= 0 && a.nbr) exact = graph_nn(a, q, nn, d2lb);
+            const bool by_graph = exact && !pre;
+            if (!exact && !a.nbr) exact = nn_search(a, sIdx, sBox, qc, own_left, q, nn, true);
+            if (a.debug && it < 32) {  // diagnostic: per point bitmasks over iterations (queued, reuse, set, graph)
+                int4 d = it == 0 ? make_int4(0, 0, 0, 0) : a.debug[i];
+                const int bit = 1 << it;
+                d.x |= exact ? 0 : bit;
+                d.y |= by_reuse ? bit : 0;
+                d.z |= by_set ? bit : 0;
+                d.w |= by_graph ? bit : 0;
+                a.debug[i] = d;
+            }
+            if (exact) {
+                a.corr_ws[i] = (nn.slot >= 0 && nn.bk < a.r2) ? nn.slot : -2 - nn.slot;
+                a.reuse_ws[i] = make_float4(q.x, q.y, q.z, seeded ? 0.f : d2lb);
+            } else {
+                queued = true;
+                qslot = nn.slot;
+            }
+        }
+        // the rest to the global queue (one atomic per warp); the warm start travels along
+        const unsigned qb = __ballot_sync(0xffffffffu, queued);
+        unsigned int base = 0u;
+        if (lane == 0 && qb) base = atomicAdd(&fs->qn, (unsigned)__popc(qb));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (queued) a.flat_queue[base + __popc(qb & ((1u << lane) - 1u))] = make_int2(i, qslot);
+    }
+}
+
+__global__ void __launch_bounds__(kFlatHardT) k_flat_hard(AlignArgs a, FlatState *fs) {
+    __shared__ double sT[12];
+    __shared__ int sBox[6];
+    __shared__ CellIndex sIdx;
+    __shared__ int sIt, sStop;
+    pdl_wait();
+    pdl_launch_dependents();
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) {
+        sStop = fs->stop;
+        sIt = fs->it;
+        load_cell_index(a, sIdx, sBox);
+    }
+    if (tid < 12) sT[tid] = fs->T[tid];
+    __syncthreads();
+    if (sStop) return;
+    const int it = sIt;
+    const int qn = (int)fs->qn;
+    const int warps = gridDim.x * (kFlatHardT / 32);
+    for (int k = blockIdx.x * (kFlatHardT / 32) + (tid >> 5); k < qn; k += warps) {
+        const int2 qe = a.flat_queue[k];
+        const int i = qe.x, sl = qe.y;
+        const float4 x = __ldg(a.spos + i);
+        double q0, q1, q2;
+        k3(sT, x.x, x.y, x.z, q0, q1, q2);
+        const Qry q(q0, q1, q2);
+        NN nn;
+        if (sl >= 0) {
+            const float4 rec = __ldg(a.tpos + sl);
+            nn.set(q.key(rec), sl, rec);
+        }
+        warp_nn(a, sIdx, sBox, q, nn, lane);
+        // the second-neighbour bound and the neighbourhood set for the next iterations
+        const bool in_r = nn.slot >= 0 && nn.bk < a.r2;
+        const float d2 = it >= kFlatD2FromIter ? warp_reuse_state(a, sIdx, sBox, q, nn, i, lane) : 0.f;
+        if (lane == 0) {
+            a.corr_ws[i] = in_r ? nn.slot : -2 - nn.slot;
+            a.reuse_ws[i] = make_float4(q.x, q.y, q.z, d2);
+        }
+    }
+}
+
+template <bool LM>
+__global__ void __launch_bounds__(kFlatT) k_flat_terms(AlignArgs a, FlatState *fs, cudaGraphConditionalHandle cond,
+                                                      int use_cond) {
+    constexpr int kW = kFlatT / 32;
+    __shared__ double sT[12];
+    __shared__ double sRed[kW][kPad];
+    __shared__ double sAcc[kPad];
+    __shared__ int sIt, sStop, sLast;
+    pdl_wait();
+    pdl_launch_dependents();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        sStop = fs->stop;
+        sIt = fs->it;
+    }
+    if (tid < 12) sT[tid] = fs->T[tid];
+    __syncthreads();
+    if (sStop) return;
+    const int it = sIt, n = *a.d_n;
+    double acc[kAlignTerms];
+#pragma unroll
+    for (int k = 0; k < kAlignTerms; ++k) acc[k] = 0.0;
+    for (int i = blockIdx.x * kFlatT + tid; i < n; i += gridDim.x * kFlatT) {
+        const int slot = a.corr_ws[i];
+        int32_t corr_val = -1;
+        if (slot >= 0) {
+            const float4 x = __ldg(a.spos + i);
+            double q0, q1, q2;
+            k3(sT, x.x, x.y, x.z, q0, q1, q2);
+            const float4 m = __ldg(a.tpos + slot);
+            if (pair_terms(sT, q0, q1, q2, __ldg(a.scov_a + i), __ldg(a.scov_b + i), m, __ldg(a.tcov_a + slot),
+                           __ldg(a.tcov_b + slot), acc))
+                corr_val = __float_as_int(m.w);
+        }
+        if (a.corr_out) a.corr_out[i] = corr_val;
+        if (a.iter_corr && it < a.iter_cap) a.iter_corr[(size_t)it * a.cap + i] = corr_val;
+    }
+#pragma unroll
+    for (int k = 0; k < kAlignTerms; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < kAlignTerms; ++k) sRed[warp][k] = acc[k];
+    }
+    __syncthreads();
+    if (tid < kAlignTerms) {
+        double t = 0.0;
+        for (int w = 0; w < kW; ++w) t += sRed[w][tid];
+        a.partials[(size_t)blockIdx.x * kPad + tid] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sLast = atomicAdd(&fs->arrive, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!sLast) return;
+    __threadfence();
+    // the last block: every partial in block order (8 chunks per term, then the chunks in order)
+    {
+        constexpr int kChunks = kFlatT / 32;
+        const int term = tid & 31, chunk = tid >> 5;
+        const int G = gridDim.x, per = (G + kChunks - 1) / kChunks;
+        double sum = 0.0;
+        if (term < kAlignTerms) {
+            const int b0 = chunk * per, b1 = min(G, b0 + per);
+            int b = b0;
+            for (; b + 4 <= b1; b += 4) {
+                const double v0 = __ldcg(a.partials + (size_t)b * kPad + term);
+                const double v1 = __ldcg(a.partials + (size_t)(b + 1) * kPad + term);
+                const double v2 = __ldcg(a.partials + (size_t)(b + 2) * kPad + term);
+                const double v3 = __ldcg(a.partials + (size_t)(b + 3) * kPad + term);
+                sum += v0;
+                sum += v1;
+                sum += v2;
+                sum += v3;
+            }
+            for (; b < b1; ++b) sum += __ldcg(a.partials + (size_t)b * kPad + term);
+        }
+        sRed[chunk][term] = sum;
+        __syncthreads();
+        if (tid < kAlignTerms) {
+            double t = 0.0;
+            for (int c = 0; c < kChunks; ++c) t += sRed[c][tid];
+            sAcc[tid] = t;
+        }
+        __syncthreads();
+    }
+    if (a.iter_rec && it < a.iter_cap && tid < 12 + kAlignTerms) {
+        double *rec = a.iter_rec + (size_t)it * kIterRec;
+        rec[tid] = tid < 12 ? sT[tid] : sAcc[tid - 12];
+    }
+    if (tid == 0) {
+        double n_in = sAcc[28], cost = sAcc[27];
+        int st = fs->status, its = fs->iters, cv = fs->converged;
+        int done;
+        if (a.linearize_only) {
+            int t = 0;
+            for (int r = 0; r < 6; ++r)
+                for (int c = r; c < 6; ++c) a.d_lin[6 * r + c] = a.d_lin[6 * c + r] = sAcc[t++];
+            for (int k = 0; k < 6; ++k) a.d_lin[36 + k] = sAcc[21 + k];
+            a.d_lin[42] = sAcc[27];
+            a.d_lin[43] = sAcc[28];
+            st = GSICP_OK;
+            done = 1;
+        } else {
+            done = solve_step_t<LM>(a, sAcc, sT, it, n, st, its, cv, fs->lm);
+            if (LM && fs->lm[42] != 0.0) {  // stats of the kept linearisation
+                n_in = fs->lm[12 + 28];
+                cost = fs->lm[12 + 27];
+            }
+        }
+        fs->status = st;
+        fs->iters = its;
+        fs->converged = cv;
+        fs->n_in = n_in;
+        fs->cost = cost;
+        for (int k = 0; k < 12; ++k) fs->T[k] = sT[k];
+        fs->it = it + 1;
+        fs->qn = 0u;
+        fs->arrive = 0u;
+        if (done) {
+            fs->stop = 1;
+            if (!a.linearize_only) {
+                for (int k = 0; k < 12; ++k) a.d_T[k] = sT[k];
+                a.d_T[12] = 0.0; a.d_T[13] = 0.0; a.d_T[14] = 0.0; a.d_T[15] = 1.0;
+            }
+            gsicp_align_stats sts;
+            sts.fitness = n > 0 ? n_in / (double)n : 0.0;
+            sts.mean_cost = n_in > 0.0 ? cost / n_in : 0.0;
+            sts.n_inliers = (int32_t)n_in;
+            sts.iters = its;
+            sts.converged = cv;
+            sts.status = st;
+            *a.d_stats = sts;
+        }
+        if (use_cond) cudaGraphSetConditional(cond, done ? 0u : 1u);
+    }
+}
+
 // Co-resident grid for the cooperative launch (0 if the kernel cannot be resident at all).
 constexpr int kMaxAlignGrid = 2048;  // partial records reserved in the workspace (>= SMs x blocks/SM)
 
@@ -1378,6 +1911,10 @@ struct AlignWs {
     double *seed_hdr;
     int32_t *seed_queue;
     int32_t *seed_qn;
+    FlatState *flat;
+    int2 *flat_queue;
+    int32_t *rset;
+    float4 *rset_hdr;
 };
 
 static AlignWs align_carve(Carver &c, int cap) {
@@ -1394,6 +1931,10 @@ static AlignWs align_carve(Carver &c, int cap) {
     w.seed_hdr = c.take<double>(16);
     w.seed_queue = c.take<int32_t>(cap);
     w.seed_qn = c.take<int32_t>(4);
+    w.flat = c.take<FlatState>(1);
+    w.flat_queue = c.take<int2>(cap);
+    w.rset = c.take<int32_t>((size_t)cap * kSetCap);
+    w.rset_hdr = c.take<float4>(cap);
     return w;
 }
 static AlignWs align_carve(void *base, int cap) {
@@ -1460,6 +2001,9 @@ static AlignArgs make_args(const gsicp_cloud &src, const gsicp_target &tgt, doub
     a.seed_ticket = 0.0;
     a.seed_queue = w.seed_queue;
     a.seed_qn = w.seed_qn;
+    a.flat_queue = w.flat_queue;
+    a.rset = w.rset;
+    a.rset_hdr = w.rset_hdr;
     a.iter_rec = g_align_iter_rec;
     a.iter_corr = g_align_iter_corr;
     a.iter_cap = g_align_iter_rec ? g_align_iter_cap : 0;
@@ -1527,17 +2071,96 @@ cudaError_t align_seed_launch(const gsicp_cloud &src, const gsicp_target &tgt, c
     return cudaSuccess;
 }
 
+// stream used to capture the flat loop's WHILE body (per host thread)
+static cudaStream_t flat_body_stream() {
+    static thread_local cudaStream_t bs = nullptr;
+    static thread_local int dev = -1;
+    int d = 0;
+    cudaGetDevice(&d);
+    if (!bs || dev != d) {
+        if (cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        dev = d;
+    }
+    return bs;
+}
+
+static cudaError_t flat_iteration(const AlignArgs &a, FlatState *fs, int cap, bool lm, cudaGraphConditionalHandle h,
+                                  int use_cond, cudaStream_t s) {
+    const unsigned g1 = std::min<unsigned>(blocks_for(cap > 0 ? cap : 1, kFlatT), (unsigned)num_sms() * 16);
+    launch_pdl(k_flat_corr, dim3(g1), dim3(kFlatT), 0, s, a, fs);
+    GSICP_LAUNCH_CHECK("k_flat_corr");
+    launch_pdl(k_flat_hard, dim3(num_sms() * 8), dim3(kFlatHardT), 0, s, a, fs);
+    GSICP_LAUNCH_CHECK("k_flat_hard");
+    const dim3 g3((unsigned)num_sms() * kFlatTermsPerSm);
+    if (lm)
+        launch_pdl(k_flat_terms<true>, g3, dim3(kFlatT), 0, s, a, fs, h, use_cond);
+    else
+        launch_pdl(k_flat_terms<false>, g3, dim3(kFlatT), 0, s, a, fs, h, use_cond);
+    GSICP_LAUNCH_CHECK("k_flat_terms");
+    return cudaSuccess;
+}
+
+// The flat GN loop (large clouds): init, then the three kernels per iteration — the body of a
+// conditional WHILE node inside a stream capture, else max_iters launches (idle after the stop).
+static cudaError_t align_flat_launch(const AlignArgs &a, const AlignWs &w, int cap, bool lm, cudaStream_t s) {
+    ktimer_mark(KT_ALIGN, false, s);
+    launch_pdl(k_flat_init, dim3(blocks_for(cap > 0 ? cap : 1, 256)), dim3(256), 0, s, a, w.flat);
+    GSICP_LAUNCH_CHECK("k_flat_init");
+    cudaError_t e = cudaSuccess;
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cst);
+    if (cst == cudaStreamCaptureStatusActive) {
+        cudaGraph_t graph = nullptr;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t nd = 0;
+        unsigned long long cid = 0;
+        if ((e = cudaStreamGetCaptureInfo(s, &cst, &cid, &graph, &deps, &nd)) != cudaSuccess) return e;
+        cudaGraphConditionalHandle h;
+        if ((e = cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault)) != cudaSuccess) return e;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        if ((e = cudaGraphAddNode(&cnode, graph, deps, nd, &cp)) != cudaSuccess) return e;
+        cudaStream_t bs = flat_body_stream();
+        if (!bs) return cudaErrorInvalidResourceHandle;
+        if ((e = cudaStreamBeginCaptureToGraph(bs, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+            return e;
+        const bool was = pdl_suspended();
+        pdl_suspended() = true;  // no programmatic edges inside the conditional body
+        const cudaError_t eb = flat_iteration(a, w.flat, cap, lm, h, 1, bs);
+        pdl_suspended() = was;
+        cudaGraph_t body_out = nullptr;
+        e = cudaStreamEndCapture(bs, &body_out);
+        if (eb != cudaSuccess) return eb;
+        if (e != cudaSuccess) return e;
+        if ((e = cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
+            return e;
+    } else {
+        const int iters = std::max(1, a.linearize_only ? 1 : a.max_iters);
+        for (int k = 0; k < iters && e == cudaSuccess; ++k) e = flat_iteration(a, w.flat, cap, lm, cudaGraphConditionalHandle{}, 0, s);
+        if (e != cudaSuccess) return e;
+    }
+    ktimer_mark(KT_ALIGN, true, s);
+    note_launch(4);
+    return cudaSuccess;
+}
+
 cudaError_t align_launch(const gsicp_cloud &src, const gsicp_target &tgt, double *d_T_inout,
                          const gsicp_align_params &p, gsicp_align_stats *d_stats, int32_t *corr_out,
                          int linearize_only, float r_lin, void *ws, cudaStream_t s) {
     AlignWs w = align_carve(ws, src.cap);
     AlignArgs a = make_args(src, tgt, d_T_inout, p, d_stats, corr_out, linearize_only, r_lin, w);
     a.seed_ticket = seed_take(ws, src.pos, tgt.pos);
+    int per_sm = 0;
+    const int G = align_grid_blocks(src.cap, &per_sm);
+    if (G >= 1 && src.cap > G * kT / GSICP_FLAT_DIV) return align_flat_launch(a, w, src.cap, p.solver == 1, s);
     launch_pdl(k_align_init, dim3(blocks_for(src.cap > 0 ? src.cap : 1, 256)), dim3(256), 0, s, w.corr_ws, w.reuse_ws, src.cap,
                w.barrier);
     GSICP_LAUNCH_CHECK("k_align_init");
-    int per_sm = 0;
-    const int G = align_grid_blocks(src.cap, &per_sm);
     if (G < 1) {
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, k_align<false>);

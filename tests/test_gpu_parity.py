@@ -640,6 +640,40 @@ def test_tracker_graph_capture(g, replica):
         assert g.decode_stats(tr.d_stats)["iters"] == st_ref["iters"]
 
 
+def test_tracker_graph_capture_large_cloud(g, tum):
+    """A stride-1 TUM frame (205k points: more than the persistent align grid holds, so the GN loop
+    runs as the flat kernels, inside the captured graph the body of a conditional WHILE node): the
+    replayed graph equals the direct (eager, one launch per iteration) call bit for bit, and the
+    iteration count and inlier count agree."""
+    w = tum
+    tr = g.Tracker(w.K.H, w.K.W, (w.K.fx, w.K.fy, w.K.cx, w.K.cy), stride=1,
+                   params=g.align_params(max_iters=12, max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6))
+    tgt = g.build_target(t(w.means), t(w.quats), t(w.scales))
+    depth = t(w.depth)
+    T_ref, st_ref = tr.track(depth, tgt, w.T_init)  # (the Tracker's own frame graph)
+    assert tr.cloud.n() > 148 * 384  # (the flat path)
+    tr.preprocess(depth)
+    T_e, st_e = g.align(tr.cloud, tgt, w.T_init, tr.params, tr.ws_align)  # eager, unseeded
+    np.testing.assert_array_equal(T_e, T_ref)
+    assert st_e["iters"] == st_ref["iters"] and st_e["n_inliers"] == st_ref["n_inliers"]
+    s = torch.cuda.Stream()
+    T0 = torch.from_numpy(w.T_init.reshape(-1).copy()).to(DEV)
+    with torch.cuda.stream(s):
+        tr.d_T.copy_(T0)
+        tr.step_async(depth, tgt)  # warm
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        tr.step_async(depth, tgt)
+    for _ in range(2):
+        tr.d_T.copy_(T0)
+        graph.replay()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(tr.d_T.cpu().numpy().reshape(4, 4), T_ref)
+        st = g.decode_stats(tr.d_stats)
+        assert st["iters"] == st_ref["iters"] and st["n_inliers"] == st_ref["n_inliers"]
+
+
 # ----------------------------------------------------------------------------------------- C5
 def test_sequence_tracking(g):
     """C5-style: a 30 Hz synthetic sequence tracked with the device-side constant-velocity init

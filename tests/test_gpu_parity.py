@@ -494,13 +494,14 @@ def test_align_per_iteration_tum(g, tum, stride, iters):
     assert _iter_parity(S, rec.iterations(), 0.1, f"tum s={stride}") == iters
 
 
-def test_align_per_iteration_batch_frame(g, replica_setup):
-    """N2: frame 0 of a 3-frame batch (the others: perturbed poses of the same frame)."""
+@pytest.mark.parametrize("B", [3, 8])
+def test_align_per_iteration_batch_frame(g, replica_setup, B):
+    """N2: frame 0 of a B-frame batch (the others: perturbed poses of the same frame); B = 3 runs
+    k_align_batch, B = 8 the flat loop over the frames."""
     S = replica_setup
     w = S["w"]
     src = S["src"]
-    B = 3
-    inits = [w.T_init, synth.perturb_pose(w.T_gt, 31), synth.perturb_pose(w.T_gt, 32)]
+    inits = [w.T_init] + [synth.perturb_pose(w.T_gt, 31 + b) for b in range(B - 1)]
     d_T = t(np.stack([np.ascontiguousarray(T, np.float64).reshape(16) for T in inits]))
     d_stats = torch.zeros((B, 32), dtype=torch.uint8, device=DEV)
     ws = [g.align_workspace(src.cap) for _ in range(B)]
@@ -895,15 +896,16 @@ def test_map_incremental_equals_rebuild(g):
     assert sa["n_inliers"] == sb["n_inliers"]
 
 
-def test_align_batch(g):
-    """N2: B = 4 frames of a sequence in one BatchTracker step (concurrent A1-A4 streams + one
-    k_align_batch launch) give the poses single-frame tracking gives (same algorithm; only the
-    grouping of the H/b partial sums differs) and, for a frame checked against the oracle from the
-    same initial pose, the oracle's pose within 1e-5 rad / 1e-5 m."""
-    seq = synth.make_sequence(2, 5, "replica", M=300_000)
+@pytest.mark.parametrize("B", [4, 8])
+def test_align_batch(g, B):
+    """N2: B frames of a sequence in one BatchTracker step (concurrent A1-A4 streams + one
+    k_align_batch launch for B = 4, the flat loop over the frames for B = 8) give the poses
+    single-frame tracking gives (same algorithm; only the grouping of the H/b partial sums differs)
+    and, for a frame checked against the oracle from the same initial pose, the oracle's pose
+    within 1e-5 rad / 1e-5 m."""
+    seq = synth.make_sequence(2, B + 1, "replica", M=300_000)
     rows = synth.render_sequence_rows(seq, DEV)
     K = seq.K
-    B = 4
     prm = g.align_params(max_iters=30, max_corr_dist=0.1)
     tgt = g.build_target(t(seq.means), t(seq.quats), t(seq.scales))
     init = np.stack([synth.perturb_pose(seq.T_gt[1 + b], 20 + b, 2.0, 0.03) for b in range(B)])
@@ -990,6 +992,32 @@ def test_align_lm_pose(g, c1_setup, replica_setup, lam0):
     assert abs(st["iters"] - ref["iters"]) <= 1 and st["n_inliers"] == ref["n_inliers"]
     gn, _ = g.align(R["src"], R["tgt"], w.T_init, g.align_params(max_iters=30, max_corr_dist=0.1))
     assert rot_angle(Tg[:3, :3], gn[:3, :3]) <= 1e-5 and np.linalg.norm(Tg[:3, 3] - gn[:3, 3]) <= 1e-5
+
+
+def test_align_flat_path_matches_persistent_and_oracle(g, replica_setup):
+    """The flat GN loop (chosen for clouds whose capacity exceeds the persistent grid) on the
+    Replica frame copied into a 120k-capacity cloud: GN and LM poses equal the persistent kernel's
+    within 1e-6 (as the frame batches: only the grouping of the H/b sums differs, and both stop
+    at an update below eps = 1e-6; measured 2e-8 rad), the same iteration and inlier counts,
+    and the oracle's LM pose within 1e-5 rad / 1e-5 m."""
+    R = replica_setup
+    w = R["w"]
+    src = R["src"]
+    n = src.n()
+    big = g.Cloud.empty(120_000)
+    for a, b in ((big.pos, src.pos), (big.cov_a, src.cov_a), (big.cov_b, src.cov_b)):
+        a[:n] = b[:n]
+    big.d_n.copy_(src.d_n)
+    assert big.cap > 148 * 384
+    for solver in (g.SOLVER_GN, g.SOLVER_LM):
+        p = g.align_params(max_iters=30, max_corr_dist=0.1, solver=solver)
+        Tp, stp = g.align(src, R["tgt"], w.T_init, p)
+        Tf, stf = g.align(big, R["tgt"], w.T_init, p)
+        assert rot_angle(Tf[:3, :3], Tp[:3, :3]) < 1e-6 and np.abs(Tf[:3, 3] - Tp[:3, 3]).max() < 1e-6
+        assert stf["iters"] == stp["iters"] and stf["n_inliers"] == stp["n_inliers"] and stf["status"] == stp["status"]
+    ref = oracle.align(R["xyz"], R["ocs"], R["txyz"], R["oct"], w.T_init, max_iters=30, max_corr_dist=0.1,
+                       use_tree=True, tree=R["tree"], solver=1, lm_lambda0=1e-4)
+    assert rot_angle(Tf[:3, :3], ref["T"][:3, :3]) <= 1e-5 and np.linalg.norm(Tf[:3, 3] - ref["T"][:3, 3]) <= 1e-5
 
 
 @pytest.mark.parametrize("h", [0.01, 0.03, 0.1])

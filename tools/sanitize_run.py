@@ -1,6 +1,6 @@
 """Workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck): C1 and the Replica
 bench frame through every entry point of the hot path, eagerly (no graphs, so each kernel launch
-is checked on its own).  python tools/sanitize_run.py [c1|replica|all]"""
+is checked on its own).  python tools/sanitize_run.py [c1|map|replica|all]"""
 import os
 import sys
 
@@ -37,6 +37,15 @@ def frame(depth, K, stride, tgt, T0, label):
     B = 2
     dTb = dT.repeat(B)
     g.align_batch_async([ci] * B, tgt, dTb.view(B, 16), torch.zeros((B, 32), dtype=torch.uint8, device=dev), p)
+    # frame batch through the flat loop (B >= 6) and one large-capacity cloud (the flat loop)
+    B = 6
+    g.align_batch_async([ci] * B, tgt, dT.repeat(B).view(B, 16), torch.zeros((B, 32), dtype=torch.uint8, device=dev), p)
+    big = g.Cloud.empty(60_000)
+    n = int(ci.d_n.item())
+    for a_, b_ in ((big.pos, ci.pos), (big.cov_a, ci.cov_a), (big.cov_b, ci.cov_b)):
+        a_[:n] = b_[:n]
+    big.d_n.copy_(ci.d_n)
+    g.align(big, tgt, T0, p)
     tr = g.Tracker(H, W, Kt, stride=stride)
     tr.track(d, tgt, T0)
     torch.cuda.synchronize()
@@ -48,6 +57,14 @@ def main():
     if which in ("c1", "all"):
         w = synth.make_c1(1)
         frame(w.depth, w.K, 1, None, np.eye(4), "c1")
+    if which in ("map", "all"):  # the brick kNN over a map-shaped cloud with floating outliers
+        dev = torch.device("cuda")
+        scene = synth.make_scene(1004)
+        means, _, _, ell = synth.sample_map(scene, 200_000, 4004)
+        c = g.Cloud.from_points(torch.from_numpy(means).to(dev))
+        g.covariances(c.pos, c.d_n, 20, g.REG_ELLIPSE, 1e-3, 3.4 * ell, 3, c.cov_a, c.cov_b)
+        torch.cuda.synchronize()
+        print("map: n=200000")
     if which in ("replica", "all"):
         w = synth.make_frame_workload(2, "replica", M=200_000, stride=4)
         dev = torch.device("cuda")

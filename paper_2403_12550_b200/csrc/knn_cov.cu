@@ -1284,14 +1284,14 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
     const float H = g.h0, R = kBrickHalo * g.h0;
     const float4 kSentinel = make_float4(__int_as_float(0x7fc00000), 0.f, 0.f, 0.f);  // NaN: never listed
     // a contiguous range of the brick list per warp (no work counter: a fetch would be one more
-    // dependent round trip per brick); the next record and the first probe of the next brick's 27
-    // neighbour cells are issued ahead, so their latency overlaps the staging / the round
+    // dependent round trip per brick), taken through a window of 32 records (one per lane): each
+    // group picks, among the untaken, the first brick whose queries still fit the round (bin
+    // packing: ~31 of 32 lanes busy instead of ~25 in list order); the first hash probe of the
+    // next likely brick's 27 neighbour cells is issued ahead, so it overlaps the staging / round
     const uint32_t W = gridDim.x * kBrickWarps, wg = blockIdx.x * kBrickWarps + wid;
     const uint32_t p1 = (uint32_t)((unsigned long long)nb * (wg + 1) / W);
-    uint32_t p = (uint32_t)((unsigned long long)nb * wg / W);
+    uint32_t wb = (uint32_t)((unsigned long long)nb * wg / W);
     const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-    uint4 rec = p < p1 ? __ldg(b.bricks + p) : zero4;
-    uint4 recn = p + 1 < p1 ? __ldg(b.bricks + p + 1) : zero4;
     auto nb_key = [&](const uint4 &r) {  // this lane's neighbour cell of brick r (own cell: lane 0)
         const unsigned long long key = ((unsigned long long)r.w << 32) | r.z;
         const int l = lane < 27 ? lane : 0;
@@ -1310,23 +1310,49 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
         if (k0 == kEmptyKey) return make_uint2(0u, 0u);
         return cell_lookup(g.table, g.mask, want);  // (collision: probe on; the scan restarts at the home slot)
     };
-    uint4 probe = p < p1 ? probe_first(rec) : zero4;
+    auto wrec_of = [&](const uint4 &wr, int c) {
+        return make_uint4(__shfl_sync(kFull, wr.x, c), __shfl_sync(kFull, wr.y, c), __shfl_sync(kFull, wr.z, c),
+                          __shfl_sync(kFull, wr.w, c));
+    };
+    uint4 wrec = wb + lane < p1 ? __ldg(b.bricks + wb + lane) : zero4;
+    unsigned avail = __ballot_sync(kFull, wb + lane < p1);
+    uint4 probe = zero4;
+    int probe_for = -1;  // window slot whose first probe is in flight
+    if (avail) {
+        probe_for = 0;
+        probe = probe_first(wrec_of(wrec, 0));
+    }
+    // at least one untaken brick in the window, reloading it when used up (false: range done)
+    auto ensure = [&]() {
+        while (avail == 0u && wb + 32u < p1) {
+            wb += 32u;
+            wrec = wb + lane < p1 ? __ldg(b.bricks + wb + lane) : zero4;
+            avail = __ballot_sync(kFull, wb + lane < p1);
+            probe_for = -1;
+        }
+        return avail != 0u;
+    };
     bool have_se = false;
+    int se_for = -1;
     uint2 se = make_uint2(0u, 0u);
     uint32_t incl = 0u, total = 0u;
-    while (p < p1) {
+    while (ensure()) {
         // ---- a group: bricks staged back to back while their queries fit one round.  Lane j
         // keeps brick j's record: first point, first query lane, candidate offset and count, cell
         int nbr = 0, gq = 0, gnc = 0;
         uint32_t qmask = 0u;
         uint32_t my_start = 0u;
         int my_qs = 0, my_off = 0, my_nc = 0, my_c0 = 0, my_c1 = 0, my_c2 = 0;
-        while (p < p1) {
+        while (ensure()) {
+            const int room = 32 - gq;
+            const unsigned fit = __ballot_sync(kFull, ((avail >> lane) & 1u) && (nbr == 0 || (int)wrec.y <= room));
+            if (!fit) break;
+            const int c = __ffs(fit) - 1;
+            const uint4 rec = wrec_of(wrec, c);
             const int cnt = (int)rec.y;
-            if (nbr > 0 && gq + cnt > 32) break;  // (the probe of this brick stays in flight over the round)
-            if (!have_se) {
+            if (!(have_se && se_for == c)) {
                 // the 27 bricks (own first): (start, count) one per lane, their prefix and total
-                se = probe_finish(probe, rec);
+                se = probe_finish(probe_for == c ? probe : probe_first(rec), rec);
                 incl = se.y;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -1335,9 +1361,11 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
                 }
                 total = __shfl_sync(kFull, incl, 31);
                 have_se = true;
+                se_for = c;
             }
             if (nbr > 0 && gnc + (int)total + 1 > kBrickCap) break;  // (total bounds the staged count)
             have_se = false;
+            avail &= ~(1u << c);
             const unsigned long long key = ((unsigned long long)rec.w << 32) | rec.z;
             const int c0 = (int)((key >> 40) & 0xFFFFFull) - kCoordOff, c1 = (int)((key >> 20) & 0xFFFFFull) - kCoordOff,
                       c2 = (int)(key & 0xFFFFFull) - kCoordOff;
@@ -1346,6 +1374,13 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
             __syncwarp();
             if (se.y) scell[__popc(ne & ((1u << lane) - 1u))] = make_uint2(se.x, excl);
             __syncwarp();
+            // the next likely brick (the first untaken): its probe goes out now
+            if (avail) {
+                probe_for = __ffs(avail) - 1;
+                probe = probe_first(wrec_of(wrec, probe_for));
+            } else {
+                probe_for = -1;
+            }
             const float elo0 = (float)c0 * H - R, elo1 = (float)c1 * H - R, elo2 = (float)c2 * H - R;
             const float ehi0 = (float)(c0 + 1) * H + R, ehi1 = (float)(c1 + 1) * H + R, ehi2 = (float)(c2 + 1) * H + R;
             // records of the 27 cells scanned as one flattened range, 4 x 32 loads in flight at once
@@ -1391,13 +1426,9 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
             gq += cnt;
             gnc += over ? 0 : nc + 1;
             ++nbr;
-            // advance: the next record is in registers, the one after it and the next probe go out now
-            ++p;
-            rec = recn;
-            recn = p + 1 < p1 ? __ldg(b.bricks + p + 1) : zero4;
-            probe = p < p1 ? probe_first(rec) : zero4;
             if (cnt > 32 || over) break;  // a big brick runs alone (several rounds)
         }
+        if (nbr == 0) break;
         __syncwarp();
         // ---- the group's queries, one per lane (several rounds only for a lone big brick)
         for (int r0 = 0; r0 < gq; r0 += 32) {

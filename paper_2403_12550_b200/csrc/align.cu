@@ -549,6 +549,9 @@ __device__ __forceinline__ void k3(const double *T, float x, float y, float z, d
     q2 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(T[8], xd), __dmul_rn(T[9], yd)), __dmul_rn(T[10], zd)), T[11]);
 }
 
+#ifndef GSICP_TERMS_STRUCTURED
+#define GSICP_TERMS_STRUCTURED 1
+#endif
 // Eq. 1 terms of one valid pair (binary64).  Returns false if Sigma is not positive definite.
 __device__ __forceinline__ bool pair_terms(const double *T, double q0, double q1, double q2, float4 ca, float4 cb,
                                            float4 m, float4 ta, float4 tb, double *acc) {
@@ -577,6 +580,46 @@ __device__ __forceinline__ bool pair_terms(const double *T, double q0, double q1
     const double id = 1.0 / det;
     const double M[3][3] = {{A00 * id, A01 * id, A02 * id}, {A01 * id, A11 * id, A12 * id}, {A02 * id, A12 * id, A22 * id}};
     const double d[3] = {(double)m.x - q0, (double)m.y - q1, (double)m.z - q2};
+#if GSICP_TERMS_STRUCTURED
+    // J = [A | -I] with A = -[q]x (columns (0, q2, -q1), (-q2, 0, q0), (q1, -q0, 0)): the products
+    // with J's literal zeros and -1 written out (IEEE arithmetic cannot drop x * 0.0 by itself),
+    // H = [[A^T M A, -A^T M], [-M A, M]], b = [A^T M d; -M d] — the same sums without the zero terms
+    double MA[3][3], AtM[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        MA[r][0] = M[r][1] * q2 - M[r][2] * q1;
+        MA[r][1] = M[r][2] * q0 - M[r][0] * q2;
+        MA[r][2] = M[r][0] * q1 - M[r][1] * q0;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {  // (A^T M)[r][c] = sum_k A[k][r] M[k][c]
+        AtM[0][c] = q2 * M[1][c] - q1 * M[2][c];
+        AtM[1][c] = q0 * M[2][c] - q2 * M[0][c];
+        AtM[2][c] = q1 * M[0][c] - q0 * M[1][c];
+    }
+    double AtMA[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        AtMA[0][c] = q2 * MA[1][c] - q1 * MA[2][c];
+        AtMA[1][c] = q0 * MA[2][c] - q2 * MA[0][c];
+        AtMA[2][c] = q1 * MA[0][c] - q0 * MA[1][c];
+    }
+    const double Md[3] = {M[0][0] * d[0] + M[0][1] * d[1] + M[0][2] * d[2], M[1][0] * d[0] + M[1][1] * d[1] + M[1][2] * d[2],
+                          M[2][0] * d[0] + M[2][1] * d[1] + M[2][2] * d[2]};
+    int t = 0;
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = r; c < 6; ++c)
+            acc[t++] += r < 3 ? (c < 3 ? AtMA[r][c] : -AtM[r][c - 3]) : M[r - 3][c - 3];
+    acc[21] += q2 * Md[1] - q1 * Md[2];
+    acc[22] += q0 * Md[2] - q2 * Md[0];
+    acc[23] += q1 * Md[0] - q0 * Md[1];
+    acc[24] -= Md[0];
+    acc[25] -= Md[1];
+    acc[26] -= Md[2];
+    acc[27] += d[0] * Md[0] + d[1] * Md[1] + d[2] * Md[2];
+#else
     const double J[3][6] = {{0.0, -q2, q1, -1.0, 0.0, 0.0}, {q2, 0.0, -q0, 0.0, -1.0, 0.0}, {-q1, q0, 0.0, 0.0, 0.0, -1.0}};
     double MJ[3][6], Md[3];
 #pragma unroll
@@ -593,6 +636,7 @@ __device__ __forceinline__ bool pair_terms(const double *T, double q0, double q1
 #pragma unroll
     for (int r = 0; r < 6; ++r) acc[21 + r] += J[0][r] * Md[0] + J[1][r] * Md[1] + J[2][r] * Md[2];
     acc[27] += d[0] * Md[0] + d[1] * Md[1] + d[2] * Md[2];
+#endif
     acc[28] += 1.0;
     return true;
 }

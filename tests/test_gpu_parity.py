@@ -283,6 +283,28 @@ def test_knn_cov_degenerate_clouds(g):
             _cov_check(g, xyz, pos, d_n, mode=mode, cell0=0.02, levels=2)
 
 
+def test_knn_cov_brick_edge_cases(g):
+    """The brick kernel's corner paths against the oracle (every query, bit-exact lists): a
+    brick holding more points than one 32-lane round (a 70-point blob: a lone brick over several
+    rounds) and one holding more than its query list (600 points in one cell), a staging
+    overflow (a 27-brick neighbourhood beyond the 448-candidate buffer), isolated points with fewer
+    than k points in their 27 bricks, and exact-distance ties on a lattice crossing brick faces."""
+    rng = np.random.default_rng(77)
+    plane = np.concatenate([rng.uniform(-0.3, 0.3, (6000, 2)), np.zeros((6000, 1))], 1)
+    blob = rng.normal(0.0, 0.002, (600, 3)) + np.array([0.05, 0.05, 0.0])
+    blob2 = rng.normal(0.0, 0.0015, (70, 3)) + np.array([-0.2, 0.1, 0.5])  # one brick, several rounds
+    far = rng.uniform(-2.0, 2.0, (40, 3)) + np.array([0.0, 0.0, 3.0])
+    lat = np.concatenate([np.stack(np.meshgrid(np.arange(12), np.arange(12)), -1).reshape(-1, 2) * 0.01 + 0.4,
+                          np.full((144, 1), 0.2)], 1)
+    xyz = np.concatenate([plane, blob, blob2, far, lat]).astype(np.float32)
+    n = xyz.shape[0]
+    pos = torch.zeros((n, 4), dtype=torch.float32, device=DEV)
+    pos[:, :3] = t(xyz)
+    d_n = torch.tensor([n], dtype=torch.int32, device=DEV)
+    for cell0, levels in ((0.02, 3), (0.04, 2)):
+        _cov_check(g, xyz, pos, d_n, mode=oracle.ELLIPSE, cell0=cell0, levels=levels)
+
+
 @pytest.mark.parametrize("cell,levels,sample", [(2.5, 1, 300), (3.4, 3, 100_000), (6.5, 1, 300)])
 def test_knn_cov_map_c4_sampled(g, cell, levels, sample):
     """C4-style: kNN covariance of a 4e6-point map (sampled queries vs the oracle's exact kd-tree /

@@ -190,6 +190,9 @@ constexpr float kReuseMargin = 1e-5f;  // relative slack on every distance of th
 #ifndef GSICP_D2_FROM_ITER
 #define GSICP_D2_FROM_ITER 2
 #endif
+#ifndef GSICP_D2_SKIP_REPEAT
+#define GSICP_D2_SKIP_REPEAT 1
+#endif
 constexpr int kD2FromIter = GSICP_D2_FROM_ITER;
 // ... and only for queries within this many cells of their match: farther off the surface (noisy
 // depth) the second neighbour is nearly as close as the first, the reuse margin d2 - d1 vanishes
@@ -935,6 +938,7 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
     __shared__ int sQslot[kT];
     __shared__ float4 sQp[kT];
     __shared__ float sQd2[kT];
+    __shared__ unsigned char sQrep[kT];  // the point was queued in the previous iteration too
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = *a.d_n;
     if (tid < 12) sT[tid] = a.d_T[tid];
@@ -1075,6 +1079,7 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
                 sQbk[k] = nn.bk;
                 sQslot[k] = nn.slot;
                 sQp[k] = nn.p;
+                sQrep[k] = it > 0 && it <= 32 ? (unsigned char)((dbg_slow >> ((it - 1) & 31)) & 1) : 0;
             }
             dbg_slow |= (exact ? 0 : 1) << (it & 31);
             ++dbg_its;
@@ -1112,7 +1117,10 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
             const bool in_r = nn.slot >= 0 && nn.bk < a.r2;
             const float base = in_r ? sqrtf(__double2float_ru(nn.bk)) : a.r;
             float d2 = 0.f;
-            if (base < INFINITY && it >= kD2FromIter) {
+            // (a point queued again — a near-tie whose bound did not hold — gets it every other
+            // iteration only: its next reuse test is then unlikely to pass anyway)
+            const bool skip_d2 = GSICP_D2_SKIP_REPEAT && sQrep[k] && (it & 1);
+            if (base < INFINITY && it >= kD2FromIter && !skip_d2) {
                 const float rho = base * 1.25f + 0.25f * a.h;
                 NN n2;
                 warp_nn(a, sIdx, sBox, q, n2, lane, rho * rho, nn.slot);

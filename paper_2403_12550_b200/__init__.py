@@ -1072,15 +1072,21 @@ def track_sequence_mapping(tr: Tracker, gmap: GaussianMap, frames_rows: torch.Te
 
 class BatchTracker:
     """N2 throughput mode: B independent frames per step against one target.  Each frame's A1 and
-    A2-A4 run on a stream of its own (concurrently), then ONE k_align_batch launch runs the B GN
-    loops side by side (gsicp_align_batch_async); the whole step is one graph replay.  Frames are
-    written into self.rows[b] (sampled depth rows, as Tracker.rows)."""
+    A2-A4 run on a stream of its own (concurrently), then one batched GN loop runs the B frames
+    side by side (gsicp_align_batch_async: k_align_batch, or the flat loop for B >= FLAT_MIN_B);
+    the whole step is one graph replay.  Frames are written into self.rows[b] (sampled depth
+    rows, as Tracker.rows)."""
+
+    FLAT_MIN_B = 6  # (GSICP_FLAT_BATCH in align.cu)
 
     def __init__(self, B: int, H: int, W: int, K, stride: int = 4, params: AlignParams | None = None,
-                 device="cuda", **kw):
+                 device="cuda", seeds: bool | None = None, **kw):
         if not 1 <= B <= int(lib().gsicp_align_batch_max()):
             raise ValueError(f"B must be in [1, {lib().gsicp_align_batch_max()}]")
         self.B = B
+        # iteration-0 seeds per frame (gsicp_align_seed): None = only for batches below the flat
+        # loop's size (the flat loop spreads the iteration-0 hard queries over the GPU itself)
+        self.seeds = (B < self.FLAT_MIN_B) if seeds is None else bool(seeds)
         self.params = params or align_params()
         self.device = torch.device(device)
         self.trs = [Tracker(H, W, K, stride=stride, params=self.params, device=device, **kw) for _ in range(B)]
@@ -1104,7 +1110,8 @@ class BatchTracker:
             tr._backproject(None, sb, self.rows[b])
             # iteration-0 correspondences at the frame's pose (needs only the points), then A2-A4;
             # the frames' streams run concurrently
-            align_seed(tr.cloud, tgt, self.d_T[b], self.params, tr.ws_align, sb)
+            if self.seeds:
+                align_seed(tr.cloud, tgt, self.d_T[b], self.params, tr.ws_align, sb)
             tr._covariances(sb)
             self._joins[b].record(sb)
             s0.wait_event(self._joins[b])

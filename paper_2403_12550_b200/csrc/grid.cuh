@@ -5,6 +5,11 @@
 //           (atomicAdd on its count) and fold the point into the bbox
 //   alloc : per occupied slot reserve a contiguous range (warp-aggregated atomicAdd)
 //   scatter: write point (and covariance) records into their cell range
+// Multi-level grids of large clouds (capacity >= kTwoPhaseMin) are built in two phases: level 0
+// from the caller's points, then insert / alloc / scatter of the coarser levels from level 0's
+// cell-ordered records (a randomly ordered map otherwise gives every lane its own cell on every
+// level: no warp aggregation, scattered writes), their alloc walking the list of cells the
+// second insert created instead of the whole table (7 kernels).
 // The order of cells in memory and of points inside a cell is not deterministic, but every
 // consumer orders candidates by the canonical (key, index) pair, so results are.
 #pragma once
@@ -13,6 +18,7 @@
 namespace gsicp {
 
 constexpr int kGridCounters = kMaxLevels + 8;
+constexpr int kTwoPhaseMin = 1 << 18;  // clouds of >= this capacity: two-phase multi-level build (grid.cu)
 
 struct GridView {
     CellEntry *table;
@@ -23,6 +29,7 @@ struct GridView {
                              // as (x, y, z, original index bits)
     float4 *scov_a, *scov_b; // nullable: cell-ordered covariances (target grids)
     uint2 *slot_rank;        // [levels * cap]
+    uint32_t *cells;         // [levels * cap] occupied table slots in creation order (length in counters[kMaxLevels + 7])
     uint32_t *counters;      // [kMaxLevels] points allocated per level, then kGridCounters - kMaxLevels
                              // work / queue counters of the search kernels (all zeroed by the build)
     uint32_t *mark;          // nullable: one bit per table slot, zeroed by the build (tile kNN units)

@@ -442,39 +442,44 @@ def bench_gpu(args):
     # graph replay per frame (no host round trip), L2 flushed between frames; ATE vs the
     # generating trajectory.  Whole-job aligns/s = frames of all ranks / max-over-ranks time.
     seq_line = None
-    if args.seq_frames > 0:
+    sq = rows_all = tgt_s = None
+    if args.seq_frames > 0 or args.batch > 0:
         import synth
 
-        sq = synth.make_sequence(rank, args.seq_frames + 1, "replica", M=1_000_000)
+        # one synthetic sequence per rank serves C5 (frames 1..seq_frames) and N2 (frames 1..B)
+        sq = synth.make_sequence(rank, max(args.seq_frames, args.batch) + 1, "replica", M=1_000_000)
         rows_all = synth.render_sequence_rows(sq, dev)
         tgt_s = g.build_target(torch.from_numpy(sq.means).to(dev), torch.from_numpy(sq.quats).to(dev),
                                torch.from_numpy(sq.scales).to(dev))
         Ks = sq.K
+    if args.seq_frames > 0:
         tr_s = g.Tracker(Ks.H, Ks.W, (Ks.fx, Ks.fy, Ks.cx, Ks.cy), stride=sq.stride, params=params, device=dev)
-        T_est, ms_s = g.track_sequence(tr_s, tgt_s, rows_all, sq.T_gt[0], flush=flush)
+        T_est, ms_s = g.track_sequence(tr_s, tgt_s, rows_all[:args.seq_frames + 1], sq.T_gt[0], flush=flush)
         seq_total = max_over_ranks(float(ms_s.sum()), dist, dev)
         seq_line = {"workload": f"C5: {args.seq_frames}-frame Replica-shaped 30 Hz sequence per rank "
                                 "(Lissajous path, 1e6-Gaussian map of its room), constant-velocity init",
                     "frames_per_rank": args.seq_frames, "aligns_per_s": job_throughput(args.seq_frames, ws, seq_total),
-                    "ms_per_frame_mean": float(ms_s.mean()), **synth.trajectory_error(T_est, sq.T_gt[1:])}
-        del rows_all, tr_s, tgt_s
+                    "ms_per_frame_mean": float(ms_s.mean()), **synth.trajectory_error(T_est, sq.T_gt[1:args.seq_frames + 1])}
+        del tr_s
 
-    # N2 throughput mode: B copies of the workload frame (B different initial poses) per step —
-    # concurrent A1-A4 streams + one k_align_batch launch, one graph replay, L2 flushed per step
+    # N2 throughput mode: B distinct frames of the rank's sequence per step (frames 1..B, each from
+    # a perturbed ground-truth pose) — A1-A4 on B concurrent streams, then one batched GN launch
+    # (k_align_batch, or the flat GN loop over the frames for B >= 6), one graph replay, L2 flushed
+    # per step.  The align stage's span (kernel timer events in the graph) gives its algorithmic
+    # bandwidth: 104 B per pair-iteration x the frames' points x their iterations.
     batch_line = None
     if args.batch > 0:
-        import synth
-
         B = args.batch
-        bt = g.BatchTracker(B, K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=w.stride, params=params, device=dev)
-        bt.rows.copy_(torch.from_numpy(w.depth[::w.stride]).to(dev).expand(B, -1, -1))
-        init_b = np.stack([synth.perturb_pose(w.T_gt, 500 + b, 2.0, 0.03) for b in range(B)])
-        bt.track_rows(tgt, init_b)
-        gb = bt.graph(tgt)
+        bt = g.BatchTracker(B, Ks.H, Ks.W, (Ks.fx, Ks.fy, Ks.cx, Ks.cy), stride=sq.stride, params=params, device=dev)
+        bt.rows.copy_(rows_all[1:1 + B])
+        init_b = np.stack([synth.perturb_pose(sq.T_gt[1 + b], 500 + b, 2.0, 0.03) for b in range(B)])
+        bt.track_rows(tgt_s, init_b)
+        g.debug_kernel_timer(1)
+        gb = bt.graph(tgt_s)
         Tb0 = torch.from_numpy(init_b.reshape(B, 16)).to(dev)
         sb = torch.cuda.current_stream(dev)
         bt.d_T.copy_(Tb0)  # one eager (untimed) step: what ncu captures (graph nodes behind a
-        bt.step_async(tgt, sb)  # conditional node are not profilable)
+        bt.step_async(tgt_s, sb)  # conditional node are not profilable)
         torch.cuda.synchronize()
         nb = max(10, min(args.steps, 50))
         evb = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nb)]
@@ -485,14 +490,25 @@ def bench_gpu(args):
             gb.replay(sb)
             e1.record(sb)
         torch.cuda.synchronize()
+        ka_b = g.debug_kernel_time(g.KT_ALIGN)  # the last replay's align stage
+        g.debug_kernel_timer(False)
         b_total = max_over_ranks(sum(a.elapsed_time(b) for a, b in evb), dist, dev)
-        Tb, stb = bt.track_rows(tgt, init_b)
-        batch_line = {"workload": f"N2: {B} copies of the workload frame per step from {B} initial poses, one "
-                                  "k_align_batch launch (G/B blocks per frame), A1-A4 on B concurrent streams",
+        Tb, stb = bt.track_rows(tgt_s, init_b)
+        nb_pts = [tr.cloud.n() for tr in bt.trs]
+        algo_b = ALGO_BYTES_ALIGN * sum(n_ * max(1, s_["iters"]) for n_, s_ in zip(nb_pts, stb))
+        batch_line = {"workload": f"N2: {B} distinct frames of a Replica-shaped sequence per step (frames 1..{B}, "
+                                  "perturbed initial poses) vs its 1e6-Gaussian map; A1-A4 on B concurrent streams, "
+                                  "one batched GN launch",
                       "B": B, "aligns_per_s": job_throughput(nb * B, ws, b_total), "ms_per_step": b_total / nb,
-                      "iters": [s_["iters"] for s_ in stb],
-                      "max_trans_err_m": float(max(np.abs(Tb[b][:3, 3] - w.T_gt[:3, 3]).max() for b in range(B)))}
+                      "iters": [s_["iters"] for s_ in stb], "points": nb_pts,
+                      "max_trans_err_m": float(max(np.abs(Tb[b][:3, 3] - sq.T_gt[1 + b][:3, 3]).max() for b in range(B))),
+                      "align_ms": ka_b,
+                      "align_roofline": None if not ka_b else {
+                          "bound": "hbm", "achieved_gbs": algo_b / (ka_b / 1000) / 1e9,
+                          "frac": algo_b / (ka_b / 1000) / 1e9 / peaks()[0], "algo_bytes": algo_b,
+                          "note": "whole align stage of the step (GN loop of all B frames) timed by events around it"}}
         del bt
+    del sq, rows_all, tgt_s
 
     # kNN-cov Mpts/s over a 4e6-point map (C4), kernel stage only
     knn_mpts = None
@@ -604,7 +620,7 @@ def main():
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--seq-frames", type=int, default=120, help="C5 sequence frames per rank (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--batch", type=int, default=4, help="N2 frames per batched step (0: skip)")
+    ap.add_argument("--batch", type=int, default=8, help="N2 frames per batched step (0: skip)")
     ap.add_argument("--no-configs", dest="configs", action="store_false", help="skip the C2 / C3 objects")
     args = ap.parse_args()
     if args.impl == "reference":

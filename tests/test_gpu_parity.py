@@ -308,7 +308,7 @@ def test_knn_cov_brick_edge_cases(g):
 @pytest.mark.parametrize("cell,levels,sample", [(2.5, 1, 300), (3.4, 3, 100_000), (6.5, 1, 300)])
 def test_knn_cov_map_c4_sampled(g, cell, levels, sample):
     """C4-style: kNN covariance of a 4e6-point map (sampled queries vs the oracle's exact kd-tree /
-    brute force); levels=1 is the warp search of every point, (3.0, 3) the bench configuration."""
+    brute force); levels=1 is the warp search of every point, (3.4, 3) the bench configuration."""
     scene = synth.make_scene(1004)
     means, _, _, ell = synth.sample_map(scene, 4_000_000, 4004)
     pos = torch.zeros((means.shape[0], 4), dtype=torch.float32, device=DEV)

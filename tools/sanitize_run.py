@@ -58,13 +58,13 @@ def main():
         w = synth.make_c1(1)
         frame(w.depth, w.K, 1, None, np.eye(4), "c1")
     if which in ("map", "all"):  # the brick kNN over a map-shaped cloud with floating outliers
-        dev = torch.device("cuda")
+        dev = torch.device("cuda")  # (3e5 points: above kTwoPhaseMin, the two-phase grid build)
         scene = synth.make_scene(1004)
-        means, _, _, ell = synth.sample_map(scene, 200_000, 4004)
+        means, _, _, ell = synth.sample_map(scene, 300_000, 4004)
         c = g.Cloud.from_points(torch.from_numpy(means).to(dev))
         g.covariances(c.pos, c.d_n, 20, g.REG_ELLIPSE, 1e-3, 3.4 * ell, 3, c.cov_a, c.cov_b)
         torch.cuda.synchronize()
-        print("map: n=200000")
+        print("map: n=300000")
     if which in ("replica", "all"):
         w = synth.make_frame_workload(2, "replica", M=200_000, stride=4)
         dev = torch.device("cuda")

@@ -544,6 +544,126 @@ __device__ void warp_nn(const AlignArgs &a, const CellIndex &idx, const int *sb,
     }
 }
 
+#ifndef GSICP_ALIGN_FUSED
+#define GSICP_ALIGN_FUSED 1  // k_align's queue: one traversal for the 1-NN and the second-neighbour bound
+#endif
+// Fused 1-NN + second neighbour for a queued point whose warm start lies inside r (k_align's
+// late iterations: near-ties, the warm start is (almost) the 1-NN): ONE traversal of the cells
+// within sqrt(Bw) of q, Bw = rho_w^2 with rho_w the reuse radius of the warm start (>= that of the
+// 1-NN: the radius is monotone in the key), every target there ranked by (key64, index) with the
+// lane's best and second-best key kept in registers and one warp reduction at the end.  The best
+// is the exact 1-NN (closer than the warm start, so inside rho_w); k2, the second-best key, is
+// the nearest other target whenever that lies within rho_w — so min(sqrt(k2), rho) equals
+// warp_nn(rho^2, excl = 1-NN)'s bound.  nn in: the warm start; out: the 1-NN.
+__device__ __forceinline__ void warp_nn_top2(const AlignArgs &a, const CellIndex &idx, const int *sb, const Qry &q,
+                                             NN &nn, int lane, float Bw, double &k2) {
+    const QueryCell qc(q.x, q.y, q.z, a.h, a.inv_h);
+    const int *blo = sb, *bhi = sb + 3;
+    double lk1 = INFINITY, lk2 = INFINITY;
+    uint32_t li1 = 0xffffffffu, ls1 = 0;
+    float4 lp1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto scan = [&](bool valid, int dx, int dy, int dz) {
+        const uint2 se = valid ? idx.one(qc.c[0] + dx, qc.c[1] + dy, qc.c[2] + dz) : make_uint2(0u, 0u);
+        uint32_t incl = se.y;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t ctot = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t base = 0; base < ctot; base += 32) {
+            const uint32_t item = base + lane;
+            int l0 = 0, l1 = 31;
+#pragma unroll
+            for (int s = 0; s < 5; ++s) {
+                const int mid = (l0 + l1) >> 1;
+                if (__shfl_sync(0xffffffffu, incl, mid) > item) l1 = mid; else l0 = mid + 1;
+            }
+            const uint32_t c_incl = __shfl_sync(0xffffffffu, incl, l0);
+            const uint32_t c_start = __shfl_sync(0xffffffffu, se.x, l0);
+            const uint32_t c_cnt = __shfl_sync(0xffffffffu, se.y, l0);
+            if (item < ctot) {
+                const uint32_t slot = c_start + (item - (c_incl - c_cnt));
+                const float4 p = __ldg(a.tpos + slot);
+                const double ck = q.key(p);
+                const uint32_t ci = (uint32_t)__float_as_int(p.w);
+                if (ck < lk1 || (ck == lk1 && ci < li1)) {
+                    lk2 = lk1;
+                    lk1 = ck;
+                    li1 = ci;
+                    ls1 = slot;
+                    lp1 = p;
+                } else if (ck < lk2) {
+                    lk2 = ck;
+                }
+            }
+        }
+    };
+    auto in_box = [&](int dx, int dy, int dz) {
+        const int x = qc.c[0] + dx, y = qc.c[1] + dy, z = qc.c[2] + dz;
+        return x >= blo[0] && x <= bhi[0] && y >= blo[1] && y <= bhi[1] && z >= blo[2] && z <= bhi[2];
+    };
+    bool done = false;
+    for (int m = 1; m <= kWarpShells && !done; ++m) {
+        const int cnt = m == 1 ? 27 : shell_count(m);
+        for (int t0 = 0; t0 < cnt; t0 += 32) {
+            const int t = t0 + lane;
+            int dx = 0, dy = 0, dz = 0;
+            bool valid = t < cnt;
+            if (valid) {
+                if (m == 1) {
+                    if (t > 0) shell_cell(1, t - 1, dx, dy, dz);
+                } else {
+                    shell_cell(m, t, dx, dy, dz);
+                }
+                valid = in_box(dx, dy, dz) && qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2) <= Bw;
+            }
+            if (!__any_sync(0xffffffffu, valid)) continue;
+            scan(valid, dx, dy, dz);
+        }
+        done = Bw < qc.certified_key(m) || qc.covers(m, blo, bhi);
+    }
+    if (!done) {  // the rest of the ball: the box of offsets whose gaps fit Bw, outside the shells
+        int lo[3], hi[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) axis_range(qc, k, Bw, blo[k], bhi[k], lo[k], hi[k]);
+        const int nx = max(hi[0] - lo[0] + 1, 0), ny = max(hi[1] - lo[1] + 1, 0), nz = max(hi[2] - lo[2] + 1, 0);
+        const long long total = (long long)nx * ny * nz;
+        for (long long t0 = 0; t0 < total; t0 += 32) {
+            const long long t = t0 + lane;
+            int dx = 0, dy = 0, dz = 0;
+            bool valid = t < total;
+            if (valid) {
+                dx = lo[0] + (int)(t % nx);
+                dy = lo[1] + (int)((t / nx) % ny);
+                dz = lo[2] + (int)(t / ((long long)nx * ny));
+                valid = max(abs(dx), max(abs(dy), abs(dz))) > kWarpShells &&
+                        qc.gap2(dx, 0) + qc.gap2(dy, 1) + qc.gap2(dz, 2) <= Bw;
+            }
+            if (!__any_sync(0xffffffffu, valid)) continue;
+            scan(valid, dx, dy, dz);
+        }
+    }
+    double mk = lk1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mk = fmin(mk, shfl_f64(mk, lane ^ o));
+    const uint32_t mi = __reduce_min_sync(0xffffffffu, lk1 == mk ? li1 : 0xffffffffu);
+    const int src = __ffs(__ballot_sync(0xffffffffu, lk1 == mk && li1 == mi)) - 1;
+    double o2 = lane == src ? lk2 : lk1;  // every lane's best is "another target" except the winner's
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) o2 = fmin(o2, shfl_f64(o2, lane ^ o));
+    k2 = o2;
+    if (mk < INFINITY) {
+        nn.bk = mk;
+        nn.bi = mi;
+        nn.slot = (int)__shfl_sync(0xffffffffu, ls1, src);
+        nn.p.x = __shfl_sync(0xffffffffu, lp1.x, src);
+        nn.p.y = __shfl_sync(0xffffffffu, lp1.y, src);
+        nn.p.z = __shfl_sync(0xffffffffu, lp1.z, src);
+        nn.p.w = __shfl_sync(0xffffffffu, lp1.w, src);
+    }
+}
+
 // K3 transform: q_r = ((R_r0 x + R_r1 y) + R_r2 z) + t_r, binary64, no contraction (R15)
 __device__ __forceinline__ void k3(const double *T, float x, float y, float z, double &q0, double &q1, double &q2) {
     const double xd = x, yd = y, zd = z;
@@ -1111,20 +1231,33 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
             NN nn;
             nn.slot = sQslot[k];
             if (nn.slot >= 0) nn.set(sQbk[k], nn.slot, sQp[k]);
-            warp_nn(a, sIdx, sBox, q, nn, lane);
-            // a lower bound on every other target's distance (exact within rho), so that the
-            // following iterations can keep this answer while the query moves little
-            const bool in_r = nn.slot >= 0 && nn.bk < a.r2;
-            const float base = in_r ? sqrtf(__double2float_ru(nn.bk)) : a.r;
             float d2 = 0.f;
-            // (a point queued again — a near-tie whose bound did not hold — gets it every other
-            // iteration only: its next reuse test is then unlikely to pass anyway)
+            // (a point queued again — a near-tie whose bound did not hold — gets the second-neighbour
+            // bound every other iteration only: its next reuse test is then unlikely to pass anyway)
             const bool skip_d2 = GSICP_D2_SKIP_REPEAT && sQrep[k] && (it & 1);
-            if (base < INFINITY && it >= kD2FromIter && !skip_d2) {
-                const float rho = base * 1.25f + 0.25f * a.h;
-                NN n2;
-                warp_nn(a, sIdx, sBox, q, n2, lane, rho * rho, nn.slot);
-                d2 = fminf(n2.slot >= 0 ? sqrtf(__double2float_rd(n2.bk)) : INFINITY, rho) * (1.f - kReuseMargin);
+            // (only for warm starts within one cell of the query: a far one makes the single ball
+            // much larger than warp_nn's shrinking one — measured on the noisy C3 frames)
+            const bool fuse_ok = GSICP_ALIGN_FUSED && nn.bk < (double)a.h * (double)a.h;
+            if (fuse_ok && it >= kD2FromIter && !skip_d2 && nn.slot >= 0 && nn.bk < a.r2) {
+                // the 1-NN and the bound from one traversal around the warm start (inside r, so the
+                // 1-NN is too: rho below is the same as after a separate warp_nn)
+                const float rw = sqrtf(__double2float_ru(nn.bk)) * 1.25f + 0.25f * a.h;
+                double k2;
+                warp_nn_top2(a, sIdx, sBox, q, nn, lane, rw * rw, k2);
+                const float rho = sqrtf(__double2float_ru(nn.bk)) * 1.25f + 0.25f * a.h;
+                d2 = fminf(k2 < INFINITY ? sqrtf(__double2float_rd(k2)) : INFINITY, rho) * (1.f - kReuseMargin);
+            } else {
+                warp_nn(a, sIdx, sBox, q, nn, lane);
+                // a lower bound on every other target's distance (exact within rho), so that the
+                // following iterations can keep this answer while the query moves little
+                const bool in_r = nn.slot >= 0 && nn.bk < a.r2;
+                const float base = in_r ? sqrtf(__double2float_ru(nn.bk)) : a.r;
+                if (base < INFINITY && it >= kD2FromIter && !skip_d2) {
+                    const float rho = base * 1.25f + 0.25f * a.h;
+                    NN n2;
+                    warp_nn(a, sIdx, sBox, q, n2, lane, rho * rho, nn.slot);
+                    d2 = fminf(n2.slot >= 0 ? sqrtf(__double2float_rd(n2.bk)) : INFINITY, rho) * (1.f - kReuseMargin);
+                }
             }
             __syncwarp();  // every lane has read entry k (above) before lane 0 overwrites it
             if (lane == 0) {

@@ -1341,17 +1341,28 @@ __device__ __forceinline__ void align_body(const AlignArgs &a, const int bid, co
                 NN nn;
                 nn.slot = sQslot[k];
                 if (nn.slot >= 0) nn.set(sQbk[k], nn.slot, sQp[k]);
-                warp_nn(a, sIdx, sBox, q, nn, lane);
-                // the second-neighbour bound for the reuse of the next iterations (as resident points)
-                const bool in_r = nn.slot >= 0 && nn.bk < a.r2;
-                const float base = in_r ? sqrtf(__double2float_ru(nn.bk)) : a.r;
+                // the second-neighbour bound for the reuse of the next iterations (as resident
+                // points, the fused traversal for a near warm start inside r included)
                 float d2 = 0.f;
-                if (base < INFINITY && it >= kD2FromIter) {
-                    const float rho = base * 1.25f + 0.25f * a.h;
-                    NN n2;
-                    warp_nn(a, sIdx, sBox, q, n2, lane, rho * rho, nn.slot);
-                    d2 = fminf(n2.slot >= 0 ? sqrtf(__double2float_rd(n2.bk)) : INFINITY, rho) * (1.f - kReuseMargin);
+                if (GSICP_ALIGN_FUSED && it >= kD2FromIter && nn.slot >= 0 && nn.bk < a.r2 &&
+                    nn.bk < (double)a.h * (double)a.h) {
+                    const float rw = sqrtf(__double2float_ru(nn.bk)) * 1.25f + 0.25f * a.h;
+                    double k2;
+                    warp_nn_top2(a, sIdx, sBox, q, nn, lane, rw * rw, k2);
+                    const float rho = sqrtf(__double2float_ru(nn.bk)) * 1.25f + 0.25f * a.h;
+                    d2 = fminf(k2 < INFINITY ? sqrtf(__double2float_rd(k2)) : INFINITY, rho) * (1.f - kReuseMargin);
+                } else {
+                    warp_nn(a, sIdx, sBox, q, nn, lane);
+                    const bool in_r0 = nn.slot >= 0 && nn.bk < a.r2;
+                    const float base = in_r0 ? sqrtf(__double2float_ru(nn.bk)) : a.r;
+                    if (base < INFINITY && it >= kD2FromIter) {
+                        const float rho = base * 1.25f + 0.25f * a.h;
+                        NN n2;
+                        warp_nn(a, sIdx, sBox, q, n2, lane, rho * rho, nn.slot);
+                        d2 = fminf(n2.slot >= 0 ? sqrtf(__double2float_rd(n2.bk)) : INFINITY, rho) * (1.f - kReuseMargin);
+                    }
                 }
+                const bool in_r = nn.slot >= 0 && nn.bk < a.r2;
                 if (lane == 0) {
                     a.corr_ws[sQtid[k]] = in_r ? nn.slot : -2 - nn.slot;
                     a.reuse_ws[sQtid[k]] = make_float4(q.x, q.y, q.z, d2);

@@ -1182,6 +1182,9 @@ __global__ void k_img_hash_n(ImgArgs im, const int32_t *__restrict__ d_n, cudaGr
 // needs: the k-th key32t t, the entries below band_lo(t), and the band resolved in binary64.
 // Queries that fail the certificate (and bricks whose neighbourhood overflows the staging buffer)
 // go to a queue that the warp search finishes.
+#ifndef GSICP_BRICK_TAU0
+#define GSICP_BRICK_TAU0 1  // the list bound starts at the certificate's limit, not +inf
+#endif
 constexpr int kBrickWarps = 4;
 constexpr int kBrickCap = 448;     // staged candidates per warp (a group of bricks, + a sentinel each)
 constexpr float kBrickHalo = 0.95f;  // R / H (< 1: the box stays inside the 27 bricks with margin)
@@ -1448,6 +1451,24 @@ __global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, Brick
             // ---- one pass: list every candidate with key <= tau (lanes without a query: none)
             // tau and the list in the key32t domain (bit patterns: unsigned order == float order)
             uint32_t tau = ok ? 0x7f800000u : 0u, lmax = 0u;
+#if GSICP_BRICK_TAU0
+            if (ok) {
+                // the certificate below needs the k-th ball inside the expanded box: a k-th key above
+                // D^2 (D = the query's distance to the box faces) fails it whatever else is listed,
+                // so no candidate beyond band_hi(D^2) can matter — start the bound there (D rounded
+                // up generously: its binary64 test has margins of ~1e-5 relative)
+                const float qv[3] = {q.x, q.y, q.z};
+                const int cv[3] = {c0, c1, c2};
+                float D = INFINITY;
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    const float lo_ = (float)cv[ax] * H - R, hi_ = (float)(cv[ax] + 1) * H + R;
+                    D = fminf(D, fminf(qv[ax] - lo_, hi_ - qv[ax]));
+                }
+                const float Du = __fadd_ru(__fmul_ru(fmaxf(D, 0.f), 1.0001f), 1e-6f);
+                tau = __float_as_uint(brick_band_hi(__fmul_ru(Du, Du))) & kBrickKeyMask;
+            }
+#endif
             int m = 0, n_events = 0;
             // compaction of this lane's list: quarter-octave buckets below tau (or, while tau is open,
             // below the largest listed key), b* = the bucket of the k-th entry, tau lowered to

@@ -1186,16 +1186,25 @@ __global__ void k_img_hash_n(ImgArgs im, const int32_t *__restrict__ d_n, cudaGr
 #define GSICP_BRICK_TAU0 1  // the list bound starts at the certificate's limit, not +inf
 #endif
 constexpr int kBrickWarps = 4;
-constexpr int kBrickCap = 448;     // staged candidates per warp (a group of bricks, + a sentinel each)
+#ifndef GSICP_BRICK_CAP
+#define GSICP_BRICK_CAP 448
+#endif
+#ifndef GSICP_BRICK_L
+#define GSICP_BRICK_L 48
+#endif
+#ifndef GSICP_BRICK_BPS
+#define GSICP_BRICK_BPS 4
+#endif
+constexpr int kBrickCap = GSICP_BRICK_CAP;     // staged candidates per warp (a group of bricks, + a sentinel each)
 constexpr float kBrickHalo = 0.95f;  // R / H (< 1: the box stays inside the 27 bricks with margin)
-constexpr int kBrickL = 48;        // per-lane list capacity
+constexpr int kBrickL = GSICP_BRICK_L;        // per-lane list capacity
 constexpr int kBrickLx = 32;       // list entries of the final selection (a 32-bit mask)
 constexpr int kBrickU = 4;         // candidates between two capacity checks (the list keeps U free)
 constexpr uint32_t kBrickSlotMask = 0x1FFu;  // staged-candidate slot in the low bits of a list entry
 static_assert(kBrickCap < (int)kBrickSlotMask, "slot field");
 // per warp: staged candidates, packed list, 27-brick cell table (13.6 KB: 4 blocks / SM)
 constexpr int kBrickSmemPerWarp = kBrickCap * 16 + kBrickL * 32 * 4 + 32 * 8;
-constexpr int kBrickBlocksPerSm = 4;
+constexpr int kBrickBlocksPerSm = GSICP_BRICK_BPS;
 constexpr uint32_t kBrickKeyMask = ~kBrickSlotMask;
 constexpr float kBrickBand = 2e-4f;  // > 3 x (11 u + 2^-14)
 __device__ __forceinline__ float brick_band_hi(float t) { return __fadd_ru(__fmul_ru(t, 1.f + kBrickBand), 1e-36f); }
@@ -1271,7 +1280,7 @@ struct BrickArgs {
 };
 
 template <int K, bool SORT>
-__global__ void __launch_bounds__(kBrickWarps * 32) k_knn_brick(KnnArgs a, BrickArgs b) {
+__global__ void __launch_bounds__(kBrickWarps * 32, kBrickBlocksPerSm) k_knn_brick(KnnArgs a, BrickArgs b) {
     static_assert(K + kBrickU < kBrickLx, "list capacity");
     pdl_wait();
     pdl_launch_dependents();

@@ -317,6 +317,20 @@ def test_knn_cov_map_c4_sampled(g, cell, levels, sample):
     _cov_check(g, means, pos, d_n, cell0=cell * ell, levels=levels, sample=sample)
 
 
+def test_knn_cov_map_two_phase_full(g):
+    """A 3e5-point map (above the two-phase grid build's 2^18 capacity threshold: level 0 from the
+    randomly ordered points, levels 1-2 from level 0's cell-ordered records, their alloc over the
+    created-cell list) at the bench's brick grid (3.4 spacings x 3 levels): EVERY query's neighbour
+    list and covariance against the oracle (the floating outliers reach the coarse levels)."""
+    scene = synth.make_scene(1004)
+    means, _, _, ell = synth.sample_map(scene, 300_000, 4104)
+    assert means.shape[0] >= 1 << 18
+    pos = torch.zeros((means.shape[0], 4), dtype=torch.float32, device=DEV)
+    pos[:, :3] = t(means)
+    d_n = torch.tensor([means.shape[0]], dtype=torch.int32, device=DEV)
+    _cov_check(g, means, pos, d_n, cell0=3.4 * ell, levels=3)
+
+
 # ----------------------------------------------------------------------------------------- A5
 @pytest.mark.parametrize("mode,log", [(oracle.ELLIPSE, False), (oracle.PLANE, False), (oracle.NONE, True)])
 def test_build_target_covariances(g, mode, log):

@@ -546,6 +546,32 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn_epilogue(KnnArgs a) {
 //   * queries that fail the projection certificate (k-th radius too large for the window: depth
 //     edges, grazing surfaces, image periphery), or whose m exceeds the list, go to a queue that
 //     the grid search finishes (the hash is only built for them).
+// 16 byte counters in two registers (buckets 0-7, 8-15): add one to bucket b
+struct Hist16 {
+    unsigned long long lo = 0ull, hi = 0ull;
+    __device__ __forceinline__ void add(int b) {
+        const unsigned long long one = 1ull << (8 * (b & 7));
+        if (b < 8) lo += one; else hi += one;
+    }
+    // first bucket whose cumulative count reaches k (16 if none); *below = the count before it
+    __device__ __forceinline__ int select(int k, int &below) const {
+        constexpr unsigned long long C = 0x0101010101010101ull;  // byte prefix sums (< 256: no carries)
+        const unsigned long long pl = lo * C;
+        const unsigned long long ph = hi * C + (pl >> 56) * C;
+        const uint32_t w0 = (uint32_t)pl, w1 = (uint32_t)(pl >> 32), w2 = (uint32_t)ph, w3 = (uint32_t)(ph >> 32);
+        const uint32_t kk = (uint32_t)k * 0x01010101u;
+        const int ge = __popc(__vcmpgeu4(w0, kk)) + __popc(__vcmpgeu4(w1, kk)) + __popc(__vcmpgeu4(w2, kk)) +
+                       __popc(__vcmpgeu4(w3, kk));
+        const int bs = 16 - ge / 8;  // prefix sums are monotone: the bytes >= k are a suffix
+        const int bb = bs - 1;
+        const uint32_t wd = bb < 4 ? w0 : (bb < 8 ? w1 : (bb < 12 ? w2 : w3));
+        below = bs == 0 ? 0 : (int)((wd >> (8 * (bb & 3))) & 0xFFu);
+        return bs;
+    }
+};
+#ifndef GSICP_IMG_SUBRANK
+#define GSICP_IMG_SUBRANK 1  // boundary-group rank within a 1/32-octave sub-bucket
+#endif
 constexpr int kImgTX = 32, kImgTY = 4, kImgThreads = kImgTX * kImgTY;
 constexpr int kImgList = 32;
 constexpr int kImgBuckets = 32;
@@ -725,12 +751,35 @@ __global__ void __launch_bounds__(kImgThreads, 4) k_knn_image(KnnArgs a, ImgArgs
             // (filled: [0, nlo) and [kImgList - nbd, kImgList)).
             const int r = k - nlo;
             float t = 0.f;
+#if GSICP_IMG_SUBRANK
+            // the boundary group split by the next 3 mantissa bits (sub-buckets monotone in the
+            // key; 0 / 9: band entries below / above b*): the r-th key lies in the first sub-bucket
+            // whose cumulative count reaches r, and is ranked among that sub-bucket's few entries
+            const int sub0 = ((base + bstar) << 3) - 1;
+            auto sub_of = [&](float key) { return min(max((int)(__float_as_uint(key) >> 18) - sub0, 0), 9); };
+            Hist16 hs;
+            for (int j = kImgList - nbd; j < kImgList; ++j) hs.add(sub_of(ki_key(list[j][tid])));
+            int sbelow;
+            const int sb = hs.select(r, sbelow);
+            const int r2 = r - sbelow;
+            for (int j = kImgList - nbd; j < kImgList; ++j) {
+                const unsigned long long e = list[j][tid];
+                if (sub_of(ki_key(e)) != sb) continue;
+                int rank = 0;
+                for (int l = kImgList - nbd; l < kImgList; ++l) {
+                    const unsigned long long o = list[l][tid];
+                    rank += (o < e && sub_of(ki_key(o)) == sb) ? 1 : 0;
+                }
+                if (rank == r2 - 1) t = ki_key(e);
+            }
+#else
             for (int j = kImgList - nbd; j < kImgList; ++j) {
                 const unsigned long long e = list[j][tid];
                 int rank = 0;
                 for (int l = kImgList - nbd; l < kImgList; ++l) rank += list[l][tid] < e ? 1 : 0;
                 if (rank == r - 1) t = ki_key(e);
             }
+#endif
             const float blo = band_lo(t), bhi = band_hi(t);
             const uint32_t filled = (nlo >= 32 ? ~0u : ((1u << nlo) - 1u)) | (nbd == 0 ? 0u : ~0u << (kImgList - nbd));
             uint32_t sel = 0u, band = 0u;
@@ -1182,6 +1231,9 @@ __global__ void k_img_hash_n(ImgArgs im, const int32_t *__restrict__ d_n, cudaGr
 // needs: the k-th key32t t, the entries below band_lo(t), and the band resolved in binary64.
 // Queries that fail the certificate (and bricks whose neighbourhood overflows the staging buffer)
 // go to a queue that the warp search finishes.
+#ifndef GSICP_BRICK_SUBRANK
+#define GSICP_BRICK_SUBRANK 1  // boundary-bucket rank within a 1/64-octave sub-bucket
+#endif
 #ifndef GSICP_BRICK_TAU0
 #define GSICP_BRICK_TAU0 1  // the list bound starts at the certificate's limit, not +inf
 #endif
@@ -1224,29 +1276,6 @@ __device__ __forceinline__ float brick_key(float ax, float ay, float az, float b
     const float dx = ax - bx, dy = ay - by, dz = az - bz;
     return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
 }
-// 16 byte counters in two registers (buckets 0-7, 8-15): add one to bucket b
-struct Hist16 {
-    unsigned long long lo = 0ull, hi = 0ull;
-    __device__ __forceinline__ void add(int b) {
-        const unsigned long long one = 1ull << (8 * (b & 7));
-        if (b < 8) lo += one; else hi += one;
-    }
-    // first bucket whose cumulative count reaches k (16 if none); *below = the count before it
-    __device__ __forceinline__ int select(int k, int &below) const {
-        constexpr unsigned long long C = 0x0101010101010101ull;  // byte prefix sums (< 256: no carries)
-        const unsigned long long pl = lo * C;
-        const unsigned long long ph = hi * C + (pl >> 56) * C;
-        const uint32_t w0 = (uint32_t)pl, w1 = (uint32_t)(pl >> 32), w2 = (uint32_t)ph, w3 = (uint32_t)(ph >> 32);
-        const uint32_t kk = (uint32_t)k * 0x01010101u;
-        const int ge = __popc(__vcmpgeu4(w0, kk)) + __popc(__vcmpgeu4(w1, kk)) + __popc(__vcmpgeu4(w2, kk)) +
-                       __popc(__vcmpgeu4(w3, kk));
-        const int bs = 16 - ge / 8;  // prefix sums are monotone: the bytes >= k are a suffix
-        const int bb = bs - 1;
-        const uint32_t wd = bb < 4 ? w0 : (bb < 8 ? w1 : (bb < 12 ? w2 : w3));
-        below = bs == 0 ? 0 : (int)((wd >> (8 * (bb & 3))) & 0xFFu);
-        return bs;
-    }
-};
 // 8 byte counters in one register (the list compaction: quarter-octave buckets, 2 octaves)
 struct Hist8 {
     unsigned long long c = 0ull;
@@ -1537,12 +1566,34 @@ __global__ void __launch_bounds__(kBrickWarps * 32, kBrickBlocksPerSm) k_knn_bri
                 for (int s = 0; s < m; ++s) bd |= (bucket16(lpk[s][lane], tau) == bs ? 1u : 0u) << s;
                 const int r = k - nlo;  // t: the r-th smallest (key32t, slot) of the boundary bucket
                 uint32_t t = 0u;
+#if GSICP_BRICK_SUBRANK
+                {   // split by the next 3 mantissa bits (monotone; clamped ends), rank inside the
+                    // sub-bucket holding the r-th entry only (cf. the image kernel)
+                    const int sub0 = (((int)(tau >> 20) - 15 + bs) << 3) - 1;
+                    auto sub_of = [&](uint32_t v) { return min(max((int)(v >> 17) - sub0, 0), 9); };
+                    Hist16 hs;
+                    for (uint32_t f = bd; f; f &= f - 1) hs.add(sub_of(lpk[__ffs(f) - 1][lane]));
+                    int sbelow;
+                    const int sb = hs.select(r, sbelow);
+                    const int r2 = r - sbelow;
+                    uint32_t bs2 = 0u;
+                    for (uint32_t f = bd; f; f &= f - 1)
+                        bs2 |= (sub_of(lpk[__ffs(f) - 1][lane]) == sb ? 1u : 0u) << (__ffs(f) - 1);
+                    for (uint32_t f = bs2; f; f &= f - 1) {
+                        const uint32_t vs = lpk[__ffs(f) - 1][lane];
+                        int rank = 0;
+                        for (uint32_t f2 = bs2; f2; f2 &= f2 - 1) rank += lpk[__ffs(f2) - 1][lane] < vs ? 1 : 0;
+                        if (rank == r2 - 1) t = vs & kBrickKeyMask;
+                    }
+                }
+#else
                 for (uint32_t f = bd; f; f &= f - 1) {
                     const uint32_t vs = lpk[__ffs(f) - 1][lane];
                     int rank = 0;
                     for (uint32_t f2 = bd; f2; f2 &= f2 - 1) rank += lpk[__ffs(f2) - 1][lane] < vs ? 1 : 0;
                     if (rank == r - 1) t = vs & kBrickKeyMask;
                 }
+#endif
                 const float blo = brick_band_lo(__uint_as_float(t)), bhi = brick_band_hi(__uint_as_float(t));
                 ok = (__float_as_uint(bhi) & kBrickKeyMask) <= tau;  // every candidate up to band_hi(t) is listed
                 if (!ok) why = 5;

@@ -968,6 +968,35 @@ def test_align_batch(g, B):
     assert rot_angle(Tb[0][:3, :3], res["T"][:3, :3]) < 1e-5 and np.abs(Tb[0][:3, 3] - res["T"][:3, 3]).max() < 1e-5
 
 
+def test_align_batch_bench_config_all_frames(g):
+    """N2 at the configuration bench.py times: 8 distinct frames of a Replica-shaped sequence vs its
+    1e6-Gaussian map (frames 1..8, initial poses perturbed with seeds 500 + b, the bench's GN
+    parameters) in one BatchTracker step through the flat GN loop; EVERY frame's pose against the
+    oracle from the same initial pose."""
+    B = 8
+    seq = synth.make_sequence(0, B + 1, "replica", M=1_000_000)
+    rows = synth.render_sequence_rows(seq, DEV)
+    K = seq.K
+    prm = g.align_params(max_iters=30, max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6)
+    tgt = g.build_target(t(seq.means), t(seq.quats), t(seq.scales))
+    init = np.stack([synth.perturb_pose(seq.T_gt[1 + b], 500 + b, 2.0, 0.03) for b in range(B)])
+    bt = g.BatchTracker(B, K.H, K.W, (K.fx, K.fy, K.cx, K.cy), stride=seq.stride, params=prm)
+    bt.rows.copy_(rows[1:1 + B])
+    Tb, stb = bt.track_rows(tgt, init)
+    oct_, _ = oracle.target_from_map(seq.quats, seq.scales)
+    tree = oracle.KDTree(seq.means)
+    for b in range(B):
+        depth = np.full((K.H, K.W), np.nan, np.float32)
+        depth[::seq.stride] = rows[1 + b].cpu().numpy()
+        xyz, _ = oracle.backproject(depth, K.fx, K.fy, K.cx, K.cy, seq.stride)
+        ocs = oracle.covariances(xyz)["cov"]
+        res = oracle.align(xyz, ocs, seq.means, oct_, init[b], max_iters=30, max_corr_dist=0.1, eps_rot=1e-6,
+                           eps_trans=1e-6, tree=tree)
+        assert rot_angle(Tb[b][:3, :3], res["T"][:3, :3]) <= 1e-5, b
+        assert np.abs(Tb[b][:3, 3] - res["T"][:3, 3]).max() <= 1e-5, b
+        assert stb[b]["n_inliers"] == res["n_inliers"] and abs(stb[b]["iters"] - res["iters"]) <= 1, b
+
+
 def test_align_batch_single_and_ragged(g):
     """B = 1 runs the same blocks and summation as the single-frame kernel: bitwise-identical pose
     and stats.  A ragged batch (one frame with a third of its depth missing, so fewer points) gives

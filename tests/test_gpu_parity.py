@@ -530,6 +530,31 @@ def test_align_per_iteration_tum(g, tum, stride, iters):
     assert _iter_parity(S, rec.iterations(), 0.1, f"tum s={stride}") == iters
 
 
+@pytest.mark.parametrize("stride", [4, 1])
+def test_align_per_iteration_tum_tracker(g, tum, stride):
+    """C3 through the bench's own path (Tracker: A1 -> image-window A2-A4 -> seeded A6-A9, one
+    graph replay; stride 1 takes the flat GN loop with seeds): every iteration of the first 8
+    against the oracle at the pose the GPU iteration used."""
+    w = tum
+    K = w.K
+    H, W = w.depth.shape
+    xyz, _ = oracle.backproject(w.depth, K.fx, K.fy, K.cx, K.cy, stride)
+    S = dict(xyz=xyz, txyz=w.means, ocs=oracle.covariances(xyz)["cov"],
+             oct=oracle.target_from_map(w.quats, w.scales)[0], tree=oracle.KDTree(w.means))
+    tgt = g.build_target(t(w.means), t(w.quats), t(w.scales))
+    iters = 8
+    tr = g.Tracker(H, W, (K.fx, K.fy, K.cx, K.cy), stride=stride,
+                   params=g.align_params(max_iters=iters, max_corr_dist=0.1, eps_rot=0.0, eps_trans=0.0))
+    if stride == 1:
+        assert tr.cap > 148 * 384  # the flat GN loop
+    with g.AlignIterations(iters, tr.cap) as rec:
+        tr.track(t(w.depth), tgt, w.T_init)
+    torch.cuda.synchronize()
+    it = rec.iterations()
+    np.testing.assert_array_equal(it[0]["T"], w.T_init)
+    assert _iter_parity(S, it, 0.1, f"tum tracker s={stride}") == iters
+
+
 @pytest.mark.parametrize("B", [3, 8])
 def test_align_per_iteration_batch_frame(g, replica_setup, B):
     """N2: frame 0 of a B-frame batch (the others: perturbed poses of the same frame); B = 3 runs

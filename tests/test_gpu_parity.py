@@ -530,6 +530,29 @@ def test_align_per_iteration_tum(g, tum, stride, iters):
     assert _iter_parity(S, rec.iterations(), 0.1, f"tum s={stride}") == iters
 
 
+def test_align_per_iteration_c2_tracker(g):
+    """C2 as bench.py times it: the Replica-shaped frame vs a 1e5-Gaussian map through the Tracker
+    (one graph replay), every GN iteration against the oracle, then the final pose."""
+    w = synth.make_frame_workload(2, "replica", M=100_000, stride=4)
+    K = w.K
+    H, W = w.depth.shape
+    xyz, _ = oracle.backproject(w.depth, K.fx, K.fy, K.cx, K.cy, 4)
+    S = dict(xyz=xyz, txyz=w.means, ocs=oracle.covariances(xyz)["cov"],
+             oct=oracle.target_from_map(w.quats, w.scales)[0], tree=oracle.KDTree(w.means))
+    tgt = g.build_target(t(w.means), t(w.quats), t(w.scales))
+    prm = g.align_params(max_iters=30, max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6)
+    tr = g.Tracker(H, W, (K.fx, K.fy, K.cx, K.cy), stride=4, params=prm)
+    with g.AlignIterations(30, tr.cap) as rec:
+        Tg, st = tr.track(t(w.depth), tgt, w.T_init)
+    torch.cuda.synchronize()
+    it = rec.iterations()
+    assert len(it) == st["iters"] >= 2
+    _iter_parity(S, it, 0.1, "c2")
+    ref = oracle.align(xyz, S["ocs"], w.means, S["oct"], w.T_init, max_iters=30, max_corr_dist=0.1, tree=S["tree"])
+    assert rot_angle(Tg[:3, :3], ref["T"][:3, :3]) <= 1e-5 and np.linalg.norm(Tg[:3, 3] - ref["T"][:3, 3]) <= 1e-5
+    assert st["n_inliers"] == ref["n_inliers"] and abs(st["iters"] - ref["iters"]) <= 1
+
+
 @pytest.mark.parametrize("stride", [4, 1])
 def test_align_per_iteration_tum_tracker(g, tum, stride):
     """C3 through the bench's own path (Tracker: A1 -> image-window A2-A4 -> seeded A6-A9, one

@@ -772,6 +772,21 @@ def test_sequence_tracking(g):
     T_est, ms = g.track_sequence(tr, tgt, rows, seq.T_gt[0])
     err = synth.trajectory_error(T_est, seq.T_gt[1:])
     assert err["ate_rmse_m"] < 5e-3 and err["rot_max_deg"] < 0.5, err
+    # frames 1..6 against the oracle, each from the constant-velocity prediction of the GPU's
+    # previous poses (zero velocity before frame 1)
+    oct_, _ = oracle.target_from_map(seq.quats, seq.scales)
+    tree = oracle.KDTree(seq.means)
+    prev2, prev1 = seq.T_gt[0], seq.T_gt[0]
+    for f in range(1, 7):
+        init = prev1 @ np.linalg.inv(prev2) @ prev1
+        depth = np.full((K.H, K.W), np.nan, np.float32)
+        depth[::seq.stride] = rows[f].cpu().numpy()
+        xyz, _ = oracle.backproject(depth, K.fx, K.fy, K.cx, K.cy, seq.stride)
+        res = oracle.align(xyz, oracle.covariances(xyz)["cov"], seq.means, oct_, init, max_iters=30,
+                           max_corr_dist=0.1, eps_rot=1e-6, eps_trans=1e-6, tree=tree)
+        Tg = T_est[f - 1]
+        assert rot_angle(Tg[:3, :3], res["T"][:3, :3]) <= 1e-5 and np.abs(Tg[:3, 3] - res["T"][:3, 3]).max() <= 1e-5, f
+        prev2, prev1 = prev1, Tg
     assert g.decode_stats(tr.d_stats)["status"] in (g.OK, g.WARN_MAX_ITERS)
     # the device-side prediction equals the constant-velocity formula on the host
     hist = torch.from_numpy(np.concatenate([seq.T_gt[3].reshape(-1), seq.T_gt[4].reshape(-1)])).to(DEV)
